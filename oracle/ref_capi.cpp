@@ -1,0 +1,469 @@
+// TEST INFRASTRUCTURE — NOT PRODUCT CODE.
+//
+// extern "C" wrapper around the UNMODIFIED reference headers
+// (/root/reference/proj/include/gmrfpde/**, header-only C++20). Built by
+// oracle/Makefile into oracle/_ref/libgmrfref.so; only tests/, smoke() and
+// bench.py's cpu_baseline / --impl reference legs load it, always as the
+// checker or the CPU baseline, never as the thing measured or shipped.
+//
+// The reference's Index is int (core/types.hpp:12), so every CSC crossing this
+// wrapper uses int32 col_ptr/row_idx — exactly the reference layout
+// (core/sparse.hpp:25-61).
+//
+// Problem builders follow SURVEY.md §8(d)'s pinned draw order.
+
+#include <chrono>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "gmrfpde/core/amd.hpp"
+#include "gmrfpde/core/cholesky.hpp"
+#include "gmrfpde/core/rng.hpp"
+#include "gmrfpde/core/sparse.hpp"
+#include "gmrfpde/core/takahashi.hpp"
+#include "gmrfpde/fem/assembly.hpp"
+#include "gmrfpde/fem/constraints.hpp"
+#include "gmrfpde/fem/mesh.hpp"
+#include "gmrfpde/fem/space.hpp"
+#include "gmrfpde/gmrf.hpp"
+#include "gmrfpde/priors/boundary.hpp"
+#include "gmrfpde/priors/matern.hpp"
+#include "gmrfpde/priors/spatiotemporal.hpp"
+#include "gmrfpde/solver/gauss_newton.hpp"
+#include "gmrfpde/solver/info_operator.hpp"
+#include "gmrfpde/solver/residual.hpp"
+#include "oracles.hpp"
+
+using namespace gmrfpde;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Bundle {
+  std::map<std::string, SparseMatrixCSC> mats;
+  std::map<std::string, Vector> vecs;
+  std::map<std::string, std::vector<Index>> ivecs;
+  std::map<std::string, double> scalars;
+};
+
+double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+
+SparseMatrixCSC make_csc(int n_rows, int n_cols, const int* cp, const int* ri, const double* v) {
+  SparseMatrixCSC m(n_rows, n_cols);
+  m.col_ptr.assign(cp, cp + n_cols + 1);
+  m.row_idx.assign(ri, ri + cp[n_cols]);
+  m.values.assign(v, v + cp[n_cols]);
+  return m;
+}
+
+// Fixed-step GN trace → flat vectors.
+void put_trace(Bundle& b, const std::vector<solver::GaussNewtonIteration>& tr) {
+  Vector obj, dec, step, bt;
+  for (const auto& r : tr) {
+    obj.push_back(r.objective);
+    dec.push_back(r.decrement);
+    step.push_back(r.step_size);
+    bt.push_back(static_cast<double>(r.backtracks));
+  }
+  b.vecs["gn_objective"] = obj;
+  b.vecs["gn_decrement"] = dec;
+  b.vecs["gn_step"] = step;
+  b.vecs["gn_backtracks"] = bt;
+}
+
+// ----- C1/C2: Matérn regression ------------------------
+Bundle* build_matern(int dim, const double* p, int np) {
+  // p: [resolution, kappa, alpha, tau, n_obs, seed, noise_prec, obs_sd, n_samples,
+  //     sample_seed, do_variance]
+  (void)np;
+  int res = static_cast<int>(p[0]);
+  priors::MaternSpec spec{p[1], static_cast<int>(p[2]), p[3]};
+  int m = static_cast<int>(p[4]);
+  Rng rng(static_cast<std::uint64_t>(p[5]));
+  double lam = p[6], sd = p[7];
+  int n_samples = static_cast<int>(p[8]);
+  auto* b = new Bundle();
+  fem::FeSpace space(dim == 1 ? fem::build_interval_mesh(res, 0.0, 1.0)
+                              : fem::build_unit_square_mesh(res),
+                     1);
+  double t0 = now_s();
+  Gmrf prior = priors::matern_prior(space, spec);
+  b->scalars["t_prior"] = now_s() - t0;
+  std::vector<Real> pts(m * dim);
+  for (auto& v : pts) v = rng.uniform();
+  Vector y(m);
+  for (int i = 0; i < m; ++i) {
+    double e = rng.normal();
+    if (dim == 1)
+      y[i] = std::sin(2 * M_PI * pts[i]) + sd * e;
+    else
+      y[i] = std::sin(3 * M_PI * pts[2 * i]) * std::cos(2 * M_PI * pts[2 * i + 1]) + sd * e;
+  }
+  auto op = solver::point_observation_operator(space, pts, y, lam);
+  t0 = now_s();
+  Gmrf post = solver::condition_on(prior, op);
+  b->scalars["t_condition"] = now_s() - t0;
+  b->mats["Q_prior"] = prior.precision();
+  b->mats["S_prior"] = prior.sqrt();
+  b->mats["A"] = op.A;
+  b->vecs["y"] = op.b;
+  b->vecs["noise"] = op.noise_precision;
+  b->vecs["points"] = pts;
+  b->mats["Q_post"] = post.precision();
+  b->vecs["mean_post"] = post.mean();
+  b->ivecs["perm_amd"] = post.factor().perm;
+  b->mats["L"] = post.factor().L;
+  if (p[10] != 0.0) {
+    t0 = now_s();
+    b->vecs["var_post"] = variance_takahashi(post);
+    b->scalars["t_variance"] = now_s() - t0;
+  }
+  Rng srng(static_cast<std::uint64_t>(p[9]));
+  Vector zs, ss;
+  t0 = now_s();
+  for (int s = 0; s < n_samples; ++s) {
+    Vector z = srng.normal_vector(post.dim());
+    Vector x = sample_direct(post, z);
+    zs.insert(zs.end(), z.begin(), z.end());
+    ss.insert(ss.end(), x.begin(), x.end());
+  }
+  b->scalars["t_samples"] = now_s() - t0;
+  b->vecs["z"] = zs;
+  b->vecs["samples"] = ss;
+  return b;
+}
+
+// ----- spatiotemporal prior (+ IC conditioning, + Burgers GN-Laplace) --------
+// p: [kind(0 heat, 1 burgers), n_el, x_a, x_b, n_t, t_end, nu, c, noise_kappa,
+//     noise_alpha, noise_tau, init_kappa, init_alpha, init_tau, tau, eps,
+//     ic_noise_prec, ic_seed, pde_noise_prec, gn_max_iters, do_variance, do_gn]
+Bundle* build_spatiotemporal(const double* p, int np) {
+  (void)np;
+  int kind = static_cast<int>(p[0]);
+  int n_el = static_cast<int>(p[1]);
+  double xa = p[2], xb = p[3];
+  int n_t = static_cast<int>(p[4]);
+  double t_end = p[5], nu = p[6], c = p[7];
+  auto* b = new Bundle();
+  fem::FeSpace space(fem::build_interval_mesh(n_el, xa, xb), 1);
+  fem::ConstraintSet cs = priors::embed_dirichlet(space, p[15]);
+  Vector t_grid(n_t);
+  for (int i = 0; i < n_t; ++i) t_grid[i] = t_end * i / static_cast<double>(n_t - 1);
+  priors::SpatiotemporalSpec st;
+  st.t_grid = t_grid;
+  st.spatial_op = kind == 0 ? fem::laplace_operator(nu)
+                            : priors::linear_proxy_operator({c}, nu);
+  st.noise_spec = {p[8], static_cast<int>(p[9]), p[10]};
+  st.initial_spec = {p[11], static_cast<int>(p[12]), p[13]};
+  st.tau = p[14];
+  double t0 = now_s();
+  auto [stp, flat] = priors::spatiotemporal_prior(space, st, cs);
+  b->scalars["t_prior"] = now_s() - t0;
+  b->mats["Q_prior"] = flat.precision();
+  b->mats["S_prior"] = flat.sqrt();
+  int n = space.n_dofs();
+  // Initial condition (runner.hpp:555-579 recipe).
+  Vector u0(n);
+  if (kind == 0) {
+    Rng rng(static_cast<std::uint64_t>(p[17]));
+    Vector a(10);
+    for (int k = 1; k <= 10; ++k) a[k - 1] = rng.normal() / k;
+    for (int d = 0; d < n; ++d) {
+      double x = space.dof_x(d), v = 0;
+      for (int k = 1; k <= 10; ++k) v += a[k - 1] * std::sin(k * M_PI * x);
+      u0[d] = v;
+    }
+  } else {
+    for (int d = 0; d < n; ++d) u0[d] = -std::sin(M_PI * space.dof_x(d));
+  }
+  std::vector<Real> ic_points(n);
+  for (int d = 0; d < n; ++d) ic_points[d] = space.dof_x(d);
+  SparseMatrixCSC e0 = fem::eval_basis(space, ic_points, {0, 0});
+  auto [e0f, shift] = fem::fold_pointwise_operator(e0, Vector(n, 0.0), cs);
+  std::vector<Triplet> ic_trips;
+  for (Index j = 0; j < n; ++j)
+    for (Index q = e0f.col_ptr[j]; q < e0f.col_ptr[j + 1]; ++q)
+      ic_trips.push_back({e0f.row_idx[q], j, e0f.values[q]});
+  solver::LinearInformationOperator ic_op;
+  ic_op.A = csc_from_triplets(n, n_t * n, std::move(ic_trips));
+  ic_op.b = u0;
+  ic_op.noise_precision.assign(n, p[16]);
+  b->mats["A_ic"] = ic_op.A;
+  b->vecs["y_ic"] = ic_op.b;
+  b->vecs["noise_ic"] = ic_op.noise_precision;
+  t0 = now_s();
+  Gmrf cond = solver::condition_on(flat, ic_op);
+  b->scalars["t_condition"] = now_s() - t0;
+  b->mats["Q_cond"] = cond.precision();
+  b->mats["S_cond"] = cond.sqrt();
+  b->vecs["mean_cond"] = cond.mean();
+  Gmrf post = cond;
+  if (kind == 1 && p[21] != 0.0) {
+    auto res = solver::burgers_fem_residual(space, t_grid, cs, nu,
+                                            solver::TimeScheme::kImplicitEuler, p[18]);
+    b->mats["J_at_mean_cond"] = res.jacobian(cond.mean());
+    b->vecs["f_at_mean_cond"] = res.eval(cond.mean());
+    solver::GaussNewtonConfig cfg;
+    cfg.max_iters = static_cast<Index>(p[19]);
+    cfg.decrement_tol = 1e-5;
+    t0 = now_s();
+    auto gn = solver::gauss_newton(cond, res, cond.mean(), cfg);
+    b->scalars["t_gn"] = now_s() - t0;
+    put_trace(*b, gn.trace);
+    b->vecs["mode"] = gn.mode;
+    b->scalars["gn_converged"] = gn.converged ? 1.0 : 0.0;
+    t0 = now_s();
+    post = solver::laplace_posterior(cond, res, gn.mode);
+    b->scalars["t_laplace_build"] = now_s() - t0;
+    b->mats["Q_la"] = post.precision();
+  }
+  b->vecs["mean_post"] = post.mean();
+  if (p[20] != 0.0) {
+    t0 = now_s();
+    b->vecs["var_post"] = variance_takahashi(post);
+    b->scalars["t_variance"] = now_s() - t0;
+  }
+  return b;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+// ----- bundles ---------------------------------------------------------------
+void* ref_build(const char* kind, const double* p, int np) {
+  try {
+    std::string k(kind);
+    if (k == "matern1d") return build_matern(1, p, np);
+    if (k == "matern2d") return build_matern(2, p, np);
+    if (k == "spatiotemporal") return build_spatiotemporal(p, np);
+    if (k == "corpus") {
+      // p: [count, seed]; matrices "Q0".."Q{count-1}"
+      auto corpus = oracle::spd_corpus(static_cast<int>(p[0]), static_cast<std::uint64_t>(p[1]));
+      auto* b = new Bundle();
+      for (std::size_t i = 0; i < corpus.size(); ++i) b->mats["Q" + std::to_string(i)] = corpus[i];
+      return b;
+    }
+    g_err = "unknown bundle kind " + k;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+  }
+  return nullptr;
+}
+
+void ref_bundle_free(void* b) { delete static_cast<Bundle*>(b); }
+
+int ref_bundle_mat_shape(void* hb, const char* name, int* nr, int* nc, int* nnz) {
+  auto* b = static_cast<Bundle*>(hb);
+  auto it = b->mats.find(name);
+  if (it == b->mats.end()) return -1;
+  *nr = it->second.nrows;
+  *nc = it->second.ncols;
+  *nnz = it->second.nnz();
+  return 0;
+}
+
+int ref_bundle_mat_copy(void* hb, const char* name, int* cp, int* ri, double* v) {
+  auto* b = static_cast<Bundle*>(hb);
+  auto it = b->mats.find(name);
+  if (it == b->mats.end()) return -1;
+  const auto& m = it->second;
+  std::memcpy(cp, m.col_ptr.data(), sizeof(int) * m.col_ptr.size());
+  std::memcpy(ri, m.row_idx.data(), sizeof(int) * m.row_idx.size());
+  std::memcpy(v, m.values.data(), sizeof(double) * m.values.size());
+  return 0;
+}
+
+long long ref_bundle_vec_len(void* hb, const char* name) {
+  auto* b = static_cast<Bundle*>(hb);
+  auto it = b->vecs.find(name);
+  if (it != b->vecs.end()) return static_cast<long long>(it->second.size());
+  auto jt = b->ivecs.find(name);
+  if (jt != b->ivecs.end()) return -2 - static_cast<long long>(jt->second.size());
+  return -1;
+}
+
+int ref_bundle_vec_copy(void* hb, const char* name, double* out) {
+  auto* b = static_cast<Bundle*>(hb);
+  auto it = b->vecs.find(name);
+  if (it != b->vecs.end()) {
+    std::memcpy(out, it->second.data(), sizeof(double) * it->second.size());
+    return 0;
+  }
+  auto jt = b->ivecs.find(name);
+  if (jt != b->ivecs.end()) {
+    for (std::size_t i = 0; i < jt->second.size(); ++i) out[i] = jt->second[i];
+    return 0;
+  }
+  return -1;
+}
+
+double ref_bundle_scalar(void* hb, const char* name) {
+  auto* b = static_cast<Bundle*>(hb);
+  auto it = b->scalars.find(name);
+  return it == b->scalars.end() ? std::nan("") : it->second;
+}
+
+// ----- core linear algebra (core/amd.hpp, core/cholesky.hpp, core/takahashi.hpp)
+int ref_amd_order(int n, const int* cp, const int* ri, int* perm) {
+  try {
+    std::vector<double> v(cp[n], 1.0);
+    auto p = amd_order(make_csc(n, n, cp, ri, v.data()));
+    std::memcpy(perm, p.data(), sizeof(int) * n);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// symbolic_analyze (cholesky.hpp:68): parent[n], col_ptr_L[n+1]
+int ref_symbolic(int n, const int* cp, const int* ri, const int* perm, int* parent,
+                 int* colptr_l) {
+  try {
+    std::vector<double> v(cp[n], 1.0);
+    std::vector<Index> pv(perm, perm + n);
+    SymbolicFactor s = symbolic_analyze(make_csc(n, n, cp, ri, v.data()), pv);
+    std::memcpy(parent, s.parent.data(), sizeof(int) * n);
+    std::memcpy(colptr_l, s.col_ptr.data(), sizeof(int) * (n + 1));
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+struct RefFactor {
+  CholeskyFactor f;
+};
+
+// cholesky_factor (cholesky.hpp:164/170). perm == nullptr → AMD. Returns
+// nullptr on failure; *bad = original index of a non-positive pivot or -1.
+void* ref_factor(int n, const int* cp, const int* ri, const double* v, const int* perm,
+                 int* bad) {
+  *bad = -1;
+  try {
+    SparseMatrixCSC q = make_csc(n, n, cp, ri, v);
+    auto* h = new RefFactor();
+    if (perm) {
+      h->f = cholesky_factor(q, std::vector<Index>(perm, perm + n));
+    } else {
+      h->f = cholesky_factor(q);
+    }
+    return h;
+  } catch (const NotPositiveDefiniteError& e) {
+    *bad = e.index();
+    g_err = e.what();
+  } catch (const std::exception& e) {
+    g_err = e.what();
+  }
+  return nullptr;
+}
+
+void ref_factor_free(void* h) { delete static_cast<RefFactor*>(h); }
+
+int ref_factor_nnz(void* h) { return static_cast<RefFactor*>(h)->f.L.nnz(); }
+
+void ref_factor_copy(void* h, int* cp, int* ri, double* v, int* perm) {
+  const auto& f = static_cast<RefFactor*>(h)->f;
+  std::memcpy(cp, f.L.col_ptr.data(), sizeof(int) * f.L.col_ptr.size());
+  std::memcpy(ri, f.L.row_idx.data(), sizeof(int) * f.L.row_idx.size());
+  std::memcpy(v, f.L.values.data(), sizeof(double) * f.L.values.size());
+  std::memcpy(perm, f.perm.data(), sizeof(int) * f.perm.size());
+}
+
+// solve_triangular (cholesky.hpp:179); mode 0 lower, 1 upper, 2 full.
+void ref_solve(void* h, int mode, const double* b, double* x) {
+  const auto& f = static_cast<RefFactor*>(h)->f;
+  Vector bb(b, b + f.dim());
+  Vector r = solve_triangular(f, bb, static_cast<TriangularMode>(mode));
+  std::memcpy(x, r.data(), sizeof(double) * r.size());
+}
+
+// takahashi_diagonal (takahashi.hpp:67)
+void ref_takahashi_diag(void* h, double* out) {
+  const auto& f = static_cast<RefFactor*>(h)->f;
+  Vector d = takahashi_diagonal(f);
+  std::memcpy(out, d.data(), sizeof(double) * d.size());
+}
+
+// takahashi_selected_inverse (takahashi.hpp:19) → bundle matrix "S"
+void* ref_takahashi_full(void* h) {
+  auto* b = new Bundle();
+  b->mats["S"] = takahashi_selected_inverse(static_cast<RefFactor*>(h)->f);
+  return b;
+}
+
+// condition_affine (gmrf.hpp:145) with diagonal noise → bundle {Q_post, mean_post}
+void* ref_condition_affine(int n, const int* qcp, const int* qri, const double* qv,
+                           const double* mu, int m, const int* acp, const int* ari,
+                           const double* av, const double* bvec, const double* y,
+                           const double* noise) {
+  try {
+    Gmrf prior(Vector(mu, mu + n), make_csc(n, n, qcp, qri, qv));
+    auto obs = AffineObservation::with_diagonal_noise(make_csc(m, n, acp, ari, av),
+                                                      Vector(bvec, bvec + m),
+                                                      Vector(y, y + m), Vector(noise, noise + m));
+    Gmrf post = condition_affine(prior, obs);
+    auto* b = new Bundle();
+    b->mats["Q_post"] = post.precision();
+    b->vecs["mean_post"] = post.mean();
+    return b;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+
+// Timed reference stages on one matrix (for the CPU baseline leg):
+// out[0]=amd s, out[1]=symbolic s, out[2]=numeric s, out[3]=full solve s,
+// out[4]=takahashi s (if do_taka), out[5]=nnz(L), out[6]=Σ c_j² flops.
+int ref_time_stages(int n, const int* cp, const int* ri, const double* v, int do_taka,
+                    double* out) {
+  try {
+    SparseMatrixCSC q = make_csc(n, n, cp, ri, v);
+    double t0 = now_s();
+    auto perm = amd_order(q);
+    double t1 = now_s();
+    auto sym = symbolic_analyze(q, perm);
+    double t2 = now_s();
+    auto f = cholesky_refactor(sym, q);
+    double t3 = now_s();
+    Vector b(n, 1.0);
+    auto x = solve(f, b);
+    double t4 = now_s();
+    out[0] = t1 - t0;
+    out[1] = t2 - t1;
+    out[2] = t3 - t2;
+    out[3] = t4 - t3;
+    out[4] = 0.0;
+    if (do_taka) {
+      auto d = takahashi_diagonal(f);
+      out[4] = now_s() - t4;
+    }
+    out[5] = f.L.nnz();
+    double fl = 0;
+    for (int j = 0; j < n; ++j) {
+      double cj = f.L.col_ptr[j + 1] - f.L.col_ptr[j];
+      fl += cj * cj;
+    }
+    out[6] = fl;
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+}  // extern "C"

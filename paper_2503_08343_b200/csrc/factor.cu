@@ -1,0 +1,523 @@
+// Host side of the device factor: plan construction and launch sequences.
+#include "factor.hpp"
+
+#include <algorithm>
+#include <climits>
+#include <string>
+
+#include "kernels.cu"  // single translation unit for all device code
+
+namespace gmrf {
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(kCuda, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+namespace {
+constexpr int kPanelSmem = (kNB * (kNB + 1) + kNB * (kTrsmRows + 1)) * sizeof(double);
+constexpr int kDiagSmem = 3 * kNB * (kNB + 1) * sizeof(double);
+
+void set_smem_attrs() {
+  static bool done = false;
+  if (done) return;
+  cuda_check(cudaFuncSetAttribute(k_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPanelSmem),
+             "smem k_panel");
+  cuda_check(
+      cudaFuncSetAttribute(k_sel_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, kPanelSmem),
+      "smem k_sel_trsm");
+  cuda_check(
+      cudaFuncSetAttribute(k_sel_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, kDiagSmem),
+      "smem k_sel_diag");
+  done = true;
+}
+
+inline int nchunks(int w) { return (w + kNB - 1) / kNB; }
+}  // namespace
+
+DeviceFactor::DeviceFactor(std::shared_ptr<const Symbolic> sym, cudaStream_t stream)
+    : sym_(std::move(sym)), stream_(stream) {
+  set_smem_attrs();
+  const Symbolic& s = *sym_;
+  first_.upload(s.sn_first, stream_);
+  rows_.upload(s.sn_rows, stream_);
+  relmap_.upload(s.relmap, stream_);
+  chptr_.upload(s.ch_ptr, stream_);
+  chlist_.upload(s.ch_list, stream_);
+  perm_.upload(s.perm, stream_);
+  col2sn_.upload(s.col2sn, stream_);
+  snparent_.upload(s.sn_parent, stream_);
+  rptr_.upload(s.sn_rptr, stream_);
+  lptr_.upload(s.lptr, stream_);
+  uptr_.upload(s.uptr, stream_);
+  qmap_.upload(s.qmap, stream_);
+  status_.alloc(1);
+  L_.alloc(std::max<int64_t>(s.lptr[s.ns], 1));
+  U_.alloc(std::max<int64_t>(s.uptr[s.ns], 1));
+  q_.alloc(std::max<size_t>(s.qri.size(), 1));
+  // solve schedule: supernodes grouped by tree level
+  lvl_ptr_.assign(s.n_levels + 1, 0);
+  for (int k = 0; k < s.ns; ++k) lvl_ptr_[s.sn_level[k] + 1]++;
+  for (int l = 0; l < s.n_levels; ++l) lvl_ptr_[l + 1] += lvl_ptr_[l];
+  std::vector<int32_t> lsn(s.ns);
+  {
+    std::vector<int64_t> nx(lvl_ptr_.begin(), lvl_ptr_.end() - 1);
+    for (int k = 0; k < s.ns; ++k) lsn[nx[s.sn_level[k]]++] = k;
+  }
+  lvl_sn_.upload(lsn, stream_);
+  std::vector<int64_t> fp(s.ns + 1, 0), up(s.ns + 1, 0);
+  for (int k = 0; k < s.ns; ++k) {
+    fp[k + 1] = fp[k] + s.rows(k);
+    up[k + 1] = up[k] + s.r(k);
+  }
+  fptr_.upload(fp, stream_);
+  uvptr_.upload(up, stream_);
+  build_factor_plan();
+  cuda_check(cudaStreamSynchronize(stream_), "factor setup");
+}
+
+DeviceFactor::~DeviceFactor() = default;
+
+SymDev DeviceFactor::symdev() const {
+  SymDev d;
+  d.sn_first = first_.p;
+  d.sn_rptr = rptr_.p;
+  d.sn_rows = rows_.p;
+  d.relmap = relmap_.p;
+  d.ch_ptr = chptr_.p;
+  d.ch_list = chlist_.p;
+  d.lptr = lptr_.p;
+  d.uptr = uptr_.p;
+  d.n = sym_->n;
+  return d;
+}
+
+int64_t DeviceFactor::device_bytes() const {
+  return static_cast<int64_t>((L_.n + U_.n + Sig_.n + q_.n + F_.n + Uv_.n + v1_.n + v2_.n) *
+                              sizeof(double)) +
+         static_cast<int64_t>(gemm_.n * sizeof(GemmTask) + sgemm_.n * sizeof(GemmTask));
+}
+
+// Chunk levels: chunk k of supernode s sits at lvl0(s)+k where lvl0(s) is one
+// above the last chunk of its deepest child.
+static void chunk_levels(const Symbolic& s, std::vector<int>& lvl0, int& nlev) {
+  lvl0.assign(s.ns, 0);
+  std::vector<int> last(s.ns, 0);
+  nlev = 0;
+  for (int k = 0; k < s.ns; ++k) {
+    int l = 0;
+    for (int q = s.ch_ptr[k]; q < s.ch_ptr[k + 1]; ++q) l = std::max(l, last[s.ch_list[q]] + 1);
+    lvl0[k] = l;
+    last[k] = l + nchunks(s.w(k)) - 1;
+    nlev = std::max(nlev, last[k] + 1);
+  }
+}
+
+void DeviceFactor::build_factor_plan() {
+  const Symbolic& s = *sym_;
+  std::vector<int> lvl0;
+  int nlev = 0;
+  chunk_levels(s, lvl0, nlev);
+  std::vector<std::vector<ColTask>> ea(nlev);
+  std::vector<std::vector<PanelTask>> pan(nlev);
+  std::vector<std::vector<GemmTask>> gm(nlev);
+  double* L = L_.p;
+  double* U = U_.p;
+  for (int k = 0; k < s.ns; ++k) {
+    const int w = s.w(k), rows = s.rows(k), r = rows - w;
+    double* Lk = L + s.lptr[k];
+    double* Uk = U + s.uptr[k];
+    const int nch = nchunks(w);
+    for (int c = 0; c < nch; ++c) {
+      const int lv = lvl0[k] + c;
+      const int c0 = c * kNB, wk = std::min(kNB, w - c0);
+      if (c == 0 && s.ch_ptr[k + 1] > s.ch_ptr[k])
+        for (int b = 0; b < rows; ++b) ea[lv].push_back({k, b});
+      const int nbelow = rows - c0 - wk;
+      const int nt = std::max(1, (nbelow + kTrsmRows - 1) / kTrsmRows);
+      for (int t = 0; t < nt; ++t)
+        pan[lv].push_back({Lk + c0 + static_cast<int64_t>(c0) * rows, rows, wk, nbelow, t,
+                           s.sn_first[k] + c0});
+      // right-looking update of the trailing panel columns with this chunk
+      for (int jb = c0 + wk; jb < w; jb += kTile)
+        for (int ib = jb; ib < rows; ib += kTile) {
+          GemmTask g{};
+          g.c = Lk + ib + static_cast<int64_t>(jb) * rows;
+          g.ldc = rows;
+          g.m = std::min(kTile, rows - ib);
+          g.n = std::min(kTile, w - jb);
+          g.a[0] = Lk + ib + static_cast<int64_t>(c0) * rows;
+          g.lda[0] = rows;
+          g.b[0] = Lk + jb + static_cast<int64_t>(c0) * rows;
+          g.ldb[0] = rows;
+          g.k[0] = wk;
+          g.flags = 2;  // B transposed
+          g.alpha = -1.0;
+          g.beta = 1.0;
+          gm[lv].push_back(g);
+        }
+      // last chunk: full-width SYRK into the update matrix, U -= L21 L21ᵀ
+      if (c == nch - 1 && r > 0)
+        for (int jb = 0; jb < r; jb += kTile)
+          for (int ib = jb; ib < r; ib += kTile) {
+            GemmTask g{};
+            g.c = Uk + ib + static_cast<int64_t>(jb) * r;
+            g.ldc = r;
+            g.m = std::min(kTile, r - ib);
+            g.n = std::min(kTile, r - jb);
+            g.a[0] = Lk + w + ib;
+            g.lda[0] = rows;
+            g.b[0] = Lk + w + jb;
+            g.ldb[0] = rows;
+            g.k[0] = w;
+            g.flags = 2;
+            g.alpha = -1.0;
+            g.beta = 1.0;
+            gm[lv].push_back(g);
+          }
+    }
+  }
+  std::vector<ColTask> eaf;
+  std::vector<PanelTask> panf;
+  std::vector<GemmTask> gmf;
+  flev_.assign(nlev, {});
+  for (int l = 0; l < nlev; ++l) {
+    flev_[l] = {static_cast<int64_t>(eaf.size()), static_cast<int64_t>(ea[l].size()),
+                static_cast<int64_t>(panf.size()), static_cast<int64_t>(pan[l].size()),
+                static_cast<int64_t>(gmf.size()), static_cast<int64_t>(gm[l].size())};
+    eaf.insert(eaf.end(), ea[l].begin(), ea[l].end());
+    panf.insert(panf.end(), pan[l].begin(), pan[l].end());
+    gmf.insert(gmf.end(), gm[l].begin(), gm[l].end());
+  }
+  ea_.upload(eaf, stream_);
+  pan_.upload(panf, stream_);
+  gemm_.upload(gmf, stream_);
+}
+
+void DeviceFactor::build_selinv_plan() {
+  const Symbolic& s = *sym_;
+  Sig_.alloc(std::max<int64_t>(s.lptr[s.ns], 1));
+  std::vector<int> lvl0;
+  int nlev = 0;
+  chunk_levels(s, lvl0, nlev);
+  std::vector<std::vector<ColTask>> ga(nlev);
+  std::vector<std::vector<GemmTask>> yg(nlev), zg(nlev);
+  std::vector<std::vector<SelChunk>> tr(nlev), dg(nlev);
+  double* L = L_.p;
+  double* U = U_.p;
+  double* S = Sig_.p;
+  for (int k = 0; k < s.ns; ++k) {
+    const int w = s.w(k), rows = s.rows(k), r = rows - w;
+    double* Lk = L + s.lptr[k];
+    double* Sk = S + s.lptr[k];
+    double* Uk = U + s.uptr[k];
+    const int nch = nchunks(w);
+    for (int c = nch - 1; c >= 0; --c) {
+      const int lv = lvl0[k] + c;
+      const int c0 = c * kNB, wk = std::min(kNB, w - c0);
+      const int p = w - c0 - wk;
+      if (c == nch - 1 && r > 0)
+        for (int b = 0; b < r; ++b) ga[lv].push_back({k, b});
+      auto ytile = [&](int i0, int i1) {
+        GemmTask g{};
+        g.c = Sk + i0 + static_cast<int64_t>(c0) * rows;
+        g.ldc = rows;
+        g.m = i1 - i0;
+        g.n = wk;
+        g.alpha = 1.0;
+        g.beta = 0.0;
+        // seg0: Σ[i, P] · L[P, J]
+        g.a[0] = Sk + i0 + static_cast<int64_t>(c0 + wk) * rows;
+        g.lda[0] = rows;
+        g.b[0] = Lk + (c0 + wk) + static_cast<int64_t>(c0) * rows;
+        g.ldb[0] = rows;
+        g.k[0] = p;
+        if (i0 < w) {
+          // seg1: Σ[R, i]ᵀ · L[R, J]
+          g.a[1] = Sk + w + static_cast<int64_t>(i0) * rows;
+          g.lda[1] = rows;
+          g.flags |= 1 << 2;  // A transposed
+        } else {
+          g.a[1] = Uk + (i0 - w);
+          g.lda[1] = std::max(r, 1);
+        }
+        g.b[1] = Lk + w + static_cast<int64_t>(c0) * rows;
+        g.ldb[1] = rows;
+        g.k[1] = r;
+        yg[lv].push_back(g);
+      };
+      for (int i0 = c0 + wk; i0 < w; i0 += kTile) ytile(i0, std::min(i0 + kTile, w));
+      for (int i0 = w; i0 < rows; i0 += kTile) ytile(i0, std::min(i0 + kTile, rows));
+      const int nbelow = rows - c0 - wk;
+      for (int t = 0; t * kTrsmRows < nbelow; ++t) tr[lv].push_back({Lk, Sk, rows, c0, wk, w, t});
+      GemmTask z{};
+      z.c = Sk + c0 + static_cast<int64_t>(c0) * rows;
+      z.ldc = rows;
+      z.m = wk;
+      z.n = wk;
+      z.a[0] = Lk + (c0 + wk) + static_cast<int64_t>(c0) * rows;
+      z.lda[0] = rows;
+      z.b[0] = Sk + (c0 + wk) + static_cast<int64_t>(c0) * rows;
+      z.ldb[0] = rows;
+      z.k[0] = nbelow;
+      z.flags = 1;  // A transposed
+      z.alpha = 1.0;
+      z.beta = 0.0;
+      zg[lv].push_back(z);
+      dg[lv].push_back({Lk, Sk, rows, c0, wk, w, 0});
+    }
+  }
+  std::vector<ColTask> gaf;
+  std::vector<GemmTask> gmf;
+  std::vector<SelChunk> trf, dgf;
+  slev_.assign(nlev, {});
+  for (int l = 0; l < nlev; ++l) {
+    SLevel& e = slev_[l];
+    e.ga0 = gaf.size();
+    e.gan = ga[l].size();
+    gaf.insert(gaf.end(), ga[l].begin(), ga[l].end());
+    e.y0 = gmf.size();
+    e.yn = yg[l].size();
+    gmf.insert(gmf.end(), yg[l].begin(), yg[l].end());
+    e.z0 = gmf.size();
+    e.zn = zg[l].size();
+    gmf.insert(gmf.end(), zg[l].begin(), zg[l].end());
+    e.t0 = trf.size();
+    e.tn = tr[l].size();
+    trf.insert(trf.end(), tr[l].begin(), tr[l].end());
+    e.d0 = dgf.size();
+    e.dn = dg[l].size();
+    dgf.insert(dgf.end(), dg[l].begin(), dg[l].end());
+  }
+  sga_.upload(gaf, stream_);
+  sgemm_.upload(gmf, stream_);
+  strsm_.upload(trf, stream_);
+  sdiag_.upload(dgf, stream_);
+  selinv_plan_ = true;
+}
+
+int32_t DeviceFactor::numeric(const double* q, bool q_on_device) {
+  const Symbolic& s = *sym_;
+  const int64_t nnzq = static_cast<int64_t>(s.qri.size());
+  const double* dq = q;
+  if (!q_on_device) {
+    if (nnzq)
+      cuda_check(cudaMemcpyAsync(q_.p, q, nnzq * sizeof(double), cudaMemcpyHostToDevice, stream_),
+                 "copy Q");
+    dq = q_.p;
+  }
+  launches_numeric_ = 0;
+  cuda_check(cudaMemsetAsync(L_.p, 0, L_.n * sizeof(double), stream_), "memset L");
+  cuda_check(cudaMemsetAsync(U_.p, 0, U_.n * sizeof(double), stream_), "memset U");
+  int init = INT_MAX;
+  cuda_check(cudaMemcpyAsync(status_.p, &init, sizeof(int), cudaMemcpyHostToDevice, stream_),
+             "status");
+  if (nnzq) {
+    int blocks = static_cast<int>(std::min<int64_t>((nnzq + 255) / 256, 148 * 16));
+    k_scatter_q<<<blocks, 256, 0, stream_>>>(dq, qmap_.p, nnzq, L_.p);
+    ++launches_numeric_;
+  }
+  const SymDev sd = symdev();
+  for (const FLevel& lv : flev_) {
+    if (lv.ean) {
+      int blocks = static_cast<int>((lv.ean * 32 + 255) / 256);
+      k_extend_add<<<blocks, 256, 0, stream_>>>(ea_.p + lv.ea0, static_cast<int>(lv.ean), sd, L_.p,
+                                               U_.p);
+      ++launches_numeric_;
+    }
+    if (lv.pann) {
+      k_panel<<<static_cast<unsigned>(lv.pann), 128, kPanelSmem, stream_>>>(pan_.p + lv.pan0,
+                                                                          status_.p);
+      ++launches_numeric_;
+    }
+    if (lv.gmn) {
+      k_gemm_tiles<<<static_cast<unsigned>(lv.gmn), 128, 0, stream_>>>(gemm_.p + lv.gm0);
+      ++launches_numeric_;
+    }
+  }
+  cuda_check(cudaGetLastError(), "factor launch");
+  int st = INT_MAX;
+  cuda_check(cudaMemcpyAsync(&st, status_.p, sizeof(int), cudaMemcpyDeviceToHost, stream_),
+             "status read");
+  cuda_check(cudaStreamSynchronize(stream_), "numeric factorization");
+  factored_ = st == INT_MAX;
+  selinv_done_ = false;
+  return st == INT_MAX ? -1 : s.perm[st];
+}
+
+void DeviceFactor::ensure_solve_ws(int nrhs) {
+  if (nrhs <= ws_nrhs_) return;
+  const Symbolic& s = *sym_;
+  int64_t fr = 0, ur = 0;
+  for (int k = 0; k < s.ns; ++k) {
+    fr += s.rows(k);
+    ur += s.r(k);
+  }
+  F_.alloc(std::max<int64_t>(fr * nrhs, 1));
+  Uv_.alloc(std::max<int64_t>(ur * nrhs, 1));
+  v1_.alloc(std::max<int64_t>(static_cast<int64_t>(s.n) * nrhs, 1));
+  v2_.alloc(std::max<int64_t>(static_cast<int64_t>(s.n) * nrhs, 1));
+  ws_nrhs_ = nrhs;
+}
+
+void DeviceFactor::solve(int mode, int nrhs, const double* b, double* x, bool on_device) {
+  require(factored_, kContract, "solve: factor not computed");
+  require(mode >= 0 && mode <= 2, kContract, "solve_triangular: unknown mode");
+  const Symbolic& s = *sym_;
+  const int n = s.n;
+  if (n == 0 || nrhs == 0) return;
+  launches_solve_ = 0;
+  const SymDev sd = symdev();
+  for (int r0 = 0; r0 < nrhs; r0 += kMaxRhs) {
+    const int nr = std::min(kMaxRhs, nrhs - r0);
+    ensure_solve_ws(nr);
+    const double* bb = b + static_cast<int64_t>(r0) * n;
+    double* xx = x + static_cast<int64_t>(r0) * n;
+    const int64_t tot = static_cast<int64_t>(n) * nr;
+    const int pblocks = static_cast<int>(std::min<int64_t>((tot + 255) / 256, 148 * 8));
+    double* y = v1_.p;
+    if (mode == 2) {
+      const double* src = bb;
+      if (!on_device) {
+        cuda_check(cudaMemcpyAsync(v2_.p, bb, tot * sizeof(double), cudaMemcpyHostToDevice, stream_),
+                   "copy b");
+        src = v2_.p;
+      }
+      k_permute_gather<<<pblocks, 256, 0, stream_>>>(src, perm_.p, n, nr, y);
+      ++launches_solve_;
+    } else {
+      cuda_check(cudaMemcpyAsync(y, bb, tot * sizeof(double),
+                                 on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                                 stream_),
+                 "copy b");
+    }
+    if (mode == 0 || mode == 2)
+      for (int l = 0; l < s.n_levels; ++l) {
+        const int cnt = static_cast<int>(lvl_ptr_[l + 1] - lvl_ptr_[l]);
+        k_solve_fwd<<<cnt, 256, 0, stream_>>>(lvl_sn_.p + lvl_ptr_[l], sd, L_.p, y, nr, F_.p,
+                                              Uv_.p, fptr_.p, uvptr_.p);
+        ++launches_solve_;
+      }
+    if (mode == 1 || mode == 2)
+      for (int l = s.n_levels - 1; l >= 0; --l) {
+        const int cnt = static_cast<int>(lvl_ptr_[l + 1] - lvl_ptr_[l]);
+        k_solve_bwd<<<cnt, 256, 0, stream_>>>(lvl_sn_.p + lvl_ptr_[l], sd, L_.p, y, nr, F_.p,
+                                              fptr_.p);
+        ++launches_solve_;
+      }
+    if (mode == 2) {
+      double* dst = on_device ? xx : v2_.p;
+      k_permute_scatter<<<pblocks, 256, 0, stream_>>>(y, perm_.p, n, nr, dst);
+      ++launches_solve_;
+      if (!on_device)
+        cuda_check(cudaMemcpyAsync(xx, v2_.p, tot * sizeof(double), cudaMemcpyDeviceToHost, stream_),
+                   "copy x");
+    } else {
+      cuda_check(cudaMemcpyAsync(xx, y, tot * sizeof(double),
+                                 on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                                 stream_),
+                 "copy x");
+    }
+  }
+  cuda_check(cudaGetLastError(), "solve launch");
+  if (!on_device) cuda_check(cudaStreamSynchronize(stream_), "solve");
+}
+
+void DeviceFactor::selinv(double* diag_out, bool on_device) {
+  require(factored_, kContract, "selinv: factor not computed");
+  if (!selinv_plan_) build_selinv_plan();
+  const Symbolic& s = *sym_;
+  launches_selinv_ = 0;
+  const SymDev sd = symdev();
+  for (int l = static_cast<int>(slev_.size()) - 1; l >= 0; --l) {
+    const SLevel& e = slev_[l];
+    if (e.gan) {
+      int blocks = static_cast<int>((e.gan * 32 + 255) / 256);
+      k_sel_gather<<<blocks, 256, 0, stream_>>>(sga_.p + e.ga0, static_cast<int>(e.gan), sd,
+                                               snparent_.p, Sig_.p, U_.p);
+      ++launches_selinv_;
+    }
+    if (e.yn) {
+      k_gemm_tiles<<<static_cast<unsigned>(e.yn), 128, 0, stream_>>>(sgemm_.p + e.y0);
+      ++launches_selinv_;
+    }
+    if (e.tn) {
+      k_sel_trsm<<<static_cast<unsigned>(e.tn), 128, kPanelSmem, stream_>>>(strsm_.p + e.t0);
+      ++launches_selinv_;
+    }
+    if (e.zn) {
+      k_gemm_tiles<<<static_cast<unsigned>(e.zn), 128, 0, stream_>>>(sgemm_.p + e.z0);
+      ++launches_selinv_;
+    }
+    if (e.dn) {
+      k_sel_diag<<<static_cast<unsigned>(e.dn), 256, kDiagSmem, stream_>>>(sdiag_.p + e.d0);
+      ++launches_selinv_;
+    }
+  }
+  double* out = diag_out;
+  if (!on_device) {
+    ensure_solve_ws(1);
+    out = v1_.p;
+  }
+  if (s.n > 0) {
+    k_extract_diag<<<std::max(1, std::min((s.n + 255) / 256, 148 * 8)), 256, 0, stream_>>>(
+        sd, col2sn_.p, perm_.p, Sig_.p, out);
+    ++launches_selinv_;
+  }
+  cuda_check(cudaGetLastError(), "selinv launch");
+  if (!on_device) {
+    cuda_check(cudaMemcpyAsync(diag_out, out, s.n * sizeof(double), cudaMemcpyDeviceToHost, stream_),
+               "copy diag");
+    cuda_check(cudaStreamSynchronize(stream_), "selinv");
+  }
+  selinv_done_ = true;
+}
+
+void DeviceFactor::copy_l_panels(std::vector<double>& out) const {
+  out.resize(L_.n);
+  cuda_check(cudaMemcpyAsync(out.data(), L_.p, L_.n * sizeof(double), cudaMemcpyDeviceToHost, stream_),
+             "copy L");
+  cuda_check(cudaStreamSynchronize(stream_), "copy L");
+}
+
+void DeviceFactor::copy_sig_panels(std::vector<double>& out) const {
+  out.resize(Sig_.n);
+  cuda_check(cudaMemcpyAsync(out.data(), Sig_.p, Sig_.n * sizeof(double), cudaMemcpyDeviceToHost,
+                             stream_),
+             "copy Sigma");
+  cuda_check(cudaStreamSynchronize(stream_), "copy Sigma");
+}
+
+void bench_fp64(double* dmma_tflops, double* dfma_tflops) {
+  int dev = 0, sms = 0;
+  cuda_check(cudaGetDevice(&dev), "dev");
+  cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "sms");
+  DevBuf<double> o;
+  o.alloc(1);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int iters = 4096, threads = 256, blocks = sms * 4;
+  k_bench_dmma<<<blocks, threads>>>(o.p, 16);
+  cudaEventRecord(e0);
+  k_bench_dmma<<<blocks, threads>>>(o.p, iters);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  // each warp-level m8n8k4 = 8*8*4*2 flops; 8 per iteration per warp
+  double flops = double(blocks) * (threads / 32) * iters * 8 * 512.0;
+  *dmma_tflops = flops / (ms * 1e-3) / 1e12;
+  k_bench_dfma<<<blocks, threads>>>(o.p, 16);
+  cudaEventRecord(e0);
+  k_bench_dfma<<<blocks, threads>>>(o.p, iters);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  cudaEventElapsedTime(&ms, e0, e1);
+  flops = double(blocks) * threads * iters * 16 * 2.0;
+  *dfma_tflops = flops / (ms * 1e-3) / 1e12;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cuda_check(cudaGetLastError(), "bench");
+}
+
+}  // namespace gmrf

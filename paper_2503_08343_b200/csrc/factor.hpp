@@ -1,0 +1,121 @@
+// Device-resident supernodal factor: storage, launch plans and the numeric
+// factorization / solve / selected-inversion sequences.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <vector>
+
+#include "kernels.cuh"
+#include "symbolic.hpp"
+
+namespace gmrf {
+
+void cuda_check(cudaError_t e, const char* what);
+
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { reset(); }
+  void reset() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void alloc(size_t count) {
+    if (count == n && p) return;
+    reset();
+    if (count == 0) return;
+    cuda_check(cudaMalloc(&p, count * sizeof(T)), "cudaMalloc");
+    n = count;
+  }
+  void upload(const std::vector<T>& v, cudaStream_t s) {
+    alloc(v.size());
+    if (!v.empty())
+      cuda_check(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s),
+                 "upload");
+  }
+};
+
+struct FactorTimes {
+  float numeric_ms = 0, solve_ms = 0, selinv_ms = 0;
+};
+
+class DeviceFactor {
+ public:
+  explicit DeviceFactor(std::shared_ptr<const Symbolic> sym, cudaStream_t stream = nullptr);
+  ~DeviceFactor();
+
+  const Symbolic& sym() const { return *sym_; }
+  void set_stream(cudaStream_t s) { stream_ = s; }
+  cudaStream_t stream() const { return stream_; }
+
+  // Numeric factorization from Q values in the symbolic's CSC order.
+  // Returns -1 on success or the ORIGINAL index of the failing pivot.
+  int32_t numeric(const double* q, bool q_on_device);
+  // Solves; b/x are n×nrhs column-major (original coordinates for kFull,
+  // permuted coordinates for kLower/kUpper, as cholesky.hpp:179-222).
+  void solve(int mode, int nrhs, const double* b, double* x, bool on_device);
+  // Selected inversion; fills the Σ panels and returns diag(Q⁻¹) in original order.
+  void selinv(double* diag_out, bool on_device);
+
+  // Host copies (tests / small n).
+  void copy_l_panels(std::vector<double>& out) const;
+  void copy_sig_panels(std::vector<double>& out) const;
+
+  double* d_l() { return L_.p; }
+  double* d_sig() { return Sig_.p; }
+  bool factored() const { return factored_; }
+  bool has_selinv() const { return selinv_done_; }
+  int64_t device_bytes() const;
+  int64_t launches_numeric() const { return launches_numeric_; }
+  int64_t launches_solve() const { return launches_solve_; }
+  int64_t launches_selinv() const { return launches_selinv_; }
+
+ private:
+  void build_factor_plan();
+  void build_selinv_plan();
+  void ensure_solve_ws(int nrhs);
+  SymDev symdev() const;
+
+  std::shared_ptr<const Symbolic> sym_;
+  cudaStream_t stream_;
+  bool factored_ = false, selinv_done_ = false;
+
+  DevBuf<int32_t> first_, rows_, relmap_, chptr_, chlist_, perm_, col2sn_, snparent_, status_;
+  DevBuf<int64_t> rptr_, lptr_, uptr_, qmap_, fptr_, uvptr_;
+  DevBuf<double> L_, U_, Sig_, q_, F_, Uv_, v1_, v2_;
+  int ws_nrhs_ = 0;
+
+  struct FLevel {
+    int64_t ea0, ean, pan0, pann, gm0, gmn;
+  };
+  std::vector<FLevel> flev_;
+  DevBuf<ColTask> ea_;
+  DevBuf<PanelTask> pan_;
+  DevBuf<GemmTask> gemm_;
+
+  struct SLevel {
+    int64_t ga0, gan, y0, yn, t0, tn, z0, zn, d0, dn;
+  };
+  std::vector<SLevel> slev_;
+  DevBuf<ColTask> sga_;
+  DevBuf<GemmTask> sgemm_;
+  DevBuf<SelChunk> strsm_, sdiag_;
+  bool selinv_plan_ = false;
+
+  std::vector<int64_t> lvl_ptr_;
+  DevBuf<int32_t> lvl_sn_;
+
+  int64_t launches_numeric_ = 0, launches_solve_ = 0, launches_selinv_ = 0;
+};
+
+// FP64 issue-rate microbenchmarks (TFLOP/s), for the roofline denominator.
+void bench_fp64(double* dmma_tflops, double* dfma_tflops);
+
+}  // namespace gmrf

@@ -1,0 +1,576 @@
+// sm_100a kernels for the supernodal multifrontal Cholesky, the supernodal
+// triangular solves and the supernodal selected inversion (FP64).
+//
+// FP64 tensor math on Blackwell is DMMA (mma.sync ... .f64); tcgen05 has no
+// f64 kind. The GEMM tile kernel stages operands through shared
+// memory with cp.async double buffering and issues m8n8k4 DMMA.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kernels.cuh"
+
+namespace gmrf {
+
+// ---------------------------------------------------------------------------
+// DMMA primitive: D(8x8) += A(8x4, row) * B(4x8, col), one f64 per lane for A
+// and B, two for C/D. Fragment layout (PTX ISA, mma.m8n8k4 .f64):
+//   A: row = lane>>2, col = lane&3;  B: row = lane&3, col = lane>>2;
+//   C: row = lane>>2, col = 2*(lane&3) + i.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile(
+      "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pred) {
+  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  int sz = pred ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// ---------------------------------------------------------------------------
+// Batched tile GEMM: one 64x64 output tile per CTA, 4 warps (2x2), each warp a
+// 32x32 sub-tile = 4x4 DMMA m8n8 fragments. K staged in chunks of 16.
+// ---------------------------------------------------------------------------
+constexpr int kKC = 16;
+constexpr int kPad = 72;  // smem row pitch (doubles): conflict-free fragment loads
+
+__device__ __forceinline__ void load_operand(double (*dst)[kPad], const double* src, int ld,
+                                             bool kcontig, int mn_lim, int k0, int k_lim,
+                                             int tid) {
+  // dst[kk][mm] = op(src)(mm, k0+kk)
+  if (!kcontig) {
+    // element (mm, kk) at src[mm + kk*ld]: mm contiguous
+#pragma unroll
+    for (int it = 0; it < (kKC * kTile) / 128; ++it) {
+      int idx = tid + it * 128;
+      int kk = idx >> 6, mm = idx & 63;
+      bool ok = mm < mn_lim && (k0 + kk) < k_lim;
+      const double* p = ok ? src + mm + static_cast<int64_t>(k0 + kk) * ld : src;
+      cp_async8(&dst[kk][mm], p, ok);
+    }
+  } else {
+    // element (mm, kk) at src[kk + mm*ld]: kk contiguous
+#pragma unroll
+    for (int it = 0; it < (kKC * kTile) / 128; ++it) {
+      int idx = tid + it * 128;
+      int mm = idx >> 4, kk = idx & 15;
+      bool ok = mm < mn_lim && (k0 + kk) < k_lim;
+      const double* p = ok ? src + (k0 + kk) + static_cast<int64_t>(mm) * ld : src;
+      cp_async8(&dst[kk][mm], p, ok);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(128) k_gemm_tiles(const GemmTask* __restrict__ tasks) {
+  __shared__ __align__(16) double As[2][kKC][kPad];
+  __shared__ __align__(16) double Bs[2][kKC][kPad];
+  const GemmTask& t = tasks[blockIdx.x];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp & 1, wn = warp >> 1;
+  const int m = t.m, n = t.n;
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  for (int seg = 0; seg < 2; ++seg) {
+    const int K = t.k[seg];
+    if (K <= 0) continue;
+    const double* A = t.a[seg];
+    const double* B = t.b[seg];
+    const int lda = t.lda[seg], ldb = t.ldb[seg];
+    // A: N → mm contiguous; T → kk contiguous. B: N → kk contiguous; T → nn contiguous.
+    const bool a_kc = (t.flags >> (2 * seg)) & 1;
+    const bool b_kc = !((t.flags >> (2 * seg + 1)) & 1);
+    const int nk = (K + kKC - 1) / kKC;
+    load_operand(As[0], A, lda, a_kc, m, 0, K, tid);
+    load_operand(Bs[0], B, ldb, b_kc, n, 0, K, tid);
+    cp_async_commit();
+    for (int kc = 0; kc < nk; ++kc) {
+      const int buf = kc & 1;
+      if (kc + 1 < nk) {
+        load_operand(As[buf ^ 1], A, lda, a_kc, m, (kc + 1) * kKC, K, tid);
+        load_operand(Bs[buf ^ 1], B, ldb, b_kc, n, (kc + 1) * kKC, K, tid);
+        cp_async_commit();
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncthreads();
+#pragma unroll
+      for (int kk = 0; kk < kKC; kk += 4) {
+        double af[4], bf[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) af[i] = As[buf][kk + (lane & 3)][wm * 32 + i * 8 + (lane >> 2)];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) bf[j] = Bs[buf][kk + (lane & 3)][wn * 32 + j * 8 + (lane >> 2)];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+      }
+      __syncthreads();
+    }
+  }
+  const double alpha = t.alpha, beta = t.beta;
+  double* C = t.c;
+  const int64_t ldc = t.ldc;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int row = wm * 32 + i * 8 + (lane >> 2);
+    if (row >= m) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int col = wn * 32 + j * 8 + (lane & 3) * 2 + e;
+        if (col < n) {
+          double* p = C + row + col * ldc;
+          *p = beta == 0.0 ? alpha * acc[i][j][e] : beta * *p + alpha * acc[i][j][e];
+        }
+      }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Panel step: factor the chunk's w×w diagonal block in shared memory (every
+// CTA of the chunk does it redundantly and identically) and solve its slab of
+// the rows below: X = B · L11⁻ᵀ. Non-positive pivots are reported as the
+// smallest failing internal column (reference cholesky.hpp:153-156 semantics).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) k_panel(const PanelTask* __restrict__ tasks,
+                                               int32_t* __restrict__ status) {
+  extern __shared__ double smem[];
+  const PanelTask& t = tasks[blockIdx.x];
+  const int w = t.w, ld = t.ld, tid = threadIdx.x;
+  double* D = smem;                       // [kNB][kNB+1] column-major: D[j*(kNB+1)+i]
+  double* X = smem + kNB * (kNB + 1);     // [kNB][kTrsmRows+1]: X[j*(kTrsmRows+1)+r]
+  constexpr int DP = kNB + 1, XP = kTrsmRows + 1;
+  for (int idx = tid; idx < w * w; idx += blockDim.x) {
+    int i = idx % w, j = idx / w;
+    if (i >= j) D[j * DP + i] = t.d[i + static_cast<int64_t>(j) * ld];
+  }
+  __syncthreads();
+  for (int j = 0; j < w; ++j) {
+    if (tid == 0) {
+      double dj = D[j * DP + j];
+      if (!(dj > 0.0) && t.tile == 0) atomicMin(status, t.gcol + j);
+      D[j * DP + j] = sqrt(dj);
+    }
+    __syncthreads();
+    const double djj = D[j * DP + j];
+    for (int i = j + 1 + tid; i < w; i += blockDim.x) D[j * DP + i] /= djj;
+    __syncthreads();
+    const int rem = w - j - 1;
+    for (int idx = tid; idx < rem * rem; idx += blockDim.x) {
+      int i = j + 1 + idx % rem, k = j + 1 + idx / rem;
+      if (i >= k) D[k * DP + i] -= D[j * DP + i] * D[j * DP + k];
+    }
+    __syncthreads();
+  }
+  if (t.tile == 0)
+    for (int idx = tid; idx < w * w; idx += blockDim.x) {
+      int i = idx % w, j = idx / w;
+      if (i >= j) t.d[i + static_cast<int64_t>(j) * ld] = D[j * DP + i];
+    }
+  const int r0 = t.tile * kTrsmRows;
+  const int nr = min(kTrsmRows, t.nbelow - r0);
+  if (nr <= 0) return;
+  double* B = t.d + w + r0;  // row (w + r0) of the chunk's columns
+  for (int idx = tid; idx < nr * w; idx += blockDim.x) {
+    int r = idx % nr, j = idx / nr;
+    X[j * XP + r] = B[r + static_cast<int64_t>(j) * ld];
+  }
+  __syncthreads();
+  if (tid < nr) {
+    for (int j = 0; j < w; ++j) {
+      double s = X[j * XP + tid];
+      for (int l = 0; l < j; ++l) s -= X[l * XP + tid] * D[l * DP + j];
+      X[j * XP + tid] = s / D[j * DP + j];
+    }
+  }
+  __syncthreads();
+  for (int idx = tid; idx < nr * w; idx += blockDim.x) {
+    int r = idx % nr, j = idx / nr;
+    B[r + static_cast<int64_t>(j) * ld] = X[j * XP + r];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Extend-add (multifrontal assembly), gather form: one warp per (front, front
+// column). Children are visited in ascending order, so every target entry
+// receives its contributions in a fixed order (deterministic, no atomics).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int find_sorted(const int32_t* a, int len, int key) {
+  int lo = 0, hi = len;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (a[mid] < key) lo = mid + 1; else hi = mid;
+  }
+  return (lo < len && a[lo] == key) ? lo : -1;
+}
+
+__global__ void k_extend_add(const ColTask* __restrict__ tasks, int ntasks, SymDev sd,
+                             double* __restrict__ L, double* __restrict__ U) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= ntasks) return;
+  const int s = tasks[warp].sn, b = tasks[warp].col;
+  const int w = sd.sn_first[s + 1] - sd.sn_first[s];
+  const int rows = static_cast<int>(sd.sn_rptr[s + 1] - sd.sn_rptr[s]);
+  const int r = rows - w;
+  double* Ls = L + sd.lptr[s];
+  double* Us = U + sd.uptr[s];
+  for (int q = sd.ch_ptr[s]; q < sd.ch_ptr[s + 1]; ++q) {
+    const int c = sd.ch_list[q];
+    const int wc = sd.sn_first[c + 1] - sd.sn_first[c];
+    const int rc = static_cast<int>(sd.sn_rptr[c + 1] - sd.sn_rptr[c]) - wc;
+    const int32_t* rel = sd.relmap + sd.sn_rptr[c] + wc;
+    const int ib = find_sorted(rel, rc, b);
+    if (ib < 0) continue;
+    const double* Uc = U + sd.uptr[c] + static_cast<int64_t>(ib) * rc;
+    if (b < w) {
+      double* dst = Ls + static_cast<int64_t>(b) * rows;
+      for (int ia = ib + lane; ia < rc; ia += 32) dst[rel[ia]] += Uc[ia];
+    } else {
+      double* dst = Us + static_cast<int64_t>(b - w) * r - w;
+      for (int ia = ib + lane; ia < rc; ia += 32) dst[rel[ia]] += Uc[ia];
+    }
+    __syncwarp();
+  }
+}
+
+// Q values → L panels through the precomputed offset map.
+__global__ void k_scatter_q(const double* __restrict__ q, const int64_t* __restrict__ qmap,
+                            int64_t nnz, double* __restrict__ L) {
+  for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < nnz;
+       p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int64_t o = qmap[p];
+    if (o >= 0) L[o] = q[p];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Triangular solves: one CTA per supernode of a tree level, all right-hand
+// sides at once so each L panel column is read once per sweep.
+// y/x: permuted vectors, n × nrhs column-major. F: per-supernode front
+// vectors (rows_s × nrhs), Uv: update vectors (r_s × nrhs).
+// ---------------------------------------------------------------------------
+constexpr int kMaxRhs = 16;
+
+__global__ void __launch_bounds__(256) k_solve_fwd(const int32_t* __restrict__ sns, SymDev sd,
+                                                   const double* __restrict__ L,
+                                                   double* __restrict__ y, int nrhs,
+                                                   double* __restrict__ F,
+                                                   double* __restrict__ Uv,
+                                                   const int64_t* __restrict__ fptr,
+                                                   const int64_t* __restrict__ uvptr) {
+  const int s = sns[blockIdx.x];
+  const int f0 = sd.sn_first[s];
+  const int w = sd.sn_first[s + 1] - f0;
+  const int rows = static_cast<int>(sd.sn_rptr[s + 1] - sd.sn_rptr[s]);
+  const int r = rows - w;
+  const int n = sd.n;
+  const double* Ls = L + sd.lptr[s];
+  double* f = F + fptr[s] * nrhs;
+  const int tid = threadIdx.x;
+  for (int idx = tid; idx < rows * nrhs; idx += blockDim.x) {
+    int a = idx % rows, rr = idx / rows;
+    f[idx] = a < w ? y[f0 + a + static_cast<int64_t>(rr) * n] : 0.0;
+  }
+  __syncthreads();
+  for (int q = sd.ch_ptr[s]; q < sd.ch_ptr[s + 1]; ++q) {
+    const int c = sd.ch_list[q];
+    const int wc = sd.sn_first[c + 1] - sd.sn_first[c];
+    const int rc = static_cast<int>(sd.sn_rptr[c + 1] - sd.sn_rptr[c]) - wc;
+    const int32_t* rel = sd.relmap + sd.sn_rptr[c] + wc;
+    const double* uc = Uv + uvptr[c] * nrhs;
+    for (int idx = tid; idx < rc * nrhs; idx += blockDim.x) {
+      int ia = idx % rc, rr = idx / rc;
+      f[rel[ia] + rr * rows] += uc[idx];
+    }
+    __syncthreads();
+  }
+  for (int j = 0; j < w; ++j) {
+    const double* lj = Ls + static_cast<int64_t>(j) * rows;
+    const double ljj = lj[j];
+    double fj[kMaxRhs];
+#pragma unroll
+    for (int rr = 0; rr < kMaxRhs; ++rr) fj[rr] = rr < nrhs ? f[j + rr * rows] / ljj : 0.0;
+    for (int i = j + 1 + tid; i < rows; i += blockDim.x) {
+      const double lij = lj[i];
+#pragma unroll
+      for (int rr = 0; rr < kMaxRhs; ++rr)
+        if (rr < nrhs) f[i + rr * rows] -= lij * fj[rr];
+    }
+    __syncthreads();
+    if (tid == 0)
+      for (int rr = 0; rr < nrhs; ++rr) f[j + rr * rows] = fj[rr];
+    __syncthreads();
+  }
+  for (int idx = tid; idx < rows * nrhs; idx += blockDim.x) {
+    int a = idx % rows, rr = idx / rows;
+    if (a < w)
+      y[f0 + a + static_cast<int64_t>(rr) * n] = f[idx];
+    else
+      Uv[uvptr[s] * nrhs + (a - w) + rr * r] = f[idx];
+  }
+}
+
+__global__ void __launch_bounds__(256) k_solve_bwd(const int32_t* __restrict__ sns, SymDev sd,
+                                                   const double* __restrict__ L,
+                                                   double* __restrict__ x, int nrhs,
+                                                   double* __restrict__ F,
+                                                   const int64_t* __restrict__ fptr) {
+  __shared__ double red[8][kMaxRhs];
+  const int s = sns[blockIdx.x];
+  const int f0 = sd.sn_first[s];
+  const int w = sd.sn_first[s + 1] - f0;
+  const int rows = static_cast<int>(sd.sn_rptr[s + 1] - sd.sn_rptr[s]);
+  const int n = sd.n;
+  const int32_t* srows = sd.sn_rows + sd.sn_rptr[s];
+  const double* Ls = L + sd.lptr[s];
+  double* f = F + fptr[s] * nrhs;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int idx = tid; idx < rows * nrhs; idx += blockDim.x) {
+    int a = idx % rows, rr = idx / rows;
+    f[idx] = x[srows[a] + static_cast<int64_t>(rr) * n];
+  }
+  __syncthreads();
+  for (int j = w - 1; j >= 0; --j) {
+    const double* lj = Ls + static_cast<int64_t>(j) * rows;
+    double part[kMaxRhs];
+#pragma unroll
+    for (int rr = 0; rr < kMaxRhs; ++rr) part[rr] = 0.0;
+    for (int i = j + 1 + tid; i < rows; i += blockDim.x) {
+      const double lij = lj[i];
+#pragma unroll
+      for (int rr = 0; rr < kMaxRhs; ++rr)
+        if (rr < nrhs) part[rr] += lij * f[i + rr * rows];
+    }
+#pragma unroll
+    for (int rr = 0; rr < kMaxRhs; ++rr) {
+      if (rr >= nrhs) break;
+      double v = part[rr];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) red[warp][rr] = v;
+    }
+    __syncthreads();
+    if (tid < nrhs) {
+      double v = 0.0;
+      for (int q = 0; q < 8; ++q) v += red[q][tid];
+      f[j + tid * rows] = (f[j + tid * rows] - v) / lj[j];
+    }
+    __syncthreads();
+  }
+  for (int idx = tid; idx < w * nrhs; idx += blockDim.x) {
+    int a = idx % w, rr = idx / w;
+    x[f0 + a + static_cast<int64_t>(rr) * n] = f[a + rr * rows];
+  }
+}
+
+// out[i + r*n] = in[perm[i] + r*n]  (gather: P b)
+__global__ void k_permute_gather(const double* __restrict__ in, const int32_t* __restrict__ perm,
+                                 int n, int nrhs, double* __restrict__ out) {
+  int64_t tot = static_cast<int64_t>(n) * nrhs;
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < tot;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int64_t r = idx / n, i = idx % n;
+    out[idx] = in[perm[i] + r * n];
+  }
+}
+// out[perm[i] + r*n] = in[i + r*n]  (scatter: Pᵀ y)
+__global__ void k_permute_scatter(const double* __restrict__ in, const int32_t* __restrict__ perm,
+                                  int n, int nrhs, double* __restrict__ out) {
+  int64_t tot = static_cast<int64_t>(n) * nrhs;
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < tot;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int64_t r = idx / n, i = idx % n;
+    out[perm[i] + r * n] = in[idx];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Selected inversion (supernodal Takahashi, top-down).
+// ---------------------------------------------------------------------------
+// Σ_RR(s) (full r×r, stored in the U buffer) gathered from the parent's Σ front.
+__global__ void k_sel_gather(const ColTask* __restrict__ tasks, int ntasks, SymDev sd,
+                             const int32_t* __restrict__ sn_parent, const double* __restrict__ Sig,
+                             double* __restrict__ U) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= ntasks) return;
+  const int s = tasks[warp].sn, b = tasks[warp].col;  // b: column of Σ_RR(s), 0..r-1
+  const int w = sd.sn_first[s + 1] - sd.sn_first[s];
+  const int r = static_cast<int>(sd.sn_rptr[s + 1] - sd.sn_rptr[s]) - w;
+  const int p = sn_parent[s];
+  const int wp = sd.sn_first[p + 1] - sd.sn_first[p];
+  const int rowsp = static_cast<int>(sd.sn_rptr[p + 1] - sd.sn_rptr[p]);
+  const int rp = rowsp - wp;
+  const int32_t* rel = sd.relmap + sd.sn_rptr[s] + w;
+  const double* Sp = Sig + sd.lptr[p];
+  const double* Up = U + sd.uptr[p];
+  double* dst = U + sd.uptr[s] + static_cast<int64_t>(b) * r;
+  const int y = rel[b];
+  for (int a = lane; a < r; a += 32) {
+    const int x = rel[a];
+    double v;
+    if (y < wp)
+      v = Sp[x + static_cast<int64_t>(y) * rowsp];       // panel column y (full in diag block)
+    else if (x < wp)
+      v = Sp[y + static_cast<int64_t>(x) * rowsp];       // mirror of panel column x
+    else
+      v = Up[(x - wp) + static_cast<int64_t>(y - wp) * rp];
+    dst[a] = v;
+  }
+}
+
+// Σ_{R_k,J} ← −Σ_{R_k,J} · L_JJ⁻¹ (in place), one slab of kTrsmRows rows.
+__global__ void __launch_bounds__(128) k_sel_trsm(const SelChunk* __restrict__ tasks) {
+  extern __shared__ double smem[];
+  const SelChunk& t = tasks[blockIdx.x];
+  const int w = t.w, ld = t.ld, tid = threadIdx.x;
+  constexpr int DP = kNB + 1, XP = kTrsmRows + 1;
+  double* D = smem;
+  double* X = smem + kNB * DP;
+  const double* Lk = t.l + t.c0 + static_cast<int64_t>(t.c0) * ld;
+  for (int idx = tid; idx < w * w; idx += blockDim.x) {
+    int i = idx % w, j = idx / w;
+    if (i >= j) D[j * DP + i] = Lk[i + static_cast<int64_t>(j) * ld];
+  }
+  const int nbelow = ld - t.c0 - w;
+  const int r0 = t.tile * kTrsmRows;
+  const int nr = min(kTrsmRows, nbelow - r0);
+  double* B = t.sig + t.c0 + w + r0 + static_cast<int64_t>(t.c0) * ld;
+  for (int idx = tid; idx < nr * w; idx += blockDim.x) {
+    int r = idx % nr, j = idx / nr;
+    X[j * XP + r] = -B[r + static_cast<int64_t>(j) * ld];
+  }
+  __syncthreads();
+  if (tid < nr) {
+    // x · L = b  → x_j = (b_j − Σ_{l>j} x_l L_lj) / L_jj, j descending
+    for (int j = w - 1; j >= 0; --j) {
+      double s = X[j * XP + tid];
+      for (int l = j + 1; l < w; ++l) s -= X[l * XP + tid] * D[j * DP + l];
+      X[j * XP + tid] = s / D[j * DP + j];
+    }
+  }
+  __syncthreads();
+  for (int idx = tid; idx < nr * w; idx += blockDim.x) {
+    int r = idx % nr, j = idx / nr;
+    B[r + static_cast<int64_t>(j) * ld] = X[j * XP + r];
+  }
+}
+
+// Σ_JJ = L_JJ⁻ᵀ (L_JJ⁻¹ − Z), Z = L_{R,J}ᵀ Σ_{R,J} already stored in the Σ
+// diagonal block; writes Σ_JJ symmetric and mirrors Σ_{P,J} into Σ_{J,P}.
+__global__ void __launch_bounds__(256) k_sel_diag(const SelChunk* __restrict__ tasks) {
+  extern __shared__ double smem[];
+  const SelChunk& t = tasks[blockIdx.x];
+  const int w = t.w, ld = t.ld, tid = threadIdx.x;
+  constexpr int P = kNB + 1;
+  double* Lm = smem;            // L_JJ (lower)
+  double* Li = smem + kNB * P;  // L_JJ⁻¹ (lower)
+  double* W = smem + 2 * kNB * P;  // L⁻¹ − Z
+  const double* Lk = t.l + t.c0 + static_cast<int64_t>(t.c0) * ld;
+  double* Sk = t.sig + t.c0 + static_cast<int64_t>(t.c0) * ld;
+  for (int idx = tid; idx < w * w; idx += blockDim.x) {
+    int i = idx % w, j = idx / w;
+    Lm[j * P + i] = i >= j ? Lk[i + static_cast<int64_t>(j) * ld] : 0.0;
+    W[j * P + i] = -Sk[i + static_cast<int64_t>(j) * ld];
+  }
+  __syncthreads();
+  if (tid < w) {
+    const int c = tid;
+    for (int i = 0; i < w; ++i) {
+      double v;
+      if (i < c) {
+        v = 0.0;
+      } else {
+        double s = (i == c) ? 1.0 : 0.0;
+        for (int l = c; l < i; ++l) s -= Lm[l * P + i] * Li[c * P + l];
+        v = s / Lm[i * P + i];
+      }
+      Li[c * P + i] = v;
+    }
+  }
+  __syncthreads();
+  for (int idx = tid; idx < w * w; idx += blockDim.x) {
+    int i = idx % w, j = idx / w;
+    W[j * P + i] += Li[j * P + i];
+  }
+  __syncthreads();
+  for (int idx = tid; idx < w * w; idx += blockDim.x) {
+    int i = idx % w, j = idx / w;
+    if (i < j) continue;
+    double s = 0.0;
+    for (int l = i; l < w; ++l) s += Li[i * P + l] * W[j * P + l];  // (L⁻ᵀ)_{i,l} = Li[l][i]
+    Sk[i + static_cast<int64_t>(j) * ld] = s;
+    Sk[j + static_cast<int64_t>(i) * ld] = s;
+  }
+  // mirror Σ_{P,J} → Σ_{J,P} for the earlier chunks of this supernode
+  const int p = t.wsn - t.c0 - w;
+  for (int idx = tid; idx < p * w; idx += blockDim.x) {
+    int pi = idx % p, j = idx / p;
+    Sk[j + static_cast<int64_t>(w + pi) * ld] = Sk[(w + pi) + static_cast<int64_t>(j) * ld];
+  }
+}
+
+// var[perm[j]] = Σ_jj
+__global__ void k_extract_diag(SymDev sd, const int32_t* __restrict__ col2sn,
+                               const int32_t* __restrict__ perm, const double* __restrict__ Sig,
+                               double* __restrict__ out) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < sd.n; j += gridDim.x * blockDim.x) {
+    const int s = col2sn[j];
+    const int f0 = sd.sn_first[s];
+    const int64_t rows = sd.sn_rptr[s + 1] - sd.sn_rptr[s];
+    const int a = j - f0;
+    out[perm[j]] = Sig[sd.lptr[s] + a + a * rows];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Microbenchmarks for the FP64 roofline denominator (DMMA vs DFMA issue rate).
+// ---------------------------------------------------------------------------
+__global__ void k_bench_dmma(double* out, int iters) {
+  double c[8][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) c[i][0] = c[i][1] = 0.0;
+  double a = 1.0 + threadIdx.x * 1e-9, b = 1.0 - threadIdx.x * 1e-9;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) dmma884(c[i][0], c[i][1], a, b);
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += c[i][0] + c[i][1];
+  if (s == 12345.678) out[0] = s;
+}
+
+__global__ void k_bench_dfma(double* out, int iters) {
+  double c[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) c[i] = i;
+  double a = 1.0 + threadIdx.x * 1e-9, b = 1e-9;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) c[i] = fma(c[i], a, b);
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) s += c[i];
+  if (s == 12345.678) out[0] = s;
+}
+
+}  // namespace gmrf

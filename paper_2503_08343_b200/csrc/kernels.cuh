@@ -1,0 +1,67 @@
+// Device-side task descriptors shared by the plan builder and the kernels.
+#pragma once
+
+#include <cstdint>
+
+namespace gmrf {
+
+constexpr int kNB = 64;        // supernode chunk width (columns per dense panel step)
+constexpr int kTile = 64;      // GEMM output tile (kTile x kTile)
+constexpr int kTrsmRows = 128; // rows per TRSM task
+
+// C = beta*C + alpha * Σ_seg opA(A_seg) · opB(B_seg), all column-major.
+// opA(A) is m×k: N → A(i,l) = a[i + l*lda]; T → a[l + i*lda].
+// opB(B) is k×n: N → B(l,j) = b[l + j*ldb]; T → b[j + l*ldb].
+struct GemmTask {
+  double* c;
+  const double* a[2];
+  const double* b[2];
+  int32_t ldc;
+  int32_t lda[2], ldb[2];
+  int32_t m, n;
+  int32_t k[2];
+  int32_t flags;  // bit (2*seg): transA, bit (2*seg+1): transB
+  double alpha, beta;
+};
+
+// Diagonal-block Cholesky + TRSM of the rows below it, for one chunk.
+struct PanelTask {
+  double* d;          // top-left of the chunk's diagonal block
+  int32_t ld;         // panel leading dimension (rows of the supernode)
+  int32_t w;          // chunk width (<= kNB)
+  int32_t nbelow;     // rows below the diagonal block
+  int32_t tile;       // which kTrsmRows-row slab of the rows below
+  int32_t gcol;       // internal index of the chunk's first column
+};
+
+// Extend-add / Σ-gather work item: one (supernode, front column) pair.
+struct ColTask {
+  int32_t sn;
+  int32_t col;
+};
+
+// Selected-inversion per-chunk dense work.
+struct SelChunk {
+  const double* l;   // L panel of the supernode
+  double* sig;       // Σ panel of the supernode
+  int32_t ld;        // rows of the supernode
+  int32_t c0;        // chunk offset inside the panel
+  int32_t w;         // chunk width
+  int32_t wsn;       // supernode width
+  int32_t tile;      // TRSM row slab (for the TRSM kernel)
+};
+
+// Device view of the symbolic structure (all arrays device-resident).
+struct SymDev {
+  const int32_t* sn_first;
+  const int64_t* sn_rptr;
+  const int32_t* sn_rows;
+  const int32_t* relmap;
+  const int32_t* ch_ptr;
+  const int32_t* ch_list;
+  const int64_t* lptr;
+  const int64_t* uptr;
+  int32_t n;
+};
+
+}  // namespace gmrf
