@@ -20,8 +20,8 @@ constexpr int kDiagSmem = 3 * kNB * (kNB + 1) * sizeof(double);
 void set_smem_attrs() {
   static bool done = false;
   if (done) return;
-  cuda_check(cudaFuncSetAttribute(k_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPanelSmem),
-             "smem k_panel");
+  cuda_check(cudaFuncSetAttribute(k_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, kPanelSmem),
+             "smem k_trsm");
   cuda_check(
       cudaFuncSetAttribute(k_sel_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, kPanelSmem),
       "smem k_sel_trsm");
@@ -118,7 +118,7 @@ void DeviceFactor::build_factor_plan() {
   int nlev = 0;
   chunk_levels(s, lvl0, nlev);
   std::vector<std::vector<ColTask>> ea(nlev);
-  std::vector<std::vector<PanelTask>> pan(nlev);
+  std::vector<std::vector<PanelTask>> pan(nlev), po(nlev);
   std::vector<std::vector<GemmTask>> gm(nlev);
   double* L = L_.p;
   double* U = U_.p;
@@ -133,10 +133,14 @@ void DeviceFactor::build_factor_plan() {
       if (c == 0 && s.ch_ptr[k + 1] > s.ch_ptr[k])
         for (int b = 0; b < rows; ++b) ea[lv].push_back({k, b});
       const int nbelow = rows - c0 - wk;
-      const int nt = std::max(1, (nbelow + kTrsmRows - 1) / kTrsmRows);
-      for (int t = 0; t < nt; ++t)
-        pan[lv].push_back({Lk + c0 + static_cast<int64_t>(c0) * rows, rows, wk, nbelow, t,
-                           s.sn_first[k] + c0});
+      const PanelTask pt{Lk + c0 + static_cast<int64_t>(c0) * rows, rows, wk, nbelow, 0,
+                         s.sn_first[k] + c0};
+      po[lv].push_back(pt);
+      for (int t = 0; t * kTrsmRows < nbelow; ++t) {
+        PanelTask tt = pt;
+        tt.tile = t;
+        pan[lv].push_back(tt);
+      }
       // right-looking update of the trailing panel columns with this chunk
       for (int jb = c0 + wk; jb < w; jb += kTile)
         for (int ib = jb; ib < rows; ib += kTile) {
@@ -177,19 +181,22 @@ void DeviceFactor::build_factor_plan() {
     }
   }
   std::vector<ColTask> eaf;
-  std::vector<PanelTask> panf;
+  std::vector<PanelTask> panf, pof;
   std::vector<GemmTask> gmf;
   flev_.assign(nlev, {});
   for (int l = 0; l < nlev; ++l) {
     flev_[l] = {static_cast<int64_t>(eaf.size()), static_cast<int64_t>(ea[l].size()),
+                static_cast<int64_t>(pof.size()), static_cast<int64_t>(po[l].size()),
                 static_cast<int64_t>(panf.size()), static_cast<int64_t>(pan[l].size()),
                 static_cast<int64_t>(gmf.size()), static_cast<int64_t>(gm[l].size())};
+    pof.insert(pof.end(), po[l].begin(), po[l].end());
     eaf.insert(eaf.end(), ea[l].begin(), ea[l].end());
     panf.insert(panf.end(), pan[l].begin(), pan[l].end());
     gmf.insert(gmf.end(), gm[l].begin(), gm[l].end());
   }
   ea_.upload(eaf, stream_);
   pan_.upload(panf, stream_);
+  po_.upload(pof, stream_);
   gemm_.upload(gmf, stream_);
 }
 
@@ -324,9 +331,12 @@ int32_t DeviceFactor::numeric(const double* q, bool q_on_device) {
                                                U_.p);
       ++launches_numeric_;
     }
+    if (lv.pon) {
+      k_potrf<<<static_cast<unsigned>(lv.pon), 128, 0, stream_>>>(po_.p + lv.po0, status_.p);
+      ++launches_numeric_;
+    }
     if (lv.pann) {
-      k_panel<<<static_cast<unsigned>(lv.pann), 128, kPanelSmem, stream_>>>(pan_.p + lv.pan0,
-                                                                          status_.p);
+      k_trsm<<<static_cast<unsigned>(lv.pann), 128, kPanelSmem, stream_>>>(pan_.p + lv.pan0);
       ++launches_numeric_;
     }
     if (lv.gmn) {

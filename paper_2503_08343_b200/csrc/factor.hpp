@@ -93,11 +93,11 @@ class DeviceFactor {
   int ws_nrhs_ = 0;
 
   struct FLevel {
-    int64_t ea0, ean, pan0, pann, gm0, gmn;
+    int64_t ea0, ean, po0, pon, pan0, pann, gm0, gmn;
   };
   std::vector<FLevel> flev_;
   DevBuf<ColTask> ea_;
-  DevBuf<PanelTask> pan_;
+  DevBuf<PanelTask> pan_, po_;
   DevBuf<GemmTask> gemm_;
 
   struct SLevel {

@@ -143,19 +143,16 @@ __global__ void __launch_bounds__(128) k_gemm_tiles(const GemmTask* __restrict__
 }
 
 // ---------------------------------------------------------------------------
-// Panel step: factor the chunk's w×w diagonal block in shared memory (every
-// CTA of the chunk does it redundantly and identically) and solve its slab of
-// the rows below: X = B · L11⁻ᵀ. Non-positive pivots are reported as the
-// smallest failing internal column (reference cholesky.hpp:153-156 semantics).
+// Panel step, part 1: Cholesky of the chunk's w×w diagonal block in shared
+// memory, one CTA per chunk. Non-positive pivots are reported as the smallest
+// failing internal column (reference cholesky.hpp:153-156 semantics).
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(128) k_panel(const PanelTask* __restrict__ tasks,
+__global__ void __launch_bounds__(128) k_potrf(const PanelTask* __restrict__ tasks,
                                                int32_t* __restrict__ status) {
-  extern __shared__ double smem[];
+  __shared__ double D[kNB * (kNB + 1)];  // column-major, pitch kNB+1
   const PanelTask& t = tasks[blockIdx.x];
   const int w = t.w, ld = t.ld, tid = threadIdx.x;
-  double* D = smem;                       // [kNB][kNB+1] column-major: D[j*(kNB+1)+i]
-  double* X = smem + kNB * (kNB + 1);     // [kNB][kTrsmRows+1]: X[j*(kTrsmRows+1)+r]
-  constexpr int DP = kNB + 1, XP = kTrsmRows + 1;
+  constexpr int DP = kNB + 1;
   for (int idx = tid; idx < w * w; idx += blockDim.x) {
     int i = idx % w, j = idx / w;
     if (i >= j) D[j * DP + i] = t.d[i + static_cast<int64_t>(j) * ld];
@@ -164,7 +161,7 @@ __global__ void __launch_bounds__(128) k_panel(const PanelTask* __restrict__ tas
   for (int j = 0; j < w; ++j) {
     if (tid == 0) {
       double dj = D[j * DP + j];
-      if (!(dj > 0.0) && t.tile == 0) atomicMin(status, t.gcol + j);
+      if (!(dj > 0.0)) atomicMin(status, t.gcol + j);
       D[j * DP + j] = sqrt(dj);
     }
     __syncthreads();
@@ -178,15 +175,29 @@ __global__ void __launch_bounds__(128) k_panel(const PanelTask* __restrict__ tas
     }
     __syncthreads();
   }
-  if (t.tile == 0)
-    for (int idx = tid; idx < w * w; idx += blockDim.x) {
-      int i = idx % w, j = idx / w;
-      if (i >= j) t.d[i + static_cast<int64_t>(j) * ld] = D[j * DP + i];
-    }
+  for (int idx = tid; idx < w * w; idx += blockDim.x) {
+    int i = idx % w, j = idx / w;
+    if (i >= j) t.d[i + static_cast<int64_t>(j) * ld] = D[j * DP + i];
+  }
+}
+
+// Panel step, part 2: X = B · L11⁻ᵀ for one kTrsmRows slab of the rows below
+// the (already factored) diagonal block.
+__global__ void __launch_bounds__(128) k_trsm(const PanelTask* __restrict__ tasks) {
+  extern __shared__ double smem[];
+  const PanelTask& t = tasks[blockIdx.x];
+  const int w = t.w, ld = t.ld, tid = threadIdx.x;
+  constexpr int DP = kNB + 1, XP = kTrsmRows + 1;
+  double* D = smem;
+  double* X = smem + kNB * DP;
   const int r0 = t.tile * kTrsmRows;
   const int nr = min(kTrsmRows, t.nbelow - r0);
   if (nr <= 0) return;
-  double* B = t.d + w + r0;  // row (w + r0) of the chunk's columns
+  for (int idx = tid; idx < w * w; idx += blockDim.x) {
+    int i = idx % w, j = idx / w;
+    if (i >= j) D[j * DP + i] = t.d[i + static_cast<int64_t>(j) * ld];
+  }
+  double* B = t.d + w + r0;
   for (int idx = tid; idx < nr * w; idx += blockDim.x) {
     int r = idx % nr, j = idx / nr;
     X[j * XP + r] = B[r + static_cast<int64_t>(j) * ld];

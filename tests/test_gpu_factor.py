@@ -146,7 +146,7 @@ def test_spatiotemporal_variances_vs_reference(fixture):
     assert bw <= 1e-14
 
 
-@pytest.mark.parametrize("shape", [(60, 60, 1), (120, 80, 2), (400, 30, 1)])
+@pytest.mark.parametrize("shape", [(60, 60, 1), (120, 80, 2), (400, 30, 1), (150, 150, 2)])
 def test_larger_grids_vs_port(port, shape):
     """Multi-level trees with wide supernodes (several chunks per supernode):
     GPU vs the C restatement on the same permutation."""
