@@ -118,6 +118,79 @@ void gmrf_factor_free(gmrf_factor_t* f);
 /* FP64 issue-rate microbenchmark (TFLOP/s) of DMMA m8n8k4 and DFMA. */
 int gmrf_bench_fp64(double* dmma_tflops, double* dfma_tflops);
 
+/* ---- Space-time posterior pipeline (1D space × implicit-Euler time) --------
+ * The chain the reference runs in bench/runner.hpp:457-632 (run_burgers):
+ *   spatiotemporal_prior (priors/spatiotemporal.hpp:79)      → device assembly
+ *   condition_on / condition_affine on the IC (gmrf.hpp:145)  → device update + factor
+ *   gauss_newton (solver/gauss_newton.hpp:93) with
+ *     burgers_fem_residual, implicit Euler (solver/residual.hpp:244)
+ *   laplace_posterior (gauss_newton.hpp:228) + variance_takahashi (gmrf.hpp:205)
+ * residual = 0 gives the linear (heat, config 3) posterior: conditioned prior. */
+typedef struct gmrf_spacetime gmrf_spacetime_t;
+
+typedef struct {
+  int32_t n_el;            /* spatial P1 elements, n_s = n_el + 1 */
+  double xa, xb;           /* spatial interval */
+  int32_t n_t;             /* time slices over [0, t_end], uniform */
+  double t_end;
+  double diffusion;        /* proxy ν (laplace_operator / linear_proxy_operator) */
+  double advection;        /* proxy c (0 for the heat proxy) */
+  double noise_kappa;      /* spatial noise Matérn {κ, α, τ} */
+  int32_t noise_alpha;
+  double noise_tau;
+  double init_kappa;       /* initial-slice Matérn {κ, α, τ} */
+  int32_t init_alpha;
+  double init_tau;
+  double tau;              /* SpatiotemporalSpec::tau */
+  double eps;              /* Dirichlet slack variance, embed_dirichlet(eps) */
+  int32_t dirichlet;       /* 1: homogeneous Dirichlet at both ends */
+  double ic_noise_prec;    /* Λ of the t=0 observation */
+  int32_t residual;        /* 0: linear posterior, 1: Burgers weak form (implicit Euler) */
+  double pde_noise_prec;   /* Λ_pde of the residual rows */
+  int32_t gn_max_iters;    /* GaussNewtonConfig (gauss_newton.hpp:19-24) */
+  double gn_decrement_tol;
+  double gn_armijo_c;
+  double gn_shrink;
+  int32_t gn_max_backtracks;
+} gmrf_spacetime_config_t;
+
+typedef struct {
+  int32_t iter;
+  double objective, decrement, step_size;
+  int32_t backtracks;
+} gmrf_gn_iter_t; /* GaussNewtonIteration, gauss_newton.hpp:35-42 */
+
+typedef struct {
+  double setup_host_ms, assemble_ms, condition_ms, gn_ms, laplace_ms, selinv_ms, numeric_ms;
+  int32_t n_factorizations;
+  int64_t kernel_launches;
+  int32_t n, n_space, n_res;
+  int64_t nnz_pattern, nnz_l, nnz_l_padded;
+  double flops_ref, flops_sn;
+} gmrf_spacetime_info_t;
+
+int gmrf_spacetime_create(const gmrf_spacetime_config_t* cfg, gmrf_spacetime_t** out);
+/* u0: IC values at the n_s nodes (host). mean/var: n outputs (host, may be NULL);
+ * trace: up to max_trace GN iterations. Returns GMRF_ERR_NUMERICAL with the
+ * trace filled on line-search stagnation (GaussNewtonStagnation). */
+int gmrf_spacetime_run(gmrf_spacetime_t* h, const double* u0, int32_t want_var, double* mean,
+                       double* var, gmrf_gn_iter_t* trace, int32_t max_trace, int32_t* n_trace,
+                       int32_t* converged);
+int gmrf_spacetime_info(const gmrf_spacetime_t* h, gmrf_spacetime_info_t* info);
+/* Device pointers of the last run's mean / variances (n doubles each). */
+int gmrf_spacetime_device_results(const gmrf_spacetime_t* h, const double** d_mean,
+                                  const double** d_var);
+/* Assembled joint precisions on the master pattern (tests): col_ptr[n+1],
+ * row_idx[nnz], Q_cond values, q_eff values. */
+int gmrf_spacetime_pattern(const gmrf_spacetime_t* h, int64_t* col_ptr, int32_t* row_idx,
+                           double* q_cond, double* q_eff);
+/* Residual rows f(u) and its Jacobian (CSR) at a host state u (tests). */
+int gmrf_spacetime_residual(gmrf_spacetime_t* h, const double* u, double* f);
+int gmrf_spacetime_jacobian_nnz(const gmrf_spacetime_t* h, int64_t* nnz);
+int gmrf_spacetime_jacobian(gmrf_spacetime_t* h, const double* u, int64_t* row_ptr,
+                            int32_t* col_idx, double* values);
+void gmrf_spacetime_free(gmrf_spacetime_t* h);
+
 #ifdef __cplusplus
 }
 #endif

@@ -41,6 +41,37 @@ class FactorStats(C.Structure):
     ]
 
 
+class SpaceTimeConfig(C.Structure):
+    _fields_ = [
+        ("n_el", C.c_int32), ("xa", C.c_double), ("xb", C.c_double), ("n_t", C.c_int32),
+        ("t_end", C.c_double), ("diffusion", C.c_double), ("advection", C.c_double),
+        ("noise_kappa", C.c_double), ("noise_alpha", C.c_int32), ("noise_tau", C.c_double),
+        ("init_kappa", C.c_double), ("init_alpha", C.c_int32), ("init_tau", C.c_double),
+        ("tau", C.c_double), ("eps", C.c_double), ("dirichlet", C.c_int32),
+        ("ic_noise_prec", C.c_double), ("residual", C.c_int32), ("pde_noise_prec", C.c_double),
+        ("gn_max_iters", C.c_int32), ("gn_decrement_tol", C.c_double), ("gn_armijo_c", C.c_double),
+        ("gn_shrink", C.c_double), ("gn_max_backtracks", C.c_int32),
+    ]
+
+
+class GnIter(C.Structure):
+    _fields_ = [("iter", C.c_int32), ("objective", C.c_double), ("decrement", C.c_double),
+                ("step_size", C.c_double), ("backtracks", C.c_int32)]
+
+
+class SpaceTimeInfo(C.Structure):
+    _fields_ = [
+        ("setup_host_ms", C.c_double), ("assemble_ms", C.c_double), ("condition_ms", C.c_double),
+        ("gn_ms", C.c_double), ("laplace_ms", C.c_double), ("selinv_ms", C.c_double),
+        ("numeric_ms", C.c_double), ("n_factorizations", C.c_int32),
+        ("kernel_launches", C.c_int64), ("n", C.c_int32), ("n_space", C.c_int32),
+        ("n_res", C.c_int32), ("nnz_pattern", C.c_int64), ("nnz_l", C.c_int64),
+        ("nnz_l_padded", C.c_int64), ("flops_ref", C.c_double), ("flops_sn", C.c_double),
+    ]
+
+
+vp = C.c_void_p
+
 # name -> (restype, argtypes); every symbol include/gmrf_b200.h declares.
 SIGNATURES = {
     "gmrf_last_error": (C.c_char_p, []),
@@ -64,6 +95,16 @@ SIGNATURES = {
     "gmrf_factor_stats": (C.c_int, [C.c_void_p, C.POINTER(FactorStats)]),
     "gmrf_factor_free": (None, [C.c_void_p]),
     "gmrf_bench_fp64": (C.c_int, [f64p, f64p]),
+    "gmrf_spacetime_create": (C.c_int, [C.POINTER(SpaceTimeConfig), C.POINTER(vp)]),
+    "gmrf_spacetime_run": (C.c_int, [vp, f64p, C.c_int32, f64p, f64p, C.POINTER(GnIter),
+                                     C.c_int32, i32p, i32p]),
+    "gmrf_spacetime_info": (C.c_int, [vp, C.POINTER(SpaceTimeInfo)]),
+    "gmrf_spacetime_device_results": (C.c_int, [vp, C.POINTER(vp), C.POINTER(vp)]),
+    "gmrf_spacetime_pattern": (C.c_int, [vp, i64p, i32p, f64p, f64p]),
+    "gmrf_spacetime_residual": (C.c_int, [vp, f64p, f64p]),
+    "gmrf_spacetime_jacobian_nnz": (C.c_int, [vp, i64p]),
+    "gmrf_spacetime_jacobian": (C.c_int, [vp, f64p, i64p, i32p, f64p]),
+    "gmrf_spacetime_free": (None, [vp]),
 }
 
 _lib = None

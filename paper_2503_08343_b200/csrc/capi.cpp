@@ -8,6 +8,7 @@
 #include <tuple>
 
 #include "factor.hpp"
+#include "spacetime.hpp"
 #include "symbolic.hpp"
 
 struct gmrf_symbolic {
@@ -16,6 +17,11 @@ struct gmrf_symbolic {
 struct gmrf_factor {
   std::shared_ptr<const gmrf::Symbolic> s;
   std::unique_ptr<gmrf::DeviceFactor> f;
+};
+struct gmrf_spacetime {
+  gmrf::GnConfig cfg;
+  std::unique_ptr<gmrf::SpaceTimePosterior> p;
+  gmrf::DevBuf<double> tmp;
 };
 
 namespace {
@@ -214,5 +220,151 @@ void gmrf_factor_free(gmrf_factor_t* f) { delete f; }
 int gmrf_bench_fp64(double* a, double* b) {
   return guard([&] { gmrf::bench_fp64(a, b); });
 }
+
+int gmrf_spacetime_create(const gmrf_spacetime_config_t* c, gmrf_spacetime_t** out) {
+  return guard([&] {
+    gmrf::SpaceTimeSpec s;
+    s.n_el = c->n_el;
+    s.xa = c->xa;
+    s.xb = c->xb;
+    s.n_t = c->n_t;
+    s.t_end = c->t_end;
+    s.diffusion = c->diffusion;
+    s.advection = c->advection;
+    s.noise = {c->noise_kappa, c->noise_alpha, c->noise_tau};
+    s.init = {c->init_kappa, c->init_alpha, c->init_tau};
+    s.tau = c->tau;
+    s.eps = c->eps;
+    s.dirichlet = c->dirichlet != 0;
+    s.ic_noise_prec = c->ic_noise_prec;
+    s.residual = c->residual;
+    s.pde_noise_prec = c->pde_noise_prec;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+      gmrf::fail(gmrf::kCuda, "no CUDA device: libgmrf_b200 has no CPU fallback");
+    auto h = std::make_unique<gmrf_spacetime>();
+    h->cfg.max_iters = c->gn_max_iters;
+    h->cfg.decrement_tol = c->gn_decrement_tol;
+    h->cfg.armijo_c = c->gn_armijo_c;
+    h->cfg.shrink = c->gn_shrink;
+    h->cfg.max_backtracks = c->gn_max_backtracks;
+    h->p = std::make_unique<gmrf::SpaceTimePosterior>(s);
+    *out = h.release();
+  });
+}
+
+int gmrf_spacetime_run(gmrf_spacetime_t* h, const double* u0, int32_t want_var, double* mean,
+                       double* var, gmrf_gn_iter_t* trace, int32_t max_trace, int32_t* n_trace,
+                       int32_t* converged) {
+  std::vector<gmrf::GnIter> tr;
+  int rc = guard([&] {
+    tr = h->p->run(u0, h->cfg, want_var != 0);
+    const int n = h->p->n();
+    if (mean)
+      gmrf::cuda_check(cudaMemcpy(mean, h->p->d_mean(), n * sizeof(double), cudaMemcpyDeviceToHost),
+                       "mean");
+    if (var && want_var)
+      gmrf::cuda_check(cudaMemcpy(var, h->p->d_var(), n * sizeof(double), cudaMemcpyDeviceToHost),
+                       "var");
+  });
+  if (n_trace) *n_trace = static_cast<int32_t>(tr.size());
+  if (trace)
+    for (size_t i = 0; i < tr.size() && static_cast<int32_t>(i) < max_trace; ++i)
+      trace[i] = {tr[i].iter, tr[i].objective, tr[i].decrement, tr[i].step_size, tr[i].backtracks};
+  if (converged) *converged = h->p->converged() ? 1 : 0;
+  return rc;
+}
+
+int gmrf_spacetime_info(const gmrf_spacetime_t* h, gmrf_spacetime_info_t* info) {
+  return guard([&] {
+    const auto& t = h->p->times();
+    const auto& s = h->p->symbolic();
+    info->setup_host_ms = t.setup_host_ms;
+    info->assemble_ms = t.assemble_ms;
+    info->condition_ms = t.condition_ms;
+    info->gn_ms = t.gn_ms;
+    info->laplace_ms = t.laplace_ms;
+    info->selinv_ms = t.selinv_ms;
+    info->numeric_ms = t.numeric_ms;
+    info->n_factorizations = t.n_factorizations;
+    info->kernel_launches = t.kernel_launches;
+    info->n = h->p->n();
+    info->n_space = h->p->n_space();
+    info->n_res = h->p->n_res();
+    info->nnz_pattern = static_cast<int64_t>(s.qri.size());
+    info->nnz_l = s.nnz_l;
+    info->nnz_l_padded = s.nnz_l_padded;
+    info->flops_ref = s.flops_ref;
+    info->flops_sn = s.flops_sn;
+  });
+}
+
+int gmrf_spacetime_device_results(const gmrf_spacetime_t* h, const double** m, const double** v) {
+  return guard([&] {
+    if (m) *m = h->p->d_mean();
+    if (v) *v = h->p->d_var();
+  });
+}
+
+int gmrf_spacetime_pattern(const gmrf_spacetime_t* h, int64_t* cp, int32_t* ri, double* qc,
+                           double* qe) {
+  return guard([&] {
+    std::vector<int64_t> c;
+    std::vector<int32_t> r;
+    std::vector<double> a, b;
+    h->p->copy_pattern(c, r);
+    h->p->copy_values(a, b);
+    if (cp) std::copy(c.begin(), c.end(), cp);
+    if (ri) std::copy(r.begin(), r.end(), ri);
+    if (qc) std::copy(a.begin(), a.end(), qc);
+    if (qe) std::copy(b.begin(), b.end(), qe);
+  });
+}
+
+static void upload_state(gmrf_spacetime_t* h, const double* u) {
+  h->tmp.alloc(h->p->n());
+  gmrf::cuda_check(cudaMemcpy(h->tmp.p, u, h->p->n() * sizeof(double), cudaMemcpyHostToDevice),
+                   "state");
+}
+
+int gmrf_spacetime_residual(gmrf_spacetime_t* h, const double* u, double* f) {
+  return guard([&] {
+    upload_state(h, u);
+    gmrf::DevBuf<double> out;
+    out.alloc(std::max(h->p->n_res(), 1));
+    h->p->residual(h->tmp.p, out.p);
+    gmrf::cuda_check(cudaMemcpy(f, out.p, h->p->n_res() * sizeof(double), cudaMemcpyDeviceToHost),
+                     "f");
+  });
+}
+
+int gmrf_spacetime_jacobian_nnz(const gmrf_spacetime_t* h, int64_t* nnz) {
+  return guard([&] {
+    std::vector<int64_t> rp;
+    std::vector<int32_t> ci;
+    std::vector<double> v;
+    gmrf::DevBuf<double> z;
+    z.alloc(std::max(h->p->n(), 1));
+    gmrf::cuda_check(cudaMemset(z.p, 0, h->p->n() * sizeof(double)), "z");
+    const_cast<gmrf_spacetime_t*>(h)->p->jacobian_csr(z.p, rp, ci, v);
+    *nnz = static_cast<int64_t>(ci.size());
+  });
+}
+
+int gmrf_spacetime_jacobian(gmrf_spacetime_t* h, const double* u, int64_t* rp_out,
+                            int32_t* ci_out, double* v_out) {
+  return guard([&] {
+    upload_state(h, u);
+    std::vector<int64_t> rp;
+    std::vector<int32_t> ci;
+    std::vector<double> v;
+    h->p->jacobian_csr(h->tmp.p, rp, ci, v);
+    std::copy(rp.begin(), rp.end(), rp_out);
+    std::copy(ci.begin(), ci.end(), ci_out);
+    std::copy(v.begin(), v.end(), v_out);
+  });
+}
+
+void gmrf_spacetime_free(gmrf_spacetime_t* h) { delete h; }
 
 }  // extern "C"

@@ -302,6 +302,13 @@ void DeviceFactor::build_selinv_plan() {
   selinv_plan_ = true;
 }
 
+void DeviceFactor::begin_numeric() {
+  launches_numeric_ = 0;
+  cuda_check(cudaMemsetAsync(L_.p, 0, L_.n * sizeof(double), stream_), "memset L");
+  cuda_check(cudaMemsetAsync(U_.p, 0, U_.n * sizeof(double), stream_), "memset U");
+  cuda_check(cudaMemsetAsync(status_.p, 0x7f, sizeof(int), stream_), "status");
+}
+
 int32_t DeviceFactor::numeric(const double* q, bool q_on_device) {
   const Symbolic& s = *sym_;
   const int64_t nnzq = static_cast<int64_t>(s.qri.size());
@@ -312,17 +319,17 @@ int32_t DeviceFactor::numeric(const double* q, bool q_on_device) {
                  "copy Q");
     dq = q_.p;
   }
-  launches_numeric_ = 0;
-  cuda_check(cudaMemsetAsync(L_.p, 0, L_.n * sizeof(double), stream_), "memset L");
-  cuda_check(cudaMemsetAsync(U_.p, 0, U_.n * sizeof(double), stream_), "memset U");
-  int init = INT_MAX;
-  cuda_check(cudaMemcpyAsync(status_.p, &init, sizeof(int), cudaMemcpyHostToDevice, stream_),
-             "status");
+  begin_numeric();
   if (nnzq) {
     int blocks = static_cast<int>(std::min<int64_t>((nnzq + 255) / 256, 148 * 16));
     k_scatter_q<<<blocks, 256, 0, stream_>>>(dq, qmap_.p, nnzq, L_.p);
     ++launches_numeric_;
   }
+  return factor_panels();
+}
+
+int32_t DeviceFactor::factor_panels() {
+  const Symbolic& s = *sym_;
   const SymDev sd = symdev();
   for (const FLevel& lv : flev_) {
     if (lv.ean) {
@@ -349,9 +356,9 @@ int32_t DeviceFactor::numeric(const double* q, bool q_on_device) {
   cuda_check(cudaMemcpyAsync(&st, status_.p, sizeof(int), cudaMemcpyDeviceToHost, stream_),
              "status read");
   cuda_check(cudaStreamSynchronize(stream_), "numeric factorization");
-  factored_ = st == INT_MAX;
+  factored_ = st == 0x7f7f7f7f;
   selinv_done_ = false;
-  return st == INT_MAX ? -1 : s.perm[st];
+  return factored_ ? -1 : s.perm[st];
 }
 
 void DeviceFactor::ensure_solve_ws(int nrhs) {

@@ -58,6 +58,12 @@ class DeviceFactor {
   // Numeric factorization from Q values in the symbolic's CSC order.
   // Returns -1 on success or the ORIGINAL index of the failing pivot.
   int32_t numeric(const double* q, bool q_on_device);
+  // Split form for callers that write the panels themselves (fixed-pattern
+  // updates, spacetime.cu): begin_numeric zeroes the storage, the caller fills
+  // L through d_qmap(), factor_panels runs the levels and returns like numeric.
+  void begin_numeric();
+  int32_t factor_panels();
+  const int64_t* d_qmap() const { return qmap_.p; }
   // Solves; b/x are n×nrhs column-major (original coordinates for kFull,
   // permuted coordinates for kLower/kUpper, as cholesky.hpp:179-222).
   void solve(int mode, int nrhs, const double* b, double* x, bool on_device);

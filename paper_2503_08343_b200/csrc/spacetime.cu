@@ -1,0 +1,692 @@
+// Space-time GMRF posterior on the device. See spacetime.hpp.
+#include "spacetime.hpp"
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <string>
+
+namespace gmrf {
+
+namespace {
+
+constexpr int kBlkCmm = 0, kBlkCgg = 1, kBlkCmg = 2, kBlkQ1 = 3, kBlkGmm = 4, kBlkGff = 5,
+              kBlkGmf = 6, kBlkGl1 = 7, kNumBlk = 8;
+
+struct BlkDev {
+  const i64* cp;   // kNumBlk * (n+1)
+  const i32* ri;
+  const double* v;
+  i32 n;
+};
+
+__device__ __forceinline__ double blk_at(const BlkDev& b, int k, int i, int j) {
+  const i64* cp = b.cp + static_cast<i64>(k) * (b.n + 1);
+  i64 lo = cp[j], hi = cp[j + 1];
+  while (lo < hi) {
+    i64 mid = (lo + hi) >> 1;
+    if (b.ri[mid] < i) lo = mid + 1; else hi = mid;
+  }
+  return (lo < cp[j + 1] && b.ri[lo] == i) ? b.v[lo] : 0.0;
+}
+
+// Joint value of the space-time precision at (R, C) before symmetrization,
+// spatiotemporal.hpp:144-155 (Q set) or the same blocks rebuilt through the
+// square root (q_eff set, gauss_newton.hpp:110-114).
+__device__ __forceinline__ double st_entry(const BlkDev& b, bool qeff, int sr, int a, int sc, int c,
+                                           int nt, double t) {
+  if (sr == sc) {
+    double v = 0.0;
+    if (!qeff) {
+      if (sr < nt - 1) v += t * blk_at(b, kBlkCmm, a, c);
+      if (sr >= 1) v += t * blk_at(b, kBlkCgg, a, c);
+      if (sr == 0) v += blk_at(b, kBlkQ1, a, c);
+    } else {
+      if (sr == 0) v += blk_at(b, kBlkGl1, a, c);
+      if (sr >= 1) v += t * blk_at(b, kBlkGff, a, c);
+      if (sr < nt - 1) v += t * blk_at(b, kBlkGmm, a, c);
+    }
+    return v;
+  }
+  if (sc == sr + 1) return -t * blk_at(b, qeff ? kBlkGmf : kBlkCmg, a, c);
+  if (sr == sc + 1) return -t * blk_at(b, qeff ? kBlkGmf : kBlkCmg, c, a);
+  return 0.0;
+}
+
+// Row 1: assembly of Q_cond = sym(Q_prior) + AᵀΛA and q_eff = sym(S Sᵀ) on the
+// master pattern, one thread per joint column. Slack (constrained) coordinates
+// carry only 1/ε² on the diagonal (spatiotemporal.hpp:248-266); the IC
+// observation A = I on slice 0 adds Λ_ic on that slice's diagonal.
+__global__ void k_st_assemble(const i64* __restrict__ pcp, const i32* __restrict__ pri, int N,
+                              int ns, int nt, double t, double inv_eps, double ic_prec,
+                              const char* __restrict__ slack, BlkDev b, double* __restrict__ qcond,
+                              double* __restrict__ qeff) {
+  for (int C = blockIdx.x * blockDim.x + threadIdx.x; C < N; C += gridDim.x * blockDim.x) {
+    const int sc = C / ns, c = C - sc * ns;
+    for (i64 p = pcp[C]; p < pcp[C + 1]; ++p) {
+      const int R = pri[p];
+      const int sr = R / ns, a = R - sr * ns;
+      double vq, ve;
+      if (slack[a] || slack[c]) {
+        vq = ve = (R == C) ? inv_eps : 0.0;
+      } else {
+        vq = 0.5 * st_entry(b, false, sr, a, sc, c, nt, t) + 0.5 * st_entry(b, false, sc, c, sr, a, nt, t);
+        ve = 0.5 * st_entry(b, true, sr, a, sc, c, nt, t) + 0.5 * st_entry(b, true, sc, c, sr, a, nt, t);
+      }
+      if (R == C && sr == 0) {
+        vq += ic_prec;
+        ve += ic_prec;
+      }
+      qcond[p] = vq;
+      qeff[p] = ve;
+    }
+  }
+}
+
+// Row 2: fixed-pattern update written straight into the supernodal panels,
+//   L[qmap[p]] = base[p] + Σ_{r ∈ col_J(R) ∩ col_J(C)} λ J_rR J_rC
+// (gauss_newton.hpp:137-138, :231-232). The JᵀΛJ entry is a merge of two
+// sorted J columns: no atomics, fixed summation order.
+__global__ void k_fill_panels(const i64* __restrict__ pcp, const i32* __restrict__ pri, int N,
+                              const i64* __restrict__ qmap, const double* __restrict__ base,
+                              const i64* __restrict__ jcp, const i32* __restrict__ jri,
+                              const i64* __restrict__ jmap, const double* __restrict__ jv,
+                              double lam, double* __restrict__ L) {
+  for (int C = blockIdx.x * blockDim.x + threadIdx.x; C < N; C += gridDim.x * blockDim.x) {
+    for (i64 p = pcp[C]; p < pcp[C + 1]; ++p) {
+      const i64 o = qmap[p];
+      if (o < 0) continue;
+      double v = base[p];
+      if (jcp) {
+        const int R = pri[p];
+        i64 x = jcp[R], xe = jcp[R + 1], y = jcp[C], ye = jcp[C + 1];
+        double s = 0.0;
+        while (x < xe && y < ye) {
+          const int rx = jri[x], ry = jri[y];
+          if (rx < ry) {
+            ++x;
+          } else if (ry < rx) {
+            ++y;
+          } else {
+            s += lam * jv[jmap[x]] * jv[jmap[y]];
+            ++x;
+            ++y;
+          }
+        }
+        v += s;
+      }
+      L[o] = v;
+    }
+  }
+}
+
+// y = A x for a CSR (or, with rp/ci of a CSC, y = Aᵀ x). vmap optional.
+__global__ void k_spmv(int nrows, const i64* __restrict__ rp, const i32* __restrict__ ci,
+                       const double* __restrict__ v, const i64* __restrict__ vmap,
+                       const double* __restrict__ x, double* __restrict__ y) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nrows; i += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (i64 p = rp[i]; p < rp[i + 1]; ++p) s += (vmap ? v[vmap[p]] : v[p]) * x[ci[p]];
+    y[i] = s;
+  }
+}
+
+__global__ void k_axpby(int n, double a, const double* __restrict__ x, double b,
+                        const double* __restrict__ y, double* __restrict__ z) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    z[i] = a * x[i] + b * y[i];
+}
+
+// Deterministic dot product: fixed grid, fixed per-thread order, tree reduce.
+constexpr int kDotBlocks = 296, kDotThreads = 256;
+__global__ void k_dot_partial(i64 n, const double* __restrict__ a, const double* __restrict__ b,
+                              double* __restrict__ part) {
+  __shared__ double sh[kDotThreads];
+  double s = 0.0;
+  for (i64 i = blockIdx.x * static_cast<i64>(kDotThreads) + threadIdx.x; i < n;
+       i += static_cast<i64>(kDotBlocks) * kDotThreads)
+    s += a[i] * b[i];
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = kDotThreads / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+}
+__global__ void k_dot_final(double* __restrict__ part, double* __restrict__ out) {
+  __shared__ double sh[512];
+  const int t = threadIdx.x;
+  sh[t] = t < kDotBlocks ? part[t] : 0.0;
+  __syncthreads();
+  for (int o = 256; o > 0; o >>= 1) {
+    if (t < o) sh[t] += sh[t + o];
+    __syncthreads();
+  }
+  if (t == 0) out[0] = sh[0];
+}
+
+// ---- Burgers weak residual, P1, implicit Euler (residual.hpp:244-382) ------
+struct BurgersDev {
+  int ns, nt, nk;           // spatial dofs, slices, kept rows per step
+  double h, dt, nu;
+  const char* slack;
+  const int* kept;          // kept row k -> dof
+};
+
+__device__ __forceinline__ double um(const BurgersDev& B, const double* u, int s, int j) {
+  return (j < 0 || j >= B.ns || B.slack[j]) ? 0.0 : u[static_cast<i64>(s) * B.ns + j];
+}
+
+// 2-point Gauss-Legendre on [0,1] (degree-3 rule of residual.hpp:208-209)
+__device__ __forceinline__ void gl2(double* xi, double* w) {
+  const double d = 0.5 / sqrt(3.0);
+  xi[0] = 0.5 - d;
+  xi[1] = 0.5 + d;
+  w[0] = w[1] = 0.5;
+}
+
+// weak advection a_d(v) = ∫ φ_d v ∂x v, v slack-masked (residual.hpp:206-235)
+__device__ double adv_row(const BurgersDev& B, const double* u, int s, int d) {
+  double xi[2], w[2];
+  gl2(xi, w);
+  double acc = 0.0;
+  for (int e = d - 1; e <= d; ++e) {
+    if (e < 0 || e >= B.ns - 1) continue;
+    const double vl = um(B, u, s, e), vr = um(B, u, s, e + 1);
+    const double dv = (vr - vl) / B.h;
+    for (int q = 0; q < 2; ++q) {
+      const double phi = (d == e) ? 1.0 - xi[q] : xi[q];
+      const double vq = vl * (1.0 - xi[q]) + vr * xi[q];
+      acc += w[q] * B.h * phi * vq * dv;
+    }
+  }
+  return acc;
+}
+
+__device__ __forceinline__ double mass_ij(const BurgersDev& B, int d, int j) {
+  if (j < 0 || j >= B.ns || B.slack[j]) return 0.0;
+  if (j == d) {
+    int ne = (d > 0) + (d < B.ns - 1);
+    return ne * B.h / 3.0;
+  }
+  return B.h / 6.0;
+}
+__device__ __forceinline__ double stiff_ij(const BurgersDev& B, int d, int j) {
+  if (j < 0 || j >= B.ns || B.slack[j]) return 0.0;
+  if (j == d) {
+    int ne = (d > 0) + (d < B.ns - 1);
+    return ne / B.h;
+  }
+  return -1.0 / B.h;
+}
+
+__global__ void k_burgers_res(BurgersDev B, const double* __restrict__ u, double* __restrict__ f) {
+  const int nrow = (B.nt - 1) * B.nk;
+  for (int row = blockIdx.x * blockDim.x + threadIdx.x; row < nrow; row += gridDim.x * blockDim.x) {
+    const int s = row / B.nk, d = B.kept[row - s * B.nk];
+    double mdu = 0.0, kd = 0.0;
+    for (int j = d - 1; j <= d + 1; ++j) {
+      mdu += mass_ij(B, d, j) * (um(B, u, s + 1, j) - um(B, u, s, j));
+      kd += stiff_ij(B, d, j) * um(B, u, s + 1, j);
+    }
+    f[row] = mdu / B.dt + (B.nu * kd + adv_row(B, u, s + 1, d));
+  }
+}
+
+// Jacobian row (step s, dof d): slice s → −M/Δt (θ = 1), slice s+1 →
+// ν K̂ + J_adv + M/Δt, columns ascending, slack columns skipped (residual.hpp:353-377).
+__global__ void k_burgers_jac(BurgersDev B, const double* __restrict__ u, const i64* __restrict__ rp,
+                              double* __restrict__ jv) {
+  const int nrow = (B.nt - 1) * B.nk;
+  double xi[2], w[2];
+  gl2(xi, w);
+  for (int row = blockIdx.x * blockDim.x + threadIdx.x; row < nrow; row += gridDim.x * blockDim.x) {
+    const int s = row / B.nk, d = B.kept[row - s * B.nk];
+    i64 p = rp[row];
+    for (int j = d - 1; j <= d + 1; ++j) {
+      if (j < 0 || j >= B.ns || B.slack[j]) continue;
+      jv[p++] = -mass_ij(B, d, j) / B.dt;
+    }
+    for (int j = d - 1; j <= d + 1; ++j) {
+      if (j < 0 || j >= B.ns || B.slack[j]) continue;
+      double ja = 0.0;
+      for (int e = d - 1; e <= d; ++e) {
+        if (e < 0 || e >= B.ns - 1) continue;
+        if (j != e && j != e + 1) continue;
+        const double vl = um(B, u, s + 1, e), vr = um(B, u, s + 1, e + 1);
+        const double dv = (vr - vl) / B.h;
+        const double dphij = (j == e ? -1.0 : 1.0) / B.h;
+        for (int q = 0; q < 2; ++q) {
+          const double phid = (d == e) ? 1.0 - xi[q] : xi[q];
+          const double phij = (j == e) ? 1.0 - xi[q] : xi[q];
+          const double vq = vl * (1.0 - xi[q]) + vr * xi[q];
+          ja += w[q] * B.h * phid * (phij * dv + vq * dphij);
+        }
+      }
+      jv[p++] = (B.nu * stiff_ij(B, d, j) + ja) + mass_ij(B, d, j) / B.dt;
+    }
+  }
+}
+
+__global__ void k_ic_rhs(int ns, const double* __restrict__ u0, double lam, double* __restrict__ rhs) {
+  for (int d = blockIdx.x * blockDim.x + threadIdx.x; d < ns; d += gridDim.x * blockDim.x)
+    rhs[d] = lam * u0[d];
+}
+
+int grid_for(i64 n, int threads = 256) {
+  return static_cast<int>(std::max<i64>(1, std::min<i64>((n + threads - 1) / threads, 148 * 16)));
+}
+
+double now_ms() {
+  return std::chrono::duration<double, std::milli>(
+             std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+
+}  // namespace
+
+SpaceTimePosterior::SpaceTimePosterior(const SpaceTimeSpec& spec, cudaStream_t stream)
+    : spec_(spec), stream_(stream) {
+  double t0 = now_ms();
+  build_host();
+  times_.setup_host_ms = now_ms() - t0;
+  t0 = now_ms();
+  assemble_device();
+  cuda_check(cudaStreamSynchronize(stream_), "assemble");
+  times_.assemble_ms = now_ms() - t0;
+}
+
+SpaceTimePosterior::~SpaceTimePosterior() = default;
+
+void SpaceTimePosterior::build_host() {
+  require(spec_.n_el >= 2 && spec_.n_t >= 2, kContract, "spacetime: need >= 2 elements and slices");
+  space_ = Space1D{spec_.n_el, spec_.xa, spec_.xb};
+  ns_ = space_.n();
+  nt_ = spec_.n_t;
+  n_ = ns_ * nt_;
+  const double dt = spec_.t_end / (nt_ - 1);
+  blk_ = spacetime_blocks(space_, spec_.diffusion, spec_.advection, dt, spec_.tau, spec_.noise,
+                          spec_.init, spec_.dirichlet, spec_.eps);
+  const auto& sl = blk_.slack;
+
+  // ---- templates: spatial patterns of the diagonal / upper off-diagonal blocks
+  auto band = [&](int rad) {
+    std::vector<Trip> t;
+    for (int j = 0; j < ns_; ++j)
+      for (int i = std::max(0, j - rad); i <= std::min(ns_ - 1, j + rad); ++i) t.push_back({i, j, 1});
+    return csc_from_trips(ns_, ns_, std::move(t));
+  };
+  auto pat = [](Csc m) {
+    for (double& v : m.v) v = 1.0;
+    return m;
+  };
+  Csc dg = band(2);
+  for (const Csc* m : {&blk_.c_mm, &blk_.c_gg, &blk_.q1, &blk_.g_mm, &blk_.g_ff, &blk_.g_l1})
+    dg = add(dg, pat(*m));
+  Csc up = band(2);
+  for (const Csc* m : {&blk_.c_mg, &blk_.g_mf}) up = add(up, pat(*m));
+  Csc lo = transpose(up);
+
+  // ---- master pattern (full symmetric, original joint indices)
+  pcp_.assign(n_ + 1, 0);
+  pri_.clear();
+  pri_.reserve(static_cast<size_t>(n_) * (dg.nnz() / ns_ + 2 * up.nnz() / ns_ + 1));
+  for (int s = 0; s < nt_; ++s)
+    for (int b = 0; b < ns_; ++b) {
+      const int C = s * ns_ + b;
+      if (sl[b]) {
+        pri_.push_back(C);
+      } else {
+        if (s >= 1)
+          for (i64 p = up.cp[b]; p < up.cp[b + 1]; ++p)
+            if (!sl[up.ri[p]]) pri_.push_back((s - 1) * ns_ + up.ri[p]);
+        for (i64 p = dg.cp[b]; p < dg.cp[b + 1]; ++p)
+          if (!sl[dg.ri[p]]) pri_.push_back(s * ns_ + dg.ri[p]);
+        if (s < nt_ - 1)
+          for (i64 p = lo.cp[b]; p < lo.cp[b + 1]; ++p)
+            if (!sl[lo.ri[p]]) pri_.push_back((s + 1) * ns_ + lo.ri[p]);
+      }
+      pcp_[C + 1] = static_cast<i64>(pri_.size());
+    }
+
+  // ---- symbolic (nested dissection), shared by every factorization of the run
+  sym_ = std::make_shared<const Symbolic>(analyze(n_, pcp_.data(), pri_.data(), nullptr));
+
+  // ---- S_cond = [S_prior | Aᵀ L_ε] (gmrf.hpp:165), CSC, columns in the reference order
+  const double st = std::sqrt(blk_.t);
+  s_ = Csc{};
+  s_.nr = n_;
+  s_.cp.assign(1, 0);
+  auto push_col = [&](int slice, const Csc& m, int k, double scale) {
+    for (i64 p = m.cp[k]; p < m.cp[k + 1]; ++p)
+      if (!sl[m.ri[p]]) {
+        s_.ri.push_back(slice * ns_ + m.ri[p]);
+        s_.v.push_back(scale * m.v[p]);
+      }
+  };
+  for (int k = 0; k < ns_; ++k) {
+    push_col(0, blk_.l1, k, 1.0);
+    s_.cp.push_back(s_.nnz());
+  }
+  for (int i = 0; i + 1 < nt_; ++i)
+    for (int k = 0; k < ns_; ++k) {
+      push_col(i, blk_.s_m, k, st);
+      push_col(i + 1, blk_.f_is, k, -st);
+      s_.cp.push_back(s_.nnz());
+    }
+  for (int d = 0; d < ns_; ++d)
+    if (sl[d])
+      for (int s = 0; s < nt_; ++s) {
+        s_.ri.push_back(s * ns_ + d);
+        s_.v.push_back(1.0 / std::sqrt(spec_.eps));
+        s_.cp.push_back(s_.nnz());
+      }
+  for (int d = 0; d < ns_; ++d) {  // IC: Aᵀ L_ε = √Λ on slice 0
+    s_.ri.push_back(d);
+    s_.v.push_back(std::sqrt(spec_.ic_noise_prec));
+    s_.cp.push_back(s_.nnz());
+  }
+  s_.nc = static_cast<i32>(s_.cp.size()) - 1;
+  ms_ = s_.nc;
+
+  // ---- Burgers Jacobian pattern (CSR rows, then CSC with a value map)
+  if (spec_.residual == 1) {
+    std::vector<int> kept;
+    for (int d = 0; d < ns_; ++d)
+      if (!sl[d]) kept.push_back(d);
+    const int nk = static_cast<int>(kept.size());
+    nres_ = (nt_ - 1) * nk;
+    jrp_.assign(nres_ + 1, 0);
+    jci_.clear();
+    for (int s = 0; s + 1 < nt_; ++s)
+      for (int k = 0; k < nk; ++k) {
+        const int d = kept[k];
+        for (int sl2 = s; sl2 <= s + 1; ++sl2)
+          for (int j = d - 1; j <= d + 1; ++j)
+            if (j >= 0 && j < ns_ && !sl[j]) jci_.push_back(sl2 * ns_ + j);
+        jrp_[s * nk + k + 1] = static_cast<i64>(jci_.size());
+      }
+    jcp_.assign(n_ + 1, 0);
+    for (i32 c : jci_) jcp_[c + 1]++;
+    for (int c = 0; c < n_; ++c) jcp_[c + 1] += jcp_[c];
+    jri_.resize(jci_.size());
+    jmap_.resize(jci_.size());
+    std::vector<i64> nx(jcp_.begin(), jcp_.end() - 1);
+    for (int r = 0; r < nres_; ++r)
+      for (i64 p = jrp_[r]; p < jrp_[r + 1]; ++p) {
+        i64 q = nx[jci_[p]]++;
+        jri_[q] = r;
+        jmap_[q] = p;
+      }
+  }
+}
+
+void SpaceTimePosterior::assemble_device() {
+  const auto& sl = blk_.slack;
+  d_pcp_.upload(pcp_, stream_);
+  d_pri_.upload(pri_, stream_);
+  // spatial blocks, concatenated
+  std::vector<i64> bcp;
+  std::vector<i32> bri;
+  std::vector<double> bv;
+  const Csc* blocks[kNumBlk] = {&blk_.c_mm, &blk_.c_gg, &blk_.c_mg, &blk_.q1,
+                                &blk_.g_mm, &blk_.g_ff, &blk_.g_mf, &blk_.g_l1};
+  for (const Csc* m : blocks) {
+    const i64 off = static_cast<i64>(bri.size());
+    for (i64 v : m->cp) bcp.push_back(off + v);
+    bri.insert(bri.end(), m->ri.begin(), m->ri.end());
+    bv.insert(bv.end(), m->v.begin(), m->v.end());
+  }
+  d_blk_cp_.upload(bcp, stream_);
+  d_blk_ri_.upload(bri, stream_);
+  d_blk_v_.upload(bv, stream_);
+  d_slack_.upload(std::vector<char>(sl.begin(), sl.end()), stream_);
+  const i64 np = static_cast<i64>(pri_.size());
+  d_qcond_.alloc(np);
+  d_qeff_.alloc(np);
+  BlkDev b{d_blk_cp_.p, d_blk_ri_.p, d_blk_v_.p, ns_};
+  k_st_assemble<<<grid_for(n_), 256, 0, stream_>>>(d_pcp_.p, d_pri_.p, n_, ns_, nt_, blk_.t,
+                                                  1.0 / spec_.eps, spec_.ic_noise_prec,
+                                                  d_slack_.p, b, d_qcond_.p, d_qeff_.p);
+  times_.kernel_launches += 1;
+  // S_cond: CSC (columns, for Sᵀx) and CSR (rows, for S w)
+  d_scp_.upload(s_.cp, stream_);
+  d_sri_.upload(s_.ri, stream_);
+  d_sv_.upload(s_.v, stream_);
+  Csc sr = transpose(s_);
+  d_srp_.upload(sr.cp, stream_);
+  d_sci_.upload(sr.ri, stream_);
+  d_svr_.upload(sr.v, stream_);
+  if (spec_.residual == 1) {
+    d_jrp_.upload(jrp_, stream_);
+    d_jci_.upload(jci_, stream_);
+    d_jcp_.upload(jcp_, stream_);
+    d_jri_.upload(jri_, stream_);
+    d_jmap_.upload(jmap_, stream_);
+    d_jv_.alloc(std::max<size_t>(jci_.size(), 1));
+    std::vector<i32> kept;
+    for (int d = 0; d < ns_; ++d)
+      if (!sl[d]) kept.push_back(d);
+    kept_.upload(kept, stream_);
+  }
+  fac_ = std::make_unique<DeviceFactor>(sym_, stream_);
+  for (DevBuf<double>* v : {&mean_cond_, &mean_, &var_, &x_, &c_, &g_, &d_, &cand_, &r1_, &u0_})
+    v->alloc(std::max(n_, 1));
+  w_.alloc(std::max(ms_, 1));
+  f_.alloc(std::max(nres_, 1));
+  fc_.alloc(std::max(nres_, 1));
+  part_.alloc(kDotBlocks + 1);
+}
+
+double SpaceTimePosterior::dot(const double* a, const double* b, i64 n) {
+  k_dot_partial<<<kDotBlocks, kDotThreads, 0, stream_>>>(n, a, b, part_.p);
+  k_dot_final<<<1, 512, 0, stream_>>>(part_.p, part_.p + kDotBlocks);
+  times_.kernel_launches += 2;
+  double out = 0.0;
+  cuda_check(cudaMemcpyAsync(&out, part_.p + kDotBlocks, sizeof(double), cudaMemcpyDeviceToHost,
+                             stream_),
+             "dot");
+  cuda_check(cudaStreamSynchronize(stream_), "dot");
+  return out;
+}
+
+void SpaceTimePosterior::eval_residual(const double* d_u, double* d_f) {
+  BurgersDev B{ns_, nt_, static_cast<int>(kept_.n), space_.h(), spec_.t_end / (nt_ - 1),
+               spec_.diffusion, d_slack_.p, kept_.p};
+  k_burgers_res<<<grid_for(nres_), 256, 0, stream_>>>(B, d_u, d_f);
+  times_.kernel_launches += 1;
+}
+
+void SpaceTimePosterior::eval_jacobian(const double* d_u) {
+  BurgersDev B{ns_, nt_, static_cast<int>(kept_.n), space_.h(), spec_.t_end / (nt_ - 1),
+               spec_.diffusion, d_slack_.p, kept_.p};
+  k_burgers_jac<<<grid_for(nres_), 256, 0, stream_>>>(B, d_u, d_jrp_.p, d_jv_.p);
+  times_.kernel_launches += 1;
+}
+
+void SpaceTimePosterior::residual(const double* d_u, double* d_r) { eval_residual(d_u, d_r); }
+
+// ½‖Sᵀ(x−μ)‖² + ½ Σ λ (y − f)², y = 0 (gauss_newton.hpp:65-83)
+double SpaceTimePosterior::objective(const double* d_x, const double* d_fx) {
+  k_axpby<<<grid_for(n_), 256, 0, stream_>>>(n_, 1.0, d_x, -1.0, mean_cond_.p, c_.p);
+  k_spmv<<<grid_for(ms_), 256, 0, stream_>>>(ms_, d_scp_.p, d_sri_.p, d_sv_.p, nullptr, c_.p, w_.p);
+  times_.kernel_launches += 2;
+  double quad = 0.5 * dot(w_.p, w_.p, ms_);
+  double fit = 0.0;
+  if (nres_ > 0) fit = spec_.pde_noise_prec * dot(d_fx, d_fx, nres_);
+  return quad + 0.5 * fit;
+}
+
+void SpaceTimePosterior::fill_panels(const double* base, bool with_jacobian) {
+  fac_->begin_numeric();
+  k_fill_panels<<<grid_for(n_), 256, 0, stream_>>>(
+      d_pcp_.p, d_pri_.p, n_, fac_->d_qmap(), base, with_jacobian ? d_jcp_.p : nullptr, d_jri_.p,
+      d_jmap_.p, d_jv_.p, spec_.pde_noise_prec, fac_->d_l());
+  times_.kernel_launches += 1;
+}
+
+std::vector<GnIter> SpaceTimePosterior::run(const double* u0, const GnConfig& cfg, bool variances) {
+  require(cfg.max_iters >= 1, kContract, "gauss-newton: max_iters must be >= 1");
+  require(cfg.decrement_tol > 0.0, kContract, "gauss-newton: decrement_tol must be positive");
+  require(cfg.armijo_c > 0.0 && cfg.armijo_c < 1.0, kContract, "gauss-newton: armijo constant in (0,1)");
+  require(cfg.shrink > 0.0 && cfg.shrink < 1.0, kContract, "gauss-newton: shrink factor in (0,1)");
+  std::vector<GnIter> trace;
+  converged_ = false;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  auto phase = [&](double& acc, auto&& body) {
+    cudaEventRecord(e0, stream_);
+    body();
+    cudaEventRecord(e1, stream_);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    acc += ms;
+  };
+  auto factor_now = [&](const char* what) {
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, stream_);
+    int32_t bad = fac_->factor_panels();
+    cudaEventRecord(b, stream_);
+    cudaEventSynchronize(b);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    times_.numeric_ms += ms;
+    times_.n_factorizations += 1;
+    times_.kernel_launches += fac_->launches_numeric();
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    if (bad >= 0)
+      throw Error(kNotSpd, std::string(what) + ": cholesky: non-positive pivot at index " +
+                               std::to_string(bad));
+  };
+
+  // ---- IC conditioning (condition_affine, gmrf.hpp:145-170) ----
+  phase(times_.condition_ms, [&] {
+    cuda_check(cudaMemcpyAsync(u0_.p, u0, ns_ * sizeof(double), cudaMemcpyHostToDevice, stream_),
+               "u0");
+    cuda_check(cudaMemsetAsync(r1_.p, 0, n_ * sizeof(double), stream_), "rhs");
+    k_ic_rhs<<<grid_for(ns_), 256, 0, stream_>>>(ns_, u0_.p, spec_.ic_noise_prec, r1_.p);
+    fill_panels(d_qcond_.p, false);
+    factor_now("conditioning");
+    fac_->solve(2, 1, r1_.p, mean_cond_.p, true);
+    times_.kernel_launches += 1 + fac_->launches_solve();
+  });
+
+  if (spec_.residual == 0) {
+    cuda_check(cudaMemcpyAsync(mean_.p, mean_cond_.p, n_ * sizeof(double), cudaMemcpyDeviceToDevice,
+                               stream_),
+               "mean");
+    if (variances)
+      phase(times_.selinv_ms, [&] {
+        fac_->selinv(var_.p, true);
+        times_.kernel_launches += fac_->launches_selinv();
+      });
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return trace;
+  }
+
+  // ---- Gauss-Newton (gauss_newton.hpp:93-224) ----
+  double t_gn0 = now_ms();
+  cuda_check(cudaMemcpyAsync(x_.p, mean_cond_.p, n_ * sizeof(double), cudaMemcpyDeviceToDevice,
+                             stream_),
+             "x0");
+  const double lam = spec_.pde_noise_prec;
+  for (int iter = 1; iter <= cfg.max_iters; ++iter) {
+    eval_residual(x_.p, f_.p);
+    eval_jacobian(x_.p);
+    // grad = S(Sᵀ(x−μ)) − Jᵀ Λ (y − f)    (y = 0)
+    k_axpby<<<grid_for(n_), 256, 0, stream_>>>(n_, 1.0, x_.p, -1.0, mean_cond_.p, c_.p);
+    k_spmv<<<grid_for(ms_), 256, 0, stream_>>>(ms_, d_scp_.p, d_sri_.p, d_sv_.p, nullptr, c_.p, w_.p);
+    k_spmv<<<grid_for(n_), 256, 0, stream_>>>(n_, d_srp_.p, d_sci_.p, d_svr_.p, nullptr, w_.p, g_.p);
+    // Jᵀ(λ f): fit term gradient is +λ Jᵀ f since y − f = −f
+    k_spmv<<<grid_for(n_), 256, 0, stream_>>>(n_, d_jcp_.p, d_jri_.p, d_jv_.p, d_jmap_.p, f_.p,
+                                              r1_.p);
+    k_axpby<<<grid_for(n_), 256, 0, stream_>>>(n_, 1.0, g_.p, lam, r1_.p, g_.p);
+    k_axpby<<<grid_for(n_), 256, 0, stream_>>>(n_, -1.0, g_.p, 0.0, g_.p, r1_.p);  // rhs = −grad
+    times_.kernel_launches += 6;
+    fill_panels(d_qeff_.p, true);
+    factor_now("gauss-newton");
+    fac_->solve(2, 1, r1_.p, d_.p, true);
+    times_.kernel_launches += fac_->launches_solve();
+    const double gd = dot(g_.p, d_.p, n_);
+    const double decrement = std::sqrt(std::max(0.0, -gd));
+    const double obj = objective(x_.p, f_.p);
+    GnIter rec{iter, obj, decrement, 0.0, 0};
+    if (decrement < cfg.decrement_tol || 0.5 * decrement * decrement <= 1e-14 * (1.0 + std::abs(obj))) {
+      trace.push_back(rec);
+      converged_ = true;
+      break;
+    }
+    const double slope = gd;
+    double alpha = 1.0;
+    int bt = 0;
+    while (true) {
+      k_axpby<<<grid_for(n_), 256, 0, stream_>>>(n_, 1.0, x_.p, alpha, d_.p, cand_.p);
+      eval_residual(cand_.p, fc_.p);
+      times_.kernel_launches += 1;
+      const double cobj = objective(cand_.p, fc_.p);
+      if (cobj <= obj + cfg.armijo_c * alpha * slope) {
+        std::swap(x_.p, cand_.p);
+        break;
+      }
+      if (++bt > cfg.max_backtracks) {
+        trace.push_back(rec);
+        throw Error(kNumerical, "gauss-newton: line search failed after " + std::to_string(bt - 1) +
+                                    " backtracks at iteration " + std::to_string(iter));
+      }
+      alpha *= cfg.shrink;
+    }
+    rec.step_size = alpha;
+    rec.backtracks = bt;
+    trace.push_back(rec);
+  }
+  cuda_check(cudaStreamSynchronize(stream_), "gn");
+  times_.gn_ms += now_ms() - t_gn0;
+
+  // ---- Laplace posterior (gauss_newton.hpp:228-240): Q_cond + J(mode)ᵀΛJ(mode) ----
+  phase(times_.laplace_ms, [&] {
+    eval_jacobian(x_.p);
+    fill_panels(d_qcond_.p, true);
+    factor_now("laplace");
+    cuda_check(cudaMemcpyAsync(mean_.p, x_.p, n_ * sizeof(double), cudaMemcpyDeviceToDevice, stream_),
+               "mode");
+  });
+  if (variances)
+    phase(times_.selinv_ms, [&] {
+      fac_->selinv(var_.p, true);
+      times_.kernel_launches += fac_->launches_selinv();
+    });
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return trace;
+}
+
+void SpaceTimePosterior::copy_pattern(std::vector<i64>& cp, std::vector<i32>& ri) const {
+  cp = pcp_;
+  ri = pri_;
+}
+
+void SpaceTimePosterior::copy_values(std::vector<double>& qcond, std::vector<double>& qeff) const {
+  qcond.resize(d_qcond_.n);
+  qeff.resize(d_qeff_.n);
+  cuda_check(cudaMemcpy(qcond.data(), d_qcond_.p, qcond.size() * 8, cudaMemcpyDeviceToHost), "q");
+  cuda_check(cudaMemcpy(qeff.data(), d_qeff_.p, qeff.size() * 8, cudaMemcpyDeviceToHost), "q");
+}
+
+void SpaceTimePosterior::jacobian_csr(const double* d_u, std::vector<i64>& rp,
+                                      std::vector<i32>& ci, std::vector<double>& v) {
+  eval_jacobian(d_u);
+  rp = jrp_;
+  ci = jci_;
+  v.resize(jci_.size());
+  cuda_check(cudaMemcpyAsync(v.data(), d_jv_.p, v.size() * 8, cudaMemcpyDeviceToHost, stream_), "J");
+  cuda_check(cudaStreamSynchronize(stream_), "J");
+}
+
+}  // namespace gmrf

@@ -1,0 +1,169 @@
+"""Space-time GMRF posterior (configs 3-4): host mirror of the reference's
+run_burgers chain (bench/runner.hpp:457-632) over the C-ABI pipeline
+``gmrf_spacetime_*`` (include/gmrf_b200.h).
+
+    spatiotemporal_prior  → condition_on(IC) → gauss_newton(burgers_fem_residual)
+    → laplace_posterior → variance_takahashi
+
+Everything after the host-side spatial blocks and symbolic analysis runs on
+the device; there is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _capi
+from ._capi import f64p, i32p, i64p, ptr
+from .core import NumericalError, _check
+
+
+@dataclass
+class MaternSpec:
+    kappa: float = 1.0
+    alpha: int = 2
+    tau: float = 1.0
+
+
+@dataclass
+class GaussNewtonConfig:
+    """gauss_newton.hpp:19-24."""
+    max_iters: int = 10
+    decrement_tol: float = 1e-5
+    armijo_c: float = 1e-4
+    shrink: float = 0.5
+    max_backtracks: int = 30
+
+
+@dataclass
+class SpaceTimeSpec:
+    n_el: int = 999
+    xa: float = -1.0
+    xb: float = 1.0
+    n_t: int = 1000
+    t_end: float = 1.0
+    diffusion: float = 0.01 / math.pi
+    advection: float = 0.5
+    noise: MaternSpec = field(default_factory=lambda: MaternSpec(10.0, 1, 1.0))
+    init: MaternSpec = field(default_factory=lambda: MaternSpec(10.0, 2, 1.0))
+    tau: float = 1.0
+    eps: float = 1e-10
+    dirichlet: bool = True
+    ic_noise_prec: float = 1e8
+    residual: int = 1
+    pde_noise_prec: float = 1e12
+
+    @staticmethod
+    def burgers(n_el=999, n_t=1000) -> "SpaceTimeSpec":
+        """Config 4."""
+        return SpaceTimeSpec(n_el=n_el, n_t=n_t)
+
+    @staticmethod
+    def heat(n_el=499, n_t=1000) -> "SpaceTimeSpec":
+        """Config 3."""
+        return SpaceTimeSpec(n_el=n_el, xa=0.0, xb=1.0, n_t=n_t, diffusion=0.1, advection=0.0,
+                             ic_noise_prec=1e6, residual=0)
+
+    def node_x(self) -> np.ndarray:
+        i = np.arange(self.n_el + 1)
+        x = self.xa + (self.xb - self.xa) * i / self.n_el
+        x[-1] = self.xb
+        return x
+
+
+@dataclass
+class GaussNewtonIteration:
+    iter: int
+    objective: float
+    decrement: float
+    step_size: float
+    backtracks: int
+
+
+class GaussNewtonStagnation(NumericalError):
+    def __init__(self, msg, trace):
+        super().__init__(msg)
+        self._trace = trace
+
+    def trace(self):
+        return self._trace
+
+
+class SpaceTimePosterior:
+    def __init__(self, spec: SpaceTimeSpec, gn: GaussNewtonConfig | None = None):
+        gn = gn or GaussNewtonConfig()
+        c = _capi.SpaceTimeConfig(
+            spec.n_el, spec.xa, spec.xb, spec.n_t, spec.t_end, spec.diffusion, spec.advection,
+            spec.noise.kappa, spec.noise.alpha, spec.noise.tau, spec.init.kappa, spec.init.alpha,
+            spec.init.tau, spec.tau, spec.eps, int(spec.dirichlet), spec.ic_noise_prec,
+            spec.residual, spec.pde_noise_prec, gn.max_iters, gn.decrement_tol, gn.armijo_c,
+            gn.shrink, gn.max_backtracks)
+        self.spec = spec
+        lib = _capi.load()
+        h = C.c_void_p()
+        _check(lib.gmrf_spacetime_create(C.byref(c), C.byref(h)))
+        self._h = h
+        self.n = self.info().n
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _capi.load().gmrf_spacetime_free(self._h)
+            self._h = None
+
+    def info(self) -> _capi.SpaceTimeInfo:
+        i = _capi.SpaceTimeInfo()
+        _check(_capi.load().gmrf_spacetime_info(self._h, C.byref(i)))
+        return i
+
+    def run(self, u0, variances=True, copy_back=True, max_trace=64):
+        """Returns (mean, var, trace, converged); mean/var None if copy_back is False."""
+        u0 = np.ascontiguousarray(u0, np.float64)
+        mean = np.empty(self.n) if copy_back else None
+        var = np.empty(self.n) if (copy_back and variances) else None
+        tr = (_capi.GnIter * max_trace)()
+        nt, conv = C.c_int32(), C.c_int32()
+        rc = _capi.load().gmrf_spacetime_run(self._h, ptr(u0, f64p), int(variances),
+                                             ptr(mean, f64p), ptr(var, f64p), tr, max_trace,
+                                             C.byref(nt), C.byref(conv))
+        trace = [GaussNewtonIteration(t.iter, t.objective, t.decrement, t.step_size, t.backtracks)
+                 for t in tr[: nt.value]]
+        if rc == 6 and trace:
+            raise GaussNewtonStagnation(_capi.load().gmrf_last_error().decode(), trace)
+        _check(rc)
+        return mean, var, trace, bool(conv.value)
+
+    def device_results(self):
+        m, v = C.c_void_p(), C.c_void_p()
+        _check(_capi.load().gmrf_spacetime_device_results(self._h, C.byref(m), C.byref(v)))
+        return m.value, v.value
+
+    def pattern(self):
+        i = self.info()
+        cp = np.empty(self.n + 1, np.int64)
+        ri = np.empty(i.nnz_pattern, np.int32)
+        qc = np.empty(i.nnz_pattern)
+        qe = np.empty(i.nnz_pattern)
+        _check(_capi.load().gmrf_spacetime_pattern(self._h, ptr(cp, i64p), ptr(ri, i32p),
+                                                   ptr(qc, f64p), ptr(qe, f64p)))
+        return cp, ri, qc, qe
+
+    def residual(self, u):
+        u = np.ascontiguousarray(u, np.float64)
+        f = np.empty(self.info().n_res)
+        _check(_capi.load().gmrf_spacetime_residual(self._h, ptr(u, f64p), ptr(f, f64p)))
+        return f
+
+    def jacobian(self, u):
+        u = np.ascontiguousarray(u, np.float64)
+        nnz = C.c_int64()
+        _check(_capi.load().gmrf_spacetime_jacobian_nnz(self._h, C.byref(nnz)))
+        nr = self.info().n_res
+        rp = np.empty(nr + 1, np.int64)
+        ci = np.empty(nnz.value, np.int32)
+        v = np.empty(nnz.value)
+        _check(_capi.load().gmrf_spacetime_jacobian(self._h, ptr(u, f64p), ptr(rp, i64p),
+                                                    ptr(ci, i32p), ptr(v, f64p)))
+        return rp, ci, v
