@@ -1,0 +1,370 @@
+#!/usr/bin/env python3
+"""Headline benchmark: config 4 of BASELINE.json — the Gauss-Newton-Laplace
+posterior (mean + marginal variances) of the 1M-unknown space-time Burgers
+GMRF (P1, 1000 nodes × 1000 implicit-Euler slices), 10 GN steps + Laplace +
+selected-inversion variances.
+
+A step is one full posterior from the IC data: prior assembly on the device,
+IC conditioning (factor + solve), 10 GN iterations (residual, Jacobian,
+H = q_eff + JᵀΛJ into the factor storage, numeric factorization, solve, Armijo
+line search), the Laplace precision, its factorization and the variances.
+Host symbolic analysis (nested dissection, supernodes, plans) is one-off per
+problem shape and reported separately as ``host_setup_s``.
+
+  value : device-timed seconds per posterior (CUDA events on the library's
+          stream; results stay in HBM), max over ranks.
+  e2e   : the same posterior through the C-ABI with host buffers (IC values in,
+          mean + variances out; copies inside the timed region).
+  --impl reference : the unmodified reference (oracle/_ref, compiled from
+          /root/reference) on a bounded sample of the same workload,
+          extrapolated to full size with the reference's own measured per-stage
+          rates.
+
+Multi-GPU (torchrun, N>1): batch sharding — each rank solves its own
+independent posterior (BASELINE config 5's "independent problems one per GPU"
+mode); no data-path collective; scaling "weak".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Gauss-Newton-Laplace posterior time (s) & Cholesky FP64 TFLOP/s, % roofline"
+UNIT = "s"
+# Reference AMD symbolic of the full config-4 matrix, computed with oracle/_ref
+# (the unmodified reference amd_order + symbolic_analyze) in the build
+# container; equals SURVEY §6's measurement.
+C4_FULL_AMD_FLOPS = 266698072912.0
+C4_FULL_AMD_NNZL = 223320550.0
+C4_FULL_N = 1_000_000
+SAMPLE = (149, 150)  # reference CPU sample: 150 nodes × 150 slices (~18 s single-core)
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+# ---------------------------------------------------------------------------
+# reference arm / CPU baseline
+# ---------------------------------------------------------------------------
+def reference_sample(n_el=SAMPLE[0], n_t=SAMPLE[1]):
+    """Times the unmodified reference (run_burgers chain: spatiotemporal_prior →
+    condition_on → gauss_newton(10) → laplace_posterior → variance_takahashi) on
+    a bounded sample, then extrapolates each stage to the full config-4 size:
+    numeric factorizations and Takahashi by the AMD flop ratio Σc², AMD +
+    symbolic by the nnz(L) ratio, everything else linearly in n."""
+    from oracle.pyoracle import Ref
+    ref = Ref()
+    p = [1, n_el, -1.0, 1.0, n_t, 1.0, 0.01 / math.pi, 0.5, 10, 1, 1, 10, 2, 1, 1.0, 1e-10, 1e8,
+         0, 1e12, 10, 1, 1]
+    t0 = time.perf_counter()
+    b = ref.build("spatiotemporal", p)
+    wall = time.perf_counter() - t0
+    q = b.mat("Q_la")
+    st = ref.time_stages(q.nrows, q.col_ptr, q.row_idx, q.values, 1)
+    n_gn = len(b.vec("gn_objective"))
+    n_fact = 1 + n_gn + 1          # conditioning, GN refactors, fresh Laplace factor
+    n_sym = 3                      # AMD + symbolic: conditioning, GN (once), Laplace
+    fact = n_fact * st["numeric_s"]
+    taka = st["takahashi_s"]
+    sym = n_sym * (st["amd_s"] + st["symbolic_s"])
+    rest = max(0.0, wall - fact - taka - sym)
+    sf = C4_FULL_AMD_FLOPS / st["flops"]
+    sl = C4_FULL_AMD_NNZL / st["nnz_l"]
+    sn = C4_FULL_N / q.nrows
+    full = (fact + taka) * sf + sym * sl + rest * sn
+    return {
+        "value": full, "unit": UNIT, "cores": 1, "kind": "reference",
+        "sample": (f"unmodified reference (oracle/_ref) run_burgers chain at {n_el + 1} nodes x "
+                   f"{n_t} slices (n={q.nrows}), {n_gn} GN steps + Laplace + Takahashi: "
+                   f"{wall:.2f} s measured single-threaded; extrapolated to n=1e6 by stage: "
+                   f"factorizations+Takahashi x{sf:.0f} (AMD flops), AMD+symbolic x{sl:.0f} "
+                   f"(nnz L), rest x{sn:.0f} (n)"),
+        "measured_sample_s": wall,
+        "stages_sample_s": {"numeric_x%d" % n_fact: fact, "takahashi": taka, "amd_symbolic": sym,
+                            "rest": rest},
+        "cpu": cpu_model(),
+    }
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip() + f" ({os.cpu_count()} threads visible)"
+    except OSError:
+        pass
+    return f"{os.cpu_count()} threads visible"
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def fp64_peak_tflops():
+    """cuBLAS DGEMM 8192³ (torch.matmul float64), best of 5 — the measured FP64
+    tensor-core denominator (MEASURED_PEAKS.json carries no FP64 entry)."""
+    import torch
+    n = 8192
+    a = torch.randn(n, n, dtype=torch.float64, device="cuda")
+    b = torch.randn(n, n, dtype=torch.float64, device="cuda")
+    for _ in range(2):
+        a @ b
+    torch.cuda.synchronize()
+    best = 1e30
+    for _ in range(5):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        a @ b
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    del a, b
+    torch.cuda.empty_cache()
+    return 2.0 * n ** 3 / (best * 1e-3) / 1e12
+
+
+# ---------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--n-el", type=int, default=999)
+    ap.add_argument("--n-t", type=int, default=1000)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    config = {"workload": "config 4: space-time Burgers GN-Laplace posterior (mean + marginal "
+                          "variances), P1 1000 nodes x 1000 implicit-Euler slices, n=1,000,000, "
+                          "10 GN steps",
+              "n_el": args.n_el, "n_t": args.n_t, "gn_steps": 10,
+              "l2": "inputs larger than L2 (factor storage ~3 GB, Sigma panels ~1.6 GB)",
+              "parallelism": f"replicas x{world} (batch sharding, one posterior per GPU)"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        rb = reference_sample()
+        line = {"impl": "reference", "metric": METRIC, "value": rb["value"], "unit": UNIT,
+                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": rb["value"] * 1e3, "higher_is_better": False, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY §8(d))",
+                "config": config, "cpu_baseline": {k: rb[k] for k in
+                                                   ("value", "unit", "cores", "kind", "sample")},
+                "e2e": {"value": rb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0},
+                "extra": {"measured_sample_s": rb["measured_sample_s"],
+                          "stages_sample_s": rb["stages_sample_s"], "cpu": rb["cpu"]}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    from paper_2503_08343_b200.spacetime import (GaussNewtonConfig, SpaceTimePosterior,
+                                                 SpaceTimeSpec)
+
+    peak_fp64 = fp64_peak_tflops()
+    peaks = load_peaks()
+    spec = SpaceTimeSpec.burgers(n_el=args.n_el, n_t=args.n_t)
+    t0 = time.perf_counter()
+    post = SpaceTimePosterior(spec, GaussNewtonConfig(max_iters=10))
+    host_setup_s = time.perf_counter() - t0
+    x = spec.node_x()
+    u0 = -np.sin(np.pi * x)
+
+    for _ in range(max(args.warmup, 0)):
+        post.run(u0, variances=True, copy_back=False)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- device-timed region: value ----
+    sampler = ClockSampler(local_rank)
+    barrier()
+    sampler.start()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    launches = 0
+    traces = []
+    e0.record()
+    for _ in range(args.steps):
+        _, _, trace, conv = post.run(u0, variances=True, copy_back=False)
+        launches += post.info().kernel_launches
+        traces.append(trace)
+    e1.record()
+    barrier()
+    clocks = sampler.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+
+    # ---- e2e through the C-ABI with host buffers ----
+    barrier()
+    w0 = time.perf_counter()
+    for _ in range(args.steps):
+        mean, var, _, _ = post.run(u0, variances=True, copy_back=True)
+    barrier()
+    e2e_s = (time.perf_counter() - w0) / args.steps
+    te = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_s = float(te.item())
+    n = post.n
+
+    # ---- one profiled (untimed) run for the per-kernel roofline ----
+    info = post.info()
+    post.set_profile(True)
+    post.run(u0, variances=True, copy_back=False)
+    stats = post.kernel_stats()
+    post.set_profile(False)
+    pinfo = post.info()
+    step_kernel_ms = sum(v["ms"] for v in stats.values())
+    dom_name, dom = max(stats.items(), key=lambda kv: kv[1]["ms"])
+    if dom["flops"] > 0:
+        achieved = dom["flops"] / (dom["ms"] * 1e-3) / 1e12
+        roof = {"kernel": dom_name, "bound": "tensor", "achieved": achieved, "peak": peak_fp64,
+                "unit": "TFLOP/s", "frac": achieved / peak_fp64, "traffic": None,
+                "peak_source": "measured in-run: cuBLAS DGEMM 8192^3 (FP64 tensor cores)",
+                "share_of_step": dom["ms"] / step_kernel_ms,
+                "avg_launch_ms": dom["ms"] / max(dom["launches"], 1),
+                "launches_per_step": dom["launches"]}
+    else:
+        hbm = peaks.get("hbm_gbs", 6650.0)
+        achieved = dom["bytes"] / (dom["ms"] * 1e-3) / 1e9
+        roof = {"kernel": dom_name, "bound": "hbm", "achieved": achieved, "peak": hbm,
+                "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                "share_of_step": dom["ms"] / step_kernel_ms}
+    numeric_ms = info.numeric_ms / max(info.n_factorizations, 1)
+    chol_tflops = info.flops_ref / (numeric_ms * 1e-3) / 1e12
+    kernels = {k: {"ms": v["ms"], "launches": v["launches"],
+                   "achieved": (v["flops"] / (v["ms"] * 1e-3) / 1e12 if v["flops"] > 0
+                                else v["bytes"] / (v["ms"] * 1e-3) / 1e9),
+                   "unit": "TFLOP/s" if v["flops"] > 0 else "GB/s"}
+               for k, v in sorted(stats.items(), key=lambda kv: -kv[1]["ms"])}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    line = {
+        "metric": METRIC, "value": ms / 1e3, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY §8(d))",
+        "config": config,
+        "e2e": {"value": e2e_s, "unit": UNIT, "h2d_bytes_per_step": 8 * len(u0),
+                "d2h_bytes_per_step": 16 * n},
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+        "roofline": roof,
+        "cholesky_fp64": {"tflops": chol_tflops, "frac": chol_tflops / peak_fp64,
+                          "flops_per_factorization": info.flops_ref,
+                          "flops_executed_padded": info.flops_sn,
+                          "numeric_ms_per_factorization": numeric_ms,
+                          "factorizations_per_step": info.n_factorizations,
+                          "note": "Sigma c_j^2 over the ND symbolic / numeric time (BASELINE.md §3)"},
+        "phases_ms": {"assemble": info.assemble_ms, "condition": info.condition_ms,
+                      "gauss_newton": info.gn_ms, "laplace": info.laplace_ms,
+                      "variances": info.selinv_ms},
+        "host_setup_s": host_setup_s,
+        "kernels": kernels,
+        "gn_trace": [[t.objective, t.decrement, t.step_size, t.backtracks] for t in traces[-1]],
+        "nnz_l": info.nnz_l, "nnz_l_padded": info.nnz_l_padded,
+        "peaks": {"fp64_tflops_dgemm": peak_fp64, "hbm_gbs": peaks.get("hbm_gbs")},
+    }
+    if not args.no_cpu_baseline and world == 1:
+        try:
+            rb = reference_sample()
+            line["cpu_baseline"] = {k: rb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        except Exception as exc:  # oracle/_ref missing on this box
+            line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference",
+                                    "sample": f"unavailable: {exc}"}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -161,7 +161,7 @@ typedef struct {
 } gmrf_gn_iter_t; /* GaussNewtonIteration, gauss_newton.hpp:35-42 */
 
 typedef struct {
-  double setup_host_ms, assemble_ms, condition_ms, gn_ms, laplace_ms, selinv_ms, numeric_ms;
+  double setup_host_ms, init_ms, assemble_ms, condition_ms, gn_ms, laplace_ms, selinv_ms, numeric_ms;
   int32_t n_factorizations;
   int64_t kernel_launches;
   int32_t n, n_space, n_res;
@@ -190,6 +190,17 @@ int gmrf_spacetime_jacobian_nnz(const gmrf_spacetime_t* h, int64_t* nnz);
 int gmrf_spacetime_jacobian(gmrf_spacetime_t* h, const double* u, int64_t* row_ptr,
                             int32_t* col_idx, double* values);
 void gmrf_spacetime_free(gmrf_spacetime_t* h);
+
+/* Per-kernel-class profile of the following runs (CUDA events on the launch
+ * stream around every launch; ALGORITHMIC flops and bytes per class). */
+typedef struct {
+  char name[40];
+  int64_t launches;
+  double ms, flops, bytes;
+} gmrf_kernel_stat_t;
+int gmrf_spacetime_set_profile(gmrf_spacetime_t* h, int32_t on);
+int gmrf_spacetime_kernel_stats(gmrf_spacetime_t* h, gmrf_kernel_stat_t* out, int32_t max,
+                                int32_t* n);
 
 #ifdef __cplusplus
 }

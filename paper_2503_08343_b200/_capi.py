@@ -61,7 +61,8 @@ class GnIter(C.Structure):
 
 class SpaceTimeInfo(C.Structure):
     _fields_ = [
-        ("setup_host_ms", C.c_double), ("assemble_ms", C.c_double), ("condition_ms", C.c_double),
+        ("setup_host_ms", C.c_double), ("init_ms", C.c_double), ("assemble_ms", C.c_double),
+        ("condition_ms", C.c_double),
         ("gn_ms", C.c_double), ("laplace_ms", C.c_double), ("selinv_ms", C.c_double),
         ("numeric_ms", C.c_double), ("n_factorizations", C.c_int32),
         ("kernel_launches", C.c_int64), ("n", C.c_int32), ("n_space", C.c_int32),
@@ -105,7 +106,14 @@ SIGNATURES = {
     "gmrf_spacetime_jacobian_nnz": (C.c_int, [vp, i64p]),
     "gmrf_spacetime_jacobian": (C.c_int, [vp, f64p, i64p, i32p, f64p]),
     "gmrf_spacetime_free": (None, [vp]),
+    "gmrf_spacetime_set_profile": (C.c_int, [vp, C.c_int32]),
+    "gmrf_spacetime_kernel_stats": (C.c_int, [vp, C.c_void_p, C.c_int32, i32p]),
 }
+
+
+class KernelStat(C.Structure):
+    _fields_ = [("name", C.c_char * 40), ("launches", C.c_int64), ("ms", C.c_double),
+                ("flops", C.c_double), ("bytes", C.c_double)]
 
 _lib = None
 

@@ -280,6 +280,7 @@ int gmrf_spacetime_info(const gmrf_spacetime_t* h, gmrf_spacetime_info_t* info) 
     const auto& t = h->p->times();
     const auto& s = h->p->symbolic();
     info->setup_host_ms = t.setup_host_ms;
+    info->init_ms = t.init_ms;
     info->assemble_ms = t.assemble_ms;
     info->condition_ms = t.condition_ms;
     info->gn_ms = t.gn_ms;
@@ -366,5 +367,33 @@ int gmrf_spacetime_jacobian(gmrf_spacetime_t* h, const double* u, int64_t* rp_ou
 }
 
 void gmrf_spacetime_free(gmrf_spacetime_t* h) { delete h; }
+
+int gmrf_spacetime_set_profile(gmrf_spacetime_t* h, int32_t on) {
+  return guard([&] {
+    h->p->prof_.reset();
+    h->p->prof_.on = on != 0;
+  });
+}
+
+int gmrf_spacetime_kernel_stats(gmrf_spacetime_t* h, gmrf_kernel_stat_t* out, int32_t max,
+                                int32_t* n) {
+  return guard([&] {
+    h->p->prof_.flush();
+    int32_t i = 0;
+    for (const auto& kv : h->p->prof_.stats) {
+      if (i < max && out) {
+        gmrf_kernel_stat_t& o = out[i];
+        std::memset(o.name, 0, sizeof(o.name));
+        std::strncpy(o.name, kv.first.c_str(), sizeof(o.name) - 1);
+        o.launches = kv.second.launches;
+        o.ms = kv.second.ms;
+        o.flops = kv.second.flops;
+        o.bytes = kv.second.bytes;
+      }
+      ++i;
+    }
+    if (n) *n = i;
+  });
+}
 
 }  // extern "C"

@@ -32,6 +32,15 @@ void set_smem_attrs() {
 }
 
 inline int nchunks(int w) { return (w + kNB - 1) / kNB; }
+
+// Algorithmic flops of one tile: 2·k per needed output entry; a tile on the
+// diagonal of a symmetric update only needs its lower trapezoid.
+inline double tile_flops(const GemmTask& g, bool diag) {
+  const double k = static_cast<double>(g.k[0]) + g.k[1];
+  const double m = g.m, n = g.n;
+  const double needed = diag ? n * m - n * (n - 1.0) / 2.0 : m * n;
+  return 2.0 * k * needed;
+}
 }  // namespace
 
 DeviceFactor::DeviceFactor(std::shared_ptr<const Symbolic> sym, cudaStream_t stream)
@@ -71,6 +80,12 @@ DeviceFactor::DeviceFactor(std::shared_ptr<const Symbolic> sym, cudaStream_t str
   }
   fptr_.upload(fp, stream_);
   uvptr_.upload(up, stream_);
+  // solve traffic per level: the L panel (8 B/entry, lower trapezoid) + row indices
+  lvl_bytes_.assign(s.n_levels, 0.0);
+  for (int k = 0; k < s.ns; ++k) {
+    const double w = s.w(k), rows = s.rows(k);
+    lvl_bytes_[s.sn_level[k]] += 8.0 * (w * rows - w * (w - 1.0) / 2.0) + 4.0 * rows;
+  }
   build_factor_plan();
   cuda_check(cudaStreamSynchronize(stream_), "factor setup");
 }
@@ -120,6 +135,7 @@ void DeviceFactor::build_factor_plan() {
   std::vector<std::vector<ColTask>> ea(nlev);
   std::vector<std::vector<PanelTask>> pan(nlev), po(nlev);
   std::vector<std::vector<GemmTask>> gm(nlev);
+  std::vector<double> ea_b(nlev, 0.0), po_f(nlev, 0.0), tr_f(nlev, 0.0), gm_f(nlev, 0.0);
   double* L = L_.p;
   double* U = U_.p;
   for (int k = 0; k < s.ns; ++k) {
@@ -130,9 +146,16 @@ void DeviceFactor::build_factor_plan() {
     for (int c = 0; c < nch; ++c) {
       const int lv = lvl0[k] + c;
       const int c0 = c * kNB, wk = std::min(kNB, w - c0);
-      if (c == 0 && s.ch_ptr[k + 1] > s.ch_ptr[k])
+      if (c == 0 && s.ch_ptr[k + 1] > s.ch_ptr[k]) {
         for (int b = 0; b < rows; ++b) ea[lv].push_back({k, b});
+        for (int q = s.ch_ptr[k]; q < s.ch_ptr[k + 1]; ++q) {
+          const double rc = s.r(s.ch_list[q]);
+          ea_b[lv] += 12.0 * rc * (rc + 1.0);  // read U_c lower (8 B) + RMW target (16 B)
+        }
+      }
       const int nbelow = rows - c0 - wk;
+      po_f[lv] += static_cast<double>(wk) * wk * wk / 3.0;
+      tr_f[lv] += static_cast<double>(nbelow) * wk * wk;
       const PanelTask pt{Lk + c0 + static_cast<int64_t>(c0) * rows, rows, wk, nbelow, 0,
                          s.sn_first[k] + c0};
       po[lv].push_back(pt);
@@ -158,6 +181,7 @@ void DeviceFactor::build_factor_plan() {
           g.alpha = -1.0;
           g.beta = 1.0;
           gm[lv].push_back(g);
+          gm_f[lv] += tile_flops(g, ib == jb);
         }
       // last chunk: full-width SYRK into the update matrix, U -= L21 L21ᵀ
       if (c == nch - 1 && r > 0)
@@ -177,6 +201,7 @@ void DeviceFactor::build_factor_plan() {
             g.alpha = -1.0;
             g.beta = 1.0;
             gm[lv].push_back(g);
+            gm_f[lv] += tile_flops(g, ib == jb);
           }
     }
   }
@@ -188,7 +213,8 @@ void DeviceFactor::build_factor_plan() {
     flev_[l] = {static_cast<int64_t>(eaf.size()), static_cast<int64_t>(ea[l].size()),
                 static_cast<int64_t>(pof.size()), static_cast<int64_t>(po[l].size()),
                 static_cast<int64_t>(panf.size()), static_cast<int64_t>(pan[l].size()),
-                static_cast<int64_t>(gmf.size()), static_cast<int64_t>(gm[l].size())};
+                static_cast<int64_t>(gmf.size()), static_cast<int64_t>(gm[l].size()),
+                ea_b[l], po_f[l], tr_f[l], gm_f[l]};
     pof.insert(pof.end(), po[l].begin(), po[l].end());
     eaf.insert(eaf.end(), ea[l].begin(), ea[l].end());
     panf.insert(panf.end(), pan[l].begin(), pan[l].end());
@@ -209,6 +235,8 @@ void DeviceFactor::build_selinv_plan() {
   std::vector<std::vector<ColTask>> ga(nlev);
   std::vector<std::vector<GemmTask>> yg(nlev), zg(nlev);
   std::vector<std::vector<SelChunk>> tr(nlev), dg(nlev);
+  std::vector<double> ga_b(nlev, 0.0), y_f(nlev, 0.0), t_f(nlev, 0.0), z_f(nlev, 0.0),
+      d_f(nlev, 0.0);
   double* L = L_.p;
   double* U = U_.p;
   double* S = Sig_.p;
@@ -222,8 +250,17 @@ void DeviceFactor::build_selinv_plan() {
       const int lv = lvl0[k] + c;
       const int c0 = c * kNB, wk = std::min(kNB, w - c0);
       const int p = w - c0 - wk;
-      if (c == nch - 1 && r > 0)
+      if (c == nch - 1 && r > 0) {
         for (int b = 0; b < r; ++b) ga[lv].push_back({k, b});
+        ga_b[lv] += 16.0 * r * r;  // read parent Σ entries + write Σ_RR
+      }
+      {
+        const double nb = rows - c0 - wk;
+        y_f[lv] += 2.0 * nb * nb * wk;
+        t_f[lv] += nb * wk * wk;
+        z_f[lv] += 2.0 * nb * wk * wk;
+        d_f[lv] += 2.0 * wk * wk * wk;
+      }
       auto ytile = [&](int i0, int i1) {
         GemmTask g{};
         g.c = Sk + i0 + static_cast<int64_t>(c0) * rows;
@@ -294,6 +331,11 @@ void DeviceFactor::build_selinv_plan() {
     e.d0 = dgf.size();
     e.dn = dg[l].size();
     dgf.insert(dgf.end(), dg[l].begin(), dg[l].end());
+    e.ga_bytes = ga_b[l];
+    e.y_flops = y_f[l];
+    e.t_flops = t_f[l];
+    e.z_flops = z_f[l];
+    e.d_flops = d_f[l];
   }
   sga_.upload(gaf, stream_);
   sgemm_.upload(gmf, stream_);
@@ -331,23 +373,32 @@ int32_t DeviceFactor::numeric(const double* q, bool q_on_device) {
 int32_t DeviceFactor::factor_panels() {
   const Symbolic& s = *sym_;
   const SymDev sd = symdev();
+  KernelProfiler& pf = *prof_;
   for (const FLevel& lv : flev_) {
     if (lv.ean) {
       int blocks = static_cast<int>((lv.ean * 32 + 255) / 256);
-      k_extend_add<<<blocks, 256, 0, stream_>>>(ea_.p + lv.ea0, static_cast<int>(lv.ean), sd, L_.p,
-                                               U_.p);
+      pf.run(stream_, "factor.extend_add", 0.0, lv.ea_bytes, [&] {
+        k_extend_add<<<blocks, 256, 0, stream_>>>(ea_.p + lv.ea0, static_cast<int>(lv.ean), sd,
+                                                 L_.p, U_.p);
+      });
       ++launches_numeric_;
     }
     if (lv.pon) {
-      k_potrf<<<static_cast<unsigned>(lv.pon), 128, 0, stream_>>>(po_.p + lv.po0, status_.p);
+      pf.run(stream_, "factor.potrf", lv.po_flops, 0.0, [&] {
+        k_potrf<<<static_cast<unsigned>(lv.pon), 128, 0, stream_>>>(po_.p + lv.po0, status_.p);
+      });
       ++launches_numeric_;
     }
     if (lv.pann) {
-      k_trsm<<<static_cast<unsigned>(lv.pann), 128, kPanelSmem, stream_>>>(pan_.p + lv.pan0);
+      pf.run(stream_, "factor.trsm", lv.tr_flops, 0.0, [&] {
+        k_trsm<<<static_cast<unsigned>(lv.pann), 128, kPanelSmem, stream_>>>(pan_.p + lv.pan0);
+      });
       ++launches_numeric_;
     }
     if (lv.gmn) {
-      k_gemm_tiles<<<static_cast<unsigned>(lv.gmn), 128, 0, stream_>>>(gemm_.p + lv.gm0);
+      pf.run(stream_, "factor.gemm_dmma", lv.gm_flops, 0.0, [&] {
+        k_gemm_tiles<<<static_cast<unsigned>(lv.gmn), 128, 0, stream_>>>(gemm_.p + lv.gm0);
+      });
       ++launches_numeric_;
     }
   }
@@ -407,18 +458,23 @@ void DeviceFactor::solve(int mode, int nrhs, const double* b, double* x, bool on
                                  stream_),
                  "copy b");
     }
+    KernelProfiler& pf = *prof_;
     if (mode == 0 || mode == 2)
       for (int l = 0; l < s.n_levels; ++l) {
         const int cnt = static_cast<int>(lvl_ptr_[l + 1] - lvl_ptr_[l]);
-        k_solve_fwd<<<cnt, 256, 0, stream_>>>(lvl_sn_.p + lvl_ptr_[l], sd, L_.p, y, nr, F_.p,
-                                              Uv_.p, fptr_.p, uvptr_.p);
+        pf.run(stream_, "solve.forward", 0.0, lvl_bytes_[l], [&] {
+          k_solve_fwd<<<cnt, 256, 0, stream_>>>(lvl_sn_.p + lvl_ptr_[l], sd, L_.p, y, nr, F_.p,
+                                                Uv_.p, fptr_.p, uvptr_.p);
+        });
         ++launches_solve_;
       }
     if (mode == 1 || mode == 2)
       for (int l = s.n_levels - 1; l >= 0; --l) {
         const int cnt = static_cast<int>(lvl_ptr_[l + 1] - lvl_ptr_[l]);
-        k_solve_bwd<<<cnt, 256, 0, stream_>>>(lvl_sn_.p + lvl_ptr_[l], sd, L_.p, y, nr, F_.p,
-                                              fptr_.p);
+        pf.run(stream_, "solve.backward", 0.0, lvl_bytes_[l], [&] {
+          k_solve_bwd<<<cnt, 256, 0, stream_>>>(lvl_sn_.p + lvl_ptr_[l], sd, L_.p, y, nr, F_.p,
+                                                fptr_.p);
+        });
         ++launches_solve_;
       }
     if (mode == 2) {
@@ -447,26 +503,37 @@ void DeviceFactor::selinv(double* diag_out, bool on_device) {
   const SymDev sd = symdev();
   for (int l = static_cast<int>(slev_.size()) - 1; l >= 0; --l) {
     const SLevel& e = slev_[l];
+    KernelProfiler& pf = *prof_;
     if (e.gan) {
       int blocks = static_cast<int>((e.gan * 32 + 255) / 256);
-      k_sel_gather<<<blocks, 256, 0, stream_>>>(sga_.p + e.ga0, static_cast<int>(e.gan), sd,
-                                               snparent_.p, Sig_.p, U_.p);
+      pf.run(stream_, "selinv.gather", 0.0, e.ga_bytes, [&] {
+        k_sel_gather<<<blocks, 256, 0, stream_>>>(sga_.p + e.ga0, static_cast<int>(e.gan), sd,
+                                                 snparent_.p, Sig_.p, U_.p);
+      });
       ++launches_selinv_;
     }
     if (e.yn) {
-      k_gemm_tiles<<<static_cast<unsigned>(e.yn), 128, 0, stream_>>>(sgemm_.p + e.y0);
+      pf.run(stream_, "selinv.gemm_dmma", e.y_flops, 0.0, [&] {
+        k_gemm_tiles<<<static_cast<unsigned>(e.yn), 128, 0, stream_>>>(sgemm_.p + e.y0);
+      });
       ++launches_selinv_;
     }
     if (e.tn) {
-      k_sel_trsm<<<static_cast<unsigned>(e.tn), 128, kPanelSmem, stream_>>>(strsm_.p + e.t0);
+      pf.run(stream_, "selinv.trsm", e.t_flops, 0.0, [&] {
+        k_sel_trsm<<<static_cast<unsigned>(e.tn), 128, kPanelSmem, stream_>>>(strsm_.p + e.t0);
+      });
       ++launches_selinv_;
     }
     if (e.zn) {
-      k_gemm_tiles<<<static_cast<unsigned>(e.zn), 128, 0, stream_>>>(sgemm_.p + e.z0);
+      pf.run(stream_, "selinv.gemm_dmma", e.z_flops, 0.0, [&] {
+        k_gemm_tiles<<<static_cast<unsigned>(e.zn), 128, 0, stream_>>>(sgemm_.p + e.z0);
+      });
       ++launches_selinv_;
     }
     if (e.dn) {
-      k_sel_diag<<<static_cast<unsigned>(e.dn), 256, kDiagSmem, stream_>>>(sdiag_.p + e.d0);
+      pf.run(stream_, "selinv.diag", e.d_flops, 0.0, [&] {
+        k_sel_diag<<<static_cast<unsigned>(e.dn), 256, kDiagSmem, stream_>>>(sdiag_.p + e.d0);
+      });
       ++launches_selinv_;
     }
   }

@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "kernels.cuh"
+#include "profiler.hpp"
 #include "symbolic.hpp"
 
 namespace gmrf {
@@ -69,6 +70,10 @@ class DeviceFactor {
   void solve(int mode, int nrhs, const double* b, double* x, bool on_device);
   // Selected inversion; fills the Σ panels and returns diag(Q⁻¹) in original order.
   void selinv(double* diag_out, bool on_device);
+  // Builds the selected-inversion plan and Σ storage ahead of time.
+  void prepare_selinv() {
+    if (!selinv_plan_) build_selinv_plan();
+  }
 
   // Host copies (tests / small n).
   void copy_l_panels(std::vector<double>& out) const;
@@ -82,6 +87,9 @@ class DeviceFactor {
   int64_t launches_numeric() const { return launches_numeric_; }
   int64_t launches_solve() const { return launches_solve_; }
   int64_t launches_selinv() const { return launches_selinv_; }
+  // Per-kernel-class timing (off unless enabled); callers may share one profiler.
+  void set_profiler(KernelProfiler* p) { prof_ = p ? p : &own_prof_; }
+  KernelProfiler& profiler() { return *prof_; }
 
  private:
   void build_factor_plan();
@@ -100,6 +108,7 @@ class DeviceFactor {
 
   struct FLevel {
     int64_t ea0, ean, po0, pon, pan0, pann, gm0, gmn;
+    double ea_bytes, po_flops, tr_flops, gm_flops;  // algorithmic work per launch
   };
   std::vector<FLevel> flev_;
   DevBuf<ColTask> ea_;
@@ -108,7 +117,11 @@ class DeviceFactor {
 
   struct SLevel {
     int64_t ga0, gan, y0, yn, t0, tn, z0, zn, d0, dn;
+    double ga_bytes, y_flops, t_flops, z_flops, d_flops;
   };
+  std::vector<double> lvl_bytes_;  // solve: L panel + row-index bytes per tree level
+  KernelProfiler own_prof_;
+  KernelProfiler* prof_ = &own_prof_;
   std::vector<SLevel> slev_;
   DevBuf<ColTask> sga_;
   DevBuf<GemmTask> sgemm_;

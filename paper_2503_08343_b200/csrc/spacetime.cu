@@ -445,11 +445,7 @@ void SpaceTimePosterior::assemble_device() {
   const i64 np = static_cast<i64>(pri_.size());
   d_qcond_.alloc(np);
   d_qeff_.alloc(np);
-  BlkDev b{d_blk_cp_.p, d_blk_ri_.p, d_blk_v_.p, ns_};
-  k_st_assemble<<<grid_for(n_), 256, 0, stream_>>>(d_pcp_.p, d_pri_.p, n_, ns_, nt_, blk_.t,
-                                                  1.0 / spec_.eps, spec_.ic_noise_prec,
-                                                  d_slack_.p, b, d_qcond_.p, d_qeff_.p);
-  times_.kernel_launches += 1;
+  assemble_values();
   // S_cond: CSC (columns, for Sᵀx) and CSR (rows, for S w)
   d_scp_.upload(s_.cp, stream_);
   d_sri_.upload(s_.ri, stream_);
@@ -471,12 +467,27 @@ void SpaceTimePosterior::assemble_device() {
     kept_.upload(kept, stream_);
   }
   fac_ = std::make_unique<DeviceFactor>(sym_, stream_);
+  fac_->prepare_selinv();
+  fac_->set_profiler(&prof_);
   for (DevBuf<double>* v : {&mean_cond_, &mean_, &var_, &x_, &c_, &g_, &d_, &cand_, &r1_, &u0_})
     v->alloc(std::max(n_, 1));
   w_.alloc(std::max(ms_, 1));
   f_.alloc(std::max(nres_, 1));
   fc_.alloc(std::max(nres_, 1));
   part_.alloc(kDotBlocks + 1);
+}
+
+// Row 1: joint prior / q_eff values on the master pattern (device).
+void SpaceTimePosterior::assemble_values() {
+  BlkDev b{d_blk_cp_.p, d_blk_ri_.p, d_blk_v_.p, ns_};
+  const double np = static_cast<double>(pri_.size());
+  // algorithmic bytes: write Q_cond and q_eff (16 B/entry) + pattern (4 B/entry + 8 B/column)
+  prof_.run(stream_, "assemble.prior", 0.0, 20.0 * np + 8.0 * n_, [&] {
+    k_st_assemble<<<grid_for(n_), 256, 0, stream_>>>(d_pcp_.p, d_pri_.p, n_, ns_, nt_, blk_.t,
+                                                    1.0 / spec_.eps, spec_.ic_noise_prec,
+                                                    d_slack_.p, b, d_qcond_.p, d_qeff_.p);
+  });
+  times_.kernel_launches += 1;
 }
 
 double SpaceTimePosterior::dot(const double* a, const double* b, i64 n) {
@@ -520,9 +531,15 @@ double SpaceTimePosterior::objective(const double* d_x, const double* d_fx) {
 
 void SpaceTimePosterior::fill_panels(const double* base, bool with_jacobian) {
   fac_->begin_numeric();
-  k_fill_panels<<<grid_for(n_), 256, 0, stream_>>>(
-      d_pcp_.p, d_pri_.p, n_, fac_->d_qmap(), base, with_jacobian ? d_jcp_.p : nullptr, d_jri_.p,
-      d_jmap_.p, d_jv_.p, spec_.pde_noise_prec, fac_->d_l());
+  // algorithmic bytes: base + qmap + pattern (20 B/entry), L writes for the
+  // lower half (4 B/entry), J values/rows/map (20 B/nnz) when JᵀΛJ is added
+  const double np = static_cast<double>(pri_.size());
+  const double bytes = 24.0 * np + (with_jacobian ? 20.0 * static_cast<double>(jci_.size()) : 0.0);
+  prof_.run(stream_, with_jacobian ? "update.h_jtlj" : "update.q_base", 0.0, bytes, [&] {
+    k_fill_panels<<<grid_for(n_), 256, 0, stream_>>>(
+        d_pcp_.p, d_pri_.p, n_, fac_->d_qmap(), base, with_jacobian ? d_jcp_.p : nullptr,
+        d_jri_.p, d_jmap_.p, d_jv_.p, spec_.pde_noise_prec, fac_->d_l());
+  });
   times_.kernel_launches += 1;
 }
 
@@ -533,6 +550,12 @@ std::vector<GnIter> SpaceTimePosterior::run(const double* u0, const GnConfig& cf
   require(cfg.shrink > 0.0 && cfg.shrink < 1.0, kContract, "gauss-newton: shrink factor in (0,1)");
   std::vector<GnIter> trace;
   converged_ = false;
+  {
+    const double setup = times_.setup_host_ms, init = times_.assemble_ms;
+    times_ = PhaseTimes{};
+    times_.setup_host_ms = setup;
+    times_.init_ms = init;
+  }
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
@@ -564,6 +587,9 @@ std::vector<GnIter> SpaceTimePosterior::run(const double* u0, const GnConfig& cf
       throw Error(kNotSpd, std::string(what) + ": cholesky: non-positive pivot at index " +
                                std::to_string(bad));
   };
+
+  // ---- prior + q_eff assembly on the device (spatiotemporal.hpp:79-195) ----
+  phase(times_.assemble_ms, [&] { assemble_values(); });
 
   // ---- IC conditioning (condition_affine, gmrf.hpp:145-170) ----
   phase(times_.condition_ms, [&] {

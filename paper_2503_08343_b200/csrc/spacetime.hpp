@@ -47,7 +47,8 @@ struct GnIter {
 
 struct PhaseTimes {
   double setup_host_ms = 0;   // host: spatial blocks, patterns, symbolic (ND)
-  double assemble_ms = 0;     // device: prior / q_eff assembly + S upload
+  double init_ms = 0;         // one-off device setup: uploads, first assembly
+  double assemble_ms = 0;     // device: prior / q_eff assembly (per run)
   double condition_ms = 0;    // IC conditioning factor + mean solve
   double gn_ms = 0;           // Gauss-Newton loop
   double laplace_ms = 0;      // Laplace precision + factorization
@@ -85,6 +86,7 @@ class SpaceTimePosterior {
  private:
   void build_host();
   void assemble_device();
+  void assemble_values();
   void fill_panels(const double* base, bool with_jacobian);
   double objective(const double* d_x, const double* d_fx);
   double dot(const double* a, const double* b, i64 n);
@@ -99,6 +101,11 @@ class SpaceTimePosterior {
   std::shared_ptr<const Symbolic> sym_;
   std::unique_ptr<DeviceFactor> fac_;
   PhaseTimes times_;
+
+ public:
+  KernelProfiler prof_;  // per-kernel-class timing (off by default)
+
+ private:
   bool converged_ = false;
 
   // host patterns

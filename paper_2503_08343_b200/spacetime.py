@@ -135,6 +135,18 @@ class SpaceTimePosterior:
         _check(rc)
         return mean, var, trace, bool(conv.value)
 
+    def set_profile(self, on: bool):
+        _check(_capi.load().gmrf_spacetime_set_profile(self._h, int(on)))
+
+    def kernel_stats(self) -> dict:
+        """{kernel class: dict(launches, ms, flops, bytes)} accumulated since set_profile(True)."""
+        arr = (_capi.KernelStat * 64)()
+        n = C.c_int32()
+        _check(_capi.load().gmrf_spacetime_kernel_stats(self._h, C.cast(arr, C.c_void_p), 64,
+                                                        C.byref(n)))
+        return {a.name.decode(): dict(launches=a.launches, ms=a.ms, flops=a.flops, bytes=a.bytes)
+                for a in arr[: n.value]}
+
     def device_results(self):
         m, v = C.c_void_p(), C.c_void_p()
         _check(_capi.load().gmrf_spacetime_device_results(self._h, C.byref(m), C.byref(v)))
