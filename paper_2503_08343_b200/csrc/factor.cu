@@ -6,6 +6,7 @@
 #include <string>
 
 #include "kernels.cu"  // single translation unit for all device code
+#include "solve.cuh"
 
 namespace gmrf {
 
@@ -32,6 +33,18 @@ void set_smem_attrs() {
 }
 
 inline int nchunks(int w) { return (w + kNB - 1) / kNB; }
+
+template <int NR>
+void set_solve_smem(int maxw) {
+  const int smem_diag = (maxw * NR + 64 * 65) * static_cast<int>(sizeof(double));
+  const int smem_off = maxw * NR * static_cast<int>(sizeof(double));
+  cuda_check(cudaFuncSetAttribute(k_fsolve_diag<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  smem_diag), "smem fsolve_diag");
+  cuda_check(cudaFuncSetAttribute(k_bsolve_diag<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  smem_diag), "smem bsolve_diag");
+  cuda_check(cudaFuncSetAttribute(k_fsolve_off<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  std::max(smem_off, 1)), "smem fsolve_off");
+}
 
 // Algorithmic flops of one tile: 2·k per needed output entry; a tile on the
 // diagonal of a symmetric update only needs its lower trapezoid.
@@ -73,13 +86,35 @@ DeviceFactor::DeviceFactor(std::shared_ptr<const Symbolic> sym, cudaStream_t str
     for (int k = 0; k < s.ns; ++k) lsn[nx[s.sn_level[k]]++] = k;
   }
   lvl_sn_.upload(lsn, stream_);
-  std::vector<int64_t> fp(s.ns + 1, 0), up(s.ns + 1, 0);
+  // solve workspaces: update vectors (r_s) and backward partials (tiles_s × w_s),
+  // plus the 128-row tiles of every supernode's rectangular block, per level
+  std::vector<int64_t> up(s.ns + 1, 0), pp(s.ns + 1, 0);
+  maxw_ = 1;
   for (int k = 0; k < s.ns; ++k) {
-    fp[k + 1] = fp[k] + s.rows(k);
-    up[k + 1] = up[k] + s.r(k);
+    const int r = s.r(k), nt = (r + kSolveRows - 1) / kSolveRows;
+    up[k + 1] = up[k] + r;
+    pp[k + 1] = pp[k] + static_cast<int64_t>(nt) * s.w(k);
+    maxw_ = std::max(maxw_, s.w(k));
   }
-  fptr_.upload(fp, stream_);
+  uv_total_ = up[s.ns];
+  p_total_ = pp[s.ns];
   uvptr_.upload(up, stream_);
+  pptr_.upload(pp, stream_);
+  {
+    std::vector<SolveTile> tl;
+    tile_ptr_.assign(s.n_levels + 1, 0);
+    for (int l = 0; l < s.n_levels; ++l) {
+      for (int64_t q = lvl_ptr_[l]; q < lvl_ptr_[l + 1]; ++q) {
+        const int k = lsn[q], r = s.r(k);
+        for (int t = 0; t * kSolveRows < r; ++t) tl.push_back({k, t * kSolveRows, t});
+      }
+      tile_ptr_[l + 1] = static_cast<int64_t>(tl.size());
+    }
+    tiles_.upload(tl, stream_);
+  }
+  set_solve_smem<1>(maxw_);
+  if ((200 * 1024 / 8 - 64 * 65) / maxw_ >= 4) set_solve_smem<4>(maxw_);
+  if ((200 * 1024 / 8 - 64 * 65) / maxw_ >= 16) set_solve_smem<16>(maxw_);
   // solve traffic per level: the L panel (8 B/entry, lower trapezoid) + row indices
   lvl_bytes_.assign(s.n_levels, 0.0);
   for (int k = 0; k < s.ns; ++k) {
@@ -107,7 +142,7 @@ SymDev DeviceFactor::symdev() const {
 }
 
 int64_t DeviceFactor::device_bytes() const {
-  return static_cast<int64_t>((L_.n + U_.n + Sig_.n + q_.n + F_.n + Uv_.n + v1_.n + v2_.n) *
+  return static_cast<int64_t>((L_.n + U_.n + Sig_.n + q_.n + P_.n + Uv_.n + v1_.n + v2_.n) *
                               sizeof(double)) +
          static_cast<int64_t>(gemm_.n * sizeof(GemmTask) + sgemm_.n * sizeof(GemmTask));
 }
@@ -415,17 +450,51 @@ int32_t DeviceFactor::factor_panels() {
 void DeviceFactor::ensure_solve_ws(int nrhs) {
   if (nrhs <= ws_nrhs_) return;
   const Symbolic& s = *sym_;
-  int64_t fr = 0, ur = 0;
-  for (int k = 0; k < s.ns; ++k) {
-    fr += s.rows(k);
-    ur += s.r(k);
-  }
-  F_.alloc(std::max<int64_t>(fr * nrhs, 1));
-  Uv_.alloc(std::max<int64_t>(ur * nrhs, 1));
+  Uv_.alloc(std::max<int64_t>(uv_total_ * nrhs, 1));
+  P_.alloc(std::max<int64_t>(p_total_ * nrhs, 1));
   v1_.alloc(std::max<int64_t>(static_cast<int64_t>(s.n) * nrhs, 1));
   v2_.alloc(std::max<int64_t>(static_cast<int64_t>(s.n) * nrhs, 1));
   ws_nrhs_ = nrhs;
 }
+
+namespace {
+template <int NR>
+void launch_solve_levels(const DeviceFactor* self, bool fwd, bool bwd, int nlev,
+                         const std::vector<int64_t>& lvl_ptr, const int32_t* lvl_sn,
+                         const std::vector<int64_t>& tile_ptr, const SolveTile* tiles, SymDev sd,
+                         const double* L, double* y, int nr, double* Uv, const int64_t* uvptr,
+                         double* P, const int64_t* pptr, int maxw, cudaStream_t st,
+                         KernelProfiler& pf, const std::vector<double>& lvl_bytes,
+                         int64_t& launches) {
+  (void)self;
+  const int smem_diag = (maxw * NR + 64 * 65) * static_cast<int>(sizeof(double));
+  const int smem_off = maxw * NR * static_cast<int>(sizeof(double));
+  if (fwd)
+    for (int l = 0; l < nlev; ++l) {
+      const int cnt = static_cast<int>(lvl_ptr[l + 1] - lvl_ptr[l]);
+      const int nt = static_cast<int>(tile_ptr[l + 1] - tile_ptr[l]);
+      pf.run(st, "solve.forward", 0.0, lvl_bytes[l], [&] {
+        k_fsolve_diag<NR><<<cnt, 256, smem_diag, st>>>(lvl_sn + lvl_ptr[l], sd, L, y, nr, Uv, uvptr);
+        if (nt)
+          k_fsolve_off<NR><<<nt, kSolveRows, smem_off, st>>>(tiles + tile_ptr[l], sd, L, y, nr, Uv,
+                                                             uvptr);
+      });
+      launches += 1 + (nt > 0);
+    }
+  if (bwd)
+    for (int l = nlev - 1; l >= 0; --l) {
+      const int cnt = static_cast<int>(lvl_ptr[l + 1] - lvl_ptr[l]);
+      const int nt = static_cast<int>(tile_ptr[l + 1] - tile_ptr[l]);
+      pf.run(st, "solve.backward", 0.0, lvl_bytes[l], [&] {
+        if (nt)
+          k_bsolve_off<NR><<<nt, 256, 0, st>>>(tiles + tile_ptr[l], sd, L, y, nr, P, pptr);
+        k_bsolve_diag<NR><<<cnt, 256, smem_diag, st>>>(lvl_sn + lvl_ptr[l], sd, L, y, nr, P, pptr);
+      });
+      launches += 1 + (nt > 0);
+    }
+}
+
+}  // namespace
 
 void DeviceFactor::solve(int mode, int nrhs, const double* b, double* x, bool on_device) {
   require(factored_, kContract, "solve: factor not computed");
@@ -435,8 +504,12 @@ void DeviceFactor::solve(int mode, int nrhs, const double* b, double* x, bool on
   if (n == 0 || nrhs == 0) return;
   launches_solve_ = 0;
   const SymDev sd = symdev();
-  for (int r0 = 0; r0 < nrhs; r0 += kMaxRhs) {
-    const int nr = std::min(kMaxRhs, nrhs - r0);
+  // right-hand sides per pass: 1, or up to 16 within the shared-memory budget
+  const int cap = static_cast<int>((200 * 1024 / 8 - 64 * 65) / std::max(maxw_, 1));
+  require(cap >= 1, kContract, "solve: supernode too wide for the shared-memory triangle");
+  const int nrb = nrhs == 1 ? 1 : (cap >= 16 ? 16 : (cap >= 4 ? 4 : 1));
+  for (int r0 = 0; r0 < nrhs; r0 += nrb) {
+    const int nr = std::min(nrb, nrhs - r0);
     ensure_solve_ws(nr);
     const double* bb = b + static_cast<int64_t>(r0) * n;
     double* xx = x + static_cast<int64_t>(r0) * n;
@@ -458,25 +531,19 @@ void DeviceFactor::solve(int mode, int nrhs, const double* b, double* x, bool on
                                  stream_),
                  "copy b");
     }
-    KernelProfiler& pf = *prof_;
-    if (mode == 0 || mode == 2)
-      for (int l = 0; l < s.n_levels; ++l) {
-        const int cnt = static_cast<int>(lvl_ptr_[l + 1] - lvl_ptr_[l]);
-        pf.run(stream_, "solve.forward", 0.0, lvl_bytes_[l], [&] {
-          k_solve_fwd<<<cnt, 256, 0, stream_>>>(lvl_sn_.p + lvl_ptr_[l], sd, L_.p, y, nr, F_.p,
-                                                Uv_.p, fptr_.p, uvptr_.p);
-        });
-        ++launches_solve_;
-      }
-    if (mode == 1 || mode == 2)
-      for (int l = s.n_levels - 1; l >= 0; --l) {
-        const int cnt = static_cast<int>(lvl_ptr_[l + 1] - lvl_ptr_[l]);
-        pf.run(stream_, "solve.backward", 0.0, lvl_bytes_[l], [&] {
-          k_solve_bwd<<<cnt, 256, 0, stream_>>>(lvl_sn_.p + lvl_ptr_[l], sd, L_.p, y, nr, F_.p,
-                                                fptr_.p);
-        });
-        ++launches_solve_;
-      }
+    const bool fwd = mode == 0 || mode == 2, bwd = mode == 1 || mode == 2;
+    if (nrb == 1)
+      launch_solve_levels<1>(this, fwd, bwd, s.n_levels, lvl_ptr_, lvl_sn_.p, tile_ptr_, tiles_.p,
+                             sd, L_.p, y, nr, Uv_.p, uvptr_.p, P_.p, pptr_.p, maxw_, stream_, *prof_,
+                             lvl_bytes_, launches_solve_);
+    else if (nrb == 4)
+      launch_solve_levels<4>(this, fwd, bwd, s.n_levels, lvl_ptr_, lvl_sn_.p, tile_ptr_, tiles_.p,
+                             sd, L_.p, y, nr, Uv_.p, uvptr_.p, P_.p, pptr_.p, maxw_, stream_, *prof_,
+                             lvl_bytes_, launches_solve_);
+    else
+      launch_solve_levels<16>(this, fwd, bwd, s.n_levels, lvl_ptr_, lvl_sn_.p, tile_ptr_, tiles_.p,
+                              sd, L_.p, y, nr, Uv_.p, uvptr_.p, P_.p, pptr_.p, maxw_, stream_,
+                              *prof_, lvl_bytes_, launches_solve_);
     if (mode == 2) {
       double* dst = on_device ? xx : v2_.p;
       k_permute_scatter<<<pblocks, 256, 0, stream_>>>(y, perm_.p, n, nr, dst);

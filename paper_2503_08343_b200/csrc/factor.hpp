@@ -9,6 +9,7 @@
 
 #include "kernels.cuh"
 #include "profiler.hpp"
+#include "solve_tile.hpp"
 #include "symbolic.hpp"
 
 namespace gmrf {
@@ -102,8 +103,12 @@ class DeviceFactor {
   bool factored_ = false, selinv_done_ = false;
 
   DevBuf<int32_t> first_, rows_, relmap_, chptr_, chlist_, perm_, col2sn_, snparent_, status_;
-  DevBuf<int64_t> rptr_, lptr_, uptr_, qmap_, fptr_, uvptr_;
-  DevBuf<double> L_, U_, Sig_, q_, F_, Uv_, v1_, v2_;
+  DevBuf<int64_t> rptr_, lptr_, uptr_, qmap_, pptr_, uvptr_;
+  DevBuf<double> L_, U_, Sig_, q_, P_, Uv_, v1_, v2_;
+  DevBuf<SolveTile> tiles_;
+  std::vector<int64_t> tile_ptr_;
+  int maxw_ = 1;
+  int64_t uv_total_ = 0, p_total_ = 0;
   int ws_nrhs_ = 0;
 
   struct FLevel {

@@ -271,125 +271,7 @@ __global__ void k_scatter_q(const double* __restrict__ q, const int64_t* __restr
   }
 }
 
-// ---------------------------------------------------------------------------
-// Triangular solves: one CTA per supernode of a tree level, all right-hand
-// sides at once so each L panel column is read once per sweep.
-// y/x: permuted vectors, n × nrhs column-major. F: per-supernode front
-// vectors (rows_s × nrhs), Uv: update vectors (r_s × nrhs).
-// ---------------------------------------------------------------------------
 constexpr int kMaxRhs = 16;
-
-__global__ void __launch_bounds__(256) k_solve_fwd(const int32_t* __restrict__ sns, SymDev sd,
-                                                   const double* __restrict__ L,
-                                                   double* __restrict__ y, int nrhs,
-                                                   double* __restrict__ F,
-                                                   double* __restrict__ Uv,
-                                                   const int64_t* __restrict__ fptr,
-                                                   const int64_t* __restrict__ uvptr) {
-  const int s = sns[blockIdx.x];
-  const int f0 = sd.sn_first[s];
-  const int w = sd.sn_first[s + 1] - f0;
-  const int rows = static_cast<int>(sd.sn_rptr[s + 1] - sd.sn_rptr[s]);
-  const int r = rows - w;
-  const int n = sd.n;
-  const double* Ls = L + sd.lptr[s];
-  double* f = F + fptr[s] * nrhs;
-  const int tid = threadIdx.x;
-  for (int idx = tid; idx < rows * nrhs; idx += blockDim.x) {
-    int a = idx % rows, rr = idx / rows;
-    f[idx] = a < w ? y[f0 + a + static_cast<int64_t>(rr) * n] : 0.0;
-  }
-  __syncthreads();
-  for (int q = sd.ch_ptr[s]; q < sd.ch_ptr[s + 1]; ++q) {
-    const int c = sd.ch_list[q];
-    const int wc = sd.sn_first[c + 1] - sd.sn_first[c];
-    const int rc = static_cast<int>(sd.sn_rptr[c + 1] - sd.sn_rptr[c]) - wc;
-    const int32_t* rel = sd.relmap + sd.sn_rptr[c] + wc;
-    const double* uc = Uv + uvptr[c] * nrhs;
-    for (int idx = tid; idx < rc * nrhs; idx += blockDim.x) {
-      int ia = idx % rc, rr = idx / rc;
-      f[rel[ia] + rr * rows] += uc[idx];
-    }
-    __syncthreads();
-  }
-  for (int j = 0; j < w; ++j) {
-    const double* lj = Ls + static_cast<int64_t>(j) * rows;
-    const double ljj = lj[j];
-    double fj[kMaxRhs];
-#pragma unroll
-    for (int rr = 0; rr < kMaxRhs; ++rr) fj[rr] = rr < nrhs ? f[j + rr * rows] / ljj : 0.0;
-    for (int i = j + 1 + tid; i < rows; i += blockDim.x) {
-      const double lij = lj[i];
-#pragma unroll
-      for (int rr = 0; rr < kMaxRhs; ++rr)
-        if (rr < nrhs) f[i + rr * rows] -= lij * fj[rr];
-    }
-    __syncthreads();
-    if (tid == 0)
-      for (int rr = 0; rr < nrhs; ++rr) f[j + rr * rows] = fj[rr];
-    __syncthreads();
-  }
-  for (int idx = tid; idx < rows * nrhs; idx += blockDim.x) {
-    int a = idx % rows, rr = idx / rows;
-    if (a < w)
-      y[f0 + a + static_cast<int64_t>(rr) * n] = f[idx];
-    else
-      Uv[uvptr[s] * nrhs + (a - w) + rr * r] = f[idx];
-  }
-}
-
-__global__ void __launch_bounds__(256) k_solve_bwd(const int32_t* __restrict__ sns, SymDev sd,
-                                                   const double* __restrict__ L,
-                                                   double* __restrict__ x, int nrhs,
-                                                   double* __restrict__ F,
-                                                   const int64_t* __restrict__ fptr) {
-  __shared__ double red[8][kMaxRhs];
-  const int s = sns[blockIdx.x];
-  const int f0 = sd.sn_first[s];
-  const int w = sd.sn_first[s + 1] - f0;
-  const int rows = static_cast<int>(sd.sn_rptr[s + 1] - sd.sn_rptr[s]);
-  const int n = sd.n;
-  const int32_t* srows = sd.sn_rows + sd.sn_rptr[s];
-  const double* Ls = L + sd.lptr[s];
-  double* f = F + fptr[s] * nrhs;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int idx = tid; idx < rows * nrhs; idx += blockDim.x) {
-    int a = idx % rows, rr = idx / rows;
-    f[idx] = x[srows[a] + static_cast<int64_t>(rr) * n];
-  }
-  __syncthreads();
-  for (int j = w - 1; j >= 0; --j) {
-    const double* lj = Ls + static_cast<int64_t>(j) * rows;
-    double part[kMaxRhs];
-#pragma unroll
-    for (int rr = 0; rr < kMaxRhs; ++rr) part[rr] = 0.0;
-    for (int i = j + 1 + tid; i < rows; i += blockDim.x) {
-      const double lij = lj[i];
-#pragma unroll
-      for (int rr = 0; rr < kMaxRhs; ++rr)
-        if (rr < nrhs) part[rr] += lij * f[i + rr * rows];
-    }
-#pragma unroll
-    for (int rr = 0; rr < kMaxRhs; ++rr) {
-      if (rr >= nrhs) break;
-      double v = part[rr];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (lane == 0) red[warp][rr] = v;
-    }
-    __syncthreads();
-    if (tid < nrhs) {
-      double v = 0.0;
-      for (int q = 0; q < 8; ++q) v += red[q][tid];
-      f[j + tid * rows] = (f[j + tid * rows] - v) / lj[j];
-    }
-    __syncthreads();
-  }
-  for (int idx = tid; idx < w * nrhs; idx += blockDim.x) {
-    int a = idx % w, rr = idx / w;
-    x[f0 + a + static_cast<int64_t>(rr) * n] = f[a + rr * rows];
-  }
-}
 
 // out[i + r*n] = in[perm[i] + r*n]  (gather: P b)
 __global__ void k_permute_gather(const double* __restrict__ in, const int32_t* __restrict__ perm,

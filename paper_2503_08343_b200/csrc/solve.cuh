@@ -1,0 +1,291 @@
+// Supernodal triangular solves (cholesky.hpp:179-222 semantics), level by
+// level over the supernodal tree. Per level and sweep, two launches:
+//   *_diag : one CTA per supernode — the dense w×w triangle L_JJ, blocked by
+//            64-column chunks whose diagonal blocks are staged in shared memory
+//            and solved by one warp;
+//   *_off  : many CTAs per supernode — the rectangular L_RJ part, 128-row tiles,
+//            streaming L once with coalesced column reads.
+// Deterministic: children are accumulated in a fixed order and the backward
+// partial sums over row tiles are reduced in tile order.
+#pragma once
+
+#include "kernels.cuh"
+#include "solve_tile.hpp"
+
+namespace gmrf {
+
+// ---- forward: diagonal triangle + children assembly -------------------------
+template <int NR>
+__global__ void __launch_bounds__(256) k_fsolve_diag(const int32_t* __restrict__ sns, SymDev sd,
+                                                     const double* __restrict__ L,
+                                                     double* __restrict__ y, int nrhs,
+                                                     double* __restrict__ Uv,
+                                                     const int64_t* __restrict__ uvptr) {
+  extern __shared__ double sm[];
+  const int s = sns[blockIdx.x];
+  const int f0 = sd.sn_first[s];
+  const int w = sd.sn_first[s + 1] - f0;
+  const int rows = static_cast<int>(sd.sn_rptr[s + 1] - sd.sn_rptr[s]);
+  const int r = rows - w;
+  const int n = sd.n;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const double* Ls = L + sd.lptr[s];
+  double* fJ = sm;                 // [rr*w + a]
+  double* Lb = sm + w * NR;        // [j*65 + i]
+  double* uS = Uv + uvptr[s] * nrhs;  // [i + rr*r]
+  for (int idx = tid; idx < w * nrhs; idx += blockDim.x) {
+    const int a = idx % w, rr = idx / w;
+    fJ[rr * w + a] = y[f0 + a + static_cast<int64_t>(rr) * n];
+  }
+  for (int idx = tid; idx < r * nrhs; idx += blockDim.x) uS[idx] = 0.0;
+  __syncthreads();
+  for (int q = sd.ch_ptr[s]; q < sd.ch_ptr[s + 1]; ++q) {
+    const int c = sd.ch_list[q];
+    const int wc = sd.sn_first[c + 1] - sd.sn_first[c];
+    const int rc = static_cast<int>(sd.sn_rptr[c + 1] - sd.sn_rptr[c]) - wc;
+    const int32_t* rel = sd.relmap + sd.sn_rptr[c] + wc;
+    const double* uc = Uv + uvptr[c] * nrhs;
+    for (int idx = tid; idx < rc * nrhs; idx += blockDim.x) {
+      const int ia = idx % rc, rr = idx / rc;
+      const int a = rel[ia];
+      const double v = uc[ia + rr * rc];
+      if (a < w) fJ[rr * w + a] += v;
+      else uS[(a - w) + rr * r] += v;
+    }
+    __syncthreads();
+  }
+  for (int c0 = 0; c0 < w; c0 += 64) {
+    const int wk = min(64, w - c0);
+    for (int idx = tid; idx < wk * wk; idx += blockDim.x) {
+      const int i = idx % wk, j = idx / wk;
+      if (i >= j) Lb[j * 65 + i] = Ls[(c0 + i) + static_cast<int64_t>(c0 + j) * rows];
+    }
+    __syncthreads();
+    if (warp == 0) {
+      double v0[NR], v1[NR];
+#pragma unroll
+      for (int rr = 0; rr < NR; ++rr) {
+        v0[rr] = (rr < nrhs && lane < wk) ? fJ[rr * w + c0 + lane] : 0.0;
+        v1[rr] = (rr < nrhs && lane + 32 < wk) ? fJ[rr * w + c0 + 32 + lane] : 0.0;
+      }
+      for (int j = 0; j < wk; ++j) {
+        const double ljj = Lb[j * 65 + j];
+        const double l0 = (lane > j && lane < wk) ? Lb[j * 65 + lane] : 0.0;
+        const double l1 = (lane + 32 > j && lane + 32 < wk) ? Lb[j * 65 + lane + 32] : 0.0;
+#pragma unroll
+        for (int rr = 0; rr < NR; ++rr) {
+          const double src = j < 32 ? v0[rr] : v1[rr];
+          const double xj = __shfl_sync(0xffffffffu, src, j & 31) / ljj;
+          if (lane == (j & 31)) {
+            if (j < 32) v0[rr] = xj; else v1[rr] = xj;
+          }
+          v0[rr] -= l0 * xj;
+          v1[rr] -= l1 * xj;
+        }
+      }
+#pragma unroll
+      for (int rr = 0; rr < NR; ++rr) {
+        if (rr >= nrhs) break;
+        if (lane < wk) fJ[rr * w + c0 + lane] = v0[rr];
+        if (lane + 32 < wk) fJ[rr * w + c0 + 32 + lane] = v1[rr];
+      }
+    }
+    __syncthreads();
+    // remaining rows of the triangle: f_i -= L[i, chunk] · x_chunk
+    for (int i = c0 + wk + tid; i < w; i += blockDim.x) {
+      double acc[NR];
+#pragma unroll
+      for (int rr = 0; rr < NR; ++rr) acc[rr] = rr < nrhs ? fJ[rr * w + i] : 0.0;
+      for (int j = 0; j < wk; ++j) {
+        const double l = Ls[i + static_cast<int64_t>(c0 + j) * rows];
+#pragma unroll
+        for (int rr = 0; rr < NR; ++rr) acc[rr] -= l * fJ[rr * w + c0 + j];
+      }
+#pragma unroll
+      for (int rr = 0; rr < NR; ++rr)
+        if (rr < nrhs) fJ[rr * w + i] = acc[rr];
+    }
+    __syncthreads();
+  }
+  for (int idx = tid; idx < w * nrhs; idx += blockDim.x) {
+    const int a = idx % w, rr = idx / w;
+    y[f0 + a + static_cast<int64_t>(rr) * n] = fJ[rr * w + a];
+  }
+}
+
+// ---- forward: u_R = f_R − L_RJ y_J, 128-row tiles ---------------------------
+template <int NR>
+__global__ void __launch_bounds__(kSolveRows) k_fsolve_off(const SolveTile* __restrict__ tiles,
+                                                          SymDev sd, const double* __restrict__ L,
+                                                          const double* __restrict__ y, int nrhs,
+                                                          double* __restrict__ Uv,
+                                                          const int64_t* __restrict__ uvptr) {
+  extern __shared__ double sm[];
+  const SolveTile t = tiles[blockIdx.x];
+  const int s = t.sn;
+  const int f0 = sd.sn_first[s];
+  const int w = sd.sn_first[s + 1] - f0;
+  const int rows = static_cast<int>(sd.sn_rptr[s + 1] - sd.sn_rptr[s]);
+  const int r = rows - w;
+  const int n = sd.n;
+  double* yJ = sm;  // [rr*w + j]
+  for (int idx = threadIdx.x; idx < w * nrhs; idx += blockDim.x) {
+    const int a = idx % w, rr = idx / w;
+    yJ[rr * w + a] = y[f0 + a + static_cast<int64_t>(rr) * n];
+  }
+  __syncthreads();
+  const int i = t.r0 + threadIdx.x;
+  if (i >= r) return;
+  const double* Lr = L + sd.lptr[s] + w + i;
+  double* u = Uv + uvptr[s] * nrhs;
+  double acc[NR];
+#pragma unroll
+  for (int rr = 0; rr < NR; ++rr) acc[rr] = rr < nrhs ? u[i + rr * r] : 0.0;
+  for (int j = 0; j < w; ++j) {
+    const double l = Lr[static_cast<int64_t>(j) * rows];
+#pragma unroll
+    for (int rr = 0; rr < NR; ++rr) acc[rr] -= l * yJ[rr * w + j];
+  }
+#pragma unroll
+  for (int rr = 0; rr < NR; ++rr)
+    if (rr < nrhs) u[i + rr * r] = acc[rr];
+}
+
+// ---- backward: partial sums t = L_RJᵀ x_R over 128-row tiles ----------------
+template <int NR>
+__global__ void __launch_bounds__(256) k_bsolve_off(const SolveTile* __restrict__ tiles, SymDev sd,
+                                                    const double* __restrict__ L,
+                                                    const double* __restrict__ x, int nrhs,
+                                                    double* __restrict__ P,
+                                                    const int64_t* __restrict__ pptr) {
+  __shared__ double xR[kSolveRows * NR];
+  const SolveTile t = tiles[blockIdx.x];
+  const int s = t.sn;
+  const int f0 = sd.sn_first[s];
+  const int w = sd.sn_first[s + 1] - f0;
+  const int rows = static_cast<int>(sd.sn_rptr[s + 1] - sd.sn_rptr[s]);
+  const int r = rows - w;
+  const int n = sd.n;
+  const int nt = min(kSolveRows, r - t.r0);
+  const int32_t* srows = sd.sn_rows + sd.sn_rptr[s] + w + t.r0;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int idx = tid; idx < nt * nrhs; idx += blockDim.x) {
+    const int ii = idx % nt, rr = idx / nt;
+    xR[rr * kSolveRows + ii] = x[srows[ii] + static_cast<int64_t>(rr) * n];
+  }
+  __syncthreads();
+  const double* Lt = L + sd.lptr[s] + w + t.r0;
+  double* Pt = P + (pptr[s] + static_cast<int64_t>(t.tidx) * w) * nrhs;  // [rr*w + j]
+  for (int j = warp; j < w; j += 8) {
+    const double* col = Lt + static_cast<int64_t>(j) * rows;
+    double acc[NR];
+#pragma unroll
+    for (int rr = 0; rr < NR; ++rr) acc[rr] = 0.0;
+    for (int ii = lane; ii < nt; ii += 32) {
+      const double l = col[ii];
+#pragma unroll
+      for (int rr = 0; rr < NR; ++rr) acc[rr] += l * xR[rr * kSolveRows + ii];
+    }
+#pragma unroll
+    for (int rr = 0; rr < NR; ++rr) {
+      double v = acc[rr];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0 && rr < nrhs) Pt[rr * w + j] = v;
+    }
+  }
+}
+
+// ---- backward: diagonal triangle  L_JJᵀ x_J = y_J − Σ_tiles t ---------------
+template <int NR>
+__global__ void __launch_bounds__(256) k_bsolve_diag(const int32_t* __restrict__ sns, SymDev sd,
+                                                     const double* __restrict__ L,
+                                                     double* __restrict__ x, int nrhs,
+                                                     const double* __restrict__ P,
+                                                     const int64_t* __restrict__ pptr) {
+  extern __shared__ double sm[];
+  const int s = sns[blockIdx.x];
+  const int f0 = sd.sn_first[s];
+  const int w = sd.sn_first[s + 1] - f0;
+  const int rows = static_cast<int>(sd.sn_rptr[s + 1] - sd.sn_rptr[s]);
+  const int r = rows - w;
+  const int n = sd.n;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const double* Ls = L + sd.lptr[s];
+  double* bJ = sm;           // [rr*w + a]
+  double* Lb = sm + w * NR;  // [j*65 + i]
+  const int ntiles = (r + kSolveRows - 1) / kSolveRows;
+  const double* Ps = P + pptr[s] * nrhs;
+  for (int idx = tid; idx < w * nrhs; idx += blockDim.x) {
+    const int a = idx % w, rr = idx / w;
+    double v = x[f0 + a + static_cast<int64_t>(rr) * n];
+    for (int t = 0; t < ntiles; ++t) v -= Ps[(static_cast<int64_t>(t) * w) * nrhs + rr * w + a];
+    bJ[rr * w + a] = v;
+  }
+  __syncthreads();
+  const int nch = (w + 63) / 64;
+  for (int ck = nch - 1; ck >= 0; --ck) {
+    const int c0 = ck * 64, wk = min(64, w - c0);
+    // contributions of the already-solved rows below the chunk inside the triangle
+    for (int j = warp; j < wk; j += 8) {
+      const double* col = Ls + static_cast<int64_t>(c0 + j) * rows;
+      double acc[NR];
+#pragma unroll
+      for (int rr = 0; rr < NR; ++rr) acc[rr] = 0.0;
+      for (int i = c0 + wk + lane; i < w; i += 32) {
+        const double l = col[i];
+#pragma unroll
+        for (int rr = 0; rr < NR; ++rr) acc[rr] += l * bJ[rr * w + i];
+      }
+#pragma unroll
+      for (int rr = 0; rr < NR; ++rr) {
+        double v = acc[rr];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0 && rr < nrhs) bJ[rr * w + c0 + j] -= v;
+      }
+    }
+    for (int idx = tid; idx < wk * wk; idx += blockDim.x) {
+      const int i = idx % wk, j = idx / wk;
+      if (i >= j) Lb[j * 65 + i] = Ls[(c0 + i) + static_cast<int64_t>(c0 + j) * rows];
+    }
+    __syncthreads();
+    if (warp == 0) {
+      double v0[NR], v1[NR];
+#pragma unroll
+      for (int rr = 0; rr < NR; ++rr) {
+        v0[rr] = (rr < nrhs && lane < wk) ? bJ[rr * w + c0 + lane] : 0.0;
+        v1[rr] = (rr < nrhs && lane + 32 < wk) ? bJ[rr * w + c0 + 32 + lane] : 0.0;
+      }
+      for (int j = wk - 1; j >= 0; --j) {
+        const double ljj = Lb[j * 65 + j];
+        // (Lᵀ)_{i,j} = L_{j,i}, stored at Lb[i*65 + j] for i < j
+        const double l0 = (lane < j) ? Lb[lane * 65 + j] : 0.0;
+        const double l1 = (lane + 32 < j) ? Lb[(lane + 32) * 65 + j] : 0.0;
+#pragma unroll
+        for (int rr = 0; rr < NR; ++rr) {
+          const double src = j < 32 ? v0[rr] : v1[rr];
+          const double xj = __shfl_sync(0xffffffffu, src, j & 31) / ljj;
+          if (lane == (j & 31)) {
+            if (j < 32) v0[rr] = xj; else v1[rr] = xj;
+          }
+          v0[rr] -= l0 * xj;
+          v1[rr] -= l1 * xj;
+        }
+      }
+#pragma unroll
+      for (int rr = 0; rr < NR; ++rr) {
+        if (rr >= nrhs) break;
+        if (lane < wk) bJ[rr * w + c0 + lane] = v0[rr];
+        if (lane + 32 < wk) bJ[rr * w + c0 + 32 + lane] = v1[rr];
+      }
+    }
+    __syncthreads();
+  }
+  for (int idx = tid; idx < w * nrhs; idx += blockDim.x) {
+    const int a = idx % w, rr = idx / w;
+    x[f0 + a + static_cast<int64_t>(rr) * n] = bJ[rr * w + a];
+  }
+}
+
+}  // namespace gmrf
