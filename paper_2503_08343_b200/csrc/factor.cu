@@ -6,6 +6,7 @@
 #include <string>
 
 #include "kernels.cu"  // single translation unit for all device code
+#include "panel.cuh"
 #include "solve.cuh"
 
 namespace gmrf {
@@ -21,8 +22,9 @@ constexpr int kDiagSmem = 3 * kNB * (kNB + 1) * sizeof(double);
 void set_smem_attrs() {
   static bool done = false;
   if (done) return;
-  cuda_check(cudaFuncSetAttribute(k_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, kPanelSmem),
-             "smem k_trsm");
+  cuda_check(cudaFuncSetAttribute(k_potrf_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kPanelFusedSmem),
+             "smem k_potrf_trsm");
   cuda_check(
       cudaFuncSetAttribute(k_sel_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, kPanelSmem),
       "smem k_sel_trsm");
@@ -73,6 +75,7 @@ DeviceFactor::DeviceFactor(std::shared_ptr<const Symbolic> sym, cudaStream_t str
   uptr_.upload(s.uptr, stream_);
   qmap_.upload(s.qmap, stream_);
   status_.alloc(1);
+  diag_.alloc(std::max(s.n, 1));
   L_.alloc(std::max<int64_t>(s.lptr[s.ns], 1));
   U_.alloc(std::max<int64_t>(s.uptr[s.ns], 1));
   q_.alloc(std::max<size_t>(s.qri.size(), 1));
@@ -193,8 +196,8 @@ void DeviceFactor::build_factor_plan() {
       tr_f[lv] += static_cast<double>(nbelow) * wk * wk;
       const PanelTask pt{Lk + c0 + static_cast<int64_t>(c0) * rows, rows, wk, nbelow, 0,
                          s.sn_first[k] + c0};
-      po[lv].push_back(pt);
-      for (int t = 0; t * kTrsmRows < nbelow; ++t) {
+      po[lv].push_back(pt);  // chunk list for the final diagonal write-back
+      for (int t = 0; t == 0 || t * kTrsmRows < nbelow; ++t) {
         PanelTask tt = pt;
         tt.tile = t;
         pan[lv].push_back(tt);
@@ -418,15 +421,10 @@ int32_t DeviceFactor::factor_panels() {
       });
       ++launches_numeric_;
     }
-    if (lv.pon) {
-      pf.run(stream_, "factor.potrf", lv.po_flops, 0.0, [&] {
-        k_potrf<<<static_cast<unsigned>(lv.pon), 128, 0, stream_>>>(po_.p + lv.po0, status_.p);
-      });
-      ++launches_numeric_;
-    }
     if (lv.pann) {
-      pf.run(stream_, "factor.trsm", lv.tr_flops, 0.0, [&] {
-        k_trsm<<<static_cast<unsigned>(lv.pann), 128, kPanelSmem, stream_>>>(pan_.p + lv.pan0);
+      pf.run(stream_, "factor.potrf_trsm", lv.po_flops + lv.tr_flops, 0.0, [&] {
+        k_potrf_trsm<<<static_cast<unsigned>(lv.pann), 128, kPanelFusedSmem, stream_>>>(
+            pan_.p + lv.pan0, status_.p, diag_.p);
       });
       ++launches_numeric_;
     }
@@ -436,6 +434,12 @@ int32_t DeviceFactor::factor_panels() {
       });
       ++launches_numeric_;
     }
+  }
+  if (po_.n) {
+    pf.run(stream_, "factor.diag_writeback", 0.0, 16.0 * s.n * kNB / 2.0, [&] {
+      k_diag_writeback<<<static_cast<unsigned>(po_.n), 128, 0, stream_>>>(po_.p, diag_.p);
+    });
+    ++launches_numeric_;
   }
   cuda_check(cudaGetLastError(), "factor launch");
   int st = INT_MAX;

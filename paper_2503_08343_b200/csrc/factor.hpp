@@ -104,7 +104,7 @@ class DeviceFactor {
 
   DevBuf<int32_t> first_, rows_, relmap_, chptr_, chlist_, perm_, col2sn_, snparent_, status_;
   DevBuf<int64_t> rptr_, lptr_, uptr_, qmap_, pptr_, uvptr_;
-  DevBuf<double> L_, U_, Sig_, q_, P_, Uv_, v1_, v2_;
+  DevBuf<double> L_, U_, Sig_, q_, P_, Uv_, v1_, v2_, diag_;
   DevBuf<SolveTile> tiles_;
   std::vector<int64_t> tile_ptr_;
   int maxw_ = 1;

@@ -143,80 +143,7 @@ __global__ void __launch_bounds__(128) k_gemm_tiles(const GemmTask* __restrict__
 }
 
 // ---------------------------------------------------------------------------
-// Panel step, part 1: Cholesky of the chunk's w×w diagonal block in shared
-// memory, one CTA per chunk. Non-positive pivots are reported as the smallest
-// failing internal column (reference cholesky.hpp:153-156 semantics).
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(128) k_potrf(const PanelTask* __restrict__ tasks,
-                                               int32_t* __restrict__ status) {
-  __shared__ double D[kNB * (kNB + 1)];  // column-major, pitch kNB+1
-  const PanelTask& t = tasks[blockIdx.x];
-  const int w = t.w, ld = t.ld, tid = threadIdx.x;
-  constexpr int DP = kNB + 1;
-  for (int idx = tid; idx < w * w; idx += blockDim.x) {
-    int i = idx % w, j = idx / w;
-    if (i >= j) D[j * DP + i] = t.d[i + static_cast<int64_t>(j) * ld];
-  }
-  __syncthreads();
-  for (int j = 0; j < w; ++j) {
-    if (tid == 0) {
-      double dj = D[j * DP + j];
-      if (!(dj > 0.0)) atomicMin(status, t.gcol + j);
-      D[j * DP + j] = sqrt(dj);
-    }
-    __syncthreads();
-    const double djj = D[j * DP + j];
-    for (int i = j + 1 + tid; i < w; i += blockDim.x) D[j * DP + i] /= djj;
-    __syncthreads();
-    const int rem = w - j - 1;
-    for (int idx = tid; idx < rem * rem; idx += blockDim.x) {
-      int i = j + 1 + idx % rem, k = j + 1 + idx / rem;
-      if (i >= k) D[k * DP + i] -= D[j * DP + i] * D[j * DP + k];
-    }
-    __syncthreads();
-  }
-  for (int idx = tid; idx < w * w; idx += blockDim.x) {
-    int i = idx % w, j = idx / w;
-    if (i >= j) t.d[i + static_cast<int64_t>(j) * ld] = D[j * DP + i];
-  }
-}
-
-// Panel step, part 2: X = B · L11⁻ᵀ for one kTrsmRows slab of the rows below
-// the (already factored) diagonal block.
-__global__ void __launch_bounds__(128) k_trsm(const PanelTask* __restrict__ tasks) {
-  extern __shared__ double smem[];
-  const PanelTask& t = tasks[blockIdx.x];
-  const int w = t.w, ld = t.ld, tid = threadIdx.x;
-  constexpr int DP = kNB + 1, XP = kTrsmRows + 1;
-  double* D = smem;
-  double* X = smem + kNB * DP;
-  const int r0 = t.tile * kTrsmRows;
-  const int nr = min(kTrsmRows, t.nbelow - r0);
-  if (nr <= 0) return;
-  for (int idx = tid; idx < w * w; idx += blockDim.x) {
-    int i = idx % w, j = idx / w;
-    if (i >= j) D[j * DP + i] = t.d[i + static_cast<int64_t>(j) * ld];
-  }
-  double* B = t.d + w + r0;
-  for (int idx = tid; idx < nr * w; idx += blockDim.x) {
-    int r = idx % nr, j = idx / nr;
-    X[j * XP + r] = B[r + static_cast<int64_t>(j) * ld];
-  }
-  __syncthreads();
-  if (tid < nr) {
-    for (int j = 0; j < w; ++j) {
-      double s = X[j * XP + tid];
-      for (int l = 0; l < j; ++l) s -= X[l * XP + tid] * D[l * DP + j];
-      X[j * XP + tid] = s / D[j * DP + j];
-    }
-  }
-  __syncthreads();
-  for (int idx = tid; idx < nr * w; idx += blockDim.x) {
-    int r = idx % nr, j = idx / nr;
-    B[r + static_cast<int64_t>(j) * ld] = X[j * XP + r];
-  }
-}
-
+// (panel step: panel.cuh)
 // ---------------------------------------------------------------------------
 // Extend-add (multifrontal assembly), gather form: one warp per (front, front
 // column). Children are visited in ascending order, so every target entry
