@@ -82,6 +82,10 @@ int gmrf_symbolic_info(const gmrf_symbolic_t* s, gmrf_symbolic_info_t* info);
 int gmrf_symbolic_export(const gmrf_symbolic_t* s, int32_t* perm, int32_t* parent,
                          int64_t* col_ptr_l);
 void gmrf_symbolic_free(gmrf_symbolic_t* s);
+/* Supernode partition (after relaxed amalgamation): first column [ns+1],
+ * front rows [ns], tree level [ns], parent supernode [ns] (-1 root). */
+int gmrf_symbolic_supernodes(const gmrf_symbolic_t* s, int32_t* first, int32_t* rows,
+                             int32_t* level, int32_t* parent);
 
 /* Device storage for a factor of the symbolic's pattern. */
 int gmrf_factor_create(const gmrf_symbolic_t* s, gmrf_factor_t** out);

@@ -82,6 +82,7 @@ SIGNATURES = {
     "gmrf_symbolic_info": (C.c_int, [C.c_void_p, C.POINTER(SymbolicInfo)]),
     "gmrf_symbolic_export": (C.c_int, [C.c_void_p, i32p, i32p, i64p]),
     "gmrf_symbolic_free": (None, [C.c_void_p]),
+    "gmrf_symbolic_supernodes": (C.c_int, [C.c_void_p, i32p, i32p, i32p, i32p]),
     "gmrf_factor_create": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
     "gmrf_factor_set_stream": (C.c_int, [C.c_void_p, C.c_void_p]),
     "gmrf_factor_numeric": (C.c_int, [C.c_void_p, f64p, i32p]),

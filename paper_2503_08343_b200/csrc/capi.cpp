@@ -94,6 +94,20 @@ int gmrf_symbolic_export(const gmrf_symbolic_t* h, int32_t* perm, int32_t* paren
 
 void gmrf_symbolic_free(gmrf_symbolic_t* h) { delete h; }
 
+int gmrf_symbolic_supernodes(const gmrf_symbolic_t* h, int32_t* first, int32_t* rows,
+                             int32_t* level, int32_t* parent) {
+  return guard([&] {
+    const gmrf::Symbolic& s = *h->s;
+    for (int k = 0; k < s.ns; ++k) {
+      if (first) first[k] = s.sn_first[k];
+      if (rows) rows[k] = s.rows(k);
+      if (level) level[k] = s.sn_level[k];
+      if (parent) parent[k] = s.sn_parent[k];
+    }
+    if (first) first[s.ns] = s.n;
+  });
+}
+
 int gmrf_factor_create(const gmrf_symbolic_t* h, gmrf_factor_t** out) {
   return guard([&] {
     auto f = std::make_unique<gmrf_factor>();
@@ -372,6 +386,7 @@ int gmrf_spacetime_set_profile(gmrf_spacetime_t* h, int32_t on) {
   return guard([&] {
     h->p->prof_.reset();
     h->p->prof_.on = on != 0;
+    h->p->prof_.level_detail = on == 2;  // 2: per-level kernel classes
   });
 }
 

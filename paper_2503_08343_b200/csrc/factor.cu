@@ -412,24 +412,26 @@ int32_t DeviceFactor::factor_panels() {
   const Symbolic& s = *sym_;
   const SymDev sd = symdev();
   KernelProfiler& pf = *prof_;
-  for (const FLevel& lv : flev_) {
+  for (size_t li = 0; li < flev_.size(); ++li) {
+    const FLevel& lv = flev_[li];
+    const int lvl = static_cast<int>(li);
     if (lv.ean) {
       int blocks = static_cast<int>((lv.ean * 32 + 255) / 256);
-      pf.run(stream_, "factor.extend_add", 0.0, lv.ea_bytes, [&] {
+      pf.run(stream_, pf.tag("factor.extend_add", lvl), 0.0, lv.ea_bytes, [&] {
         k_extend_add<<<blocks, 256, 0, stream_>>>(ea_.p + lv.ea0, static_cast<int>(lv.ean), sd,
                                                  L_.p, U_.p);
       });
       ++launches_numeric_;
     }
     if (lv.pann) {
-      pf.run(stream_, "factor.potrf_trsm", lv.po_flops + lv.tr_flops, 0.0, [&] {
+      pf.run(stream_, pf.tag("factor.potrf_trsm", lvl), lv.po_flops + lv.tr_flops, 0.0, [&] {
         k_potrf_trsm<<<static_cast<unsigned>(lv.pann), 128, kPanelFusedSmem, stream_>>>(
             pan_.p + lv.pan0, status_.p, diag_.p);
       });
       ++launches_numeric_;
     }
     if (lv.gmn) {
-      pf.run(stream_, "factor.gemm_dmma", lv.gm_flops, 0.0, [&] {
+      pf.run(stream_, pf.tag("factor.gemm_dmma", lvl), lv.gm_flops, 0.0, [&] {
         k_gemm_tiles<<<static_cast<unsigned>(lv.gmn), 128, 0, stream_>>>(gemm_.p + lv.gm0);
       });
       ++launches_numeric_;

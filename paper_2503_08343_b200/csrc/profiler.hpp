@@ -19,9 +19,14 @@ struct KernelStat {
 class KernelProfiler {
  public:
   bool on = false;
+  bool level_detail = false;  // suffix kernel classes with "@<level>"
+
+  std::string tag(const char* base, int level) const {
+    return level_detail ? std::string(base) + "@" + std::to_string(level) : std::string(base);
+  }
 
   template <typename F>
-  void run(cudaStream_t s, const char* name, double flops, double bytes, F&& launch) {
+  void run(cudaStream_t s, const std::string& name, double flops, double bytes, F&& launch) {
     if (!on) {
       launch();
       return;

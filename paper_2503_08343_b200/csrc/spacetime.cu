@@ -350,8 +350,25 @@ void SpaceTimePosterior::build_host() {
       pcp_[C + 1] = static_cast<i64>(pri_.size());
     }
 
-  // ---- symbolic (nested dissection), shared by every factorization of the run
-  sym_ = std::make_shared<const Symbolic>(analyze(n_, pcp_.data(), pri_.data(), nullptr));
+  // ---- symbolic: geometric nested dissection of the space-time grid (separator
+  // thickness = the coupling radii of the pattern), shared by every
+  // factorization of the run
+  {
+    int rx = 1, rt = 1;
+    for (int C = 0; C < n_; ++C)
+      for (i64 p = pcp_[C]; p < pcp_[C + 1]; ++p) {
+        const int R = pri_[p];
+        rx = std::max(rx, std::abs(R % ns_ - C % ns_));
+        rt = std::max(rt, std::abs(R / ns_ - C / ns_));
+      }
+    std::vector<char> first(static_cast<size_t>(n_), 0);
+    for (int s = 0; s < nt_; ++s)
+      for (int d = 0; d < ns_; ++d) first[static_cast<size_t>(s) * ns_ + d] = sl[d];
+    std::vector<i32> perm = grid_nd_order(ns_, nt_, rx, rt, first);
+    SymbolicOptions opt;
+    opt.postorder_given = true;
+    sym_ = std::make_shared<const Symbolic>(analyze(n_, pcp_.data(), pri_.data(), perm.data(), opt));
+  }
 
   // ---- S_cond = [S_prior | Aᵀ L_ε] (gmrf.hpp:165), CSC, columns in the reference order
   const double st = std::sqrt(blk_.t);

@@ -142,6 +142,62 @@ std::vector<i32> nd_order(i32 n, const i64* qcp, const i32* qri) {
   return perm;
 }
 
+std::vector<i32> grid_nd_order(i32 nx, i32 nt, i32 xw, i32 tw, const std::vector<char>& first,
+                               i32 leaf) {
+  std::vector<i32> perm;
+  perm.reserve(static_cast<size_t>(nx) * nt);
+  for (i32 t = 0; t < nt; ++t)
+    for (i32 x = 0; x < nx; ++x)
+      if (first[static_cast<size_t>(t) * nx + x]) perm.push_back(t * nx + x);
+  auto emit = [&](i32 x0, i32 x1, i32 t0, i32 t1) {
+    for (i32 t = t0; t < t1; ++t)
+      for (i32 x = x0; x < x1; ++x)
+        if (!first[static_cast<size_t>(t) * nx + x]) perm.push_back(t * nx + x);
+  };
+  struct Box {
+    i32 x0, x1, t0, t1;
+  };
+  // explicit recursion: (box, stage) with stage 0 = split, 1 = emit separator
+  struct Frame {
+    Box b, sep;
+    int stage;
+  };
+  std::vector<Frame> st;
+  st.push_back({{0, nx, 0, nt}, {0, 0, 0, 0}, 0});
+  while (!st.empty()) {
+    Frame f = st.back();
+    st.pop_back();
+    if (f.stage == 1) {
+      emit(f.sep.x0, f.sep.x1, f.sep.t0, f.sep.t1);
+      continue;
+    }
+    const Box b = f.b;
+    const i32 ex = b.x1 - b.x0, et = b.t1 - b.t0;
+    if (static_cast<i64>(ex) * et <= leaf || (ex <= xw + 1 && et <= tw + 1)) {
+      emit(b.x0, b.x1, b.t0, b.t1);
+      continue;
+    }
+    const bool cut_t = et > tw + 1 && (ex <= xw + 1 || static_cast<double>(et) / tw >=
+                                                          static_cast<double>(ex) / xw);
+    Box lo, hi, sep;
+    if (cut_t) {
+      const i32 tm = b.t0 + (et - tw) / 2;
+      lo = {b.x0, b.x1, b.t0, tm};
+      sep = {b.x0, b.x1, tm, tm + tw};
+      hi = {b.x0, b.x1, tm + tw, b.t1};
+    } else {
+      const i32 xm = b.x0 + (ex - xw) / 2;
+      lo = {b.x0, xm, b.t0, b.t1};
+      sep = {xm, xm + xw, b.t0, b.t1};
+      hi = {xm + xw, b.x1, b.t0, b.t1};
+    }
+    st.push_back({b, sep, 1});
+    st.push_back({hi, {}, 0});
+    st.push_back({lo, {}, 0});
+  }
+  return perm;
+}
+
 Symbolic analyze(i32 n, const i64* qcp, const i32* qri, const i32* perm_in,
                  const SymbolicOptions& opt) {
   require(n >= 0, kDimension, "symbolic_analyze: negative dimension");
@@ -174,7 +230,7 @@ Symbolic analyze(i32 n, const i64* qcp, const i32* qri, const i32* perm_in,
   permuted_upper(n, qcp, qri, s.pinv, ucp, uri);
   s.parent = etree(n, ucp, uri);
 
-  if (!perm_in && opt.postorder) {
+  if ((!perm_in && opt.postorder) || (perm_in && opt.postorder_given)) {
     std::vector<i32> post = postorder(n, s.parent);
     std::vector<i32> p2(n);
     for (i32 i = 0; i < n; ++i) p2[i] = s.perm[post[i]];

@@ -23,7 +23,8 @@ struct SymbolicOptions {
   double relax_z2 = 0.25;
   double relax_z3 = 0.03;      // any width with zeros below this
   bool amalgamate = true;
-  bool postorder = true;       // only applied to orderings computed here
+  bool postorder = true;       // applied to orderings computed here
+  bool postorder_given = false;  // also postorder a caller-supplied ordering
 };
 
 struct Symbolic {
@@ -72,6 +73,15 @@ Symbolic analyze(i32 n, const i64* qcp, const i32* qri, const i32* perm,
 
 // METIS NodeND fill-reducing ordering (new -> old) of a symmetric pattern.
 std::vector<i32> nd_order(i32 n, const i64* qcp, const i32* qri);
+
+// Geometric nested dissection of a structured nx × nt space-time grid (node
+// t·nx + x): recursively cut the axis with the larger
+// extent/thickness; separators are `tw` slices thick in time and `xw` nodes
+// thick in space (the coupling radii of the precision); halves first, then
+// the separator. Nodes flagged in `first` (decoupled slack coordinates) are
+// ordered first. Deterministic and O(n).
+std::vector<i32> grid_nd_order(i32 nx, i32 nt, i32 xw, i32 tw, const std::vector<char>& first,
+                               i32 leaf = 64);
 
 // Exact reference L pattern (col_ptr from s.colptr_l): row indices per column,
 // ascending, diagonal first — the layout of CholeskyFactor::L
