@@ -177,13 +177,19 @@ __global__ void k_extend_add(const ColTask* __restrict__ tasks, int ntasks, SymD
     const int ib = find_sorted(rel, rc, b);
     if (ib < 0) continue;
     const double* Uc = U + sd.uptr[c] + static_cast<int64_t>(ib) * rc;
-    if (b < w) {
-      double* dst = Ls + static_cast<int64_t>(b) * rows;
-      for (int ia = ib + lane; ia < rc; ia += 32) dst[rel[ia]] += Uc[ia];
-    } else {
-      double* dst = Us + static_cast<int64_t>(b - w) * r - w;
-      for (int ia = ib + lane; ia < rc; ia += 32) dst[rel[ia]] += Uc[ia];
+    double* dst = b < w ? Ls + static_cast<int64_t>(b) * rows : Us + static_cast<int64_t>(b - w) * r - w;
+    // 4 independent gathers in flight per lane (memory-level parallelism)
+    int ia = ib + lane;
+    for (; ia + 96 < rc; ia += 128) {
+      int t0 = rel[ia], t1 = rel[ia + 32], t2 = rel[ia + 64], t3 = rel[ia + 96];
+      double u0 = Uc[ia], u1 = Uc[ia + 32], u2 = Uc[ia + 64], u3 = Uc[ia + 96];
+      double d0 = dst[t0], d1 = dst[t1], d2 = dst[t2], d3 = dst[t3];
+      dst[t0] = d0 + u0;
+      dst[t1] = d1 + u1;
+      dst[t2] = d2 + u2;
+      dst[t3] = d3 + u3;
     }
+    for (; ia < rc; ia += 32) dst[rel[ia]] += Uc[ia];
     __syncwarp();
   }
 }

@@ -58,8 +58,9 @@ __global__ void __launch_bounds__(256) k_fsolve_diag(const int32_t* __restrict__
     const int wk = min(64, w - c0);
     for (int idx = tid; idx < wk * wk; idx += blockDim.x) {
       const int i = idx % wk, j = idx / wk;
-      if (i >= j) Lb[j * 65 + i] = Ls[(c0 + i) + static_cast<int64_t>(c0 + j) * rows];
+      if (i >= j) cpasync8(&Lb[j * 65 + i], Ls + (c0 + i) + static_cast<int64_t>(c0 + j) * rows);
     }
+    cpasync_wait_all();
     __syncthreads();
     if (warp == 0) {
       double v0[NR], v1[NR];
@@ -247,8 +248,9 @@ __global__ void __launch_bounds__(256) k_bsolve_diag(const int32_t* __restrict__
     }
     for (int idx = tid; idx < wk * wk; idx += blockDim.x) {
       const int i = idx % wk, j = idx / wk;
-      if (i >= j) Lb[j * 65 + i] = Ls[(c0 + i) + static_cast<int64_t>(c0 + j) * rows];
+      if (i >= j) cpasync8(&Lb[j * 65 + i], Ls + (c0 + i) + static_cast<int64_t>(c0 + j) * rows);
     }
+    cpasync_wait_all();
     __syncthreads();
     if (warp == 0) {
       double v0[NR], v1[NR];

@@ -140,9 +140,9 @@ class SpaceTimePosterior:
 
     def kernel_stats(self) -> dict:
         """{kernel class: dict(launches, ms, flops, bytes)} accumulated since set_profile(True)."""
-        arr = (_capi.KernelStat * 64)()
+        arr = (_capi.KernelStat * 4096)()
         n = C.c_int32()
-        _check(_capi.load().gmrf_spacetime_kernel_stats(self._h, C.cast(arr, C.c_void_p), 64,
+        _check(_capi.load().gmrf_spacetime_kernel_stats(self._h, C.cast(arr, C.c_void_p), 4096,
                                                         C.byref(n)))
         return {a.name.decode(): dict(launches=a.launches, ms=a.ms, flops=a.flops, bytes=a.bytes)
                 for a in arr[: n.value]}
