@@ -22,8 +22,11 @@ constexpr int kDiagSmem = 3 * kNB * (kNB + 1) * sizeof(double);
 void set_smem_attrs() {
   static bool done = false;
   if (done) return;
-  cuda_check(cudaFuncSetAttribute(k_potrf_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  kPanelFusedSmem),
+  cuda_check(cudaFuncSetAttribute(k_potrf_trsm<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  panel_smem_bytes<64>()),
+             "smem k_potrf_trsm");
+  cuda_check(cudaFuncSetAttribute(k_potrf_trsm<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  panel_smem_bytes<32>()),
              "smem k_potrf_trsm");
   cuda_check(
       cudaFuncSetAttribute(k_sel_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, kPanelSmem),
@@ -174,6 +177,7 @@ void DeviceFactor::build_factor_plan() {
   std::vector<std::vector<PanelTask>> pan(nlev), po(nlev);
   std::vector<std::vector<GemmTask>> gm(nlev);
   std::vector<double> ea_b(nlev, 0.0), po_f(nlev, 0.0), tr_f(nlev, 0.0), gm_f(nlev, 0.0);
+  std::vector<int> pan_w(nlev, 1);
   double* L = L_.p;
   double* U = U_.p;
   for (int k = 0; k < s.ns; ++k) {
@@ -197,6 +201,7 @@ void DeviceFactor::build_factor_plan() {
       const PanelTask pt{Lk + c0 + static_cast<int64_t>(c0) * rows, rows, wk, nbelow, 0,
                          s.sn_first[k] + c0};
       po[lv].push_back(pt);  // chunk list for the final diagonal write-back
+      pan_w[lv] = std::max(pan_w[lv], wk);
       for (int t = 0; t == 0 || t * kTrsmRows < nbelow; ++t) {
         PanelTask tt = pt;
         tt.tile = t;
@@ -252,7 +257,7 @@ void DeviceFactor::build_factor_plan() {
                 static_cast<int64_t>(pof.size()), static_cast<int64_t>(po[l].size()),
                 static_cast<int64_t>(panf.size()), static_cast<int64_t>(pan[l].size()),
                 static_cast<int64_t>(gmf.size()), static_cast<int64_t>(gm[l].size()),
-                ea_b[l], po_f[l], tr_f[l], gm_f[l]};
+                ea_b[l], po_f[l], tr_f[l], gm_f[l], pan_w[l]};
     pof.insert(pof.end(), po[l].begin(), po[l].end());
     eaf.insert(eaf.end(), ea[l].begin(), ea[l].end());
     panf.insert(panf.end(), pan[l].begin(), pan[l].end());
@@ -425,8 +430,16 @@ int32_t DeviceFactor::factor_panels() {
     }
     if (lv.pann) {
       pf.run(stream_, pf.tag("factor.potrf_trsm", lvl), lv.po_flops + lv.tr_flops, 0.0, [&] {
-        k_potrf_trsm<<<static_cast<unsigned>(lv.pann), 128, kPanelFusedSmem, stream_>>>(
-            pan_.p + lv.pan0, status_.p, diag_.p);
+        const unsigned g = static_cast<unsigned>(lv.pann);
+        const PanelTask* tk = pan_.p + lv.pan0;
+        if (lv.pan_w <= 8)
+          k_potrf_trsm<8><<<g, 128, panel_smem_bytes<8>(), stream_>>>(tk, status_.p, diag_.p);
+        else if (lv.pan_w <= 16)
+          k_potrf_trsm<16><<<g, 128, panel_smem_bytes<16>(), stream_>>>(tk, status_.p, diag_.p);
+        else if (lv.pan_w <= 32)
+          k_potrf_trsm<32><<<g, 128, panel_smem_bytes<32>(), stream_>>>(tk, status_.p, diag_.p);
+        else
+          k_potrf_trsm<64><<<g, 128, panel_smem_bytes<64>(), stream_>>>(tk, status_.p, diag_.p);
       });
       ++launches_numeric_;
     }
