@@ -177,7 +177,6 @@ void DeviceFactor::build_factor_plan() {
   std::vector<std::vector<PanelTask>> pan(nlev), po(nlev);
   std::vector<std::vector<GemmTask>> gm(nlev);
   std::vector<double> ea_b(nlev, 0.0), po_f(nlev, 0.0), tr_f(nlev, 0.0), gm_f(nlev, 0.0);
-  std::vector<int> pan_w(nlev, 1);
   double* L = L_.p;
   double* U = U_.p;
   for (int k = 0; k < s.ns; ++k) {
@@ -201,7 +200,6 @@ void DeviceFactor::build_factor_plan() {
       const PanelTask pt{Lk + c0 + static_cast<int64_t>(c0) * rows, rows, wk, nbelow, 0,
                          s.sn_first[k] + c0};
       po[lv].push_back(pt);  // chunk list for the final diagonal write-back
-      pan_w[lv] = std::max(pan_w[lv], wk);
       for (int t = 0; t == 0 || t * kTrsmRows < nbelow; ++t) {
         PanelTask tt = pt;
         tt.tile = t;
@@ -257,10 +255,19 @@ void DeviceFactor::build_factor_plan() {
                 static_cast<int64_t>(pof.size()), static_cast<int64_t>(po[l].size()),
                 static_cast<int64_t>(panf.size()), static_cast<int64_t>(pan[l].size()),
                 static_cast<int64_t>(gmf.size()), static_cast<int64_t>(gm[l].size()),
-                ea_b[l], po_f[l], tr_f[l], gm_f[l], pan_w[l]};
+                ea_b[l], po_f[l], tr_f[l], gm_f[l], {0, 0, 0}, {0, 0, 0}};
     pof.insert(pof.end(), po[l].begin(), po[l].end());
     eaf.insert(eaf.end(), ea[l].begin(), ea[l].end());
-    panf.insert(panf.end(), pan[l].begin(), pan[l].end());
+    // panel tasks grouped by width bucket (16 / 32 / 64) so each sub-launch
+    // reserves only the shared memory its chunks need
+    for (int bk = 0; bk < 3; ++bk) {
+      flev_[l].pb0[bk] = static_cast<int64_t>(panf.size());
+      for (const PanelTask& pt : pan[l]) {
+        const int b = pt.w <= 16 ? 0 : (pt.w <= 32 ? 1 : 2);
+        if (b == bk) panf.push_back(pt);
+      }
+      flev_[l].pbn[bk] = static_cast<int64_t>(panf.size()) - flev_[l].pb0[bk];
+    }
     gmf.insert(gmf.end(), gm[l].begin(), gm[l].end());
   }
   ea_.upload(eaf, stream_);
@@ -430,18 +437,17 @@ int32_t DeviceFactor::factor_panels() {
     }
     if (lv.pann) {
       pf.run(stream_, pf.tag("factor.potrf_trsm", lvl), lv.po_flops + lv.tr_flops, 0.0, [&] {
-        const unsigned g = static_cast<unsigned>(lv.pann);
-        const PanelTask* tk = pan_.p + lv.pan0;
-        if (lv.pan_w <= 8)
-          k_potrf_trsm<8><<<g, 128, panel_smem_bytes<8>(), stream_>>>(tk, status_.p, diag_.p);
-        else if (lv.pan_w <= 16)
-          k_potrf_trsm<16><<<g, 128, panel_smem_bytes<16>(), stream_>>>(tk, status_.p, diag_.p);
-        else if (lv.pan_w <= 32)
-          k_potrf_trsm<32><<<g, 128, panel_smem_bytes<32>(), stream_>>>(tk, status_.p, diag_.p);
-        else
-          k_potrf_trsm<64><<<g, 128, panel_smem_bytes<64>(), stream_>>>(tk, status_.p, diag_.p);
+        if (lv.pbn[0])
+          k_potrf_trsm<16><<<static_cast<unsigned>(lv.pbn[0]), 128, panel_smem_bytes<16>(),
+                             stream_>>>(pan_.p + lv.pb0[0], status_.p, diag_.p);
+        if (lv.pbn[1])
+          k_potrf_trsm<32><<<static_cast<unsigned>(lv.pbn[1]), 128, panel_smem_bytes<32>(),
+                             stream_>>>(pan_.p + lv.pb0[1], status_.p, diag_.p);
+        if (lv.pbn[2])
+          k_potrf_trsm<64><<<static_cast<unsigned>(lv.pbn[2]), 128, panel_smem_bytes<64>(),
+                             stream_>>>(pan_.p + lv.pb0[2], status_.p, diag_.p);
       });
-      ++launches_numeric_;
+      launches_numeric_ += (lv.pbn[0] > 0) + (lv.pbn[1] > 0) + (lv.pbn[2] > 0);
     }
     if (lv.gmn) {
       pf.run(stream_, pf.tag("factor.gemm_dmma", lvl), lv.gm_flops, 0.0, [&] {

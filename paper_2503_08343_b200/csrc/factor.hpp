@@ -114,7 +114,7 @@ class DeviceFactor {
   struct FLevel {
     int64_t ea0, ean, po0, pon, pan0, pann, gm0, gmn;
     double ea_bytes, po_flops, tr_flops, gm_flops;  // algorithmic work per launch
-    int pan_w;                                      // widest chunk of the level
+    int64_t pb0[3], pbn[3];  // panel tasks split by width bucket 16 / 32 / 64
   };
   std::vector<FLevel> flev_;
   DevBuf<ColTask> ea_;
