@@ -8,6 +8,7 @@
 #include "kernels.cu"  // single translation unit for all device code
 #include "panel.cuh"
 #include "solve.cuh"
+#include "splitk.cuh"
 
 namespace gmrf {
 
@@ -79,6 +80,7 @@ DeviceFactor::DeviceFactor(std::shared_ptr<const Symbolic> sym, cudaStream_t str
   qmap_.upload(s.qmap, stream_);
   status_.alloc(1);
   diag_.alloc(std::max(s.n, 1));
+  rdiag_.alloc(std::max(s.n, 1));
   L_.alloc(std::max<int64_t>(s.lptr[s.ns], 1));
   U_.alloc(std::max<int64_t>(s.uptr[s.ns], 1));
   q_.alloc(std::max<size_t>(s.qri.size(), 1));
@@ -249,13 +251,27 @@ void DeviceFactor::build_factor_plan() {
   std::vector<ColTask> eaf;
   std::vector<PanelTask> panf, pof;
   std::vector<GemmTask> gmf;
+  std::vector<ReduceTask> rdf;
+  int64_t maxp = 1;
+  for (int l = 0; l < nlev; ++l) maxp = std::max(maxp, split_k_parts(gm[l]));
+  parts_.alloc(maxp * kTile * kTile);  // one level's split-K partial tiles at a time
   flev_.assign(nlev, {});
   for (int l = 0; l < nlev; ++l) {
     flev_[l] = {static_cast<int64_t>(eaf.size()), static_cast<int64_t>(ea[l].size()),
                 static_cast<int64_t>(pof.size()), static_cast<int64_t>(po[l].size()),
                 static_cast<int64_t>(panf.size()), static_cast<int64_t>(pan[l].size()),
-                static_cast<int64_t>(gmf.size()), static_cast<int64_t>(gm[l].size()),
-                ea_b[l], po_f[l], tr_f[l], gm_f[l], {0, 0, 0}, {0, 0, 0}};
+                0, 0, ea_b[l], po_f[l], tr_f[l], gm_f[l], {0, 0, 0}, {0, 0, 0}, 0, 0};
+    {
+      std::vector<GemmTask> gs;
+      std::vector<ReduceTask> rs;
+      split_k_level(gm[l], gs, rs, parts_.p);
+      flev_[l].gm0 = static_cast<int64_t>(gmf.size());
+      flev_[l].gmn = static_cast<int64_t>(gs.size());
+      gmf.insert(gmf.end(), gs.begin(), gs.end());
+      flev_[l].rd0 = static_cast<int64_t>(rdf.size());
+      flev_[l].rdn = static_cast<int64_t>(rs.size());
+      rdf.insert(rdf.end(), rs.begin(), rs.end());
+    }
     pof.insert(pof.end(), po[l].begin(), po[l].end());
     eaf.insert(eaf.end(), ea[l].begin(), ea[l].end());
     // panel tasks grouped by width bucket (16 / 32 / 64) so each sub-launch
@@ -268,12 +284,12 @@ void DeviceFactor::build_factor_plan() {
       }
       flev_[l].pbn[bk] = static_cast<int64_t>(panf.size()) - flev_[l].pb0[bk];
     }
-    gmf.insert(gmf.end(), gm[l].begin(), gm[l].end());
   }
   ea_.upload(eaf, stream_);
   pan_.upload(panf, stream_);
   po_.upload(pof, stream_);
   gemm_.upload(gmf, stream_);
+  red_.upload(rdf, stream_);
 }
 
 void DeviceFactor::build_selinv_plan() {
@@ -363,18 +379,35 @@ void DeviceFactor::build_selinv_plan() {
   std::vector<ColTask> gaf;
   std::vector<GemmTask> gmf;
   std::vector<SelChunk> trf, dgf;
+  std::vector<ReduceTask> rdf;
+  int64_t maxp = 1;
+  for (int l = 0; l < nlev; ++l)
+    maxp = std::max(maxp, std::max(split_k_parts(yg[l]), split_k_parts(zg[l])));
+  sparts_.alloc(maxp * kTile * kTile);
   slev_.assign(nlev, {});
   for (int l = 0; l < nlev; ++l) {
     SLevel& e = slev_[l];
     e.ga0 = gaf.size();
     e.gan = ga[l].size();
     gaf.insert(gaf.end(), ga[l].begin(), ga[l].end());
+    std::vector<GemmTask> gs;
+    std::vector<ReduceTask> rs;
+    split_k_level(yg[l], gs, rs, sparts_.p);
     e.y0 = gmf.size();
-    e.yn = yg[l].size();
-    gmf.insert(gmf.end(), yg[l].begin(), yg[l].end());
+    e.yn = gs.size();
+    gmf.insert(gmf.end(), gs.begin(), gs.end());
+    e.yr0 = rdf.size();
+    e.yrn = rs.size();
+    rdf.insert(rdf.end(), rs.begin(), rs.end());
+    gs.clear();
+    rs.clear();
+    split_k_level(zg[l], gs, rs, sparts_.p);
     e.z0 = gmf.size();
-    e.zn = zg[l].size();
-    gmf.insert(gmf.end(), zg[l].begin(), zg[l].end());
+    e.zn = gs.size();
+    gmf.insert(gmf.end(), gs.begin(), gs.end());
+    e.zr0 = rdf.size();
+    e.zrn = rs.size();
+    rdf.insert(rdf.end(), rs.begin(), rs.end());
     e.t0 = trf.size();
     e.tn = tr[l].size();
     trf.insert(trf.end(), tr[l].begin(), tr[l].end());
@@ -389,6 +422,7 @@ void DeviceFactor::build_selinv_plan() {
   }
   sga_.upload(gaf, stream_);
   sgemm_.upload(gmf, stream_);
+  sred_.upload(rdf, stream_);
   strsm_.upload(trf, stream_);
   sdiag_.upload(dgf, stream_);
   selinv_plan_ = true;
@@ -452,13 +486,17 @@ int32_t DeviceFactor::factor_panels() {
     if (lv.gmn) {
       pf.run(stream_, pf.tag("factor.gemm_dmma", lvl), lv.gm_flops, 0.0, [&] {
         k_gemm_tiles<<<static_cast<unsigned>(lv.gmn), 128, 0, stream_>>>(gemm_.p + lv.gm0);
+        if (lv.rdn)
+          k_reduce_parts<<<static_cast<unsigned>(lv.rdn), 256, 0, stream_>>>(red_.p + lv.rd0,
+                                                                             parts_.p);
       });
-      ++launches_numeric_;
+      launches_numeric_ += 1 + (lv.rdn > 0);
     }
   }
   if (po_.n) {
     pf.run(stream_, "factor.diag_writeback", 0.0, 16.0 * s.n * kNB / 2.0, [&] {
-      k_diag_writeback<<<static_cast<unsigned>(po_.n), 128, 0, stream_>>>(po_.p, diag_.p);
+      k_diag_writeback<<<static_cast<unsigned>(po_.n), 128, 0, stream_>>>(po_.p, diag_.p,
+                                                                         rdiag_.p);
     });
     ++launches_numeric_;
   }
@@ -484,22 +522,22 @@ void DeviceFactor::ensure_solve_ws(int nrhs) {
 
 namespace {
 template <int NR>
-void launch_solve_levels(const DeviceFactor* self, bool fwd, bool bwd, int nlev,
+void launch_solve_levels(const double* rdiag, bool fwd, bool bwd, int nlev,
                          const std::vector<int64_t>& lvl_ptr, const int32_t* lvl_sn,
                          const std::vector<int64_t>& tile_ptr, const SolveTile* tiles, SymDev sd,
                          const double* L, double* y, int nr, double* Uv, const int64_t* uvptr,
                          double* P, const int64_t* pptr, int maxw, cudaStream_t st,
                          KernelProfiler& pf, const std::vector<double>& lvl_bytes,
                          int64_t& launches) {
-  (void)self;
   const int smem_diag = (maxw * NR + 64 * 65) * static_cast<int>(sizeof(double));
   const int smem_off = maxw * NR * static_cast<int>(sizeof(double));
   if (fwd)
     for (int l = 0; l < nlev; ++l) {
       const int cnt = static_cast<int>(lvl_ptr[l + 1] - lvl_ptr[l]);
       const int nt = static_cast<int>(tile_ptr[l + 1] - tile_ptr[l]);
-      pf.run(st, "solve.forward", 0.0, lvl_bytes[l], [&] {
-        k_fsolve_diag<NR><<<cnt, 256, smem_diag, st>>>(lvl_sn + lvl_ptr[l], sd, L, y, nr, Uv, uvptr);
+      pf.run(st, pf.tag("solve.forward", l), 0.0, lvl_bytes[l], [&] {
+        k_fsolve_diag<NR><<<cnt, 256, smem_diag, st>>>(lvl_sn + lvl_ptr[l], sd, L, y, nr, Uv, uvptr,
+                                                       rdiag);
         if (nt)
           k_fsolve_off<NR><<<nt, kSolveRows, smem_off, st>>>(tiles + tile_ptr[l], sd, L, y, nr, Uv,
                                                              uvptr);
@@ -510,10 +548,11 @@ void launch_solve_levels(const DeviceFactor* self, bool fwd, bool bwd, int nlev,
     for (int l = nlev - 1; l >= 0; --l) {
       const int cnt = static_cast<int>(lvl_ptr[l + 1] - lvl_ptr[l]);
       const int nt = static_cast<int>(tile_ptr[l + 1] - tile_ptr[l]);
-      pf.run(st, "solve.backward", 0.0, lvl_bytes[l], [&] {
+      pf.run(st, pf.tag("solve.backward", l), 0.0, lvl_bytes[l], [&] {
         if (nt)
           k_bsolve_off<NR><<<nt, 256, 0, st>>>(tiles + tile_ptr[l], sd, L, y, nr, P, pptr);
-        k_bsolve_diag<NR><<<cnt, 256, smem_diag, st>>>(lvl_sn + lvl_ptr[l], sd, L, y, nr, P, pptr);
+        k_bsolve_diag<NR><<<cnt, 256, smem_diag, st>>>(lvl_sn + lvl_ptr[l], sd, L, y, nr, P, pptr,
+                                                       rdiag);
       });
       launches += 1 + (nt > 0);
     }
@@ -558,15 +597,15 @@ void DeviceFactor::solve(int mode, int nrhs, const double* b, double* x, bool on
     }
     const bool fwd = mode == 0 || mode == 2, bwd = mode == 1 || mode == 2;
     if (nrb == 1)
-      launch_solve_levels<1>(this, fwd, bwd, s.n_levels, lvl_ptr_, lvl_sn_.p, tile_ptr_, tiles_.p,
+      launch_solve_levels<1>(rdiag_.p, fwd, bwd, s.n_levels, lvl_ptr_, lvl_sn_.p, tile_ptr_, tiles_.p,
                              sd, L_.p, y, nr, Uv_.p, uvptr_.p, P_.p, pptr_.p, maxw_, stream_, *prof_,
                              lvl_bytes_, launches_solve_);
     else if (nrb == 4)
-      launch_solve_levels<4>(this, fwd, bwd, s.n_levels, lvl_ptr_, lvl_sn_.p, tile_ptr_, tiles_.p,
+      launch_solve_levels<4>(rdiag_.p, fwd, bwd, s.n_levels, lvl_ptr_, lvl_sn_.p, tile_ptr_, tiles_.p,
                              sd, L_.p, y, nr, Uv_.p, uvptr_.p, P_.p, pptr_.p, maxw_, stream_, *prof_,
                              lvl_bytes_, launches_solve_);
     else
-      launch_solve_levels<16>(this, fwd, bwd, s.n_levels, lvl_ptr_, lvl_sn_.p, tile_ptr_, tiles_.p,
+      launch_solve_levels<16>(rdiag_.p, fwd, bwd, s.n_levels, lvl_ptr_, lvl_sn_.p, tile_ptr_, tiles_.p,
                               sd, L_.p, y, nr, Uv_.p, uvptr_.p, P_.p, pptr_.p, maxw_, stream_,
                               *prof_, lvl_bytes_, launches_solve_);
     if (mode == 2) {
@@ -607,8 +646,11 @@ void DeviceFactor::selinv(double* diag_out, bool on_device) {
     if (e.yn) {
       pf.run(stream_, "selinv.gemm_dmma", e.y_flops, 0.0, [&] {
         k_gemm_tiles<<<static_cast<unsigned>(e.yn), 128, 0, stream_>>>(sgemm_.p + e.y0);
+        if (e.yrn)
+          k_reduce_parts<<<static_cast<unsigned>(e.yrn), 256, 0, stream_>>>(sred_.p + e.yr0,
+                                                                            sparts_.p);
       });
-      ++launches_selinv_;
+      launches_selinv_ += 1 + (e.yrn > 0);
     }
     if (e.tn) {
       pf.run(stream_, "selinv.trsm", e.t_flops, 0.0, [&] {
@@ -619,8 +661,11 @@ void DeviceFactor::selinv(double* diag_out, bool on_device) {
     if (e.zn) {
       pf.run(stream_, "selinv.gemm_dmma", e.z_flops, 0.0, [&] {
         k_gemm_tiles<<<static_cast<unsigned>(e.zn), 128, 0, stream_>>>(sgemm_.p + e.z0);
+        if (e.zrn)
+          k_reduce_parts<<<static_cast<unsigned>(e.zrn), 256, 0, stream_>>>(sred_.p + e.zr0,
+                                                                            sparts_.p);
       });
-      ++launches_selinv_;
+      launches_selinv_ += 1 + (e.zrn > 0);
     }
     if (e.dn) {
       pf.run(stream_, "selinv.diag", e.d_flops, 0.0, [&] {

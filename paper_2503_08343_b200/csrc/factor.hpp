@@ -104,7 +104,7 @@ class DeviceFactor {
 
   DevBuf<int32_t> first_, rows_, relmap_, chptr_, chlist_, perm_, col2sn_, snparent_, status_;
   DevBuf<int64_t> rptr_, lptr_, uptr_, qmap_, pptr_, uvptr_;
-  DevBuf<double> L_, U_, Sig_, q_, P_, Uv_, v1_, v2_, diag_;
+  DevBuf<double> L_, U_, Sig_, q_, P_, Uv_, v1_, v2_, diag_, rdiag_;
   DevBuf<SolveTile> tiles_;
   std::vector<int64_t> tile_ptr_;
   int maxw_ = 1;
@@ -115,6 +115,7 @@ class DeviceFactor {
     int64_t ea0, ean, po0, pon, pan0, pann, gm0, gmn;
     double ea_bytes, po_flops, tr_flops, gm_flops;  // algorithmic work per launch
     int64_t pb0[3], pbn[3];  // panel tasks split by width bucket 16 / 32 / 64
+    int64_t rd0, rdn;        // split-K reductions of the level's GEMM tiles
   };
   std::vector<FLevel> flev_;
   DevBuf<ColTask> ea_;
@@ -124,7 +125,10 @@ class DeviceFactor {
   struct SLevel {
     int64_t ga0, gan, y0, yn, t0, tn, z0, zn, d0, dn;
     double ga_bytes, y_flops, t_flops, z_flops, d_flops;
+    int64_t yr0, yrn, zr0, zrn;  // split-K reductions of the Y and Z tiles
   };
+  DevBuf<ReduceTask> red_, sred_;
+  DevBuf<double> parts_, sparts_;  // split-K partial tiles
   std::vector<double> lvl_bytes_;  // solve: L panel + row-index bytes per tree level
   KernelProfiler own_prof_;
   KernelProfiler* prof_ = &own_prof_;

@@ -24,6 +24,15 @@ struct GemmTask {
   double alpha, beta;
 };
 
+// Split-K reduction of one output tile (splitk.cuh).
+struct ReduceTask {
+  double* c;
+  int32_t ldc, m, n;
+  int32_t nparts;
+  int64_t part0;  // first partial tile (index into the scratch, kTile*kTile each)
+  double alpha, beta;
+};
+
 // Diagonal-block Cholesky + TRSM of the rows below it, for one chunk.
 struct PanelTask {
   double* d;          // top-left of the chunk's diagonal block

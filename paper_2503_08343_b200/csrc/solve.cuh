@@ -20,7 +20,8 @@ __global__ void __launch_bounds__(256) k_fsolve_diag(const int32_t* __restrict__
                                                      const double* __restrict__ L,
                                                      double* __restrict__ y, int nrhs,
                                                      double* __restrict__ Uv,
-                                                     const int64_t* __restrict__ uvptr) {
+                                                     const int64_t* __restrict__ uvptr,
+                                                     const double* __restrict__ rdiag) {
   extern __shared__ double sm[];
   const int s = sns[blockIdx.x];
   const int f0 = sd.sn_first[s];
@@ -70,13 +71,13 @@ __global__ void __launch_bounds__(256) k_fsolve_diag(const int32_t* __restrict__
         v1[rr] = (rr < nrhs && lane + 32 < wk) ? fJ[rr * w + c0 + 32 + lane] : 0.0;
       }
       for (int j = 0; j < wk; ++j) {
-        const double ljj = Lb[j * 65 + j];
+        const double rjj = rdiag[f0 + c0 + j];  // 1/L_jj, from the factorization
         const double l0 = (lane > j && lane < wk) ? Lb[j * 65 + lane] : 0.0;
         const double l1 = (lane + 32 > j && lane + 32 < wk) ? Lb[j * 65 + lane + 32] : 0.0;
 #pragma unroll
         for (int rr = 0; rr < NR; ++rr) {
           const double src = j < 32 ? v0[rr] : v1[rr];
-          const double xj = __shfl_sync(0xffffffffu, src, j & 31) / ljj;
+          const double xj = __shfl_sync(0xffffffffu, src, j & 31) * rjj;
           if (lane == (j & 31)) {
             if (j < 32) v0[rr] = xj; else v1[rr] = xj;
           }
@@ -203,7 +204,8 @@ __global__ void __launch_bounds__(256) k_bsolve_diag(const int32_t* __restrict__
                                                      const double* __restrict__ L,
                                                      double* __restrict__ x, int nrhs,
                                                      const double* __restrict__ P,
-                                                     const int64_t* __restrict__ pptr) {
+                                                     const int64_t* __restrict__ pptr,
+                                                     const double* __restrict__ rdiag) {
   extern __shared__ double sm[];
   const int s = sns[blockIdx.x];
   const int f0 = sd.sn_first[s];
@@ -260,14 +262,14 @@ __global__ void __launch_bounds__(256) k_bsolve_diag(const int32_t* __restrict__
         v1[rr] = (rr < nrhs && lane + 32 < wk) ? bJ[rr * w + c0 + 32 + lane] : 0.0;
       }
       for (int j = wk - 1; j >= 0; --j) {
-        const double ljj = Lb[j * 65 + j];
+        const double rjj = rdiag[f0 + c0 + j];  // 1/L_jj, from the factorization
         // (Lᵀ)_{i,j} = L_{j,i}, stored at Lb[i*65 + j] for i < j
         const double l0 = (lane < j) ? Lb[lane * 65 + j] : 0.0;
         const double l1 = (lane + 32 < j) ? Lb[(lane + 32) * 65 + j] : 0.0;
 #pragma unroll
         for (int rr = 0; rr < NR; ++rr) {
           const double src = j < 32 ? v0[rr] : v1[rr];
-          const double xj = __shfl_sync(0xffffffffu, src, j & 31) / ljj;
+          const double xj = __shfl_sync(0xffffffffu, src, j & 31) * rjj;
           if (lane == (j & 31)) {
             if (j < 32) v0[rr] = xj; else v1[rr] = xj;
           }
