@@ -23,6 +23,7 @@ __global__ void __launch_bounds__(256) k_fsolve_diag(const int32_t* __restrict__
                                                      const int64_t* __restrict__ uvptr,
                                                      const double* __restrict__ rdiag) {
   extern __shared__ double sm[];
+  __shared__ double rdl[64];  // 1/L_jj of the current chunk
   const int s = sns[blockIdx.x];
   const int f0 = sd.sn_first[s];
   const int w = sd.sn_first[s + 1] - f0;
@@ -61,6 +62,7 @@ __global__ void __launch_bounds__(256) k_fsolve_diag(const int32_t* __restrict__
       const int i = idx % wk, j = idx / wk;
       if (i >= j) cpasync8(&Lb[j * 65 + i], Ls + (c0 + i) + static_cast<int64_t>(c0 + j) * rows);
     }
+    if (tid < wk) cpasync8(&rdl[tid], rdiag + f0 + c0 + tid);
     cpasync_wait_all();
     __syncthreads();
     if (warp == 0) {
@@ -71,7 +73,7 @@ __global__ void __launch_bounds__(256) k_fsolve_diag(const int32_t* __restrict__
         v1[rr] = (rr < nrhs && lane + 32 < wk) ? fJ[rr * w + c0 + 32 + lane] : 0.0;
       }
       for (int j = 0; j < wk; ++j) {
-        const double rjj = rdiag[f0 + c0 + j];  // 1/L_jj, from the factorization
+        const double rjj = rdl[j];  // 1/L_jj, from the factorization
         const double l0 = (lane > j && lane < wk) ? Lb[j * 65 + lane] : 0.0;
         const double l1 = (lane + 32 > j && lane + 32 < wk) ? Lb[j * 65 + lane + 32] : 0.0;
 #pragma unroll
@@ -207,6 +209,7 @@ __global__ void __launch_bounds__(256) k_bsolve_diag(const int32_t* __restrict__
                                                      const int64_t* __restrict__ pptr,
                                                      const double* __restrict__ rdiag) {
   extern __shared__ double sm[];
+  __shared__ double rdl[64];  // 1/L_jj of the current chunk
   const int s = sns[blockIdx.x];
   const int f0 = sd.sn_first[s];
   const int w = sd.sn_first[s + 1] - f0;
@@ -252,6 +255,7 @@ __global__ void __launch_bounds__(256) k_bsolve_diag(const int32_t* __restrict__
       const int i = idx % wk, j = idx / wk;
       if (i >= j) cpasync8(&Lb[j * 65 + i], Ls + (c0 + i) + static_cast<int64_t>(c0 + j) * rows);
     }
+    if (tid < wk) cpasync8(&rdl[tid], rdiag + f0 + c0 + tid);
     cpasync_wait_all();
     __syncthreads();
     if (warp == 0) {
@@ -262,7 +266,7 @@ __global__ void __launch_bounds__(256) k_bsolve_diag(const int32_t* __restrict__
         v1[rr] = (rr < nrhs && lane + 32 < wk) ? bJ[rr * w + c0 + 32 + lane] : 0.0;
       }
       for (int j = wk - 1; j >= 0; --j) {
-        const double rjj = rdiag[f0 + c0 + j];  // 1/L_jj, from the factorization
+        const double rjj = rdl[j];  // 1/L_jj, from the factorization
         // (Lᵀ)_{i,j} = L_{j,i}, stored at Lb[i*65 + j] for i < j
         const double l0 = (lane < j) ? Lb[lane * 65 + j] : 0.0;
         const double l1 = (lane + 32 < j) ? Lb[(lane + 32) * 65 + j] : 0.0;
