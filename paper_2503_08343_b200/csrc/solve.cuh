@@ -100,8 +100,19 @@ __global__ void __launch_bounds__(256) k_fsolve_diag(const int32_t* __restrict__
       double acc[NR];
 #pragma unroll
       for (int rr = 0; rr < NR; ++rr) acc[rr] = rr < nrhs ? fJ[rr * w + i] : 0.0;
-      for (int j = 0; j < wk; ++j) {
-        const double l = Ls[i + static_cast<int64_t>(c0 + j) * rows];
+      const double* li = Ls + i + static_cast<int64_t>(c0) * rows;
+      int j = 0;
+      for (; j + 8 <= wk; j += 8) {  // 8 independent loads in flight
+        double l[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) l[u] = li[static_cast<int64_t>(j + u) * rows];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+#pragma unroll
+          for (int rr = 0; rr < NR; ++rr) acc[rr] -= l[u] * fJ[rr * w + c0 + j + u];
+      }
+      for (; j < wk; ++j) {
+        const double l = li[static_cast<int64_t>(j) * rows];
 #pragma unroll
         for (int rr = 0; rr < NR; ++rr) acc[rr] -= l * fJ[rr * w + c0 + j];
       }
@@ -145,7 +156,17 @@ __global__ void __launch_bounds__(kSolveRows) k_fsolve_off(const SolveTile* __re
   double acc[NR];
 #pragma unroll
   for (int rr = 0; rr < NR; ++rr) acc[rr] = rr < nrhs ? u[i + rr * r] : 0.0;
-  for (int j = 0; j < w; ++j) {
+  int j = 0;
+  for (; j + 8 <= w; j += 8) {  // 8 independent loads in flight
+    double l[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) l[u] = Lr[static_cast<int64_t>(j + u) * rows];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+#pragma unroll
+      for (int rr = 0; rr < NR; ++rr) acc[rr] -= l[u] * yJ[rr * w + j + u];
+  }
+  for (; j < w; ++j) {
     const double l = Lr[static_cast<int64_t>(j) * rows];
 #pragma unroll
     for (int rr = 0; rr < NR; ++rr) acc[rr] -= l * yJ[rr * w + j];
@@ -185,6 +206,7 @@ __global__ void __launch_bounds__(256) k_bsolve_off(const SolveTile* __restrict_
     double acc[NR];
 #pragma unroll
     for (int rr = 0; rr < NR; ++rr) acc[rr] = 0.0;
+#pragma unroll 4
     for (int ii = lane; ii < nt; ii += 32) {
       const double l = col[ii];
 #pragma unroll
@@ -238,7 +260,15 @@ __global__ void __launch_bounds__(256) k_bsolve_diag(const int32_t* __restrict__
       double acc[NR];
 #pragma unroll
       for (int rr = 0; rr < NR; ++rr) acc[rr] = 0.0;
-      for (int i = c0 + wk + lane; i < w; i += 32) {
+      int i = c0 + wk + lane;
+      for (; i + 96 < w; i += 128) {  // 4 independent loads in flight per lane
+        const double l0 = col[i], l1 = col[i + 32], l2 = col[i + 64], l3 = col[i + 96];
+#pragma unroll
+        for (int rr = 0; rr < NR; ++rr)
+          acc[rr] += l0 * bJ[rr * w + i] + l1 * bJ[rr * w + i + 32] +
+                     l2 * bJ[rr * w + i + 64] + l3 * bJ[rr * w + i + 96];
+      }
+      for (; i < w; i += 32) {
         const double l = col[i];
 #pragma unroll
         for (int rr = 0; rr < NR; ++rr) acc[rr] += l * bJ[rr * w + i];
