@@ -1,0 +1,189 @@
+// Drop-in replacement for the reference's gmrfpde/core/cholesky.hpp
+// (/root/reference/proj/include/gmrfpde/core/cholesky.hpp), backed by the
+// B200 engine through the C-ABI (include/gmrf_b200.h).
+//
+// Put this directory BEFORE the reference include directory: every reference
+// header that includes "gmrfpde/core/cholesky.hpp" (gmrf.hpp, takahashi.hpp,
+// gauss_newton.hpp, spatiotemporal.hpp, the tests) then factors and solves on
+// the GPU with unchanged source. Same names, signatures, argument meaning and
+// exceptions as the reference (cholesky.hpp:16-229); the carrier types
+// (SparseMatrixCSC, Index, exceptions) and amd_order still come from the
+// reference headers.
+//
+// Differences, all documented in INTEGRATION.md:
+//  * cholesky_factor(q) orders with nested dissection (METIS), not AMD;
+//  * CholeskyFactor::L is materialised on the host eagerly (reference layout,
+//    exact pattern) only when n <= GMRF_HOST_L_MAX (default 200000); larger
+//    factors stay device-resident and L is left empty.
+#pragma once
+
+#include <cmath>
+#include <cstdint>
+#include <cstdlib>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "gmrf_b200.h"
+#include "gmrfpde/core/amd.hpp"
+#include "gmrfpde/core/sparse.hpp"
+#include "gmrfpde/core/types.hpp"
+
+namespace gmrfpde {
+
+namespace b200 {
+
+[[noreturn]] inline void raise(int rc, int32_t bad = -1) {
+  std::string msg = gmrf_last_error();
+  switch (rc) {
+    case GMRF_ERR_NOT_SPD: throw NotPositiveDefiniteError(msg, bad);
+    case GMRF_ERR_DIMENSION: throw DimensionError(msg);
+    case GMRF_ERR_STRUCTURAL: throw StructuralError(msg);
+    case GMRF_ERR_CONTRACT: throw ContractError(msg);
+    default: throw NumericalError(msg);
+  }
+}
+inline void check(int rc) {
+  if (rc != GMRF_OK) raise(rc);
+}
+
+inline std::vector<int64_t> colptr64(const SparseMatrixCSC& q) {
+  return std::vector<int64_t>(q.col_ptr.begin(), q.col_ptr.end());
+}
+
+struct SymbolicHandle {
+  gmrf_symbolic_t* h = nullptr;
+  std::vector<int64_t> cp;
+  std::vector<Index> ri;
+  ~SymbolicHandle() {
+    if (h) gmrf_symbolic_free(h);
+  }
+};
+struct FactorHandle {
+  gmrf_factor_t* h = nullptr;
+  std::shared_ptr<SymbolicHandle> sym;
+  ~FactorHandle() {
+    if (h) gmrf_factor_free(h);
+  }
+};
+
+inline int64_t host_l_max() {
+  const char* e = std::getenv("GMRF_HOST_L_MAX");
+  return e ? std::atoll(e) : 200000;
+}
+
+}  // namespace b200
+
+/// Symbolic phase (cholesky.hpp:16-23): same fields, plus the device handle.
+struct SymbolicFactor {
+  std::vector<Index> perm;      // new -> old
+  std::vector<Index> perm_inv;  // old -> new
+  std::vector<Index> parent;    // elimination tree over permuted indices
+  std::vector<Index> col_ptr;   // column layout of L (including diagonal)
+  Index n = 0;
+  Index nnz_L = 0;
+  std::shared_ptr<b200::SymbolicHandle> handle;
+};
+
+/// symbolic_analyze (cholesky.hpp:68). Bit-exact parent/col_ptr for the same perm.
+inline SymbolicFactor symbolic_analyze(const SparseMatrixCSC& q, const std::vector<Index>& perm) {
+  if (q.nrows != q.ncols) throw DimensionError("symbolic_analyze: matrix not square");
+  auto h = std::make_shared<b200::SymbolicHandle>();
+  h->cp = b200::colptr64(q);
+  h->ri = q.row_idx;
+  const Index n = q.nrows;
+  if (static_cast<Index>(perm.size()) != n)
+    throw DimensionError("symbolic_analyze: permutation length mismatch");
+  b200::check(gmrf_symbolic_analyze(n, h->cp.data(), h->ri.data(), perm.data(), &h->h));
+  SymbolicFactor s;
+  s.n = n;
+  s.perm.resize(n);
+  s.parent.resize(n);
+  std::vector<int64_t> cpl(n + 1);
+  b200::check(gmrf_symbolic_export(h->h, s.perm.data(), s.parent.data(), cpl.data()));
+  s.perm_inv = invert_permutation(s.perm);
+  s.col_ptr.assign(cpl.begin(), cpl.end());
+  s.nnz_L = static_cast<Index>(cpl[n]);
+  s.handle = std::move(h);
+  return s;
+}
+
+/// P Q Pᵀ = L Lᵀ (cholesky.hpp:92-109); the numeric factor lives on the GPU.
+struct CholeskyFactor {
+  SparseMatrixCSC L;            // reference layout, filled when n <= GMRF_HOST_L_MAX
+  std::vector<Index> perm;      // new -> old
+  std::vector<Index> perm_inv;  // old -> new
+  std::shared_ptr<b200::FactorHandle> device;
+
+  Index dim() const { return static_cast<Index>(perm.size()); }
+
+  Vector apply_perm(const Vector& x) const {
+    Vector y(x.size());
+    for (std::size_t i = 0; i < x.size(); ++i) y[i] = x[perm[i]];
+    return y;
+  }
+  Vector apply_perm_inv(const Vector& x) const {
+    Vector y(x.size());
+    for (std::size_t i = 0; i < x.size(); ++i) y[perm[i]] = x[i];
+    return y;
+  }
+};
+
+/// cholesky_refactor (cholesky.hpp:113): numeric factorization on the GPU.
+inline CholeskyFactor cholesky_refactor(const SymbolicFactor& s, const SparseMatrixCSC& q) {
+  const Index n = s.n;
+  if (q.nrows != n || q.ncols != n) throw DimensionError("cholesky_refactor: dimension mismatch");
+  auto fh = std::make_shared<b200::FactorHandle>();
+  fh->sym = s.handle;
+  b200::check(gmrf_factor_create(s.handle->h, &fh->h));
+  int32_t bad = -1;
+  const int rc = gmrf_factor_numeric(fh->h, q.values.data(), &bad);
+  if (rc != GMRF_OK) b200::raise(rc, bad);
+  CholeskyFactor f;
+  f.perm = s.perm;
+  f.perm_inv = s.perm_inv;
+  f.device = fh;
+  f.L.nrows = f.L.ncols = n;
+  if (n <= b200::host_l_max()) {
+    std::vector<int64_t> cp(n + 1);
+    f.L.row_idx.resize(s.nnz_L);
+    f.L.values.resize(s.nnz_L);
+    b200::check(gmrf_factor_l(fh->h, cp.data(), f.L.row_idx.data(), f.L.values.data(), nullptr));
+    f.L.col_ptr.assign(cp.begin(), cp.end());
+  }
+  return f;
+}
+
+/// cholesky_factor(q, perm) (cholesky.hpp:164).
+inline CholeskyFactor cholesky_factor(const SparseMatrixCSC& q, const std::vector<Index>& perm) {
+  return cholesky_refactor(symbolic_analyze(q, perm), q);
+}
+
+/// cholesky_factor(q) (cholesky.hpp:170): nested dissection instead of AMD.
+inline CholeskyFactor cholesky_factor(const SparseMatrixCSC& q) {
+  if (q.nrows != q.ncols) throw DimensionError("symbolic_analyze: matrix not square");
+  std::vector<int64_t> cp = b200::colptr64(q);
+  std::vector<Index> perm(q.nrows);
+  b200::check(gmrf_nd_order(q.nrows, cp.data(), q.row_idx.data(), perm.data()));
+  return cholesky_factor(q, perm);
+}
+
+enum class TriangularMode { kLower, kUpper, kFull };
+
+/// solve_triangular (cholesky.hpp:179): kLower/kUpper in permuted coordinates,
+/// kFull returns Q⁻¹ b in original coordinates.
+inline Vector solve_triangular(const CholeskyFactor& f, const Vector& b, TriangularMode mode) {
+  const Index n = f.dim();
+  if (static_cast<Index>(b.size()) != n)
+    throw DimensionError("solve_triangular: dimension mismatch");
+  Vector x(n);
+  b200::check(gmrf_solve(f.device->h, static_cast<int>(mode), 1, b.data(), x.data()));
+  return x;
+}
+
+/// solve (cholesky.hpp:225).
+inline Vector solve(const CholeskyFactor& f, const Vector& b) {
+  return solve_triangular(f, b, TriangularMode::kFull);
+}
+
+}  // namespace gmrfpde
