@@ -256,6 +256,8 @@ def solve_triangular(f: CholeskyFactor, b, mode: int) -> np.ndarray:
         raise DimensionError("solve_triangular: dimension mismatch")
     if mode not in (0, 1, 2):
         raise ContractError("solve_triangular: unknown mode")
+    if n == 0:
+        return b.copy()
     bb = np.asfortranarray(b.reshape(n, -1))
     x = np.empty_like(bb, order="F")
     _check(_capi.load().gmrf_solve(f._h, int(mode), bb.shape[1], ptr(bb, f64p), ptr(x, f64p)))

@@ -1,0 +1,121 @@
+"""Edge cases through the C-ABI (GPU): empty and 1×1 systems, decoupled
+(diagonal / disconnected) patterns, many right-hand sides (> one 16-wide
+pass), lower/upper modes against the C restatement, refactor with new values,
+non-SPD inside a larger matrix, and wide supernodes (> several 64-chunks)."""
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+import paper_2503_08343_b200 as g
+
+pytestmark = pytest.mark.gpu
+
+
+def csc(m):
+    m = sp.csc_matrix(m)
+    m.sort_indices()
+    return g.SparseMatrixCSC.from_scipy(m)
+
+
+def rel(a, b):
+    return np.linalg.norm(np.asarray(a) - b) / max(np.linalg.norm(b), 1e-300)
+
+
+def test_empty_and_one_by_one():
+    q0 = g.SparseMatrixCSC.from_arrays(0, 0, [0], [], [])
+    f0 = g.cholesky_factor(q0)
+    assert g.solve(f0, np.zeros(0)).shape == (0,)
+    assert g.takahashi_diagonal(f0).shape == (0,)
+    q1 = g.SparseMatrixCSC.from_arrays(1, 1, [0, 1], [0], [9.0])
+    f1 = g.cholesky_factor(q1)
+    assert f1.L.values[0] == pytest.approx(3.0)
+    assert g.solve(f1, [18.0])[0] == pytest.approx(2.0)
+    assert g.takahashi_diagonal(f1)[0] == pytest.approx(1.0 / 9.0)
+
+
+def test_decoupled_patterns():
+    rng = np.random.default_rng(4)
+    d = rng.uniform(1, 5, 500)
+    f = g.cholesky_factor(csc(sp.diags(d)))
+    np.testing.assert_allclose(g.takahashi_diagonal(f), 1.0 / d, rtol=1e-14)
+    # two disconnected grid components plus isolated nodes
+    a = sp.diags([-1.0, 4.0, -1.0], [-1, 0, 1], (40, 40))
+    m = sp.block_diag([a, sp.eye(7) * 2.0, a * 2.0]).tocsc()
+    q = csc(m)
+    f = g.cholesky_factor(q)
+    b = rng.standard_normal(m.shape[0])
+    assert rel(g.solve(f, b), np.linalg.solve(m.toarray(), b)) <= 1e-13
+    np.testing.assert_allclose(g.takahashi_diagonal(f), np.diag(np.linalg.inv(m.toarray())),
+                               rtol=1e-12)
+
+
+def test_many_rhs_and_modes_vs_port(port):
+    gx = 70
+    a = sp.diags([-1.0, 4.2, -1.0], [-1, 0, 1], (gx, gx))
+    m = (sp.kron(sp.eye(gx), a) + sp.kron(sp.diags([-1.0, -1.0], [-1, 1], (gx, gx)), sp.eye(gx)))
+    q = csc(m)
+    n = q.nrows
+    f = g.cholesky_factor(q)
+    lcp, lri, lv, bad = port.cholesky(n, q.col_ptr, q.row_idx, q.values, f.perm)
+    rng = np.random.default_rng(9)
+    b = rng.standard_normal((n, 37))  # 16 + 16 + 5 right-hand sides
+    for mode in (0, 1, 2):
+        x = g.solve_triangular(f, b, mode)
+        xo = port.solve(n, lcp, lri, lv, f.perm, mode, b)
+        assert rel(x, xo) <= 1e-12, mode
+
+
+def test_refactor_new_values_and_failure():
+    gx = 30
+    a = sp.diags([-1.0, 4.0, -1.0], [-1, 0, 1], (gx, gx))
+    m = (sp.kron(sp.eye(gx), a) + sp.kron(sp.diags([-1.0, -1.0], [-1, 1], (gx, gx)), sp.eye(gx)))
+    q = csc(m)
+    sym = g.symbolic_analyze(q)
+    f = g.CholeskyFactor(sym)
+    rng = np.random.default_rng(2)
+    for shift in (0.5, 3.0):
+        v = q.values.copy()
+        dmask = np.zeros_like(v, bool)
+        for j in range(q.ncols):
+            for p in range(q.col_ptr[j], q.col_ptr[j + 1]):
+                dmask[p] = q.row_idx[p] == j
+        v[dmask] += shift
+        f.refactor(v)
+        mm = sp.csc_matrix((v, q.row_idx, q.col_ptr), shape=m.shape)
+        b = rng.standard_normal(q.nrows)
+        assert rel(g.solve(f, b), np.linalg.solve(mm.toarray(), b)) <= 1e-12
+    # make one diagonal entry strongly negative: reported in original numbering
+    v = q.values.copy()
+    k = 417
+    p = q.col_ptr[k] + np.searchsorted(q.row_idx[q.col_ptr[k]:q.col_ptr[k + 1]], k)
+    v[p] = -50.0
+    with pytest.raises(g.NotPositiveDefiniteError) as e:
+        f.refactor(v)
+    assert 0 <= e.value.index() < q.nrows
+    # the factor recovers on the next valid refactor
+    f.refactor(q.values)
+    b = np.ones(q.nrows)
+    assert rel(g.solve(f, b), np.linalg.solve(m.toarray(), b)) <= 1e-12
+
+
+def test_wide_supernodes_dense_block(port):
+    # a dense 300x300 SPD block coupled to a chain: one supernode of ~5 chunks
+    rng = np.random.default_rng(1)
+    a = rng.standard_normal((300, 300))
+    dense = a @ a.T + 300 * np.eye(300)
+    chain = sp.diags([-1.0, 3.0, -1.0], [-1, 0, 1], (200, 200)).toarray()
+    m = np.zeros((500, 500))
+    m[:300, :300] = dense
+    m[300:, 300:] = chain
+    m[299, 300] = m[300, 299] = -0.5
+    q = csc(m)
+    f = g.cholesky_factor(q)
+    info = f.sym.info
+    assert info.max_front >= 300
+    n = q.nrows
+    lcp, lri, lv, bad = port.cholesky(n, q.col_ptr, q.row_idx, q.values, f.perm)
+    assert rel(f.L.values, lv) <= 1e-12
+    inv = np.linalg.inv(m)
+    np.testing.assert_allclose(g.takahashi_diagonal(f), np.diag(inv), rtol=1e-10)
+    s = g.takahashi_selected_inverse(f).to_scipy().tocoo()
+    assert np.abs(s.data - inv[s.row, s.col]).max() <= 1e-12
