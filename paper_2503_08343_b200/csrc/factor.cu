@@ -7,6 +7,7 @@
 
 #include "kernels.cu"  // single translation unit for all device code
 #include "panel.cuh"
+#include "small_front.cuh"
 #include "solve.cuh"
 #include "splitk.cuh"
 
@@ -29,6 +30,9 @@ void set_smem_attrs() {
   cuda_check(cudaFuncSetAttribute(k_potrf_trsm<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   panel_smem_bytes<32>()),
              "smem k_potrf_trsm");
+  cuda_check(cudaFuncSetAttribute(k_small_front<96>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  small_front_smem_bytes<96>()),
+             "smem k_small_front");
   cuda_check(
       cudaFuncSetAttribute(k_sel_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, kPanelSmem),
       "smem k_sel_trsm");
@@ -156,8 +160,10 @@ int64_t DeviceFactor::device_bytes() const {
 }
 
 // Chunk levels: chunk k of supernode s sits at lvl0(s)+k where lvl0(s) is one
-// above the last chunk of its deepest child.
-static void chunk_levels(const Symbolic& s, std::vector<int>& lvl0, int& nlev) {
+// above the last chunk of its deepest child. Small fronts (rows ≤ small_rows)
+// are factored whole by one CTA and occupy a single level.
+static void chunk_levels(const Symbolic& s, std::vector<int>& lvl0, int& nlev,
+                         int small_rows = 0) {
   lvl0.assign(s.ns, 0);
   std::vector<int> last(s.ns, 0);
   nlev = 0;
@@ -165,7 +171,7 @@ static void chunk_levels(const Symbolic& s, std::vector<int>& lvl0, int& nlev) {
     int l = 0;
     for (int q = s.ch_ptr[k]; q < s.ch_ptr[k + 1]; ++q) l = std::max(l, last[s.ch_list[q]] + 1);
     lvl0[k] = l;
-    last[k] = l + nchunks(s.w(k)) - 1;
+    last[k] = s.rows(k) <= small_rows ? l : l + nchunks(s.w(k)) - 1;
     nlev = std::max(nlev, last[k] + 1);
   }
 }
@@ -174,15 +180,24 @@ void DeviceFactor::build_factor_plan() {
   const Symbolic& s = *sym_;
   std::vector<int> lvl0;
   int nlev = 0;
-  chunk_levels(s, lvl0, nlev);
+  chunk_levels(s, lvl0, nlev, kSmallRows);
   std::vector<std::vector<ColTask>> ea(nlev);
   std::vector<std::vector<PanelTask>> pan(nlev), po(nlev);
   std::vector<std::vector<GemmTask>> gm(nlev);
-  std::vector<double> ea_b(nlev, 0.0), po_f(nlev, 0.0), tr_f(nlev, 0.0), gm_f(nlev, 0.0);
+  std::vector<std::vector<int32_t>> sm[3];
+  for (auto& v : sm) v.resize(nlev);
+  std::vector<double> ea_b(nlev, 0.0), po_f(nlev, 0.0), tr_f(nlev, 0.0), gm_f(nlev, 0.0),
+      sm_f(nlev, 0.0);
   double* L = L_.p;
   double* U = U_.p;
   for (int k = 0; k < s.ns; ++k) {
     const int w = s.w(k), rows = s.rows(k), r = rows - w;
+    if (rows <= kSmallRows) {  // fused small-front kernel, bucketed by front size
+      const int lv = lvl0[k];
+      sm[rows <= 32 ? 0 : (rows <= 64 ? 1 : 2)][lv].push_back(k);
+      for (int j = 0; j < w; ++j) sm_f[lv] += static_cast<double>(rows - j) * (rows - j);
+      continue;
+    }
     double* Lk = L + s.lptr[k];
     double* Uk = U + s.uptr[k];
     const int nch = nchunks(w);
@@ -252,6 +267,7 @@ void DeviceFactor::build_factor_plan() {
   std::vector<PanelTask> panf, pof;
   std::vector<GemmTask> gmf;
   std::vector<ReduceTask> rdf;
+  std::vector<int32_t> smf;
   int64_t maxp = 1;
   for (int l = 0; l < nlev; ++l) maxp = std::max(maxp, split_k_parts(gm[l]));
   parts_.alloc(maxp * kTile * kTile);  // one level's split-K partial tiles at a time
@@ -260,7 +276,8 @@ void DeviceFactor::build_factor_plan() {
     flev_[l] = {static_cast<int64_t>(eaf.size()), static_cast<int64_t>(ea[l].size()),
                 static_cast<int64_t>(pof.size()), static_cast<int64_t>(po[l].size()),
                 static_cast<int64_t>(panf.size()), static_cast<int64_t>(pan[l].size()),
-                0, 0, ea_b[l], po_f[l], tr_f[l], gm_f[l], {0, 0, 0}, {0, 0, 0}, 0, 0};
+                0, 0, ea_b[l], po_f[l], tr_f[l], gm_f[l], {0, 0, 0}, {0, 0, 0}, 0, 0,
+                {0, 0, 0}, {0, 0, 0}, 0.0};
     {
       std::vector<GemmTask> gs;
       std::vector<ReduceTask> rs;
@@ -284,12 +301,19 @@ void DeviceFactor::build_factor_plan() {
       }
       flev_[l].pbn[bk] = static_cast<int64_t>(panf.size()) - flev_[l].pb0[bk];
     }
+    for (int bk = 0; bk < 3; ++bk) {
+      flev_[l].sm0[bk] = static_cast<int64_t>(smf.size());
+      flev_[l].smn[bk] = static_cast<int64_t>(sm[bk][l].size());
+      smf.insert(smf.end(), sm[bk][l].begin(), sm[bk][l].end());
+    }
+    flev_[l].sm_flops = sm_f[l];
   }
   ea_.upload(eaf, stream_);
   pan_.upload(panf, stream_);
   po_.upload(pof, stream_);
   gemm_.upload(gmf, stream_);
   red_.upload(rdf, stream_);
+  small_.upload(smf, stream_);
 }
 
 void DeviceFactor::build_selinv_plan() {
@@ -461,6 +485,20 @@ int32_t DeviceFactor::factor_panels() {
   for (size_t li = 0; li < flev_.size(); ++li) {
     const FLevel& lv = flev_[li];
     const int lvl = static_cast<int>(li);
+    if (lv.smn[0] + lv.smn[1] + lv.smn[2] > 0) {
+      pf.run(stream_, pf.tag("factor.small_front", lvl), lv.sm_flops, 0.0, [&] {
+        if (lv.smn[0])
+          k_small_front<32><<<static_cast<unsigned>(lv.smn[0]), 256, small_front_smem_bytes<32>(),
+                              stream_>>>(small_.p + lv.sm0[0], sd, L_.p, U_.p, status_.p, rdiag_.p);
+        if (lv.smn[1])
+          k_small_front<64><<<static_cast<unsigned>(lv.smn[1]), 256, small_front_smem_bytes<64>(),
+                              stream_>>>(small_.p + lv.sm0[1], sd, L_.p, U_.p, status_.p, rdiag_.p);
+        if (lv.smn[2])
+          k_small_front<96><<<static_cast<unsigned>(lv.smn[2]), 256, small_front_smem_bytes<96>(),
+                              stream_>>>(small_.p + lv.sm0[2], sd, L_.p, U_.p, status_.p, rdiag_.p);
+      });
+      launches_numeric_ += (lv.smn[0] > 0) + (lv.smn[1] > 0) + (lv.smn[2] > 0);
+    }
     if (lv.ean) {
       int blocks = static_cast<int>((lv.ean * 32 + 255) / 256);
       pf.run(stream_, pf.tag("factor.extend_add", lvl), 0.0, lv.ea_bytes, [&] {

@@ -116,7 +116,10 @@ class DeviceFactor {
     double ea_bytes, po_flops, tr_flops, gm_flops;  // algorithmic work per launch
     int64_t pb0[3], pbn[3];  // panel tasks split by width bucket 16 / 32 / 64
     int64_t rd0, rdn;        // split-K reductions of the level's GEMM tiles
+    int64_t sm0[3], smn[3];  // small fronts (rows <= 32 / 64 / 96), one CTA each
+    double sm_flops;
   };
+  DevBuf<int32_t> small_;
   std::vector<FLevel> flev_;
   DevBuf<ColTask> ea_;
   DevBuf<PanelTask> pan_, po_;
