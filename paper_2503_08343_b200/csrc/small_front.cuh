@@ -61,16 +61,17 @@ __global__ void __launch_bounds__(256) k_small_front(const int32_t* __restrict__
   // 3. right-looking partial Cholesky of the w pivot columns
   for (int j = 0; j < w; ++j) {
     if (tid == 0) {
+      // correctly rounded pivot and division, as cholesky.hpp:143,158
       const double d = F[j * FP + j];
       if (!(d > 0.0)) atomicMin(status, f0 + j);
-      const double rs = rsqrt_nr(d);
-      F[j * FP + j] = d * rs;
-      sh_rs = rs;
-      rdiag[f0 + j] = rs;
+      const double p = sqrt(d);
+      F[j * FP + j] = p;
+      sh_rs = p;
+      rdiag[f0 + j] = 1.0 / p;
     }
     __syncthreads();
-    const double rs = sh_rs;
-    for (int i = j + 1 + tid; i < rows; i += blockDim.x) F[j * FP + i] *= rs;
+    const double p = sh_rs;
+    for (int i = j + 1 + tid; i < rows; i += blockDim.x) F[j * FP + i] /= p;
     __syncthreads();
     for (int k = j + 1 + warp; k < rows; k += 8) {
       const double lk = F[j * FP + k];
