@@ -9,6 +9,7 @@
 #include "panel.cuh"
 #include "small_front.cuh"
 #include "solve.cuh"
+#include "solve_wide.cuh"
 #include "splitk.cuh"
 
 namespace gmrf {
@@ -47,13 +48,18 @@ inline int nchunks(int w) { return (w + kNB - 1) / kNB; }
 template <int NR>
 void set_solve_smem(int maxw) {
   const int smem_diag = (maxw * NR + 64 * 65) * static_cast<int>(sizeof(double));
-  const int smem_off = maxw * NR * static_cast<int>(sizeof(double));
   cuda_check(cudaFuncSetAttribute(k_fsolve_diag<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   smem_diag), "smem fsolve_diag");
   cuda_check(cudaFuncSetAttribute(k_bsolve_diag<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   smem_diag), "smem bsolve_diag");
-  cuda_check(cudaFuncSetAttribute(k_fsolve_off<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  std::max(smem_off, 1)), "smem fsolve_off");
+}
+
+template <int NR>
+void set_wide_smem() {
+  cuda_check(cudaFuncSetAttribute(k_fsolve_wide<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  wide_smem_bytes<NR>()), "smem fsolve_wide");
+  cuda_check(cudaFuncSetAttribute(k_bsolve_wide<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  wide_smem_bytes<NR>()), "smem bsolve_wide");
 }
 
 // Algorithmic flops of one tile: 2·k per needed output entry; a tile on the
@@ -97,16 +103,56 @@ DeviceFactor::DeviceFactor(std::shared_ptr<const Symbolic> sym, cudaStream_t str
     std::vector<int64_t> nx(lvl_ptr_.begin(), lvl_ptr_.end() - 1);
     for (int k = 0; k < s.ns; ++k) lsn[nx[s.sn_level[k]]++] = k;
   }
+  // wide supernodes go last in their level and get one CTA per 64-row block of
+  // the triangle (solve_wide.cuh); a launch holds at most wide_cap CTAs so all
+  // of them are co-resident
+  set_wide_smem<1>();
+  set_wide_smem<4>();
+  set_wide_smem<16>();
+  int nsm = 0, occ = 0;
+  cuda_check(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0), "sm count");
+  cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fsolve_wide<16>, 256,
+                                                           wide_smem_bytes<16>()),
+             "wide occupancy");
+  const int64_t wide_cap = static_cast<int64_t>(nsm) * std::max(occ, 0);
+  auto is_wide = [&](int k) { return s.w(k) > kWideW && nchunks(s.w(k)) <= wide_cap; };
+  lvl_nrm_.assign(s.n_levels, 0);
+  wl_ptr_.assign(s.n_levels + 1, 0);
+  wgroups_.clear();
+  {
+    std::vector<WideBlock> wf, wb;
+    int64_t nflag = 0;
+    for (int l = 0; l < s.n_levels; ++l) {
+      auto b = lsn.begin() + lvl_ptr_[l], e = lsn.begin() + lvl_ptr_[l + 1];
+      auto mid = std::stable_partition(b, e, [&](int32_t k) { return !is_wide(k); });
+      lvl_nrm_[l] = mid - b;
+      for (auto it = mid; it != e; ++it) {
+        const int k = *it, nb = nchunks(s.w(k));
+        if (wgroups_.size() == static_cast<size_t>(wl_ptr_[l]) ||
+            wgroups_.back().nt + nb > wide_cap)
+          wgroups_.push_back({static_cast<int64_t>(wf.size()), 0});
+        for (int q = 0; q < nb; ++q) wf.push_back({k, q, nb, static_cast<int32_t>(nflag)});
+        for (int q = nb - 1; q >= 0; --q) wb.push_back({k, q, nb, static_cast<int32_t>(nflag)});
+        wgroups_.back().nt += nb;
+        nflag += nb;
+      }
+      wl_ptr_[l + 1] = static_cast<int64_t>(wgroups_.size());
+    }
+    wide_blocks_ = nflag;
+    wfwd_.upload(wf, stream_);
+    wbwd_.upload(wb, stream_);
+    wflags_.alloc(std::max<int64_t>(2 * nflag, 1));
+  }
   lvl_sn_.upload(lsn, stream_);
   // solve workspaces: update vectors (r_s) and backward partials (tiles_s × w_s),
   // plus the 128-row tiles of every supernode's rectangular block, per level
   std::vector<int64_t> up(s.ns + 1, 0), pp(s.ns + 1, 0);
-  maxw_ = 1;
+  maxw_ = 1;  // widest supernode solved by the one-CTA triangle kernels
   for (int k = 0; k < s.ns; ++k) {
     const int r = s.r(k), nt = (r + kSolveRows - 1) / kSolveRows;
     up[k + 1] = up[k] + r;
     pp[k + 1] = pp[k] + static_cast<int64_t>(nt) * s.w(k);
-    maxw_ = std::max(maxw_, s.w(k));
+    if (!is_wide(k)) maxw_ = std::max(maxw_, s.w(k));
   }
   uv_total_ = up[s.ns];
   p_total_ = pp[s.ns];
@@ -558,45 +604,82 @@ void DeviceFactor::ensure_solve_ws(int nrhs) {
   ws_nrhs_ = nrhs;
 }
 
-namespace {
 template <int NR>
-void launch_solve_levels(const double* rdiag, bool fwd, bool bwd, int nlev,
-                         const std::vector<int64_t>& lvl_ptr, const int32_t* lvl_sn,
-                         const std::vector<int64_t>& tile_ptr, const SolveTile* tiles, SymDev sd,
-                         const double* L, double* y, int nr, double* Uv, const int64_t* uvptr,
-                         double* P, const int64_t* pptr, int maxw, cudaStream_t st,
-                         KernelProfiler& pf, const std::vector<double>& lvl_bytes,
-                         int64_t& launches) {
-  const int smem_diag = (maxw * NR + 64 * 65) * static_cast<int>(sizeof(double));
-  const int smem_off = maxw * NR * static_cast<int>(sizeof(double));
+void DeviceFactor::launch_solve_levels(bool fwd, bool bwd, double* y, int nr) {
+  const Symbolic& s = *sym_;
+  const SymDev sd = symdev();
+  KernelProfiler& pf = *prof_;
+  cudaStream_t st = stream_;
+  const double* L = L_.p;
+  const double* rdiag = rdiag_.p;
+  const int32_t* lvl_sn = lvl_sn_.p;
+  const int smem_diag = (maxw_ * NR + 64 * 65) * static_cast<int>(sizeof(double));
+  constexpr int smem_wide = wide_smem_bytes<NR>();
+  int64_t& launches = launches_solve_;
+  if (wide_blocks_) {
+    cuda_check(cudaMemsetAsync(wflags_.p, 0, 2 * wide_blocks_ * sizeof(int32_t), st), "flags");
+    ++launches;
+  }
+  auto coop = [&](const void* fn, int64_t grid, void** args) {
+    cuda_check(cudaLaunchCooperativeKernel(fn, dim3(static_cast<unsigned>(grid)), dim3(256), args,
+                                           smem_wide, st),
+               "wide solve launch");
+    ++launches;
+  };
   if (fwd)
-    for (int l = 0; l < nlev; ++l) {
-      const int cnt = static_cast<int>(lvl_ptr[l + 1] - lvl_ptr[l]);
-      const int nt = static_cast<int>(tile_ptr[l + 1] - tile_ptr[l]);
-      pf.run(st, pf.tag("solve.forward", l), 0.0, lvl_bytes[l], [&] {
-        k_fsolve_diag<NR><<<cnt, 256, smem_diag, st>>>(lvl_sn + lvl_ptr[l], sd, L, y, nr, Uv, uvptr,
-                                                       rdiag);
-        if (nt)
-          k_fsolve_off<NR><<<nt, kSolveRows, smem_off, st>>>(tiles + tile_ptr[l], sd, L, y, nr, Uv,
-                                                             uvptr);
+    for (int l = 0; l < s.n_levels; ++l) {
+      const int nrm = static_cast<int>(lvl_nrm_[l]);
+      const int nw = static_cast<int>(lvl_ptr_[l + 1] - lvl_ptr_[l]) - nrm;
+      const int nt = static_cast<int>(tile_ptr_[l + 1] - tile_ptr_[l]);
+      pf.run(st, pf.tag("solve.forward", l), 0.0, lvl_bytes_[l], [&] {
+        if (nrm) {
+          k_fsolve_diag<NR><<<nrm, 256, smem_diag, st>>>(lvl_sn + lvl_ptr_[l], sd, L, y, nr, Uv_.p,
+                                                         uvptr_.p, rdiag);
+          ++launches;
+        }
+        if (nw) {
+          k_fsolve_wide_prep<NR><<<nw, 256, 0, st>>>(lvl_sn + lvl_ptr_[l] + nrm, sd, y, nr, Uv_.p,
+                                                     uvptr_.p);
+          ++launches;
+          for (int64_t g = wl_ptr_[l]; g < wl_ptr_[l + 1]; ++g) {
+            const WideBlock* tasks = wfwd_.p + wgroups_[g].t0;
+            int32_t* flags = wflags_.p;
+            void* args[] = {&tasks, const_cast<SymDev*>(&sd), &L, &y, &nr, &rdiag, &flags};
+            coop(reinterpret_cast<const void*>(k_fsolve_wide<NR>), wgroups_[g].nt, args);
+          }
+        }
+        if (nt) {
+          k_fsolve_off<NR><<<nt, kSolveRows, 0, st>>>(tiles_.p + tile_ptr_[l], sd, L, y, nr, Uv_.p,
+                                                      uvptr_.p);
+          ++launches;
+        }
       });
-      launches += 1 + (nt > 0);
     }
   if (bwd)
-    for (int l = nlev - 1; l >= 0; --l) {
-      const int cnt = static_cast<int>(lvl_ptr[l + 1] - lvl_ptr[l]);
-      const int nt = static_cast<int>(tile_ptr[l + 1] - tile_ptr[l]);
-      pf.run(st, pf.tag("solve.backward", l), 0.0, lvl_bytes[l], [&] {
-        if (nt)
-          k_bsolve_off<NR><<<nt, 256, 0, st>>>(tiles + tile_ptr[l], sd, L, y, nr, P, pptr);
-        k_bsolve_diag<NR><<<cnt, 256, smem_diag, st>>>(lvl_sn + lvl_ptr[l], sd, L, y, nr, P, pptr,
-                                                       rdiag);
+    for (int l = s.n_levels - 1; l >= 0; --l) {
+      const int nrm = static_cast<int>(lvl_nrm_[l]);
+      const int nt = static_cast<int>(tile_ptr_[l + 1] - tile_ptr_[l]);
+      pf.run(st, pf.tag("solve.backward", l), 0.0, lvl_bytes_[l], [&] {
+        if (nt) {
+          k_bsolve_off<NR><<<nt, 256, 0, st>>>(tiles_.p + tile_ptr_[l], sd, L, y, nr, P_.p, pptr_.p);
+          ++launches;
+        }
+        if (nrm) {
+          k_bsolve_diag<NR><<<nrm, 256, smem_diag, st>>>(lvl_sn + lvl_ptr_[l], sd, L, y, nr, P_.p,
+                                                         pptr_.p, rdiag);
+          ++launches;
+        }
+        for (int64_t g = wl_ptr_[l]; g < wl_ptr_[l + 1]; ++g) {
+          const WideBlock* tasks = wbwd_.p + wgroups_[g].t0;
+          const double* P = P_.p;
+          const int64_t* pptr = pptr_.p;
+          int32_t* flags = wflags_.p + wide_blocks_;
+          void* args[] = {&tasks, const_cast<SymDev*>(&sd), &L, &y, &nr, &P, &pptr, &rdiag, &flags};
+          coop(reinterpret_cast<const void*>(k_bsolve_wide<NR>), wgroups_[g].nt, args);
+        }
       });
-      launches += 1 + (nt > 0);
     }
 }
-
-}  // namespace
 
 void DeviceFactor::solve(int mode, int nrhs, const double* b, double* x, bool on_device) {
   require(factored_, kContract, "solve: factor not computed");
@@ -605,7 +688,6 @@ void DeviceFactor::solve(int mode, int nrhs, const double* b, double* x, bool on
   const int n = s.n;
   if (n == 0 || nrhs == 0) return;
   launches_solve_ = 0;
-  const SymDev sd = symdev();
   // right-hand sides per pass: 1, or up to 16 within the shared-memory budget
   const int cap = static_cast<int>((200 * 1024 / 8 - 64 * 65) / std::max(maxw_, 1));
   require(cap >= 1, kContract, "solve: supernode too wide for the shared-memory triangle");
@@ -634,18 +716,9 @@ void DeviceFactor::solve(int mode, int nrhs, const double* b, double* x, bool on
                  "copy b");
     }
     const bool fwd = mode == 0 || mode == 2, bwd = mode == 1 || mode == 2;
-    if (nrb == 1)
-      launch_solve_levels<1>(rdiag_.p, fwd, bwd, s.n_levels, lvl_ptr_, lvl_sn_.p, tile_ptr_, tiles_.p,
-                             sd, L_.p, y, nr, Uv_.p, uvptr_.p, P_.p, pptr_.p, maxw_, stream_, *prof_,
-                             lvl_bytes_, launches_solve_);
-    else if (nrb == 4)
-      launch_solve_levels<4>(rdiag_.p, fwd, bwd, s.n_levels, lvl_ptr_, lvl_sn_.p, tile_ptr_, tiles_.p,
-                             sd, L_.p, y, nr, Uv_.p, uvptr_.p, P_.p, pptr_.p, maxw_, stream_, *prof_,
-                             lvl_bytes_, launches_solve_);
-    else
-      launch_solve_levels<16>(rdiag_.p, fwd, bwd, s.n_levels, lvl_ptr_, lvl_sn_.p, tile_ptr_, tiles_.p,
-                              sd, L_.p, y, nr, Uv_.p, uvptr_.p, P_.p, pptr_.p, maxw_, stream_,
-                              *prof_, lvl_bytes_, launches_solve_);
+    if (nrb == 1) launch_solve_levels<1>(fwd, bwd, y, nr);
+    else if (nrb == 4) launch_solve_levels<4>(fwd, bwd, y, nr);
+    else launch_solve_levels<16>(fwd, bwd, y, nr);
     if (mode == 2) {
       double* dst = on_device ? xx : v2_.p;
       k_permute_scatter<<<pblocks, 256, 0, stream_>>>(y, perm_.p, n, nr, dst);

@@ -96,6 +96,8 @@ class DeviceFactor {
   void build_factor_plan();
   void build_selinv_plan();
   void ensure_solve_ws(int nrhs);
+  template <int NR>
+  void launch_solve_levels(bool fwd, bool bwd, double* y, int nr);
   SymDev symdev() const;
 
   std::shared_ptr<const Symbolic> sym_;
@@ -143,6 +145,20 @@ class DeviceFactor {
 
   std::vector<int64_t> lvl_ptr_;
   DevBuf<int32_t> lvl_sn_;
+  // wide supernodes (solve_wide.cuh): per level, the first lvl_nrm_[l] entries
+  // of the level's lvl_sn_ range are narrow, the rest wide; their 64-row blocks
+  // form cooperative launch groups wgroups_[wl_ptr_[l] .. wl_ptr_[l+1])
+ public:
+  struct WideGroup {
+    int64_t t0, nt;  // tasks [t0, t0+nt) of wfwd_ / wbwd_
+  };
+
+ private:
+  std::vector<int64_t> lvl_nrm_, wl_ptr_;
+  std::vector<WideGroup> wgroups_;
+  DevBuf<WideBlock> wfwd_, wbwd_;
+  DevBuf<int32_t> wflags_;
+  int64_t wide_blocks_ = 0;
 
   int64_t launches_numeric_ = 0, launches_solve_ = 0, launches_selinv_ = 0;
 };

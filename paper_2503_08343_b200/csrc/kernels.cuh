@@ -61,6 +61,15 @@ struct SelChunk {
   int32_t tile;      // TRSM row slab (for the TRSM kernel)
 };
 
+// One 64-row block of a wide supernode's triangle in the solves (solve_wide.cuh).
+constexpr int kWideW = 256;  // supernodes wider than this use the wide solve kernels
+struct WideBlock {
+  int32_t sn;
+  int32_t b;      // block index inside the triangle
+  int32_t nb;     // blocks in this supernode
+  int32_t flag0;  // flag index of block 0 of this supernode
+};
+
 // Device view of the symbolic structure (all arrays device-resident).
 struct SymDev {
   const int32_t* sn_first;

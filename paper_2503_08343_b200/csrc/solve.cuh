@@ -135,7 +135,8 @@ __global__ void __launch_bounds__(kSolveRows) k_fsolve_off(const SolveTile* __re
                                                           const double* __restrict__ y, int nrhs,
                                                           double* __restrict__ Uv,
                                                           const int64_t* __restrict__ uvptr) {
-  extern __shared__ double sm[];
+  constexpr int CW = kSolveOffCols;
+  __shared__ double yJ[CW * NR];  // [rr*CW + j], one column chunk of y_J
   const SolveTile t = tiles[blockIdx.x];
   const int s = t.sn;
   const int f0 = sd.sn_first[s];
@@ -143,34 +144,40 @@ __global__ void __launch_bounds__(kSolveRows) k_fsolve_off(const SolveTile* __re
   const int rows = static_cast<int>(sd.sn_rptr[s + 1] - sd.sn_rptr[s]);
   const int r = rows - w;
   const int n = sd.n;
-  double* yJ = sm;  // [rr*w + j]
-  for (int idx = threadIdx.x; idx < w * nrhs; idx += blockDim.x) {
-    const int a = idx % w, rr = idx / w;
-    yJ[rr * w + a] = y[f0 + a + static_cast<int64_t>(rr) * n];
-  }
-  __syncthreads();
   const int i = t.r0 + threadIdx.x;
-  if (i >= r) return;
+  const bool active = i < r;
   const double* Lr = L + sd.lptr[s] + w + i;
   double* u = Uv + uvptr[s] * nrhs;
   double acc[NR];
 #pragma unroll
-  for (int rr = 0; rr < NR; ++rr) acc[rr] = rr < nrhs ? u[i + rr * r] : 0.0;
-  int j = 0;
-  for (; j + 8 <= w; j += 8) {  // 8 independent loads in flight
-    double l[8];
+  for (int rr = 0; rr < NR; ++rr) acc[rr] = (active && rr < nrhs) ? u[i + rr * r] : 0.0;
+  for (int c0 = 0; c0 < w; c0 += CW) {
+    const int wc = min(CW, w - c0);
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < wc * nrhs; idx += blockDim.x) {
+      const int a = idx % wc, rr = idx / wc;
+      yJ[rr * CW + a] = y[f0 + c0 + a + static_cast<int64_t>(rr) * n];
+    }
+    __syncthreads();
+    if (!active) continue;
+    const double* Lc = Lr + static_cast<int64_t>(c0) * rows;
+    int j = 0;
+    for (; j + 8 <= wc; j += 8) {  // 8 independent loads in flight
+      double l[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) l[u] = Lr[static_cast<int64_t>(j + u) * rows];
+      for (int q = 0; q < 8; ++q) l[q] = Lc[static_cast<int64_t>(j + q) * rows];
 #pragma unroll
-    for (int u = 0; u < 8; ++u)
+      for (int q = 0; q < 8; ++q)
 #pragma unroll
-      for (int rr = 0; rr < NR; ++rr) acc[rr] -= l[u] * yJ[rr * w + j + u];
+        for (int rr = 0; rr < NR; ++rr) acc[rr] -= l[q] * yJ[rr * CW + j + q];
+    }
+    for (; j < wc; ++j) {
+      const double l = Lc[static_cast<int64_t>(j) * rows];
+#pragma unroll
+      for (int rr = 0; rr < NR; ++rr) acc[rr] -= l * yJ[rr * CW + j];
+    }
   }
-  for (; j < w; ++j) {
-    const double l = Lr[static_cast<int64_t>(j) * rows];
-#pragma unroll
-    for (int rr = 0; rr < NR; ++rr) acc[rr] -= l * yJ[rr * w + j];
-  }
+  if (!active) return;
 #pragma unroll
   for (int rr = 0; rr < NR; ++rr)
     if (rr < nrhs) u[i + rr * r] = acc[rr];

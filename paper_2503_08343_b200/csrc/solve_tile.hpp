@@ -6,6 +6,7 @@
 namespace gmrf {
 
 constexpr int kSolveRows = 128;
+constexpr int kSolveOffCols = 256;  // y_J columns staged per pass in k_fsolve_off
 
 struct SolveTile {
   int32_t sn;
