@@ -27,7 +27,7 @@ __global__ void __launch_bounds__(256) k_small_front(const int32_t* __restrict__
                                                      double* __restrict__ rdiag) {
   extern __shared__ double F[];  // F[j*FP + i], front rows × rows, column-major
   constexpr int FP = RB + 1;
-  __shared__ double sh_rs;
+  __shared__ double sh_rs, sh_rp;
   const int s = sns[blockIdx.x];
   const int f0 = sd.sn_first[s];
   const int w = sd.sn_first[s + 1] - f0;
@@ -64,14 +64,16 @@ __global__ void __launch_bounds__(256) k_small_front(const int32_t* __restrict__
       // correctly rounded pivot and division, as cholesky.hpp:143,158
       const double d = F[j * FP + j];
       if (!(d > 0.0)) atomicMin(status, f0 + j);
-      const double p = sqrt(d);
+      const double p = sqrt_rn_pos(d);
+      const double rp = recip_nr(p);
       F[j * FP + j] = p;
       sh_rs = p;
-      rdiag[f0 + j] = 1.0 / p;
+      sh_rp = rp;
+      rdiag[f0 + j] = div_rn(1.0, p, rp);
     }
     __syncthreads();
-    const double p = sh_rs;
-    for (int i = j + 1 + tid; i < rows; i += blockDim.x) F[j * FP + i] /= p;
+    const double p = sh_rs, rp = sh_rp;
+    for (int i = j + 1 + tid; i < rows; i += blockDim.x) F[j * FP + i] = div_rn(F[j * FP + i], p, rp);
     __syncthreads();
     for (int k = j + 1 + warp; k < rows; k += 8) {
       const double lk = F[j * FP + k];
