@@ -44,6 +44,7 @@ void set_smem_attrs() {
 }
 
 inline int nchunks(int w) { return (w + kNB - 1) / kNB; }
+constexpr unsigned kRowsMaxCtas = 148;  // one CTA per SM (k_panel_rows uses ~254 registers)
 
 template <int NR>
 void set_solve_smem(int maxw) {
@@ -554,16 +555,37 @@ int32_t DeviceFactor::factor_panels() {
       ++launches_numeric_;
     }
     if (lv.pann) {
+      // latency-bound levels (one wave) use the row-per-thread sweep; levels
+      // with several waves of chunk slabs keep the blocked smem kernel, whose
+      // CTAs are small enough to co-reside 4-5 per SM
       pf.run(stream_, pf.tag("factor.potrf_trsm", lvl), lv.po_flops + lv.tr_flops, 0.0, [&] {
-        if (lv.pbn[0])
-          k_potrf_trsm<16><<<static_cast<unsigned>(lv.pbn[0]), 128, panel_smem_bytes<16>(),
-                             stream_>>>(pan_.p + lv.pb0[0], status_.p, diag_.p);
-        if (lv.pbn[1])
-          k_potrf_trsm<32><<<static_cast<unsigned>(lv.pbn[1]), 128, panel_smem_bytes<32>(),
-                             stream_>>>(pan_.p + lv.pb0[1], status_.p, diag_.p);
-        if (lv.pbn[2])
-          k_potrf_trsm<64><<<static_cast<unsigned>(lv.pbn[2]), 128, panel_smem_bytes<64>(),
-                             stream_>>>(pan_.p + lv.pb0[2], status_.p, diag_.p);
+        if (lv.pbn[0]) {
+          const unsigned g = static_cast<unsigned>(lv.pbn[0]);
+          if (g <= kRowsMaxCtas)
+            k_panel_rows<16, kTrsmRows><<<g, panel_rows_threads<16, kTrsmRows>(), 0, stream_>>>(
+                pan_.p + lv.pb0[0], status_.p, diag_.p);
+          else
+            k_potrf_trsm<16><<<g, 128, panel_smem_bytes<16>(), stream_>>>(pan_.p + lv.pb0[0],
+                                                                          status_.p, diag_.p);
+        }
+        if (lv.pbn[1]) {
+          const unsigned g = static_cast<unsigned>(lv.pbn[1]);
+          if (g <= kRowsMaxCtas)
+            k_panel_rows<32, kTrsmRows><<<g, panel_rows_threads<32, kTrsmRows>(), 0, stream_>>>(
+                pan_.p + lv.pb0[1], status_.p, diag_.p);
+          else
+            k_potrf_trsm<32><<<g, 128, panel_smem_bytes<32>(), stream_>>>(pan_.p + lv.pb0[1],
+                                                                          status_.p, diag_.p);
+        }
+        if (lv.pbn[2]) {
+          const unsigned g = static_cast<unsigned>(lv.pbn[2]);
+          if (g <= kRowsMaxCtas)
+            k_panel_rows<64, kTrsmRows><<<g, panel_rows_threads<64, kTrsmRows>(), 0, stream_>>>(
+                pan_.p + lv.pb0[2], status_.p, diag_.p);
+          else
+            k_potrf_trsm<64><<<g, 128, panel_smem_bytes<64>(), stream_>>>(pan_.p + lv.pb0[2],
+                                                                          status_.p, diag_.p);
+        }
       });
       launches_numeric_ += (lv.pbn[0] > 0) + (lv.pbn[1] > 0) + (lv.pbn[2] > 0);
     }
