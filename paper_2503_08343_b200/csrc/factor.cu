@@ -9,6 +9,7 @@
 #include "panel.cuh"
 #include "small_front.cuh"
 #include "solve.cuh"
+#include "selinv.cuh"
 #include "solve_wide.cuh"
 #include "splitk.cuh"
 
@@ -19,8 +20,6 @@ void cuda_check(cudaError_t e, const char* what) {
 }
 
 namespace {
-constexpr int kPanelSmem = (kNB * (kNB + 1) + kNB * (kTrsmRows + 1)) * sizeof(double);
-constexpr int kDiagSmem = 3 * kNB * (kNB + 1) * sizeof(double);
 
 void set_smem_attrs() {
   static bool done = false;
@@ -34,12 +33,9 @@ void set_smem_attrs() {
   cuda_check(cudaFuncSetAttribute(k_small_front<96>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   small_front_smem_bytes<96>()),
              "smem k_small_front");
-  cuda_check(
-      cudaFuncSetAttribute(k_sel_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, kPanelSmem),
-      "smem k_sel_trsm");
-  cuda_check(
-      cudaFuncSetAttribute(k_sel_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, kDiagSmem),
-      "smem k_sel_diag");
+  cuda_check(cudaFuncSetAttribute(k_sel_diag_w<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  sel_diag_smem_bytes<64>()),
+             "smem k_sel_diag");
   done = true;
 }
 
@@ -371,7 +367,7 @@ void DeviceFactor::build_selinv_plan() {
   chunk_levels(s, lvl0, nlev);
   std::vector<std::vector<ColTask>> ga(nlev);
   std::vector<std::vector<GemmTask>> yg(nlev), zg(nlev);
-  std::vector<std::vector<SelChunk>> tr(nlev), dg(nlev);
+  std::vector<std::vector<SelChunk>> tr(nlev), dg(nlev), mi(nlev);
   std::vector<double> ga_b(nlev, 0.0), y_f(nlev, 0.0), t_f(nlev, 0.0), z_f(nlev, 0.0),
       d_f(nlev, 0.0);
   double* L = L_.p;
@@ -429,7 +425,8 @@ void DeviceFactor::build_selinv_plan() {
       for (int i0 = c0 + wk; i0 < w; i0 += kTile) ytile(i0, std::min(i0 + kTile, w));
       for (int i0 = w; i0 < rows; i0 += kTile) ytile(i0, std::min(i0 + kTile, rows));
       const int nbelow = rows - c0 - wk;
-      for (int t = 0; t * kTrsmRows < nbelow; ++t) tr[lv].push_back({Lk, Sk, rows, c0, wk, w, t});
+      const double* rdc = rdiag_.p + s.sn_first[k] + c0;
+      for (int t = 0; t * kTrsmRows < nbelow; ++t) tr[lv].push_back({Lk, Sk, rows, c0, wk, w, t, rdc});
       GemmTask z{};
       z.c = Sk + c0 + static_cast<int64_t>(c0) * rows;
       z.ldc = rows;
@@ -444,12 +441,13 @@ void DeviceFactor::build_selinv_plan() {
       z.alpha = 1.0;
       z.beta = 0.0;
       zg[lv].push_back(z);
-      dg[lv].push_back({Lk, Sk, rows, c0, wk, w, 0});
+      dg[lv].push_back({Lk, Sk, rows, c0, wk, w, 0, rdc});
+      for (int t = 0; t * 64 < p; ++t) mi[lv].push_back({Lk, Sk, rows, c0, wk, w, t, rdc});
     }
   }
   std::vector<ColTask> gaf;
   std::vector<GemmTask> gmf;
-  std::vector<SelChunk> trf, dgf;
+  std::vector<SelChunk> trf, dgf, mif;
   std::vector<ReduceTask> rdf;
   int64_t maxp = 1;
   for (int l = 0; l < nlev; ++l)
@@ -481,10 +479,22 @@ void DeviceFactor::build_selinv_plan() {
     rdf.insert(rdf.end(), rs.begin(), rs.end());
     e.t0 = trf.size();
     e.tn = tr[l].size();
-    trf.insert(trf.end(), tr[l].begin(), tr[l].end());
     e.d0 = dgf.size();
     e.dn = dg[l].size();
-    dgf.insert(dgf.end(), dg[l].begin(), dg[l].end());
+    auto bucket = [](int w) { return w <= 16 ? 0 : (w <= 32 ? 1 : 2); };
+    for (int bk = 0; bk < 3; ++bk) {
+      e.tb0[bk] = trf.size();
+      for (const SelChunk& c : tr[l])
+        if (bucket(c.w) == bk) trf.push_back(c);
+      e.tbn[bk] = static_cast<int64_t>(trf.size()) - e.tb0[bk];
+      e.db0[bk] = dgf.size();
+      for (const SelChunk& c : dg[l])
+        if (bucket(c.w) == bk) dgf.push_back(c);
+      e.dbn[bk] = static_cast<int64_t>(dgf.size()) - e.db0[bk];
+    }
+    e.mi0 = mif.size();
+    e.min_ = mi[l].size();
+    mif.insert(mif.end(), mi[l].begin(), mi[l].end());
     e.ga_bytes = ga_b[l];
     e.y_flops = y_f[l];
     e.t_flops = t_f[l];
@@ -496,6 +506,7 @@ void DeviceFactor::build_selinv_plan() {
   sred_.upload(rdf, stream_);
   strsm_.upload(trf, stream_);
   sdiag_.upload(dgf, stream_);
+  smir_.upload(mif, stream_);
   selinv_plan_ = true;
 }
 
@@ -770,14 +781,14 @@ void DeviceFactor::selinv(double* diag_out, bool on_device) {
     KernelProfiler& pf = *prof_;
     if (e.gan) {
       int blocks = static_cast<int>((e.gan * 32 + 255) / 256);
-      pf.run(stream_, "selinv.gather", 0.0, e.ga_bytes, [&] {
+      pf.run(stream_, pf.tag("selinv.gather", l), 0.0, e.ga_bytes, [&] {
         k_sel_gather<<<blocks, 256, 0, stream_>>>(sga_.p + e.ga0, static_cast<int>(e.gan), sd,
                                                  snparent_.p, Sig_.p, U_.p);
       });
       ++launches_selinv_;
     }
     if (e.yn) {
-      pf.run(stream_, "selinv.gemm_dmma", e.y_flops, 0.0, [&] {
+      pf.run(stream_, pf.tag("selinv.gemm_dmma", l), e.y_flops, 0.0, [&] {
         k_gemm_tiles<<<static_cast<unsigned>(e.yn), 128, 0, stream_>>>(sgemm_.p + e.y0);
         if (e.yrn)
           k_reduce_parts<<<static_cast<unsigned>(e.yrn), 256, 0, stream_>>>(sred_.p + e.yr0,
@@ -786,13 +797,21 @@ void DeviceFactor::selinv(double* diag_out, bool on_device) {
       launches_selinv_ += 1 + (e.yrn > 0);
     }
     if (e.tn) {
-      pf.run(stream_, "selinv.trsm", e.t_flops, 0.0, [&] {
-        k_sel_trsm<<<static_cast<unsigned>(e.tn), 128, kPanelSmem, stream_>>>(strsm_.p + e.t0);
+      pf.run(stream_, pf.tag("selinv.trsm", l), e.t_flops, 0.0, [&] {
+        if (e.tbn[0])
+          k_sel_trsm_w<16><<<static_cast<unsigned>(e.tbn[0]), kTrsmRows, 0, stream_>>>(strsm_.p +
+                                                                                       e.tb0[0]);
+        if (e.tbn[1])
+          k_sel_trsm_w<32><<<static_cast<unsigned>(e.tbn[1]), kTrsmRows, 0, stream_>>>(strsm_.p +
+                                                                                       e.tb0[1]);
+        if (e.tbn[2])
+          k_sel_trsm_w<64><<<static_cast<unsigned>(e.tbn[2]), kTrsmRows, 0, stream_>>>(strsm_.p +
+                                                                                       e.tb0[2]);
       });
-      ++launches_selinv_;
+      launches_selinv_ += (e.tbn[0] > 0) + (e.tbn[1] > 0) + (e.tbn[2] > 0);
     }
     if (e.zn) {
-      pf.run(stream_, "selinv.gemm_dmma", e.z_flops, 0.0, [&] {
+      pf.run(stream_, pf.tag("selinv.gemm_dmma", l), e.z_flops, 0.0, [&] {
         k_gemm_tiles<<<static_cast<unsigned>(e.zn), 128, 0, stream_>>>(sgemm_.p + e.z0);
         if (e.zrn)
           k_reduce_parts<<<static_cast<unsigned>(e.zrn), 256, 0, stream_>>>(sred_.p + e.zr0,
@@ -801,8 +820,22 @@ void DeviceFactor::selinv(double* diag_out, bool on_device) {
       launches_selinv_ += 1 + (e.zrn > 0);
     }
     if (e.dn) {
-      pf.run(stream_, "selinv.diag", e.d_flops, 0.0, [&] {
-        k_sel_diag<<<static_cast<unsigned>(e.dn), 256, kDiagSmem, stream_>>>(sdiag_.p + e.d0);
+      pf.run(stream_, pf.tag("selinv.diag", l), e.d_flops, 0.0, [&] {
+        if (e.dbn[0])
+          k_sel_diag_w<16><<<static_cast<unsigned>(e.dbn[0]), 32, sel_diag_smem_bytes<16>(),
+                             stream_>>>(sdiag_.p + e.db0[0]);
+        if (e.dbn[1])
+          k_sel_diag_w<32><<<static_cast<unsigned>(e.dbn[1]), 32, sel_diag_smem_bytes<32>(),
+                             stream_>>>(sdiag_.p + e.db0[1]);
+        if (e.dbn[2])
+          k_sel_diag_w<64><<<static_cast<unsigned>(e.dbn[2]), 64, sel_diag_smem_bytes<64>(),
+                             stream_>>>(sdiag_.p + e.db0[2]);
+      });
+      launches_selinv_ += (e.dbn[0] > 0) + (e.dbn[1] > 0) + (e.dbn[2] > 0);
+    }
+    if (e.min_) {
+      pf.run(stream_, pf.tag("selinv.mirror", l), 0.0, 0.0, [&] {
+        k_sel_mirror<<<static_cast<unsigned>(e.min_), 256, 0, stream_>>>(smir_.p + e.mi0);
       });
       ++launches_selinv_;
     }

@@ -131,6 +131,8 @@ class DeviceFactor {
     int64_t ga0, gan, y0, yn, t0, tn, z0, zn, d0, dn;
     double ga_bytes, y_flops, t_flops, z_flops, d_flops;
     int64_t yr0, yrn, zr0, zrn;  // split-K reductions of the Y and Z tiles
+    int64_t tb0[3], tbn[3], db0[3], dbn[3];  // TRSM / diag chunks by width bucket 16/32/64
+    int64_t mi0, min_;                       // Σ_{P,J} → Σ_{J,P} mirror tiles
   };
   DevBuf<ReduceTask> red_, sred_;
   DevBuf<double> parts_, sparts_;  // split-K partial tiles
@@ -140,7 +142,7 @@ class DeviceFactor {
   std::vector<SLevel> slev_;
   DevBuf<ColTask> sga_;
   DevBuf<GemmTask> sgemm_;
-  DevBuf<SelChunk> strsm_, sdiag_;
+  DevBuf<SelChunk> strsm_, sdiag_, smir_;
   bool selinv_plan_ = false;
 
   std::vector<int64_t> lvl_ptr_;

@@ -262,96 +262,7 @@ __global__ void k_sel_gather(const ColTask* __restrict__ tasks, int ntasks, SymD
   }
 }
 
-// Σ_{R_k,J} ← −Σ_{R_k,J} · L_JJ⁻¹ (in place), one slab of kTrsmRows rows.
-__global__ void __launch_bounds__(128) k_sel_trsm(const SelChunk* __restrict__ tasks) {
-  extern __shared__ double smem[];
-  const SelChunk& t = tasks[blockIdx.x];
-  const int w = t.w, ld = t.ld, tid = threadIdx.x;
-  constexpr int DP = kNB + 1, XP = kTrsmRows + 1;
-  double* D = smem;
-  double* X = smem + kNB * DP;
-  const double* Lk = t.l + t.c0 + static_cast<int64_t>(t.c0) * ld;
-  for (int idx = tid; idx < w * w; idx += blockDim.x) {
-    int i = idx % w, j = idx / w;
-    if (i >= j) D[j * DP + i] = Lk[i + static_cast<int64_t>(j) * ld];
-  }
-  const int nbelow = ld - t.c0 - w;
-  const int r0 = t.tile * kTrsmRows;
-  const int nr = min(kTrsmRows, nbelow - r0);
-  double* B = t.sig + t.c0 + w + r0 + static_cast<int64_t>(t.c0) * ld;
-  for (int idx = tid; idx < nr * w; idx += blockDim.x) {
-    int r = idx % nr, j = idx / nr;
-    X[j * XP + r] = -B[r + static_cast<int64_t>(j) * ld];
-  }
-  __syncthreads();
-  if (tid < nr) {
-    // x · L = b  → x_j = (b_j − Σ_{l>j} x_l L_lj) / L_jj, j descending
-    for (int j = w - 1; j >= 0; --j) {
-      double s = X[j * XP + tid];
-      for (int l = j + 1; l < w; ++l) s -= X[l * XP + tid] * D[j * DP + l];
-      X[j * XP + tid] = s / D[j * DP + j];
-    }
-  }
-  __syncthreads();
-  for (int idx = tid; idx < nr * w; idx += blockDim.x) {
-    int r = idx % nr, j = idx / nr;
-    B[r + static_cast<int64_t>(j) * ld] = X[j * XP + r];
-  }
-}
-
-// Σ_JJ = L_JJ⁻ᵀ (L_JJ⁻¹ − Z), Z = L_{R,J}ᵀ Σ_{R,J} already stored in the Σ
-// diagonal block; writes Σ_JJ symmetric and mirrors Σ_{P,J} into Σ_{J,P}.
-__global__ void __launch_bounds__(256) k_sel_diag(const SelChunk* __restrict__ tasks) {
-  extern __shared__ double smem[];
-  const SelChunk& t = tasks[blockIdx.x];
-  const int w = t.w, ld = t.ld, tid = threadIdx.x;
-  constexpr int P = kNB + 1;
-  double* Lm = smem;            // L_JJ (lower)
-  double* Li = smem + kNB * P;  // L_JJ⁻¹ (lower)
-  double* W = smem + 2 * kNB * P;  // L⁻¹ − Z
-  const double* Lk = t.l + t.c0 + static_cast<int64_t>(t.c0) * ld;
-  double* Sk = t.sig + t.c0 + static_cast<int64_t>(t.c0) * ld;
-  for (int idx = tid; idx < w * w; idx += blockDim.x) {
-    int i = idx % w, j = idx / w;
-    Lm[j * P + i] = i >= j ? Lk[i + static_cast<int64_t>(j) * ld] : 0.0;
-    W[j * P + i] = -Sk[i + static_cast<int64_t>(j) * ld];
-  }
-  __syncthreads();
-  if (tid < w) {
-    const int c = tid;
-    for (int i = 0; i < w; ++i) {
-      double v;
-      if (i < c) {
-        v = 0.0;
-      } else {
-        double s = (i == c) ? 1.0 : 0.0;
-        for (int l = c; l < i; ++l) s -= Lm[l * P + i] * Li[c * P + l];
-        v = s / Lm[i * P + i];
-      }
-      Li[c * P + i] = v;
-    }
-  }
-  __syncthreads();
-  for (int idx = tid; idx < w * w; idx += blockDim.x) {
-    int i = idx % w, j = idx / w;
-    W[j * P + i] += Li[j * P + i];
-  }
-  __syncthreads();
-  for (int idx = tid; idx < w * w; idx += blockDim.x) {
-    int i = idx % w, j = idx / w;
-    if (i < j) continue;
-    double s = 0.0;
-    for (int l = i; l < w; ++l) s += Li[i * P + l] * W[j * P + l];  // (L⁻ᵀ)_{i,l} = Li[l][i]
-    Sk[i + static_cast<int64_t>(j) * ld] = s;
-    Sk[j + static_cast<int64_t>(i) * ld] = s;
-  }
-  // mirror Σ_{P,J} → Σ_{J,P} for the earlier chunks of this supernode
-  const int p = t.wsn - t.c0 - w;
-  for (int idx = tid; idx < p * w; idx += blockDim.x) {
-    int pi = idx % p, j = idx / p;
-    Sk[j + static_cast<int64_t>(w + pi) * ld] = Sk[(w + pi) + static_cast<int64_t>(j) * ld];
-  }
-}
+// (selected-inversion chunk kernels: selinv.cuh)
 
 // var[perm[j]] = Σ_jj
 __global__ void k_extract_diag(SymDev sd, const int32_t* __restrict__ col2sn,

@@ -59,6 +59,7 @@ struct SelChunk {
   int32_t w;         // chunk width
   int32_t wsn;       // supernode width
   int32_t tile;      // TRSM row slab (for the TRSM kernel)
+  const double* rd;  // 1/L_jj of the chunk's first column (factorization pivots)
 };
 
 // One 64-row block of a wide supernode's triangle in the solves (solve_wide.cuh).

@@ -1,0 +1,144 @@
+// Per-chunk dense steps of the supernodal selected inversion (takahashi.hpp
+// recurrences, supernodal form), register resident and barrier free:
+//   k_sel_trsm<W>: Σ_{R,J} = −Y · L_JJ⁻¹ for one 128-row slab, one row per
+//                  thread (x·L = b, right-looking over the columns, j descending);
+//   k_sel_diag<W>: Σ_JJ = L_JJ⁻ᵀ (L_JJ⁻¹ − Z), one column per thread:
+//                  forward solve L x = e_c, subtract z_c, backward solve Lᵀ s = x.
+// W is the chunk width bucket (16/32/64, identity padded). L_JJ is staged once
+// in shared memory and read by broadcast; divisions are correctly rounded
+// (div_rn with the correctly rounded 1/L_jj of the factorization).
+#pragma once
+
+#include "kernels.cuh"
+#include "panel.cuh"
+
+namespace gmrf {
+
+template <int W>
+constexpr int sel_diag_smem_bytes() {
+  return (2 * W * (W + 1) + W) * static_cast<int>(sizeof(double));
+}
+
+template <int W>
+__global__ void __launch_bounds__(kTrsmRows) k_sel_trsm_w(const SelChunk* __restrict__ tasks) {
+  __shared__ __align__(16) double Lr[W * W];  // Lr[j*W + k] = L_jk (row j of L_JJ, k < j)
+  __shared__ double dg[W], rd[W];
+  const SelChunk& t = tasks[blockIdx.x];
+  const int w = t.w, ld = t.ld, tid = threadIdx.x;
+  const double* Lk = t.l + t.c0 + static_cast<int64_t>(t.c0) * ld;
+  for (int idx = tid; idx < W * W; idx += blockDim.x) {
+    const int j = idx / W, k = idx % W;  // consecutive threads: consecutive k (row j)
+    Lr[idx] = (k < j && j < w) ? Lk[j + static_cast<int64_t>(k) * ld] : 0.0;
+  }
+  if (tid < W) {
+    dg[tid] = tid < w ? Lk[tid + static_cast<int64_t>(tid) * ld] : 1.0;
+    rd[tid] = tid < w ? t.rd[tid] : 1.0;
+  }
+  const int nbelow = ld - t.c0 - w;
+  const int r0 = t.tile * kTrsmRows;
+  const int nr = min(kTrsmRows, nbelow - r0);
+  double* B = t.sig + t.c0 + w + r0 + tid + static_cast<int64_t>(t.c0) * ld;
+  const bool act = tid < nr;
+  double b[W];
+#pragma unroll
+  for (int j = 0; j < W; ++j) b[j] = (act && j < w) ? -B[static_cast<int64_t>(j) * ld] : 0.0;
+  __syncthreads();
+#pragma unroll
+  for (int j = W - 1; j >= 0; --j) {
+    const double x = div_rn(b[j], dg[j], rd[j]);
+    b[j] = x;
+    const double* lj = Lr + j * W;
+#pragma unroll
+    for (int k = 0; k + 1 < j; k += 2) {
+      const double2 v = *reinterpret_cast<const double2*>(lj + k);
+      b[k] = fma(-x, v.x, b[k]);
+      b[k + 1] = fma(-x, v.y, b[k + 1]);
+    }
+    if (j & 1) b[j - 1] = fma(-x, lj[j - 1], b[j - 1]);
+  }
+  if (act) {
+#pragma unroll
+    for (int j = 0; j < W; ++j)
+      if (j < w) B[static_cast<int64_t>(j) * ld] = b[j];
+  }
+}
+
+template <int W>
+__global__ void __launch_bounds__(W < 32 ? 32 : W) k_sel_diag_w(const SelChunk* __restrict__ tasks) {
+  extern __shared__ __align__(16) double sm[];
+  constexpr int P = W + 1;
+  double* Lc = sm;          // Lc[i*P + k] = L_ki (column i), k > i
+  double* Lt = sm + W * P;  // Lt[i*P + k] = L_ik (row i),    k < i
+  double* rd = sm + 2 * W * P;
+  const SelChunk& t = tasks[blockIdx.x];
+  const int w = t.w, ld = t.ld, tid = threadIdx.x;
+  const double* Lk = t.l + t.c0 + static_cast<int64_t>(t.c0) * ld;
+  double* Sk = t.sig + t.c0 + static_cast<int64_t>(t.c0) * ld;
+  for (int idx = tid; idx < W * W; idx += blockDim.x) {
+    const int i = idx / W, k = idx % W;
+    const bool in = i < w && k < w;
+    Lc[i * P + k] = (in && k >= i) ? Lk[k + static_cast<int64_t>(i) * ld] : (k == i ? 1.0 : 0.0);
+    Lt[i * P + k] = (in && k <= i) ? Lk[i + static_cast<int64_t>(k) * ld] : (k == i ? 1.0 : 0.0);
+  }
+  if (tid < W) rd[tid] = tid < w ? t.rd[tid] : 1.0;
+  const int c = tid;
+  const bool act = c < w;
+  double x[W];
+#pragma unroll
+  for (int k = 0; k < W; ++k) x[k] = (k == c) ? 1.0 : 0.0;
+  __syncthreads();
+  // L x = e_c
+#pragma unroll
+  for (int i = 0; i < W; ++i) {
+    const double xi = div_rn(x[i], Lc[i * P + i], rd[i]);
+    x[i] = xi;
+#pragma unroll
+    for (int k = i + 1; k < W; ++k) x[k] = fma(-xi, Lc[i * P + k], x[k]);
+  }
+  // x − z_c  (Z = L_{R,J}ᵀ Σ_{R,J}, stored in the Σ diagonal block)
+  if (act) {
+    const double* zc = Sk + static_cast<int64_t>(c) * ld;
+#pragma unroll
+    for (int k = 0; k < W; ++k)
+      if (k < w) x[k] -= zc[k];
+  }
+  // Lᵀ s = x
+#pragma unroll
+  for (int i = W - 1; i >= 0; --i) {
+    const double si = div_rn(x[i], Lt[i * P + i], rd[i]);
+    x[i] = si;
+#pragma unroll
+    for (int k = 0; k < i; ++k) x[k] = fma(-si, Lt[i * P + k], x[k]);
+  }
+  __syncthreads();  // every thread has read its z column before Σ_JJ is overwritten
+  if (act) {
+#pragma unroll
+    for (int i = 0; i < W; ++i)
+      if (i >= c && i < w) {
+        Sk[i + static_cast<int64_t>(c) * ld] = x[i];
+        Sk[c + static_cast<int64_t>(i) * ld] = x[i];
+      }
+  }
+}
+
+// Mirror Σ_{P,J} → Σ_{J,P} (P = the supernode's later columns) for one 64-row
+// tile of P, transposed through shared memory so reads and writes coalesce.
+__global__ void __launch_bounds__(256) k_sel_mirror(const SelChunk* __restrict__ tasks) {
+  __shared__ double T[64][65];
+  const SelChunk& t = tasks[blockIdx.x];
+  const int w = t.w, ld = t.ld, tid = threadIdx.x;
+  const int p = t.wsn - t.c0 - w;
+  const int p0 = t.tile * 64, np = min(64, p - p0);
+  double* Sk = t.sig + t.c0 + static_cast<int64_t>(t.c0) * ld;
+  for (int idx = tid; idx < 64 * w; idx += blockDim.x) {  // read: rows of P contiguous
+    const int i = idx & 63, j = idx >> 6;
+    if (i < np) T[j][i] = Sk[(w + p0 + i) + static_cast<int64_t>(j) * ld];
+  }
+  __syncthreads();
+  for (int idx = tid; idx < 64 * w; idx += blockDim.x) {  // write: chunk columns contiguous
+    const int j = idx % w, i = idx / w;
+    if (i < np) Sk[j + static_cast<int64_t>(w + p0 + i) * ld] = T[j][i];
+  }
+}
+
+}  // namespace gmrf
