@@ -70,18 +70,38 @@ __device__ __forceinline__ void load_operand(double (*dst)[kPad], const double* 
   }
 }
 
-__global__ void __launch_bounds__(128) k_gemm_tiles(const GemmTask* __restrict__ tasks) {
+// The accumulator starts from beta*C (issued with the first operand loads, so
+// the C round trip overlaps them instead of trailing the MMA loop) and alpha is
+// folded into the A fragments (alpha = ±1 in every plan: exact).
+__global__ void __launch_bounds__(128, 4) k_gemm_tiles(const GemmTask* __restrict__ tasks) {
   __shared__ __align__(16) double As[2][kKC][kPad];
   __shared__ __align__(16) double Bs[2][kKC][kPad];
   const GemmTask& t = tasks[blockIdx.x];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp & 1, wn = warp >> 1;
   const int m = t.m, n = t.n;
+  const double alpha = t.alpha, beta = t.beta;
+  double* C = t.c;
+  const int64_t ldc = t.ldc;
   double acc[4][4][2];
+  if (beta == 0.0) {
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+      for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int row = wm * 32 + i * 8 + (lane >> 2);
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int col = wn * 32 + j * 8 + (lane & 3) * 2 + e;
+          acc[i][j][e] = (row < m && col < n) ? beta * C[row + col * ldc] : 0.0;
+        }
+    }
+  }
 
   for (int seg = 0; seg < 2; ++seg) {
     const int K = t.k[seg];
@@ -111,7 +131,8 @@ __global__ void __launch_bounds__(128) k_gemm_tiles(const GemmTask* __restrict__
       for (int kk = 0; kk < kKC; kk += 4) {
         double af[4], bf[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) af[i] = As[buf][kk + (lane & 3)][wm * 32 + i * 8 + (lane >> 2)];
+        for (int i = 0; i < 4; ++i)
+          af[i] = alpha * As[buf][kk + (lane & 3)][wm * 32 + i * 8 + (lane >> 2)];
 #pragma unroll
         for (int j = 0; j < 4; ++j) bf[j] = Bs[buf][kk + (lane & 3)][wn * 32 + j * 8 + (lane >> 2)];
 #pragma unroll
@@ -122,9 +143,6 @@ __global__ void __launch_bounds__(128) k_gemm_tiles(const GemmTask* __restrict__
       __syncthreads();
     }
   }
-  const double alpha = t.alpha, beta = t.beta;
-  double* C = t.c;
-  const int64_t ldc = t.ldc;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int row = wm * 32 + i * 8 + (lane >> 2);
@@ -134,10 +152,7 @@ __global__ void __launch_bounds__(128) k_gemm_tiles(const GemmTask* __restrict__
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int col = wn * 32 + j * 8 + (lane & 3) * 2 + e;
-        if (col < n) {
-          double* p = C + row + col * ldc;
-          *p = beta == 0.0 ? alpha * acc[i][j][e] : beta * *p + alpha * acc[i][j][e];
-        }
+        if (col < n) C[row + col * ldc] = acc[i][j][e];
       }
   }
 }
