@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <string>
 
 #include "kernels.cu"  // single translation unit for all device code
@@ -40,6 +41,11 @@ void set_smem_attrs() {
 }
 
 inline int nchunks(int w) { return (w + kNB - 1) / kNB; }
+
+// Tile GEMM launch: one CTA per 64×64 output tile.
+void launch_gemm(const GemmTask* tasks, int64_t n, cudaStream_t st) {
+  k_gemm_tiles<<<static_cast<unsigned>(n), 128, 0, st>>>(tasks);
+}
 constexpr unsigned kRowsMaxCtas = 148;  // one CTA per SM (k_panel_rows uses ~254 registers)
 
 template <int NR>
@@ -177,10 +183,29 @@ DeviceFactor::DeviceFactor(std::shared_ptr<const Symbolic> sym, cudaStream_t str
     lvl_bytes_[s.sn_level[k]] += 8.0 * (w * rows - w * (w - 1.0) / 2.0) + 4.0 * rows;
   }
   build_factor_plan();
+  {  // lookahead streams: the critical chain at high priority, the bulk updates low
+    int lo = 0, hi = 0;
+    cuda_check(cudaDeviceGetStreamPriorityRange(&lo, &hi), "priorities");
+    cuda_check(cudaStreamCreateWithPriority(&main_, cudaStreamNonBlocking, hi), "main stream");
+    cuda_check(cudaStreamCreateWithPriority(&aux_, cudaStreamNonBlocking, lo), "aux stream");
+    cuda_check(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming), "event");
+  }
+  ev_panel_.resize(flev_.size());
+  ev_rest_.resize(flev_.size());
+  for (size_t l = 0; l < flev_.size(); ++l) {
+    cuda_check(cudaEventCreateWithFlags(&ev_panel_[l], cudaEventDisableTiming), "event");
+    cuda_check(cudaEventCreateWithFlags(&ev_rest_[l], cudaEventDisableTiming), "event");
+  }
   cuda_check(cudaStreamSynchronize(stream_), "factor setup");
 }
 
-DeviceFactor::~DeviceFactor() = default;
+DeviceFactor::~DeviceFactor() {
+  for (cudaEvent_t e : ev_panel_) cudaEventDestroy(e);
+  for (cudaEvent_t e : ev_rest_) cudaEventDestroy(e);
+  if (ev_fork_) cudaEventDestroy(ev_fork_);
+  if (aux_) cudaStreamDestroy(aux_);
+  if (main_) cudaStreamDestroy(main_);
+}
 
 SymDev DeviceFactor::symdev() const {
   SymDev d;
@@ -226,11 +251,14 @@ void DeviceFactor::build_factor_plan() {
   chunk_levels(s, lvl0, nlev, kSmallRows);
   std::vector<std::vector<ColTask>> ea(nlev);
   std::vector<std::vector<PanelTask>> pan(nlev), po(nlev);
-  std::vector<std::vector<GemmTask>> gm(nlev);
+  // GEMM tasks per level: gm = the update of the chunk's NEXT column block (on
+  // the critical chain), gr = the rest of the trailing update + the U SYRK
+  // (overlapped with the next level's panel on the second stream)
+  std::vector<std::vector<GemmTask>> gm(nlev), gr(nlev);
   std::vector<std::vector<int32_t>> sm[3];
   for (auto& v : sm) v.resize(nlev);
   std::vector<double> ea_b(nlev, 0.0), po_f(nlev, 0.0), tr_f(nlev, 0.0), gm_f(nlev, 0.0),
-      sm_f(nlev, 0.0);
+      gr_f(nlev, 0.0), sm_f(nlev, 0.0);
   double* L = L_.p;
   double* U = U_.p;
   for (int k = 0; k < s.ns; ++k) {
@@ -281,8 +309,13 @@ void DeviceFactor::build_factor_plan() {
           g.flags = 2;  // B transposed
           g.alpha = -1.0;
           g.beta = 1.0;
-          gm[lv].push_back(g);
-          gm_f[lv] += tile_flops(g, ib == jb);
+          if (jb == c0 + wk) {
+            gm[lv].push_back(g);
+            gm_f[lv] += tile_flops(g, ib == jb);
+          } else {
+            gr[lv].push_back(g);
+            gr_f[lv] += tile_flops(g, ib == jb);
+          }
         }
       // last chunk: full-width SYRK into the update matrix, U -= L21 L21ᵀ
       if (c == nch - 1 && r > 0)
@@ -301,8 +334,8 @@ void DeviceFactor::build_factor_plan() {
             g.flags = 2;
             g.alpha = -1.0;
             g.beta = 1.0;
-            gm[lv].push_back(g);
-            gm_f[lv] += tile_flops(g, ib == jb);
+            gr[lv].push_back(g);
+            gr_f[lv] += tile_flops(g, ib == jb);
           }
     }
   }
@@ -311,9 +344,14 @@ void DeviceFactor::build_factor_plan() {
   std::vector<GemmTask> gmf;
   std::vector<ReduceTask> rdf;
   std::vector<int32_t> smf;
-  int64_t maxp = 1;
-  for (int l = 0; l < nlev; ++l) maxp = std::max(maxp, split_k_parts(gm[l]));
-  parts_.alloc(maxp * kTile * kTile);  // one level's split-K partial tiles at a time
+  int64_t maxp = 1, maxr = 1;
+  for (int l = 0; l < nlev; ++l) {
+    maxp = std::max(maxp, split_k_parts(gm[l]));
+    maxr = std::max(maxr, split_k_parts(gr[l]));
+  }
+  // one level's split-K partial tiles at a time, per stream
+  parts_.alloc(maxp * kTile * kTile);
+  rparts_.alloc(maxr * kTile * kTile);
   flev_.assign(nlev, {});
   for (int l = 0; l < nlev; ++l) {
     flev_[l] = {static_cast<int64_t>(eaf.size()), static_cast<int64_t>(ea[l].size()),
@@ -331,6 +369,16 @@ void DeviceFactor::build_factor_plan() {
       flev_[l].rd0 = static_cast<int64_t>(rdf.size());
       flev_[l].rdn = static_cast<int64_t>(rs.size());
       rdf.insert(rdf.end(), rs.begin(), rs.end());
+      gs.clear();
+      rs.clear();
+      split_k_level(gr[l], gs, rs, rparts_.p);
+      flev_[l].gr0 = static_cast<int64_t>(gmf.size());
+      flev_[l].grn = static_cast<int64_t>(gs.size());
+      gmf.insert(gmf.end(), gs.begin(), gs.end());
+      flev_[l].rr0 = static_cast<int64_t>(rdf.size());
+      flev_[l].rrn = static_cast<int64_t>(rs.size());
+      rdf.insert(rdf.end(), rs.begin(), rs.end());
+      flev_[l].gr_flops = gr_f[l];
     }
     pof.insert(pof.end(), po[l].begin(), po[l].end());
     eaf.insert(eaf.end(), ea[l].begin(), ea[l].end());
@@ -540,27 +588,44 @@ int32_t DeviceFactor::factor_panels() {
   const Symbolic& s = *sym_;
   const SymDev sd = symdev();
   KernelProfiler& pf = *prof_;
+  const bool la = lookahead_ && !pf.on;
+  cudaStream_t sa = la ? main_ : stream_;  // critical chain
+  cudaStream_t sb = la ? aux_ : stream_;   // bulk trailing updates
+  if (la) {
+    cuda_check(cudaEventRecord(ev_fork_, stream_), "record");
+    cuda_check(cudaStreamWaitEvent(sa, ev_fork_, 0), "wait");
+  }
   for (size_t li = 0; li < flev_.size(); ++li) {
     const FLevel& lv = flev_[li];
     const int lvl = static_cast<int>(li);
+    // Lookahead (two streams): sa runs assembly → panel → next-block
+    // update; aux_ runs the rest of the level's trailing update and the U
+    // SYRKs, concurrently with the next level's panel. Ordering:
+    //   rest(l)               after panel(l)           (reads the chunk's L)
+    //   assembly(l)           after rest(l-1)          (children's U SYRKs)
+    //   next(l)               after rest(l-1)          (same tiles, k order)
+    // Profiling runs keep one stream so every launch is attributed to its class.
+    const bool assembles = lv.ean > 0 || lv.smn[0] + lv.smn[1] + lv.smn[2] > 0;
+    if (la && li > 0 && assembles)
+      cuda_check(cudaStreamWaitEvent(sa, ev_rest_[li - 1], 0), "wait");
     if (lv.smn[0] + lv.smn[1] + lv.smn[2] > 0) {
-      pf.run(stream_, pf.tag("factor.small_front", lvl), lv.sm_flops, 0.0, [&] {
+      pf.run(sa, pf.tag("factor.small_front", lvl), lv.sm_flops, 0.0, [&] {
         if (lv.smn[0])
           k_small_front<32><<<static_cast<unsigned>(lv.smn[0]), 256, small_front_smem_bytes<32>(),
-                              stream_>>>(small_.p + lv.sm0[0], sd, L_.p, U_.p, status_.p, rdiag_.p);
+                              sa>>>(small_.p + lv.sm0[0], sd, L_.p, U_.p, status_.p, rdiag_.p);
         if (lv.smn[1])
           k_small_front<64><<<static_cast<unsigned>(lv.smn[1]), 256, small_front_smem_bytes<64>(),
-                              stream_>>>(small_.p + lv.sm0[1], sd, L_.p, U_.p, status_.p, rdiag_.p);
+                              sa>>>(small_.p + lv.sm0[1], sd, L_.p, U_.p, status_.p, rdiag_.p);
         if (lv.smn[2])
           k_small_front<96><<<static_cast<unsigned>(lv.smn[2]), 256, small_front_smem_bytes<96>(),
-                              stream_>>>(small_.p + lv.sm0[2], sd, L_.p, U_.p, status_.p, rdiag_.p);
+                              sa>>>(small_.p + lv.sm0[2], sd, L_.p, U_.p, status_.p, rdiag_.p);
       });
       launches_numeric_ += (lv.smn[0] > 0) + (lv.smn[1] > 0) + (lv.smn[2] > 0);
     }
     if (lv.ean) {
       int blocks = static_cast<int>((lv.ean * 32 + 255) / 256);
-      pf.run(stream_, pf.tag("factor.extend_add", lvl), 0.0, lv.ea_bytes, [&] {
-        k_extend_add<<<blocks, 256, 0, stream_>>>(ea_.p + lv.ea0, static_cast<int>(lv.ean), sd,
+      pf.run(sa, pf.tag("factor.extend_add", lvl), 0.0, lv.ea_bytes, [&] {
+        k_extend_add<<<blocks, 256, 0, sa>>>(ea_.p + lv.ea0, static_cast<int>(lv.ean), sd,
                                                  L_.p, U_.p);
       });
       ++launches_numeric_;
@@ -569,46 +634,64 @@ int32_t DeviceFactor::factor_panels() {
       // latency-bound levels (one wave) use the row-per-thread sweep; levels
       // with several waves of chunk slabs keep the blocked smem kernel, whose
       // CTAs are small enough to co-reside 4-5 per SM
-      pf.run(stream_, pf.tag("factor.potrf_trsm", lvl), lv.po_flops + lv.tr_flops, 0.0, [&] {
+      pf.run(sa, pf.tag("factor.potrf_trsm", lvl), lv.po_flops + lv.tr_flops, 0.0, [&] {
         if (lv.pbn[0]) {
           const unsigned g = static_cast<unsigned>(lv.pbn[0]);
           if (g <= kRowsMaxCtas)
-            k_panel_rows<16, kTrsmRows><<<g, panel_rows_threads<16, kTrsmRows>(), 0, stream_>>>(
+            k_panel_rows<16, kTrsmRows><<<g, panel_rows_threads<16, kTrsmRows>(), 0, sa>>>(
                 pan_.p + lv.pb0[0], status_.p, diag_.p);
           else
-            k_potrf_trsm<16><<<g, 128, panel_smem_bytes<16>(), stream_>>>(pan_.p + lv.pb0[0],
+            k_potrf_trsm<16><<<g, 128, panel_smem_bytes<16>(), sa>>>(pan_.p + lv.pb0[0],
                                                                           status_.p, diag_.p);
         }
         if (lv.pbn[1]) {
           const unsigned g = static_cast<unsigned>(lv.pbn[1]);
           if (g <= kRowsMaxCtas)
-            k_panel_rows<32, kTrsmRows><<<g, panel_rows_threads<32, kTrsmRows>(), 0, stream_>>>(
+            k_panel_rows<32, kTrsmRows><<<g, panel_rows_threads<32, kTrsmRows>(), 0, sa>>>(
                 pan_.p + lv.pb0[1], status_.p, diag_.p);
           else
-            k_potrf_trsm<32><<<g, 128, panel_smem_bytes<32>(), stream_>>>(pan_.p + lv.pb0[1],
+            k_potrf_trsm<32><<<g, 128, panel_smem_bytes<32>(), sa>>>(pan_.p + lv.pb0[1],
                                                                           status_.p, diag_.p);
         }
         if (lv.pbn[2]) {
           const unsigned g = static_cast<unsigned>(lv.pbn[2]);
           if (g <= kRowsMaxCtas)
-            k_panel_rows<64, kTrsmRows><<<g, panel_rows_threads<64, kTrsmRows>(), 0, stream_>>>(
+            k_panel_rows<64, kTrsmRows><<<g, panel_rows_threads<64, kTrsmRows>(), 0, sa>>>(
                 pan_.p + lv.pb0[2], status_.p, diag_.p);
           else
-            k_potrf_trsm<64><<<g, 128, panel_smem_bytes<64>(), stream_>>>(pan_.p + lv.pb0[2],
+            k_potrf_trsm<64><<<g, 128, panel_smem_bytes<64>(), sa>>>(pan_.p + lv.pb0[2],
                                                                           status_.p, diag_.p);
         }
       });
       launches_numeric_ += (lv.pbn[0] > 0) + (lv.pbn[1] > 0) + (lv.pbn[2] > 0);
     }
+    if (la) cuda_check(cudaEventRecord(ev_panel_[li], sa), "record");
+    if (la && li > 0) cuda_check(cudaStreamWaitEvent(sa, ev_rest_[li - 1], 0), "wait");
     if (lv.gmn) {
-      pf.run(stream_, pf.tag("factor.gemm_dmma", lvl), lv.gm_flops, 0.0, [&] {
-        k_gemm_tiles<<<static_cast<unsigned>(lv.gmn), 128, 0, stream_>>>(gemm_.p + lv.gm0);
+      pf.run(sa, pf.tag("factor.gemm_dmma", lvl), lv.gm_flops, 0.0, [&] {
+        launch_gemm(gemm_.p + lv.gm0, lv.gmn, sa);
         if (lv.rdn)
-          k_reduce_parts<<<static_cast<unsigned>(lv.rdn), 256, 0, stream_>>>(red_.p + lv.rd0,
+          k_reduce_parts<<<static_cast<unsigned>(lv.rdn), 256, 0, sa>>>(red_.p + lv.rd0,
                                                                              parts_.p);
       });
       launches_numeric_ += 1 + (lv.rdn > 0);
     }
+    if (la) cuda_check(cudaStreamWaitEvent(sb, ev_panel_[li], 0), "wait");
+    if (lv.grn) {
+      pf.run(sb, pf.tag("factor.gemm_dmma", lvl), lv.gr_flops, 0.0, [&] {
+        launch_gemm(gemm_.p + lv.gr0, lv.grn, sb);
+        if (lv.rrn)
+          k_reduce_parts<<<static_cast<unsigned>(lv.rrn), 256, 0, sb>>>(red_.p + lv.rr0,
+                                                                        rparts_.p);
+      });
+      launches_numeric_ += 1 + (lv.rrn > 0);
+    }
+    if (la) cuda_check(cudaEventRecord(ev_rest_[li], sb), "record");
+  }
+  if (la) {  // join: the caller's stream continues after both chains
+    if (!flev_.empty()) cuda_check(cudaStreamWaitEvent(sa, ev_rest_[flev_.size() - 1], 0), "wait");
+    cuda_check(cudaEventRecord(ev_fork_, sa), "record");
+    cuda_check(cudaStreamWaitEvent(stream_, ev_fork_, 0), "wait");
   }
   if (po_.n) {
     pf.run(stream_, "factor.diag_writeback", 0.0, 16.0 * s.n * kNB / 2.0, [&] {
@@ -789,7 +872,7 @@ void DeviceFactor::selinv(double* diag_out, bool on_device) {
     }
     if (e.yn) {
       pf.run(stream_, pf.tag("selinv.gemm_dmma", l), e.y_flops, 0.0, [&] {
-        k_gemm_tiles<<<static_cast<unsigned>(e.yn), 128, 0, stream_>>>(sgemm_.p + e.y0);
+        launch_gemm(sgemm_.p + e.y0, e.yn, stream_);
         if (e.yrn)
           k_reduce_parts<<<static_cast<unsigned>(e.yrn), 256, 0, stream_>>>(sred_.p + e.yr0,
                                                                             sparts_.p);
@@ -812,7 +895,7 @@ void DeviceFactor::selinv(double* diag_out, bool on_device) {
     }
     if (e.zn) {
       pf.run(stream_, pf.tag("selinv.gemm_dmma", l), e.z_flops, 0.0, [&] {
-        k_gemm_tiles<<<static_cast<unsigned>(e.zn), 128, 0, stream_>>>(sgemm_.p + e.z0);
+        launch_gemm(sgemm_.p + e.z0, e.zn, stream_);
         if (e.zrn)
           k_reduce_parts<<<static_cast<unsigned>(e.zrn), 256, 0, stream_>>>(sred_.p + e.zr0,
                                                                             sparts_.p);

@@ -120,6 +120,8 @@ class DeviceFactor {
     int64_t rd0, rdn;        // split-K reductions of the level's GEMM tiles
     int64_t sm0[3], smn[3];  // small fronts (rows <= 32 / 64 / 96), one CTA each
     double sm_flops;
+    int64_t gr0, grn, rr0, rrn;  // rest of the trailing update + U SYRK (second stream)
+    double gr_flops;
   };
   DevBuf<int32_t> small_;
   std::vector<FLevel> flev_;
@@ -135,7 +137,12 @@ class DeviceFactor {
     int64_t mi0, min_;                       // Σ_{P,J} → Σ_{J,P} mirror tiles
   };
   DevBuf<ReduceTask> red_, sred_;
-  DevBuf<double> parts_, sparts_;  // split-K partial tiles
+  DevBuf<double> parts_, rparts_, sparts_;  // split-K partial tiles
+  // lookahead: the rest-of-update GEMMs run on aux_ (events order the levels)
+  cudaStream_t main_ = nullptr, aux_ = nullptr;
+  cudaEvent_t ev_fork_ = nullptr;
+  std::vector<cudaEvent_t> ev_panel_, ev_rest_;
+  bool lookahead_ = true;
   std::vector<double> lvl_bytes_;  // solve: L panel + row-index bytes per tree level
   KernelProfiler own_prof_;
   KernelProfiler* prof_ = &own_prof_;
