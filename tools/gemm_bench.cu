@@ -1,0 +1,121 @@
+// Microbenchmark of the DMMA tile GEMM (kernels.cu) on synthetic task lists
+// shaped like the factorization's launches:
+//   update64 : 64x64 tiles, K=64, lower trapezoid of a 2048-wide trailing block
+//   small    : 18k tiles 48x48, K=32 (bottom-of-tree SYRKs)
+//   syrk1k   : 64x64 tiles, K=1024, lower triangle of a 1024x1024 update
+//   nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a \
+//        -I paper_2503_08343_b200/csrc tools/gemm_bench.cu -o tools/gemm_bench
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <vector>
+
+#include "kernels.cu"
+
+using namespace gmrf;
+
+static double run(const char* name, std::vector<GemmTask>& tasks, double flops) {
+  GemmTask* dt;
+  cudaMalloc(&dt, tasks.size() * sizeof(GemmTask));
+  cudaMemcpy(dt, tasks.data(), tasks.size() * sizeof(GemmTask), cudaMemcpyHostToDevice);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  float best = 1e9f;
+  for (int rep = 0; rep < 8; ++rep) {
+    cudaEventRecord(e0);
+    k_gemm_tiles<<<static_cast<unsigned>(tasks.size()), 128>>>(dt);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (rep > 0 && ms < best) best = ms;
+  }
+  printf("%-9s %6zu tiles  %8.1f us  %6.2f TF/s  (%s)\n", name, tasks.size(), best * 1e3,
+         flops / (best * 1e-3) / 1e12, cudaGetErrorString(cudaGetLastError()));
+  cudaFree(dt);
+  return best;
+}
+
+int main() {
+  const int64_t N = 4096;
+  double* buf;
+  cudaMalloc(&buf, N * N * sizeof(double) * 3);
+  cudaMemset(buf, 0, N * N * sizeof(double) * 3);
+  double* A = buf;
+  double* C = buf + N * N;
+  {  // update64: trailing block 2048 wide, rows 2048, K = 64 (A panel = 2048 x 64)
+    std::vector<GemmTask> t;
+    double fl = 0;
+    const int w = 2048;
+    for (int jb = 0; jb < w; jb += 64)
+      for (int ib = jb; ib < w; ib += 64) {
+        GemmTask g{};
+        g.c = C + ib + static_cast<int64_t>(jb) * w;
+        g.ldc = w;
+        g.m = 64;
+        g.n = 64;
+        g.a[0] = A + ib;
+        g.lda[0] = w;
+        g.b[0] = A + jb;
+        g.ldb[0] = w;
+        g.k[0] = 64;
+        g.flags = 2;
+        g.alpha = -1.0;
+        g.beta = 1.0;
+        t.push_back(g);
+        fl += 2.0 * 64 * 64 * 64;
+      }
+    run("update64", t, fl);
+    t.resize(500);
+    run("upd64x500", t, 2.0 * 64 * 64 * 64 * 500);
+  }
+  {  // small: 18k independent 48x48 K=32 tiles spread over the buffer
+    std::vector<GemmTask> t;
+    double fl = 0;
+    for (int q = 0; q < 18000; ++q) {
+      GemmTask g{};
+      const int64_t off = (static_cast<int64_t>(q) * 4099) % (N * N - 64 * 200);
+      g.c = C + off;
+      g.ldc = 97;
+      g.m = 48;
+      g.n = 48;
+      g.a[0] = A + off;
+      g.lda[0] = 97;
+      g.b[0] = A + off + 50;
+      g.ldb[0] = 97;
+      g.k[0] = 32;
+      g.flags = 2;
+      g.alpha = -1.0;
+      g.beta = 1.0;
+      t.push_back(g);
+      fl += 2.0 * 48 * 48 * 32;
+    }
+    run("small", t, fl);
+  }
+  {  // syrk1k: U (1024 x 1024 lower) -= L_R L_Rᵀ, K = 1024
+    std::vector<GemmTask> t;
+    double fl = 0;
+    const int r = 1024;
+    for (int jb = 0; jb < r; jb += 64)
+      for (int ib = jb; ib < r; ib += 64) {
+        GemmTask g{};
+        g.c = C + ib + static_cast<int64_t>(jb) * r;
+        g.ldc = r;
+        g.m = 64;
+        g.n = 64;
+        g.a[0] = A + ib;
+        g.lda[0] = 2048;
+        g.b[0] = A + jb;
+        g.ldb[0] = 2048;
+        g.k[0] = 1024;
+        g.flags = 2;
+        g.alpha = -1.0;
+        g.beta = 1.0;
+        t.push_back(g);
+        fl += 2.0 * 64 * 64 * 1024;
+      }
+    run("syrk1k", t, fl);
+  }
+  return 0;
+}
