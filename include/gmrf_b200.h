@@ -149,13 +149,16 @@ typedef struct {
   double eps;              /* Dirichlet slack variance, embed_dirichlet(eps) */
   int32_t dirichlet;       /* 1: homogeneous Dirichlet at both ends */
   double ic_noise_prec;    /* Λ of the t=0 observation */
-  int32_t residual;        /* 0: linear posterior, 1: Burgers weak form (implicit Euler) */
+  int32_t residual;        /* 0: linear posterior, 1: Burgers weak form (implicit Euler, 1-D),
+                              2: Allen-Cahn weak form (implicit Euler, lumped cubic, 1-D/2-D) */
   double pde_noise_prec;   /* Λ_pde of the residual rows */
   int32_t gn_max_iters;    /* GaussNewtonConfig (gauss_newton.hpp:19-24) */
   double gn_decrement_tol;
   double gn_armijo_c;
   double gn_shrink;
   int32_t gn_max_backtracks;
+  int32_t dim;             /* 1: interval [xa, xb] with n_el elements; 2: unit square with
+                              n_el × n_el cells split into triangles (mesh.hpp:108-149) */
 } gmrf_spacetime_config_t;
 
 typedef struct {

@@ -236,6 +236,166 @@ Bundle* build_spatiotemporal(const double* p, int np) {
   return b;
 }
 
+// ----- C5: Allen-Cahn space-time residual (absent from the reference) --------
+// CPU restatement written for this oracle, following the layout of
+// burgers_fem_residual (solver/residual.hpp:244-382: rows = steps × kept test
+// DoFs, weak (u⁺−u)/Δt time term with the folded mass, implicit Euler) and the
+// lumped reaction of nonlinear_elliptic_residual (residual.hpp:431-441,478-482),
+// with the Allen-Cahn sign: u_t = ε²Δu − (u³ − u), so per step s
+//   r_s = M(u_{s+1} − u_s)/Δt + ε² K u_{s+1} + M̃ (u_{s+1}³ − u_{s+1}),
+//   J_s = [−M/Δt | M/Δt + ε² K + diag(M̃ (3u² − 1))]   (slices s, s+1).
+// C5 has no constraints (natural BC), so every DoF is a kept row.
+solver::NonlinearResidual allen_cahn_residual(const fem::FeSpace& space, const Vector& t_grid,
+                                              Real eps2, Real noise_prec) {
+  struct Data {
+    SparseMatrixCSC mass, stiff;
+    Vector lumped, t_grid;
+    Index n;
+    Real eps2;
+  };
+  auto d = std::make_shared<Data>();
+  d->mass = fem::assemble_mass(space);
+  d->stiff = fem::assemble_stiffness(space, fem::laplace_operator(1.0));
+  d->lumped = fem::lumped_mass_vector(d->mass);
+  d->t_grid = t_grid;
+  d->n = space.n_dofs();
+  d->eps2 = eps2;
+  const Index n_steps = static_cast<Index>(t_grid.size()) - 1;
+  solver::NonlinearResidual res;
+  res.input_dim = static_cast<Index>(t_grid.size()) * d->n;
+  res.output_dim = n_steps * d->n;
+  res.noise_precision.assign(res.output_dim, noise_prec);
+  res.target.assign(res.output_dim, 0.0);
+  res.eval = [d](const Vector& u) {
+    const Index n = d->n, ns = static_cast<Index>(d->t_grid.size()) - 1;
+    Vector r(ns * n, 0.0);
+    for (Index s = 0; s < ns; ++s) {
+      const Real dt = d->t_grid[s + 1] - d->t_grid[s];
+      Vector du(n), u1(u.begin() + (s + 1) * n, u.begin() + (s + 2) * n);
+      for (Index i = 0; i < n; ++i) du[i] = u[(s + 1) * n + i] - u[s * n + i];
+      Vector mdu = matvec(d->mass, du), ku = matvec(d->stiff, u1);
+      for (Index i = 0; i < n; ++i) {
+        const Real v = u1[i];
+        r[s * n + i] = mdu[i] / dt + (d->eps2 * ku[i] + d->lumped[i] * (v * v * v - v));
+      }
+    }
+    return r;
+  };
+  res.jacobian = [d](const Vector& u) {
+    const Index n = d->n, ns = static_cast<Index>(d->t_grid.size()) - 1;
+    std::vector<Triplet> t;
+    for (Index s = 0; s < ns; ++s) {
+      const Real dt = d->t_grid[s + 1] - d->t_grid[s];
+      for (Index j = 0; j < n; ++j) {
+        for (Index p = d->mass.col_ptr[j]; p < d->mass.col_ptr[j + 1]; ++p)
+          t.push_back({s * n + d->mass.row_idx[p], s * n + j, -d->mass.values[p] / dt});
+        for (Index p = d->mass.col_ptr[j]; p < d->mass.col_ptr[j + 1]; ++p)
+          t.push_back({s * n + d->mass.row_idx[p], (s + 1) * n + j, d->mass.values[p] / dt});
+        for (Index p = d->stiff.col_ptr[j]; p < d->stiff.col_ptr[j + 1]; ++p)
+          t.push_back({s * n + d->stiff.row_idx[p], (s + 1) * n + j, d->eps2 * d->stiff.values[p]});
+        const Real v = u[(s + 1) * n + j];
+        t.push_back({s * n + j, (s + 1) * n + j, d->lumped[j] * (3.0 * v * v - 1.0)});
+      }
+    }
+    return csc_from_triplets(ns * n, static_cast<Index>(d->t_grid.size()) * n, std::move(t));
+  };
+  return res;
+}
+
+// ----- C5-shaped space-time Allen-Cahn GN-Laplace on the unit square ----------
+// p: [n_per_dim, n_t, t_end, eps2, noise_kappa, noise_alpha, noise_tau,
+//     init_kappa, init_alpha, init_tau, tau, ic_noise_prec, ic_seed,
+//     pde_noise_prec, gn_max_iters, do_variance, do_gn, fd_check]
+Bundle* build_allen_cahn(const double* p, int np) {
+  (void)np;
+  const int npd = static_cast<int>(p[0]);
+  const int n_t = static_cast<int>(p[1]);
+  const double t_end = p[2], eps2 = p[3];
+  auto* b = new Bundle();
+  fem::FeSpace space(fem::build_unit_square_mesh(npd), 1);
+  fem::ConstraintSet cs;  // natural boundary conditions
+  Vector t_grid(n_t);
+  for (int i = 0; i < n_t; ++i) t_grid[i] = t_end * i / static_cast<double>(n_t - 1);
+  priors::SpatiotemporalSpec st;
+  st.t_grid = t_grid;
+  st.spatial_op = fem::laplace_operator(eps2);
+  st.noise_spec = {p[4], static_cast<int>(p[5]), p[6]};
+  st.initial_spec = {p[7], static_cast<int>(p[8]), p[9]};
+  st.tau = p[10];
+  double t0 = now_s();
+  auto [stp, flat] = priors::spatiotemporal_prior(space, st, cs);
+  b->scalars["t_prior"] = now_s() - t0;
+  b->mats["Q_prior"] = flat.precision();
+  b->mats["S_prior"] = flat.sqrt();
+  const int n = space.n_dofs();
+  // IC draw: u0_d = −0.1 + 0.2·uniform in DoF order
+  Rng rng(static_cast<std::uint64_t>(p[12]));
+  Vector u0(n);
+  for (int d = 0; d < n; ++d) u0[d] = -0.1 + 0.2 * rng.uniform();
+  b->vecs["u0"] = u0;
+  std::vector<Triplet> ic;  // P1 nodes = DoFs: point evaluation at the nodes
+  for (int d = 0; d < n; ++d) ic.push_back({d, d, 1.0});
+  solver::LinearInformationOperator ic_op;
+  ic_op.A = csc_from_triplets(n, n_t * n, std::move(ic));
+  ic_op.b = u0;
+  ic_op.noise_precision.assign(n, p[11]);
+  t0 = now_s();
+  Gmrf cond = solver::condition_on(flat, ic_op);
+  b->scalars["t_condition"] = now_s() - t0;
+  b->mats["Q_cond"] = cond.precision();
+  b->mats["S_cond"] = cond.sqrt();
+  b->vecs["mean_cond"] = cond.mean();
+  Gmrf post = cond;
+  auto res = allen_cahn_residual(space, t_grid, eps2, p[13]);
+  b->mats["J_at_mean_cond"] = res.jacobian(cond.mean());
+  b->vecs["f_at_mean_cond"] = res.eval(cond.mean());
+  if (p[17] != 0.0) {  // finite-difference check of the Jacobian (acceptance.cpp:503-608 pattern)
+    Vector x = cond.mean();
+    for (std::size_t i = 0; i < x.size(); ++i) x[i] += 0.3 * std::sin(0.37 * static_cast<double>(i));
+    SparseMatrixCSC jac = res.jacobian(x);
+    Vector f0 = res.eval(x);
+    Rng drng(77);
+    Vector dir(x.size());
+    for (auto& v : dir) v = drng.normal();
+    const double hstep = 1e-6;
+    Vector xp(x), xm(x);
+    for (std::size_t i = 0; i < x.size(); ++i) {
+      xp[i] += hstep * dir[i];
+      xm[i] -= hstep * dir[i];
+    }
+    Vector fp = res.eval(xp), fm = res.eval(xm), jd = matvec(jac, dir);
+    double num = 0, den = 0;
+    for (std::size_t i = 0; i < f0.size(); ++i) {
+      const double fd = (fp[i] - fm[i]) / (2 * hstep);
+      num = std::max(num, std::abs(fd - jd[i]));
+      den = std::max(den, std::abs(jd[i]));
+    }
+    b->scalars["fd_rel_err"] = num / std::max(den, 1e-300);
+  }
+  if (p[16] != 0.0) {
+    solver::GaussNewtonConfig cfg;
+    cfg.max_iters = static_cast<Index>(p[14]);
+    cfg.decrement_tol = 1e-5;
+    t0 = now_s();
+    auto gn = solver::gauss_newton(cond, res, cond.mean(), cfg);
+    b->scalars["t_gn"] = now_s() - t0;
+    put_trace(*b, gn.trace);
+    b->vecs["mode"] = gn.mode;
+    b->scalars["gn_converged"] = gn.converged ? 1.0 : 0.0;
+    t0 = now_s();
+    post = solver::laplace_posterior(cond, res, gn.mode);
+    b->scalars["t_laplace_build"] = now_s() - t0;
+    b->mats["Q_la"] = post.precision();
+  }
+  b->vecs["mean_post"] = post.mean();
+  if (p[15] != 0.0) {
+    t0 = now_s();
+    b->vecs["var_post"] = variance_takahashi(post);
+    b->scalars["t_variance"] = now_s() - t0;
+  }
+  return b;
+}
+
 }  // namespace
 
 extern "C" {
@@ -249,6 +409,7 @@ void* ref_build(const char* kind, const double* p, int np) {
     if (k == "matern1d") return build_matern(1, p, np);
     if (k == "matern2d") return build_matern(2, p, np);
     if (k == "spatiotemporal") return build_spatiotemporal(p, np);
+    if (k == "allen_cahn") return build_allen_cahn(p, np);
     if (k == "corpus") {
       // p: [count, seed]; matrices "Q0".."Q{count-1}"
       auto corpus = oracle::spd_corpus(static_cast<int>(p[0]), static_cast<std::uint64_t>(p[1]));

@@ -50,7 +50,7 @@ class SpaceTimeConfig(C.Structure):
         ("tau", C.c_double), ("eps", C.c_double), ("dirichlet", C.c_int32),
         ("ic_noise_prec", C.c_double), ("residual", C.c_int32), ("pde_noise_prec", C.c_double),
         ("gn_max_iters", C.c_int32), ("gn_decrement_tol", C.c_double), ("gn_armijo_c", C.c_double),
-        ("gn_shrink", C.c_double), ("gn_max_backtracks", C.c_int32),
+        ("gn_shrink", C.c_double), ("gn_max_backtracks", C.c_int32), ("dim", C.c_int32),
     ]
 
 

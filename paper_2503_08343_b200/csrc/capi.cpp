@@ -253,6 +253,7 @@ int gmrf_spacetime_create(const gmrf_spacetime_config_t* c, gmrf_spacetime_t** o
     s.ic_noise_prec = c->ic_noise_prec;
     s.residual = c->residual;
     s.pde_noise_prec = c->pde_noise_prec;
+    s.dim = c->dim == 0 ? 1 : c->dim;
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
       gmrf::fail(gmrf::kCuda, "no CUDA device: libgmrf_b200 has no CPU fallback");

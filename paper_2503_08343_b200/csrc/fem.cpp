@@ -182,6 +182,56 @@ Csc p1_stiffness(const Space1D& s, double diff, double adv, double react) {
   return csc_from_trips(s.n(), s.n(), std::move(t));
 }
 
+// Triangles (v00, v10, v11) and (v00, v11, v01) per cell (mesh.hpp:140-147);
+// P1 element mass |T|/12·(1 + δ_ij), stiffness |T| ∇φ_i·∇φ_j (exact).
+namespace {
+template <typename F>
+void for_each_triangle(const Space2D& s, F&& f) {
+  const i32 nc = s.n_cells, side = s.side();
+  const double h = s.h();
+  for (i32 iy = 0; iy < nc; ++iy)
+    for (i32 ix = 0; ix < nc; ++ix) {
+      const i32 v00 = iy * side + ix, v10 = v00 + 1, v11 = v00 + side + 1, v01 = v00 + side;
+      const double x0 = ix * h, y0 = iy * h, x1 = (ix + 1) * h, y1 = (iy + 1) * h;
+      const i32 t0[3] = {v00, v10, v11}, t1[3] = {v00, v11, v01};
+      const double p0[3][2] = {{x0, y0}, {x1, y0}, {x1, y1}};
+      const double p1[3][2] = {{x0, y0}, {x1, y1}, {x0, y1}};
+      f(t0, p0);
+      f(t1, p1);
+    }
+}
+}  // namespace
+
+Csc p1_mass(const Space2D& s) {
+  std::vector<Trip> t;
+  for_each_triangle(s, [&](const i32* v, const double (*p)[2]) {
+    const double area = 0.5 * ((p[1][0] - p[0][0]) * (p[2][1] - p[0][1]) -
+                               (p[2][0] - p[0][0]) * (p[1][1] - p[0][1]));
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) t.push_back({v[i], v[j], area / 12.0 * (i == j ? 2.0 : 1.0)});
+  });
+  return csc_from_trips(s.n(), s.n(), std::move(t));
+}
+
+Csc p1_laplace(const Space2D& s) {
+  std::vector<Trip> t;
+  for_each_triangle(s, [&](const i32* v, const double (*p)[2]) {
+    const double det = (p[1][0] - p[0][0]) * (p[2][1] - p[0][1]) -
+                       (p[2][0] - p[0][0]) * (p[1][1] - p[0][1]);
+    const double area = 0.5 * det;
+    double g[3][2];
+    for (int i = 0; i < 3; ++i) {
+      const int j = (i + 1) % 3, k = (i + 2) % 3;
+      g[i][0] = (p[j][1] - p[k][1]) / det;
+      g[i][1] = (p[k][0] - p[j][0]) / det;
+    }
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j)
+        t.push_back({v[i], v[j], area * (g[i][0] * g[j][0] + g[i][1] * g[j][1])});
+  });
+  return csc_from_trips(s.n(), s.n(), std::move(t));
+}
+
 std::vector<char> dirichlet_mask(const Space1D& s, bool enabled) {
   std::vector<char> m(s.n(), 0);
   if (enabled) m.front() = m.back() = 1;
@@ -206,11 +256,31 @@ std::vector<double> lumped_mass(const Csc& m) {
   return d;
 }
 
-MaternPrior matern_prior(const Space1D& s, const MaternSpec& spec, const std::vector<char>& mask,
-                         double eps) {
+SpatialOps spatial_ops(const Space1D& s, double diff, double adv, bool dirichlet) {
+  SpatialOps o;
+  o.n = s.n();
+  o.mass = p1_mass(s);
+  o.lap = p1_stiffness(s, 1.0, 0.0, 0.0);
+  o.op = p1_stiffness(s, diff, adv, 0.0);
+  o.slack = dirichlet_mask(s, dirichlet);
+  return o;
+}
+
+SpatialOps spatial_ops(const Space2D& s, double diff) {
+  SpatialOps o;
+  o.n = s.n();
+  o.mass = p1_mass(s);
+  o.lap = p1_laplace(s);
+  o.op = scale(o.lap, diff);  // laplace_operator(diff) (assembly.hpp:48)
+  o.slack.assign(o.n, 0);     // natural boundary conditions
+  return o;
+}
+
+MaternPrior matern_prior(const SpatialOps& ops, const MaternSpec& spec, double eps) {
   require(spec.kappa > 0 && spec.alpha >= 1 && spec.tau > 0, kContract, "matern: bad spec");
-  Csc mass = p1_mass(s);
-  Csc k = add(p1_stiffness(s, 1.0, 0.0, 0.0), mass, 1.0, spec.kappa * spec.kappa);
+  const std::vector<char>& mask = ops.slack;
+  const Csc& mass = ops.mass;
+  Csc k = add(ops.lap, mass, 1.0, spec.kappa * spec.kappa);
   Csc k_hat = mask_constrained(k, mask, 1.0);
   Csc m_hat = mask_constrained(mass, mask, eps);
   std::vector<double> lum = lumped_mass(m_hat), inv(lum.size()), isq(lum.size());
@@ -229,19 +299,16 @@ MaternPrior matern_prior(const Space1D& s, const MaternSpec& spec, const std::ve
   return {symmetrize(q), l};
 }
 
-SpaceTimeBlocks spacetime_blocks(const Space1D& s, double diff, double adv, double dt,
-                                 double tau, const MaternSpec& noise, const MaternSpec& init,
-                                 bool dirichlet, double eps) {
+SpaceTimeBlocks spacetime_blocks(const SpatialOps& ops, double dt, double tau,
+                                 const MaternSpec& noise, const MaternSpec& init, double eps) {
   SpaceTimeBlocks b;
-  b.n = s.n();
+  b.n = ops.n;
   b.eps = eps;
-  b.slack = dirichlet_mask(s, dirichlet);
-  Csc mass = p1_mass(s);
-  Csc k = p1_stiffness(s, diff, adv, 0.0);
-  Csc k_hat = mask_constrained(k, b.slack, 1.0);
-  Csc m_hat = mask_constrained(mass, b.slack, eps);
-  MaternPrior nz = matern_prior(s, noise, b.slack, eps);
-  MaternPrior in = matern_prior(s, init, b.slack, eps);
+  b.slack = ops.slack;
+  Csc k_hat = mask_constrained(ops.op, b.slack, 1.0);
+  Csc m_hat = mask_constrained(ops.mass, b.slack, eps);
+  MaternPrior nz = matern_prior(ops, noise, eps);
+  MaternPrior in = matern_prior(ops, init, eps);
   std::vector<double> lum = lumped_mass(m_hat), inv(lum.size());
   for (size_t i = 0; i < lum.size(); ++i) inv[i] = 1.0 / lum[i];
   Csc w1 = scale_cols(m_hat, inv);

@@ -1,11 +1,14 @@
 // Host-side spatial discretisation: a small CSC toolkit, P1 FEM on 1D interval
-// meshes, homogeneous-Dirichlet constraint folding, the Matérn SPDE prior and
-// the per-step spatial blocks of the implicit-Euler space-time prior.
+// meshes and on the structured triangulated unit square, homogeneous-Dirichlet
+// constraint folding, the Matérn SPDE prior and the per-step spatial blocks of
+// the implicit-Euler space-time prior (dimension-generic: they only see the
+// spatial mass / Laplacian / proxy-operator matrices).
 //
 // These are n_s-sized (one time slice) and computed once; the joint space-time
 // matrices (n_s·n_t) are assembled on the device from them (assembly.cu).
 // Semantics follow the reference:
 //   P1 mass/stiffness ........ fem/assembly.hpp:81-161
+//   unit-square triangulation  fem/mesh.hpp:108-149
 //   Dirichlet fold + mask .... fem/constraints.hpp:111-128,158-173, priors/boundary.hpp:15-29
 //   lumped mass .............. fem/assembly.hpp:241-262
 //   Matérn Q, sqrt ........... priors/matern.hpp:53-80
@@ -55,6 +58,28 @@ Csc p1_mass(const Space1D& s);
 // ∫ diff·φ'_i φ'_j + ∫ φ_i c φ'_j + react ∫ φ_i φ_j
 Csc p1_stiffness(const Space1D& s, double diff, double adv, double react);
 
+// P1 on the unit square, n_cells² cells each split along the lower-left →
+// upper-right diagonal; node (ix, iy) has DoF iy·(n_cells+1) + ix.
+struct Space2D {
+  i32 n_cells;
+  i32 side() const { return n_cells + 1; }
+  i32 n() const { return side() * side(); }
+  double h() const { return 1.0 / n_cells; }
+};
+Csc p1_mass(const Space2D& s);
+Csc p1_laplace(const Space2D& s);  // ∫ ∇φ_i · ∇φ_j
+
+// The spatial matrices everything downstream needs, for any dimension.
+struct SpatialOps {
+  i32 n = 0;
+  Csc mass;                 // consistent P1 mass
+  Csc lap;                  // ∫ ∇φ·∇φ (Matérn priors)
+  Csc op;                   // proxy operator of the space-time prior
+  std::vector<char> slack;  // constrained (Dirichlet) DoFs
+};
+SpatialOps spatial_ops(const Space1D& s, double diff, double adv, bool dirichlet);
+SpatialOps spatial_ops(const Space2D& s, double diff);
+
 // Homogeneous Dirichlet on both end nodes: slack coordinates.
 std::vector<char> dirichlet_mask(const Space1D& s, bool enabled);
 // fold_and_mask with T = I: constrained rows/cols removed, `diag` inserted.
@@ -69,8 +94,7 @@ struct MaternSpec {
 struct MaternPrior {
   Csc q, sqrt;
 };
-MaternPrior matern_prior(const Space1D& s, const MaternSpec& spec, const std::vector<char>& mask,
-                         double eps);
+MaternPrior matern_prior(const SpatialOps& ops, const MaternSpec& spec, double eps);
 
 // Per-step spatial blocks of the space-time prior for a uniform time grid.
 struct SpaceTimeBlocks {
@@ -85,8 +109,7 @@ struct SpaceTimeBlocks {
   std::vector<char> slack;  // constrained (slack) spatial coordinates
   double eps = 1e-10;       // slack noise variance
 };
-SpaceTimeBlocks spacetime_blocks(const Space1D& s, double diff, double adv, double dt,
-                                 double tau, const MaternSpec& noise, const MaternSpec& init,
-                                 bool dirichlet, double eps);
+SpaceTimeBlocks spacetime_blocks(const SpatialOps& ops, double dt, double tau,
+                                 const MaternSpec& noise, const MaternSpec& init, double eps);
 
 }  // namespace gmrf

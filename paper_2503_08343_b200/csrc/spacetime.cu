@@ -269,6 +269,49 @@ __global__ void k_burgers_jac(BurgersDev B, const double* __restrict__ u, const 
   }
 }
 
+// ---- Allen-Cahn weak residual, implicit Euler, lumped cubic -----------------
+// r_s = M(u_{s+1} − u_s)/Δt + (ε² K u_{s+1} + M̃(u_{s+1}³ − u_{s+1})), the
+// restatement in oracle/ref_capi.cpp (burgers_fem_residual layout,
+// residual.hpp:244-382; lumped reaction as residual.hpp:431-441), slack
+// columns masked. M, K: CSR rows on the stencil (ascending columns).
+__global__ void k_ac_res(AcDev A, const double* __restrict__ u, double* __restrict__ f) {
+  const int nrow = (A.nt - 1) * A.nk;
+  for (int row = blockIdx.x * blockDim.x + threadIdx.x; row < nrow; row += gridDim.x * blockDim.x) {
+    const int s = row / A.nk, d = A.kept[row - s * A.nk];
+    const double* u0 = u + static_cast<i64>(s) * A.ns;
+    const double* u1 = u0 + A.ns;
+    double mdu = 0.0, ku = 0.0;
+    for (i64 p = A.rp[d]; p < A.rp[d + 1]; ++p) {
+      const int j = A.ci[p];
+      if (A.slack[j]) continue;
+      mdu += A.mv[p] * (u1[j] - u0[j]);
+      ku += A.kv[p] * u1[j];
+    }
+    const double v = u1[d];
+    f[row] = mdu / A.dt + (A.eps2 * ku + A.ml[d] * (v * v * v - v));
+  }
+}
+
+// J row (s, d): slice s → −M/Δt; slice s+1 → (M/Δt + ε² K) + M̃(3u² − 1) on the diagonal.
+__global__ void k_ac_jac(AcDev A, const double* __restrict__ u, const i64* __restrict__ jrp,
+                         double* __restrict__ jv) {
+  const int nrow = (A.nt - 1) * A.nk;
+  for (int row = blockIdx.x * blockDim.x + threadIdx.x; row < nrow; row += gridDim.x * blockDim.x) {
+    const int s = row / A.nk, d = A.kept[row - s * A.nk];
+    i64 q = jrp[row];
+    for (i64 p = A.rp[d]; p < A.rp[d + 1]; ++p)
+      if (!A.slack[A.ci[p]]) jv[q++] = -A.mv[p] / A.dt;
+    const double v = u[static_cast<i64>(s + 1) * A.ns + d];
+    for (i64 p = A.rp[d]; p < A.rp[d + 1]; ++p) {
+      const int j = A.ci[p];
+      if (A.slack[j]) continue;
+      double x = A.mv[p] / A.dt + A.eps2 * A.kv[p];
+      if (j == d) x += A.ml[d] * (3.0 * v * v - 1.0);
+      jv[q++] = x;
+    }
+  }
+}
+
 __global__ void k_ic_rhs(int ns, const double* __restrict__ u0, double lam, double* __restrict__ rhs) {
   for (int d = blockIdx.x * blockDim.x + threadIdx.x; d < ns; d += gridDim.x * blockDim.x)
     rhs[d] = lam * u0[d];
@@ -301,30 +344,37 @@ SpaceTimePosterior::~SpaceTimePosterior() = default;
 
 void SpaceTimePosterior::build_host() {
   require(spec_.n_el >= 2 && spec_.n_t >= 2, kContract, "spacetime: need >= 2 elements and slices");
-  space_ = Space1D{spec_.n_el, spec_.xa, spec_.xb};
-  ns_ = space_.n();
+  require(spec_.dim == 1 || spec_.dim == 2, kContract, "spacetime: dim must be 1 or 2");
+  require(spec_.residual >= 0 && spec_.residual <= 2, kContract, "spacetime: unknown residual");
+  require(spec_.dim == 1 || (spec_.residual != 1 && spec_.advection == 0.0 && !spec_.dirichlet),
+          kContract, "spacetime: 2-D supports the heat proxy, natural BC, linear/Allen-Cahn residuals");
+  if (spec_.dim == 1) {
+    space_ = Space1D{spec_.n_el, spec_.xa, spec_.xb};
+    ops_ = spatial_ops(space_, spec_.diffusion, spec_.advection, spec_.dirichlet);
+  } else {
+    ops_ = spatial_ops(Space2D{spec_.n_el}, spec_.diffusion);
+  }
+  ns_ = ops_.n;
   nt_ = spec_.n_t;
   n_ = ns_ * nt_;
   const double dt = spec_.t_end / (nt_ - 1);
-  blk_ = spacetime_blocks(space_, spec_.diffusion, spec_.advection, dt, spec_.tau, spec_.noise,
-                          spec_.init, spec_.dirichlet, spec_.eps);
+  blk_ = spacetime_blocks(ops_, dt, spec_.tau, spec_.noise, spec_.init, spec_.eps);
   const auto& sl = blk_.slack;
+  // spatial coupling stencil (P1 element adjacency = the mass pattern)
+  Csc stencil = ops_.mass;
 
   // ---- templates: spatial patterns of the diagonal / upper off-diagonal blocks
-  auto band = [&](int rad) {
-    std::vector<Trip> t;
-    for (int j = 0; j < ns_; ++j)
-      for (int i = std::max(0, j - rad); i <= std::min(ns_ - 1, j + rad); ++i) t.push_back({i, j, 1});
-    return csc_from_trips(ns_, ns_, std::move(t));
-  };
+  // (every prior block, plus stencil² which carries JᵀΛJ of a residual whose
+  // rows couple the stencil of a DoF in two consecutive slices)
   auto pat = [](Csc m) {
     for (double& v : m.v) v = 1.0;
     return m;
   };
-  Csc dg = band(2);
+  const Csc st2 = pat(multiply(pat(stencil), pat(stencil)));
+  Csc dg = st2;
   for (const Csc* m : {&blk_.c_mm, &blk_.c_gg, &blk_.q1, &blk_.g_mm, &blk_.g_ff, &blk_.g_l1})
     dg = add(dg, pat(*m));
-  Csc up = band(2);
+  Csc up = st2;
   for (const Csc* m : {&blk_.c_mg, &blk_.g_mf}) up = add(up, pat(*m));
   Csc lo = transpose(up);
 
@@ -354,17 +404,19 @@ void SpaceTimePosterior::build_host() {
   // thickness = the coupling radii of the pattern), shared by every
   // factorization of the run
   {
-    int rx = 1, rt = 1;
+    const int nx = spec_.dim == 1 ? ns_ : spec_.n_el + 1, ny = ns_ / nx;
+    int rx = 1, ry = 1, rt = 1;
     for (int C = 0; C < n_; ++C)
       for (i64 p = pcp_[C]; p < pcp_[C + 1]; ++p) {
-        const int R = pri_[p];
-        rx = std::max(rx, std::abs(R % ns_ - C % ns_));
+        const int R = pri_[p], dr = R % ns_, dc = C % ns_;
+        rx = std::max(rx, std::abs(dr % nx - dc % nx));
+        ry = std::max(ry, std::abs(dr / nx - dc / nx));
         rt = std::max(rt, std::abs(R / ns_ - C / ns_));
       }
     std::vector<char> first(static_cast<size_t>(n_), 0);
     for (int s = 0; s < nt_; ++s)
       for (int d = 0; d < ns_; ++d) first[static_cast<size_t>(s) * ns_ + d] = sl[d];
-    std::vector<i32> perm = grid_nd_order(ns_, nt_, rx, rt, first);
+    std::vector<i32> perm = grid_nd_order3(nx, ny, nt_, rx, ry, rt, first);
     SymbolicOptions opt;
     opt.postorder_given = true;
     sym_ = std::make_shared<const Symbolic>(analyze(n_, pcp_.data(), pri_.data(), perm.data(), opt));
@@ -407,8 +459,10 @@ void SpaceTimePosterior::build_host() {
   s_.nc = static_cast<i32>(s_.cp.size()) - 1;
   ms_ = s_.nc;
 
-  // ---- Burgers Jacobian pattern (CSR rows, then CSC with a value map)
-  if (spec_.residual == 1) {
+  // ---- residual Jacobian pattern (CSR rows, then CSC with a value map): row
+  // (step s, kept DoF d) couples the stencil of d in slices s and s+1, slack
+  // columns skipped (residual.hpp:353-377)
+  if (spec_.residual != 0) {
     std::vector<int> kept;
     for (int d = 0; d < ns_; ++d)
       if (!sl[d]) kept.push_back(d);
@@ -420,8 +474,8 @@ void SpaceTimePosterior::build_host() {
       for (int k = 0; k < nk; ++k) {
         const int d = kept[k];
         for (int sl2 = s; sl2 <= s + 1; ++sl2)
-          for (int j = d - 1; j <= d + 1; ++j)
-            if (j >= 0 && j < ns_ && !sl[j]) jci_.push_back(sl2 * ns_ + j);
+          for (i64 p = stencil.cp[d]; p < stencil.cp[d + 1]; ++p)
+            if (!sl[stencil.ri[p]]) jci_.push_back(sl2 * ns_ + stencil.ri[p]);
         jrp_[s * nk + k + 1] = static_cast<i64>(jci_.size());
       }
     jcp_.assign(n_ + 1, 0);
@@ -471,7 +525,18 @@ void SpaceTimePosterior::assemble_device() {
   d_srp_.upload(sr.cp, stream_);
   d_sci_.upload(sr.ri, stream_);
   d_svr_.upload(sr.v, stream_);
-  if (spec_.residual == 1) {
+  if (spec_.residual == 2) {  // spatial M, K rows on the stencil + lumped mass
+    const Csc& m = ops_.mass;
+    std::vector<double> kv(m.ri.size(), 0.0);
+    for (i32 j = 0; j < m.nc; ++j)
+      for (i64 p = m.cp[j]; p < m.cp[j + 1]; ++p) kv[p] = ops_.lap.at(m.ri[p], j);
+    d_mrp_.upload(m.cp, stream_);
+    d_mci_.upload(m.ri, stream_);
+    d_mv_.upload(m.v, stream_);
+    d_kv_.upload(kv, stream_);
+    d_ml_.upload(lumped_mass(m), stream_);
+  }
+  if (spec_.residual != 0) {
     d_jrp_.upload(jrp_, stream_);
     d_jci_.upload(jci_, stream_);
     d_jcp_.upload(jcp_, stream_);
@@ -520,6 +585,11 @@ double SpaceTimePosterior::dot(const double* a, const double* b, i64 n) {
 }
 
 void SpaceTimePosterior::eval_residual(const double* d_u, double* d_f) {
+  if (spec_.residual == 2) {
+    k_ac_res<<<grid_for(nres_), 256, 0, stream_>>>(ac_dev(), d_u, d_f);
+    times_.kernel_launches += 1;
+    return;
+  }
   BurgersDev B{ns_, nt_, static_cast<int>(kept_.n), space_.h(), spec_.t_end / (nt_ - 1),
                spec_.diffusion, d_slack_.p, kept_.p};
   k_burgers_res<<<grid_for(nres_), 256, 0, stream_>>>(B, d_u, d_f);
@@ -527,6 +597,11 @@ void SpaceTimePosterior::eval_residual(const double* d_u, double* d_f) {
 }
 
 void SpaceTimePosterior::eval_jacobian(const double* d_u) {
+  if (spec_.residual == 2) {
+    k_ac_jac<<<grid_for(nres_), 256, 0, stream_>>>(ac_dev(), d_u, d_jrp_.p, d_jv_.p);
+    times_.kernel_launches += 1;
+    return;
+  }
   BurgersDev B{ns_, nt_, static_cast<int>(kept_.n), space_.h(), spec_.t_end / (nt_ - 1),
                spec_.diffusion, d_slack_.p, kept_.p};
   k_burgers_jac<<<grid_for(nres_), 256, 0, stream_>>>(B, d_u, d_jrp_.p, d_jv_.p);
@@ -534,6 +609,11 @@ void SpaceTimePosterior::eval_jacobian(const double* d_u) {
 }
 
 void SpaceTimePosterior::residual(const double* d_u, double* d_r) { eval_residual(d_u, d_r); }
+
+AcDev SpaceTimePosterior::ac_dev() const {
+  return AcDev{ns_, nt_, static_cast<int>(kept_.n), spec_.t_end / (nt_ - 1), spec_.diffusion,
+               d_slack_.p, kept_.p, d_mrp_.p, d_mci_.p, d_mv_.p, d_kv_.p, d_ml_.p};
+}
 
 // ½‖Sᵀ(x−μ)‖² + ½ Σ λ (y − f)², y = 0 (gauss_newton.hpp:65-83)
 double SpaceTimePosterior::objective(const double* d_x, const double* d_fx) {

@@ -15,6 +15,17 @@
 
 namespace gmrf {
 
+// Device view of the Allen-Cahn residual data (spacetime.cu).
+struct AcDev {
+  int ns, nt, nk;
+  double dt, eps2;
+  const char* slack;
+  const int* kept;
+  const i64* rp;
+  const i32* ci;
+  const double *mv, *kv, *ml;
+};
+
 struct SpaceTimeSpec {
   i32 n_el = 999;          // spatial elements (n_s = n_el + 1)
   double xa = -1.0, xb = 1.0;
@@ -27,8 +38,10 @@ struct SpaceTimeSpec {
   double eps = 1e-10;      // Dirichlet slack variance (priors/boundary.hpp:20)
   bool dirichlet = true;
   double ic_noise_prec = 1e8;
-  int residual = 1;        // 0: linear (conditioned prior is the posterior), 1: Burgers weak IE
+  int residual = 1;        // 0: linear (conditioned prior is the posterior), 1: Burgers weak IE,
+                           // 2: Allen-Cahn weak IE (lumped cubic)
   double pde_noise_prec = 1e12;
+  int dim = 1;             // 1: interval [xa, xb]; 2: unit square, n_el × n_el cells (triangles)
 };
 
 struct GnConfig {
@@ -92,10 +105,12 @@ class SpaceTimePosterior {
   double dot(const double* a, const double* b, i64 n);
   void eval_residual(const double* d_u, double* d_f);
   void eval_jacobian(const double* d_u);
+  AcDev ac_dev() const;
 
   SpaceTimeSpec spec_;
   cudaStream_t stream_;
   Space1D space_{};
+  SpatialOps ops_;
   SpaceTimeBlocks blk_;
   i32 ns_ = 0, nt_ = 0, n_ = 0, nres_ = 0, ms_ = 0;  // ms_: columns of S
   std::shared_ptr<const Symbolic> sym_;
@@ -126,6 +141,10 @@ class SpaceTimePosterior {
   DevBuf<i32> d_blk_ri_;
   DevBuf<double> d_blk_v_;
   DevBuf<char> d_slack_;
+  // Allen-Cahn: spatial M and K on the mass pattern (CSR) and the lumped mass
+  DevBuf<i64> d_mrp_;
+  DevBuf<i32> d_mci_;
+  DevBuf<double> d_mv_, d_kv_, d_ml_;
   DevBuf<double> mean_cond_, mean_, var_, x_, c_, w_, g_, d_, cand_, f_, fc_, r1_, part_, u0_;
 };
 

@@ -144,56 +144,77 @@ std::vector<i32> nd_order(i32 n, const i64* qcp, const i32* qri) {
 
 std::vector<i32> grid_nd_order(i32 nx, i32 nt, i32 xw, i32 tw, const std::vector<char>& first,
                                i32 leaf) {
+  return grid_nd_order3(nx, 1, nt, xw, 1, tw, first, leaf);
+}
+
+// Geometric nested dissection of an nx × ny × nt grid (DoF t·nx·ny + y·nx + x):
+// recursively cut the box across the axis with the largest extent / separator
+// thickness (thickness = the pattern's coupling radius along that axis),
+// number both halves, then the separator slab; boxes of ≤ leaf unknowns are
+// numbered directly. `first` unknowns (Dirichlet slack) are numbered first.
+std::vector<i32> grid_nd_order3(i32 nx, i32 ny, i32 nt, i32 xw, i32 yw, i32 tw,
+                                const std::vector<char>& first, i32 leaf) {
+  const i64 plane = static_cast<i64>(nx) * ny;
   std::vector<i32> perm;
-  perm.reserve(static_cast<size_t>(nx) * nt);
-  for (i32 t = 0; t < nt; ++t)
-    for (i32 x = 0; x < nx; ++x)
-      if (first[static_cast<size_t>(t) * nx + x]) perm.push_back(t * nx + x);
-  auto emit = [&](i32 x0, i32 x1, i32 t0, i32 t1) {
-    for (i32 t = t0; t < t1; ++t)
-      for (i32 x = x0; x < x1; ++x)
-        if (!first[static_cast<size_t>(t) * nx + x]) perm.push_back(t * nx + x);
-  };
+  perm.reserve(static_cast<size_t>(plane * nt));
+  for (i64 i = 0; i < plane * nt; ++i)
+    if (first[static_cast<size_t>(i)]) perm.push_back(static_cast<i32>(i));
   struct Box {
-    i32 x0, x1, t0, t1;
+    i32 lo[3], hi[3];
   };
+  auto emit = [&](const Box& b) {
+    for (i32 t = b.lo[2]; t < b.hi[2]; ++t)
+      for (i32 y = b.lo[1]; y < b.hi[1]; ++y)
+        for (i32 x = b.lo[0]; x < b.hi[0]; ++x) {
+          const i64 id = t * plane + static_cast<i64>(y) * nx + x;
+          if (!first[static_cast<size_t>(id)]) perm.push_back(static_cast<i32>(id));
+        }
+  };
+  const i32 wid[3] = {xw, yw, tw};
   // explicit recursion: (box, stage) with stage 0 = split, 1 = emit separator
   struct Frame {
-    Box b, sep;
+    Box b;
     int stage;
   };
   std::vector<Frame> st;
-  st.push_back({{0, nx, 0, nt}, {0, 0, 0, 0}, 0});
+  st.push_back({{{0, 0, 0}, {nx, ny, nt}}, 0});
   while (!st.empty()) {
     Frame f = st.back();
     st.pop_back();
     if (f.stage == 1) {
-      emit(f.sep.x0, f.sep.x1, f.sep.t0, f.sep.t1);
+      emit(f.b);
       continue;
     }
     const Box b = f.b;
-    const i32 ex = b.x1 - b.x0, et = b.t1 - b.t0;
-    if (static_cast<i64>(ex) * et <= leaf || (ex <= xw + 1 && et <= tw + 1)) {
-      emit(b.x0, b.x1, b.t0, b.t1);
+    i32 ext[3];
+    i64 vol = 1;
+    for (int a = 0; a < 3; ++a) {
+      ext[a] = b.hi[a] - b.lo[a];
+      vol *= ext[a];
+    }
+    int axis = -1;
+    double best = 0.0;
+    for (int a = 0; a < 3; ++a)
+      if (ext[a] > wid[a] + 1) {
+        const double r = static_cast<double>(ext[a]) / wid[a];
+        if (axis < 0 || r > best || (r == best && a == 2)) {
+          axis = a;
+          best = r;
+        }
+      }
+    if (vol <= leaf || axis < 0) {
+      emit(b);
       continue;
     }
-    const bool cut_t = et > tw + 1 && (ex <= xw + 1 || static_cast<double>(et) / tw >=
-                                                          static_cast<double>(ex) / xw);
-    Box lo, hi, sep;
-    if (cut_t) {
-      const i32 tm = b.t0 + (et - tw) / 2;
-      lo = {b.x0, b.x1, b.t0, tm};
-      sep = {b.x0, b.x1, tm, tm + tw};
-      hi = {b.x0, b.x1, tm + tw, b.t1};
-    } else {
-      const i32 xm = b.x0 + (ex - xw) / 2;
-      lo = {b.x0, xm, b.t0, b.t1};
-      sep = {xm, xm + xw, b.t0, b.t1};
-      hi = {xm + xw, b.x1, b.t0, b.t1};
-    }
-    st.push_back({b, sep, 1});
-    st.push_back({hi, {}, 0});
-    st.push_back({lo, {}, 0});
+    const i32 mid = b.lo[axis] + (ext[axis] - wid[axis]) / 2;
+    Box lo = b, sep = b, hi = b;
+    lo.hi[axis] = mid;
+    sep.lo[axis] = mid;
+    sep.hi[axis] = mid + wid[axis];
+    hi.lo[axis] = mid + wid[axis];
+    st.push_back({sep, 1});
+    st.push_back({hi, 0});
+    st.push_back({lo, 0});
   }
   return perm;
 }

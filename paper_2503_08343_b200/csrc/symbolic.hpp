@@ -82,6 +82,8 @@ std::vector<i32> nd_order(i32 n, const i64* qcp, const i32* qri);
 // ordered first. Deterministic and O(n).
 std::vector<i32> grid_nd_order(i32 nx, i32 nt, i32 xw, i32 tw, const std::vector<char>& first,
                                i32 leaf = 64);
+std::vector<i32> grid_nd_order3(i32 nx, i32 ny, i32 nt, i32 xw, i32 yw, i32 tw,
+                                const std::vector<char>& first, i32 leaf = 64);
 
 // Exact reference L pattern (col_ptr from s.colptr_l): row indices per column,
 // ascending, diagonal first — the layout of CholeskyFactor::L

@@ -1,9 +1,13 @@
-"""Space-time GMRF posterior (configs 3-4): host mirror of the reference's
+"""Space-time GMRF posterior (configs 3-5): host mirror of the reference's
 run_burgers chain (bench/runner.hpp:457-632) over the C-ABI pipeline
 ``gmrf_spacetime_*`` (include/gmrf_b200.h).
 
-    spatiotemporal_prior  → condition_on(IC) → gauss_newton(burgers_fem_residual)
+    spatiotemporal_prior  → condition_on(IC) → gauss_newton(residual)
     → laplace_posterior → variance_takahashi
+
+residual: Burgers weak form (config 4, 1-D), or the Allen-Cahn weak form
+(config 5, 2-D unit square; restated in oracle/ref_capi.cpp since the reference
+has no Allen-Cahn residual).
 
 Everything after the host-side spatial blocks and symbolic analysis runs on
 the device; there is no CPU path.
@@ -55,6 +59,7 @@ class SpaceTimeSpec:
     ic_noise_prec: float = 1e8
     residual: int = 1
     pde_noise_prec: float = 1e12
+    dim: int = 1
 
     @staticmethod
     def burgers(n_el=999, n_t=1000) -> "SpaceTimeSpec":
@@ -66,6 +71,24 @@ class SpaceTimeSpec:
         """Config 3."""
         return SpaceTimeSpec(n_el=n_el, xa=0.0, xb=1.0, n_t=n_t, diffusion=0.1, advection=0.0,
                              ic_noise_prec=1e6, residual=0)
+
+    @staticmethod
+    def allen_cahn(n_cells=127, n_t=256) -> "SpaceTimeSpec":
+        """Config 5: 128² unit-square P1 nodes × 256 slices over
+        [0, 0.5], heat proxy laplace_operator(ε² = 0.0025), natural BC, IC Λ = 1e6,
+        Allen-Cahn residual with Λ_pde = 1e12 (GN 8 steps)."""
+        return SpaceTimeSpec(n_el=n_cells, xa=0.0, xb=1.0, n_t=n_t, t_end=0.5, diffusion=0.0025,
+                             advection=0.0, dirichlet=False, ic_noise_prec=1e6, residual=2, dim=2)
+
+    @property
+    def n_space(self) -> int:
+        return (self.n_el + 1) ** self.dim
+
+    def node_xy(self) -> np.ndarray:
+        """2-D node coordinates, DoF iy·(n+1) + ix (mesh.hpp:118-131)."""
+        a = np.arange(self.n_el + 1) / self.n_el
+        x, y = np.meshgrid(a, a)
+        return np.stack([x.ravel(), y.ravel()], axis=1)
 
     def node_x(self) -> np.ndarray:
         i = np.arange(self.n_el + 1)
@@ -100,7 +123,7 @@ class SpaceTimePosterior:
             spec.noise.kappa, spec.noise.alpha, spec.noise.tau, spec.init.kappa, spec.init.alpha,
             spec.init.tau, spec.tau, spec.eps, int(spec.dirichlet), spec.ic_noise_prec,
             spec.residual, spec.pde_noise_prec, gn.max_iters, gn.decrement_tol, gn.armijo_c,
-            gn.shrink, gn.max_backtracks)
+            gn.shrink, gn.max_backtracks, spec.dim)
         self.spec = spec
         lib = _capi.load()
         h = C.c_void_p()

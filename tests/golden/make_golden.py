@@ -88,6 +88,21 @@ def spatiotemporal(ref, kind, n_el, n_t, name, gn_iters=0):
     np.savez_compressed(os.path.join(HERE, name), **out)
 
 
+def allen_cahn(ref, n_cells, n_t, name, gn_iters=8):
+    """C5 shape at reduced size: unit square, Allen-Cahn residual restated in
+    oracle/ref_capi.cpp, driven by the reference gauss_newton / laplace_posterior
+    / variance_takahashi (with a finite-difference check of its Jacobian)."""
+    p = [n_cells, n_t, 0.5, 0.0025, 10, 1, 1, 10, 2, 1, 1.0, 1e6, 1005, 1e12, gn_iters, 1, 1, 1]
+    b = ref.build("allen_cahn", p)
+    out = {"params": np.array(p, np.float64), "fd_rel_err": np.array([b.scalar("fd_rel_err")])}
+    for k in ["Q_prior", "Q_cond", "S_cond", "Q_la", "J_at_mean_cond"]:
+        out.update(mat(k, b.mat(k)))
+    for k in ["u0", "mean_cond", "f_at_mean_cond", "mode", "mean_post", "var_post",
+              "gn_objective", "gn_decrement", "gn_step", "gn_backtracks"]:
+        out[k] = b.vec(k)
+    np.savez_compressed(os.path.join(HERE, name), **out)
+
+
 def main():
     ref = Ref()
     corpus(ref, 50, 20240817, "corpus_acceptance.npz")   # acceptance.cpp:67 criterion 1
@@ -95,6 +110,7 @@ def main():
     matern1d(ref)
     spatiotemporal(ref, 0, 19, 20, "c3_heat_20x20.npz")
     spatiotemporal(ref, 1, 19, 20, "c4_burgers_20x20.npz", gn_iters=4)
+    allen_cahn(ref, 8, 16, "c5_allen_cahn_8x8x16.npz")
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))

@@ -108,3 +108,50 @@ def test_burgers_gn_laplace_vs_reference(port):
     floor, _ = ordering_floor(port, qla, qla @ z["mode"])
     assert rel(mean, z["mode"]) <= max(100 * floor, 1e-8), (rel(mean, z["mode"]), floor)
     assert rel(var, z["var_post"]) <= 1e-6
+
+
+# ---- config 5 shape: 2-D unit square, Allen-Cahn residual -------------------
+def spec_ac(params):
+    p = params
+    return SpaceTimeSpec(n_el=int(p[0]), xa=0.0, xb=1.0, n_t=int(p[1]), t_end=p[2], diffusion=p[3],
+                         advection=0.0, noise=MaternSpec(p[4], int(p[5]), p[6]),
+                         init=MaternSpec(p[7], int(p[8]), p[9]), tau=p[10], dirichlet=False,
+                         ic_noise_prec=p[11], residual=2, pde_noise_prec=p[13], dim=2)
+
+
+def test_allen_cahn_assembly_residual_jacobian_match_reference():
+    z = load_golden("c5_allen_cahn_8x8x16.npz")
+    post = SpaceTimePosterior(spec_ac(z["params"]))
+    assert post.n == 81 * 16
+    qref = golden_mat(z, "Q_cond").to_scipy()
+    q = ours_matrix(post, "cond")
+    assert sp.linalg.norm(q - qref) / sp.linalg.norm(qref) <= 1e-13
+    s = golden_mat(z, "S_cond").to_scipy()
+    qeff_ref = s @ s.T
+    qeff_ref = 0.5 * (qeff_ref + qeff_ref.T)
+    assert sp.linalg.norm(ours_matrix(post, "eff") - qeff_ref) / sp.linalg.norm(qeff_ref) <= 1e-13
+    u = z["mean_cond"]
+    f = post.residual(u)
+    assert rel(f, z["f_at_mean_cond"]) <= 1e-12
+    rp, ci, v = post.jacobian(u)
+    j = sp.csr_matrix((v, ci, rp), shape=(len(f), post.n))
+    jref = golden_mat(z, "J_at_mean_cond").to_scipy()
+    assert sp.linalg.norm(j - jref) / sp.linalg.norm(jref) <= 1e-13
+    assert j.nnz == jref.nnz
+
+
+def test_allen_cahn_gn_laplace_vs_reference(port):
+    z = load_golden("c5_allen_cahn_8x8x16.npz")
+    p = z["params"]
+    from paper_2503_08343_b200.spacetime import GaussNewtonConfig
+    post = SpaceTimePosterior(spec_ac(p), GaussNewtonConfig(max_iters=int(p[14])))
+    mean, var, trace, conv = post.run(z["u0"], variances=True)
+    assert len(trace) == len(z["gn_objective"])            # identical GN iteration count
+    np.testing.assert_array_equal([t.backtracks for t in trace], z["gn_backtracks"])
+    np.testing.assert_array_equal([t.step_size for t in trace], z["gn_step"])
+    obj = np.array([t.objective for t in trace])
+    assert np.max(np.abs(obj - z["gn_objective"]) / np.abs(z["gn_objective"])) <= 1e-6
+    qla = golden_mat(z, "Q_la").to_scipy()
+    floor, _ = ordering_floor(port, qla, qla @ z["mode"])
+    assert rel(mean, z["mode"]) <= max(100 * floor, 1e-8), (rel(mean, z["mode"]), floor)
+    assert rel(var, z["var_post"]) <= 1e-6

@@ -141,3 +141,14 @@ def test_port_against_live_reference(port, ref):
             np.testing.assert_array_equal(lv, rv)
             np.testing.assert_array_equal(port.takahashi_diag(n, lcp, lri, lv, perm),
                                           f.takahashi_diag())
+
+
+def test_allen_cahn_restatement_pins():
+    """The C5 residual is absent from the reference; its CPU
+    restatement must pass the reference's finite-difference Jacobian check
+    pattern (acceptance.cpp:503-608, tolerance 1e-5) and drive the reference
+    gauss_newton to convergence on the fixture."""
+    z = load_golden("c5_allen_cahn_8x8x16.npz")
+    assert z["fd_rel_err"][0] <= 1e-5
+    assert len(z["gn_objective"]) >= 2 and z["gn_objective"][-1] < z["gn_objective"][0]
+    assert np.all(z["var_post"] > 0)
