@@ -162,16 +162,31 @@ DeviceFactor::DeviceFactor(std::shared_ptr<const Symbolic> sym, cudaStream_t str
   uvptr_.upload(up, stream_);
   pptr_.upload(pp, stream_);
   {
+    // row tiles of L_RJ; wide supernodes split each row tile into column blocks
+    // (forward partials in pf_, one self-resetting arrival counter per row tile)
     std::vector<SolveTile> tl;
+    int32_t nslot = 0, nctr = 0;
     tile_ptr_.assign(s.n_levels + 1, 0);
     for (int l = 0; l < s.n_levels; ++l) {
       for (int64_t q = lvl_ptr_[l]; q < lvl_ptr_[l + 1]; ++q) {
-        const int k = lsn[q], r = s.r(k);
-        for (int t = 0; t * kSolveRows < r; ++t) tl.push_back({k, t * kSolveRows, t});
+        const int k = lsn[q], r = s.r(k), w = s.w(k);
+        const int np = w > kSolveSplitCols ? (w + kSolveSplitCols - 1) / kSolveSplitCols : 1;
+        for (int t = 0; t * kSolveRows < r; ++t) {
+          const int32_t slot = np > 1 ? nslot : 0, ctr = np > 1 ? nctr++ : 0;
+          for (int p = 0; p < np; ++p) {
+            const int c0 = np > 1 ? p * kSolveSplitCols : 0;
+            const int c1 = np > 1 ? std::min(w, c0 + kSolveSplitCols) : w;
+            tl.push_back({k, t * kSolveRows, t, c0, c1, p, np, slot, ctr});
+          }
+          if (np > 1) nslot += np;
+        }
       }
       tile_ptr_[l + 1] = static_cast<int64_t>(tl.size());
     }
     tiles_.upload(tl, stream_);
+    pf_.alloc(std::max<int64_t>(static_cast<int64_t>(nslot) * kMaxRhs * kSolveRows, 1));
+    pfctr_.alloc(std::max(nctr, 1));
+    cuda_check(cudaMemsetAsync(pfctr_.p, 0, pfctr_.n * sizeof(unsigned), stream_), "counters");
   }
   set_solve_smem<1>(maxw_);
   if ((200 * 1024 / 8 - 64 * 65) / maxw_ >= 4) set_solve_smem<4>(maxw_);
@@ -764,22 +779,24 @@ void DeviceFactor::launch_solve_levels(bool fwd, bool bwd, double* y, int nr) {
             coop(reinterpret_cast<const void*>(k_fsolve_wide<NR>), wgroups_[g].nt, args);
           }
         }
-        if (nt) {
-          k_fsolve_off<NR><<<nt, kSolveRows, 0, st>>>(tiles_.p + tile_ptr_[l], sd, L, y, nr, Uv_.p,
-                                                      uvptr_.p);
-          ++launches;
-        }
       });
+      if (nt)
+        pf.run(st, pf.tag("solve.forward_off", l), 0.0, 0.0, [&] {
+          k_fsolve_off<NR><<<nt, kSolveRows, 0, st>>>(tiles_.p + tile_ptr_[l], sd, L, y, nr, Uv_.p,
+                                                      uvptr_.p, pf_.p, pfctr_.p);
+          ++launches;
+        });
     }
   if (bwd)
     for (int l = s.n_levels - 1; l >= 0; --l) {
       const int nrm = static_cast<int>(lvl_nrm_[l]);
       const int nt = static_cast<int>(tile_ptr_[l + 1] - tile_ptr_[l]);
-      pf.run(st, pf.tag("solve.backward", l), 0.0, lvl_bytes_[l], [&] {
-        if (nt) {
+      if (nt)
+        pf.run(st, pf.tag("solve.backward_off", l), 0.0, 0.0, [&] {
           k_bsolve_off<NR><<<nt, 256, 0, st>>>(tiles_.p + tile_ptr_[l], sd, L, y, nr, P_.p, pptr_.p);
           ++launches;
-        }
+        });
+      pf.run(st, pf.tag("solve.backward", l), 0.0, lvl_bytes_[l], [&] {
         if (nrm) {
           k_bsolve_diag<NR><<<nrm, 256, smem_diag, st>>>(lvl_sn + lvl_ptr_[l], sd, L, y, nr, P_.p,
                                                          pptr_.p, rdiag);

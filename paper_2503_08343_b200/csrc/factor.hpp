@@ -108,6 +108,8 @@ class DeviceFactor {
   DevBuf<int64_t> rptr_, lptr_, uptr_, qmap_, pptr_, uvptr_;
   DevBuf<double> L_, U_, Sig_, q_, P_, Uv_, v1_, v2_, diag_, rdiag_;
   DevBuf<SolveTile> tiles_;
+  DevBuf<double> pf_;       // forward column-block partials (solve.cuh)
+  DevBuf<unsigned> pfctr_;  // their arrival counters
   std::vector<int64_t> tile_ptr_;
   int maxw_ = 1;
   int64_t uv_total_ = 0, p_total_ = 0;

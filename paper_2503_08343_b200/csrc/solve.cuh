@@ -129,14 +129,21 @@ __global__ void __launch_bounds__(256) k_fsolve_diag(const int32_t* __restrict__
 }
 
 // ---- forward: u_R = f_R − L_RJ y_J, 128-row tiles ---------------------------
+// Row tiles of wide supernodes are split into column blocks (kSolveSplitCols):
+// each block writes its partial Σ_j L_ij y_j to PF, and the CTA that arrives
+// last for the row tile subtracts the partials from u in block order (fixed
+// order; the arrival counter wraps back to 0 by itself via atomicInc).
 template <int NR>
 __global__ void __launch_bounds__(kSolveRows) k_fsolve_off(const SolveTile* __restrict__ tiles,
                                                           SymDev sd, const double* __restrict__ L,
                                                           const double* __restrict__ y, int nrhs,
                                                           double* __restrict__ Uv,
-                                                          const int64_t* __restrict__ uvptr) {
+                                                          const int64_t* __restrict__ uvptr,
+                                                          double* __restrict__ PF,
+                                                          unsigned* __restrict__ ctr) {
   constexpr int CW = kSolveOffCols;
   __shared__ double yJ[CW * NR];  // [rr*CW + j], one column chunk of y_J
+  __shared__ bool last;
   const SolveTile t = tiles[blockIdx.x];
   const int s = t.sn;
   const int f0 = sd.sn_first[s];
@@ -146,13 +153,14 @@ __global__ void __launch_bounds__(kSolveRows) k_fsolve_off(const SolveTile* __re
   const int n = sd.n;
   const int i = t.r0 + threadIdx.x;
   const bool active = i < r;
+  const bool split = t.nparts > 1;
   const double* Lr = L + sd.lptr[s] + w + i;
   double* u = Uv + uvptr[s] * nrhs;
   double acc[NR];
 #pragma unroll
-  for (int rr = 0; rr < NR; ++rr) acc[rr] = (active && rr < nrhs) ? u[i + rr * r] : 0.0;
-  for (int c0 = 0; c0 < w; c0 += CW) {
-    const int wc = min(CW, w - c0);
+  for (int rr = 0; rr < NR; ++rr) acc[rr] = (active && rr < nrhs && !split) ? u[i + rr * r] : 0.0;
+  for (int c0 = t.c0; c0 < t.c1; c0 += CW) {
+    const int wc = min(CW, t.c1 - c0);
     __syncthreads();
     for (int idx = threadIdx.x; idx < wc * nrhs; idx += blockDim.x) {
       const int a = idx % wc, rr = idx / wc;
@@ -177,10 +185,32 @@ __global__ void __launch_bounds__(kSolveRows) k_fsolve_off(const SolveTile* __re
       for (int rr = 0; rr < NR; ++rr) acc[rr] -= l * yJ[rr * CW + j];
     }
   }
-  if (!active) return;
+  if (!split) {
+    if (!active) return;
 #pragma unroll
-  for (int rr = 0; rr < NR; ++rr)
-    if (rr < nrhs) u[i + rr * r] = acc[rr];
+    for (int rr = 0; rr < NR; ++rr)
+      if (rr < nrhs) u[i + rr * r] = acc[rr];
+    return;
+  }
+  // partial (already negated) → PF[slot][rr][row]
+  double* mine = PF + static_cast<int64_t>(t.pf + t.part) * NR * kSolveRows;
+#pragma unroll
+  for (int rr = 0; rr < NR; ++rr) mine[rr * kSolveRows + threadIdx.x] = acc[rr];
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicInc(ctr + t.ctr, t.nparts - 1) == static_cast<unsigned>(t.nparts - 1);
+  __syncthreads();
+  if (!last || !active) return;
+  __threadfence();
+  const double* base = PF + static_cast<int64_t>(t.pf) * NR * kSolveRows;
+#pragma unroll
+  for (int rr = 0; rr < NR; ++rr) {
+    if (rr >= nrhs) break;
+    double v = u[i + rr * r];
+    for (int p = 0; p < t.nparts; ++p)
+      v += __ldcg(base + static_cast<int64_t>(p) * NR * kSolveRows + rr * kSolveRows + threadIdx.x);
+    u[i + rr * r] = v;
+  }
 }
 
 // ---- backward: partial sums t = L_RJᵀ x_R over 128-row tiles ----------------
@@ -208,7 +238,7 @@ __global__ void __launch_bounds__(256) k_bsolve_off(const SolveTile* __restrict_
   __syncthreads();
   const double* Lt = L + sd.lptr[s] + w + t.r0;
   double* Pt = P + (pptr[s] + static_cast<int64_t>(t.tidx) * w) * nrhs;  // [rr*w + j]
-  for (int j = warp; j < w; j += 8) {
+  for (int j = t.c0 + warp; j < t.c1; j += 8) {
     const double* col = Lt + static_cast<int64_t>(j) * rows;
     double acc[NR];
 #pragma unroll
