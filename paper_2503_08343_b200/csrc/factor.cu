@@ -50,7 +50,7 @@ constexpr unsigned kRowsMaxCtas = 148;  // one CTA per SM (k_panel_rows uses ~25
 
 template <int NR>
 void set_solve_smem(int maxw) {
-  const int smem_diag = (maxw * NR + 64 * 65) * static_cast<int>(sizeof(double));
+  const int smem_diag = (maxw * NR + 64 * 65 + kSolveFuseRows * NR) * static_cast<int>(sizeof(double));
   cuda_check(cudaFuncSetAttribute(k_fsolve_diag<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   smem_diag), "smem fsolve_diag");
   cuda_check(cudaFuncSetAttribute(k_bsolve_diag<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -170,6 +170,7 @@ DeviceFactor::DeviceFactor(std::shared_ptr<const Symbolic> sym, cudaStream_t str
     for (int l = 0; l < s.n_levels; ++l) {
       for (int64_t q = lvl_ptr_[l]; q < lvl_ptr_[l + 1]; ++q) {
         const int k = lsn[q], r = s.r(k), w = s.w(k);
+        if (!is_wide(k) && r <= kSolveFuseRows) continue;  // done inside the *_diag kernels
         const int np = w > kSolveSplitCols ? (w + kSolveSplitCols - 1) / kSolveSplitCols : 1;
         for (int t = 0; t * kSolveRows < r; ++t) {
           const int32_t slot = np > 1 ? nslot : 0, ctr = np > 1 ? nctr++ : 0;
@@ -189,8 +190,8 @@ DeviceFactor::DeviceFactor(std::shared_ptr<const Symbolic> sym, cudaStream_t str
     cuda_check(cudaMemsetAsync(pfctr_.p, 0, pfctr_.n * sizeof(unsigned), stream_), "counters");
   }
   set_solve_smem<1>(maxw_);
-  if ((200 * 1024 / 8 - 64 * 65) / maxw_ >= 4) set_solve_smem<4>(maxw_);
-  if ((200 * 1024 / 8 - 64 * 65) / maxw_ >= 16) set_solve_smem<16>(maxw_);
+  if ((200 * 1024 / 8 - 64 * 65) / (maxw_ + kSolveFuseRows) >= 4) set_solve_smem<4>(maxw_);
+  if ((200 * 1024 / 8 - 64 * 65) / (maxw_ + kSolveFuseRows) >= 16) set_solve_smem<16>(maxw_);
   // solve traffic per level: the L panel (8 B/entry, lower trapezoid) + row indices
   lvl_bytes_.assign(s.n_levels, 0.0);
   for (int k = 0; k < s.ns; ++k) {
@@ -744,7 +745,8 @@ void DeviceFactor::launch_solve_levels(bool fwd, bool bwd, double* y, int nr) {
   const double* L = L_.p;
   const double* rdiag = rdiag_.p;
   const int32_t* lvl_sn = lvl_sn_.p;
-  const int smem_diag = (maxw_ * NR + 64 * 65) * static_cast<int>(sizeof(double));
+  const int smem_diag =
+      (maxw_ * NR + 64 * 65 + kSolveFuseRows * NR) * static_cast<int>(sizeof(double));
   constexpr int smem_wide = wide_smem_bytes<NR>();
   int64_t& launches = launches_solve_;
   if (wide_blocks_) {
@@ -822,7 +824,7 @@ void DeviceFactor::solve(int mode, int nrhs, const double* b, double* x, bool on
   if (n == 0 || nrhs == 0) return;
   launches_solve_ = 0;
   // right-hand sides per pass: 1, or up to 16 within the shared-memory budget
-  const int cap = static_cast<int>((200 * 1024 / 8 - 64 * 65) / std::max(maxw_, 1));
+  const int cap = static_cast<int>((200 * 1024 / 8 - 64 * 65) / (maxw_ + kSolveFuseRows));
   require(cap >= 1, kContract, "solve: supernode too wide for the shared-memory triangle");
   const int nrb = nrhs == 1 ? 1 : (cap >= 16 ? 16 : (cap >= 4 ? 4 : 1));
   for (int r0 = 0; r0 < nrhs; r0 += nrb) {

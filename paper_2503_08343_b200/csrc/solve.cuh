@@ -5,6 +5,9 @@
 //            and solved by one warp;
 //   *_off  : many CTAs per supernode — the rectangular L_RJ part, 128-row tiles,
 //            streaming L once with coalesced column reads.
+// Supernodes with at most kSolveFuseRows rows below the triangle do their
+// rectangular part inside the *_diag kernel (no tiles, one launch per level for
+// the many small supernodes of the lower tree levels).
 // Deterministic: children are accumulated in a fixed order and the backward
 // partial sums over row tiles are reduced in tile order.
 #pragma once
@@ -121,6 +124,32 @@ __global__ void __launch_bounds__(256) k_fsolve_diag(const int32_t* __restrict__
         if (rr < nrhs) fJ[rr * w + i] = acc[rr];
     }
     __syncthreads();
+  }
+  if (r <= kSolveFuseRows) {  // u_R = f_R − L_RJ y_J here (no off-diagonal tiles)
+    for (int i = tid; i < r; i += blockDim.x) {
+      double acc[NR];
+#pragma unroll
+      for (int rr = 0; rr < NR; ++rr) acc[rr] = rr < nrhs ? uS[i + rr * r] : 0.0;
+      const double* li = Ls + w + i;
+      int j = 0;
+      for (; j + 8 <= w; j += 8) {  // 8 independent loads in flight
+        double l[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) l[u] = li[static_cast<int64_t>(j + u) * rows];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+#pragma unroll
+          for (int rr = 0; rr < NR; ++rr) acc[rr] -= l[u] * fJ[rr * w + j + u];
+      }
+      for (; j < w; ++j) {
+        const double l = li[static_cast<int64_t>(j) * rows];
+#pragma unroll
+        for (int rr = 0; rr < NR; ++rr) acc[rr] -= l * fJ[rr * w + j];
+      }
+#pragma unroll
+      for (int rr = 0; rr < NR; ++rr)
+        if (rr < nrhs) uS[i + rr * r] = acc[rr];
+    }
   }
   for (int idx = tid; idx < w * nrhs; idx += blockDim.x) {
     const int a = idx % w, rr = idx / w;
@@ -279,13 +308,42 @@ __global__ void __launch_bounds__(256) k_bsolve_diag(const int32_t* __restrict__
   const double* Ls = L + sd.lptr[s];
   double* bJ = sm;           // [rr*w + a]
   double* Lb = sm + w * NR;  // [j*65 + i]
-  const int ntiles = (r + kSolveRows - 1) / kSolveRows;
-  const double* Ps = P + pptr[s] * nrhs;
-  for (int idx = tid; idx < w * nrhs; idx += blockDim.x) {
-    const int a = idx % w, rr = idx / w;
-    double v = x[f0 + a + static_cast<int64_t>(rr) * n];
-    for (int t = 0; t < ntiles; ++t) v -= Ps[(static_cast<int64_t>(t) * w) * nrhs + rr * w + a];
-    bJ[rr * w + a] = v;
+  if (r <= kSolveFuseRows) {  // b_J = y_J − L_RJᵀ x_R here (no off-diagonal tiles)
+    double* xR = Lb + 64 * 65;  // [rr*r + i]
+    const int32_t* srows = sd.sn_rows + sd.sn_rptr[s] + w;
+    for (int idx = tid; idx < r * nrhs; idx += blockDim.x) {
+      const int i = idx % r, rr = idx / r;
+      xR[rr * r + i] = x[srows[i] + static_cast<int64_t>(rr) * n];
+    }
+    __syncthreads();
+    for (int j = warp; j < w; j += 8) {
+      const double* col = Ls + w + static_cast<int64_t>(j) * rows;
+      double acc[NR];
+#pragma unroll
+      for (int rr = 0; rr < NR; ++rr) acc[rr] = 0.0;
+#pragma unroll 4
+      for (int i = lane; i < r; i += 32) {
+        const double l = col[i];
+#pragma unroll
+        for (int rr = 0; rr < NR; ++rr) acc[rr] += l * xR[rr * r + i];
+      }
+#pragma unroll
+      for (int rr = 0; rr < NR; ++rr) {
+        double v = acc[rr];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0 && rr < nrhs) bJ[rr * w + j] = x[f0 + j + static_cast<int64_t>(rr) * n] - v;
+      }
+    }
+  } else {
+    const int ntiles = (r + kSolveRows - 1) / kSolveRows;
+    const double* Ps = P + pptr[s] * nrhs;
+    for (int idx = tid; idx < w * nrhs; idx += blockDim.x) {
+      const int a = idx % w, rr = idx / w;
+      double v = x[f0 + a + static_cast<int64_t>(rr) * n];
+      for (int t = 0; t < ntiles; ++t) v -= Ps[(static_cast<int64_t>(t) * w) * nrhs + rr * w + a];
+      bJ[rr * w + a] = v;
+    }
   }
   __syncthreads();
   const int nch = (w + 63) / 64;
