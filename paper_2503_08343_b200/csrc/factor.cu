@@ -265,7 +265,9 @@ void DeviceFactor::build_factor_plan() {
   std::vector<int> lvl0;
   int nlev = 0;
   chunk_levels(s, lvl0, nlev, kSmallRows);
-  std::vector<std::vector<ColTask>> ea(nlev);
+  std::vector<std::vector<EaTask>> ea(nlev);
+  std::vector<int2> ea_pairs;  // (child, first row of its update column), child order
+  std::vector<int32_t> cnt;
   std::vector<std::vector<PanelTask>> pan(nlev), po(nlev);
   // GEMM tasks per level: gm = the update of the chunk's NEXT column block (on
   // the critical chain), gr = the rest of the trailing update + the U SYRK
@@ -292,10 +294,24 @@ void DeviceFactor::build_factor_plan() {
       const int lv = lvl0[k] + c;
       const int c0 = c * kNB, wk = std::min(kNB, w - c0);
       if (c == 0 && s.ch_ptr[k + 1] > s.ch_ptr[k]) {
-        for (int b = 0; b < rows; ++b) ea[lv].push_back({k, b});
+        // front column b receives child c's update column ia where rel_c[ia] = b
+        cnt.assign(rows + 1, 0);
         for (int q = s.ch_ptr[k]; q < s.ch_ptr[k + 1]; ++q) {
-          const double rc = s.r(s.ch_list[q]);
+          const int ch = s.ch_list[q], wc = s.w(ch), rc = s.r(ch);
+          const int32_t* rel = s.relmap.data() + s.sn_rptr[ch] + wc;
+          for (int ia = 0; ia < rc; ++ia) cnt[rel[ia] + 1]++;
           ea_b[lv] += 12.0 * rc * (rc + 1.0);  // read U_c lower (8 B) + RMW target (16 B)
+        }
+        const int64_t base = static_cast<int64_t>(ea_pairs.size());
+        for (int b = 0; b < rows; ++b) {
+          if (cnt[b + 1]) ea[lv].push_back({k, b, static_cast<int32_t>(base + cnt[b]), cnt[b + 1]});
+          cnt[b + 1] += cnt[b];
+        }
+        ea_pairs.resize(base + cnt[rows]);
+        for (int q = s.ch_ptr[k]; q < s.ch_ptr[k + 1]; ++q) {
+          const int ch = s.ch_list[q], wc = s.w(ch), rc = s.r(ch);
+          const int32_t* rel = s.relmap.data() + s.sn_rptr[ch] + wc;
+          for (int ia = 0; ia < rc; ++ia) ea_pairs[base + cnt[rel[ia]]++] = make_int2(ch, ia);
         }
       }
       const int nbelow = rows - c0 - wk;
@@ -355,7 +371,7 @@ void DeviceFactor::build_factor_plan() {
           }
     }
   }
-  std::vector<ColTask> eaf;
+  std::vector<EaTask> eaf;
   std::vector<PanelTask> panf, pof;
   std::vector<GemmTask> gmf;
   std::vector<ReduceTask> rdf;
@@ -416,6 +432,7 @@ void DeviceFactor::build_factor_plan() {
     flev_[l].sm_flops = sm_f[l];
   }
   ea_.upload(eaf, stream_);
+  eap_.upload(ea_pairs, stream_);
   pan_.upload(panf, stream_);
   po_.upload(pof, stream_);
   gemm_.upload(gmf, stream_);
@@ -641,7 +658,7 @@ int32_t DeviceFactor::factor_panels() {
     if (lv.ean) {
       int blocks = static_cast<int>((lv.ean * 32 + 255) / 256);
       pf.run(sa, pf.tag("factor.extend_add", lvl), 0.0, lv.ea_bytes, [&] {
-        k_extend_add<<<blocks, 256, 0, sa>>>(ea_.p + lv.ea0, static_cast<int>(lv.ean), sd,
+        k_extend_add<<<blocks, 256, 0, sa>>>(ea_.p + lv.ea0, static_cast<int>(lv.ean), eap_.p, sd,
                                                  L_.p, U_.p);
       });
       ++launches_numeric_;

@@ -127,7 +127,8 @@ class DeviceFactor {
   };
   DevBuf<int32_t> small_;
   std::vector<FLevel> flev_;
-  DevBuf<ColTask> ea_;
+  DevBuf<EaTask> ea_;
+  DevBuf<int2> eap_;
   DevBuf<PanelTask> pan_, po_;
   DevBuf<GemmTask> gemm_;
 

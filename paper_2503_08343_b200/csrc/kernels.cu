@@ -161,7 +161,9 @@ __global__ void __launch_bounds__(128, 4) k_gemm_tiles(const GemmTask* __restric
 // (panel step: panel.cuh)
 // ---------------------------------------------------------------------------
 // Extend-add (multifrontal assembly), gather form: one warp per (front, front
-// column). Children are visited in ascending order, so every target entry
+// column) that some child updates; the plan lists the contributing children
+// and the row where each child's update column starts (no searching on the
+// device). Children are visited in ascending order, so every target entry
 // receives its contributions in a fixed order (deterministic, no atomics).
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ int find_sorted(const int32_t* a, int len, int key) {
@@ -173,26 +175,27 @@ __device__ __forceinline__ int find_sorted(const int32_t* a, int len, int key) {
   return (lo < len && a[lo] == key) ? lo : -1;
 }
 
-__global__ void k_extend_add(const ColTask* __restrict__ tasks, int ntasks, SymDev sd,
-                             double* __restrict__ L, double* __restrict__ U) {
+__global__ void k_extend_add(const EaTask* __restrict__ tasks, int ntasks,
+                             const int2* __restrict__ pairs, SymDev sd, double* __restrict__ L,
+                             double* __restrict__ U) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= ntasks) return;
-  const int s = tasks[warp].sn, b = tasks[warp].col;
+  const EaTask t = tasks[warp];
+  const int s = t.sn, b = t.col;
   const int w = sd.sn_first[s + 1] - sd.sn_first[s];
   const int rows = static_cast<int>(sd.sn_rptr[s + 1] - sd.sn_rptr[s]);
   const int r = rows - w;
   double* Ls = L + sd.lptr[s];
   double* Us = U + sd.uptr[s];
-  for (int q = sd.ch_ptr[s]; q < sd.ch_ptr[s + 1]; ++q) {
-    const int c = sd.ch_list[q];
+  double* dst = b < w ? Ls + static_cast<int64_t>(b) * rows : Us + static_cast<int64_t>(b - w) * r - w;
+  for (int p = t.p0; p < t.p0 + t.np; ++p) {
+    const int2 cp = pairs[p];
+    const int c = cp.x, ib = cp.y;
     const int wc = sd.sn_first[c + 1] - sd.sn_first[c];
     const int rc = static_cast<int>(sd.sn_rptr[c + 1] - sd.sn_rptr[c]) - wc;
     const int32_t* rel = sd.relmap + sd.sn_rptr[c] + wc;
-    const int ib = find_sorted(rel, rc, b);
-    if (ib < 0) continue;
     const double* Uc = U + sd.uptr[c] + static_cast<int64_t>(ib) * rc;
-    double* dst = b < w ? Ls + static_cast<int64_t>(b) * rows : Us + static_cast<int64_t>(b - w) * r - w;
     // 4 independent gathers in flight per lane (memory-level parallelism)
     int ia = ib + lane;
     for (; ia + 96 < rc; ia += 128) {

@@ -44,7 +44,17 @@ struct PanelTask {
   int32_t gcol;       // internal index of the chunk's first column
 };
 
-// Extend-add / Σ-gather work item: one (supernode, front column) pair.
+// Extend-add work item: one front column b of supernode sn, receiving the
+// children listed in pairs[p0 .. p0+np) = (child, first row index in the
+// child's update column) in child order.
+struct EaTask {
+  int32_t sn;
+  int32_t col;
+  int32_t p0;
+  int32_t np;
+};
+
+// Σ-gather work item: one (supernode, front column) pair.
 struct ColTask {
   int32_t sn;
   int32_t col;
