@@ -87,6 +87,28 @@ __global__ void k_st_assemble(const i64* __restrict__ pcp, const i32* __restrict
 //   L[qmap[p]] = base[p] + Σ_{r ∈ col_J(R) ∩ col_J(C)} λ J_rR J_rC
 // (gauss_newton.hpp:137-138, :231-232). The JᵀΛJ entry is a merge of two
 // sorted J columns: no atomics, fixed summation order.
+// JᵀΛJ through a precomputed product map: for master-pattern entry p (lower
+// half only), pairs [off[p], off[p+1]) are the J value indices of the rows
+// shared by J columns R and C, ascending — the same terms in the same order as
+// the merge in k_fill_panels, so the result is bit-identical, without the
+// dependent index chasing.
+__global__ void k_fill_panels_map(i64 np, const i64* __restrict__ qmap,
+                                  const double* __restrict__ base, const i32* __restrict__ off,
+                                  const int2* __restrict__ pairs, const double* __restrict__ jv,
+                                  double lam, double* __restrict__ L) {
+  for (i64 p = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; p < np;
+       p += static_cast<i64>(gridDim.x) * blockDim.x) {
+    const i64 o = qmap[p];
+    if (o < 0) continue;
+    double s = 0.0;
+    for (i32 k = off[p]; k < off[p + 1]; ++k) {
+      const int2 ab = pairs[k];
+      s += lam * jv[ab.x] * jv[ab.y];
+    }
+    L[o] = base[p] + s;
+  }
+}
+
 __global__ void k_fill_panels(const i64* __restrict__ pcp, const i32* __restrict__ pri, int N,
                               const i64* __restrict__ qmap, const double* __restrict__ base,
                               const i64* __restrict__ jcp, const i32* __restrict__ jri,
@@ -490,6 +512,30 @@ void SpaceTimePosterior::build_host() {
         jri_[q] = r;
         jmap_[q] = p;
       }
+    // JᵀΛJ product map over the master pattern's lower-stored entries
+    const std::vector<i64>& qm = sym_->qmap;
+    jt_off_.assign(pri_.size() + 1, 0);
+    jt_pairs_.clear();
+    for (int C = 0; C < n_; ++C)
+      for (i64 p = pcp_[C]; p < pcp_[C + 1]; ++p) {
+        if (qm[p] >= 0) {
+          const int R = pri_[p];
+          i64 x = jcp_[R], xe = jcp_[R + 1], y = jcp_[C], ye = jcp_[C + 1];
+          while (x < xe && y < ye) {
+            if (jri_[x] < jri_[y]) {
+              ++x;
+            } else if (jri_[y] < jri_[x]) {
+              ++y;
+            } else {
+              jt_pairs_.push_back({static_cast<i32>(jmap_[x]), static_cast<i32>(jmap_[y])});
+              ++x;
+              ++y;
+            }
+          }
+        }
+        require(jt_pairs_.size() < (1ull << 31), kContract, "JtJ map exceeds int32");
+        jt_off_[p + 1] = static_cast<i32>(jt_pairs_.size());
+      }
   }
 }
 
@@ -537,6 +583,12 @@ void SpaceTimePosterior::assemble_device() {
     d_ml_.upload(lumped_mass(m), stream_);
   }
   if (spec_.residual != 0) {
+    d_jt_off_.upload(jt_off_, stream_);
+    {
+      std::vector<int2> pr(jt_pairs_.size());
+      for (size_t i = 0; i < pr.size(); ++i) pr[i] = make_int2(jt_pairs_[i].first, jt_pairs_[i].second);
+      d_jt_pairs_.upload(pr, stream_);
+    }
     d_jrp_.upload(jrp_, stream_);
     d_jci_.upload(jci_, stream_);
     d_jcp_.upload(jcp_, stream_);
@@ -633,9 +685,14 @@ void SpaceTimePosterior::fill_panels(const double* base, bool with_jacobian) {
   const double np = static_cast<double>(pri_.size());
   const double bytes = 24.0 * np + (with_jacobian ? 20.0 * static_cast<double>(jci_.size()) : 0.0);
   prof_.run(stream_, with_jacobian ? "update.h_jtlj" : "update.q_base", 0.0, bytes, [&] {
-    k_fill_panels<<<grid_for(n_), 256, 0, stream_>>>(
-        d_pcp_.p, d_pri_.p, n_, fac_->d_qmap(), base, with_jacobian ? d_jcp_.p : nullptr,
-        d_jri_.p, d_jmap_.p, d_jv_.p, spec_.pde_noise_prec, fac_->d_l());
+    if (with_jacobian)
+      k_fill_panels_map<<<grid_for(static_cast<i64>(pri_.size())), 256, 0, stream_>>>(
+          static_cast<i64>(pri_.size()), fac_->d_qmap(), base, d_jt_off_.p, d_jt_pairs_.p,
+          d_jv_.p, spec_.pde_noise_prec, fac_->d_l());
+    else
+      k_fill_panels<<<grid_for(n_), 256, 0, stream_>>>(d_pcp_.p, d_pri_.p, n_, fac_->d_qmap(),
+                                                       base, nullptr, d_jri_.p, d_jmap_.p, d_jv_.p,
+                                                       spec_.pde_noise_prec, fac_->d_l());
   });
   times_.kernel_launches += 1;
 }

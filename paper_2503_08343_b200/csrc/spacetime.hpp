@@ -132,10 +132,13 @@ class SpaceTimePosterior {
   std::vector<i64> jcp_;      // J CSC column pointers
   std::vector<i32> jri_;      // J CSC rows
   std::vector<i64> jmap_;     // CSC position -> CSR value index
+  std::vector<i32> jt_off_;   // JᵀΛJ product map: pattern entry -> pair range
+  std::vector<std::pair<i32, i32>> jt_pairs_;  // (J value index, J value index)
 
   // device
   DevBuf<i64> d_pcp_, d_qmap_, d_scp_, d_srp_, d_jrp_, d_jcp_, d_jmap_;
-  DevBuf<i32> d_pri_, d_sri_, d_sci_, d_jci_, d_jri_, kept_;
+  DevBuf<i32> d_pri_, d_sri_, d_sci_, d_jci_, d_jri_, kept_, d_jt_off_;
+  DevBuf<int2> d_jt_pairs_;
   DevBuf<double> d_qcond_, d_qeff_, d_sv_, d_svr_, d_jv_;
   DevBuf<i64> d_blk_cp_;
   DevBuf<i32> d_blk_ri_;
