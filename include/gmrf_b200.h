@@ -119,6 +119,51 @@ int gmrf_factor_l(gmrf_factor_t* f, int64_t* col_ptr, int32_t* row_idx, double* 
 int gmrf_factor_stats(const gmrf_factor_t* f, gmrf_factor_stats_t* st);
 void gmrf_factor_free(gmrf_factor_t* f);
 
+/* ---- Partitioned factorization across ranks (multi-GPU) -----
+ * No reference analogue (the reference is single-threaded):
+ * the supernodal tree is split along its top nested-dissection separators
+ * (subtree-to-subcube: whole subtrees per rank, each separator on the lowest
+ * rank of the range below it). A partitioned handle behaves like a
+ * gmrf_factor_t — gmrf_factor_numeric*, gmrf_solve*, gmrf_selinv_diag* keep
+ * their semantics and return complete results on every rank — but stores
+ * and factors only its own supernodes. Cross-rank data (Schur complements
+ * child → parent in the factorization, update vectors in the forward solve,
+ * x rows parent → child in the backward solve, Σ blocks parent → child in
+ * the selected inversion) moves through a caller-supplied exchange function,
+ * e.g. torch.distributed over NCCL (paper_2503_08343_b200/partition.py). */
+enum { GMRF_MSG_SEND = 0, GMRF_MSG_RECV = 1, GMRF_MSG_ALLREDUCE_SUM_F64 = 2,
+       GMRF_MSG_ALLREDUCE_MIN_I32 = 3 };
+enum { GMRF_PHASE_FACTOR = 0, GMRF_PHASE_FSOLVE = 1, GMRF_PHASE_BSOLVE = 2,
+       GMRF_PHASE_SELINV = 3 };
+
+typedef struct {
+  int32_t kind;   /* GMRF_MSG_* */
+  int32_t peer;   /* other rank (send / recv), -1 for all-reduces */
+  int32_t tag;    /* child supernode of the cross edge, -1 for all-reduces */
+  int32_t phase;  /* GMRF_PHASE_*, -1 for all-reduces */
+  void* dptr;     /* device buffer */
+  int64_t count;  /* elements (double, or int32 for ALLREDUCE_MIN_I32) */
+} gmrf_msg_t;
+
+/* Called at every exchange point with this rank's messages of that point, in
+ * the same order on both sides of each pair. It must complete the messages, or
+ * enqueue them on `cuda_stream` so that later work on that stream sees them,
+ * and return 0. All-reduces are called on every rank. */
+typedef int (*gmrf_exchange_fn)(void* ctx, const gmrf_msg_t* msgs, int32_t count,
+                                void* cuda_stream);
+
+/* Owner rank of each supernode (ns entries) for nranks ranks. Host only. */
+int gmrf_partition_owners(const gmrf_symbolic_t* s, int32_t nranks, int32_t* owner);
+/* The full cross-edge message schedule for an owner map (host only, tests):
+ * rows of 6 int64 (phase, point, src, dst, child supernode, count [per RHS
+ * for the solve phases]). Call with rows == NULL for the count. */
+int gmrf_partition_schedule(const gmrf_symbolic_t* s, const int32_t* owner, int64_t* rows,
+                            int64_t* n_rows);
+/* This rank's share of the factor. owner == NULL: gmrf_partition_owners. */
+int gmrf_factor_create_partitioned(const gmrf_symbolic_t* s, int32_t nranks, int32_t rank,
+                                   const int32_t* owner, gmrf_exchange_fn fn, void* ctx,
+                                   gmrf_factor_t** out);
+
 /* FP64 issue-rate microbenchmark (TFLOP/s) of DMMA m8n8k4 and DFMA. */
 int gmrf_bench_fp64(double* dmma_tflops, double* dfma_tflops);
 
@@ -197,6 +242,12 @@ int gmrf_spacetime_jacobian_nnz(const gmrf_spacetime_t* h, int64_t* nnz);
 int gmrf_spacetime_jacobian(gmrf_spacetime_t* h, const double* u, int64_t* row_ptr,
                             int32_t* col_idx, double* values);
 void gmrf_spacetime_free(gmrf_spacetime_t* h);
+/* The same pipeline with this rank's share of a partitioned factorization
+ * (see gmrf_factor_create_partitioned); assembly, residuals and the line
+ * search are replicated, every rank returns the complete mean and variances. */
+int gmrf_spacetime_create_partitioned(const gmrf_spacetime_config_t* cfg, int32_t nranks,
+                                      int32_t rank, gmrf_exchange_fn fn, void* ctx,
+                                      gmrf_spacetime_t** out);
 
 /* Per-kernel-class profile of the following runs (CUDA events on the launch
  * stream around every launch; ALGORITHMIC flops and bytes per class). */

@@ -73,6 +73,16 @@ class SpaceTimeInfo(C.Structure):
 
 vp = C.c_void_p
 
+
+class Msg(C.Structure):
+    """gmrf_msg_t: one message of an exchange point of a partitioned factor."""
+    _fields_ = [("kind", C.c_int32), ("peer", C.c_int32), ("tag", C.c_int32),
+                ("phase", C.c_int32), ("dptr", C.c_void_p), ("count", C.c_int64)]
+
+
+# int (*gmrf_exchange_fn)(void* ctx, const gmrf_msg_t* msgs, int32_t count, void* cuda_stream)
+EXCHANGE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(Msg), C.c_int32, C.c_void_p)
+
 # name -> (restype, argtypes); every symbol include/gmrf_b200.h declares.
 SIGNATURES = {
     "gmrf_last_error": (C.c_char_p, []),
@@ -97,6 +107,12 @@ SIGNATURES = {
     "gmrf_factor_stats": (C.c_int, [C.c_void_p, C.POINTER(FactorStats)]),
     "gmrf_factor_free": (None, [C.c_void_p]),
     "gmrf_bench_fp64": (C.c_int, [f64p, f64p]),
+    "gmrf_partition_owners": (C.c_int, [vp, C.c_int32, i32p]),
+    "gmrf_partition_schedule": (C.c_int, [vp, i32p, i64p, i64p]),
+    "gmrf_factor_create_partitioned": (C.c_int, [vp, C.c_int32, C.c_int32, i32p, EXCHANGE_FN, vp,
+                                                 C.POINTER(vp)]),
+    "gmrf_spacetime_create_partitioned": (C.c_int, [C.POINTER(SpaceTimeConfig), C.c_int32,
+                                                    C.c_int32, EXCHANGE_FN, vp, C.POINTER(vp)]),
     "gmrf_spacetime_create": (C.c_int, [C.POINTER(SpaceTimeConfig), C.POINTER(vp)]),
     "gmrf_spacetime_run": (C.c_int, [vp, f64p, C.c_int32, f64p, f64p, C.POINTER(GnIter),
                                      C.c_int32, i32p, i32p]),

@@ -2,13 +2,19 @@
 #include "../../include/gmrf_b200.h"
 
 #include <algorithm>
+#include <cstddef>
 #include <cstring>
 #include <memory>
 #include <string>
 #include <tuple>
 
 #include "factor.hpp"
+#include "partition.hpp"
 #include "spacetime.hpp"
+
+static_assert(sizeof(gmrf_msg_t) == sizeof(gmrf::XferMsg), "gmrf_msg_t layout");
+static_assert(offsetof(gmrf_msg_t, dptr) == offsetof(gmrf::XferMsg, dptr), "gmrf_msg_t layout");
+static_assert(offsetof(gmrf_msg_t, count) == offsetof(gmrf::XferMsg, count), "gmrf_msg_t layout");
 #include "symbolic.hpp"
 
 struct gmrf_symbolic {
@@ -120,6 +126,54 @@ int gmrf_factor_create(const gmrf_symbolic_t* h, gmrf_factor_t** out) {
   });
 }
 
+int gmrf_partition_owners(const gmrf_symbolic_t* h, int32_t nranks, int32_t* owner) {
+  return guard([&] {
+    gmrf::require(nranks >= 1, gmrf::kContract, "partition: nranks < 1");
+    auto o = gmrf::partition_owners(*h->s, nranks);
+    std::copy(o.begin(), o.end(), owner);
+  });
+}
+
+int gmrf_partition_schedule(const gmrf_symbolic_t* h, const int32_t* owner, int64_t* rows,
+                            int64_t* n_rows) {
+  return guard([&] {
+    const gmrf::Symbolic& s = *h->s;
+    std::vector<int32_t> o(owner, owner + s.ns);
+    auto e = gmrf::partition_schedule(s, o);
+    if (n_rows) *n_rows = static_cast<int64_t>(e.size());
+    if (rows)
+      for (size_t i = 0; i < e.size(); ++i) {
+        int64_t* r = rows + 6 * i;
+        r[0] = e[i].phase;
+        r[1] = e[i].point;
+        r[2] = e[i].src;
+        r[3] = e[i].dst;
+        r[4] = e[i].sn;
+        r[5] = e[i].count;
+      }
+  });
+}
+
+int gmrf_factor_create_partitioned(const gmrf_symbolic_t* h, int32_t nranks, int32_t rank,
+                                   const int32_t* owner, gmrf_exchange_fn fn, void* ctx,
+                                   gmrf_factor_t** out) {
+  return guard([&] {
+    auto f = std::make_unique<gmrf_factor>();
+    f->s = h->s;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+      gmrf::fail(gmrf::kCuda, "no CUDA device: libgmrf_b200 has no CPU fallback");
+    gmrf::PartitionSpec ps;
+    ps.nranks = nranks;
+    ps.rank = rank;
+    if (owner) ps.owner.assign(owner, owner + h->s->ns);
+    ps.fn = reinterpret_cast<gmrf::ExchangeFn>(fn);
+    ps.ctx = ctx;
+    f->f = std::make_unique<gmrf::DeviceFactor>(h->s, nullptr, &ps);
+    *out = f.release();
+  });
+}
+
 int gmrf_factor_set_stream(gmrf_factor_t* f, void* stream) {
   return guard([&] { f->f->set_stream(static_cast<cudaStream_t>(stream)); });
 }
@@ -177,6 +231,7 @@ int gmrf_selinv_pattern_nnz(gmrf_factor_t* f, int64_t* nnz) {
 int gmrf_selinv_pattern(gmrf_factor_t* f, int64_t* cp, int32_t* ri, double* v) {
   return guard([&] {
     gmrf::require(f->f->has_selinv(), gmrf::kContract, "selinv_pattern: run selinv first");
+    gmrf::require(!f->f->partitioned(), gmrf::kContract, "selinv_pattern: partitioned factor");
     const gmrf::Symbolic& s = *f->s;
     std::vector<double> sig;
     f->f->copy_sig_panels(sig);
@@ -206,6 +261,7 @@ int gmrf_selinv_pattern(gmrf_factor_t* f, int64_t* cp, int32_t* ri, double* v) {
 int gmrf_factor_l(gmrf_factor_t* f, int64_t* cp, int32_t* ri, double* v, int32_t* perm) {
   return guard([&] {
     gmrf::require(f->f->factored(), gmrf::kContract, "factor_l: factor not computed");
+    gmrf::require(!f->f->partitioned(), gmrf::kContract, "factor_l: partitioned factor");
     const gmrf::Symbolic& s = *f->s;
     std::vector<double> pan;
     f->f->copy_l_panels(pan);
@@ -235,7 +291,8 @@ int gmrf_bench_fp64(double* a, double* b) {
   return guard([&] { gmrf::bench_fp64(a, b); });
 }
 
-int gmrf_spacetime_create(const gmrf_spacetime_config_t* c, gmrf_spacetime_t** out) {
+static int spacetime_create(const gmrf_spacetime_config_t* c, const gmrf::PartitionSpec* part,
+                            gmrf_spacetime_t** out) {
   return guard([&] {
     gmrf::SpaceTimeSpec s;
     s.n_el = c->n_el;
@@ -263,9 +320,24 @@ int gmrf_spacetime_create(const gmrf_spacetime_config_t* c, gmrf_spacetime_t** o
     h->cfg.armijo_c = c->gn_armijo_c;
     h->cfg.shrink = c->gn_shrink;
     h->cfg.max_backtracks = c->gn_max_backtracks;
-    h->p = std::make_unique<gmrf::SpaceTimePosterior>(s);
+    h->p = std::make_unique<gmrf::SpaceTimePosterior>(s, nullptr, part);
     *out = h.release();
   });
+}
+
+int gmrf_spacetime_create(const gmrf_spacetime_config_t* c, gmrf_spacetime_t** out) {
+  return spacetime_create(c, nullptr, out);
+}
+
+int gmrf_spacetime_create_partitioned(const gmrf_spacetime_config_t* c, int32_t nranks,
+                                      int32_t rank, gmrf_exchange_fn fn, void* ctx,
+                                      gmrf_spacetime_t** out) {
+  gmrf::PartitionSpec ps;
+  ps.nranks = nranks;
+  ps.rank = rank;
+  ps.fn = reinterpret_cast<gmrf::ExchangeFn>(fn);
+  ps.ctx = ctx;
+  return spacetime_create(c, &ps, out);
 }
 
 int gmrf_spacetime_run(gmrf_spacetime_t* h, const double* u0, int32_t want_var, double* mean,

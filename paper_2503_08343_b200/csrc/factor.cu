@@ -75,10 +75,51 @@ inline double tile_flops(const GemmTask& g, bool diag) {
 }
 }  // namespace
 
-DeviceFactor::DeviceFactor(std::shared_ptr<const Symbolic> sym, cudaStream_t stream)
+DeviceFactor::DeviceFactor(std::shared_ptr<const Symbolic> sym, cudaStream_t stream,
+                           const PartitionSpec* part)
     : sym_(std::move(sym)), stream_(stream) {
   set_smem_attrs();
   const Symbolic& s = *sym_;
+  if (part && part->nranks > 1) {
+    require(part->rank >= 0 && part->rank < part->nranks, kContract, "partition: bad rank");
+    require(part->fn != nullptr, kContract, "partition: no exchange function");
+    part_ = true;
+    nranks_ = part->nranks;
+    rank_ = part->rank;
+    owner_ = part->owner.empty() ? partition_owners(s, nranks_) : part->owner;
+    require(static_cast<i32>(owner_.size()) == s.ns, kContract, "partition: owner size");
+    for (i32 o : owner_) require(o >= 0 && o < nranks_, kContract, "partition: owner out of range");
+    xfn_ = part->fn;
+    xctx_ = part->ctx;
+    for (const XEdge& e : partition_schedule(s, owner_))
+      if (e.src == rank_ || e.dst == rank_) sched_.push_back(e);
+  }
+  // storage offsets: panels of owned supernodes; update matrices of owned
+  // supernodes and of the other ranks' children of owned supernodes (the
+  // Schur complements received before their extend-add)
+  lptr_h_.assign(s.ns + 1, 0);
+  uptr_h_.assign(s.ns + 1, 0);
+  for (int k = 0; k < s.ns; ++k) {
+    const int p = s.sn_parent[k];
+    const bool hu = mine(k) || (p >= 0 && mine(p));
+    lptr_h_[k + 1] = lptr_h_[k] + (mine(k) ? static_cast<i64>(s.rows(k)) * s.w(k) : 0);
+    uptr_h_[k + 1] = uptr_h_[k] + (hu ? static_cast<i64>(s.r(k)) * s.r(k) : 0);
+  }
+  std::vector<i64> qm;
+  if (part_) {  // Q entries of other ranks' supernodes are not stored here
+    qm.resize(s.qmap.size());
+    for (size_t p = 0; p < s.qmap.size(); ++p) {
+      const i64 o = s.qmap[p];
+      qm[p] = -1;
+      if (o < 0) continue;
+      const int k = static_cast<int>(std::upper_bound(s.lptr.begin(), s.lptr.end(), o) -
+                                     s.lptr.begin()) - 1;
+      if (mine(k)) qm[p] = o - s.lptr[k] + lptr_h_[k];
+    }
+    std::vector<char> cm(s.n);
+    for (int j = 0; j < s.n; ++j) cm[j] = mine(s.col2sn[j]) ? 1 : 0;
+    colmine_.upload(cm, stream_);
+  }
   first_.upload(s.sn_first, stream_);
   rows_.upload(s.sn_rows, stream_);
   relmap_.upload(s.relmap, stream_);
@@ -88,23 +129,25 @@ DeviceFactor::DeviceFactor(std::shared_ptr<const Symbolic> sym, cudaStream_t str
   col2sn_.upload(s.col2sn, stream_);
   snparent_.upload(s.sn_parent, stream_);
   rptr_.upload(s.sn_rptr, stream_);
-  lptr_.upload(s.lptr, stream_);
-  uptr_.upload(s.uptr, stream_);
-  qmap_.upload(s.qmap, stream_);
+  lptr_.upload(lptr_h_, stream_);
+  uptr_.upload(uptr_h_, stream_);
+  qmap_.upload(part_ ? qm : s.qmap, stream_);
   status_.alloc(1);
   diag_.alloc(std::max(s.n, 1));
   rdiag_.alloc(std::max(s.n, 1));
-  L_.alloc(std::max<int64_t>(s.lptr[s.ns], 1));
-  U_.alloc(std::max<int64_t>(s.uptr[s.ns], 1));
+  L_.alloc(std::max<int64_t>(lptr_h_[s.ns], 1));
+  U_.alloc(std::max<int64_t>(uptr_h_[s.ns], 1));
   q_.alloc(std::max<size_t>(s.qri.size(), 1));
   // solve schedule: supernodes grouped by tree level
   lvl_ptr_.assign(s.n_levels + 1, 0);
-  for (int k = 0; k < s.ns; ++k) lvl_ptr_[s.sn_level[k] + 1]++;
+  for (int k = 0; k < s.ns; ++k)
+    if (mine(k)) lvl_ptr_[s.sn_level[k] + 1]++;
   for (int l = 0; l < s.n_levels; ++l) lvl_ptr_[l + 1] += lvl_ptr_[l];
-  std::vector<int32_t> lsn(s.ns);
+  std::vector<int32_t> lsn(lvl_ptr_[s.n_levels]);
   {
     std::vector<int64_t> nx(lvl_ptr_.begin(), lvl_ptr_.end() - 1);
-    for (int k = 0; k < s.ns; ++k) lsn[nx[s.sn_level[k]]++] = k;
+    for (int k = 0; k < s.ns; ++k)
+      if (mine(k)) lsn[nx[s.sn_level[k]]++] = k;
   }
   // wide supernodes go last in their level and get one CTA per 64-row block of
   // the triangle (solve_wide.cuh); a launch holds at most wide_cap CTAs so all
@@ -153,10 +196,14 @@ DeviceFactor::DeviceFactor(std::shared_ptr<const Symbolic> sym, cudaStream_t str
   maxw_ = 1;  // widest supernode solved by the one-CTA triangle kernels
   for (int k = 0; k < s.ns; ++k) {
     const int r = s.r(k), nt = (r + kSolveRows - 1) / kSolveRows;
-    up[k + 1] = up[k] + r;
-    pp[k + 1] = pp[k] + static_cast<int64_t>(nt) * s.w(k);
+    const int p = s.sn_parent[k];
+    up[k + 1] = up[k] + ((mine(k) || (p >= 0 && mine(p))) ? r : 0);
+    pp[k + 1] = pp[k] + (mine(k) ? static_cast<int64_t>(nt) * s.w(k) : 0);
+    // over ALL supernodes: the right-hand-side blocking derived from it must be
+    // the same on every rank of a partition (same exchange sequence)
     if (!is_wide(k)) maxw_ = std::max(maxw_, s.w(k));
   }
+  uvptr_h_ = up;
   uv_total_ = up[s.ns];
   p_total_ = pp[s.ns];
   uvptr_.upload(up, stream_);
@@ -195,8 +242,33 @@ DeviceFactor::DeviceFactor(std::shared_ptr<const Symbolic> sym, cudaStream_t str
   // solve traffic per level: the L panel (8 B/entry, lower trapezoid) + row indices
   lvl_bytes_.assign(s.n_levels, 0.0);
   for (int k = 0; k < s.ns; ++k) {
+    if (!mine(k)) continue;
     const double w = s.w(k), rows = s.rows(k);
     lvl_bytes_[s.sn_level[k]] += 8.0 * (w * rows - w * (w - 1.0) / 2.0) + 4.0 * rows;
+  }
+  if (part_) {  // backward-solve exchange: x rows packed per cross edge
+    std::vector<RowXfer> pk, un;
+    std::vector<std::vector<RowXfer>> pkl(s.n_levels), unl(s.n_levels);
+    int64_t off = 0;
+    for (const XEdge& e : sched_) {
+      if (e.phase != kXBsolve) continue;
+      const RowXfer t{rows_.p + s.sn_rptr[e.sn] + s.w(e.sn), static_cast<int32_t>(e.count), off};
+      bx_off_.push_back(off);
+      (e.src == rank_ ? pkl : unl)[e.point].push_back(t);
+      off += e.count;
+    }
+    bx_.assign(s.n_levels, {});
+    std::vector<RowXfer> all;
+    for (int l = 0; l < s.n_levels; ++l) {
+      bx_[l].pk0 = static_cast<int64_t>(all.size());
+      bx_[l].pkn = static_cast<int64_t>(pkl[l].size());
+      all.insert(all.end(), pkl[l].begin(), pkl[l].end());
+      bx_[l].up0 = static_cast<int64_t>(all.size());
+      bx_[l].upn = static_cast<int64_t>(unl[l].size());
+      all.insert(all.end(), unl[l].begin(), unl[l].end());
+    }
+    xt_.upload(all, stream_);
+    xb_.alloc(std::max<int64_t>(off * kMaxRhs, 1));
   }
   build_factor_plan();
   {  // lookahead streams: the critical chain at high priority, the bulk updates low
@@ -243,28 +315,11 @@ int64_t DeviceFactor::device_bytes() const {
          static_cast<int64_t>(gemm_.n * sizeof(GemmTask) + sgemm_.n * sizeof(GemmTask));
 }
 
-// Chunk levels: chunk k of supernode s sits at lvl0(s)+k where lvl0(s) is one
-// above the last chunk of its deepest child. Small fronts (rows ≤ small_rows)
-// are factored whole by one CTA and occupy a single level.
-static void chunk_levels(const Symbolic& s, std::vector<int>& lvl0, int& nlev,
-                         int small_rows = 0) {
-  lvl0.assign(s.ns, 0);
-  std::vector<int> last(s.ns, 0);
-  nlev = 0;
-  for (int k = 0; k < s.ns; ++k) {
-    int l = 0;
-    for (int q = s.ch_ptr[k]; q < s.ch_ptr[k + 1]; ++q) l = std::max(l, last[s.ch_list[q]] + 1);
-    lvl0[k] = l;
-    last[k] = s.rows(k) <= small_rows ? l : l + nchunks(s.w(k)) - 1;
-    nlev = std::max(nlev, last[k] + 1);
-  }
-}
-
 void DeviceFactor::build_factor_plan() {
   const Symbolic& s = *sym_;
-  std::vector<int> lvl0;
+  std::vector<int> lvl0, last;
   int nlev = 0;
-  chunk_levels(s, lvl0, nlev, kSmallRows);
+  chunk_levels(s, lvl0, last, nlev, kSmallRows);
   std::vector<std::vector<EaTask>> ea(nlev);
   std::vector<int2> ea_pairs;  // (child, first row of its update column), child order
   std::vector<int32_t> cnt;
@@ -279,7 +334,18 @@ void DeviceFactor::build_factor_plan() {
       gr_f(nlev, 0.0), sm_f(nlev, 0.0);
   double* L = L_.p;
   double* U = U_.p;
+  std::vector<int64_t> gpan(3 * static_cast<size_t>(nlev), 0);  // panel tasks of all ranks
   for (int k = 0; k < s.ns; ++k) {
+    const int w = s.w(k), rows = s.rows(k);
+    if (rows <= kSmallRows) continue;
+    for (int c = 0; c < nchunks(w); ++c) {
+      const int c0 = c * kNB, wk = std::min(kNB, w - c0), nbelow = rows - c0 - wk;
+      gpan[3 * (lvl0[k] + c) + (wk <= 16 ? 0 : (wk <= 32 ? 1 : 2))] +=
+          std::max(1, (nbelow + kTrsmRows - 1) / kTrsmRows);
+    }
+  }
+  for (int k = 0; k < s.ns; ++k) {
+    if (!mine(k)) continue;
     const int w = s.w(k), rows = s.rows(k), r = rows - w;
     if (rows <= kSmallRows) {  // fused small-front kernel, bucketed by front size
       const int lv = lvl0[k];
@@ -287,8 +353,8 @@ void DeviceFactor::build_factor_plan() {
       for (int j = 0; j < w; ++j) sm_f[lv] += static_cast<double>(rows - j) * (rows - j);
       continue;
     }
-    double* Lk = L + s.lptr[k];
-    double* Uk = U + s.uptr[k];
+    double* Lk = L + lptr_h_[k];
+    double* Uk = U + uptr_h_[k];
     const int nch = nchunks(w);
     for (int c = 0; c < nch; ++c) {
       const int lv = lvl0[k] + c;
@@ -430,6 +496,7 @@ void DeviceFactor::build_factor_plan() {
       smf.insert(smf.end(), sm[bk][l].begin(), sm[bk][l].end());
     }
     flev_[l].sm_flops = sm_f[l];
+    for (int bk = 0; bk < 3; ++bk) flev_[l].prow[bk] = gpan[3 * l + bk] <= kRowsMaxCtas;
   }
   ea_.upload(eaf, stream_);
   eap_.upload(ea_pairs, stream_);
@@ -438,15 +505,20 @@ void DeviceFactor::build_factor_plan() {
   gemm_.upload(gmf, stream_);
   red_.upload(rdf, stream_);
   small_.upload(smf, stream_);
+  fx_.assign(nlev, {});
+  for (const XEdge& e : sched_)
+    if (e.phase == kXFactor)
+      fx_[e.point].push_back({e.src == rank_ ? 0 : 1, e.src == rank_ ? e.dst : e.src, e.sn,
+                              kXFactor, U + uptr_h_[e.sn], e.count});
 }
 
 void DeviceFactor::build_selinv_plan() {
   const Symbolic& s = *sym_;
-  Sig_.alloc(std::max<int64_t>(s.lptr[s.ns], 1));
-  std::vector<int> lvl0;
+  Sig_.alloc(std::max<int64_t>(lptr_h_[s.ns], 1));
+  std::vector<int> lvl0, last;
   int nlev = 0;
-  chunk_levels(s, lvl0, nlev);
-  std::vector<std::vector<ColTask>> ga(nlev);
+  chunk_levels(s, lvl0, last, nlev, 0);
+  std::vector<std::vector<ColTask>> ga(nlev), gg(nlev);
   std::vector<std::vector<GemmTask>> yg(nlev), zg(nlev);
   std::vector<std::vector<SelChunk>> tr(nlev), dg(nlev), mi(nlev);
   std::vector<double> ga_b(nlev, 0.0), y_f(nlev, 0.0), t_f(nlev, 0.0), z_f(nlev, 0.0),
@@ -456,15 +528,25 @@ void DeviceFactor::build_selinv_plan() {
   double* S = Sig_.p;
   for (int k = 0; k < s.ns; ++k) {
     const int w = s.w(k), rows = s.rows(k), r = rows - w;
-    double* Lk = L + s.lptr[k];
-    double* Sk = S + s.lptr[k];
-    double* Uk = U + s.uptr[k];
+    const int par = s.sn_parent[k];
+    if (!mine(k)) {
+      // another rank's child of an owned supernode: its Σ_RR is gathered here
+      // from the parent's Σ front once the parent is done, then sent
+      if (par >= 0 && mine(par) && r > 0) {
+        for (int b = 0; b < r; ++b) gg[lvl0[par]].push_back({k, b});
+        ga_b[lvl0[par]] += 16.0 * r * r;
+      }
+      continue;
+    }
+    double* Lk = L + lptr_h_[k];
+    double* Sk = S + lptr_h_[k];
+    double* Uk = U + uptr_h_[k];
     const int nch = nchunks(w);
     for (int c = nch - 1; c >= 0; --c) {
       const int lv = lvl0[k] + c;
       const int c0 = c * kNB, wk = std::min(kNB, w - c0);
       const int p = w - c0 - wk;
-      if (c == nch - 1 && r > 0) {
+      if (c == nch - 1 && r > 0 && mine(par)) {  // else received from the parent's rank
         for (int b = 0; b < r; ++b) ga[lv].push_back({k, b});
         ga_b[lv] += 16.0 * r * r;  // read parent Σ entries + write Σ_RR
       }
@@ -540,6 +622,9 @@ void DeviceFactor::build_selinv_plan() {
     e.ga0 = gaf.size();
     e.gan = ga[l].size();
     gaf.insert(gaf.end(), ga[l].begin(), ga[l].end());
+    e.gg0 = gaf.size();
+    e.ggn = gg[l].size();
+    gaf.insert(gaf.end(), gg[l].begin(), gg[l].end());
     std::vector<GemmTask> gs;
     std::vector<ReduceTask> rs;
     split_k_level(yg[l], gs, rs, sparts_.p);
@@ -588,6 +673,11 @@ void DeviceFactor::build_selinv_plan() {
   strsm_.upload(trf, stream_);
   sdiag_.upload(dgf, stream_);
   smir_.upload(mif, stream_);
+  sx_.assign(nlev, {});
+  for (const XEdge& e : sched_)
+    if (e.phase == kXSelinv)
+      sx_[e.point].push_back({e.src == rank_ ? 0 : 1, e.src == rank_ ? e.dst : e.src, e.sn,
+                              kXSelinv, U + uptr_h_[e.sn], e.count});
   selinv_plan_ = true;
 }
 
@@ -670,7 +760,7 @@ int32_t DeviceFactor::factor_panels() {
       pf.run(sa, pf.tag("factor.potrf_trsm", lvl), lv.po_flops + lv.tr_flops, 0.0, [&] {
         if (lv.pbn[0]) {
           const unsigned g = static_cast<unsigned>(lv.pbn[0]);
-          if (g <= kRowsMaxCtas)
+          if (lv.prow[0])
             k_panel_rows<16, kTrsmRows><<<g, panel_rows_threads<16, kTrsmRows>(), 0, sa>>>(
                 pan_.p + lv.pb0[0], status_.p, diag_.p);
           else
@@ -679,7 +769,7 @@ int32_t DeviceFactor::factor_panels() {
         }
         if (lv.pbn[1]) {
           const unsigned g = static_cast<unsigned>(lv.pbn[1]);
-          if (g <= kRowsMaxCtas)
+          if (lv.prow[1])
             k_panel_rows<32, kTrsmRows><<<g, panel_rows_threads<32, kTrsmRows>(), 0, sa>>>(
                 pan_.p + lv.pb0[1], status_.p, diag_.p);
           else
@@ -688,7 +778,7 @@ int32_t DeviceFactor::factor_panels() {
         }
         if (lv.pbn[2]) {
           const unsigned g = static_cast<unsigned>(lv.pbn[2]);
-          if (g <= kRowsMaxCtas)
+          if (lv.prow[2])
             k_panel_rows<64, kTrsmRows><<<g, panel_rows_threads<64, kTrsmRows>(), 0, sa>>>(
                 pan_.p + lv.pb0[2], status_.p, diag_.p);
           else
@@ -720,6 +810,20 @@ int32_t DeviceFactor::factor_panels() {
       launches_numeric_ += 1 + (lv.rrn > 0);
     }
     if (la) cuda_check(cudaEventRecord(ev_rest_[li], sb), "record");
+    if (part_ && !fx_[li].empty()) {
+      // Schur complements completed at this level move to the parent's rank:
+      // join both chains into stream_, exchange there, fork again
+      if (la) {
+        cuda_check(cudaStreamWaitEvent(sa, ev_rest_[li], 0), "wait");
+        cuda_check(cudaEventRecord(ev_fork_, sa), "record");
+        cuda_check(cudaStreamWaitEvent(stream_, ev_fork_, 0), "wait");
+      }
+      exchange(fx_[li]);
+      if (la) {
+        cuda_check(cudaEventRecord(ev_fork_, stream_), "record");
+        cuda_check(cudaStreamWaitEvent(sa, ev_fork_, 0), "wait");
+      }
+    }
   }
   if (la) {  // join: the caller's stream continues after both chains
     if (!flev_.empty()) cuda_check(cudaStreamWaitEvent(sa, ev_rest_[flev_.size() - 1], 0), "wait");
@@ -734,6 +838,7 @@ int32_t DeviceFactor::factor_panels() {
     ++launches_numeric_;
   }
   cuda_check(cudaGetLastError(), "factor launch");
+  if (part_) exchange({{3, -1, -1, -1, status_.p, 1}});  // smallest failing pivot over ranks
   int st = INT_MAX;
   cuda_check(cudaMemcpyAsync(&st, status_.p, sizeof(int), cudaMemcpyDeviceToHost, stream_),
              "status read");
@@ -741,6 +846,41 @@ int32_t DeviceFactor::factor_panels() {
   factored_ = st == 0x7f7f7f7f;
   selinv_done_ = false;
   return factored_ ? -1 : s.perm[st];
+}
+
+void DeviceFactor::exchange(const std::vector<XferMsg>& m) {
+  if (m.empty()) return;
+  cuda_check(cudaGetLastError(), "launch before exchange");
+  const int rc = xfn_(xctx_, m.data(), static_cast<int32_t>(m.size()), stream_);
+  require(rc == 0, kCuda, "partitioned factor: exchange callback failed (" + std::to_string(rc) + ")");
+}
+
+// Solve exchange after supernode level `level`: forward — update vectors of
+// cross-edge children go to the parent's rank; backward — x on the child's
+// rows below its diagonal block goes from the parent's rank to the child's.
+void DeviceFactor::exchange_solve(int phase, int level, int nr, double* y) {
+  std::vector<XferMsg> m;
+  size_t be = 0;  // index among this rank's bsolve edges (bx_off_)
+  for (const XEdge& e : sched_) {
+    if (e.phase == kXBsolve) ++be;
+    if (e.phase != phase || e.point != level) continue;
+    const bool snd = e.src == rank_;
+    double* p = phase == kXFsolve ? Uv_.p + uvptr_h_[e.sn] * nr : xb_.p + bx_off_[be - 1] * nr;
+    m.push_back({snd ? 0 : 1, snd ? e.dst : e.src, e.sn, phase, p, e.count * nr});
+  }
+  if (m.empty()) return;
+  const int n = sym_->n;
+  if (phase == kXBsolve && bx_[level].pkn) {
+    k_rows_xfer<true><<<static_cast<unsigned>(bx_[level].pkn), 256, 0, stream_>>>(
+        xt_.p + bx_[level].pk0, y, n, nr, xb_.p);
+    ++launches_solve_;
+  }
+  exchange(m);
+  if (phase == kXBsolve && bx_[level].upn) {
+    k_rows_xfer<false><<<static_cast<unsigned>(bx_[level].upn), 256, 0, stream_>>>(
+        xt_.p + bx_[level].up0, y, n, nr, xb_.p);
+    ++launches_solve_;
+  }
 }
 
 void DeviceFactor::ensure_solve_ws(int nrhs) {
@@ -805,6 +945,7 @@ void DeviceFactor::launch_solve_levels(bool fwd, bool bwd, double* y, int nr) {
                                                       uvptr_.p, pf_.p, pfctr_.p);
           ++launches;
         });
+      if (part_) exchange_solve(kXFsolve, l, nr, y);
     }
   if (bwd)
     for (int l = s.n_levels - 1; l >= 0; --l) {
@@ -830,6 +971,7 @@ void DeviceFactor::launch_solve_levels(bool fwd, bool bwd, double* y, int nr) {
           coop(reinterpret_cast<const void*>(k_bsolve_wide<NR>), wgroups_[g].nt, args);
         }
       });
+      if (part_) exchange_solve(kXBsolve, l, nr, y);
     }
 }
 
@@ -871,6 +1013,11 @@ void DeviceFactor::solve(int mode, int nrhs, const double* b, double* x, bool on
     if (nrb == 1) launch_solve_levels<1>(fwd, bwd, y, nr);
     else if (nrb == 4) launch_solve_levels<4>(fwd, bwd, y, nr);
     else launch_solve_levels<16>(fwd, bwd, y, nr);
+    if (part_) {  // each rank holds its own columns: complete y on every rank
+      k_mask_cols<<<pblocks, 256, 0, stream_>>>(y, colmine_.p, n, nr);
+      ++launches_solve_;
+      exchange({{2, -1, -1, -1, y, tot}});
+    }
     if (mode == 2) {
       double* dst = on_device ? xx : v2_.p;
       k_permute_scatter<<<pblocks, 256, 0, stream_>>>(y, perm_.p, n, nr, dst);
@@ -958,6 +1105,15 @@ void DeviceFactor::selinv(double* diag_out, bool on_device) {
       });
       ++launches_selinv_;
     }
+    if (e.ggn) {  // Σ_RR of other ranks' children, now that their parents are done
+      int blocks = static_cast<int>((e.ggn * 32 + 255) / 256);
+      pf.run(stream_, pf.tag("selinv.gather", l), 0.0, 0.0, [&] {
+        k_sel_gather<<<blocks, 256, 0, stream_>>>(sga_.p + e.gg0, static_cast<int>(e.ggn), sd,
+                                                 snparent_.p, Sig_.p, U_.p);
+      });
+      ++launches_selinv_;
+    }
+    if (part_) exchange(sx_[l]);
   }
   double* out = diag_out;
   if (!on_device) {
@@ -966,8 +1122,9 @@ void DeviceFactor::selinv(double* diag_out, bool on_device) {
   }
   if (s.n > 0) {
     k_extract_diag<<<std::max(1, std::min((s.n + 255) / 256, 148 * 8)), 256, 0, stream_>>>(
-        sd, col2sn_.p, perm_.p, Sig_.p, out);
+        sd, col2sn_.p, perm_.p, Sig_.p, part_ ? colmine_.p : nullptr, out);
     ++launches_selinv_;
+    if (part_) exchange({{2, -1, -1, -1, out, static_cast<int64_t>(s.n)}});
   }
   cuda_check(cudaGetLastError(), "selinv launch");
   if (!on_device) {

@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "kernels.cuh"
+#include "partition.hpp"
 #include "profiler.hpp"
 #include "solve_tile.hpp"
 #include "symbolic.hpp"
@@ -44,13 +45,47 @@ struct DevBuf {
   }
 };
 
+// One message of an exchange point of a partitioned factor (same layout as
+// gmrf_msg_t, include/gmrf_b200.h). kind: 0 send, 1 receive, 2 all-reduce sum
+// of doubles, 3 all-reduce min of int32.
+struct XferMsg {
+  int32_t kind;
+  int32_t peer;
+  int32_t tag;    // child supernode of the cross edge (-1 for all-reduces)
+  int32_t phase;  // XPhase, or -1 for all-reduces
+  void* dptr;     // device buffer
+  int64_t count;  // elements
+};
+// Completes (or enqueues on `stream`) every message before returning 0.
+using ExchangeFn = int (*)(void* ctx, const XferMsg* msgs, int32_t count, void* stream);
+
+struct PartitionSpec {
+  int nranks = 1, rank = 0;
+  std::vector<i32> owner;  // per supernode; empty: partition_owners(sym, nranks)
+  ExchangeFn fn = nullptr;
+  void* ctx = nullptr;
+};
+
+// Row gather/scatter of x for the backward-solve exchange (x[rows[i] + rr*n]).
+struct RowXfer {
+  const int32_t* rows;
+  int32_t cnt;
+  int64_t off;  // offset in the pack buffer, per right-hand side
+};
+
 struct FactorTimes {
   float numeric_ms = 0, solve_ms = 0, selinv_ms = 0;
 };
 
 class DeviceFactor {
  public:
-  explicit DeviceFactor(std::shared_ptr<const Symbolic> sym, cudaStream_t stream = nullptr);
+  // part: nullptr (or nranks == 1) = the whole factor on this GPU; otherwise
+  // this rank's share of a partitioned factor (partition.hpp): storage and
+  // kernels for the supernodes it owns, the cross-edge exchanges through
+  // part->fn. numeric/solve/selinv keep their semantics: every rank returns
+  // the complete status, solution and variances.
+  explicit DeviceFactor(std::shared_ptr<const Symbolic> sym, cudaStream_t stream = nullptr,
+                        const PartitionSpec* part = nullptr);
   ~DeviceFactor();
 
   const Symbolic& sym() const { return *sym_; }
@@ -80,6 +115,11 @@ class DeviceFactor {
   void copy_l_panels(std::vector<double>& out) const;
   void copy_sig_panels(std::vector<double>& out) const;
 
+  bool partitioned() const { return part_; }
+  int rank() const { return rank_; }
+  int nranks() const { return nranks_; }
+  const std::vector<i32>& owners() const { return owner_; }
+
   double* d_l() { return L_.p; }
   double* d_sig() { return Sig_.p; }
   bool factored() const { return factored_; }
@@ -99,9 +139,30 @@ class DeviceFactor {
   template <int NR>
   void launch_solve_levels(bool fwd, bool bwd, double* y, int nr);
   SymDev symdev() const;
+  bool mine(int k) const { return !part_ || owner_[k] == rank_; }
+  void exchange(const std::vector<XferMsg>& m);
+  void exchange_solve(int phase, int level, int nr, double* y);
 
   std::shared_ptr<const Symbolic> sym_;
   cudaStream_t stream_;
+  // partition (single GPU: part_ false, every supernode mine)
+  bool part_ = false;
+  int nranks_ = 1, rank_ = 0;
+  std::vector<i32> owner_;
+  ExchangeFn xfn_ = nullptr;
+  void* xctx_ = nullptr;
+  std::vector<XEdge> sched_;              // this rank's cross-edge messages
+  std::vector<i64> lptr_h_, uptr_h_, uvptr_h_;  // this rank's storage offsets
+  std::vector<std::vector<XferMsg>> fx_;  // factor messages after each chunk level
+  std::vector<std::vector<XferMsg>> sx_;  // selinv messages after each chunk level
+  struct BxPoint {
+    int64_t pk0, pkn, up0, upn;  // pack / unpack tasks in xt_
+  };
+  std::vector<BxPoint> bx_;       // backward-solve exchange per supernode level
+  std::vector<int64_t> bx_off_;   // pack-buffer offset of each bsolve edge in sched_ order
+  DevBuf<RowXfer> xt_;
+  DevBuf<double> xb_;             // backward-solve pack buffer (Σ r_c × kMaxRhs)
+  DevBuf<char> colmine_;          // per internal column: owned by this rank
   bool factored_ = false, selinv_done_ = false;
 
   DevBuf<int32_t> first_, rows_, relmap_, chptr_, chlist_, perm_, col2sn_, snparent_, status_;
@@ -124,6 +185,9 @@ class DeviceFactor {
     double sm_flops;
     int64_t gr0, grn, rr0, rrn;  // rest of the trailing update + U SYRK (second stream)
     double gr_flops;
+    bool prow[3];  // panel kernel per bucket: row sweep (one wave) or blocked; decided on
+                   // the level's task count over ALL supernodes, so a partitioned factor
+                   // runs the same kernels (same rounding) as the single-GPU one
   };
   DevBuf<int32_t> small_;
   std::vector<FLevel> flev_;
@@ -134,6 +198,7 @@ class DeviceFactor {
 
   struct SLevel {
     int64_t ga0, gan, y0, yn, t0, tn, z0, zn, d0, dn;
+    int64_t gg0, ggn;  // ghost gathers: Σ_RR of other ranks' children of this level's supernodes
     double ga_bytes, y_flops, t_flops, z_flops, d_flops;
     int64_t yr0, yrn, zr0, zrn;  // split-K reductions of the Y and Z tiles
     int64_t tb0[3], tbn[3], db0[3], dbn[3];  // TRSM / diag chunks by width bucket 16/32/64

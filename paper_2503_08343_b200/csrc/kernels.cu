@@ -282,17 +282,49 @@ __global__ void k_sel_gather(const ColTask* __restrict__ tasks, int ntasks, SymD
 
 // (selected-inversion chunk kernels: selinv.cuh)
 
-// var[perm[j]] = Σ_jj
+// var[perm[j]] = Σ_jj (a partitioned factor writes 0 for columns it does not
+// own; the all-reduce over ranks then completes the vector exactly)
 __global__ void k_extract_diag(SymDev sd, const int32_t* __restrict__ col2sn,
                                const int32_t* __restrict__ perm, const double* __restrict__ Sig,
-                               double* __restrict__ out) {
+                               const char* __restrict__ colmine, double* __restrict__ out) {
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < sd.n; j += gridDim.x * blockDim.x) {
+    if (colmine && !colmine[j]) {
+      out[perm[j]] = 0.0;
+      continue;
+    }
     const int s = col2sn[j];
     const int f0 = sd.sn_first[s];
     const int64_t rows = sd.sn_rptr[s + 1] - sd.sn_rptr[s];
     const int a = j - f0;
     out[perm[j]] = Sig[sd.lptr[s] + a + a * rows];
   }
+}
+
+// ---------------------------------------------------------------------------
+// Partitioned factor (partition.hpp): backward-solve row exchange and result masking.
+// ---------------------------------------------------------------------------
+// kPack: buf[off*nr + rr*cnt + i] = x[rows[i] + rr*n]; else the reverse.
+template <bool kPack>
+__global__ void __launch_bounds__(256) k_rows_xfer(const RowXfer* __restrict__ tasks,
+                                                   double* __restrict__ x, int n, int nr,
+                                                   double* __restrict__ buf) {
+  const RowXfer t = tasks[blockIdx.x];
+  double* b = buf + t.off * nr;
+  for (int idx = threadIdx.x; idx < t.cnt * nr; idx += blockDim.x) {
+    const int i = idx % t.cnt, rr = idx / t.cnt;
+    double* xv = x + t.rows[i] + static_cast<int64_t>(rr) * n;
+    if (kPack) b[idx] = *xv;
+    else *xv = b[idx];
+  }
+}
+
+// y[i + r*n] = 0 for the columns this rank does not own (before the all-reduce).
+__global__ void k_mask_cols(double* __restrict__ y, const char* __restrict__ colmine, int n,
+                            int nrhs) {
+  const int64_t tot = static_cast<int64_t>(n) * nrhs;
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < tot;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    if (!colmine[idx % n]) y[idx] = 0.0;
 }
 
 // ---------------------------------------------------------------------------

@@ -1,0 +1,57 @@
+// Partitioned (multi-GPU) factorization: supernode ownership along the top
+// nested-dissection separators and the exchange schedule.
+//
+// The reference is single-threaded and has no distributed
+// path; this is the north_star's "partition the factorisation along the top
+// nested-dissection separators ... separator Schur-complement contributions
+// reduced over NVLink". Ownership is subtree-to-subcube: each rank owns whole
+// subtrees of the supernodal elimination tree, the separators above them are
+// owned by the lowest rank of the rank range below them. A parent/child pair
+// with different owners is a cross edge; every exchange is attached to one:
+//
+//   factor  : U_c (the child's r_c × r_c update matrix = its Schur-complement
+//             contribution) child owner → parent owner, after the chunk level
+//             that completes U_c; the parent's extend-add sums it in child order
+//             exactly as on one GPU (bit-identical results).
+//   fsolve  : the child's update vector u_c (r_c × nrhs), after the child's level.
+//   bsolve  : x restricted to the child's below-diagonal rows R_c
+//             (r_c × nrhs), parent owner → child owner, after the parent's level.
+//   selinv  : Σ_RR(c) (r_c × r_c) gathered from the parent's Σ front on the
+//             parent owner → child owner, after the parent's first chunk level.
+//
+// Both sides derive the same schedule from the same symbolic, so every rank
+// lists its sends and receives of an exchange point in the same order.
+#pragma once
+
+#include <vector>
+
+#include "symbolic.hpp"
+
+namespace gmrf {
+
+enum XPhase : i32 { kXFactor = 0, kXFsolve = 1, kXBsolve = 2, kXSelinv = 3 };
+
+struct XEdge {
+  i32 phase;   // XPhase
+  i32 point;   // level after which the message moves (ascending levels for
+               // factor/fsolve, descending for bsolve/selinv)
+  i32 src, dst;
+  i32 sn;      // the child supernode of the cross edge
+  i64 count;   // doubles (per right-hand side for the solve phases)
+};
+
+// Chunk levels of the factorization / selected-inversion plans: chunk k of
+// supernode s sits at lvl0(s)+k, one above the last chunk of its deepest child;
+// fronts with rows <= small_rows are factored whole and occupy one level.
+// last[s] = level of the chunk that completes U_s.
+void chunk_levels(const Symbolic& s, std::vector<int>& lvl0, std::vector<int>& last, int& nlev,
+                  int small_rows);
+
+// Subtree-to-subcube ownership of the supernodes for `nranks` ranks, balanced by
+// subtree flops. nranks == 1 gives all zeros.
+std::vector<i32> partition_owners(const Symbolic& s, int nranks);
+
+// Every cross-edge message of all four phases, ordered by (phase, point, sn).
+std::vector<XEdge> partition_schedule(const Symbolic& s, const std::vector<i32>& owner);
+
+}  // namespace gmrf

@@ -351,8 +351,10 @@ double now_ms() {
 
 }  // namespace
 
-SpaceTimePosterior::SpaceTimePosterior(const SpaceTimeSpec& spec, cudaStream_t stream)
+SpaceTimePosterior::SpaceTimePosterior(const SpaceTimeSpec& spec, cudaStream_t stream,
+                                       const PartitionSpec* part)
     : spec_(spec), stream_(stream) {
+  if (part) pspec_ = *part;
   double t0 = now_ms();
   build_host();
   times_.setup_host_ms = now_ms() - t0;
@@ -600,7 +602,7 @@ void SpaceTimePosterior::assemble_device() {
       if (!sl[d]) kept.push_back(d);
     kept_.upload(kept, stream_);
   }
-  fac_ = std::make_unique<DeviceFactor>(sym_, stream_);
+  fac_ = std::make_unique<DeviceFactor>(sym_, stream_, pspec_.nranks > 1 ? &pspec_ : nullptr);
   fac_->prepare_selinv();
   fac_->set_profiler(&prof_);
   for (DevBuf<double>* v : {&mean_cond_, &mean_, &var_, &x_, &c_, &g_, &d_, &cand_, &r1_, &u0_})

@@ -73,7 +73,10 @@ struct PhaseTimes {
 
 class SpaceTimePosterior {
  public:
-  explicit SpaceTimePosterior(const SpaceTimeSpec& spec, cudaStream_t stream = nullptr);
+  // part: partitioned factorization (partition.hpp) across ranks; the O(n)
+  // work (assembly, residuals, line search) is replicated on every rank.
+  explicit SpaceTimePosterior(const SpaceTimeSpec& spec, cudaStream_t stream = nullptr,
+                              const PartitionSpec* part = nullptr);
   ~SpaceTimePosterior();
 
   // Full pipeline from the IC values u0 (n_s, host). Returns the GN trace.
@@ -109,6 +112,7 @@ class SpaceTimePosterior {
 
   SpaceTimeSpec spec_;
   cudaStream_t stream_;
+  PartitionSpec pspec_;
   Space1D space_{};
   SpatialOps ops_;
   SpaceTimeBlocks blk_;

@@ -116,7 +116,12 @@ class GaussNewtonStagnation(NumericalError):
 
 
 class SpaceTimePosterior:
-    def __init__(self, spec: SpaceTimeSpec, gn: GaussNewtonConfig | None = None):
+    def __init__(self, spec: SpaceTimeSpec, gn: GaussNewtonConfig | None = None,
+                 partition=None):
+        """partition: None (whole problem on this GPU) or (nranks, rank, exchange)
+        with an ``Exchange`` from paper_2503_08343_b200.partition — this rank's
+        share of an ND-partitioned factorization; every rank gets the complete
+        posterior."""
         gn = gn or GaussNewtonConfig()
         c = _capi.SpaceTimeConfig(
             spec.n_el, spec.xa, spec.xb, spec.n_t, spec.t_end, spec.diffusion, spec.advection,
@@ -127,7 +132,13 @@ class SpaceTimePosterior:
         self.spec = spec
         lib = _capi.load()
         h = C.c_void_p()
-        _check(lib.gmrf_spacetime_create(C.byref(c), C.byref(h)))
+        if partition is None:
+            _check(lib.gmrf_spacetime_create(C.byref(c), C.byref(h)))
+        else:
+            nranks, rank, exchange = partition
+            self._exchange = exchange  # the C callback must outlive the handle
+            _check(lib.gmrf_spacetime_create_partitioned(C.byref(c), nranks, rank, exchange.fn,
+                                                         None, C.byref(h)))
         self._h = h
         self.n = self.info().n
 
