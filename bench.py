@@ -22,7 +22,11 @@ problem shape and reported separately as ``host_setup_s``.
 
 Multi-GPU (torchrun, N>1): batch sharding — each rank solves its own
 independent posterior (BASELINE config 5's "independent problems one per GPU"
-mode); no data-path collective; scaling "weak".
+mode); no data-path collective; scaling "weak". With --partition: ONE
+posterior whose factorization, solves and selected inversion are partitioned
+along the top nested-dissection separators across the ranks (Schur
+complements and solve vectors over NCCL, paper_2503_08343_b200/partition.py);
+scaling "strong".
 """
 from __future__ import annotations
 
@@ -203,6 +207,10 @@ def main():
     ap.add_argument("--n-el", type=int, default=999)
     ap.add_argument("--n-t", type=int, default=1000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--partition", action="store_true",
+                    help="N>1: one posterior, its factorization / solves / selected inversion "
+                         "partitioned along the top ND separators across the ranks (NCCL), "
+                         "strong scaling; default: one independent posterior per GPU")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -214,6 +222,10 @@ def main():
               "n_el": args.n_el, "n_t": args.n_t, "gn_steps": 10,
               "l2": "inputs larger than L2 (factor storage ~3 GB, Sigma panels ~1.6 GB)",
               "parallelism": f"replicas x{world} (batch sharding, one posterior per GPU)"}
+    partitioned = args.partition and world > 1
+    if partitioned:
+        config["parallelism"] = (f"nd-partition x{world} (one posterior; supernodal tree split "
+                                 f"along its top nested-dissection separators, NCCL exchange)")
 
     if args.impl == "reference":
         if rank != 0:
@@ -244,7 +256,12 @@ def main():
     peaks = load_peaks()
     spec = SpaceTimeSpec.burgers(n_el=args.n_el, n_t=args.n_t)
     t0 = time.perf_counter()
-    post = SpaceTimePosterior(spec, GaussNewtonConfig(max_iters=10))
+    if partitioned:
+        from paper_2503_08343_b200.partition import TorchExchange
+        post = SpaceTimePosterior(spec, GaussNewtonConfig(max_iters=10),
+                                  partition=(world, rank, TorchExchange()))
+    else:
+        post = SpaceTimePosterior(spec, GaussNewtonConfig(max_iters=10))
     host_setup_s = time.perf_counter() - t0
     x = spec.node_x()
     u0 = -np.sin(np.pi * x)
@@ -331,7 +348,8 @@ def main():
         return
     line = {
         "metric": METRIC, "value": ms / 1e3, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
+        "scaling": "strong" if partitioned else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY §8(d))",
         "config": config,
         "e2e": {"value": e2e_s, "unit": UNIT, "h2d_bytes_per_step": 8 * len(u0),
