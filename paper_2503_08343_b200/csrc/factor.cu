@@ -80,6 +80,7 @@ DeviceFactor::DeviceFactor(std::shared_ptr<const Symbolic> sym, cudaStream_t str
     : sym_(std::move(sym)), stream_(stream) {
   set_smem_attrs();
   const Symbolic& s = *sym_;
+  if (const char* e = std::getenv("GMRF_NO_GRAPH")) use_graph_ = e[0] == '0';
   if (part && part->nranks > 1) {
     require(part->rank >= 0 && part->rank < part->nranks, kContract, "partition: bad rank");
     require(part->fn != nullptr, kContract, "partition: no exchange function");
@@ -288,6 +289,7 @@ DeviceFactor::DeviceFactor(std::shared_ptr<const Symbolic> sym, cudaStream_t str
 }
 
 DeviceFactor::~DeviceFactor() {
+  if (fgraph_) cudaGraphExecDestroy(fgraph_);
   for (cudaEvent_t e : ev_panel_) cudaEventDestroy(e);
   for (cudaEvent_t e : ev_rest_) cudaEventDestroy(e);
   if (ev_fork_) cudaEventDestroy(ev_fork_);
@@ -709,12 +711,54 @@ int32_t DeviceFactor::numeric(const double* q, bool q_on_device) {
 
 int32_t DeviceFactor::factor_panels() {
   const Symbolic& s = *sym_;
-  const SymDev sd = symdev();
   KernelProfiler& pf = *prof_;
   const bool la = lookahead_ && !pf.on;
-  cudaStream_t sa = la ? main_ : stream_;  // critical chain
-  cudaStream_t sb = la ? aux_ : stream_;   // bulk trailing updates
-  if (la) {
+  // The level sequence is fixed per symbolic: captured once into a CUDA graph
+  // (both lookahead streams, their event edges) and replayed per factorization,
+  // so the ~100-level chain at the top of the tree is not paced by host launches.
+  if (la && !part_ && use_graph_) {
+    if (!fgraph_) {
+      const int64_t l0 = launches_numeric_;
+      cuda_check(cudaStreamBeginCapture(main_, cudaStreamCaptureModeThreadLocal), "capture");
+      enqueue_levels(main_, aux_, true, true);
+      cudaGraph_t g = nullptr;
+      cuda_check(cudaStreamEndCapture(main_, &g), "end capture");
+      cuda_check(cudaGraphInstantiate(&fgraph_, g, 0), "graph instantiate");
+      cuda_check(cudaGraphDestroy(g), "graph destroy");
+      graph_launches_ = launches_numeric_ - l0;
+      launches_numeric_ = l0;
+    }
+    cuda_check(cudaGraphLaunch(fgraph_, stream_), "graph launch");
+    launches_numeric_ += graph_launches_;
+  } else {
+    enqueue_levels(la ? main_ : stream_, la ? aux_ : stream_, la, false);
+  }
+  if (po_.n) {
+    pf.run(stream_, "factor.diag_writeback", 0.0, 16.0 * s.n * kNB / 2.0, [&] {
+      k_diag_writeback<<<static_cast<unsigned>(po_.n), 128, 0, stream_>>>(po_.p, diag_.p,
+                                                                         rdiag_.p);
+    });
+    ++launches_numeric_;
+  }
+  cuda_check(cudaGetLastError(), "factor launch");
+  if (part_) exchange({{3, -1, -1, -1, status_.p, 1}});  // smallest failing pivot over ranks
+  int st = INT_MAX;
+  cuda_check(cudaMemcpyAsync(&st, status_.p, sizeof(int), cudaMemcpyDeviceToHost, stream_),
+             "status read");
+  cuda_check(cudaStreamSynchronize(stream_), "numeric factorization");
+  factored_ = st == 0x7f7f7f7f;
+  selinv_done_ = false;
+  return factored_ ? -1 : s.perm[st];
+}
+
+// The chunk levels of one numeric factorization on the chain stream sa and the
+// bulk stream sb (la: two-stream lookahead, else sa == sb == stream_). In a
+// graph capture sa is the origin stream and the fork/join to stream_ is left
+// to the graph launch.
+void DeviceFactor::enqueue_levels(cudaStream_t sa, cudaStream_t sb, bool la, bool in_graph) {
+  const SymDev sd = symdev();
+  KernelProfiler& pf = *prof_;
+  if (la && !in_graph) {
     cuda_check(cudaEventRecord(ev_fork_, stream_), "record");
     cuda_check(cudaStreamWaitEvent(sa, ev_fork_, 0), "wait");
   }
@@ -827,25 +871,11 @@ int32_t DeviceFactor::factor_panels() {
   }
   if (la) {  // join: the caller's stream continues after both chains
     if (!flev_.empty()) cuda_check(cudaStreamWaitEvent(sa, ev_rest_[flev_.size() - 1], 0), "wait");
-    cuda_check(cudaEventRecord(ev_fork_, sa), "record");
-    cuda_check(cudaStreamWaitEvent(stream_, ev_fork_, 0), "wait");
+    if (!in_graph) {
+      cuda_check(cudaEventRecord(ev_fork_, sa), "record");
+      cuda_check(cudaStreamWaitEvent(stream_, ev_fork_, 0), "wait");
+    }
   }
-  if (po_.n) {
-    pf.run(stream_, "factor.diag_writeback", 0.0, 16.0 * s.n * kNB / 2.0, [&] {
-      k_diag_writeback<<<static_cast<unsigned>(po_.n), 128, 0, stream_>>>(po_.p, diag_.p,
-                                                                         rdiag_.p);
-    });
-    ++launches_numeric_;
-  }
-  cuda_check(cudaGetLastError(), "factor launch");
-  if (part_) exchange({{3, -1, -1, -1, status_.p, 1}});  // smallest failing pivot over ranks
-  int st = INT_MAX;
-  cuda_check(cudaMemcpyAsync(&st, status_.p, sizeof(int), cudaMemcpyDeviceToHost, stream_),
-             "status read");
-  cuda_check(cudaStreamSynchronize(stream_), "numeric factorization");
-  factored_ = st == 0x7f7f7f7f;
-  selinv_done_ = false;
-  return factored_ ? -1 : s.perm[st];
 }
 
 void DeviceFactor::exchange(const std::vector<XferMsg>& m) {

@@ -141,6 +141,7 @@ class DeviceFactor {
   SymDev symdev() const;
   bool mine(int k) const { return !part_ || owner_[k] == rank_; }
   void exchange(const std::vector<XferMsg>& m);
+  void enqueue_levels(cudaStream_t sa, cudaStream_t sb, bool la, bool in_graph);
   void exchange_solve(int phase, int level, int nr, double* y);
 
   std::shared_ptr<const Symbolic> sym_;
@@ -211,6 +212,9 @@ class DeviceFactor {
   cudaEvent_t ev_fork_ = nullptr;
   std::vector<cudaEvent_t> ev_panel_, ev_rest_;
   bool lookahead_ = true;
+  bool use_graph_ = true;             // GMRF_NO_GRAPH=1 disables (A/B)
+  cudaGraphExec_t fgraph_ = nullptr;  // captured chunk-level sequence
+  int64_t graph_launches_ = 0;
   std::vector<double> lvl_bytes_;  // solve: L panel + row-index bytes per tree level
   KernelProfiler own_prof_;
   KernelProfiler* prof_ = &own_prof_;
