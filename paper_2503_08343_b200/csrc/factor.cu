@@ -8,6 +8,7 @@
 
 #include "kernels.cu"  // single translation unit for all device code
 #include "panel.cuh"
+#include "panel2.cuh"
 #include "small_front.cuh"
 #include "solve.cuh"
 #include "selinv.cuh"
@@ -81,6 +82,7 @@ DeviceFactor::DeviceFactor(std::shared_ptr<const Symbolic> sym, cudaStream_t str
   set_smem_attrs();
   const Symbolic& s = *sym_;
   if (const char* e = std::getenv("GMRF_NO_GRAPH")) use_graph_ = e[0] == '0';
+  if (const char* e = std::getenv("GMRF_PANEL1")) panel2_ = e[0] == '0';
   if (part && part->nranks > 1) {
     require(part->rank >= 0 && part->rank < part->nranks, kContract, "partition: bad rank");
     require(part->fn != nullptr, kContract, "partition: no exchange function");
@@ -325,7 +327,7 @@ void DeviceFactor::build_factor_plan() {
   std::vector<std::vector<EaTask>> ea(nlev);
   std::vector<int2> ea_pairs;  // (child, first row of its update column), child order
   std::vector<int32_t> cnt;
-  std::vector<std::vector<PanelTask>> pan(nlev), po(nlev);
+  std::vector<std::vector<PanelTask>> pan(nlev), po(nlev), pdg(nlev), ptr2(nlev);
   // GEMM tasks per level: gm = the update of the chunk's NEXT column block (on
   // the critical chain), gr = the rest of the trailing update + the U SYRK
   // (overlapped with the next level's panel on the second stream)
@@ -388,6 +390,16 @@ void DeviceFactor::build_factor_plan() {
       const PanelTask pt{Lk + c0 + static_cast<int64_t>(c0) * rows, rows, wk, nbelow, 0,
                          s.sn_first[k] + c0};
       po[lv].push_back(pt);  // chunk list for the final diagonal write-back
+      {  // two-phase panel (panel2.cuh): one diagonal task + 64-row slabs
+        PanelTask dt = pt;
+        dt.slot = static_cast<int32_t>(pdg[lv].size());
+        pdg[lv].push_back(dt);
+        for (int t = 0; t * kTrsm2Rows < nbelow; ++t) {
+          PanelTask tt = dt;
+          tt.tile = t;
+          ptr2[lv].push_back(tt);
+        }
+      }
       for (int t = 0; t == 0 || t * kTrsmRows < nbelow; ++t) {
         PanelTask tt = pt;
         tt.tile = t;
@@ -440,7 +452,8 @@ void DeviceFactor::build_factor_plan() {
     }
   }
   std::vector<EaTask> eaf;
-  std::vector<PanelTask> panf, pof;
+  std::vector<PanelTask> panf, pof, pdf, ptf;
+  size_t max_slots = 1;
   std::vector<GemmTask> gmf;
   std::vector<ReduceTask> rdf;
   std::vector<int32_t> smf;
@@ -492,6 +505,17 @@ void DeviceFactor::build_factor_plan() {
       }
       flev_[l].pbn[bk] = static_cast<int64_t>(panf.size()) - flev_[l].pb0[bk];
     }
+    max_slots = std::max(max_slots, pdg[l].size());
+    for (int bk = 0; bk < 3; ++bk) {
+      flev_[l].pd0[bk] = static_cast<int64_t>(pdf.size());
+      for (const PanelTask& pt : pdg[l])
+        if ((pt.w <= 16 ? 0 : (pt.w <= 32 ? 1 : 2)) == bk) pdf.push_back(pt);
+      flev_[l].pdn[bk] = static_cast<int64_t>(pdf.size()) - flev_[l].pd0[bk];
+      flev_[l].pt0[bk] = static_cast<int64_t>(ptf.size());
+      for (const PanelTask& pt : ptr2[l])
+        if ((pt.w <= 16 ? 0 : (pt.w <= 32 ? 1 : 2)) == bk) ptf.push_back(pt);
+      flev_[l].ptn[bk] = static_cast<int64_t>(ptf.size()) - flev_[l].pt0[bk];
+    }
     for (int bk = 0; bk < 3; ++bk) {
       flev_[l].sm0[bk] = static_cast<int64_t>(smf.size());
       flev_[l].smn[bk] = static_cast<int64_t>(sm[bk][l].size());
@@ -504,6 +528,9 @@ void DeviceFactor::build_factor_plan() {
   eap_.upload(ea_pairs, stream_);
   pan_.upload(panf, stream_);
   po_.upload(pof, stream_);
+  pd_.upload(pdf, stream_);
+  pt_.upload(ptf, stream_);
+  stage_.alloc(max_slots * kL11Slot);
   gemm_.upload(gmf, stream_);
   red_.upload(rdf, stream_);
   small_.upload(smf, stream_);
@@ -797,7 +824,34 @@ void DeviceFactor::enqueue_levels(cudaStream_t sa, cudaStream_t sb, bool la, boo
       });
       ++launches_numeric_;
     }
-    if (lv.pann) {
+    // one-wave levels (the chain at the top of the tree) keep the fused row
+    // sweep: one launch, no staging round trip; multi-wave levels split
+    const bool two_phase = panel2_ && !(lv.prow[0] && lv.prow[1] && lv.prow[2]);
+    if (lv.pann && two_phase) {
+      // two-phase panel: diagonal blocks once per chunk, then barrier-free
+      // row-per-thread TRSM slabs (panel2.cuh)
+      pf.run(sa, pf.tag("factor.potrf_trsm", lvl), lv.po_flops + lv.tr_flops, 0.0, [&] {
+        if (lv.pdn[0])
+          k_panel_diag<16><<<static_cast<unsigned>(lv.pdn[0]), panel_rows_diag<16>(), 0, sa>>>(
+              pd_.p + lv.pd0[0], status_.p, diag_.p, rdiag_.p, stage_.p);
+        if (lv.pdn[1])
+          k_panel_diag<32><<<static_cast<unsigned>(lv.pdn[1]), panel_rows_diag<32>(), 0, sa>>>(
+              pd_.p + lv.pd0[1], status_.p, diag_.p, rdiag_.p, stage_.p);
+        if (lv.pdn[2])
+          k_panel_diag<64><<<static_cast<unsigned>(lv.pdn[2]), panel_rows_diag<64>(), 0, sa>>>(
+              pd_.p + lv.pd0[2], status_.p, diag_.p, rdiag_.p, stage_.p);
+        if (lv.ptn[0])
+          k_panel_trsm<16><<<static_cast<unsigned>(lv.ptn[0]), kTrsm2Rows, 0, sa>>>(
+              pt_.p + lv.pt0[0], stage_.p);
+        if (lv.ptn[1])
+          k_panel_trsm<32><<<static_cast<unsigned>(lv.ptn[1]), kTrsm2Rows, 0, sa>>>(
+              pt_.p + lv.pt0[1], stage_.p);
+        if (lv.ptn[2])
+          k_panel_trsm<64><<<static_cast<unsigned>(lv.ptn[2]), kTrsm2Rows, 0, sa>>>(
+              pt_.p + lv.pt0[2], stage_.p);
+      });
+      for (int bk = 0; bk < 3; ++bk) launches_numeric_ += (lv.pdn[bk] > 0) + (lv.ptn[bk] > 0);
+    } else if (lv.pann) {
       // latency-bound levels (one wave) use the row-per-thread sweep; levels
       // with several waves of chunk slabs keep the blocked smem kernel, whose
       // CTAs are small enough to co-reside 4-5 per SM

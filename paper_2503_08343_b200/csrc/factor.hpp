@@ -186,6 +186,7 @@ class DeviceFactor {
     double sm_flops;
     int64_t gr0, grn, rr0, rrn;  // rest of the trailing update + U SYRK (second stream)
     double gr_flops;
+    int64_t pd0[3], pdn[3], pt0[3], ptn[3];  // two-phase panel: diagonal / TRSM tasks
     bool prow[3];  // panel kernel per bucket: row sweep (one wave) or blocked; decided on
                    // the level's task count over ALL supernodes, so a partitioned factor
                    // runs the same kernels (same rounding) as the single-GPU one
@@ -213,6 +214,9 @@ class DeviceFactor {
   std::vector<cudaEvent_t> ev_panel_, ev_rest_;
   bool lookahead_ = true;
   bool use_graph_ = true;             // GMRF_NO_GRAPH=1 disables (A/B)
+  bool panel2_ = true;                // GMRF_PANEL1=1: fused one-phase panel kernels (A/B)
+  DevBuf<PanelTask> pd_, pt_;         // two-phase panel tasks
+  DevBuf<double> stage_;              // per-level L11 staging slots (panel2.cuh)
   cudaGraphExec_t fgraph_ = nullptr;  // captured chunk-level sequence
   int64_t graph_launches_ = 0;
   std::vector<double> lvl_bytes_;  // solve: L panel + row-index bytes per tree level

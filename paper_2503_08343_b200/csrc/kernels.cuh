@@ -42,6 +42,7 @@ struct PanelTask {
   int32_t nbelow;     // rows below the diagonal block
   int32_t tile;       // which kTrsmRows-row slab of the rows below
   int32_t gcol;       // internal index of the chunk's first column
+  int32_t slot;       // chunk's L11 staging slot in its level (panel2.cuh)
 };
 
 // Extend-add work item: one front column b of supernode sn, receiving the
