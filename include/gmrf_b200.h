@@ -105,6 +105,20 @@ int gmrf_solve_device(gmrf_factor_t* f, int mode, int32_t nrhs, const double* d_
 /* takahashi_diagonal (core/takahashi.hpp:67): diag(Q⁻¹) in original order. */
 int gmrf_selinv_diag(gmrf_factor_t* f, double* diag);
 int gmrf_selinv_diag_device(gmrf_factor_t* f, double* d_diag);
+/* sample_direct (gmrf.hpp:173,182) repeated n_samples times with one
+ * Rng(seed) stream (core/rng.hpp, same draws as the reference):
+ * out[:, s] = mean + Pᵀ L⁻ᵀ z_s (n × n_samples column-major, host). Batched
+ * multi-right-hand-side upper solves on the device. */
+int gmrf_sample_direct(gmrf_factor_t* f, const double* mean, int32_t n_samples, uint64_t seed,
+                       double* out);
+/* rbmc_variance (gmrf.hpp:213-240): Rao-Blackwellized Monte Carlo marginal
+ * variances of N(mean, Q⁻¹) from n_samples exact samples of Rng(seed).
+ * q_values: Q (the factored matrix) in the symbolic's CSC order. Errors:
+ * GMRF_ERR_CONTRACT if n_samples < 2, GMRF_ERR_NUMERICAL for a non-positive
+ * Q_ii (as the reference). */
+int gmrf_rbmc_variance(gmrf_factor_t* f, const double* q_values, const double* mean,
+                       int32_t n_samples, uint64_t seed, double* var);
+
 /* takahashi_selected_inverse (core/takahashi.hpp:19): Σ on the pattern of
  * L+Lᵀ mapped back to original indices (sorted CSC). Call after selinv_diag.
  * nnz query first (host memory, small n). */

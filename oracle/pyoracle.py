@@ -131,6 +131,9 @@ class Ref:
         lib.ref_condition_affine.argtypes = [C.c_int, i32p, i32p, f64p, f64p, C.c_int, i32p, i32p,
                                              f64p, f64p, f64p, f64p]
         lib.ref_time_stages.argtypes = [C.c_int, i32p, i32p, f64p, C.c_int, f64p]
+        for nm in ("ref_sample_direct", "ref_rbmc_variance"):
+            getattr(lib, nm).argtypes = [C.c_int, i32p, i32p, f64p, i32p, f64p, C.c_int,
+                                         C.c_ulonglong, f64p]
         self.lib = lib
 
     def err(self):
@@ -188,6 +191,28 @@ class Ref:
         if not h:
             raise RuntimeError(self.err())
         return Bundle(self, h)
+
+    def sample_direct(self, n, cp, ri, v, perm, mu, ns, seed):
+        """ns draws of sample_direct(g, rng) (gmrf.hpp:182), factor in `perm`."""
+        cp, ri, v = self._csc32(cp, ri, v)
+        out = np.empty((n, ns), order="F")
+        if self.lib.ref_sample_direct(n, _p(cp, i32p), _p(ri, i32p), _p(v, f64p),
+                                      _p(np.ascontiguousarray(perm, np.int32), i32p),
+                                      _p(np.ascontiguousarray(mu, np.float64), f64p), ns, seed,
+                                      _p(out, f64p)) != 0:
+            raise RuntimeError(self.err())
+        return out
+
+    def rbmc_variance(self, n, cp, ri, v, perm, mu, ns, seed):
+        """rbmc_variance (gmrf.hpp:213), factor in `perm`."""
+        cp, ri, v = self._csc32(cp, ri, v)
+        out = np.empty(n)
+        if self.lib.ref_rbmc_variance(n, _p(cp, i32p), _p(ri, i32p), _p(v, f64p),
+                                      _p(np.ascontiguousarray(perm, np.int32), i32p),
+                                      _p(np.ascontiguousarray(mu, np.float64), f64p), ns, seed,
+                                      _p(out, f64p)) != 0:
+            raise RuntimeError(self.err())
+        return out
 
     def time_stages(self, n, cp, ri, v, do_taka):
         cp, ri, v = self._csc32(cp, ri, v)

@@ -588,6 +588,45 @@ void* ref_condition_affine(int n, const int* qcp, const int* qri, const double* 
   }
 }
 
+// sample_direct (gmrf.hpp:173,182) n_samples times from Rng(seed), and
+// rbmc_variance (gmrf.hpp:213-240), on Gmrf(mu, Q) with the factor attached
+// for the given permutation (attach_factor, gmrf.hpp:49-51) so the draws use
+// the same L ordering as the GPU. out: n × ns column-major / n.
+int ref_sample_direct(int n, const int* cp, const int* ri, const double* v, const int* perm,
+                      const double* mu, int ns, unsigned long long seed, double* out) {
+  try {
+    SparseMatrixCSC q = make_csc(n, n, cp, ri, v);
+    Gmrf g(Vector(mu, mu + n), q);
+    g.attach_factor(std::make_shared<const CholeskyFactor>(
+        cholesky_factor(q, std::vector<Index>(perm, perm + n))));
+    Rng rng(seed);
+    for (int k = 0; k < ns; ++k) {
+      Vector x = sample_direct(g, rng);
+      std::memcpy(out + static_cast<size_t>(k) * n, x.data(), sizeof(double) * n);
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+int ref_rbmc_variance(int n, const int* cp, const int* ri, const double* v, const int* perm,
+                      const double* mu, int ns, unsigned long long seed, double* out) {
+  try {
+    SparseMatrixCSC q = make_csc(n, n, cp, ri, v);
+    Gmrf g(Vector(mu, mu + n), q);
+    g.attach_factor(std::make_shared<const CholeskyFactor>(
+        cholesky_factor(q, std::vector<Index>(perm, perm + n))));
+    Vector var = rbmc_variance(g, ns, seed);
+    std::memcpy(out, var.data(), sizeof(double) * n);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
 // Timed reference stages on one matrix (for the CPU baseline leg):
 // out[0]=amd s, out[1]=symbolic s, out[2]=numeric s, out[3]=full solve s,
 // out[4]=takahashi s (if do_taka), out[5]=nnz(L), out[6]=Σ c_j² flops.

@@ -20,6 +20,8 @@ from .core import (  # noqa: F401
     cholesky_factor,
     cholesky_refactor,
     nd_order,
+    rbmc_variance,
+    sample_direct,
     solve,
     solve_triangular,
     symbolic_analyze,

@@ -101,6 +101,8 @@ SIGNATURES = {
     "gmrf_solve_device": (C.c_int, [C.c_void_p, C.c_int, C.c_int32, C.c_void_p, C.c_void_p]),
     "gmrf_selinv_diag": (C.c_int, [C.c_void_p, f64p]),
     "gmrf_selinv_diag_device": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "gmrf_sample_direct": (C.c_int, [C.c_void_p, f64p, C.c_int32, C.c_uint64, f64p]),
+    "gmrf_rbmc_variance": (C.c_int, [C.c_void_p, f64p, f64p, C.c_int32, C.c_uint64, f64p]),
     "gmrf_selinv_pattern_nnz": (C.c_int, [C.c_void_p, i64p]),
     "gmrf_selinv_pattern": (C.c_int, [C.c_void_p, i64p, i32p, f64p]),
     "gmrf_factor_l": (C.c_int, [C.c_void_p, i64p, i32p, f64p, i32p]),

@@ -276,6 +276,34 @@ def takahashi_diagonal(f: CholeskyFactor) -> np.ndarray:
     return d
 
 
+def sample_direct(f: CholeskyFactor, mean, n_samples: int, seed: int) -> np.ndarray:
+    """gmrf.hpp:173/182 — ``n_samples`` draws μ + Pᵀ L⁻ᵀ z from one Rng(seed)
+    stream (the reference's draw order); returns (n, n_samples)."""
+    n = f.dim()
+    mu = np.ascontiguousarray(mean, np.float64)
+    if mu.shape[0] != n:
+        raise DimensionError("sample_direct: mean length mismatch")
+    out = np.empty((n, int(n_samples)), order="F")
+    _check(_capi.load().gmrf_sample_direct(f._h, ptr(mu, f64p), int(n_samples), int(seed),
+                                           ptr(out, f64p)))
+    return out
+
+
+def rbmc_variance(f: CholeskyFactor, q: SparseMatrixCSC, mean, n_samples: int,
+                  seed: int) -> np.ndarray:
+    """gmrf.hpp:213-240 — Rao-Blackwellized Monte Carlo marginal variances of
+    N(mean, Q⁻¹) (f = the factor of q)."""
+    n = f.dim()
+    mu = np.ascontiguousarray(mean, np.float64)
+    if mu.shape[0] != n or q.nrows != n:
+        raise DimensionError("rbmc_variance: dimension mismatch")
+    qv = np.ascontiguousarray(q.values, np.float64)
+    var = np.empty(n)
+    _check(_capi.load().gmrf_rbmc_variance(f._h, ptr(qv, f64p), ptr(mu, f64p), int(n_samples),
+                                           int(seed), ptr(var, f64p)))
+    return var
+
+
 def takahashi_selected_inverse(f: CholeskyFactor) -> SparseMatrixCSC:
     """takahashi.hpp:19 — Σ on the pattern of L+Lᵀ, original indices."""
     lib = _capi.load()

@@ -211,6 +211,40 @@ int gmrf_selinv_diag_device(gmrf_factor_t* f, double* d) {
   return guard([&] { f->f->selinv(d, true); });
 }
 
+int gmrf_sample_direct(gmrf_factor_t* f, const double* mean, int32_t ns, uint64_t seed,
+                       double* out) {
+  return guard([&] {
+    const int n = f->s->n;
+    gmrf::require(ns >= 0, gmrf::kContract, "sample_direct: negative sample count");
+    if (n == 0 || ns == 0) return;
+    gmrf::DevBuf<double> m, o;
+    m.alloc(n);
+    o.alloc(static_cast<size_t>(n) * ns);
+    gmrf::cuda_check(cudaMemcpy(m.p, mean, sizeof(double) * n, cudaMemcpyHostToDevice), "mean");
+    f->f->sample_direct(m.p, ns, seed, o.p);
+    gmrf::cuda_check(cudaMemcpy(out, o.p, sizeof(double) * n * static_cast<size_t>(ns),
+                                cudaMemcpyDeviceToHost), "samples");
+  });
+}
+
+int gmrf_rbmc_variance(gmrf_factor_t* f, const double* qv, const double* mean, int32_t ns,
+                       uint64_t seed, double* var) {
+  return guard([&] {
+    const int n = f->s->n;
+    gmrf::require(ns >= 2, gmrf::kContract, "rbmc_variance: need at least 2 samples");
+    if (n == 0) return;
+    const size_t nnz = f->s->qri.size();
+    gmrf::DevBuf<double> q, m, v;
+    q.alloc(std::max<size_t>(nnz, 1));
+    m.alloc(n);
+    v.alloc(n);
+    gmrf::cuda_check(cudaMemcpy(q.p, qv, sizeof(double) * nnz, cudaMemcpyHostToDevice), "Q");
+    gmrf::cuda_check(cudaMemcpy(m.p, mean, sizeof(double) * n, cudaMemcpyHostToDevice), "mean");
+    f->f->rbmc_variance(q.p, m.p, ns, seed, v.p);
+    gmrf::cuda_check(cudaMemcpy(var, v.p, sizeof(double) * n, cudaMemcpyDeviceToHost), "var");
+  });
+}
+
 // Value of the lower-triangular panel entry (i, j), i >= j, internal order.
 static double panel_at(const gmrf::Symbolic& s, const std::vector<double>& pan, int i, int j) {
   const int k = s.col2sn[j];

@@ -9,6 +9,7 @@
 #include "kernels.cu"  // single translation unit for all device code
 #include "panel.cuh"
 #include "panel2.cuh"
+#include "rng.hpp"
 #include "small_front.cuh"
 #include "solve.cuh"
 #include "selinv.cuh"
@@ -1217,6 +1218,85 @@ void DeviceFactor::selinv(double* diag_out, bool on_device) {
     cuda_check(cudaStreamSynchronize(stream_), "selinv");
   }
   selinv_done_ = true;
+}
+
+// Batches of up to kMaxRhs samples: z drawn on the host in the reference's
+// order, one multi-RHS upper solve (kUpper, cholesky.hpp:194-201), Pᵀ, + μ.
+void DeviceFactor::sample_direct(const double* d_mean, int ns, uint64_t seed, double* d_out) {
+  require(factored_, kContract, "sample_direct: factor not computed");
+  const Symbolic& s = *sym_;
+  const int n = s.n;
+  if (n == 0 || ns <= 0) return;
+  HostRng rng(seed);
+  std::vector<double> z(static_cast<size_t>(n) * kMaxRhs);
+  zb_.alloc(z.size());
+  wb_.alloc(z.size());
+  for (int s0 = 0; s0 < ns; s0 += kMaxRhs) {
+    const int nb = std::min(kMaxRhs, ns - s0);
+    for (size_t q = 0; q < static_cast<size_t>(n) * nb; ++q) z[q] = rng.normal();
+    cuda_check(cudaMemcpyAsync(zb_.p, z.data(), sizeof(double) * n * nb, cudaMemcpyHostToDevice,
+                               stream_), "upload z");
+    solve(1, nb, zb_.p, wb_.p, true);
+    double* u = d_out + static_cast<int64_t>(s0) * n;
+    const int64_t tot = static_cast<int64_t>(n) * nb;
+    const int blocks = static_cast<int>(std::min<int64_t>((tot + 255) / 256, 148 * 8));
+    k_permute_scatter<<<blocks, 256, 0, stream_>>>(wb_.p, perm_.p, n, nb, u);
+    k_add_mean<<<blocks, 256, 0, stream_>>>(d_mean, n, nb, u);
+    // z is reused by the next batch: the copy above must have been consumed
+    cuda_check(cudaStreamSynchronize(stream_), "sample batch");
+  }
+  cuda_check(cudaGetLastError(), "sample launch");
+}
+
+void DeviceFactor::rbmc_variance(const double* d_qv, const double* d_mean, int ns, uint64_t seed,
+                                 double* d_var) {
+  require(ns >= 2, kContract, "rbmc_variance: need at least 2 samples");
+  require(factored_, kContract, "rbmc_variance: factor not computed");
+  const Symbolic& s = *sym_;
+  const int n = s.n;
+  if (n == 0) return;
+  if (!qcp_d_.p) {
+    qcp_d_.upload(s.qcp, stream_);
+    qri_d_.upload(s.qri, stream_);
+  }
+  const int gb = std::max(1, std::min((n + 255) / 256, 148 * 8));
+  qdg_.alloc(n);
+  k_csc_diag<<<gb, 256, 0, stream_>>>(qcp_d_.p, qri_d_.p, d_qv, n, qdg_.p);
+  {
+    std::vector<double> qd(n);
+    cuda_check(cudaMemcpyAsync(qd.data(), qdg_.p, sizeof(double) * n, cudaMemcpyDeviceToHost,
+                               stream_), "qdiag");
+    cuda_check(cudaStreamSynchronize(stream_), "qdiag");
+    for (double v : qd)
+      if (!(v > 0.0)) fail(kNumerical, "rbmc_variance: non-positive precision diagonal");
+  }
+  rbm_.alloc(n);
+  rbm2_.alloc(n);
+  cuda_check(cudaMemsetAsync(rbm_.p, 0, sizeof(double) * n, stream_), "mm");
+  cuda_check(cudaMemsetAsync(rbm2_.p, 0, sizeof(double) * n, stream_), "m2");
+  ub_.alloc(static_cast<size_t>(n) * kMaxRhs);
+  qc_.alloc(static_cast<size_t>(n) * kMaxRhs);
+  HostRng rng(seed);
+  std::vector<double> z(static_cast<size_t>(n) * kMaxRhs);
+  zb_.alloc(z.size());
+  wb_.alloc(z.size());
+  for (int s0 = 0; s0 < ns; s0 += kMaxRhs) {
+    const int nb = std::min(kMaxRhs, ns - s0);
+    for (size_t q = 0; q < static_cast<size_t>(n) * nb; ++q) z[q] = rng.normal();
+    cuda_check(cudaMemcpyAsync(zb_.p, z.data(), sizeof(double) * n * nb, cudaMemcpyHostToDevice,
+                               stream_), "upload z");
+    solve(1, nb, zb_.p, wb_.p, true);
+    const int64_t tot = static_cast<int64_t>(n) * nb;
+    const int blocks = static_cast<int>(std::min<int64_t>((tot + 255) / 256, 148 * 8));
+    k_permute_scatter<<<blocks, 256, 0, stream_>>>(wb_.p, perm_.p, n, nb, ub_.p);
+    k_add_mean<<<blocks, 256, 0, stream_>>>(d_mean, n, nb, ub_.p);
+    k_rbmc_spmv<<<blocks, 256, 0, stream_>>>(qcp_d_.p, qri_d_.p, d_qv, d_mean, ub_.p, n, nb, qc_.p);
+    k_rbmc_welford<<<gb, 256, 0, stream_>>>(d_mean, ub_.p, qc_.p, qdg_.p, n, nb, s0, rbm_.p,
+                                            rbm2_.p);
+    cuda_check(cudaStreamSynchronize(stream_), "rbmc batch");
+  }
+  k_rbmc_final<<<gb, 256, 0, stream_>>>(qdg_.p, rbm2_.p, n, ns, d_var);
+  cuda_check(cudaGetLastError(), "rbmc launch");
 }
 
 void DeviceFactor::copy_l_panels(std::vector<double>& out) const {

@@ -111,6 +111,15 @@ class DeviceFactor {
     if (!selinv_plan_) build_selinv_plan();
   }
 
+  // sample_direct (gmrf.hpp:173,182) repeated: out[:, s] = mean + Pᵀ L⁻ᵀ z_s with
+  // z_s the s-th normal_vector(n) of Rng(seed) (core/rng.hpp); device pointers,
+  // out is n × ns column-major.
+  void sample_direct(const double* d_mean, int ns, uint64_t seed, double* d_out);
+  // rbmc_variance (gmrf.hpp:213-240): Rao-Blackwellized Monte Carlo marginal
+  // variances from ns exact samples; q_values (device) in the symbolic's CSC order.
+  void rbmc_variance(const double* d_qvals, const double* d_mean, int ns, uint64_t seed,
+                     double* d_var);
+
   // Host copies (tests / small n).
   void copy_l_panels(std::vector<double>& out) const;
   void copy_sig_panels(std::vector<double>& out) const;
@@ -164,6 +173,10 @@ class DeviceFactor {
   DevBuf<RowXfer> xt_;
   DevBuf<double> xb_;             // backward-solve pack buffer (Σ r_c × kMaxRhs)
   DevBuf<char> colmine_;          // per internal column: owned by this rank
+  // sampling / RBMC workspaces (pattern of Q for the SpMV, sample batches)
+  DevBuf<int64_t> qcp_d_;
+  DevBuf<int32_t> qri_d_;
+  DevBuf<double> zb_, wb_, ub_, qc_, rbm_, rbm2_, qdg_;
   bool factored_ = false, selinv_done_ = false;
 
   DevBuf<int32_t> first_, rows_, relmap_, chptr_, chlist_, perm_, col2sn_, snparent_, status_;

@@ -328,6 +328,77 @@ __global__ void k_mask_cols(double* __restrict__ y, const char* __restrict__ col
 }
 
 // ---------------------------------------------------------------------------
+// Sampling and RBMC variances (gmrf.hpp:173-240).
+// ---------------------------------------------------------------------------
+// u[:, b] = mean + x[:, b] (vec_add, gmrf.hpp:179)
+__global__ void k_add_mean(const double* __restrict__ mean, int n, int nb,
+                           double* __restrict__ u) {
+  const int64_t tot = static_cast<int64_t>(n) * nb;
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < tot;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    u[idx] = __dadd_rn(mean[idx % n], u[idx]);
+}
+
+// y[i, b] = Σ_j Q_ij c_j with c = u[:, b] − mean (vec_sub), Q symmetric: column i
+// of the full CSC in ascending j — the accumulation order of matvec(Q, c)
+// (sparse.hpp:130-147) for row i.
+__global__ void k_rbmc_spmv(const int64_t* __restrict__ cp, const int32_t* __restrict__ ri,
+                            const double* __restrict__ qv, const double* __restrict__ mean,
+                            const double* __restrict__ u, int n, int nb,
+                            double* __restrict__ y) {
+  const int64_t tot = static_cast<int64_t>(n) * nb;
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < tot;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int i = static_cast<int>(idx % n);
+    const double* ub = u + (idx / n) * n;
+    double s = 0.0;
+    for (int64_t p = cp[i]; p < cp[i + 1]; ++p) {
+      const int j = ri[p];
+      s = __dadd_rn(s, __dmul_rn(qv[p], __dadd_rn(ub[j], -mean[j])));
+    }
+    y[idx] = s;
+  }
+}
+
+// Welford update per coordinate over the batch's samples in draw order
+// (gmrf.hpp:226-235): m = μ + c − (Qc)_i / Q_ii.
+__global__ void k_rbmc_welford(const double* __restrict__ mean, const double* __restrict__ u,
+                               const double* __restrict__ qc, const double* __restrict__ qdiag,
+                               int n, int nb, int s0, double* __restrict__ mm,
+                               double* __restrict__ m2) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double a = mm[i], b = m2[i];
+    const double mu = mean[i], qd = qdiag[i];
+    for (int k = 0; k < nb; ++k) {
+      const double c = __dadd_rn(u[i + static_cast<int64_t>(k) * n], -mu);
+      const double m = __dadd_rn(__dadd_rn(mu, c), -__ddiv_rn(qc[i + static_cast<int64_t>(k) * n], qd));
+      const double delta = __dadd_rn(m, -a);
+      a = __dadd_rn(a, __ddiv_rn(delta, static_cast<double>(s0 + k + 1)));
+      b = __dadd_rn(b, __dmul_rn(delta, __dadd_rn(m, -a)));
+    }
+    mm[i] = a;
+    m2[i] = b;
+  }
+}
+
+__global__ void k_rbmc_final(const double* __restrict__ qdiag, const double* __restrict__ m2,
+                             int n, int ns, double* __restrict__ var) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    var[i] = __dadd_rn(__ddiv_rn(1.0, qdiag[i]), __ddiv_rn(m2[i], static_cast<double>(ns - 1)));
+}
+
+// Q_ii from the full CSC (csc_diag); 0 if the diagonal is not stored
+__global__ void k_csc_diag(const int64_t* __restrict__ cp, const int32_t* __restrict__ ri,
+                           const double* __restrict__ qv, int n, double* __restrict__ d) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double v = 0.0;
+    for (int64_t p = cp[i]; p < cp[i + 1]; ++p)
+      if (ri[p] == i) v = qv[p];
+    d[i] = v;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Microbenchmarks for the FP64 roofline denominator (DMMA vs DFMA issue rate).
 // ---------------------------------------------------------------------------
 __global__ void k_bench_dmma(double* out, int iters) {

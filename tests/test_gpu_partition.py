@@ -29,7 +29,7 @@ def grid_q(nx, ny, shift=0.05):
 def outputs(f, b, z):
     return (g.solve(f, b), g.solve_triangular(f, z, g.TriangularMode.kLower),
             g.solve_triangular(f, z, g.TriangularMode.kUpper), g.solve(f, z),
-            g.takahashi_diagonal(f))
+            g.takahashi_diagonal(f), g.sample_direct(f, b, 3, 2001))
 
 
 # (48, 40): narrow supernodes only; (300, 280): top separators wider than 256
@@ -51,7 +51,7 @@ def test_partitioned_matches_single_gpu_bitwise(shape, nranks):
     grp.run_ranks(lambda r: fs[r].refactor(q.values))
     res = grp.run_ranks(lambda r: outputs(fs[r], b, z))
     for r in range(nranks):
-        for a, e, what in zip(res[r], ref, ["solve", "lower", "upper", "solve16", "var"]):
+        for a, e, what in zip(res[r], ref, ["solve", "lower", "upper", "solve16", "var", "samples"]):
             assert np.array_equal(a, e), (r, what, np.abs(a - e).max())
         # each rank holds its own panels only
         assert fs[r].stats().device_bytes < single_bytes
