@@ -133,6 +133,32 @@ int gmrf_factor_l(gmrf_factor_t* f, int64_t* col_ptr, int32_t* row_idx, double* 
 int gmrf_factor_stats(const gmrf_factor_t* f, gmrf_factor_stats_t* st);
 void gmrf_factor_free(gmrf_factor_t* f);
 
+/* ---- Conjugate gradients (core/cg.hpp:39-105) and CG sampling --------------
+ * Matrix-free alternative to the factorization (gmrf.hpp:188-202). Same
+ * recurrence, stopping rule ‖r‖ ≤ max(rtol‖b‖, atol) and breakdown error as
+ * the reference; reductions are deterministic device trees. */
+typedef struct {
+  double rtol;             /* CGConfig::rtol (> 0) */
+  double atol;
+  int64_t max_iter;        /* 0: 10·n */
+  int32_t preconditioner;  /* 0 kNone, 1 kJacobi (diag of Q) */
+} gmrf_cg_config_t;
+typedef struct {
+  int64_t iterations;
+  double final_residual;
+  int32_t converged;
+} gmrf_cg_result_t; /* CGResult (cg.hpp:29-34) */
+/* cg_solve(q, b, x0, cfg) (cg.hpp:98): Q full CSC n × n; x0 may be NULL. */
+int gmrf_cg_solve(int32_t n, const int64_t* col_ptr, const int32_t* row_idx, const double* values,
+                  const double* b, const double* x0, const gmrf_cg_config_t* cfg, double* x,
+                  gmrf_cg_result_t* res);
+/* sample_cg (gmrf.hpp:188): out = mean + Q⁻¹ S z, S the n × m square root (CSC);
+ * GMRF_ERR_NUMERICAL if CG does not converge. */
+int gmrf_sample_cg(int32_t n, const int64_t* q_col_ptr, const int32_t* q_row_idx,
+                   const double* q_values, int32_t m, const int64_t* s_col_ptr,
+                   const int32_t* s_row_idx, const double* s_values, const double* mean,
+                   const double* z, const gmrf_cg_config_t* cfg, double* out);
+
 /* ---- Partitioned factorization across ranks (multi-GPU) -----
  * No reference analogue (the reference is single-threaded):
  * the supernodal tree is split along its top nested-dissection separators

@@ -131,6 +131,8 @@ class Ref:
         lib.ref_condition_affine.argtypes = [C.c_int, i32p, i32p, f64p, f64p, C.c_int, i32p, i32p,
                                              f64p, f64p, f64p, f64p]
         lib.ref_time_stages.argtypes = [C.c_int, i32p, i32p, f64p, C.c_int, f64p]
+        lib.ref_cg_solve.argtypes = [C.c_int, i32p, i32p, f64p, f64p, C.c_double, C.c_double,
+                                     C.c_longlong, C.c_int, f64p, f64p]
         for nm in ("ref_sample_direct", "ref_rbmc_variance"):
             getattr(lib, nm).argtypes = [C.c_int, i32p, i32p, f64p, i32p, f64p, C.c_int,
                                          C.c_ulonglong, f64p]
@@ -213,6 +215,17 @@ class Ref:
                                       _p(out, f64p)) != 0:
             raise RuntimeError(self.err())
         return out
+
+    def cg_solve(self, n, cp, ri, v, b, rtol=1e-8, atol=0.0, max_iter=0, jacobi=False):
+        """cg_solve (cg.hpp:98) → (x, iterations, final_residual, converged)."""
+        cp, ri, v = self._csc32(cp, ri, v)
+        x = np.empty(n)
+        info = np.zeros(3)
+        if self.lib.ref_cg_solve(n, _p(cp, i32p), _p(ri, i32p), _p(v, f64p),
+                                 _p(np.ascontiguousarray(b, np.float64), f64p), rtol, atol,
+                                 max_iter, int(jacobi), _p(x, f64p), _p(info, f64p)) != 0:
+            raise RuntimeError(self.err())
+        return x, int(info[0]), float(info[1]), bool(info[2])
 
     def time_stages(self, n, cp, ri, v, do_taka):
         cp, ri, v = self._csc32(cp, ri, v)

@@ -22,6 +22,7 @@
 #include <vector>
 
 #include "gmrfpde/core/amd.hpp"
+#include "gmrfpde/core/cg.hpp"
 #include "gmrfpde/core/cholesky.hpp"
 #include "gmrfpde/core/rng.hpp"
 #include "gmrfpde/core/sparse.hpp"
@@ -620,6 +621,29 @@ int ref_rbmc_variance(int n, const int* cp, const int* ri, const double* v, cons
         cholesky_factor(q, std::vector<Index>(perm, perm + n))));
     Vector var = rbmc_variance(g, ns, seed);
     std::memcpy(out, var.data(), sizeof(double) * n);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// cg_solve (cg.hpp:98), matrix-backed; out_info = {iterations, final_residual, converged}
+int ref_cg_solve(int n, const int* cp, const int* ri, const double* v, const double* b,
+                 double rtol, double atol, long long max_iter, int jacobi, double* x,
+                 double* out_info) {
+  try {
+    SparseMatrixCSC q = make_csc(n, n, cp, ri, v);
+    CGConfig cfg;
+    cfg.rtol = rtol;
+    cfg.atol = atol;
+    cfg.max_iter = static_cast<Index>(max_iter);
+    cfg.preconditioner = jacobi ? Preconditioner::kJacobi : Preconditioner::kNone;
+    CGResult r = cg_solve(q, Vector(b, b + n), Vector(), cfg);
+    std::memcpy(x, r.x.data(), sizeof(double) * n);
+    out_info[0] = static_cast<double>(r.iterations);
+    out_info[1] = r.final_residual;
+    out_info[2] = r.converged ? 1.0 : 0.0;
     return 0;
   } catch (const std::exception& e) {
     g_err = e.what();

@@ -6,6 +6,11 @@ factorization, triangular solves and selected inversion. This package is the
 host-side mirror of the reference API (gmrfpde core/*).
 """
 from .core import (  # noqa: F401
+    CGConfig,
+    CGResult,
+    Preconditioner,
+    cg_solve,
+    sample_cg,
     CholeskyFactor,
     ContractError,
     DeviceError,

@@ -74,6 +74,16 @@ class SpaceTimeInfo(C.Structure):
 vp = C.c_void_p
 
 
+class CgConfig(C.Structure):
+    _fields_ = [("rtol", C.c_double), ("atol", C.c_double), ("max_iter", C.c_int64),
+                ("preconditioner", C.c_int32)]
+
+
+class CgResult(C.Structure):
+    _fields_ = [("iterations", C.c_int64), ("final_residual", C.c_double),
+                ("converged", C.c_int32)]
+
+
 class Msg(C.Structure):
     """gmrf_msg_t: one message of an exchange point of a partitioned factor."""
     _fields_ = [("kind", C.c_int32), ("peer", C.c_int32), ("tag", C.c_int32),
@@ -109,6 +119,10 @@ SIGNATURES = {
     "gmrf_factor_stats": (C.c_int, [C.c_void_p, C.POINTER(FactorStats)]),
     "gmrf_factor_free": (None, [C.c_void_p]),
     "gmrf_bench_fp64": (C.c_int, [f64p, f64p]),
+    "gmrf_cg_solve": (C.c_int, [C.c_int32, i64p, i32p, f64p, f64p, f64p, C.POINTER(CgConfig),
+                                f64p, C.POINTER(CgResult)]),
+    "gmrf_sample_cg": (C.c_int, [C.c_int32, i64p, i32p, f64p, C.c_int32, i64p, i32p, f64p, f64p,
+                                 f64p, C.POINTER(CgConfig), f64p]),
     "gmrf_partition_owners": (C.c_int, [vp, C.c_int32, i32p]),
     "gmrf_partition_schedule": (C.c_int, [vp, i32p, i64p, i64p]),
     "gmrf_factor_create_partitioned": (C.c_int, [vp, C.c_int32, C.c_int32, i32p, EXCHANGE_FN, vp,

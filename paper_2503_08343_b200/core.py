@@ -304,6 +304,69 @@ def rbmc_variance(f: CholeskyFactor, q: SparseMatrixCSC, mean, n_samples: int,
     return var
 
 
+class Preconditioner:
+    kNone = 0
+    kJacobi = 1
+
+
+@dataclass
+class CGConfig:
+    """cg.hpp:14-25."""
+    rtol: float = 1e-8
+    atol: float = 0.0
+    max_iter: int = 0
+    preconditioner: int = Preconditioner.kNone
+
+    def _c(self):
+        return _capi.CgConfig(self.rtol, self.atol, self.max_iter, self.preconditioner)
+
+
+@dataclass
+class CGResult:
+    """cg.hpp:29-34."""
+    x: np.ndarray
+    iterations: int
+    final_residual: float
+    converged: bool
+
+
+def cg_solve(q: SparseMatrixCSC, b, x0=None, cfg: CGConfig | None = None) -> CGResult:
+    """cg.hpp:98 (matrix-backed cg_solve) on the device."""
+    cfg = cfg or CGConfig()
+    _validate_square(q, "cg_solve")
+    n = q.nrows
+    bb = np.ascontiguousarray(b, np.float64)
+    if bb.shape[0] != n:
+        raise DimensionError("cg: b dimension mismatch")
+    xx0 = None if x0 is None or len(x0) == 0 else np.ascontiguousarray(x0, np.float64)
+    if xx0 is not None and xx0.shape[0] != n:
+        raise DimensionError("cg: x0 dimension mismatch")
+    x = np.empty(n)
+    r = _capi.CgResult()
+    c = cfg._c()
+    _check(_capi.load().gmrf_cg_solve(n, ptr(q.col_ptr, i64p), ptr(q.row_idx, i32p),
+                                      ptr(q.values, f64p), ptr(bb, f64p), ptr(xx0, f64p),
+                                      C.byref(c), ptr(x, f64p), C.byref(r)))
+    return CGResult(x, int(r.iterations), float(r.final_residual), bool(r.converged))
+
+
+def sample_cg(q: SparseMatrixCSC, s: SparseMatrixCSC, mean, z, cfg: CGConfig | None = None):
+    """gmrf.hpp:188 — mean + Q⁻¹ S z by CG (S = the square root, n × m)."""
+    cfg = cfg or CGConfig()
+    n = q.nrows
+    zz = np.ascontiguousarray(z, np.float64)
+    if zz.shape[0] != s.ncols:
+        raise DimensionError("sample_cg: z length must equal sqrt column count")
+    mu = np.ascontiguousarray(mean, np.float64)
+    out = np.empty(n)
+    c = cfg._c()
+    _check(_capi.load().gmrf_sample_cg(n, ptr(q.col_ptr, i64p), ptr(q.row_idx, i32p),
+                                       ptr(q.values, f64p), s.ncols, ptr(s.col_ptr, i64p),
+                                       ptr(s.row_idx, i32p), ptr(s.values, f64p), ptr(mu, f64p),
+                                       ptr(zz, f64p), C.byref(c), ptr(out, f64p)))
+    return out
+
+
 def takahashi_selected_inverse(f: CholeskyFactor) -> SparseMatrixCSC:
     """takahashi.hpp:19 — Σ on the pattern of L+Lᵀ, original indices."""
     lib = _capi.load()

@@ -8,6 +8,7 @@
 #include <string>
 #include <tuple>
 
+#include "cg.hpp"
 #include "factor.hpp"
 #include "partition.hpp"
 #include "spacetime.hpp"
@@ -123,6 +124,45 @@ int gmrf_factor_create(const gmrf_symbolic_t* h, gmrf_factor_t** out) {
       gmrf::fail(gmrf::kCuda, "no CUDA device: libgmrf_b200 has no CPU fallback");
     f->f = std::make_unique<gmrf::DeviceFactor>(h->s);
     *out = f.release();
+  });
+}
+
+static gmrf::CgOptions cg_opts(const gmrf_cg_config_t* c) {
+  gmrf::CgOptions o;
+  if (c) {
+    o.rtol = c->rtol;
+    o.atol = c->atol;
+    o.max_iter = c->max_iter;
+    gmrf::require(c->preconditioner == 0 || c->preconditioner == 1, gmrf::kContract,
+                  "cg: unknown preconditioner");
+    o.jacobi = c->preconditioner == 1;
+  }
+  return o;
+}
+
+static void need_device() {
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    gmrf::fail(gmrf::kCuda, "no CUDA device: libgmrf_b200 has no CPU fallback");
+}
+
+int gmrf_cg_solve(int32_t n, const int64_t* cp, const int32_t* ri, const double* v,
+                  const double* b, const double* x0, const gmrf_cg_config_t* cfg, double* x,
+                  gmrf_cg_result_t* res) {
+  return guard([&] {
+    need_device();
+    gmrf::CgOutcome r = gmrf::cg_solve_device(n, cp, ri, v, b, x0, cg_opts(cfg), x);
+    if (res) *res = {r.iterations, r.final_residual, r.converged ? 1 : 0};
+  });
+}
+
+int gmrf_sample_cg(int32_t n, const int64_t* qcp, const int32_t* qri, const double* qv,
+                   int32_t m, const int64_t* scp, const int32_t* sri, const double* sv,
+                   const double* mean, const double* z, const gmrf_cg_config_t* cfg,
+                   double* out) {
+  return guard([&] {
+    need_device();
+    gmrf::sample_cg_device(n, qcp, qri, qv, m, scp, sri, sv, mean, z, cg_opts(cfg), out);
   });
 }
 
