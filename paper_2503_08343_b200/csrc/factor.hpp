@@ -66,13 +66,6 @@ struct PartitionSpec {
   void* ctx = nullptr;
 };
 
-// Row gather/scatter of x for the backward-solve exchange (x[rows[i] + rr*n]).
-struct RowXfer {
-  const int32_t* rows;
-  int32_t cnt;
-  int64_t off;  // offset in the pack buffer, per right-hand side
-};
-
 struct FactorTimes {
   float numeric_ms = 0, solve_ms = 0, selinv_ms = 0;
 };

@@ -82,6 +82,14 @@ struct WideBlock {
   int32_t flag0;  // flag index of block 0 of this supernode
 };
 
+// Row gather/scatter of x for the partitioned backward-solve exchange
+// (x[rows[i] + rr*n], partition.hpp).
+struct RowXfer {
+  const int32_t* rows;
+  int32_t cnt;
+  int64_t off;  // offset in the pack buffer, per right-hand side
+};
+
 // Device view of the symbolic structure (all arrays device-resident).
 struct SymDev {
   const int32_t* sn_first;

@@ -10,34 +10,53 @@
 #include <cstdio>
 #include <vector>
 
-#include "kernels.cu"
+#include "../tools/gemm_variants.cuh"
 
 using namespace gmrf;
 
-static double run(const char* name, std::vector<GemmTask>& tasks, double flops) {
+typedef void (*KFn)(const GemmTask*);
+struct Var {
+  const char* name;
+  KFn fn;
+  int threads;
+  int smem = 0;
+};
+static std::vector<Var> g_vars;
+
+static void run(const char* name, std::vector<GemmTask>& tasks, double flops) {
   GemmTask* dt;
   cudaMalloc(&dt, tasks.size() * sizeof(GemmTask));
   cudaMemcpy(dt, tasks.data(), tasks.size() * sizeof(GemmTask), cudaMemcpyHostToDevice);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  float best = 1e9f;
-  for (int rep = 0; rep < 8; ++rep) {
-    cudaEventRecord(e0);
-    k_gemm_tiles<<<static_cast<unsigned>(tasks.size()), 128>>>(dt);
-    cudaEventRecord(e1);
-    cudaEventSynchronize(e1);
-    float ms;
-    cudaEventElapsedTime(&ms, e0, e1);
-    if (rep > 0 && ms < best) best = ms;
+  for (const Var& v : g_vars) {
+    float best = 1e9f;
+    for (int rep = 0; rep < 8; ++rep) {
+      cudaEventRecord(e0);
+      v.fn<<<static_cast<unsigned>(tasks.size()), v.threads, v.smem>>>(dt);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      if (rep > 0 && ms < best) best = ms;
+    }
+    printf("%-9s %-14s %6zu tiles  %8.1f us  %6.2f TF/s  (%s)\n", name, v.name, tasks.size(),
+           best * 1e3, flops / (best * 1e-3) / 1e12, cudaGetErrorString(cudaGetLastError()));
   }
-  printf("%-9s %6zu tiles  %8.1f us  %6.2f TF/s  (%s)\n", name, tasks.size(), best * 1e3,
-         flops / (best * 1e-3) / 1e12, cudaGetErrorString(cudaGetLastError()));
   cudaFree(dt);
-  return best;
 }
 
 int main() {
+  g_vars = {{"base", k_gemm_tiles, 128},
+            {"var_ref", k_gemm_var<2, 2, 16, false, 4, false, 0>, 128},
+            {"nomul", k_gemm_var<2, 2, 16, false, 4, false, 3>, 128},
+            {"nomul_nv", k_gemm_var<2, 2, 16, false, 4, true, 3>, 128},
+            {"nomul_w2x4", k_gemm_var<2, 4, 16, false, 3, true, 3>, 256}};
+  cudaFuncSetAttribute(k_gemm_ms<3, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm_ms_smem<3>());
+  cudaFuncSetAttribute(k_gemm_ms<4, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm_ms_smem<4>());
+  cudaFuncSetAttribute(k_gemm_ms<5, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm_ms_smem<5>());
+  cudaFuncSetAttribute(k_gemm_ms<5, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm_ms_smem<5>());
   const int64_t N = 4096;
   double* buf;
   cudaMalloc(&buf, N * N * sizeof(double) * 3);
@@ -116,6 +135,16 @@ int main() {
         fl += 2.0 * 64 * 64 * 1024;
       }
     run("syrk1k", t, fl);
+    std::vector<GemmTask> t4;
+    for (int c = 0; c < 4; ++c)
+      for (GemmTask g : t) {
+        g.c += static_cast<int64_t>(c) * 1024 * 1024 * 2;
+        t4.push_back(g);
+      }
+    run("syrk1k_x4", t4, 4 * fl);
+    std::vector<GemmTask> t2(t4.begin(), t4.end());
+    for (GemmTask& g : t2) g.k[0] = 256;
+    run("syrk256_x4", t2, fl);
   }
   return 0;
 }
