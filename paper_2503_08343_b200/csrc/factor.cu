@@ -364,6 +364,11 @@ void DeviceFactor::build_factor_plan() {
     for (int c = 0; c < nch; ++c) {
       const int lv = lvl0[k] + c;
       const int c0 = c * kNB, wk = std::min(kNB, w - c0);
+      if (c == 0 && s.ch_ptr[k + 1] == s.ch_ptr[k] && r > 0) {
+        // no children: the extend-add tasks only zero the update block
+        for (int b = w; b < rows; ++b) ea[lv].push_back({k, b, 0, 0});
+        ea_b[lv] += 4.0 * r * (r + 1.0);
+      }
       if (c == 0 && s.ch_ptr[k + 1] > s.ch_ptr[k]) {
         // front column b receives child c's update column ia where rel_c[ia] = b
         cnt.assign(rows + 1, 0);
@@ -374,10 +379,14 @@ void DeviceFactor::build_factor_plan() {
           ea_b[lv] += 12.0 * rc * (rc + 1.0);  // read U_c lower (8 B) + RMW target (16 B)
         }
         const int64_t base = static_cast<int64_t>(ea_pairs.size());
+        // every update-block column gets a task: it zeroes the column first
+        // (replaces a memset of all update matrices per factorization)
         for (int b = 0; b < rows; ++b) {
-          if (cnt[b + 1]) ea[lv].push_back({k, b, static_cast<int32_t>(base + cnt[b]), cnt[b + 1]});
+          if (cnt[b + 1] || b >= w)
+            ea[lv].push_back({k, b, static_cast<int32_t>(base + cnt[b]), cnt[b + 1]});
           cnt[b + 1] += cnt[b];
         }
+        ea_b[lv] += 4.0 * r * (r + 1.0);
         ea_pairs.resize(base + cnt[rows]);
         for (int q = s.ch_ptr[k]; q < s.ch_ptr[k + 1]; ++q) {
           const int ch = s.ch_list[q], wc = s.w(ch), rc = s.r(ch);
@@ -714,7 +723,8 @@ void DeviceFactor::build_selinv_plan() {
 void DeviceFactor::begin_numeric() {
   launches_numeric_ = 0;
   cuda_check(cudaMemsetAsync(L_.p, 0, L_.n * sizeof(double), stream_), "memset L");
-  cuda_check(cudaMemsetAsync(U_.p, 0, U_.n * sizeof(double), stream_), "memset U");
+  // update matrices: zeroed column by column by the extend-add tasks of their
+  // level (k_extend_add); small fronts write theirs whole
   cuda_check(cudaMemsetAsync(status_.p, 0x7f, sizeof(int), stream_), "status");
 }
 

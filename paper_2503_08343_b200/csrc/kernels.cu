@@ -161,7 +161,9 @@ __global__ void __launch_bounds__(128, 4) k_gemm_tiles(const GemmTask* __restric
 // (panel step: panel.cuh)
 // ---------------------------------------------------------------------------
 // Extend-add (multifrontal assembly), gather form: one warp per (front, front
-// column) that some child updates; the plan lists the contributing children
+// column) that some child updates, and per column of the front's update block
+// (zeroed here first, so no per-factorization memset of the update matrices);
+// the plan lists the contributing children
 // and the row where each child's update column starts (no searching on the
 // device). Children are visited in ascending order, so every target entry
 // receives its contributions in a fixed order (deterministic, no atomics).
@@ -189,6 +191,10 @@ __global__ void k_extend_add(const EaTask* __restrict__ tasks, int ntasks,
   double* Ls = L + sd.lptr[s];
   double* Us = U + sd.uptr[s];
   double* dst = b < w ? Ls + static_cast<int64_t>(b) * rows : Us + static_cast<int64_t>(b - w) * r - w;
+  if (b >= w) {  // update-block column: starts from zero (lower part, rows b..rows-1)
+    for (int a = b + lane; a < rows; a += 32) dst[a] = 0.0;
+    __syncwarp();
+  }
   for (int p = t.p0; p < t.p0 + t.np; ++p) {
     const int2 cp = pairs[p];
     const int c = cp.x, ib = cp.y;
