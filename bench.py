@@ -207,6 +207,12 @@ def main():
     ap.add_argument("--n-el", type=int, default=999)
     ap.add_argument("--n-t", type=int, default=1000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", choices=["c4", "c5"], default="c4",
+                    help="c4 (default, the headline): config-4 Burgers posterior at full size; "
+                         "c5: config-5 Allen-Cahn posterior at the largest shape one B200 holds "
+                         "(--c5-cells x --c5-cells cells x --c5-slices), seed 1005+rank")
+    ap.add_argument("--c5-cells", type=int, default=64)
+    ap.add_argument("--c5-slices", type=int, default=128)
     ap.add_argument("--partition", action="store_true",
                     help="N>1: one posterior, its factorization / solves / selected inversion "
                          "partitioned along the top ND separators across the ranks (NCCL), "
@@ -222,6 +228,18 @@ def main():
               "n_el": args.n_el, "n_t": args.n_t, "gn_steps": 10,
               "l2": "inputs larger than L2 (factor storage ~3 GB, Sigma panels ~1.6 GB)",
               "parallelism": f"replicas x{world} (batch sharding, one posterior per GPU)"}
+    c5 = args.workload == "c5"
+    if c5:
+        nn = args.c5_cells + 1
+        config = {"workload": f"config 5 (reduced to one B200): space-time Allen-Cahn GN-Laplace "
+                              f"posterior, P1 {nn}x{nn}-node unit square x {args.c5_slices} "
+                              f"implicit-Euler slices over [0, 0.5], n={nn * nn * args.c5_slices:,}, "
+                              f"8 GN steps (full config 5 is 128x128x256: nnz(L) ~2.5e10, over "
+                              f"one GPU's HBM)",
+                  "n_cells": args.c5_cells, "n_t": args.c5_slices, "gn_steps": 8,
+                  "l2": "inputs larger than L2",
+                  "parallelism": f"replicas x{world} (batch of independent seeds 1005+rank, one "
+                                 f"per GPU)"}
     partitioned = args.partition and world > 1
     if partitioned:
         config["parallelism"] = (f"nd-partition x{world} (one posterior; supernodal tree split "
@@ -229,6 +247,11 @@ def main():
 
     if args.impl == "reference":
         if rank != 0:
+            return
+        if c5:
+            print(json.dumps({"impl": "reference", "unavailable": (
+                "config 5 at >= 64x64x128 overflows the reference's int32 nnz(L) "
+                "(BASELINE.md §2); its CPU arm is measured on config 4")}), flush=True)
             return
         rb = reference_sample()
         line = {"impl": "reference", "metric": METRIC, "value": rb["value"], "unit": UNIT,
@@ -254,17 +277,26 @@ def main():
 
     peak_fp64 = fp64_peak_tflops()
     peaks = load_peaks()
-    spec = SpaceTimeSpec.burgers(n_el=args.n_el, n_t=args.n_t)
+    if c5:
+        spec = SpaceTimeSpec.allen_cahn(n_cells=args.c5_cells, n_t=args.c5_slices)
+        gn_iters = 8
+    else:
+        spec = SpaceTimeSpec.burgers(n_el=args.n_el, n_t=args.n_t)
+        gn_iters = 10
     t0 = time.perf_counter()
     if partitioned:
         from paper_2503_08343_b200.partition import TorchExchange
-        post = SpaceTimePosterior(spec, GaussNewtonConfig(max_iters=10),
+        post = SpaceTimePosterior(spec, GaussNewtonConfig(max_iters=gn_iters),
                                   partition=(world, rank, TorchExchange()))
     else:
-        post = SpaceTimePosterior(spec, GaussNewtonConfig(max_iters=10))
+        post = SpaceTimePosterior(spec, GaussNewtonConfig(max_iters=gn_iters))
     host_setup_s = time.perf_counter() - t0
-    x = spec.node_x()
-    u0 = -np.sin(np.pi * x)
+    if c5:  # u0_d = -0.1 + 0.2·Rng(1005+b).uniform() in DoF order
+        from paper_2503_08343_b200 import Rng
+        u0 = -0.1 + 0.2 * Rng(1005 + rank).uniforms(spec.n_space)
+    else:
+        x = spec.node_x()
+        u0 = -np.sin(np.pi * x)
 
     for _ in range(max(args.warmup, 0)):
         post.run(u0, variances=True, copy_back=False)
@@ -372,7 +404,11 @@ def main():
         "nnz_l": info.nnz_l, "nnz_l_padded": info.nnz_l_padded,
         "peaks": {"fp64_tflops_dgemm": peak_fp64, "hbm_gbs": peaks.get("hbm_gbs")},
     }
-    if not args.no_cpu_baseline and world == 1:
+    if c5:
+        line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference",
+                                "sample": "not run for config 5: the reference's int32 nnz(L) "
+                                          "overflows at this shape (BASELINE.md §2)"}
+    elif not args.no_cpu_baseline and world == 1:
         try:
             rb = reference_sample()
             line["cpu_baseline"] = {k: rb[k] for k in ("value", "unit", "cores", "kind", "sample")}

@@ -204,6 +204,11 @@ int gmrf_factor_create_partitioned(const gmrf_symbolic_t* s, int32_t nranks, int
                                    const int32_t* owner, gmrf_exchange_fn fn, void* ctx,
                                    gmrf_factor_t** out);
 
+/* Rng (core/rng.hpp:14-47): n draws of Rng(seed).uniform() (kind 0) or
+ * .normal() (kind 1, Box-Muller with the cached spare), host only — the
+ * reference's seeded synthetic inputs without the reference. */
+int gmrf_rng_fill(uint64_t seed, int32_t kind, int64_t n, double* out);
+
 /* FP64 issue-rate microbenchmark (TFLOP/s) of DMMA m8n8k4 and DFMA. */
 int gmrf_bench_fp64(double* dmma_tflops, double* dfma_tflops);
 

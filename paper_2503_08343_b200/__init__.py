@@ -9,6 +9,7 @@ from .core import (  # noqa: F401
     CGConfig,
     CGResult,
     Preconditioner,
+    Rng,
     cg_solve,
     sample_cg,
     CholeskyFactor,

@@ -119,6 +119,7 @@ SIGNATURES = {
     "gmrf_factor_stats": (C.c_int, [C.c_void_p, C.POINTER(FactorStats)]),
     "gmrf_factor_free": (None, [C.c_void_p]),
     "gmrf_bench_fp64": (C.c_int, [f64p, f64p]),
+    "gmrf_rng_fill": (C.c_int, [C.c_uint64, C.c_int32, C.c_int64, f64p]),
     "gmrf_cg_solve": (C.c_int, [C.c_int32, i64p, i32p, f64p, f64p, f64p, C.POINTER(CgConfig),
                                 f64p, C.POINTER(CgResult)]),
     "gmrf_sample_cg": (C.c_int, [C.c_int32, i64p, i32p, f64p, C.c_int32, i64p, i32p, f64p, f64p,

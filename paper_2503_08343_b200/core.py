@@ -381,6 +381,27 @@ def takahashi_selected_inverse(f: CholeskyFactor) -> SparseMatrixCSC:
     return SparseMatrixCSC(n, n, cp, ri, v)
 
 
+class Rng:
+    """core/rng.hpp:14-47 draws (mt19937_64 + Box-Muller with a cached spare),
+    generated in the library (host); the stream restarts per call."""
+
+    def __init__(self, seed: int):
+        self.seed = int(seed)
+
+    def _fill(self, kind, n):
+        out = np.empty(int(n))
+        _check(_capi.load().gmrf_rng_fill(self.seed, kind, int(n), ptr(out, f64p)))
+        return out
+
+    def uniforms(self, n):
+        """The first n values of uniform() from a fresh Rng(seed)."""
+        return self._fill(0, n)
+
+    def normal_vector(self, n):
+        """normal_vector(n) of a fresh Rng(seed)."""
+        return self._fill(1, n)
+
+
 def bench_fp64() -> tuple[float, float]:
     a, b = C.c_double(), C.c_double()
     _check(_capi.load().gmrf_bench_fp64(C.byref(a), C.byref(b)))

@@ -11,6 +11,7 @@
 #include "cg.hpp"
 #include "factor.hpp"
 #include "partition.hpp"
+#include "rng.hpp"
 #include "spacetime.hpp"
 
 static_assert(sizeof(gmrf_msg_t) == sizeof(gmrf::XferMsg), "gmrf_msg_t layout");
@@ -360,6 +361,14 @@ int gmrf_factor_stats(const gmrf_factor_t* f, gmrf_factor_stats_t* st) {
 }
 
 void gmrf_factor_free(gmrf_factor_t* f) { delete f; }
+
+int gmrf_rng_fill(uint64_t seed, int32_t kind, int64_t n, double* out) {
+  return guard([&] {
+    gmrf::require(kind == 0 || kind == 1, gmrf::kContract, "rng_fill: kind must be 0 or 1");
+    gmrf::HostRng r(seed);
+    for (int64_t i = 0; i < n; ++i) out[i] = kind == 0 ? r.uniform() : r.normal();
+  });
+}
 
 int gmrf_bench_fp64(double* a, double* b) {
   return guard([&] { gmrf::bench_fp64(a, b); });
