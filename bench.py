@@ -402,6 +402,7 @@ def main():
         "kernels": kernels,
         "gn_trace": [[t.objective, t.decrement, t.step_size, t.backtracks] for t in traces[-1]],
         "nnz_l": info.nnz_l, "nnz_l_padded": info.nnz_l_padded,
+        "factor_device_gb": info.factor_device_bytes / 1e9,
         "peaks": {"fp64_tflops_dgemm": peak_fp64, "hbm_gbs": peaks.get("hbm_gbs")},
     }
     if c5:

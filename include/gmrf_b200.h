@@ -264,6 +264,7 @@ typedef struct {
   int32_t n, n_space, n_res;
   int64_t nnz_pattern, nnz_l, nnz_l_padded;
   double flops_ref, flops_sn;
+  int64_t factor_device_bytes; /* L panels + lifetime-packed update matrices + Σ panels + work */
 } gmrf_spacetime_info_t;
 
 int gmrf_spacetime_create(const gmrf_spacetime_config_t* cfg, gmrf_spacetime_t** out);

@@ -68,6 +68,7 @@ class SpaceTimeInfo(C.Structure):
         ("kernel_launches", C.c_int64), ("n", C.c_int32), ("n_space", C.c_int32),
         ("n_res", C.c_int32), ("nnz_pattern", C.c_int64), ("nnz_l", C.c_int64),
         ("nnz_l_padded", C.c_int64), ("flops_ref", C.c_double), ("flops_sn", C.c_double),
+        ("factor_device_bytes", C.c_int64),
     ]
 
 

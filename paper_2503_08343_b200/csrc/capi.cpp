@@ -467,6 +467,7 @@ int gmrf_spacetime_info(const gmrf_spacetime_t* h, gmrf_spacetime_info_t* info) 
     info->nnz_l_padded = s.nnz_l_padded;
     info->flops_ref = s.flops_ref;
     info->flops_sn = s.flops_sn;
+    info->factor_device_bytes = const_cast<gmrf_spacetime_t*>(h)->p->factor().device_bytes();
   });
 }
 

@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <map>
 #include <cstdlib>
 #include <string>
 
@@ -100,15 +101,12 @@ DeviceFactor::DeviceFactor(std::shared_ptr<const Symbolic> sym, cudaStream_t str
   }
   // storage offsets: panels of owned supernodes; update matrices of owned
   // supernodes and of the other ranks' children of owned supernodes (the
-  // Schur complements received before their extend-add)
+  // Schur complements received before their extend-add), packed by lifetime
   lptr_h_.assign(s.ns + 1, 0);
-  uptr_h_.assign(s.ns + 1, 0);
-  for (int k = 0; k < s.ns; ++k) {
-    const int p = s.sn_parent[k];
-    const bool hu = mine(k) || (p >= 0 && mine(p));
+  for (int k = 0; k < s.ns; ++k)
     lptr_h_[k + 1] = lptr_h_[k] + (mine(k) ? static_cast<i64>(s.rows(k)) * s.w(k) : 0);
-    uptr_h_[k + 1] = uptr_h_[k] + (hu ? static_cast<i64>(s.r(k)) * s.r(k) : 0);
-  }
+  if (const char* e = std::getenv("GMRF_U_STATIC")) u_static_ = e[0] != '0';
+  plan_update_storage();
   std::vector<i64> qm;
   if (part_) {  // Q entries of other ranks' supernodes are not stored here
     qm.resize(s.qmap.size());
@@ -135,12 +133,13 @@ DeviceFactor::DeviceFactor(std::shared_ptr<const Symbolic> sym, cudaStream_t str
   rptr_.upload(s.sn_rptr, stream_);
   lptr_.upload(lptr_h_, stream_);
   uptr_.upload(uptr_h_, stream_);
+  uptrs_.upload(uptrs_h_, stream_);
   qmap_.upload(part_ ? qm : s.qmap, stream_);
   status_.alloc(1);
   diag_.alloc(std::max(s.n, 1));
   rdiag_.alloc(std::max(s.n, 1));
   L_.alloc(std::max<int64_t>(lptr_h_[s.ns], 1));
-  U_.alloc(std::max<int64_t>(uptr_h_[s.ns], 1));
+  U_.alloc(std::max<int64_t>(u_arena_, 1));
   q_.alloc(std::max<size_t>(s.qri.size(), 1));
   // solve schedule: supernodes grouped by tree level
   lvl_ptr_.assign(s.n_levels + 1, 0);
@@ -298,6 +297,149 @@ DeviceFactor::~DeviceFactor() {
   if (ev_fork_) cudaEventDestroy(ev_fork_);
   if (aux_) cudaStreamDestroy(aux_);
   if (main_) cudaStreamDestroy(main_);
+}
+
+// Lifetime-packed update-matrix storage, per phase. Factorization: U_k lives
+// from its supernode's first chunk level (extend-add, zeroing) to the parent's
+// first chunk level (the parent's extend-add reads it); a Schur complement
+// received from another rank from the exchange after the child's last level.
+// Selected inversion (levels top-down): Σ_RR(k) lives from its gather (or
+// receipt) to the last of its readers — k's own chunks and its children's
+// gathers. Regions are reused first-fit once their interval has ended, so the
+// buffer holds the live matrices of a level front, not Σ_s r_s² (C4: see
+// gmrf_factor_stats device_bytes). GMRF_U_STATIC=1: one slot per supernode.
+static std::vector<i64> plan_arena(const std::vector<i64>& size, const std::vector<int>& start,
+                                   const std::vector<int>& end, int ntime, i64& total) {
+  const int n = static_cast<int>(size.size());
+  std::vector<i64> off(n, 0);
+  std::vector<std::vector<int>> st(std::max(ntime, 1)), en(std::max(ntime, 1));
+  for (int k = 0; k < n; ++k)
+    if (size[k] > 0) {
+      st[start[k]].push_back(k);
+      en[end[k]].push_back(k);
+    }
+  std::map<i64, i64> by_off;             // free blocks: offset -> size
+  std::multimap<i64, i64> by_size;       // size -> offset
+  auto erase_free = [&](i64 o, i64 z) {
+    auto r = by_size.equal_range(z);
+    for (auto it = r.first; it != r.second; ++it)
+      if (it->second == o) {
+        by_size.erase(it);
+        break;
+      }
+    by_off.erase(o);
+  };
+  total = 0;
+  for (int t = 0; t < ntime; ++t) {
+    std::vector<int>& a = st[t];
+    std::stable_sort(a.begin(), a.end(), [&](int x, int y) { return size[x] > size[y]; });
+    for (int k : a) {
+      auto it = by_size.lower_bound(size[k]);
+      if (it == by_size.end()) {
+        off[k] = total;
+        total += size[k];
+        continue;
+      }
+      const i64 z = it->first, o = it->second;
+      erase_free(o, z);
+      off[k] = o;
+      if (z > size[k]) {
+        by_off[o + size[k]] = z - size[k];
+        by_size.insert({z - size[k], o + size[k]});
+      }
+    }
+    for (int k : en[t]) {
+      i64 o = off[k], z = size[k];
+      auto nx = by_off.lower_bound(o);
+      if (nx != by_off.end() && nx->first == o + z) {
+        const i64 no = nx->first, nz = nx->second;
+        erase_free(no, nz);
+        z += nz;
+      }
+      auto pv = by_off.lower_bound(o);
+      if (pv != by_off.begin()) {
+        --pv;
+        if (pv->first + pv->second == o) {
+          const i64 po = pv->first, pz = pv->second;
+          erase_free(po, pz);
+          o = po;
+          z += pz;
+        }
+      }
+      by_off[o] = z;
+      by_size.insert({z, o});
+    }
+  }
+  return off;
+}
+
+void DeviceFactor::plan_update_storage() {
+  const Symbolic& s = *sym_;
+  std::vector<i64> size(s.ns, 0);
+  for (int k = 0; k < s.ns; ++k) {
+    const int p = s.sn_parent[k];
+    if (p >= 0 && (mine(k) || mine(p))) size[k] = static_cast<i64>(s.r(k)) * s.r(k);
+  }
+  uptr_h_.assign(s.ns + 1, 0);
+  uptrs_h_.assign(s.ns + 1, 0);
+  if (u_static_) {
+    for (int k = 0; k < s.ns; ++k) uptr_h_[k + 1] = uptr_h_[k] + size[k];
+    uptrs_h_ = uptr_h_;
+    u_arena_ = uptr_h_[s.ns];
+    u_arena_f_ = u_arena_s_ = u_arena_;
+    return;
+  }
+  std::vector<int> f0, fl, s0, sl;
+  int nf = 0, nsl = 0;
+  chunk_levels(s, f0, fl, nf, kSmallRows);
+  chunk_levels(s, s0, sl, nsl, 0);
+  std::vector<int> a(s.ns, 0), b(s.ns, 0);
+  for (int k = 0; k < s.ns; ++k) {
+    const int p = s.sn_parent[k];
+    if (!size[k]) continue;
+    if (mine(k) && mine(p)) {
+      a[k] = f0[k];
+      b[k] = f0[p];
+    } else if (mine(k)) {  // sent to the parent's rank after its last level
+      a[k] = f0[k];
+      b[k] = fl[k];
+    } else {  // received from the child's rank
+      a[k] = fl[k];
+      b[k] = f0[p];
+    }
+  }
+  std::vector<i64> fo = plan_arena(size, a, b, nf, u_arena_f_);
+  // selected inversion, time = nsl - 1 - level
+  auto T = [&](int lvl) { return nsl - 1 - lvl; };
+  for (int k = 0; k < s.ns; ++k) {
+    const int p = s.sn_parent[k];
+    if (!size[k]) continue;
+    if (!mine(k)) {  // ghost gather on the parent's rank, sent right away
+      a[k] = b[k] = T(s0[p]);
+      continue;
+    }
+    int last = s0[k];  // lowest level still reading Σ_RR(k)
+    for (int q = s.ch_ptr[k]; q < s.ch_ptr[k + 1]; ++q) {
+      const int c = s.ch_list[q];
+      if (mine(c)) last = std::min(last, sl[c]);
+    }
+    a[k] = T(mine(p) ? sl[k] : s0[p]);
+    b[k] = T(last);
+  }
+  std::vector<i64> so = plan_arena(size, a, b, nsl, u_arena_s_);
+  for (int k = 0; k < s.ns; ++k) {
+    uptr_h_[k] = fo[k];
+    uptrs_h_[k] = so[k];
+  }
+  uptr_h_[s.ns] = u_arena_f_;
+  uptrs_h_[s.ns] = u_arena_s_;
+  u_arena_ = std::max(u_arena_f_, u_arena_s_);
+}
+
+SymDev DeviceFactor::symdev_sel() const {
+  SymDev d = symdev();
+  d.uptr = uptrs_.p;
+  return d;
 }
 
 SymDev DeviceFactor::symdev() const {
@@ -579,7 +721,7 @@ void DeviceFactor::build_selinv_plan() {
     }
     double* Lk = L + lptr_h_[k];
     double* Sk = S + lptr_h_[k];
-    double* Uk = U + uptr_h_[k];
+    double* Uk = U + uptrs_h_[k];
     const int nch = nchunks(w);
     for (int c = nch - 1; c >= 0; --c) {
       const int lv = lvl0[k] + c;
@@ -716,7 +858,7 @@ void DeviceFactor::build_selinv_plan() {
   for (const XEdge& e : sched_)
     if (e.phase == kXSelinv)
       sx_[e.point].push_back({e.src == rank_ ? 0 : 1, e.src == rank_ ? e.dst : e.src, e.sn,
-                              kXSelinv, U + uptr_h_[e.sn], e.count});
+                              kXSelinv, U + uptrs_h_[e.sn], e.count});
   selinv_plan_ = true;
 }
 
@@ -1136,7 +1278,7 @@ void DeviceFactor::selinv(double* diag_out, bool on_device) {
   if (!selinv_plan_) build_selinv_plan();
   const Symbolic& s = *sym_;
   launches_selinv_ = 0;
-  const SymDev sd = symdev();
+  const SymDev sd = symdev_sel();
   for (int l = static_cast<int>(slev_.size()) - 1; l >= 0; --l) {
     const SLevel& e = slev_[l];
     KernelProfiler& pf = *prof_;

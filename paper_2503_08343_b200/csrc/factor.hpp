@@ -141,6 +141,8 @@ class DeviceFactor {
   template <int NR>
   void launch_solve_levels(bool fwd, bool bwd, double* y, int nr);
   SymDev symdev() const;
+  SymDev symdev_sel() const;  // same, with the selected inversion's U offsets
+  void plan_update_storage();
   bool mine(int k) const { return !part_ || owner_[k] == rank_; }
   void exchange(const std::vector<XferMsg>& m);
   void enqueue_levels(cudaStream_t sa, cudaStream_t sb, bool la, bool in_graph);
@@ -156,6 +158,9 @@ class DeviceFactor {
   void* xctx_ = nullptr;
   std::vector<XEdge> sched_;              // this rank's cross-edge messages
   std::vector<i64> lptr_h_, uptr_h_, uvptr_h_;  // this rank's storage offsets
+  std::vector<i64> uptrs_h_;                    // U offsets during the selected inversion
+  i64 u_arena_ = 0, u_arena_f_ = 0, u_arena_s_ = 0;
+  bool u_static_ = false;                       // GMRF_U_STATIC=1: Σ r² layout (A/B)
   std::vector<std::vector<XferMsg>> fx_;  // factor messages after each chunk level
   std::vector<std::vector<XferMsg>> sx_;  // selinv messages after each chunk level
   struct BxPoint {
@@ -173,7 +178,7 @@ class DeviceFactor {
   bool factored_ = false, selinv_done_ = false;
 
   DevBuf<int32_t> first_, rows_, relmap_, chptr_, chlist_, perm_, col2sn_, snparent_, status_;
-  DevBuf<int64_t> rptr_, lptr_, uptr_, qmap_, pptr_, uvptr_;
+  DevBuf<int64_t> rptr_, lptr_, uptr_, uptrs_, qmap_, pptr_, uvptr_;
   DevBuf<double> L_, U_, Sig_, q_, P_, Uv_, v1_, v2_, diag_, rdiag_;
   DevBuf<SolveTile> tiles_;
   DevBuf<double> pf_;       // forward column-block partials (solve.cuh)
