@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdio>
 #include <map>
 #include <cstdlib>
 #include <string>
@@ -274,6 +275,18 @@ DeviceFactor::DeviceFactor(std::shared_ptr<const Symbolic> sym, cudaStream_t str
     xb_.alloc(std::max<int64_t>(off * kMaxRhs, 1));
   }
   build_factor_plan();
+  if (std::getenv("GMRF_VERBOSE"))
+    std::fprintf(stderr,
+                 "[gmrf] factor storage GB: L %.2f, U arena %.2f (factor %.2f, selinv %.2f, "
+                 "static %.2f), GEMM tasks %.2f, EA %.2f, solve ws/tiles %.2f\n",
+                 L_.n * 8e-9, u_arena_ * 8e-9, u_arena_f_ * 8e-9, u_arena_s_ * 8e-9,
+                 [&] {
+                   double t = 0;
+                   for (int k = 0; k < s.ns; ++k) t += double(s.r(k)) * s.r(k);
+                   return t * 8e-9;
+                 }(),
+                 gemm_.n * sizeof(GemmTask) * 1e-9, (ea_.n * sizeof(EaTask) + eap_.n * 8) * 1e-9,
+                 (tiles_.n * sizeof(SolveTile)) * 1e-9);
   {  // lookahead streams: the critical chain at high priority, the bulk updates low
     int lo = 0, hi = 0;
     cuda_check(cudaDeviceGetStreamPriorityRange(&lo, &hi), "priorities");
@@ -482,13 +495,20 @@ void DeviceFactor::build_factor_plan() {
   double* L = L_.p;
   double* U = U_.p;
   std::vector<int64_t> gpan(3 * static_cast<size_t>(nlev), 0);  // panel tasks of all ranks
+  std::vector<int64_t> ggm(nlev, 0), ggr(nlev, 0);                // GEMM tiles of all ranks
   for (int k = 0; k < s.ns; ++k) {
-    const int w = s.w(k), rows = s.rows(k);
+    const int w = s.w(k), rows = s.rows(k), r = rows - w;
     if (rows <= kSmallRows) continue;
-    for (int c = 0; c < nchunks(w); ++c) {
+    const int nch = nchunks(w);
+    for (int c = 0; c < nch; ++c) {
       const int c0 = c * kNB, wk = std::min(kNB, w - c0), nbelow = rows - c0 - wk;
-      gpan[3 * (lvl0[k] + c) + (wk <= 16 ? 0 : (wk <= 32 ? 1 : 2))] +=
+      const int lv = lvl0[k] + c;
+      gpan[3 * lv + (wk <= 16 ? 0 : (wk <= 32 ? 1 : 2))] +=
           std::max(1, (nbelow + kTrsmRows - 1) / kTrsmRows);
+      for (int jb = c0 + wk; jb < w; jb += kTile)
+        (jb == c0 + wk ? ggm : ggr)[lv] += (rows - jb + kTile - 1) / kTile;
+      if (c == nch - 1)
+        for (int jb = 0; jb < r; jb += kTile) ggr[lv] += (r - jb + kTile - 1) / kTile;
     }
   }
   for (int k = 0; k < s.ns; ++k) {
@@ -611,8 +631,8 @@ void DeviceFactor::build_factor_plan() {
   std::vector<int32_t> smf;
   int64_t maxp = 1, maxr = 1;
   for (int l = 0; l < nlev; ++l) {
-    maxp = std::max(maxp, split_k_parts(gm[l]));
-    maxr = std::max(maxr, split_k_parts(gr[l]));
+    maxp = std::max(maxp, split_k_parts(gm[l], ggm[l]));
+    maxr = std::max(maxr, split_k_parts(gr[l], ggr[l]));
   }
   // one level's split-K partial tiles at a time, per stream
   parts_.alloc(maxp * kTile * kTile);
@@ -627,7 +647,7 @@ void DeviceFactor::build_factor_plan() {
     {
       std::vector<GemmTask> gs;
       std::vector<ReduceTask> rs;
-      split_k_level(gm[l], gs, rs, parts_.p);
+      split_k_level(gm[l], gs, rs, parts_.p, ggm[l]);
       flev_[l].gm0 = static_cast<int64_t>(gmf.size());
       flev_[l].gmn = static_cast<int64_t>(gs.size());
       gmf.insert(gmf.end(), gs.begin(), gs.end());
@@ -636,7 +656,7 @@ void DeviceFactor::build_factor_plan() {
       rdf.insert(rdf.end(), rs.begin(), rs.end());
       gs.clear();
       rs.clear();
-      split_k_level(gr[l], gs, rs, rparts_.p);
+      split_k_level(gr[l], gs, rs, rparts_.p, ggr[l]);
       flev_[l].gr0 = static_cast<int64_t>(gmf.size());
       flev_[l].grn = static_cast<int64_t>(gs.size());
       gmf.insert(gmf.end(), gs.begin(), gs.end());
@@ -789,13 +809,22 @@ void DeviceFactor::build_selinv_plan() {
       for (int t = 0; t * 64 < p; ++t) mi[lv].push_back({Lk, Sk, rows, c0, wk, w, t, rdc});
     }
   }
+  std::vector<int64_t> gyt(nlev, 0), gzt(nlev, 0);  // Y / Z tiles of all ranks per level
+  for (int k = 0; k < s.ns; ++k) {
+    const int w = s.w(k), rows = s.rows(k);
+    for (int c = 0; c < nchunks(w); ++c) {
+      const int c0 = c * kNB, wk = std::min(kNB, w - c0);
+      gyt[lvl0[k] + c] += (w - c0 - wk + kTile - 1) / kTile + (rows - w + kTile - 1) / kTile;
+      gzt[lvl0[k] + c] += 1;
+    }
+  }
   std::vector<ColTask> gaf;
   std::vector<GemmTask> gmf;
   std::vector<SelChunk> trf, dgf, mif;
   std::vector<ReduceTask> rdf;
   int64_t maxp = 1;
   for (int l = 0; l < nlev; ++l)
-    maxp = std::max(maxp, std::max(split_k_parts(yg[l]), split_k_parts(zg[l])));
+    maxp = std::max(maxp, std::max(split_k_parts(yg[l], gyt[l]), split_k_parts(zg[l], gzt[l])));
   sparts_.alloc(maxp * kTile * kTile);
   slev_.assign(nlev, {});
   for (int l = 0; l < nlev; ++l) {
@@ -808,7 +837,7 @@ void DeviceFactor::build_selinv_plan() {
     gaf.insert(gaf.end(), gg[l].begin(), gg[l].end());
     std::vector<GemmTask> gs;
     std::vector<ReduceTask> rs;
-    split_k_level(yg[l], gs, rs, sparts_.p);
+    split_k_level(yg[l], gs, rs, sparts_.p, gyt[l]);
     e.y0 = gmf.size();
     e.yn = gs.size();
     gmf.insert(gmf.end(), gs.begin(), gs.end());
@@ -817,7 +846,7 @@ void DeviceFactor::build_selinv_plan() {
     rdf.insert(rdf.end(), rs.begin(), rs.end());
     gs.clear();
     rs.clear();
-    split_k_level(zg[l], gs, rs, sparts_.p);
+    split_k_level(zg[l], gs, rs, sparts_.p, gzt[l]);
     e.z0 = gmf.size();
     e.zn = gs.size();
     gmf.insert(gmf.end(), gs.begin(), gs.end());

@@ -2,6 +2,7 @@
 #include "spacetime.hpp"
 
 #include <algorithm>
+#include <cstdio>
 #include <chrono>
 #include <cmath>
 #include <string>
@@ -602,8 +603,20 @@ void SpaceTimePosterior::assemble_device() {
       if (!sl[d]) kept.push_back(d);
     kept_.upload(kept, stream_);
   }
+  if (std::getenv("GMRF_VERBOSE"))
+    std::fprintf(stderr, "[gmrf] spacetime n %d pattern nnz %zu, JtJ pairs %zu (%.2f GB), nnz(L) %lld\n",
+                 n_, pri_.size(), jt_pairs_.size(), jt_pairs_.size() * 8e-9,
+                 static_cast<long long>(sym_->nnz_l_padded));
   fac_ = std::make_unique<DeviceFactor>(sym_, stream_, pspec_.nranks > 1 ? &pspec_ : nullptr);
+  auto mem = [&](const char* what) {
+    if (!std::getenv("GMRF_VERBOSE")) return;
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    std::fprintf(stderr, "[gmrf] after %s: device free %.1f of %.1f GB\n", what, fr * 1e-9, tot * 1e-9);
+  };
+  mem("factor storage");
   fac_->prepare_selinv();
+  mem("selected-inversion storage");
   fac_->set_profiler(&prof_);
   for (DevBuf<double>* v : {&mean_cond_, &mean_, &var_, &x_, &c_, &g_, &d_, &cand_, &r1_, &u0_})
     v->alloc(std::max(n_, 1));
