@@ -14,6 +14,7 @@
 #include "rng.hpp"
 #include "small_front.cuh"
 #include "solve.cuh"
+#include "solve_small.cuh"
 #include "selinv.cuh"
 #include "solve_wide.cuh"
 #include "splitk.cuh"
@@ -107,6 +108,7 @@ DeviceFactor::DeviceFactor(std::shared_ptr<const Symbolic> sym, cudaStream_t str
   for (int k = 0; k < s.ns; ++k)
     lptr_h_[k + 1] = lptr_h_[k] + (mine(k) ? static_cast<i64>(s.rows(k)) * s.w(k) : 0);
   if (const char* e = std::getenv("GMRF_U_STATIC")) u_static_ = e[0] != '0';
+  if (const char* e = std::getenv("GMRF_DEFER")) defer_ = std::max(1, atoi(e));
   plan_update_storage();
   std::vector<i64> qm;
   if (part_) {  // Q entries of other ranks' supernodes are not stored here
@@ -167,6 +169,7 @@ DeviceFactor::DeviceFactor(std::shared_ptr<const Symbolic> sym, cudaStream_t str
   const int64_t wide_cap = static_cast<int64_t>(nsm) * std::max(occ, 0);
   auto is_wide = [&](int k) { return s.w(k) > kWideW && nchunks(s.w(k)) <= wide_cap; };
   lvl_nrm_.assign(s.n_levels, 0);
+  lvl_nsm_.assign(s.n_levels, 0);
   wl_ptr_.assign(s.n_levels + 1, 0);
   wgroups_.clear();
   {
@@ -176,6 +179,11 @@ DeviceFactor::DeviceFactor(std::shared_ptr<const Symbolic> sym, cudaStream_t str
       auto b = lsn.begin() + lvl_ptr_[l], e = lsn.begin() + lvl_ptr_[l + 1];
       auto mid = std::stable_partition(b, e, [&](int32_t k) { return !is_wide(k); });
       lvl_nrm_[l] = mid - b;
+      // small supernodes first: one warp each in the 1- and 4-RHS solves (solve_small.cuh)
+      auto sm_end = std::stable_partition(b, mid, [&](int32_t k) {
+        return s.w(k) <= kSmallSolveW && s.rows(k) <= kSmallSolveRows;
+      });
+      lvl_nsm_[l] = sm_end - b;
       for (auto it = mid; it != e; ++it) {
         const int k = *it, nb = nchunks(s.w(k));
         if (wgroups_.size() == static_cast<size_t>(wl_ptr_[l]) ||
@@ -475,6 +483,27 @@ int64_t DeviceFactor::device_bytes() const {
          static_cast<int64_t>(gemm_.n * sizeof(GemmTask) + sgemm_.n * sizeof(GemmTask));
 }
 
+// Trailing updates of chunk c of a w-wide supernode (chunks of kNB columns),
+// with deferral depth D = defer_: chunk f is a flush point when (f+1) % D == 0;
+// a flush updates the blocks b >= f+1+D with the D chunks of its group in one
+// K = D·kNB GEMM (off the chain, D levels of slack before anything touches
+// those blocks), and the chain's next-block GEMM updates block c+1 with every
+// chunk not yet applied to it: (last flush f <= c-D, c]. D = 1 is plain
+// right-looking (next block with chunk c; rest with chunk c).
+//   emit(crit, j0, j1, k0, k1): columns [j0, j1) -= L[:, k0:k1] L[j0:j1, k0:k1]ᵀ
+template <class F>
+void DeviceFactor::trailing_jobs(int w, int c, F&& emit) const {
+  const int D = defer_, nch = nchunks(w);
+  auto last_flush_le = [D](int x) { return x < -1 ? -1 : ((x + 1) / D) * D - 1; };
+  const int c1 = std::min(w, (c + 1) * kNB);
+  if (c + 1 < nch) {
+    const int fb = last_flush_le(c - D);
+    emit(true, c1, std::min(w, c1 + kNB), (fb + 1) * kNB, c1);
+  }
+  if ((c + 1) % D == 0 && c + 1 + D < nch)
+    emit(false, (c + 1 + D) * kNB, w, (c + 1 - D) * kNB, c1);
+}
+
 void DeviceFactor::build_factor_plan() {
   const Symbolic& s = *sym_;
   std::vector<int> lvl0, last;
@@ -504,9 +533,10 @@ void DeviceFactor::build_factor_plan() {
       const int c0 = c * kNB, wk = std::min(kNB, w - c0), nbelow = rows - c0 - wk;
       const int lv = lvl0[k] + c;
       gpan[3 * lv + (wk <= 16 ? 0 : (wk <= 32 ? 1 : 2))] +=
-          std::max(1, (nbelow + kTrsmRows - 1) / kTrsmRows);
-      for (int jb = c0 + wk; jb < w; jb += kTile)
-        (jb == c0 + wk ? ggm : ggr)[lv] += (rows - jb + kTile - 1) / kTile;
+          std::max(1, (nbelow + kRowsSR - 1) / kRowsSR);
+      trailing_jobs(w, c, [&](bool crit, int j0, int j1, int, int) {
+        for (int jb = j0; jb < j1; jb += kTile) (crit ? ggm : ggr)[lv] += (rows - jb + kTile - 1) / kTile;
+      });
       if (c == nch - 1)
         for (int jb = 0; jb < r; jb += kTile) ggr[lv] += (r - jb + kTile - 1) / kTile;
     }
@@ -572,35 +602,34 @@ void DeviceFactor::build_factor_plan() {
           ptr2[lv].push_back(tt);
         }
       }
-      for (int t = 0; t == 0 || t * kTrsmRows < nbelow; ++t) {
+      for (int t = 0; t == 0 || t * kRowsSR < nbelow; ++t) {
         PanelTask tt = pt;
         tt.tile = t;
         pan[lv].push_back(tt);
       }
-      // right-looking update of the trailing panel columns with this chunk
-      for (int jb = c0 + wk; jb < w; jb += kTile)
-        for (int ib = jb; ib < rows; ib += kTile) {
-          GemmTask g{};
-          g.c = Lk + ib + static_cast<int64_t>(jb) * rows;
-          g.ldc = rows;
-          g.m = std::min(kTile, rows - ib);
-          g.n = std::min(kTile, w - jb);
-          g.a[0] = Lk + ib + static_cast<int64_t>(c0) * rows;
-          g.lda[0] = rows;
-          g.b[0] = Lk + jb + static_cast<int64_t>(c0) * rows;
-          g.ldb[0] = rows;
-          g.k[0] = wk;
-          g.flags = 2;  // B transposed
-          g.alpha = -1.0;
-          g.beta = 1.0;
-          if (jb == c0 + wk) {
-            gm[lv].push_back(g);
-            gm_f[lv] += tile_flops(g, ib == jb);
-          } else {
-            gr[lv].push_back(g);
-            gr_f[lv] += tile_flops(g, ib == jb);
+      // right-looking update of the trailing panel columns [j0, j1) with the
+      // finished columns [k0, k1) (trailing_jobs: next block on the chain,
+      // deferred bulk updates of the blocks further right)
+      trailing_jobs(w, c, [&](bool crit, int j0, int j1, int k0, int k1) {
+        for (int jb = j0; jb < j1; jb += kTile)
+          for (int ib = jb; ib < rows; ib += kTile) {
+            GemmTask g{};
+            g.c = Lk + ib + static_cast<int64_t>(jb) * rows;
+            g.ldc = rows;
+            g.m = std::min(kTile, rows - ib);
+            g.n = std::min(kTile, w - jb);
+            g.a[0] = Lk + ib + static_cast<int64_t>(k0) * rows;
+            g.lda[0] = rows;
+            g.b[0] = Lk + jb + static_cast<int64_t>(k0) * rows;
+            g.ldb[0] = rows;
+            g.k[0] = k1 - k0;
+            g.flags = 2;  // B transposed
+            g.alpha = -1.0;
+            g.beta = 1.0;
+            (crit ? gm : gr)[lv].push_back(g);
+            (crit ? gm_f : gr_f)[lv] += tile_flops(g, ib == jb);
           }
-        }
+      });
       // last chunk: full-width SYRK into the update matrix, U -= L21 L21ᵀ
       if (c == nch - 1 && r > 0)
         for (int jb = 0; jb < r; jb += kTile)
@@ -967,6 +996,7 @@ int32_t DeviceFactor::factor_panels() {
 void DeviceFactor::enqueue_levels(cudaStream_t sa, cudaStream_t sb, bool la, bool in_graph) {
   const SymDev sd = symdev();
   KernelProfiler& pf = *prof_;
+  static const int whatif = std::getenv("GMRF_WHATIF") ? atoi(std::getenv("GMRF_WHATIF")) : 0;
   if (la && !in_graph) {
     cuda_check(cudaEventRecord(ev_fork_, stream_), "record");
     cuda_check(cudaStreamWaitEvent(sa, ev_fork_, 0), "wait");
@@ -998,7 +1028,7 @@ void DeviceFactor::enqueue_levels(cudaStream_t sa, cudaStream_t sb, bool la, boo
       });
       launches_numeric_ += (lv.smn[0] > 0) + (lv.smn[1] > 0) + (lv.smn[2] > 0);
     }
-    if (lv.ean) {
+    if (lv.ean && !(whatif & 8)) {
       int blocks = static_cast<int>((lv.ean * 32 + 255) / 256);
       pf.run(sa, pf.tag("factor.extend_add", lvl), 0.0, lv.ea_bytes, [&] {
         k_extend_add<<<blocks, 256, 0, sa>>>(ea_.p + lv.ea0, static_cast<int>(lv.ean), eap_.p, sd,
@@ -1009,7 +1039,7 @@ void DeviceFactor::enqueue_levels(cudaStream_t sa, cudaStream_t sb, bool la, boo
     // one-wave levels (the chain at the top of the tree) keep the fused row
     // sweep: one launch, no staging round trip; multi-wave levels split
     const bool two_phase = panel2_ && !(lv.prow[0] && lv.prow[1] && lv.prow[2]);
-    if (lv.pann && two_phase) {
+    if (lv.pann && two_phase && !(whatif & 2)) {
       // two-phase panel: diagonal blocks once per chunk, then barrier-free
       // row-per-thread TRSM slabs (panel2.cuh)
       pf.run(sa, pf.tag("factor.potrf_trsm", lvl), lv.po_flops + lv.tr_flops, 0.0, [&] {
@@ -1033,7 +1063,7 @@ void DeviceFactor::enqueue_levels(cudaStream_t sa, cudaStream_t sb, bool la, boo
               pt_.p + lv.pt0[2], stage_.p);
       });
       for (int bk = 0; bk < 3; ++bk) launches_numeric_ += (lv.pdn[bk] > 0) + (lv.ptn[bk] > 0);
-    } else if (lv.pann) {
+    } else if (lv.pann && !(whatif & 2)) {
       // latency-bound levels (one wave) use the row-per-thread sweep; levels
       // with several waves of chunk slabs keep the blocked smem kernel, whose
       // CTAs are small enough to co-reside 4-5 per SM
@@ -1041,7 +1071,7 @@ void DeviceFactor::enqueue_levels(cudaStream_t sa, cudaStream_t sb, bool la, boo
         if (lv.pbn[0]) {
           const unsigned g = static_cast<unsigned>(lv.pbn[0]);
           if (lv.prow[0])
-            k_panel_rows<16, kTrsmRows><<<g, panel_rows_threads<16, kTrsmRows>(), 0, sa>>>(
+            k_panel_rows<16, kRowsSR><<<g, panel_rows_threads<16, kRowsSR>(), 0, sa>>>(
                 pan_.p + lv.pb0[0], status_.p, diag_.p);
           else
             k_potrf_trsm<16><<<g, 128, panel_smem_bytes<16>(), sa>>>(pan_.p + lv.pb0[0],
@@ -1050,7 +1080,7 @@ void DeviceFactor::enqueue_levels(cudaStream_t sa, cudaStream_t sb, bool la, boo
         if (lv.pbn[1]) {
           const unsigned g = static_cast<unsigned>(lv.pbn[1]);
           if (lv.prow[1])
-            k_panel_rows<32, kTrsmRows><<<g, panel_rows_threads<32, kTrsmRows>(), 0, sa>>>(
+            k_panel_rows<32, kRowsSR><<<g, panel_rows_threads<32, kRowsSR>(), 0, sa>>>(
                 pan_.p + lv.pb0[1], status_.p, diag_.p);
           else
             k_potrf_trsm<32><<<g, 128, panel_smem_bytes<32>(), sa>>>(pan_.p + lv.pb0[1],
@@ -1059,7 +1089,7 @@ void DeviceFactor::enqueue_levels(cudaStream_t sa, cudaStream_t sb, bool la, boo
         if (lv.pbn[2]) {
           const unsigned g = static_cast<unsigned>(lv.pbn[2]);
           if (lv.prow[2])
-            k_panel_rows<64, kTrsmRows><<<g, panel_rows_threads<64, kTrsmRows>(), 0, sa>>>(
+            k_panel_rows<64, kRowsSR><<<g, panel_rows_threads<64, kRowsSR>(), 0, sa>>>(
                 pan_.p + lv.pb0[2], status_.p, diag_.p);
           else
             k_potrf_trsm<64><<<g, 128, panel_smem_bytes<64>(), sa>>>(pan_.p + lv.pb0[2],
@@ -1069,8 +1099,10 @@ void DeviceFactor::enqueue_levels(cudaStream_t sa, cudaStream_t sb, bool la, boo
       launches_numeric_ += (lv.pbn[0] > 0) + (lv.pbn[1] > 0) + (lv.pbn[2] > 0);
     }
     if (la) cuda_check(cudaEventRecord(ev_panel_[li], sa), "record");
-    if (la && li > 0) cuda_check(cudaStreamWaitEvent(sa, ev_rest_[li - 1], 0), "wait");
-    if (lv.gmn) {
+    // next(l) writes block c+1, last written off the chain by the flush D levels back
+    if (la && li >= static_cast<size_t>(defer_))
+      cuda_check(cudaStreamWaitEvent(sa, ev_rest_[li - defer_], 0), "wait");
+    if (lv.gmn && !(whatif & 4)) {
       pf.run(sa, pf.tag("factor.gemm_dmma", lvl), lv.gm_flops, 0.0, [&] {
         launch_gemm(gemm_.p + lv.gm0, lv.gmn, sa);
         if (lv.rdn)
@@ -1080,7 +1112,7 @@ void DeviceFactor::enqueue_levels(cudaStream_t sa, cudaStream_t sb, bool la, boo
       launches_numeric_ += 1 + (lv.rdn > 0);
     }
     if (la) cuda_check(cudaStreamWaitEvent(sb, ev_panel_[li], 0), "wait");
-    if (lv.grn) {
+    if (lv.grn && !(whatif & 1)) {
       pf.run(sb, pf.tag("factor.gemm_dmma", lvl), lv.gr_flops, 0.0, [&] {
         launch_gemm(gemm_.p + lv.gr0, lv.grn, sb);
         if (lv.rrn)
@@ -1187,10 +1219,17 @@ void DeviceFactor::launch_solve_levels(bool fwd, bool bwd, double* y, int nr) {
       const int nrm = static_cast<int>(lvl_nrm_[l]);
       const int nw = static_cast<int>(lvl_ptr_[l + 1] - lvl_ptr_[l]) - nrm;
       const int nt = static_cast<int>(tile_ptr_[l + 1] - tile_ptr_[l]);
+      const int nsm = NR <= 4 ? static_cast<int>(lvl_nsm_[l]) : 0;
       pf.run(st, pf.tag("solve.forward", l), 0.0, lvl_bytes_[l], [&] {
-        if (nrm) {
-          k_fsolve_diag<NR><<<nrm, 256, smem_diag, st>>>(lvl_sn + lvl_ptr_[l], sd, L, y, nr, Uv_.p,
-                                                         uvptr_.p, rdiag);
+        if constexpr (NR <= 4) if (nsm) {
+          k_fsolve_small<NR><<<(nsm + kSmallSolveWarps - 1) / kSmallSolveWarps, 32 * kSmallSolveWarps,
+                               0, st>>>(lvl_sn + lvl_ptr_[l], nsm, sd, L, y, nr, Uv_.p, uvptr_.p,
+                                        rdiag);
+          ++launches;
+        }
+        if (nrm > nsm) {
+          k_fsolve_diag<NR><<<nrm - nsm, 256, smem_diag, st>>>(lvl_sn + lvl_ptr_[l] + nsm, sd, L, y,
+                                                               nr, Uv_.p, uvptr_.p, rdiag);
           ++launches;
         }
         if (nw) {
@@ -1222,10 +1261,16 @@ void DeviceFactor::launch_solve_levels(bool fwd, bool bwd, double* y, int nr) {
           k_bsolve_off<NR><<<nt, 256, 0, st>>>(tiles_.p + tile_ptr_[l], sd, L, y, nr, P_.p, pptr_.p);
           ++launches;
         });
+      const int nsm = NR <= 4 ? static_cast<int>(lvl_nsm_[l]) : 0;
       pf.run(st, pf.tag("solve.backward", l), 0.0, lvl_bytes_[l], [&] {
-        if (nrm) {
-          k_bsolve_diag<NR><<<nrm, 256, smem_diag, st>>>(lvl_sn + lvl_ptr_[l], sd, L, y, nr, P_.p,
-                                                         pptr_.p, rdiag);
+        if constexpr (NR <= 4) if (nsm) {
+          k_bsolve_small<NR><<<(nsm + kSmallSolveWarps - 1) / kSmallSolveWarps, 32 * kSmallSolveWarps,
+                               0, st>>>(lvl_sn + lvl_ptr_[l], nsm, sd, L, y, nr, rdiag);
+          ++launches;
+        }
+        if (nrm > nsm) {
+          k_bsolve_diag<NR><<<nrm - nsm, 256, smem_diag, st>>>(lvl_sn + lvl_ptr_[l] + nsm, sd, L, y,
+                                                               nr, P_.p, pptr_.p, rdiag);
           ++launches;
         }
         for (int64_t g = wl_ptr_[l]; g < wl_ptr_[l + 1]; ++g) {

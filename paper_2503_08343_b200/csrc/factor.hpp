@@ -224,6 +224,10 @@ class DeviceFactor {
   cudaEvent_t ev_fork_ = nullptr;
   std::vector<cudaEvent_t> ev_panel_, ev_rest_;
   bool lookahead_ = true;
+  int defer_ = 1;
+  bool gemm_cap_ = true;  // cap bulk GEMM residency on one-wave levels (launch_gemm)  // trailing-update deferral depth (chunks per flush), trailing_jobs
+  template <class F>
+  void trailing_jobs(int w, int c, F&& emit) const;
   bool use_graph_ = true;             // GMRF_NO_GRAPH=1 disables (A/B)
   bool panel2_ = true;                // GMRF_PANEL1=1: fused one-phase panel kernels (A/B)
   DevBuf<PanelTask> pd_, pt_;         // two-phase panel tasks
@@ -250,7 +254,7 @@ class DeviceFactor {
   };
 
  private:
-  std::vector<int64_t> lvl_nrm_, wl_ptr_;
+  std::vector<int64_t> lvl_nrm_, lvl_nsm_, wl_ptr_;
   std::vector<WideGroup> wgroups_;
   DevBuf<WideBlock> wfwd_, wbwd_;
   DevBuf<int32_t> wflags_;

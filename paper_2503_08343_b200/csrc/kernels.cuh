@@ -8,6 +8,7 @@ namespace gmrf {
 constexpr int kNB = 64;        // supernode chunk width (columns per dense panel step)
 constexpr int kTile = 64;      // GEMM output tile (kTile x kTile)
 constexpr int kTrsmRows = 128; // rows per TRSM task
+constexpr int kRowsSR = 64;    // slab rows per k_panel_rows CTA (one-wave levels)
 constexpr int kSmallRows = 96; // fronts with at most this many rows use k_small_front
 
 // C = beta*C + alpha * Σ_seg opA(A_seg) · opB(B_seg), all column-major.

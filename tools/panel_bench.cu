@@ -51,7 +51,9 @@ int main(int argc, char** argv) {
       else
       {
         const unsigned g = static_cast<unsigned>(tasks_r.size());
-        if (sr == 64)
+        if (sr == 32)
+          k_panel_rows<64, 32><<<g, nbelow == 0 ? 64 : panel_rows_threads<64, 32>()>>>(dtr, status, diag);
+        else if (sr == 64)
           k_panel_rows<64, 64><<<g, nbelow == 0 ? 64 : panel_rows_threads<64, 64>()>>>(dtr, status, diag);
         else
           k_panel_rows<64, 128><<<g, nbelow == 0 ? 64 : panel_rows_threads<64, 128>()>>>(dtr, status, diag);
