@@ -39,6 +39,15 @@ void set_smem_attrs() {
   cuda_check(cudaFuncSetAttribute(k_small_front<96>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   small_front_smem_bytes<96>()),
              "smem k_small_front");
+  cuda_check(cudaFuncSetAttribute(k_small_front_rows<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  small_front_smem_bytes<96>()),
+             "smem k_small_front_rows");
+  cuda_check(cudaFuncSetAttribute(k_small_front_rows<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  small_front_smem_bytes<96>()),
+             "smem k_small_front_rows");
+  cuda_check(cudaFuncSetAttribute(k_small_front_rows<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  small_front_smem_bytes<96>()),
+             "smem k_small_front_rows");
   cuda_check(cudaFuncSetAttribute(k_sel_diag_w<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   sel_diag_smem_bytes<64>()),
              "smem k_sel_diag");
@@ -517,7 +526,9 @@ void DeviceFactor::build_factor_plan() {
   // the critical chain), gr = the rest of the trailing update + the U SYRK
   // (overlapped with the next level's panel on the second stream)
   std::vector<std::vector<GemmTask>> gm(nlev), gr(nlev);
-  std::vector<std::vector<int32_t>> sm[3];
+  // small-front buckets: rows ≤ 32 / ≤ 64 (k_small_front), rows ≤ 96 with
+  // w ≤ 16 / 32 / 64 (k_small_front_rows), rows ≤ 96 with w > 64 (k_small_front)
+  std::vector<std::vector<int32_t>> sm[kSmBuckets];
   for (auto& v : sm) v.resize(nlev);
   std::vector<double> ea_b(nlev, 0.0), po_f(nlev, 0.0), tr_f(nlev, 0.0), gm_f(nlev, 0.0),
       gr_f(nlev, 0.0), sm_f(nlev, 0.0);
@@ -546,7 +557,8 @@ void DeviceFactor::build_factor_plan() {
     const int w = s.w(k), rows = s.rows(k), r = rows - w;
     if (rows <= kSmallRows) {  // fused small-front kernel, bucketed by front size
       const int lv = lvl0[k];
-      sm[rows <= 32 ? 0 : (rows <= 64 ? 1 : 2)][lv].push_back(k);
+      sm[rows <= 32 ? 0 : (rows <= 64 ? 1 : (w <= 16 ? 2 : (w <= 32 ? 3 : (w <= 64 ? 4 : 5))))][lv]
+          .push_back(k);
       for (int j = 0; j < w; ++j) sm_f[lv] += static_cast<double>(rows - j) * (rows - j);
       continue;
     }
@@ -717,7 +729,7 @@ void DeviceFactor::build_factor_plan() {
         if ((pt.w <= 16 ? 0 : (pt.w <= 32 ? 1 : 2)) == bk) ptf.push_back(pt);
       flev_[l].ptn[bk] = static_cast<int64_t>(ptf.size()) - flev_[l].pt0[bk];
     }
-    for (int bk = 0; bk < 3; ++bk) {
+    for (int bk = 0; bk < kSmBuckets; ++bk) {
       flev_[l].sm0[bk] = static_cast<int64_t>(smf.size());
       flev_[l].smn[bk] = static_cast<int64_t>(sm[bk][l].size());
       smf.insert(smf.end(), sm[bk][l].begin(), sm[bk][l].end());
@@ -1009,24 +1021,37 @@ void DeviceFactor::enqueue_levels(cudaStream_t sa, cudaStream_t sb, bool la, boo
     // SYRKs, concurrently with the next level's panel. Ordering:
     //   rest(l)               after panel(l)           (reads the chunk's L)
     //   assembly(l)           after rest(l-1)          (children's U SYRKs)
-    //   next(l)               after rest(l-1)          (same tiles, k order)
+    //   next(l)               after rest(l-D)          (same tiles, k order; D = defer_)
     // Profiling runs keep one stream so every launch is attributed to its class.
-    const bool assembles = lv.ean > 0 || lv.smn[0] + lv.smn[1] + lv.smn[2] > 0;
+    int64_t nsmall = 0;
+    for (int bk = 0; bk < kSmBuckets; ++bk) nsmall += lv.smn[bk];
+    const bool assembles = lv.ean > 0 || nsmall > 0;
     if (la && li > 0 && assembles)
       cuda_check(cudaStreamWaitEvent(sa, ev_rest_[li - 1], 0), "wait");
-    if (lv.smn[0] + lv.smn[1] + lv.smn[2] > 0) {
+    if (nsmall > 0) {
       pf.run(sa, pf.tag("factor.small_front", lvl), lv.sm_flops, 0.0, [&] {
+        auto g = [&](int bk) { return static_cast<unsigned>(lv.smn[bk]); };
+        auto sn = [&](int bk) { return small_.p + lv.sm0[bk]; };
         if (lv.smn[0])
-          k_small_front<32><<<static_cast<unsigned>(lv.smn[0]), 256, small_front_smem_bytes<32>(),
-                              sa>>>(small_.p + lv.sm0[0], sd, L_.p, U_.p, status_.p, rdiag_.p);
+          k_small_front<32><<<g(0), 256, small_front_smem_bytes<32>(), sa>>>(sn(0), sd, L_.p, U_.p,
+                                                                           status_.p, rdiag_.p);
         if (lv.smn[1])
-          k_small_front<64><<<static_cast<unsigned>(lv.smn[1]), 256, small_front_smem_bytes<64>(),
-                              sa>>>(small_.p + lv.sm0[1], sd, L_.p, U_.p, status_.p, rdiag_.p);
+          k_small_front<64><<<g(1), 256, small_front_smem_bytes<64>(), sa>>>(sn(1), sd, L_.p, U_.p,
+                                                                           status_.p, rdiag_.p);
         if (lv.smn[2])
-          k_small_front<96><<<static_cast<unsigned>(lv.smn[2]), 256, small_front_smem_bytes<96>(),
-                              sa>>>(small_.p + lv.sm0[2], sd, L_.p, U_.p, status_.p, rdiag_.p);
+          k_small_front_rows<16><<<g(2), small_rows_threads<16>(), small_front_smem_bytes<96>(),
+                                   sa>>>(sn(2), sd, L_.p, U_.p, status_.p, rdiag_.p);
+        if (lv.smn[3])
+          k_small_front_rows<32><<<g(3), small_rows_threads<32>(), small_front_smem_bytes<96>(),
+                                   sa>>>(sn(3), sd, L_.p, U_.p, status_.p, rdiag_.p);
+        if (lv.smn[4])
+          k_small_front_rows<64><<<g(4), small_rows_threads<64>(), small_front_smem_bytes<96>(),
+                                   sa>>>(sn(4), sd, L_.p, U_.p, status_.p, rdiag_.p);
+        if (lv.smn[5])
+          k_small_front<96><<<g(5), 256, small_front_smem_bytes<96>(), sa>>>(sn(5), sd, L_.p, U_.p,
+                                                                           status_.p, rdiag_.p);
       });
-      launches_numeric_ += (lv.smn[0] > 0) + (lv.smn[1] > 0) + (lv.smn[2] > 0);
+      for (int bk = 0; bk < kSmBuckets; ++bk) launches_numeric_ += lv.smn[bk] > 0;
     }
     if (lv.ean && !(whatif & 8)) {
       int blocks = static_cast<int>((lv.ean * 32 + 255) / 256);

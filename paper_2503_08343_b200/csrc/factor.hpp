@@ -188,12 +188,13 @@ class DeviceFactor {
   int64_t uv_total_ = 0, p_total_ = 0;
   int ws_nrhs_ = 0;
 
+  static constexpr int kSmBuckets = 6;
   struct FLevel {
     int64_t ea0, ean, po0, pon, pan0, pann, gm0, gmn;
     double ea_bytes, po_flops, tr_flops, gm_flops;  // algorithmic work per launch
     int64_t pb0[3], pbn[3];  // panel tasks split by width bucket 16 / 32 / 64
     int64_t rd0, rdn;        // split-K reductions of the level's GEMM tiles
-    int64_t sm0[3], smn[3];  // small fronts (rows <= 32 / 64 / 96), one CTA each
+    int64_t sm0[kSmBuckets], smn[kSmBuckets];  // small fronts (build_factor_plan), one CTA each
     double sm_flops;
     int64_t gr0, grn, rr0, rrn;  // rest of the trailing update + U SYRK (second stream)
     double gr_flops;
