@@ -973,7 +973,10 @@ int32_t DeviceFactor::factor_panels() {
       enqueue_levels(main_, aux_, true, true);
       cudaGraph_t g = nullptr;
       cuda_check(cudaStreamEndCapture(main_, &g), "end capture");
-      cuda_check(cudaGraphInstantiate(&fgraph_, g, 0), "graph instantiate");
+      // per-node priorities (copied from the capturing streams): the chain runs
+      // ahead of the bulk updates, as it does with plain stream launches
+      cuda_check(cudaGraphInstantiate(&fgraph_, g, cudaGraphInstantiateFlagUseNodePriority),
+                 "graph instantiate");
       cuda_check(cudaGraphDestroy(g), "graph destroy");
       graph_launches_ = launches_numeric_ - l0;
       launches_numeric_ = l0;

@@ -8,12 +8,14 @@ from paper_2503_08343_b200.spacetime import SpaceTimePosterior, SpaceTimeSpec, G
 spec = SpaceTimeSpec.burgers()
 post = SpaceTimePosterior(spec, GaussNewtonConfig(max_iters=1))
 u0 = -np.sin(np.pi * spec.node_x())
-ts = []
+ts, sv = [], []
+var = len(sys.argv) > 1 and sys.argv[1] == "var"
 for rep in range(4):
     try:
-        post.run(u0, variances=False, copy_back=False)
+        post.run(u0, variances=var, copy_back=False)
     except Exception as e:  # noqa: BLE001
         pass
     i = post.info()
     ts.append(i.numeric_ms / max(1, i.n_factorizations))
-print("per-factorization ms", [round(t, 3) for t in ts])
+    sv.append(i.selinv_ms)
+print("per-factorization ms", [round(t, 3) for t in ts], "selinv ms", [round(t, 3) for t in sv])
