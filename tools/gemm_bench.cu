@@ -52,7 +52,9 @@ int main() {
             {"var_ref", k_gemm_var<2, 2, 16, false, 4, false, 0>, 128},
             {"nomul", k_gemm_var<2, 2, 16, false, 4, false, 3>, 128},
             {"nomul_nv", k_gemm_var<2, 2, 16, false, 4, true, 3>, 128},
-            {"nomul_w2x4", k_gemm_var<2, 4, 16, false, 3, true, 3>, 256}};
+            {"nomul_w2x4", k_gemm_var<2, 4, 16, false, 3, true, 3>, 256},
+            {"ld16", k_gemm_var<2, 2, 16, false, 4, false, 4>, 128}
+            };
   cudaFuncSetAttribute(k_gemm_ms<3, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm_ms_smem<3>());
   cudaFuncSetAttribute(k_gemm_ms<4, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm_ms_smem<4>());
   cudaFuncSetAttribute(k_gemm_ms<5, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm_ms_smem<5>());

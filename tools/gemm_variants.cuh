@@ -44,6 +44,29 @@ __device__ __forceinline__ void load_op_v(double (*dst)[kPad], const double* src
   }
 }
 
+// 16-byte cp.async for mm-contiguous operands (requires 16-B aligned columns:
+// even ld and even row offset); falls back to 8-byte copies otherwise
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+template <int NT, int KC>
+__device__ __forceinline__ void load_op16(double (*dst)[kPad], const double* src, int ld,
+                                          bool kcontig, int mn_lim, int k0, int k_lim, int tid) {
+  const bool al = !kcontig && ((reinterpret_cast<uintptr_t>(src) | (static_cast<uintptr_t>(ld) * 8)) & 15) == 0 &&
+                  mn_lim == 64 && k0 + KC <= k_lim;
+  if (!al) {
+    load_op_v<NT, KC>(dst, src, ld, kcontig, mn_lim, k0, k_lim, tid);
+    return;
+  }
+#pragma unroll
+  for (int it = 0; it < (KC * kTile) / (2 * NT); ++it) {
+    int idx = tid + it * NT;
+    int kk = idx >> 5, mm = (idx & 31) * 2;
+    cp_async16(&dst[kk][mm], src + mm + static_cast<int64_t>(k0 + kk) * ld);
+  }
+}
+
 template <int WM, int WN, int KC, bool M16, int MINB, bool NV = false, int MODE = 0>
 __global__ void __launch_bounds__(32 * WM * WN, MINB) k_gemm_var(const GemmTask* __restrict__ tasks) {
   constexpr int NT = 32 * WM * WN;
@@ -80,14 +103,24 @@ __global__ void __launch_bounds__(32 * WM * WN, MINB) k_gemm_var(const GemmTask*
     const bool a_kc = (t.flags >> (2 * seg)) & 1;
     const bool b_kc = !((t.flags >> (2 * seg + 1)) & 1);
     const int nk = (K + KC - 1) / KC;
-    load_op_v<NT, KC>(As[0], A, lda, a_kc, m, 0, K, tid);
-    load_op_v<NT, KC>(Bs[0], B, ldb, b_kc, n, 0, K, tid);
+    if constexpr (MODE == 4) {
+      load_op16<NT, KC>(As[0], A, lda, a_kc, m, 0, K, tid);
+      load_op16<NT, KC>(Bs[0], B, ldb, b_kc, n, 0, K, tid);
+    } else {
+      load_op_v<NT, KC>(As[0], A, lda, a_kc, m, 0, K, tid);
+      load_op_v<NT, KC>(Bs[0], B, ldb, b_kc, n, 0, K, tid);
+    }
     cp_async_commit();
     for (int kc = 0; kc < nk; ++kc) {
       const int buf = kc & 1;
       if (kc + 1 < nk) {
+        if constexpr (MODE == 4) {
+          load_op16<NT, KC>(As[buf ^ 1], A, lda, a_kc, m, (kc + 1) * KC, K, tid);
+          load_op16<NT, KC>(Bs[buf ^ 1], B, ldb, b_kc, n, (kc + 1) * KC, K, tid);
+        } else {
         load_op_v<NT, KC>(As[buf ^ 1], A, lda, a_kc, m, (kc + 1) * KC, K, tid);
         load_op_v<NT, KC>(Bs[buf ^ 1], B, ldb, b_kc, n, (kc + 1) * KC, K, tid);
+        }
         cp_async_commit();
         cp_async_wait<1>();
       } else {
