@@ -34,7 +34,9 @@ struct DevBuf {
     if (count == n && p) return;
     reset();
     if (count == 0) return;
-    cuda_check(cudaMalloc(&p, count * sizeof(T)), "cudaMalloc");
+    // + slack: 16-byte operand copies (load_operand) read whole 64-row tile columns,
+    // past the last row of a partial tile at the end of a buffer
+    cuda_check(cudaMalloc(&p, count * sizeof(T) + 1024), "cudaMalloc");
     n = count;
   }
   void upload(const std::vector<T>& v, cudaStream_t s) {

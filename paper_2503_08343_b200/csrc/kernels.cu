@@ -43,20 +43,43 @@ __device__ __forceinline__ void cp_async_wait() {
 constexpr int kKC = 16;
 constexpr int kPad = 72;  // smem row pitch (doubles): conflict-free fragment loads
 
+// 16-byte copy, zero-filled when !pred
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
+  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  int sz = pred ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+}
+
+// Parity (in doubles) of an operand column's start address: a column-major
+// panel with an odd leading dimension alternates between 16-byte-aligned and
+// 8-byte-offset columns.
+__device__ __forceinline__ int col_phase(const double* p) {
+  return static_cast<int>((reinterpret_cast<uintptr_t>(p) >> 3) & 1);
+}
+
 __device__ __forceinline__ void load_operand(double (*dst)[kPad], const double* src, int ld,
                                              bool kcontig, int mn_lim, int k0, int k_lim,
                                              int tid) {
-  // dst[kk][mm] = op(src)(mm, k0+kk)
   if (!kcontig) {
-    // element (mm, kk) at src[mm + kk*ld]: mm contiguous
+    // element (mm, kk) at src[mm + kk*ld]: mm contiguous. Column kk is copied in
+    // 16-byte chunks from its 16-byte-aligned start (one element early when the
+    // column starts 8 bytes into a chunk): dst[kk][mm + ph(kk)] = element (mm, kk),
+    // ph(kk) = the column's phase. Elements past mn_lim are copied too (they only
+    // reach output rows/columns that are never stored); columns past k_lim are zero.
+    // Allocations carry slack (DevBuf) for the last tile of a buffer.
+    constexpr int CH = kTile / 2 + 1;  // chunks per column
 #pragma unroll
-    for (int it = 0; it < (kKC * kTile) / 128; ++it) {
-      int idx = tid + it * 128;
-      int kk = idx >> 6, mm = idx & 63;
-      bool ok = mm < mn_lim && (k0 + kk) < k_lim;
-      const double* p = ok ? src + mm + static_cast<int64_t>(k0 + kk) * ld : src;
-      cp_async8(&dst[kk][mm], p, ok);
+    for (int it = 0; it < (kKC * CH + 127) / 128; ++it) {
+      const int idx = tid + it * 128;
+      if (idx < kKC * CH) {
+        const int kk = idx / CH, ch = idx - kk * CH;
+        const bool ok = (k0 + kk) < k_lim;
+        const double* col = src + static_cast<int64_t>(k0 + kk) * ld;
+        const double* p = ok ? col - col_phase(col) + 2 * ch : src - col_phase(src);
+        cp_async16(&dst[kk][2 * ch], p, ok);
+      }
     }
+    (void)mn_lim;
   } else {
     // element (mm, kk) at src[kk + mm*ld]: kk contiguous
 #pragma unroll
@@ -113,6 +136,10 @@ __global__ void __launch_bounds__(128, 4) k_gemm_tiles(const GemmTask* __restric
     const bool a_kc = (t.flags >> (2 * seg)) & 1;
     const bool b_kc = !((t.flags >> (2 * seg + 1)) & 1);
     const int nk = (K + kKC - 1) / kKC;
+    // smem column shift of an mm-contiguous operand (load_operand): the phase of
+    // column kk is ph0 ^ (kk & ld) — stage offsets k0 are even
+    const int pa0 = a_kc ? 0 : col_phase(A), la = a_kc ? 0 : (lda & 1);
+    const int pb0 = b_kc ? 0 : col_phase(B), lb = b_kc ? 0 : (ldb & 1);
     load_operand(As[0], A, lda, a_kc, m, 0, K, tid);
     load_operand(Bs[0], B, ldb, b_kc, n, 0, K, tid);
     cp_async_commit();
@@ -130,11 +157,13 @@ __global__ void __launch_bounds__(128, 4) k_gemm_tiles(const GemmTask* __restric
 #pragma unroll
       for (int kk = 0; kk < kKC; kk += 4) {
         double af[4], bf[4];
+        const int kr = kk + (lane & 3);
+        const int sa = pa0 ^ (kr & la), sb = pb0 ^ (kr & lb);
 #pragma unroll
         for (int i = 0; i < 4; ++i)
-          af[i] = alpha * As[buf][kk + (lane & 3)][wm * 32 + i * 8 + (lane >> 2)];
+          af[i] = alpha * As[buf][kr][wm * 32 + i * 8 + (lane >> 2) + sa];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) bf[j] = Bs[buf][kk + (lane & 3)][wn * 32 + j * 8 + (lane >> 2)];
+        for (int j = 0; j < 4; ++j) bf[j] = Bs[buf][kr][wn * 32 + j * 8 + (lane >> 2) + sb];
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
