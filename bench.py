@@ -351,10 +351,18 @@ def main():
     pinfo = post.info()
     step_kernel_ms = sum(v["ms"] for v in stats.values())
     dom_name, dom = max(stats.items(), key=lambda kv: kv[1]["ms"])
+    # DRAM traffic per launch of the dominant kernel class, from the committed ncu
+    # capture (profiles/r01_ncu_traffic.json, tools/ncu_traffic.py), when present
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")) as fh:
+            traffic = json.load(fh).get(dom_name, {}).get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        traffic = None
     if dom["flops"] > 0:
         achieved = dom["flops"] / (dom["ms"] * 1e-3) / 1e12
         roof = {"kernel": dom_name, "bound": "tensor", "achieved": achieved, "peak": peak_fp64,
-                "unit": "TFLOP/s", "frac": achieved / peak_fp64, "traffic": None,
+                "unit": "TFLOP/s", "frac": achieved / peak_fp64, "traffic": traffic,
                 "peak_source": "measured in-run: cuBLAS DGEMM 8192^3 (FP64 tensor cores)",
                 "share_of_step": dom["ms"] / step_kernel_ms,
                 "avg_launch_ms": dom["ms"] / max(dom["launches"], 1),
@@ -363,7 +371,7 @@ def main():
         hbm = peaks.get("hbm_gbs", 6650.0)
         achieved = dom["bytes"] / (dom["ms"] * 1e-3) / 1e9
         roof = {"kernel": dom_name, "bound": "hbm", "achieved": achieved, "peak": hbm,
-                "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
+                "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs",
                 "share_of_step": dom["ms"] / step_kernel_ms}
     numeric_ms = info.numeric_ms / max(info.n_factorizations, 1)

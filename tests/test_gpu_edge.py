@@ -161,3 +161,62 @@ def test_wide_supernodes_many_per_level(port):
     assert np.array_equal(x1, x2)
     xs = g.solve(f, b[:, 0])
     assert rel(m @ xs, b[:, 0]) <= 1e-10
+
+
+def _supernodes(sym):
+    import ctypes as C
+    from paper_2503_08343_b200 import _capi
+    ns = int(sym.info.n_supernodes)
+    first = np.zeros(ns + 1, np.int32)
+    rows = np.zeros(ns, np.int32)
+    p32 = lambda a: a.ctypes.data_as(C.POINTER(C.c_int32))  # noqa: E731
+    assert _capi.load().gmrf_symbolic_supernodes(sym._h, p32(first), p32(rows), None, None) == 0
+    return np.diff(first), rows
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_small_front_buckets_and_warp_solves(port, seed):
+    # dense leaf blocks of width w all coupled to one separator of size s: each
+    # leaf is one front with rows = w + s. (w, s) picks every small-front kernel
+    # (rows <= 32, <= 64, and 64 < rows <= 96 with w <= 16 / 32 / 64 / > 64) and
+    # the warp-per-supernode solves (w <= 64, rows <= 128)
+    rng = np.random.default_rng(seed)
+    shapes = [(10, 12), (20, 30), (12, 70), (24, 60), (48, 40), (70, 20), (40, 80)]
+    blocks, cols, n0 = [], [], 0
+    sep = 90
+    for w, s in shapes:
+        blocks.append((n0, w, s))
+        n0 += w
+    n = n0 + sep
+    m = np.zeros((n, n))
+    for b0, w, s in blocks:
+        a = rng.standard_normal((w, w))
+        m[b0:b0 + w, b0:b0 + w] = a @ a.T + w * np.eye(w)
+        c = rng.standard_normal((s, w)) * 0.1
+        m[n0:n0 + s, b0:b0 + w] = c
+        m[b0:b0 + w, n0:n0 + s] = c.T
+    d = rng.standard_normal((sep, sep))
+    m[n0:, n0:] += d @ d.T / sep + 40.0 * np.eye(sep)
+    q = csc(m)
+    f = g.cholesky_factor(q, np.arange(n))  # leaves first, separator last
+    widths, rows = _supernodes(f.sym)
+    got = {(int(w), int(r)) for w, r in zip(widths, rows)}
+    for w, s in shapes:
+        assert (w, w + s) in got, (w, s, sorted(got))
+    lcp, lri, lv, bad = port.cholesky(n, q.col_ptr, q.row_idx, q.values, f.perm)
+    assert bad < 0
+    assert rel(f.L.values, lv) <= 1e-12
+    b = rng.standard_normal((n, 6))
+    for mode in (0, 1, 2):
+        for k in (1, 4, 6):
+            x = g.solve_triangular(f, b[:, :k], mode)
+            xo = port.solve(n, lcp, lri, lv, f.perm, mode, b[:, :k])
+            assert rel(x, xo) <= 1e-12, (mode, k)
+    np.testing.assert_allclose(g.takahashi_diagonal(f), np.diag(np.linalg.inv(m)), rtol=1e-10)
+    # a non-positive pivot inside a row-sweep small front reports its original index
+    m2 = m.copy()
+    b0, w, s = blocks[4]  # (48, 40): k_small_front_rows<64>
+    m2[b0 + 30, b0 + 30] = -5.0
+    with pytest.raises(g.NotPositiveDefiniteError) as e:
+        g.cholesky_factor(csc(m2), np.arange(n))
+    assert e.value.index() == b0 + 30
