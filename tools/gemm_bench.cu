@@ -148,5 +148,50 @@ int main() {
     for (GemmTask& g : t2) g.k[0] = 256;
     run("syrk256_x4", t2, fl);
   }
+  {  // wide tiles 64x128 over the same syrk/update shapes (K = 64 / 256 / 1024)
+    auto wide = [&](const char* name, int K, int rmax, int reps) {
+      std::vector<GemmTask> t;
+      double fl = 0;
+      for (int rep = 0; rep < reps; ++rep)
+        for (int jb = 0; jb < rmax; jb += 128)
+          for (int ib = jb; ib < rmax; ib += 64) {
+            GemmTask g{};
+            g.c = C + ib + static_cast<int64_t>(jb) * 2048 + rep * 2048 * 2048;
+            g.ldc = 2048; g.m = 64; g.n = 128;
+            g.a[0] = A + ib; g.lda[0] = 2048;
+            g.b[0] = A + jb; g.ldb[0] = 2048;
+            g.k[0] = K; g.flags = 2; g.alpha = -1.0; g.beta = 1.0;
+            t.push_back(g);
+            fl += 2.0 * 64 * 128 * K;
+          }
+      GemmTask* dt;
+      cudaMalloc(&dt, t.size() * sizeof(GemmTask));
+      cudaMemcpy(dt, t.data(), t.size() * sizeof(GemmTask), cudaMemcpyHostToDevice);
+      cudaEvent_t e0, e1;
+      cudaEventCreate(&e0); cudaEventCreate(&e1);
+      auto timeit = [&](auto fn, int smem, const char* v) {
+        float best = 1e9f;
+        for (int r = 0; r < 8; ++r) {
+          cudaEventRecord(e0);
+          fn<<<static_cast<unsigned>(t.size()), 128, smem>>>(dt);
+          cudaEventRecord(e1); cudaEventSynchronize(e1);
+          float ms; cudaEventElapsedTime(&ms, e0, e1);
+          if (r > 0 && ms < best) best = ms;
+        }
+        printf("%-10s %-12s %6zu tiles  %8.1f us  %6.2f TF/s  (%s)\n", name, v, t.size(), best * 1e3,
+               fl / (best * 1e-3) / 1e12, cudaGetErrorString(cudaGetLastError()));
+      };
+      cudaFuncSetAttribute(k_gemm_big<128, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm_big_smem<128, 3>());
+      cudaFuncSetAttribute(k_gemm_big<128, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm_big_smem<128, 4>());
+      cudaFuncSetAttribute(k_gemm_big<128, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm_big_smem<128, 2>());
+      timeit(k_gemm_big<128, 2>, gemm_big_smem<128, 2>(), "w128_s2");
+      timeit(k_gemm_big<128, 3>, gemm_big_smem<128, 3>(), "w128_s3");
+      timeit(k_gemm_big<128, 4>, gemm_big_smem<128, 4>(), "w128_s4");
+      cudaFree(dt);
+    };
+    wide("wupd64", 64, 2048, 1);
+    wide("wsyrk256x4", 256, 1024, 4);
+    wide("wsyrk1kx4", 1024, 1024, 4);
+  }
   return 0;
 }

@@ -265,3 +265,96 @@ constexpr int gemm_ms_smem() {
   return 2 * NS * kKC * kPad * static_cast<int>(sizeof(double));
 }
 }  // namespace gmrf
+
+namespace gmrf {
+// Wide-tile variant: CTA tile 64 x TN (TN = 128), 4 warps 2x2 of 32 x TN/2, so a
+// warp issues 4 A + TN/16 B fragment loads per 4*TN/16... DMMAs (better DMMA:LDS
+// ratio than 32x32 warp tiles); NS-stage cp.async pipeline in dynamic shared
+// memory, 16-byte copies (operands 16-B aligned, mm contiguous: bench only).
+template <int TN, int NS>
+constexpr int gemm_big_smem() {
+  return NS * 16 * ((64 + 8) + (TN + 8)) * static_cast<int>(sizeof(double));
+}
+template <int TN, int NS>
+__global__ void __launch_bounds__(128, 2) k_gemm_big(const GemmTask* __restrict__ tasks) {
+  constexpr int KC = 16, PA = 64 + 8, PB = TN + 8, FM = 4, FN = TN / 16;
+  extern __shared__ __align__(16) double smb[];
+  double* As = smb;                 // [NS][KC][PA]
+  double* Bs = smb + NS * KC * PA;  // [NS][KC][PB]
+  const GemmTask& t = tasks[blockIdx.x];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp & 1, wn = warp >> 1;
+  const int m = t.m, n = t.n;
+  const double alpha = t.alpha, beta = t.beta;
+  double* C = t.c;
+  const int64_t ldc = t.ldc;
+  double acc[FM][FN][2];
+#pragma unroll
+  for (int i = 0; i < FM; ++i)
+#pragma unroll
+    for (int j = 0; j < FN; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int row = wm * 32 + i * 8 + (lane >> 2);
+        const int col = wn * (TN / 2) + j * 8 + (lane & 3) * 2 + e;
+        acc[i][j][e] = (beta != 0.0 && row < m && col < n) ? beta * C[row + col * ldc] : 0.0;
+      }
+  const int K = t.k[0];
+  const double* A = t.a[0];
+  const double* B = t.b[0];
+  const int lda = t.lda[0], ldb = t.ldb[0];
+  const int nk = (K + KC - 1) / KC;
+  auto load = [&](int st, int k0) {
+    double* a = As + st * KC * PA;
+    double* b = Bs + st * KC * PB;
+#pragma unroll
+    for (int it = 0; it < (KC * 64) / (2 * 128); ++it) {
+      const int idx = tid + it * 128, kk = idx >> 5, mm = (idx & 31) * 2;
+      cp_async16(a + kk * PA + mm, A + mm + static_cast<int64_t>(k0 + kk) * lda);
+    }
+#pragma unroll
+    for (int it = 0; it < (KC * TN) / (2 * 128); ++it) {
+      const int idx = tid + it * 128, kk = idx / (TN / 2), mm = (idx % (TN / 2)) * 2;
+      cp_async16(b + kk * PB + mm, B + mm + static_cast<int64_t>(k0 + kk) * ldb);
+    }
+  };
+#pragma unroll
+  for (int s = 0; s < NS - 1; ++s) {
+    if (s < nk) load(s, s * KC);
+    cp_async_commit();
+  }
+  for (int kc = 0; kc < nk; ++kc) {
+    cp_async_wait<NS - 2>();
+    __syncthreads();
+    if (kc + NS - 1 < nk) load((kc + NS - 1) % NS, (kc + NS - 1) * KC);
+    cp_async_commit();
+    const double* a = As + (kc % NS) * KC * PA;
+    const double* b = Bs + (kc % NS) * KC * PB;
+#pragma unroll
+    for (int kk = 0; kk < KC; kk += 4) {
+      const int kr = kk + (lane & 3);
+      double af[FM], bf[FN];
+#pragma unroll
+      for (int i = 0; i < FM; ++i) af[i] = alpha * a[kr * PA + wm * 32 + i * 8 + (lane >> 2)];
+#pragma unroll
+      for (int j = 0; j < FN; ++j) bf[j] = b[kr * PB + wn * (TN / 2) + j * 8 + (lane >> 2)];
+#pragma unroll
+      for (int i = 0; i < FM; ++i)
+#pragma unroll
+        for (int j = 0; j < FN; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < FM; ++i) {
+    const int row = wm * 32 + i * 8 + (lane >> 2);
+    if (row >= m) continue;
+#pragma unroll
+    for (int j = 0; j < FN; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int col = wn * (TN / 2) + j * 8 + (lane & 3) * 2 + e;
+        if (col < n) C[row + col * ldc] = acc[i][j][e];
+      }
+  }
+}
+}  // namespace gmrf
