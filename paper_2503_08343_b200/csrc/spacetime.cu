@@ -623,7 +623,7 @@ void SpaceTimePosterior::assemble_device() {
   w_.alloc(std::max(ms_, 1));
   f_.alloc(std::max(nres_, 1));
   fc_.alloc(std::max(nres_, 1));
-  part_.alloc(kDotBlocks + 1);
+  part_.alloc(2 * (kDotBlocks + 1));
 }
 
 // Row 1: joint prior / q_eff values on the master pattern (device).
@@ -682,15 +682,27 @@ AcDev SpaceTimePosterior::ac_dev() const {
                d_slack_.p, kept_.p, d_mrp_.p, d_mci_.p, d_mv_.p, d_kv_.p, d_ml_.p};
 }
 
-// ½‖Sᵀ(x−μ)‖² + ½ Σ λ (y − f)², y = 0 (gauss_newton.hpp:65-83)
+// ½‖Sᵀ(x−μ)‖² + ½ Σ λ (y − f)², y = 0 (gauss_newton.hpp:65-83); both sums
+// are read back with one host synchronization
 double SpaceTimePosterior::objective(const double* d_x, const double* d_fx) {
   k_axpby<<<grid_for(n_), 256, 0, stream_>>>(n_, 1.0, d_x, -1.0, mean_cond_.p, c_.p);
   k_spmv<<<grid_for(ms_), 256, 0, stream_>>>(ms_, d_scp_.p, d_sri_.p, d_sv_.p, nullptr, c_.p, w_.p);
   times_.kernel_launches += 2;
-  double quad = 0.5 * dot(w_.p, w_.p, ms_);
-  double fit = 0.0;
-  if (nres_ > 0) fit = spec_.pde_noise_prec * dot(d_fx, d_fx, nres_);
-  return quad + 0.5 * fit;
+  if (nres_ == 0) return 0.5 * dot(w_.p, w_.p, ms_);
+  double* p2 = part_.p + kDotBlocks + 1;
+  k_dot_partial<<<kDotBlocks, kDotThreads, 0, stream_>>>(ms_, w_.p, w_.p, part_.p);
+  k_dot_final<<<1, 512, 0, stream_>>>(part_.p, part_.p + kDotBlocks);
+  k_dot_partial<<<kDotBlocks, kDotThreads, 0, stream_>>>(nres_, d_fx, d_fx, p2);
+  k_dot_final<<<1, 512, 0, stream_>>>(p2, p2 + kDotBlocks);
+  times_.kernel_launches += 4;
+  double ww = 0.0, ff = 0.0;
+  cuda_check(cudaMemcpyAsync(&ww, part_.p + kDotBlocks, sizeof(double), cudaMemcpyDeviceToHost,
+                             stream_),
+             "objective");
+  cuda_check(cudaMemcpyAsync(&ff, p2 + kDotBlocks, sizeof(double), cudaMemcpyDeviceToHost, stream_),
+             "objective");
+  cuda_check(cudaStreamSynchronize(stream_), "objective");
+  return 0.5 * ww + 0.5 * (spec_.pde_noise_prec * ff);
 }
 
 void SpaceTimePosterior::fill_panels(const double* base, bool with_jacobian) {
@@ -792,8 +804,12 @@ std::vector<GnIter> SpaceTimePosterior::run(const double* u0, const GnConfig& cf
                              stream_),
              "x0");
   const double lam = spec_.pde_noise_prec;
+  // the accepted line-search candidate's residual and objective are the next
+  // iterate's (same buffers, same kernels): carried over instead of recomputed
+  bool carried = false;
+  double obj_carry = 0.0;
   for (int iter = 1; iter <= cfg.max_iters; ++iter) {
-    eval_residual(x_.p, f_.p);
+    if (!carried) eval_residual(x_.p, f_.p);
     eval_jacobian(x_.p);
     // grad = S(Sᵀ(x−μ)) − Jᵀ Λ (y − f)    (y = 0)
     k_axpby<<<grid_for(n_), 256, 0, stream_>>>(n_, 1.0, x_.p, -1.0, mean_cond_.p, c_.p);
@@ -811,7 +827,7 @@ std::vector<GnIter> SpaceTimePosterior::run(const double* u0, const GnConfig& cf
     times_.kernel_launches += fac_->launches_solve();
     const double gd = dot(g_.p, d_.p, n_);
     const double decrement = std::sqrt(std::max(0.0, -gd));
-    const double obj = objective(x_.p, f_.p);
+    const double obj = carried ? obj_carry : objective(x_.p, f_.p);
     GnIter rec{iter, obj, decrement, 0.0, 0};
     if (decrement < cfg.decrement_tol || 0.5 * decrement * decrement <= 1e-14 * (1.0 + std::abs(obj))) {
       trace.push_back(rec);
@@ -828,6 +844,9 @@ std::vector<GnIter> SpaceTimePosterior::run(const double* u0, const GnConfig& cf
       const double cobj = objective(cand_.p, fc_.p);
       if (cobj <= obj + cfg.armijo_c * alpha * slope) {
         std::swap(x_.p, cand_.p);
+        std::swap(f_.p, fc_.p);
+        obj_carry = cobj;
+        carried = true;
         break;
       }
       if (++bt > cfg.max_backtracks) {
