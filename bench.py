@@ -356,7 +356,9 @@ def main():
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")) as fh:
-            traffic = json.load(fh).get(dom_name, {}).get("dram_bytes_per_launch")
+            tr = json.load(fh).get(dom_name, {})
+            if tr.get("workload", "c4") == args.workload:
+                traffic = tr.get("dram_bytes_per_launch")
     except (OSError, ValueError):
         traffic = None
     if dom["flops"] > 0:
