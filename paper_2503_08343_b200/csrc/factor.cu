@@ -176,7 +176,10 @@ DeviceFactor::DeviceFactor(std::shared_ptr<const Symbolic> sym, cudaStream_t str
                                                            wide_smem_bytes<16>()),
              "wide occupancy");
   const int64_t wide_cap = static_cast<int64_t>(nsm) * std::max(occ, 0);
-  auto is_wide = [&](int k) { return s.w(k) > kWideW && nchunks(s.w(k)) <= wide_cap; };
+  const int wide_w = std::getenv("GMRF_WIDE_W") ? std::atoi(std::getenv("GMRF_WIDE_W")) : kWideW;
+  const int split_cols =
+      std::getenv("GMRF_SPLIT_COLS") ? std::atoi(std::getenv("GMRF_SPLIT_COLS")) : kSolveSplitCols;
+  auto is_wide = [&](int k) { return s.w(k) > wide_w && nchunks(s.w(k)) <= wide_cap; };
   lvl_nrm_.assign(s.n_levels, 0);
   lvl_nsm_.assign(s.n_levels, 0);
   wl_ptr_.assign(s.n_levels + 1, 0);
@@ -208,7 +211,7 @@ DeviceFactor::DeviceFactor(std::shared_ptr<const Symbolic> sym, cudaStream_t str
     wide_blocks_ = nflag;
     wfwd_.upload(wf, stream_);
     wbwd_.upload(wb, stream_);
-    wflags_.alloc(std::max<int64_t>(2 * nflag, 1));
+    wx_.alloc(std::max<int64_t>(2 * nflag * 64 * kMaxRhs, 1));
   }
   lvl_sn_.upload(lsn, stream_);
   // solve workspaces: update vectors (r_s) and backward partials (tiles_s × w_s),
@@ -239,12 +242,12 @@ DeviceFactor::DeviceFactor(std::shared_ptr<const Symbolic> sym, cudaStream_t str
       for (int64_t q = lvl_ptr_[l]; q < lvl_ptr_[l + 1]; ++q) {
         const int k = lsn[q], r = s.r(k), w = s.w(k);
         if (!is_wide(k) && r <= kSolveFuseRows) continue;  // done inside the *_diag kernels
-        const int np = w > kSolveSplitCols ? (w + kSolveSplitCols - 1) / kSolveSplitCols : 1;
+        const int np = w > split_cols ? (w + split_cols - 1) / split_cols : 1;
         for (int t = 0; t * kSolveRows < r; ++t) {
           const int32_t slot = np > 1 ? nslot : 0, ctr = np > 1 ? nctr++ : 0;
           for (int p = 0; p < np; ++p) {
-            const int c0 = np > 1 ? p * kSolveSplitCols : 0;
-            const int c1 = np > 1 ? std::min(w, c0 + kSolveSplitCols) : w;
+            const int c0 = np > 1 ? p * split_cols : 0;
+            const int c1 = np > 1 ? std::min(w, c0 + split_cols) : w;
             tl.push_back({k, t * kSolveRows, t, c0, c1, p, np, slot, ctr});
           }
           if (np > 1) nslot += np;
@@ -266,6 +269,26 @@ DeviceFactor::DeviceFactor(std::shared_ptr<const Symbolic> sym, cudaStream_t str
     if (!mine(k)) continue;
     const double w = s.w(k), rows = s.rows(k);
     lvl_bytes_[s.sn_level[k]] += 8.0 * (w * rows - w * (w - 1.0) / 2.0) + 4.0 * rows;
+  }
+  if (std::getenv("GMRF_SOLVE_STATS")) {  // diagnostic: solve schedule per level
+    for (int l = 0; l < s.n_levels; ++l) {
+      int64_t nsn = lvl_ptr_[l + 1] - lvl_ptr_[l], maxw = 0, maxr = 0;
+      double tri = 0, rect = 0;
+      for (int64_t q = lvl_ptr_[l]; q < lvl_ptr_[l + 1]; ++q) {
+        const int k = lsn[q];
+        const double w = s.w(k), r = s.r(k);
+        maxw = std::max<int64_t>(maxw, s.w(k));
+        maxr = std::max<int64_t>(maxr, s.r(k));
+        tri += 8.0 * w * (w + 1) / 2;
+        rect += 8.0 * w * r;
+      }
+      std::fprintf(stderr,
+                   "solve level %d: sn %lld small %lld diag %lld wide %lld maxw %lld maxr %lld "
+                   "tri %.1f MB rect %.1f MB tiles %lld\n",
+                   l, (long long)nsn, (long long)lvl_nsm_[l], (long long)(lvl_nrm_[l] - lvl_nsm_[l]),
+                   (long long)(nsn - lvl_nrm_[l]), (long long)maxw, (long long)maxr, tri / 1e6,
+                   rect / 1e6, (long long)(tile_ptr_[l + 1] - tile_ptr_[l]));
+    }
   }
   if (part_) {  // backward-solve exchange: x rows packed per cross edge
     std::vector<RowXfer> pk, un;
@@ -1233,7 +1256,9 @@ void DeviceFactor::launch_solve_levels(bool fwd, bool bwd, double* y, int nr) {
   constexpr int smem_wide = wide_smem_bytes<NR>();
   int64_t& launches = launches_solve_;
   if (wide_blocks_) {
-    cuda_check(cudaMemsetAsync(wflags_.p, 0, 2 * wide_blocks_ * sizeof(int32_t), st), "flags");
+    // every slot back to the all-ones sentinel (k_*solve_wide poll their inputs)
+    cuda_check(cudaMemsetAsync(wx_.p, 0xFF, 2 * wide_blocks_ * 64 * nr * sizeof(double), st),
+               "wide exchange");
     ++launches;
   }
   auto coop = [&](const void* fn, int64_t grid, void** args) {
@@ -1266,8 +1291,8 @@ void DeviceFactor::launch_solve_levels(bool fwd, bool bwd, double* y, int nr) {
           ++launches;
           for (int64_t g = wl_ptr_[l]; g < wl_ptr_[l + 1]; ++g) {
             const WideBlock* tasks = wfwd_.p + wgroups_[g].t0;
-            int32_t* flags = wflags_.p;
-            void* args[] = {&tasks, const_cast<SymDev*>(&sd), &L, &y, &nr, &rdiag, &flags};
+            double* xw = wx_.p;
+            void* args[] = {&tasks, const_cast<SymDev*>(&sd), &L, &y, &nr, &rdiag, &xw};
             coop(reinterpret_cast<const void*>(k_fsolve_wide<NR>), wgroups_[g].nt, args);
           }
         }
@@ -1305,8 +1330,8 @@ void DeviceFactor::launch_solve_levels(bool fwd, bool bwd, double* y, int nr) {
           const WideBlock* tasks = wbwd_.p + wgroups_[g].t0;
           const double* P = P_.p;
           const int64_t* pptr = pptr_.p;
-          int32_t* flags = wflags_.p + wide_blocks_;
-          void* args[] = {&tasks, const_cast<SymDev*>(&sd), &L, &y, &nr, &P, &pptr, &rdiag, &flags};
+          double* xw = wx_.p + wide_blocks_ * 64 * nr;
+          void* args[] = {&tasks, const_cast<SymDev*>(&sd), &L, &y, &nr, &P, &pptr, &rdiag, &xw};
           coop(reinterpret_cast<const void*>(k_bsolve_wide<NR>), wgroups_[g].nt, args);
         }
       });

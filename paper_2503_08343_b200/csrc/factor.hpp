@@ -260,7 +260,7 @@ class DeviceFactor {
   std::vector<int64_t> lvl_nrm_, lvl_nsm_, wl_ptr_;
   std::vector<WideGroup> wgroups_;
   DevBuf<WideBlock> wfwd_, wbwd_;
-  DevBuf<int32_t> wflags_;
+  DevBuf<double> wx_;  // wide-solve block exchange: solved 64-row blocks, sentinel until written
   int64_t wide_blocks_ = 0;
 
   int64_t launches_numeric_ = 0, launches_solve_ = 0, launches_selinv_ = 0;

@@ -75,7 +75,7 @@ struct SelChunk {
 };
 
 // One 64-row block of a wide supernode's triangle in the solves (solve_wide.cuh).
-constexpr int kWideW = 256;  // supernodes wider than this use the wide solve kernels
+constexpr int kWideW = 128;  // supernodes wider than this use the wide solve kernels
 struct WideBlock {
   int32_t sn;
   int32_t b;      // block index inside the triangle

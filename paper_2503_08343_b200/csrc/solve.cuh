@@ -17,6 +17,66 @@
 
 namespace gmrf {
 
+// acc[rr] -= Σ_j li[j·ld] · v[rr·vs + j] for j = 0..nj-1, in ascending j (the
+// same accumulation order as a plain loop), with kGemvU independent L loads in
+// flight per thread: a thread walks one row of a column-major panel, so its
+// loads are strided and each batch costs a full memory round trip.
+template <int NR>
+__device__ __forceinline__ void row_gemv_sub(double (&acc)[NR], const double* __restrict__ li,
+                                             int64_t ld, const double* v, int vs, int nrhs,
+                                             int nj) {
+  constexpr int U = NR == 1 ? 32 : 16;
+  int j = 0;
+  for (; j + U <= nj; j += U) {
+    double l[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) l[u] = li[static_cast<int64_t>(j + u) * ld];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int rr = 0; rr < NR; ++rr) acc[rr] -= l[u] * v[rr * vs + j + u];
+  }
+  for (; j + 8 <= nj; j += 8) {
+    double l[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) l[u] = li[static_cast<int64_t>(j + u) * ld];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+#pragma unroll
+      for (int rr = 0; rr < NR; ++rr) acc[rr] -= l[u] * v[rr * vs + j + u];
+  }
+  for (; j < nj; ++j) {
+    const double l = li[static_cast<int64_t>(j) * ld];
+#pragma unroll
+    for (int rr = 0; rr < NR; ++rr) acc[rr] -= l * v[rr * vs + j];
+  }
+  (void)nrhs;
+}
+
+
+// Warp dot products over CJ columns at once: acc[c][rr] += Σ_i col_c[i] · x[rr·xs + i]
+// for i = lane, lane+32, … < nt (per-lane partials in ascending i, as a
+// one-column loop), columns col0 + c·cs for c < nc; CJ columns' loads in flight.
+template <int NR, int CJ>
+__device__ __forceinline__ void warp_col_dots(double (&acc)[CJ][NR], const double* __restrict__ col0,
+                                              int64_t cs, int nc, const double* x, int xs, int nt,
+                                              int lane) {
+#pragma unroll
+  for (int c = 0; c < CJ; ++c)
+#pragma unroll
+    for (int rr = 0; rr < NR; ++rr) acc[c][rr] = 0.0;
+#pragma unroll 4
+  for (int ii = lane; ii < nt; ii += 32) {
+    double l[CJ];
+#pragma unroll
+    for (int c = 0; c < CJ; ++c) l[c] = c < nc ? col0[c * cs + ii] : 0.0;
+#pragma unroll
+    for (int c = 0; c < CJ; ++c)
+#pragma unroll
+      for (int rr = 0; rr < NR; ++rr) acc[c][rr] += l[c] * x[rr * xs + ii];
+  }
+}
+
 // ---- forward: diagonal triangle + children assembly -------------------------
 template <int NR>
 __global__ void __launch_bounds__(256) k_fsolve_diag(const int32_t* __restrict__ sns, SymDev sd,
@@ -103,22 +163,7 @@ __global__ void __launch_bounds__(256) k_fsolve_diag(const int32_t* __restrict__
       double acc[NR];
 #pragma unroll
       for (int rr = 0; rr < NR; ++rr) acc[rr] = rr < nrhs ? fJ[rr * w + i] : 0.0;
-      const double* li = Ls + i + static_cast<int64_t>(c0) * rows;
-      int j = 0;
-      for (; j + 8 <= wk; j += 8) {  // 8 independent loads in flight
-        double l[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) l[u] = li[static_cast<int64_t>(j + u) * rows];
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-#pragma unroll
-          for (int rr = 0; rr < NR; ++rr) acc[rr] -= l[u] * fJ[rr * w + c0 + j + u];
-      }
-      for (; j < wk; ++j) {
-        const double l = li[static_cast<int64_t>(j) * rows];
-#pragma unroll
-        for (int rr = 0; rr < NR; ++rr) acc[rr] -= l * fJ[rr * w + c0 + j];
-      }
+      row_gemv_sub<NR>(acc, Ls + i + static_cast<int64_t>(c0) * rows, rows, fJ + c0, w, nrhs, wk);
 #pragma unroll
       for (int rr = 0; rr < NR; ++rr)
         if (rr < nrhs) fJ[rr * w + i] = acc[rr];
@@ -130,22 +175,7 @@ __global__ void __launch_bounds__(256) k_fsolve_diag(const int32_t* __restrict__
       double acc[NR];
 #pragma unroll
       for (int rr = 0; rr < NR; ++rr) acc[rr] = rr < nrhs ? uS[i + rr * r] : 0.0;
-      const double* li = Ls + w + i;
-      int j = 0;
-      for (; j + 8 <= w; j += 8) {  // 8 independent loads in flight
-        double l[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) l[u] = li[static_cast<int64_t>(j + u) * rows];
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-#pragma unroll
-          for (int rr = 0; rr < NR; ++rr) acc[rr] -= l[u] * fJ[rr * w + j + u];
-      }
-      for (; j < w; ++j) {
-        const double l = li[static_cast<int64_t>(j) * rows];
-#pragma unroll
-        for (int rr = 0; rr < NR; ++rr) acc[rr] -= l * fJ[rr * w + j];
-      }
+      row_gemv_sub<NR>(acc, Ls + w + i, rows, fJ, w, nrhs, w);
 #pragma unroll
       for (int rr = 0; rr < NR; ++rr)
         if (rr < nrhs) uS[i + rr * r] = acc[rr];
@@ -197,22 +227,7 @@ __global__ void __launch_bounds__(kSolveRows) k_fsolve_off(const SolveTile* __re
     }
     __syncthreads();
     if (!active) continue;
-    const double* Lc = Lr + static_cast<int64_t>(c0) * rows;
-    int j = 0;
-    for (; j + 8 <= wc; j += 8) {  // 8 independent loads in flight
-      double l[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) l[q] = Lc[static_cast<int64_t>(j + q) * rows];
-#pragma unroll
-      for (int q = 0; q < 8; ++q)
-#pragma unroll
-        for (int rr = 0; rr < NR; ++rr) acc[rr] -= l[q] * yJ[rr * CW + j + q];
-    }
-    for (; j < wc; ++j) {
-      const double l = Lc[static_cast<int64_t>(j) * rows];
-#pragma unroll
-      for (int rr = 0; rr < NR; ++rr) acc[rr] -= l * yJ[rr * CW + j];
-    }
+    row_gemv_sub<NR>(acc, Lr + static_cast<int64_t>(c0) * rows, rows, yJ, CW, nrhs, wc);
   }
   if (!split) {
     if (!active) return;
@@ -267,24 +282,21 @@ __global__ void __launch_bounds__(256) k_bsolve_off(const SolveTile* __restrict_
   __syncthreads();
   const double* Lt = L + sd.lptr[s] + w + t.r0;
   double* Pt = P + (pptr[s] + static_cast<int64_t>(t.tidx) * w) * nrhs;  // [rr*w + j]
-  for (int j = t.c0 + warp; j < t.c1; j += 8) {
-    const double* col = Lt + static_cast<int64_t>(j) * rows;
-    double acc[NR];
+  constexpr int CJ = NR <= 4 ? 4 : 1;  // columns j, j+8, … per warp pass
+  for (int j0 = t.c0 + warp; j0 < t.c1; j0 += 8 * CJ) {
+    double acc[CJ][NR];
+    const int nc = min(CJ, (t.c1 - j0 + 7) / 8);
+    warp_col_dots<NR, CJ>(acc, Lt + static_cast<int64_t>(j0) * rows, 8 * static_cast<int64_t>(rows),
+                          nc, xR, kSolveRows, nt, lane);
 #pragma unroll
-    for (int rr = 0; rr < NR; ++rr) acc[rr] = 0.0;
-#pragma unroll 4
-    for (int ii = lane; ii < nt; ii += 32) {
-      const double l = col[ii];
+    for (int c = 0; c < CJ; ++c)
 #pragma unroll
-      for (int rr = 0; rr < NR; ++rr) acc[rr] += l * xR[rr * kSolveRows + ii];
-    }
+      for (int rr = 0; rr < NR; ++rr) {
+        double v = acc[c][rr];
 #pragma unroll
-    for (int rr = 0; rr < NR; ++rr) {
-      double v = acc[rr];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (lane == 0 && rr < nrhs) Pt[rr * w + j] = v;
-    }
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0 && rr < nrhs && c < nc) Pt[rr * w + j0 + 8 * c] = v;
+      }
   }
 }
 
@@ -316,24 +328,23 @@ __global__ void __launch_bounds__(256) k_bsolve_diag(const int32_t* __restrict__
       xR[rr * r + i] = x[srows[i] + static_cast<int64_t>(rr) * n];
     }
     __syncthreads();
-    for (int j = warp; j < w; j += 8) {
-      const double* col = Ls + w + static_cast<int64_t>(j) * rows;
-      double acc[NR];
+    constexpr int CJ = NR <= 4 ? 4 : 1;  // columns j, j+8, … per warp pass
+    for (int j0 = warp; j0 < w; j0 += 8 * CJ) {
+      double acc[CJ][NR];
+      const int nc = min(CJ, (w - j0 + 7) / 8);
+      warp_col_dots<NR, CJ>(acc, Ls + w + static_cast<int64_t>(j0) * rows,
+                            8 * static_cast<int64_t>(rows), nc, xR, r, r, lane);
 #pragma unroll
-      for (int rr = 0; rr < NR; ++rr) acc[rr] = 0.0;
-#pragma unroll 4
-      for (int i = lane; i < r; i += 32) {
-        const double l = col[i];
+      for (int c = 0; c < CJ; ++c)
 #pragma unroll
-        for (int rr = 0; rr < NR; ++rr) acc[rr] += l * xR[rr * r + i];
-      }
+        for (int rr = 0; rr < NR; ++rr) {
+          double v = acc[c][rr];
 #pragma unroll
-      for (int rr = 0; rr < NR; ++rr) {
-        double v = acc[rr];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (lane == 0 && rr < nrhs) bJ[rr * w + j] = x[f0 + j + static_cast<int64_t>(rr) * n] - v;
-      }
+          for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+          const int j = j0 + 8 * c;
+          if (lane == 0 && rr < nrhs && c < nc)
+            bJ[rr * w + j] = x[f0 + j + static_cast<int64_t>(rr) * n] - v;
+        }
     }
   } else {
     const int ntiles = (r + kSolveRows - 1) / kSolveRows;

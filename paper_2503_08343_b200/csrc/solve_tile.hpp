@@ -7,7 +7,7 @@ namespace gmrf {
 
 constexpr int kSolveRows = 128;
 constexpr int kSolveOffCols = 256;  // y_J columns staged per pass in k_fsolve_off
-constexpr int kSolveSplitCols = 128;
+constexpr int kSolveSplitCols = 64;
 constexpr int kSolveFuseRows = 256;  // narrow supernodes with r ≤ this: no off-diagonal tiles  // wider supernodes split their row tiles by column blocks
 
 struct SolveTile {

@@ -9,10 +9,10 @@
 //              L[b,m]·y_m, solves its 64×64 diagonal block, publishes y_b;
 //   backward — block b waits for blocks m = nb-1..b+1 IN ORDER, subtracts
 //              L[m,b]ᵀ·x_m, solves with L_bbᵀ, publishes x_b.
-// The L tiles do not depend on the flags, so each CTA prefetches them with
+// The L tiles do not depend on the exchange, so each CTA prefetches them with
 // cp.async (double buffered) while it waits; the dependent chain per block is
-// one flag round trip + a 64×64 GEMV + the 64-step warp solve.
-// The update order of every entry is fixed (m order, 4 fixed partial sums), so
+// one L2 round trip for the polled block values + a 64×64 GEMV + the 64-step
+// warp solve. The update order of every entry is fixed (m order, 4 fixed partial sums), so
 // results are bit-identical from run to run. All CTAs of a launch are
 // co-resident (cooperative launch), and a CTA only waits on CTAs with a lower
 // blockIdx (tasks are ordered by dependency), so the spin-waits cannot deadlock.
@@ -31,17 +31,25 @@ constexpr int wide_smem_bytes() {
   return (3 * 64 * kWideLd + 6 * 64 * NR + 64) * static_cast<int>(sizeof(double));
 }
 
-__device__ __forceinline__ void wide_wait(const int* flag) {
-  if (threadIdx.x == 0) {
-    while (*reinterpret_cast<const volatile int*>(flag) == 0) __nanosleep(32);
-    __threadfence();
-  }
-  __syncthreads();
+// Block exchange without flags: each solved 64-row block is published into its
+// own slot of XW (64·nrhs doubles, reset to the all-ones NaN pattern before the
+// sweep), and a consumer polls the values it needs until none is the sentinel.
+// The value is its own ready flag, so there is no fence + flag store on the
+// producer and no flag round trip before the data load on the consumer.
+constexpr unsigned long long kWideSentinel = ~0ull;
+__device__ __forceinline__ void wide_publish(double* slot, double v) {
+  unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(v));
+  if (b == kWideSentinel) b = 0x7ff8000000000000ull;  // a NaN result must not read as "not ready"
+  __stcg(reinterpret_cast<unsigned long long*>(slot), b);
 }
-__device__ __forceinline__ void wide_post(int* flag) {
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) atomicExch(flag, 1);
+__device__ __forceinline__ double wide_poll(const double* slot) {
+  const volatile unsigned long long* p = reinterpret_cast<const volatile unsigned long long*>(slot);
+  unsigned long long b = *p;
+  while (b == kWideSentinel) {
+    __nanosleep(20);
+    b = *p;
+  }
+  return __longlong_as_double(static_cast<long long>(b));
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
@@ -109,7 +117,7 @@ __global__ void __launch_bounds__(256) k_fsolve_wide(const WideBlock* __restrict
                                                      SymDev sd, const double* __restrict__ L,
                                                      double* __restrict__ y, int nrhs,
                                                      const double* __restrict__ rdiag,
-                                                     int* __restrict__ flags) {
+                                                     double* __restrict__ xw) {
   extern __shared__ double sm[];
   double* Lb = sm;                      // diagonal block, [j*65 + i]
   double* T0 = Lb + 64 * kWideLd;       // L[b, m] tiles, double buffered
@@ -139,9 +147,10 @@ __global__ void __launch_bounds__(256) k_fsolve_wide(const WideBlock* __restrict
     if (m + 1 < t.b)
       wide_stage_tile(T0 + ((m + 1) & 1) * 64 * kWideLd, Ls, rows, i0, nbr, (m + 1) * 64, 64);
     cp_commit();
-    wide_wait(flags + t.flag0 + m);
-    for (int idx = tid; idx < 64 * nrhs; idx += blockDim.x)
-      ym[idx] = __ldcg(y + f0 + m * 64 + (idx & 63) + static_cast<int64_t>(idx >> 6) * n);
+    {
+      const double* slot = xw + static_cast<int64_t>(t.flag0 + m) * 64 * nrhs;
+      for (int idx = tid; idx < 64 * nrhs; idx += blockDim.x) ym[idx] = wide_poll(slot + idx);
+    }
     cp_wait<1>();  // tile m (and the diagonal block) landed
     __syncthreads();
     double part[NR];
@@ -191,11 +200,15 @@ __global__ void __launch_bounds__(256) k_fsolve_wide(const WideBlock* __restrict
 #pragma unroll
     for (int rr = 0; rr < NR; ++rr) {
       if (rr >= nrhs) break;
+      double* slot = xw + static_cast<int64_t>(t.flag0 + t.b) * 64 * nrhs + rr * 64;
+      if (t.b + 1 < t.nb) {  // later blocks of this supernode wait on these values
+        if (lane < nbr) wide_publish(slot + lane, v0[rr]);
+        if (lane + 32 < nbr) wide_publish(slot + 32 + lane, v1[rr]);
+      }
       if (lane < nbr) y[f0 + i0 + lane + static_cast<int64_t>(rr) * n] = v0[rr];
       if (lane + 32 < nbr) y[f0 + i0 + 32 + lane + static_cast<int64_t>(rr) * n] = v1[rr];
     }
   }
-  wide_post(flags + t.flag0 + t.b);
 }
 
 // ---- backward: L_JJᵀ x_J = y_J − Σ_tiles P (row-tile partials of L_RJᵀ x_R) ----
@@ -206,7 +219,7 @@ __global__ void __launch_bounds__(256) k_bsolve_wide(const WideBlock* __restrict
                                                      const double* __restrict__ P,
                                                      const int64_t* __restrict__ pptr,
                                                      const double* __restrict__ rdiag,
-                                                     int* __restrict__ flags) {
+                                                     double* __restrict__ xw) {
   extern __shared__ double sm[];
   double* Lb = sm;
   double* T0 = Lb + 64 * kWideLd;       // L[m, b] tiles, double buffered
@@ -245,11 +258,11 @@ __global__ void __launch_bounds__(256) k_bsolve_wide(const WideBlock* __restrict
     if (m - 1 > t.b)
       wide_stage_tile(T0 + ((it + 1) & 1) * 64 * kWideLd, Ls, rows, (m - 1) * 64, 64, i0, nbr);
     cp_commit();
-    wide_wait(flags + t.flag0 + m);
     const int nm = min(64, w - m * 64);
-    for (int idx = tid; idx < 64 * nrhs; idx += blockDim.x) {
-      const int ii = idx & 63;
-      xm[idx] = ii < nm ? __ldcg(x + f0 + m * 64 + ii + static_cast<int64_t>(idx >> 6) * n) : 0.0;
+    {
+      const double* slot = xw + static_cast<int64_t>(t.flag0 + m) * 64 * nrhs;
+      for (int idx = tid; idx < 64 * nrhs; idx += blockDim.x)
+        xm[idx] = (idx & 63) < nm ? wide_poll(slot + idx) : 0.0;
     }
     cp_wait<1>();
     __syncthreads();
@@ -300,11 +313,15 @@ __global__ void __launch_bounds__(256) k_bsolve_wide(const WideBlock* __restrict
 #pragma unroll
     for (int rr = 0; rr < NR; ++rr) {
       if (rr >= nrhs) break;
+      double* slot = xw + static_cast<int64_t>(t.flag0 + t.b) * 64 * nrhs + rr * 64;
+      if (t.b > 0) {  // earlier blocks of this supernode wait on these values
+        if (lane < nbr) wide_publish(slot + lane, v0[rr]);
+        if (lane + 32 < nbr) wide_publish(slot + 32 + lane, v1[rr]);
+      }
       if (lane < nbr) x[f0 + i0 + lane + static_cast<int64_t>(rr) * n] = v0[rr];
       if (lane + 32 < nbr) x[f0 + i0 + 32 + lane + static_cast<int64_t>(rr) * n] = v1[rr];
     }
   }
-  wide_post(flags + t.flag0 + t.b);
 }
 
 }  // namespace gmrf
