@@ -104,4 +104,38 @@ struct SymDev {
   int32_t n;
 };
 
+
+#ifdef __CUDACC__
+// Children assembly of the solves: for every entry (ia, rr) of a child's update
+// vector uc (rc × nrhs), *tgt(rel[ia], rr) += uc[ia + rr·rc]. rel is injective
+// within one child, so the U entries a thread handles per pass are independent:
+// all their loads (rel, uc, then the targets) are issued before any store —
+// the compiler cannot reorder them itself, as the targets may alias uc.
+template <int U, typename Tgt>
+__device__ __forceinline__ void child_scatter(const int32_t* __restrict__ rel, const double* uc,
+                                              int rc, int nrhs, Tgt tgt) {
+  const int tot = rc * nrhs;
+  for (int base = threadIdx.x; base < tot; base += U * blockDim.x) {
+    double* p[U];
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int idx = base + u * blockDim.x;
+      p[u] = nullptr;
+      if (idx < tot) {
+        const int ia = idx % rc, rr = idx / rc;
+        p[u] = tgt(__ldg(rel + ia), rr);
+        v[u] = uc[ia + rr * rc];
+      }
+    }
+    double old[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) old[u] = p[u] ? *p[u] : 0.0;
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (p[u]) *p[u] = old[u] + v[u];
+  }
+}
+#endif
+
 }  // namespace gmrf

@@ -110,13 +110,9 @@ __global__ void __launch_bounds__(256) k_fsolve_diag(const int32_t* __restrict__
     const int rc = static_cast<int>(sd.sn_rptr[c + 1] - sd.sn_rptr[c]) - wc;
     const int32_t* rel = sd.relmap + sd.sn_rptr[c] + wc;
     const double* uc = Uv + uvptr[c] * nrhs;
-    for (int idx = tid; idx < rc * nrhs; idx += blockDim.x) {
-      const int ia = idx % rc, rr = idx / rc;
-      const int a = rel[ia];
-      const double v = uc[ia + rr * rc];
-      if (a < w) fJ[rr * w + a] += v;
-      else uS[(a - w) + rr * r] += v;
-    }
+    child_scatter<4>(rel, uc, rc, nrhs, [&](int a, int rr) {
+      return a < w ? fJ + rr * w + a : uS + (a - w) + rr * r;
+    });
     __syncthreads();
   }
   for (int c0 = 0; c0 < w; c0 += 64) {
