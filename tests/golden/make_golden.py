@@ -64,6 +64,21 @@ def matern1d(ref):
     np.savez_compressed(os.path.join(HERE, "c1_matern1d.npz"), **out)
 
 
+def matern2d(ref):
+    """C2: 2D Matérn regression, full size (256² nodes, 2000
+    observations, Rng(1002) interleaved (x, y) then noises), mean, Takahashi
+    variances and the first 2 of the 16 samples (Rng(2002); z is re-drawn by the
+    test through the Rng mirror). The factor L is not stored (8.1M entries)."""
+    b = ref.build("matern2d", [255, 10.0, 2, 1.0, 2000, 1002, 400.0, 0.05, 2, 2002, 1])
+    out = {}
+    for k in ["A", "Q_post"]:
+        out.update(mat(k, b.mat(k)))
+    for k in ["y", "noise", "points", "mean_post", "var_post", "samples", "perm_amd"]:
+        out[k] = b.vec(k)
+    out["perm_amd"] = out["perm_amd"].astype(np.int32)
+    np.savez_compressed(os.path.join(HERE, "c2_matern2d.npz"), **out)
+
+
 def spatiotemporal(ref, kind, n_el, n_t, name, gn_iters=0):
     """C3 (heat) / C4 (Burgers) shapes at reduced size."""
     if kind == 0:
@@ -105,9 +120,14 @@ def allen_cahn(ref, n_cells, n_t, name, gn_iters=8):
 
 def main():
     ref = Ref()
+    if len(sys.argv) > 1:  # selected fixtures only, e.g. `make_golden.py matern2d`
+        for name in sys.argv[1:]:
+            globals()[name](ref)
+        return
     corpus(ref, 50, 20240817, "corpus_acceptance.npz")   # acceptance.cpp:67 criterion 1
     corpus(ref, 12, 31415, "corpus_variance.npz")        # acceptance.cpp:652 criterion 10
     matern1d(ref)
+    matern2d(ref)
     spatiotemporal(ref, 0, 19, 20, "c3_heat_20x20.npz")
     spatiotemporal(ref, 1, 19, 20, "c4_burgers_20x20.npz", gn_iters=4)
     allen_cahn(ref, 8, 16, "c5_allen_cahn_8x8x16.npz")

@@ -129,6 +129,30 @@ def test_c1_posterior_vs_reference():
     assert rel(samples, z["samples"].reshape(8, n).T) <= 1e-10
 
 
+def test_c2_posterior_vs_reference():
+    """C2 (2D Matérn on 256² nodes, n=65,536, 2000 observations): mean ≤1e-10 and
+    Takahashi variances ≤1e-8 against the reference (north_star), with the
+    reference's AMD permutation and with our nested dissection; the first two of
+    the reference's 16 samples (Rng(2002), gmrf.hpp:182-184) under the same
+    permutation, z re-drawn through the Rng mirror."""
+    z = load_golden("c2_matern2d.npz")
+    q = golden_mat(z, "Q_post")
+    a = golden_mat(z, "A").to_scipy()
+    n = q.nrows
+    assert n == 65536 and a.shape == (2000, n)
+    rhs = a.T @ (z["noise"] * z["y"])
+    for perm in [z["perm_amd"], None]:
+        f = g.cholesky_factor(q, perm)
+        assert rel(g.solve(f, rhs), z["mean_post"]) <= 1e-10
+        assert rel(g.takahashi_diagonal(f), z["var_post"]) <= 1e-8
+    f = g.cholesky_factor(q, z["perm_amd"])
+    zz = g.Rng(2002).normal_vector(2 * n).reshape(2, n).T.copy()
+    w = g.solve_triangular(f, zz, g.TriangularMode.kUpper)
+    x = np.empty_like(w)
+    x[f.perm] = w
+    assert rel(x + z["mean_post"][:, None], z["samples"].reshape(2, n).T) <= 1e-10
+
+
 @pytest.mark.parametrize("fixture", ["c3_heat_20x20.npz", "c4_burgers_20x20.npz"])
 def test_spatiotemporal_variances_vs_reference(fixture):
     """Space-time posteriors: the reference's own FP64 floor is ~1e-5 (SURVEY §0.7);

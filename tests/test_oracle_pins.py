@@ -97,6 +97,30 @@ def test_port_tridiagonal_takahashi_vs_dense(port):
     np.testing.assert_allclose(d, np.diag(np.linalg.inv(m.toarray())), atol=1e-12)
 
 
+def test_port_c2_mean_and_samples_match_reference(port):
+    """C2 posterior (2D Matérn, n = 65,536): from the reference's Q_post bits and
+    AMD permutation the port reproduces the reference's mean and its first two
+    samples (z from the Rng mirror, core/rng.hpp). The variances (≈70 s of
+    single-core Takahashi) are checked on the GPU against the same fixture."""
+    import paper_2503_08343_b200 as g
+    z = load_golden("c2_matern2d.npz")
+    q = golden_mat(z, "Q_post")
+    n = q.nrows
+    perm = z["perm_amd"]
+    lcp, lri, lv, bad = port.cholesky(n, q.col_ptr, q.row_idx, q.values, perm)
+    assert bad == -1
+    rhs = golden_mat(z, "A").to_scipy().T @ (z["noise"] * z["y"])
+    mean = port.solve(n, lcp, lri, lv, perm, 2, rhs)[:, 0]
+    assert np.linalg.norm(mean - z["mean_post"]) <= 1e-13 * np.linalg.norm(z["mean_post"])
+    zz = g.Rng(2002).normal_vector(2 * n).reshape(2, n)
+    ss = z["samples"].reshape(2, n)
+    for k in range(2):
+        w = port.solve(n, lcp, lri, lv, perm, 1, zz[k])[:, 0]
+        x = np.empty(n)
+        x[perm] = w
+        np.testing.assert_allclose(x + z["mean_post"], ss[k], rtol=0, atol=1e-13)
+
+
 def test_port_c1_pipeline_matches_reference(port):
     """C1 posterior: the port reproduces the reference's mean,
     Takahashi variances and sample draws from the reference's Q_post bits."""
