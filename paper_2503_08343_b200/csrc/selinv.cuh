@@ -26,7 +26,10 @@ __global__ void __launch_bounds__(kTrsmRows) k_sel_trsm_w(const SelChunk* __rest
   const SelChunk& t = tasks[blockIdx.x];
   const int w = t.w, ld = t.ld, tid = threadIdx.x;
   const double* Lk = t.l + t.c0 + static_cast<int64_t>(t.c0) * ld;
-  for (int idx = tid; idx < W * W; idx += blockDim.x) {
+  // fully unrolled (compile-time trip count): every thread's loads are in flight
+  // together instead of one memory round trip per element
+#pragma unroll
+  for (int idx = tid; idx < W * W; idx += kTrsmRows) {
     const int j = idx / W, k = idx % W;  // consecutive threads: consecutive k (row j)
     Lr[idx] = (k < j && j < w) ? Lk[j + static_cast<int64_t>(k) * ld] : 0.0;
   }
@@ -74,13 +77,22 @@ __global__ void __launch_bounds__(W < 32 ? 32 : W) k_sel_diag_w(const SelChunk* 
   const int w = t.w, ld = t.ld, tid = threadIdx.x;
   const double* Lk = t.l + t.c0 + static_cast<int64_t>(t.c0) * ld;
   double* Sk = t.sig + t.c0 + static_cast<int64_t>(t.c0) * ld;
-  for (int idx = tid; idx < W * W; idx += blockDim.x) {
+  // L_JJ read once, coalesced (consecutive threads: consecutive rows k of column
+  // i), all of a thread's loads in flight together; the row copy Lt is the
+  // shared-memory transpose
+  constexpr int NT = W < 32 ? 32 : W;
+#pragma unroll 16
+  for (int idx = tid; idx < W * W; idx += NT) {
     const int i = idx / W, k = idx % W;
     const bool in = i < w && k < w;
     Lc[i * P + k] = (in && k >= i) ? Lk[k + static_cast<int64_t>(i) * ld] : (k == i ? 1.0 : 0.0);
-    Lt[i * P + k] = (in && k <= i) ? Lk[i + static_cast<int64_t>(k) * ld] : (k == i ? 1.0 : 0.0);
   }
   if (tid < W) rd[tid] = tid < w ? t.rd[tid] : 1.0;
+  __syncthreads();
+  for (int idx = tid; idx < W * W; idx += NT) {
+    const int i = idx / W, k = idx % W;
+    Lt[i * P + k] = k <= i ? Lc[k * P + i] : 0.0;  // L_ik = column k's entry i (1 on the padding)
+  }
   const int c = tid;
   const bool act = c < w;
   double x[W];
