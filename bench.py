@@ -383,6 +383,30 @@ def main():
                                 else v["bytes"] / (v["ms"] * 1e-3) / 1e9),
                    "unit": "TFLOP/s" if v["flops"] > 0 else "GB/s"}
                for k, v in sorted(stats.items(), key=lambda kv: -kv[1]["ms"])}
+    # north_star's per-subsystem rooflines: FP64 tensor peak for the
+    # factorization, HBM for assembly, the conditioning update and the solves; the
+    # selected inversion is reported against both (its GEMM part dominates)
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+
+    def agg(prefix):
+        sel = [v for k, v in stats.items() if k.startswith(prefix)]
+        ms_ = sum(v["ms"] for v in sel)
+        fl, by = sum(v["flops"] for v in sel), sum(v["bytes"] for v in sel)
+        out = {"ms_per_step": ms_, "launches": sum(v["launches"] for v in sel)}
+        if ms_ > 0:
+            out["gbs"] = by / (ms_ * 1e-3) / 1e9
+            out["hbm_frac"] = out["gbs"] / hbm_peak
+            if fl > 0:
+                out["tflops"] = fl / (ms_ * 1e-3) / 1e12
+                out["fp64_frac"] = out["tflops"] / peak_fp64
+        return out
+
+    rows = {"1_assembly": agg("assemble."), "2_conditioning_update": agg("update."),
+            "3_factorization": {**agg("factor."), "tflops": chol_tflops,
+                                "fp64_frac": chol_tflops / peak_fp64},
+            "4_solves": agg("solve."), "5_selected_inversion": agg("selinv."),
+            "note": "profiled (serialized) kernel time per step; bytes = algorithmic (DESIGN.md §3); "
+                    "factorization tflops = Sigma c_j^2 / numeric time"}
 
     if rank != 0:
         if world > 1:
@@ -410,6 +434,7 @@ def main():
                       "variances": info.selinv_ms},
         "host_setup_s": host_setup_s,
         "kernels": kernels,
+        "rooflines_by_row": rows,
         "gn_trace": [[t.objective, t.decrement, t.step_size, t.backtracks] for t in traces[-1]],
         "nnz_l": info.nnz_l, "nnz_l_padded": info.nnz_l_padded,
         "factor_device_gb": info.factor_device_bytes / 1e9,
