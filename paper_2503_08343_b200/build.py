@@ -1,6 +1,7 @@
 """Builds libgmrf_b200.so in-tree for sm_100a (nvcc cross-compiles without a GPU)."""
 from __future__ import annotations
 
+import concurrent.futures
 import glob
 import os
 import subprocess
@@ -33,11 +34,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(os.path.dirname(LIB), exist_ok=True)
     headers = glob.glob(os.path.join(CSRC, "*.hpp")) + glob.glob(os.path.join(CSRC, "*.cuh")) + \
         [os.path.join(HERE, "..", "include", "gmrf_b200.h")]
-    objs = []
+    objs, jobs = [], []
     for src in sorted(glob.glob(os.path.join(CSRC, "*.cpp"))):
         o = os.path.join(OBJ, os.path.basename(src) + ".o")
         if force or _stale(o, [src] + headers):
-            _run(["g++", *CXX_FLAGS, "-c", src, "-o", o])
+            jobs.append(["g++", *CXX_FLAGS, "-c", src, "-o", o])
         objs.append(o)
     for src in sorted(glob.glob(os.path.join(CSRC, "*.cu"))):
         if os.path.basename(src) == "kernels.cu":
@@ -45,10 +46,16 @@ def build(force: bool = False, verbose: bool = False) -> str:
         o = os.path.join(OBJ, os.path.basename(src) + ".o")
         deps = [src, os.path.join(CSRC, "kernels.cu")] + headers
         if force or _stale(o, deps):
-            _run(["nvcc", *NVCC_FLAGS, "-c", src, "-o", o] + (["-Xptxas", "-v"] if verbose else []))
+            jobs.append(["nvcc", *NVCC_FLAGS, "-c", src, "-o", o] +
+                        (["-Xptxas", "-v"] if verbose else []))
         objs.append(o)
+    # translation units compile in parallel (factor.cu dominates)
+    with concurrent.futures.ThreadPoolExecutor(max_workers=max(1, min(len(jobs), 6))) as ex:
+        for f in [ex.submit(_run, j) for j in jobs]:
+            f.result()
     if force or _stale(LIB, objs):
-        _run(["nvcc", "-shared", "-o", LIB, *objs, METIS, "-lcudart", "-lm"])
+        _run(["nvcc", "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB, *objs,
+              METIS, "-lcudart", "-lm"])
     return LIB
 
 

@@ -426,9 +426,8 @@ int gmrf_spacetime_create_partitioned(const gmrf_spacetime_config_t* c, int32_t 
 int gmrf_spacetime_run(gmrf_spacetime_t* h, const double* u0, int32_t want_var, double* mean,
                        double* var, gmrf_gn_iter_t* trace, int32_t max_trace, int32_t* n_trace,
                        int32_t* converged) {
-  std::vector<gmrf::GnIter> tr;
   int rc = guard([&] {
-    tr = h->p->run(u0, h->cfg, want_var != 0);
+    h->p->run(u0, h->cfg, want_var != 0);
     const int n = h->p->n();
     if (mean)
       gmrf::cuda_check(cudaMemcpy(mean, h->p->d_mean(), n * sizeof(double), cudaMemcpyDeviceToHost),
@@ -437,6 +436,8 @@ int gmrf_spacetime_run(gmrf_spacetime_t* h, const double* u0, int32_t want_var, 
       gmrf::cuda_check(cudaMemcpy(var, h->p->d_var(), n * sizeof(double), cudaMemcpyDeviceToHost),
                        "var");
   });
+  // the trace is complete on the error path too (line-search stagnation)
+  const std::vector<gmrf::GnIter>& tr = h->p->last_trace();
   if (n_trace) *n_trace = static_cast<int32_t>(tr.size());
   if (trace)
     for (size_t i = 0; i < tr.size() && static_cast<int32_t>(i) < max_trace; ++i)

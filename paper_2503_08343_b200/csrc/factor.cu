@@ -1034,7 +1034,13 @@ int32_t DeviceFactor::factor_panels() {
 void DeviceFactor::enqueue_levels(cudaStream_t sa, cudaStream_t sb, bool la, bool in_graph) {
   const SymDev sd = symdev();
   KernelProfiler& pf = *prof_;
+  // GMRF_WHATIF_BUILD: diagnostic-only build (tools/) that drops launch classes to
+  // time the rest; compiled out of the product library (results would be invalid)
+#ifdef GMRF_WHATIF_BUILD
   static const int whatif = std::getenv("GMRF_WHATIF") ? atoi(std::getenv("GMRF_WHATIF")) : 0;
+#else
+  constexpr int whatif = 0;
+#endif
   if (la && !in_graph) {
     cuda_check(cudaEventRecord(ev_fork_, stream_), "record");
     cuda_check(cudaStreamWaitEvent(sa, ev_fork_, 0), "wait");

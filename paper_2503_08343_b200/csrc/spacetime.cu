@@ -365,7 +365,10 @@ SpaceTimePosterior::SpaceTimePosterior(const SpaceTimeSpec& spec, cudaStream_t s
   times_.assemble_ms = now_ms() - t0;
 }
 
-SpaceTimePosterior::~SpaceTimePosterior() = default;
+SpaceTimePosterior::~SpaceTimePosterior() {
+  for (cudaEvent_t e : ev_)
+    if (e) cudaEventDestroy(e);
+}
 
 void SpaceTimePosterior::build_host() {
   require(spec_.n_el >= 2 && spec_.n_t >= 2, kContract, "spacetime: need >= 2 elements and slices");
@@ -729,7 +732,8 @@ std::vector<GnIter> SpaceTimePosterior::run(const double* u0, const GnConfig& cf
   require(cfg.decrement_tol > 0.0, kContract, "gauss-newton: decrement_tol must be positive");
   require(cfg.armijo_c > 0.0 && cfg.armijo_c < 1.0, kContract, "gauss-newton: armijo constant in (0,1)");
   require(cfg.shrink > 0.0 && cfg.shrink < 1.0, kContract, "gauss-newton: shrink factor in (0,1)");
-  std::vector<GnIter> trace;
+  std::vector<GnIter>& trace = trace_;
+  trace.clear();
   converged_ = false;
   {
     const double setup = times_.setup_host_ms, init = times_.assemble_ms;
@@ -737,9 +741,9 @@ std::vector<GnIter> SpaceTimePosterior::run(const double* u0, const GnConfig& cf
     times_.setup_host_ms = setup;
     times_.init_ms = init;
   }
-  cudaEvent_t e0, e1;
-  cudaEventCreate(&e0);
-  cudaEventCreate(&e1);
+  if (!ev_[0])
+    for (cudaEvent_t& e : ev_) cuda_check(cudaEventCreate(&e), "event");
+  cudaEvent_t e0 = ev_[0], e1 = ev_[1];
   auto phase = [&](double& acc, auto&& body) {
     cudaEventRecord(e0, stream_);
     body();
@@ -750,9 +754,7 @@ std::vector<GnIter> SpaceTimePosterior::run(const double* u0, const GnConfig& cf
     acc += ms;
   };
   auto factor_now = [&](const char* what) {
-    cudaEvent_t a, b;
-    cudaEventCreate(&a);
-    cudaEventCreate(&b);
+    cudaEvent_t a = ev_[2], b = ev_[3];
     cudaEventRecord(a, stream_);
     int32_t bad = fac_->factor_panels();
     cudaEventRecord(b, stream_);
@@ -762,8 +764,6 @@ std::vector<GnIter> SpaceTimePosterior::run(const double* u0, const GnConfig& cf
     times_.numeric_ms += ms;
     times_.n_factorizations += 1;
     times_.kernel_launches += fac_->launches_numeric();
-    cudaEventDestroy(a);
-    cudaEventDestroy(b);
     if (bad >= 0)
       throw Error(kNotSpd, std::string(what) + ": cholesky: non-positive pivot at index " +
                                std::to_string(bad));
@@ -793,8 +793,6 @@ std::vector<GnIter> SpaceTimePosterior::run(const double* u0, const GnConfig& cf
         fac_->selinv(var_.p, true);
         times_.kernel_launches += fac_->launches_selinv();
       });
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
     return trace;
   }
 
@@ -876,8 +874,6 @@ std::vector<GnIter> SpaceTimePosterior::run(const double* u0, const GnConfig& cf
       fac_->selinv(var_.p, true);
       times_.kernel_launches += fac_->launches_selinv();
     });
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
   return trace;
 }
 

@@ -91,6 +91,9 @@ class SpaceTimePosterior {
   const double* d_mean_cond() const { return mean_cond_.p; }
   const PhaseTimes& times() const { return times_; }
   bool converged() const { return converged_; }
+  // trace of the last run, complete also when it ended in a throw (line-search
+  // stagnation: GaussNewtonStagnation carries it, gauss_newton.hpp:208-214)
+  const std::vector<GnIter>& last_trace() const { return trace_; }
   // Master pattern and the assembled values (tests)
   void copy_pattern(std::vector<i64>& cp, std::vector<i32>& ri) const;
   void copy_values(std::vector<double>& qcond, std::vector<double>& qeff) const;
@@ -126,6 +129,8 @@ class SpaceTimePosterior {
 
  private:
   bool converged_ = false;
+  std::vector<GnIter> trace_;
+  cudaEvent_t ev_[4] = {};  // phase (0, 1) and factorization (2, 3) timing, reused
 
   // host patterns
   std::vector<i64> pcp_;

@@ -20,7 +20,9 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
+#include <cstring>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -51,19 +53,56 @@ inline std::vector<int64_t> colptr64(const SparseMatrixCSC& q) {
   return std::vector<int64_t>(q.col_ptr.begin(), q.col_ptr.end());
 }
 
+// Device factors of a symbolic are pooled: a CholeskyFactor that goes out of
+// scope hands its device storage (panels, plans, captured CUDA graph) back to
+// its SymbolicFactor, and the next cholesky_refactor of that symbolic reuses it
+// (gauss_newton.hpp:139-140 refactors once per iteration on one symbolic).
 struct SymbolicHandle {
   gmrf_symbolic_t* h = nullptr;
   std::vector<int64_t> cp;
   std::vector<Index> ri;
+  std::mutex mu;
+  std::vector<gmrf_factor_t*> pool;
   ~SymbolicHandle() {
+    for (gmrf_factor_t* f : pool) gmrf_factor_free(f);
     if (h) gmrf_symbolic_free(h);
+  }
+  gmrf_factor_t* acquire() {
+    {
+      std::lock_guard<std::mutex> g(mu);
+      if (!pool.empty()) {
+        gmrf_factor_t* f = pool.back();
+        pool.pop_back();
+        return f;
+      }
+    }
+    gmrf_factor_t* f = nullptr;
+    const int rc = gmrf_factor_create(h, &f);
+    if (rc != GMRF_OK) raise(rc);
+    return f;
+  }
+  void release(gmrf_factor_t* f) {
+    std::lock_guard<std::mutex> g(mu);
+    pool.push_back(f);
+  }
+  // the reference re-permutes q on every refactor (cholesky.hpp:117); here the
+  // values are consumed in the analysed CSC order, so the pattern must match
+  bool same_pattern(const SparseMatrixCSC& q) const {
+    if (static_cast<int64_t>(q.col_ptr.size()) != static_cast<int64_t>(cp.size()) ||
+        q.row_idx.size() != ri.size() || q.values.size() != ri.size())
+      return false;
+    for (std::size_t j = 0; j < cp.size(); ++j)
+      if (static_cast<int64_t>(q.col_ptr[j]) != cp[j]) return false;
+    return ri.empty() || std::memcmp(q.row_idx.data(), ri.data(), ri.size() * sizeof(Index)) == 0;
   }
 };
 struct FactorHandle {
   gmrf_factor_t* h = nullptr;
   std::shared_ptr<SymbolicHandle> sym;
   ~FactorHandle() {
-    if (h) gmrf_factor_free(h);
+    if (!h) return;
+    if (sym) sym->release(h);
+    else gmrf_factor_free(h);
   }
 };
 
@@ -133,9 +172,11 @@ struct CholeskyFactor {
 inline CholeskyFactor cholesky_refactor(const SymbolicFactor& s, const SparseMatrixCSC& q) {
   const Index n = s.n;
   if (q.nrows != n || q.ncols != n) throw DimensionError("cholesky_refactor: dimension mismatch");
+  if (!s.handle->same_pattern(q))
+    throw StructuralError("cholesky_refactor: sparsity pattern differs from the analysed one");
   auto fh = std::make_shared<b200::FactorHandle>();
   fh->sym = s.handle;
-  b200::check(gmrf_factor_create(s.handle->h, &fh->h));
+  fh->h = s.handle->acquire();
   int32_t bad = -1;
   const int rc = gmrf_factor_numeric(fh->h, q.values.data(), &bad);
   if (rc != GMRF_OK) b200::raise(rc, bad);

@@ -1,0 +1,102 @@
+"""Generates the BASELINE-size golden fixtures from the REFERENCE itself.
+
+TEST INFRASTRUCTURE. Runs the unmodified reference (oracle/_ref/libgmrfref.so,
+the /root/reference headers compiled by oracle/Makefile) single-threaded on the
+seeded inputs of SURVEY §8(d), once, in the build container (hours for C4: the
+reference's AMD factorization is ~190 s per GN step and its Takahashi pass
+~3-4 h), and stores only the vectors the GPU tests compare against:
+
+  c4_burgers_full.npz   C4 999 elements x 1000 slices (n = 1e6): 10-step GN
+                        trace (objective, decrement, step, backtracks), mode,
+                        Laplace Takahashi variances, reference stage timings.
+  c3_heat_full.npz      C3 499 x 1000 (n = 500,000): IC-conditioned mean and
+                        Takahashi variances, timings.
+  c5_allen_cahn_<k>.npz C5 shape at k^2 nodes x (2k) slices (k = 16, 32): 8-step
+                        GN trace, mode, variances, timings (k = 32 is n = 65,536,
+                        the largest the reference's int32 nnz(L) survives).
+  c4_burgers_200.npz    C4 shape at 199 x 200 with the full 10-step GN budget.
+
+Usage: python tests/golden/make_golden_full.py c4 | c3 | c5_16 | c5_32 | c4_200
+Each run writes its fixture atomically (tmp + rename) plus a .log with timings.
+"""
+from __future__ import annotations
+
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.abspath(os.path.join(HERE, "..", "..")))
+
+from oracle.pyoracle import Ref  # noqa: E402
+
+TIMERS = ["t_prior", "t_condition", "t_gn", "t_laplace_build", "t_variance"]
+
+
+def _save(name, out, b, t_wall):
+    times = {}
+    for k in TIMERS:
+        try:
+            times[k] = float(b.scalar(k))
+        except Exception:  # stage not run for this config
+            pass
+    times["t_wall"] = t_wall
+    out["ref_times_json"] = np.array(json.dumps(times))
+    tmp = os.path.join(HERE, name + ".tmp.npz")
+    np.savez_compressed(tmp, **out)
+    os.replace(tmp, os.path.join(HERE, name))
+    print(name, json.dumps(times), flush=True)
+
+
+def burgers(n_el, n_t, gn_iters, name):
+    # make_golden.spatiotemporal parameter layout (oracle/ref_capi.cpp:147-149)
+    p = [1, n_el, -1.0, 1.0, n_t, 1.0, 0.01 / np.pi, 0.5, 10, 1, 1, 10, 2, 1, 1.0, 1e-10, 1e8,
+         0, 1e12, gn_iters, 1, 1]
+    t0 = time.time()
+    b = Ref().build("spatiotemporal", p)
+    out = {"params": np.array(p, np.float64)}
+    for k in ["mean_cond", "mode", "mean_post", "var_post", "gn_objective", "gn_decrement",
+              "gn_step", "gn_backtracks"]:
+        out[k] = b.vec(k)
+    out["gn_converged"] = np.array(b.scalar("gn_converged"))
+    _save(name, out, b, time.time() - t0)
+
+
+def heat(n_el, n_t, name):
+    p = [0, n_el, 0.0, 1.0, n_t, 1.0, 0.1, 0.0, 10, 1, 1, 10, 2, 1, 1.0, 1e-10, 1e6, 1003,
+         0, 0, 1, 0]
+    t0 = time.time()
+    b = Ref().build("spatiotemporal", p)
+    out = {"params": np.array(p, np.float64)}
+    for k in ["y_ic", "mean_post", "var_post"]:
+        out[k] = b.vec(k)
+    _save(name, out, b, time.time() - t0)
+
+
+def allen_cahn(n_cells, n_t, name, gn_iters=8):
+    p = [n_cells, n_t, 0.5, 0.0025, 10, 1, 1, 10, 2, 1, 1.0, 1e6, 1005, 1e12, gn_iters, 1, 1, 1]
+    t0 = time.time()
+    b = Ref().build("allen_cahn", p)
+    out = {"params": np.array(p, np.float64), "fd_rel_err": np.array([b.scalar("fd_rel_err")])}
+    for k in ["u0", "mean_cond", "mode", "mean_post", "var_post", "gn_objective",
+              "gn_decrement", "gn_step", "gn_backtracks"]:
+        out[k] = b.vec(k)
+    out["gn_converged"] = np.array(b.scalar("gn_converged"))
+    _save(name, out, b, time.time() - t0)
+
+
+JOBS = {
+    "c4": lambda: burgers(999, 1000, 10, "c4_burgers_full.npz"),
+    "c4_200": lambda: burgers(199, 200, 10, "c4_burgers_200.npz"),
+    "c4_500": lambda: burgers(499, 500, 10, "c4_burgers_500.npz"),
+    "c3": lambda: heat(499, 1000, "c3_heat_full.npz"),
+    "c5_16": lambda: allen_cahn(15, 32, "c5_allen_cahn_16.npz"),
+    "c5_32": lambda: allen_cahn(31, 64, "c5_allen_cahn_32.npz"),
+}
+
+if __name__ == "__main__":
+    for job in sys.argv[1:]:
+        JOBS[job]()

@@ -155,3 +155,19 @@ def test_allen_cahn_gn_laplace_vs_reference(port):
     floor, _ = ordering_floor(port, qla, qla @ z["mode"])
     assert rel(mean, z["mode"]) <= max(100 * floor, 1e-8), (rel(mean, z["mode"]), floor)
     assert rel(var, z["var_post"]) <= 1e-6
+
+
+def test_gn_stagnation_carries_trace():
+    """GaussNewtonStagnation(msg, trace) (gauss_newton.hpp:208-214): with no
+    backtracks allowed, the reference's first C4 step (step 0.25 at 20x20) fails
+    the Armijo test; the exception carries the trace up to that iteration."""
+    from paper_2503_08343_b200.spacetime import GaussNewtonConfig, GaussNewtonStagnation
+    z = load_golden("c4_burgers_20x20.npz")
+    p = z["params"]
+    assert z["gn_backtracks"][0] > 0
+    post = SpaceTimePosterior(spec_from(p), GaussNewtonConfig(max_iters=4, max_backtracks=0))
+    with pytest.raises(GaussNewtonStagnation) as ei:
+        post.run(z["y_ic"], variances=False)
+    tr = ei.value.trace()
+    assert len(tr) == 1 and tr[0].iter == 1
+    assert abs(tr[0].objective - z["gn_objective"][0]) <= 1e-6 * abs(z["gn_objective"][0])
