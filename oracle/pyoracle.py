@@ -18,6 +18,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 PORT_SO = os.path.join(HERE, "_build", "liboracle.so")
 REF_SO = os.path.join(HERE, "_ref", "libgmrfref.so")
+REF_ND_SO = os.path.join(HERE, "_ref", "libgmrfref_nd.so")
 
 i32p = C.POINTER(C.c_int32)
 i64p = C.POINTER(C.c_int64)
@@ -103,8 +104,11 @@ class Ref:
     def available() -> bool:
         return os.path.exists(REF_SO)
 
-    def __init__(self):
-        lib = C.CDLL(REF_SO)
+    def __init__(self, so: str = REF_SO):
+        """so: REF_SO, or REF_ND_SO — the ordering-floor probe build (the chain's AMD
+        redirected to METIS nested dissection, oracle/ref_capi.cpp); load one per
+        process."""
+        lib = C.CDLL(so)
         lib.ref_last_error.restype = C.c_char_p
         lib.ref_build.restype = C.c_void_p
         lib.ref_build.argtypes = [C.c_char_p, f64p, C.c_int]

@@ -27,6 +27,43 @@
 #include "gmrfpde/core/rng.hpp"
 #include "gmrfpde/core/sparse.hpp"
 #include "gmrfpde/core/takahashi.hpp"
+
+#ifdef GMRF_ORDERING_PROBE
+// Ordering-floor probe build (oracle/_ref/libgmrfref_nd.so, same source): the
+// unmodified reference headers with the fill-reducing ordering that the chain
+// uses — amd_order in gauss_newton.hpp:139 and the AMD inside
+// cholesky_factor(q) at gmrf.hpp:55,160 — redirected to METIS nested
+// dissection. The reference's own algorithms then run with another elimination
+// order; how far their outputs move (tests/golden/make_golden_full.py floor:*)
+// is the reference's FP64 ordering floor, SURVEY §8(c).
+extern "C" int METIS_NodeND(int64_t* nvtxs, int64_t* xadj, int64_t* adjncy, int64_t* vwgt,
+                            int64_t* options, int64_t* perm, int64_t* iperm);
+namespace gmrfpde {
+inline std::vector<Index> nd_probe_order(const SparseMatrixCSC& a) {
+  const int64_t n = a.ncols;
+  std::vector<int64_t> xadj(n + 1, 0), adj;
+  for (Index j = 0; j < a.ncols; ++j) {
+    for (Index p = a.col_ptr[j]; p < a.col_ptr[j + 1]; ++p)
+      if (a.row_idx[p] != j) adj.push_back(a.row_idx[p]);
+    xadj[j + 1] = static_cast<int64_t>(adj.size());
+  }
+  std::vector<int64_t> perm(n), iperm(n);
+  int64_t nv = n;
+  if (METIS_NodeND(&nv, xadj.data(), adj.data(), nullptr, nullptr, perm.data(), iperm.data()) != 1)
+    throw NumericalError("METIS_NodeND failed");
+  return std::vector<Index>(perm.begin(), perm.end());  // new -> old, as amd_order
+}
+inline CholeskyFactor cholesky_factor_probe(const SparseMatrixCSC& q) {
+  return cholesky_factor(q, nd_probe_order(q));
+}
+inline CholeskyFactor cholesky_factor_probe(const SparseMatrixCSC& q, const std::vector<Index>& p) {
+  return cholesky_factor(q, p);
+}
+}  // namespace gmrfpde
+#define amd_order nd_probe_order
+#define cholesky_factor cholesky_factor_probe
+#endif
+
 #include "gmrfpde/fem/assembly.hpp"
 #include "gmrfpde/fem/constraints.hpp"
 #include "gmrfpde/fem/mesh.hpp"
@@ -64,6 +101,25 @@ SparseMatrixCSC make_csc(int n_rows, int n_cols, const int* cp, const int* ri, c
   m.row_idx.assign(ri, ri + cp[n_cols]);
   m.values.assign(v, v + cp[n_cols]);
   return m;
+}
+
+// FP64 floor probe (SURVEY §8(c) "floor2"): multiply every input value by
+// (1 ± 2⁻⁵²), signs from Rng(seed); seed 0 leaves the input untouched. Running the
+// unmodified reference chain on perturbed inputs (initial condition, prior
+// precision — re-symmetrized — and prior square root) measures how far its own
+// outputs move under one ulp of input noise: the tolerance scale for GPU parity
+// (the device assembles Q and q_eff in a different operation order).
+void ulp_perturb(Vector& v, double seed) {
+  if (seed == 0.0) return;
+  Rng r(static_cast<std::uint64_t>(seed));
+  for (double& x : v) x *= (r.uniform() < 0.5 ? 1.0 - 0x1p-52 : 1.0 + 0x1p-52);
+}
+Gmrf ulp_perturb_prior(const Gmrf& g, double seed) {
+  if (seed == 0.0) return g;
+  SparseMatrixCSC q = g.precision(), s = g.sqrt();
+  ulp_perturb(q.values, seed + 1);
+  ulp_perturb(s.values, seed + 2);
+  return Gmrf(g.mean(), symmetrize(q), std::move(s));
 }
 
 // Fixed-step GN trace → flat vectors.
@@ -146,7 +202,8 @@ Bundle* build_matern(int dim, const double* p, int np) {
 // ----- spatiotemporal prior (+ IC conditioning, + Burgers GN-Laplace) --------
 // p: [kind(0 heat, 1 burgers), n_el, x_a, x_b, n_t, t_end, nu, c, noise_kappa,
 //     noise_alpha, noise_tau, init_kappa, init_alpha, init_tau, tau, eps,
-//     ic_noise_prec, ic_seed, pde_noise_prec, gn_max_iters, do_variance, do_gn]
+//     ic_noise_prec, ic_seed, pde_noise_prec, gn_max_iters, do_variance, do_gn,
+//     prior_only, floor_seed]
 Bundle* build_spatiotemporal(const double* p, int np) {
   (void)np;
   int kind = static_cast<int>(p[0]);
@@ -186,6 +243,10 @@ Bundle* build_spatiotemporal(const double* p, int np) {
     }
   } else {
     for (int d = 0; d < n; ++d) u0[d] = -std::sin(M_PI * space.dof_x(d));
+  }
+  if (np > 23) {  // p[23]: floor-probe seed (0: off)
+    ulp_perturb(u0, p[23]);
+    flat = ulp_perturb_prior(flat, p[23]);
   }
   std::vector<Real> ic_points(n);
   for (int d = 0; d < n; ++d) ic_points[d] = space.dof_x(d);
@@ -306,7 +367,7 @@ solver::NonlinearResidual allen_cahn_residual(const fem::FeSpace& space, const V
 // ----- C5-shaped space-time Allen-Cahn GN-Laplace on the unit square ----------
 // p: [n_per_dim, n_t, t_end, eps2, noise_kappa, noise_alpha, noise_tau,
 //     init_kappa, init_alpha, init_tau, tau, ic_noise_prec, ic_seed,
-//     pde_noise_prec, gn_max_iters, do_variance, do_gn, fd_check]
+//     pde_noise_prec, gn_max_iters, do_variance, do_gn, fd_check, floor_seed]
 Bundle* build_allen_cahn(const double* p, int np) {
   (void)np;
   const int npd = static_cast<int>(p[0]);
@@ -333,6 +394,10 @@ Bundle* build_allen_cahn(const double* p, int np) {
   Rng rng(static_cast<std::uint64_t>(p[12]));
   Vector u0(n);
   for (int d = 0; d < n; ++d) u0[d] = -0.1 + 0.2 * rng.uniform();
+  if (np > 18) {  // p[18]: floor-probe seed (0: off)
+    ulp_perturb(u0, p[18]);
+    flat = ulp_perturb_prior(flat, p[18]);
+  }
   b->vecs["u0"] = u0;
   std::vector<Triplet> ic;  // P1 nodes = DoFs: point evaluation at the nodes
   for (int d = 0; d < n; ++d) ic.push_back({d, d, 1.0});

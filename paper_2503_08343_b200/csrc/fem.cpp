@@ -149,11 +149,14 @@ Csc diagonal(const std::vector<double>& d) {
 
 // P1 element matrices in closed form (quadrature-exact for degree 2 rules,
 // assembly.hpp:82-83,107): mass h/6·[[2,1],[1,2]], stiffness diff/h·[[1,-1],[-1,1]],
-// advection c/2·[[-1,1],[-1,1]] (∫ φ_i c φ'_j).
+// advection c/2·[[-1,1],[-1,1]] (∫ φ_i c φ'_j). h is each element's own length
+// from the node coordinates (mesh.hpp:44-46, 63-70): the nodes are rounded, so
+// element lengths differ by ulps of the coordinates — relative 1e-13 of h at
+// 1000 elements, which the ill-conditioned space-time precisions amplify.
 Csc p1_mass(const Space1D& s) {
   std::vector<Trip> t;
-  const double h = s.h();
   for (i32 e = 0; e < s.n_el; ++e) {
+    const double h = s.x(e + 1) - s.x(e);
     const double d = h / 3.0, o = h / 6.0;
     t.push_back({e, e, d});
     t.push_back({e + 1, e, o});
@@ -165,8 +168,8 @@ Csc p1_mass(const Space1D& s) {
 
 Csc p1_stiffness(const Space1D& s, double diff, double adv, double react) {
   std::vector<Trip> t;
-  const double h = s.h();
   for (i32 e = 0; e < s.n_el; ++e) {
+    const double h = s.x(e + 1) - s.x(e);
     double loc[2][2];
     for (int i = 0; i < 2; ++i)
       for (int j = 0; j < 2; ++j) {
@@ -188,11 +191,10 @@ namespace {
 template <typename F>
 void for_each_triangle(const Space2D& s, F&& f) {
   const i32 nc = s.n_cells, side = s.side();
-  const double h = s.h();
   for (i32 iy = 0; iy < nc; ++iy)
     for (i32 ix = 0; ix < nc; ++ix) {
       const i32 v00 = iy * side + ix, v10 = v00 + 1, v11 = v00 + side + 1, v01 = v00 + side;
-      const double x0 = ix * h, y0 = iy * h, x1 = (ix + 1) * h, y1 = (iy + 1) * h;
+      const double x0 = s.coord(ix), y0 = s.coord(iy), x1 = s.coord(ix + 1), y1 = s.coord(iy + 1);
       const i32 t0[3] = {v00, v10, v11}, t1[3] = {v00, v11, v01};
       const double p0[3][2] = {{x0, y0}, {x1, y0}, {x1, y1}};
       const double p1[3][2] = {{x0, y0}, {x1, y1}, {x0, y1}};

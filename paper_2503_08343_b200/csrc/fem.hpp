@@ -51,7 +51,10 @@ struct Space1D {
   double xa, xb;
   i32 n() const { return n_el + 1; }
   double h() const { return (xb - xa) / n_el; }
-  double x(i32 d) const { return d == n_el ? xb : xa + (xb - xa) * d / n_el; }
+  // node coordinate (build_interval_mesh, mesh.hpp:63-70)
+  double x(i32 d) const {
+    return d == n_el ? xb : xa + (xb - xa) * static_cast<double>(d) / static_cast<double>(n_el);
+  }
 };
 
 Csc p1_mass(const Space1D& s);
@@ -65,6 +68,8 @@ struct Space2D {
   i32 side() const { return n_cells + 1; }
   i32 n() const { return side() * side(); }
   double h() const { return 1.0 / n_cells; }
+  // axis coordinate i/n (build_unit_square_mesh, mesh.hpp:142-147)
+  double coord(i32 i) const { return static_cast<double>(i) / static_cast<double>(n_cells); }
 };
 Csc p1_mass(const Space2D& s);
 Csc p1_laplace(const Space2D& s);  // ∫ ∇φ_i · ∇φ_j

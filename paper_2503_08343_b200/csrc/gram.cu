@@ -1,0 +1,156 @@
+// Fixed-pattern weighted Gram update (gram.hpp).
+#include "gram.hpp"
+
+#include <algorithm>
+#include <string>
+
+namespace gmrf {
+
+namespace {
+
+// wa = w[row] · a  (scale_rows, core/sparse.hpp)
+__global__ void k_gram_weight(i64 na, const i32* __restrict__ arow, const double* __restrict__ w,
+                              const double* __restrict__ a, double* __restrict__ wa) {
+  for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < na;
+       i += static_cast<i64>(gridDim.x) * blockDim.x)
+    wa[i] = w[arow[i]] * a[i];
+}
+
+// One thread per computed entry; pairs (x, y) = (A_kR, A_kC) value indices,
+// ascending k. s1 is the (R, C) product, s2 the (C, R) one; their average
+// with the base is the reference's symmetrize(add(base, c·AᵀWA)).
+__global__ void k_gram(i64 ne, const i64* __restrict__ ent, const i64* __restrict__ off,
+                       const int2* __restrict__ pairs, const double* __restrict__ a,
+                       const double* __restrict__ wa, double c, const double* __restrict__ base,
+                       double* __restrict__ out, const i64* __restrict__ qmap,
+                       double* __restrict__ L) {
+  for (i64 t = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; t < ne;
+       t += static_cast<i64>(gridDim.x) * blockDim.x) {
+    const i64 p = ent ? ent[t] : t;
+    double s1 = 0.0, s2 = 0.0;
+    const i64 k1 = off[t + 1];
+    for (i64 k = off[t]; k < k1; ++k) {
+      const int2 xy = pairs[k];
+      const double ax = a[xy.x], ay = a[xy.y];
+      s1 += ax * wa[xy.y];
+      s2 += ay * wa[xy.x];
+    }
+    const double b = base ? base[p] : 0.0;
+    const double v = 0.5 * (b + c * s1) + 0.5 * (b + c * s2);
+    if (out) out[p] = v;
+    if (L) {
+      const i64 o = qmap[p];
+      if (o >= 0) L[o] = v;
+    }
+  }
+}
+
+int grid_of(i64 n) {
+  return static_cast<int>(std::max<i64>(1, std::min<i64>((n + 255) / 256, 148 * 16)));
+}
+
+}  // namespace
+
+GramPlan::GramPlan(i32 n, const i64* pcp, const i32* pri, i32 m, const i64* arp, const i32* aci,
+                   const std::vector<char>* need, cudaStream_t stream) {
+  m_ = m;
+  np_ = pcp[n];
+  na_ = arp[m];
+  // A by columns: (row k, CSR value index), rows ascending
+  std::vector<i64> acp(static_cast<size_t>(n) + 1, 0);
+  for (i64 i = 0; i < na_; ++i) {
+    require(aci[i] >= 0 && aci[i] < n, kDimension, "gram: operator column out of range");
+    acp[aci[i] + 1]++;
+  }
+  for (i32 j = 0; j < n; ++j) acp[j + 1] += acp[j];
+  std::vector<i32> ak(na_);
+  std::vector<i32> av(na_);
+  std::vector<i32> arow(na_);
+  {
+    std::vector<i64> nx(acp.begin(), acp.end() - 1);
+    for (i32 k = 0; k < m; ++k)
+      for (i64 i = arp[k]; i < arp[k + 1]; ++i) {
+        require(i == arp[k] || aci[i] > aci[i - 1], kStructural,
+                "gram: operator columns must be strictly ascending per row");
+        const i64 q = nx[aci[i]]++;
+        ak[q] = k;
+        av[q] = static_cast<i32>(i);
+        arow[i] = k;
+      }
+  }
+  require(na_ < (1ll << 31), kContract, "gram: operator nnz exceeds int32 value indices");
+  // product map over the computed entries
+  std::vector<i64> ent, off(1, 0);
+  std::vector<int2> pr;
+  i64 covered = 0;
+  for (i32 C = 0; C < n; ++C)
+    for (i64 p = pcp[C]; p < pcp[C + 1]; ++p) {
+      const i32 R = pri[p];
+      const bool want = !need || (*need)[p];
+      i64 x = acp[R], xe = acp[R + 1], y = acp[C], ye = acp[C + 1];
+      i64 cnt = 0;
+      while (x < xe && y < ye) {
+        if (ak[x] < ak[y]) {
+          ++x;
+        } else if (ak[y] < ak[x]) {
+          ++y;
+        } else {
+          if (want) pr.push_back(make_int2(av[x], av[y]));
+          ++cnt;
+          ++x;
+          ++y;
+        }
+      }
+      covered += cnt;
+      if (want) {
+        if (need) ent.push_back(p);
+        off.push_back(static_cast<i64>(pr.size()));
+      }
+    }
+  // every product A_kR A_kC must have a home in the pattern
+  i64 total = 0;
+  for (i32 k = 0; k < m; ++k) total += (arp[k + 1] - arp[k]) * (arp[k + 1] - arp[k]);
+  require(covered == total, kStructural,
+          "gram: pattern does not contain the operator's product pattern (" +
+              std::to_string(covered) + " of " + std::to_string(total) + " products)");
+  npairs_ = static_cast<i64>(pr.size());
+  off_.upload(off, stream);
+  pairs_.upload(pr, stream);
+  arow_.upload(arow, stream);
+  wa_.alloc(std::max<i64>(na_, 1));
+  if (need) {
+    ent_.upload(ent, stream);
+    ne_ = static_cast<i64>(ent.size());
+  } else {
+    ne_ = np_;
+  }
+  cuda_check(cudaStreamSynchronize(stream), "gram plan upload");
+}
+
+void GramPlan::apply(const double* d_a, const double* d_w, double c, const double* d_base,
+                     double* d_out, const i64* d_qmap, double* d_L, cudaStream_t stream) {
+  const double* wa = d_a;
+  if (d_w && na_ > 0) {
+    k_gram_weight<<<grid_of(na_), 256, 0, stream>>>(na_, arow_.p, d_w, d_a, wa_.p);
+    wa = wa_.p;
+  }
+  if (ne_ > 0)
+    k_gram<<<grid_of(ne_), 256, 0, stream>>>(ne_, ent_.p, off_.p, pairs_.p, d_a, wa, c, d_base,
+                                             d_out, d_qmap, d_L);
+  cuda_check(cudaGetLastError(), "gram apply");
+}
+
+int GramPlan::launches(bool weighted) const { return (weighted && na_ > 0 ? 1 : 0) + (ne_ > 0); }
+
+double GramPlan::bytes(bool base, bool out, bool panels) const {
+  // A values (+ weights / scaled copy) once, offsets, pairs, entry list, base,
+  // outputs, map
+  double b = 16.0 * na_ + 8.0 * (ne_ + 1) + 8.0 * npairs_;
+  if (ne_ != np_) b += 8.0 * ne_;
+  if (base) b += 8.0 * ne_;
+  if (out) b += 8.0 * ne_;
+  if (panels) b += 16.0 * ne_;
+  return b;
+}
+
+}  // namespace gmrf

@@ -31,85 +31,54 @@ __device__ __forceinline__ double blk_at(const BlkDev& b, int k, int i, int j) {
   return (lo < cp[j + 1] && b.ri[lo] == i) ? b.v[lo] : 0.0;
 }
 
-// Joint value of the space-time precision at (R, C) before symmetrization,
-// spatiotemporal.hpp:144-155 (Q set) or the same blocks rebuilt through the
-// square root (q_eff set, gauss_newton.hpp:110-114).
-__device__ __forceinline__ double st_entry(const BlkDev& b, bool qeff, int sr, int a, int sc, int c,
-                                           int nt, double t) {
+// Joint value of the space-time precision at (R, C) before symmetrization:
+// the triplets spatiotemporal.hpp:112-156 appends, with the per-step
+// T_s = 1/(Δt_s τ²): slice s's diagonal block collects T_{s-1}·C_gg (step s−1)
+// and T_s·C_mm (step s) (slice 0: Q1 + T_0·C_mm), the off-diagonal blocks
+// (−T_s)·C_mg and its transpose. Two terms per entry at most, so the sum is
+// order-independent.
+__device__ __forceinline__ double st_entry(const BlkDev& b, const double* T, int sr, int a, int sc,
+                                           int c, int nt) {
   if (sr == sc) {
     double v = 0.0;
-    if (!qeff) {
-      if (sr < nt - 1) v += t * blk_at(b, kBlkCmm, a, c);
-      if (sr >= 1) v += t * blk_at(b, kBlkCgg, a, c);
-      if (sr == 0) v += blk_at(b, kBlkQ1, a, c);
-    } else {
-      if (sr == 0) v += blk_at(b, kBlkGl1, a, c);
-      if (sr >= 1) v += t * blk_at(b, kBlkGff, a, c);
-      if (sr < nt - 1) v += t * blk_at(b, kBlkGmm, a, c);
-    }
+    if (sr < nt - 1) v += T[sr] * blk_at(b, kBlkCmm, a, c);
+    if (sr >= 1) v += T[sr - 1] * blk_at(b, kBlkCgg, a, c);
+    if (sr == 0) v += blk_at(b, kBlkQ1, a, c);
     return v;
   }
-  if (sc == sr + 1) return -t * blk_at(b, qeff ? kBlkGmf : kBlkCmg, a, c);
-  if (sr == sc + 1) return -t * blk_at(b, qeff ? kBlkGmf : kBlkCmg, c, a);
+  if (sc == sr + 1) return (-T[sr]) * blk_at(b, kBlkCmg, a, c);
+  if (sr == sc + 1) return (-T[sc]) * blk_at(b, kBlkCmg, c, a);
   return 0.0;
 }
 
-// Row 1: assembly of Q_cond = sym(Q_prior) + AᵀΛA and q_eff = sym(S Sᵀ) on the
-// master pattern, one thread per joint column. Slack (constrained) coordinates
-// carry only 1/ε² on the diagonal (spatiotemporal.hpp:248-266); the IC
-// observation A = I on slice 0 adds Λ_ic on that slice's diagonal.
+// Row 1: assembly of Q_cond = sym(Q_prior) + AᵀΛA on the master pattern, one
+// thread per joint column (q_eff = sym(S Sᵀ) is a GramPlan product). Slack
+// (constrained) coordinates carry only 1/ε on the diagonal
+// (spatiotemporal.hpp:166-183); the IC observation A = I on slice 0 adds Λ_ic
+// on that slice's diagonal.
 __global__ void k_st_assemble(const i64* __restrict__ pcp, const i32* __restrict__ pri, int N,
-                              int ns, int nt, double t, double inv_eps, double ic_prec,
-                              const char* __restrict__ slack, BlkDev b, double* __restrict__ qcond,
-                              double* __restrict__ qeff) {
+                              int ns, int nt, const double* __restrict__ T, double inv_eps,
+                              double ic_prec, const char* __restrict__ slack, BlkDev b,
+                              double* __restrict__ qcond) {
   for (int C = blockIdx.x * blockDim.x + threadIdx.x; C < N; C += gridDim.x * blockDim.x) {
     const int sc = C / ns, c = C - sc * ns;
     for (i64 p = pcp[C]; p < pcp[C + 1]; ++p) {
       const int R = pri[p];
       const int sr = R / ns, a = R - sr * ns;
-      double vq, ve;
+      double vq;
       if (slack[a] || slack[c]) {
-        vq = ve = (R == C) ? inv_eps : 0.0;
+        vq = (R == C) ? inv_eps : 0.0;
       } else {
-        vq = 0.5 * st_entry(b, false, sr, a, sc, c, nt, t) + 0.5 * st_entry(b, false, sc, c, sr, a, nt, t);
-        ve = 0.5 * st_entry(b, true, sr, a, sc, c, nt, t) + 0.5 * st_entry(b, true, sc, c, sr, a, nt, t);
+        vq = 0.5 * st_entry(b, T, sr, a, sc, c, nt) + 0.5 * st_entry(b, T, sc, c, sr, a, nt);
       }
-      if (R == C && sr == 0) {
-        vq += ic_prec;
-        ve += ic_prec;
-      }
+      if (R == C && sr == 0) vq += ic_prec;
       qcond[p] = vq;
-      qeff[p] = ve;
     }
   }
 }
 
-// Row 2: fixed-pattern update written straight into the supernodal panels,
-//   L[qmap[p]] = base[p] + Σ_{r ∈ col_J(R) ∩ col_J(C)} λ J_rR J_rC
-// (gauss_newton.hpp:137-138, :231-232). The JᵀΛJ entry is a merge of two
-// sorted J columns: no atomics, fixed summation order.
-// JᵀΛJ through a precomputed product map: for master-pattern entry p (lower
-// half only), pairs [off[p], off[p+1]) are the J value indices of the rows
-// shared by J columns R and C, ascending — the same terms in the same order as
-// the merge in k_fill_panels, so the result is bit-identical, without the
-// dependent index chasing.
-__global__ void k_fill_panels_map(i64 np, const i64* __restrict__ qmap,
-                                  const double* __restrict__ base, const i32* __restrict__ off,
-                                  const int2* __restrict__ pairs, const double* __restrict__ jv,
-                                  double lam, double* __restrict__ L) {
-  for (i64 p = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; p < np;
-       p += static_cast<i64>(gridDim.x) * blockDim.x) {
-    const i64 o = qmap[p];
-    if (o < 0) continue;
-    double s = 0.0;
-    for (i32 k = off[p]; k < off[p + 1]; ++k) {
-      const int2 ab = pairs[k];
-      s += lam * jv[ab.x] * jv[ab.y];
-    }
-    L[o] = base[p] + s;
-  }
-}
-
+// Conditioning base: L[qmap[p]] = base[p] (the Gauss-Newton and Laplace
+// updates add JᵀΛJ through GramPlan, gram.hpp).
 __global__ void k_fill_panels(const i64* __restrict__ pcp, const i32* __restrict__ pri, int N,
                               const i64* __restrict__ qmap, const double* __restrict__ base,
                               const i64* __restrict__ jcp, const i32* __restrict__ jri,
@@ -154,6 +123,12 @@ __global__ void k_spmv(int nrows, const i64* __restrict__ rp, const i32* __restr
   }
 }
 
+__global__ void k_weighted_misfit(int m, double lam, const double* __restrict__ f,
+                                  double* __restrict__ w) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x)
+    w[i] = lam * (0.0 - f[i]);
+}
+
 __global__ void k_axpby(int n, double a, const double* __restrict__ x, double b,
                         const double* __restrict__ y, double* __restrict__ z) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
@@ -190,9 +165,14 @@ __global__ void k_dot_final(double* __restrict__ part, double* __restrict__ out)
 }
 
 // ---- Burgers weak residual, P1, implicit Euler (residual.hpp:244-382) ------
+// Element e spans nodes e, e+1 with its own length x[e+1] − x[e] (the node
+// coordinates are rounded, mesh.hpp:63-70); step s has its own Δt_s
+// (t_grid differences, residual.hpp:304,371).
 struct BurgersDev {
   int ns, nt, nk;           // spatial dofs, slices, kept rows per step
-  double h, dt, nu;
+  double nu;
+  const double* x;          // node coordinates [ns]
+  const double* dt;         // per-step Δt [nt-1]
   const char* slack;
   const int* kept;          // kept row k -> dof
 };
@@ -200,6 +180,7 @@ struct BurgersDev {
 __device__ __forceinline__ double um(const BurgersDev& B, const double* u, int s, int j) {
   return (j < 0 || j >= B.ns || B.slack[j]) ? 0.0 : u[static_cast<i64>(s) * B.ns + j];
 }
+__device__ __forceinline__ double elen(const BurgersDev& B, int e) { return B.x[e + 1] - B.x[e]; }
 
 // 2-point Gauss-Legendre on [0,1] (degree-3 rule of residual.hpp:208-209)
 __device__ __forceinline__ void gl2(double* xi, double* w) {
@@ -209,39 +190,46 @@ __device__ __forceinline__ void gl2(double* xi, double* w) {
   w[0] = w[1] = 0.5;
 }
 
-// weak advection a_d(v) = ∫ φ_d v ∂x v, v slack-masked (residual.hpp:206-235)
+// weak advection a_d(v) = ∫ φ_d v ∂x v, v slack-masked (residual.hpp:206-235):
+// per quadrature point v_q = Σ v φ, ∂x v_q = Σ v φ'/h, term (w h) φ_d v_q ∂x v_q
 __device__ double adv_row(const BurgersDev& B, const double* u, int s, int d) {
   double xi[2], w[2];
   gl2(xi, w);
   double acc = 0.0;
   for (int e = d - 1; e <= d; ++e) {
     if (e < 0 || e >= B.ns - 1) continue;
+    const double h = elen(B, e);
     const double vl = um(B, u, s, e), vr = um(B, u, s, e + 1);
-    const double dv = (vr - vl) / B.h;
+    const double dv = vl * (-1.0 / h) + vr * (1.0 / h);
     for (int q = 0; q < 2; ++q) {
       const double phi = (d == e) ? 1.0 - xi[q] : xi[q];
       const double vq = vl * (1.0 - xi[q]) + vr * xi[q];
-      acc += w[q] * B.h * phi * vq * dv;
+      acc += w[q] * h * phi * vq * dv;
     }
   }
   return acc;
 }
 
+// P1 mass / stiffness entries of row d (closed form per element, slack masked)
 __device__ __forceinline__ double mass_ij(const BurgersDev& B, int d, int j) {
   if (j < 0 || j >= B.ns || B.slack[j]) return 0.0;
   if (j == d) {
-    int ne = (d > 0) + (d < B.ns - 1);
-    return ne * B.h / 3.0;
+    double v = 0.0;
+    if (d > 0) v += elen(B, d - 1) / 3.0;
+    if (d < B.ns - 1) v += elen(B, d) / 3.0;
+    return v;
   }
-  return B.h / 6.0;
+  return elen(B, j < d ? j : d) / 6.0;
 }
 __device__ __forceinline__ double stiff_ij(const BurgersDev& B, int d, int j) {
   if (j < 0 || j >= B.ns || B.slack[j]) return 0.0;
   if (j == d) {
-    int ne = (d > 0) + (d < B.ns - 1);
-    return ne / B.h;
+    double v = 0.0;
+    if (d > 0) v += 1.0 / elen(B, d - 1);
+    if (d < B.ns - 1) v += 1.0 / elen(B, d);
+    return v;
   }
-  return -1.0 / B.h;
+  return -1.0 / elen(B, j < d ? j : d);
 }
 
 __global__ void k_burgers_res(BurgersDev B, const double* __restrict__ u, double* __restrict__ f) {
@@ -253,12 +241,13 @@ __global__ void k_burgers_res(BurgersDev B, const double* __restrict__ u, double
       mdu += mass_ij(B, d, j) * (um(B, u, s + 1, j) - um(B, u, s, j));
       kd += stiff_ij(B, d, j) * um(B, u, s + 1, j);
     }
-    f[row] = mdu / B.dt + (B.nu * kd + adv_row(B, u, s + 1, d));
+    f[row] = mdu / B.dt[s] + (B.nu * kd + adv_row(B, u, s + 1, d));
   }
 }
 
-// Jacobian row (step s, dof d): slice s → −M/Δt (θ = 1), slice s+1 →
-// ν K̂ + J_adv + M/Δt, columns ascending, slack columns skipped (residual.hpp:353-377).
+// Jacobian row (step s, dof d): slice s → (−1/Δt)·M (θ = 1), slice s+1 →
+// (ν K̂ + J_adv) + (1/Δt)·M, columns ascending, slack columns skipped
+// (residual.hpp:353-377: θ-scaled slice Jacobian plus mass_coeff·M̂).
 __global__ void k_burgers_jac(BurgersDev B, const double* __restrict__ u, const i64* __restrict__ rp,
                               double* __restrict__ jv) {
   const int nrow = (B.nt - 1) * B.nk;
@@ -266,10 +255,11 @@ __global__ void k_burgers_jac(BurgersDev B, const double* __restrict__ u, const 
   gl2(xi, w);
   for (int row = blockIdx.x * blockDim.x + threadIdx.x; row < nrow; row += gridDim.x * blockDim.x) {
     const int s = row / B.nk, d = B.kept[row - s * B.nk];
+    const double inv_dt = 1.0 / B.dt[s];
     i64 p = rp[row];
     for (int j = d - 1; j <= d + 1; ++j) {
       if (j < 0 || j >= B.ns || B.slack[j]) continue;
-      jv[p++] = -mass_ij(B, d, j) / B.dt;
+      jv[p++] = (-inv_dt) * mass_ij(B, d, j);
     }
     for (int j = d - 1; j <= d + 1; ++j) {
       if (j < 0 || j >= B.ns || B.slack[j]) continue;
@@ -277,17 +267,18 @@ __global__ void k_burgers_jac(BurgersDev B, const double* __restrict__ u, const 
       for (int e = d - 1; e <= d; ++e) {
         if (e < 0 || e >= B.ns - 1) continue;
         if (j != e && j != e + 1) continue;
+        const double h = elen(B, e);
         const double vl = um(B, u, s + 1, e), vr = um(B, u, s + 1, e + 1);
-        const double dv = (vr - vl) / B.h;
-        const double dphij = (j == e ? -1.0 : 1.0) / B.h;
+        const double dv = vl * (-1.0 / h) + vr * (1.0 / h);
+        const double dphij = (j == e ? -1.0 : 1.0) / h;
         for (int q = 0; q < 2; ++q) {
           const double phid = (d == e) ? 1.0 - xi[q] : xi[q];
           const double phij = (j == e) ? 1.0 - xi[q] : xi[q];
           const double vq = vl * (1.0 - xi[q]) + vr * xi[q];
-          ja += w[q] * B.h * phid * (phij * dv + vq * dphij);
+          ja += w[q] * h * phid * (phij * dv + vq * dphij);
         }
       }
-      jv[p++] = (B.nu * stiff_ij(B, d, j) + ja) + mass_ij(B, d, j) / B.dt;
+      jv[p++] = (B.nu * stiff_ij(B, d, j) + ja) + inv_dt * mass_ij(B, d, j);
     }
   }
 }
@@ -311,11 +302,12 @@ __global__ void k_ac_res(AcDev A, const double* __restrict__ u, double* __restri
       ku += A.kv[p] * u1[j];
     }
     const double v = u1[d];
-    f[row] = mdu / A.dt + (A.eps2 * ku + A.ml[d] * (v * v * v - v));
+    f[row] = mdu / A.dt[s] + (A.eps2 * ku + A.ml[d] * (v * v * v - v));
   }
 }
 
-// J row (s, d): slice s → −M/Δt; slice s+1 → (M/Δt + ε² K) + M̃(3u² − 1) on the diagonal.
+// J row (s, d): slice s → −M/Δt; slice s+1 → (M/Δt + ε² K) + M̃(3u² − 1) on the
+// diagonal (the oracle restatement's triplet order, oracle/ref_capi.cpp).
 __global__ void k_ac_jac(AcDev A, const double* __restrict__ u, const i64* __restrict__ jrp,
                          double* __restrict__ jv) {
   const int nrow = (A.nt - 1) * A.nk;
@@ -323,12 +315,12 @@ __global__ void k_ac_jac(AcDev A, const double* __restrict__ u, const i64* __res
     const int s = row / A.nk, d = A.kept[row - s * A.nk];
     i64 q = jrp[row];
     for (i64 p = A.rp[d]; p < A.rp[d + 1]; ++p)
-      if (!A.slack[A.ci[p]]) jv[q++] = -A.mv[p] / A.dt;
+      if (!A.slack[A.ci[p]]) jv[q++] = -A.mv[p] / A.dt[s];
     const double v = u[static_cast<i64>(s + 1) * A.ns + d];
     for (i64 p = A.rp[d]; p < A.rp[d + 1]; ++p) {
       const int j = A.ci[p];
       if (A.slack[j]) continue;
-      double x = A.mv[p] / A.dt + A.eps2 * A.kv[p];
+      double x = A.mv[p] / A.dt[s] + A.eps2 * A.kv[p];
       if (j == d) x += A.ml[d] * (3.0 * v * v - 1.0);
       jv[q++] = x;
     }
@@ -385,8 +377,19 @@ void SpaceTimePosterior::build_host() {
   ns_ = ops_.n;
   nt_ = spec_.n_t;
   n_ = ns_ * nt_;
-  const double dt = spec_.t_end / (nt_ - 1);
-  blk_ = spacetime_blocks(ops_, dt, spec_.tau, spec_.noise, spec_.init, spec_.eps);
+  tg_.resize(nt_);
+  for (int i = 0; i < nt_; ++i)
+    tg_[i] = spec_.t_end * static_cast<double>(i) / static_cast<double>(nt_ - 1);
+  dts_.resize(nt_ - 1);
+  tstep_.resize(nt_ - 1);
+  sqt_.resize(nt_ - 1);
+  for (int i = 0; i + 1 < nt_; ++i) {
+    dts_[i] = tg_[i + 1] - tg_[i];
+    tstep_[i] = 1.0 / (dts_[i] * spec_.tau * spec_.tau);
+    sqt_[i] = std::sqrt(tstep_[i]);
+  }
+  // uniform grid: the spatial blocks use the first step's Δt (spatiotemporal.hpp:114-126)
+  blk_ = spacetime_blocks(ops_, dts_[0], spec_.tau, spec_.noise, spec_.init, spec_.eps);
   const auto& sl = blk_.slack;
   // spatial coupling stencil (P1 element adjacency = the mass pattern)
   Csc stencil = ops_.mass;
@@ -451,7 +454,6 @@ void SpaceTimePosterior::build_host() {
   }
 
   // ---- S_cond = [S_prior | Aᵀ L_ε] (gmrf.hpp:165), CSC, columns in the reference order
-  const double st = std::sqrt(blk_.t);
   s_ = Csc{};
   s_.nr = n_;
   s_.cp.assign(1, 0);
@@ -468,8 +470,8 @@ void SpaceTimePosterior::build_host() {
   }
   for (int i = 0; i + 1 < nt_; ++i)
     for (int k = 0; k < ns_; ++k) {
-      push_col(i, blk_.s_m, k, st);
-      push_col(i + 1, blk_.f_is, k, -st);
+      push_col(i, blk_.s_m, k, sqt_[i]);
+      push_col(i + 1, blk_.f_is, k, -sqt_[i]);
       s_.cp.push_back(s_.nnz());
     }
   for (int d = 0; d < ns_; ++d)
@@ -518,30 +520,6 @@ void SpaceTimePosterior::build_host() {
         jri_[q] = r;
         jmap_[q] = p;
       }
-    // JᵀΛJ product map over the master pattern's lower-stored entries
-    const std::vector<i64>& qm = sym_->qmap;
-    jt_off_.assign(pri_.size() + 1, 0);
-    jt_pairs_.clear();
-    for (int C = 0; C < n_; ++C)
-      for (i64 p = pcp_[C]; p < pcp_[C + 1]; ++p) {
-        if (qm[p] >= 0) {
-          const int R = pri_[p];
-          i64 x = jcp_[R], xe = jcp_[R + 1], y = jcp_[C], ye = jcp_[C + 1];
-          while (x < xe && y < ye) {
-            if (jri_[x] < jri_[y]) {
-              ++x;
-            } else if (jri_[y] < jri_[x]) {
-              ++y;
-            } else {
-              jt_pairs_.push_back({static_cast<i32>(jmap_[x]), static_cast<i32>(jmap_[y])});
-              ++x;
-              ++y;
-            }
-          }
-        }
-        require(jt_pairs_.size() < (1ull << 31), kContract, "JtJ map exceeds int32");
-        jt_off_[p + 1] = static_cast<i32>(jt_pairs_.size());
-      }
   }
 }
 
@@ -568,11 +546,22 @@ void SpaceTimePosterior::assemble_device() {
   const i64 np = static_cast<i64>(pri_.size());
   d_qcond_.alloc(np);
   d_qeff_.alloc(np);
-  assemble_values();
+  d_tstep_.upload(tstep_, stream_);
+  d_dts_.upload(dts_, stream_);
+  if (spec_.dim == 1) {
+    std::vector<double> xn(ns_);
+    for (int d = 0; d < ns_; ++d) xn[d] = space_.x(d);
+    d_xn_.upload(xn, stream_);
+  }
   // S_cond: CSC (columns, for Sᵀx) and CSR (rows, for S w)
   d_scp_.upload(s_.cp, stream_);
   d_sri_.upload(s_.ri, stream_);
   d_sv_.upload(s_.v, stream_);
+  // q_eff = sym(S Sᵀ) (gauss_newton.hpp:112-113): Gram product of Sᵀ, whose rows
+  // are S's columns, over the master pattern
+  gram_s_ = std::make_unique<GramPlan>(n_, pcp_.data(), pri_.data(), ms_, s_.cp.data(),
+                                       s_.ri.data(), nullptr, stream_);
+  assemble_values();
   Csc sr = transpose(s_);
   d_srp_.upload(sr.cp, stream_);
   d_sci_.upload(sr.ri, stream_);
@@ -589,12 +578,13 @@ void SpaceTimePosterior::assemble_device() {
     d_ml_.upload(lumped_mass(m), stream_);
   }
   if (spec_.residual != 0) {
-    d_jt_off_.upload(jt_off_, stream_);
-    {
-      std::vector<int2> pr(jt_pairs_.size());
-      for (size_t i = 0; i < pr.size(); ++i) pr[i] = make_int2(jt_pairs_[i].first, jt_pairs_[i].second);
-      d_jt_pairs_.upload(pr, stream_);
-    }
+    // JᵀΛJ over the entries the factorization reads (qmap >= 0), written into the panels
+    std::vector<char> need(pri_.size());
+    for (size_t p = 0; p < need.size(); ++p) need[p] = sym_->qmap[p] >= 0;
+    gram_j_ = std::make_unique<GramPlan>(n_, pcp_.data(), pri_.data(), nres_, jrp_.data(),
+                                         jci_.data(), &need, stream_);
+    d_lam_.upload(std::vector<double>(nres_, spec_.pde_noise_prec), stream_);
+    d_wf_.alloc(std::max(nres_, 1));
     d_jrp_.upload(jrp_, stream_);
     d_jci_.upload(jci_, stream_);
     d_jcp_.upload(jcp_, stream_);
@@ -607,8 +597,9 @@ void SpaceTimePosterior::assemble_device() {
     kept_.upload(kept, stream_);
   }
   if (std::getenv("GMRF_VERBOSE"))
-    std::fprintf(stderr, "[gmrf] spacetime n %d pattern nnz %zu, JtJ pairs %zu (%.2f GB), nnz(L) %lld\n",
-                 n_, pri_.size(), jt_pairs_.size(), jt_pairs_.size() * 8e-9,
+    std::fprintf(stderr, "[gmrf] spacetime n %d pattern nnz %zu, JtJ pairs %lld, SSt pairs %lld, nnz(L) %lld\n",
+                 n_, pri_.size(), static_cast<long long>(gram_j_ ? gram_j_->pairs() : 0),
+                 static_cast<long long>(gram_s_->pairs()),
                  static_cast<long long>(sym_->nnz_l_padded));
   fac_ = std::make_unique<DeviceFactor>(sym_, stream_, pspec_.nranks > 1 ? &pspec_ : nullptr);
   auto mem = [&](const char* what) {
@@ -629,17 +620,20 @@ void SpaceTimePosterior::assemble_device() {
   part_.alloc(2 * (kDotBlocks + 1));
 }
 
-// Row 1: joint prior / q_eff values on the master pattern (device).
+// Row 1: joint prior (Q_cond) and q_eff = sym(S Sᵀ) values on the master pattern (device).
 void SpaceTimePosterior::assemble_values() {
   BlkDev b{d_blk_cp_.p, d_blk_ri_.p, d_blk_v_.p, ns_};
   const double np = static_cast<double>(pri_.size());
-  // algorithmic bytes: write Q_cond and q_eff (16 B/entry) + pattern (4 B/entry + 8 B/column)
-  prof_.run(stream_, "assemble.prior", 0.0, 20.0 * np + 8.0 * n_, [&] {
-    k_st_assemble<<<grid_for(n_), 256, 0, stream_>>>(d_pcp_.p, d_pri_.p, n_, ns_, nt_, blk_.t,
+  // algorithmic bytes: write Q_cond (8 B/entry) + pattern (4 B/entry + 8 B/column)
+  prof_.run(stream_, "assemble.prior", 0.0, 12.0 * np + 8.0 * n_, [&] {
+    k_st_assemble<<<grid_for(n_), 256, 0, stream_>>>(d_pcp_.p, d_pri_.p, n_, ns_, nt_, d_tstep_.p,
                                                     1.0 / spec_.eps, spec_.ic_noise_prec,
-                                                    d_slack_.p, b, d_qcond_.p, d_qeff_.p);
+                                                    d_slack_.p, b, d_qcond_.p);
   });
-  times_.kernel_launches += 1;
+  prof_.run(stream_, "assemble.q_eff", 0.0, gram_s_->bytes(false, true, false), [&] {
+    gram_s_->apply(d_sv_.p, nullptr, 1.0, nullptr, d_qeff_.p, nullptr, nullptr, stream_);
+  });
+  times_.kernel_launches += 1 + gram_s_->launches(false);
 }
 
 double SpaceTimePosterior::dot(const double* a, const double* b, i64 n) {
@@ -660,8 +654,8 @@ void SpaceTimePosterior::eval_residual(const double* d_u, double* d_f) {
     times_.kernel_launches += 1;
     return;
   }
-  BurgersDev B{ns_, nt_, static_cast<int>(kept_.n), space_.h(), spec_.t_end / (nt_ - 1),
-               spec_.diffusion, d_slack_.p, kept_.p};
+  BurgersDev B{ns_, nt_, static_cast<int>(kept_.n), spec_.diffusion, d_xn_.p, d_dts_.p,
+               d_slack_.p, kept_.p};
   k_burgers_res<<<grid_for(nres_), 256, 0, stream_>>>(B, d_u, d_f);
   times_.kernel_launches += 1;
 }
@@ -672,8 +666,8 @@ void SpaceTimePosterior::eval_jacobian(const double* d_u) {
     times_.kernel_launches += 1;
     return;
   }
-  BurgersDev B{ns_, nt_, static_cast<int>(kept_.n), space_.h(), spec_.t_end / (nt_ - 1),
-               spec_.diffusion, d_slack_.p, kept_.p};
+  BurgersDev B{ns_, nt_, static_cast<int>(kept_.n), spec_.diffusion, d_xn_.p, d_dts_.p,
+               d_slack_.p, kept_.p};
   k_burgers_jac<<<grid_for(nres_), 256, 0, stream_>>>(B, d_u, d_jrp_.p, d_jv_.p);
   times_.kernel_launches += 1;
 }
@@ -681,7 +675,7 @@ void SpaceTimePosterior::eval_jacobian(const double* d_u) {
 void SpaceTimePosterior::residual(const double* d_u, double* d_r) { eval_residual(d_u, d_r); }
 
 AcDev SpaceTimePosterior::ac_dev() const {
-  return AcDev{ns_, nt_, static_cast<int>(kept_.n), spec_.t_end / (nt_ - 1), spec_.diffusion,
+  return AcDev{ns_, nt_, static_cast<int>(kept_.n), d_dts_.p, spec_.diffusion,
                d_slack_.p, kept_.p, d_mrp_.p, d_mci_.p, d_mv_.p, d_kv_.p, d_ml_.p};
 }
 
@@ -710,19 +704,20 @@ double SpaceTimePosterior::objective(const double* d_x, const double* d_fx) {
 
 void SpaceTimePosterior::fill_panels(const double* base, bool with_jacobian) {
   fac_->begin_numeric();
-  // algorithmic bytes: base + qmap + pattern (20 B/entry), L writes for the
-  // lower half (4 B/entry), J values/rows/map (20 B/nnz) when JᵀΛJ is added
+  if (with_jacobian) {
+    // H = sym(base + Jᵀ Λ J) straight into the panels (gauss_newton.hpp:137-138, :231-232)
+    prof_.run(stream_, "update.h_jtlj", 0.0, gram_j_->bytes(true, false, true), [&] {
+      gram_j_->apply(d_jv_.p, d_lam_.p, 1.0, base, nullptr, fac_->d_qmap(), fac_->d_l(), stream_);
+    });
+    times_.kernel_launches += gram_j_->launches(true);
+    return;
+  }
+  // base + pattern + qmap (20 B/entry) read, lower-half L writes (4 B/entry)
   const double np = static_cast<double>(pri_.size());
-  const double bytes = 24.0 * np + (with_jacobian ? 20.0 * static_cast<double>(jci_.size()) : 0.0);
-  prof_.run(stream_, with_jacobian ? "update.h_jtlj" : "update.q_base", 0.0, bytes, [&] {
-    if (with_jacobian)
-      k_fill_panels_map<<<grid_for(static_cast<i64>(pri_.size())), 256, 0, stream_>>>(
-          static_cast<i64>(pri_.size()), fac_->d_qmap(), base, d_jt_off_.p, d_jt_pairs_.p,
-          d_jv_.p, spec_.pde_noise_prec, fac_->d_l());
-    else
-      k_fill_panels<<<grid_for(n_), 256, 0, stream_>>>(d_pcp_.p, d_pri_.p, n_, fac_->d_qmap(),
-                                                       base, nullptr, d_jri_.p, d_jmap_.p, d_jv_.p,
-                                                       spec_.pde_noise_prec, fac_->d_l());
+  prof_.run(stream_, "update.q_base", 0.0, 24.0 * np, [&] {
+    k_fill_panels<<<grid_for(n_), 256, 0, stream_>>>(d_pcp_.p, d_pri_.p, n_, fac_->d_qmap(), base,
+                                                     nullptr, d_jri_.p, d_jmap_.p, d_jv_.p,
+                                                     spec_.pde_noise_prec, fac_->d_l());
   });
   times_.kernel_launches += 1;
 }
@@ -813,12 +808,13 @@ std::vector<GnIter> SpaceTimePosterior::run(const double* u0, const GnConfig& cf
     k_axpby<<<grid_for(n_), 256, 0, stream_>>>(n_, 1.0, x_.p, -1.0, mean_cond_.p, c_.p);
     k_spmv<<<grid_for(ms_), 256, 0, stream_>>>(ms_, d_scp_.p, d_sri_.p, d_sv_.p, nullptr, c_.p, w_.p);
     k_spmv<<<grid_for(n_), 256, 0, stream_>>>(n_, d_srp_.p, d_sci_.p, d_svr_.p, nullptr, w_.p, g_.p);
-    // Jᵀ(λ f): fit term gradient is +λ Jᵀ f since y − f = −f
-    k_spmv<<<grid_for(n_), 256, 0, stream_>>>(n_, d_jcp_.p, d_jri_.p, d_jv_.p, d_jmap_.p, f_.p,
+    // weighted = Λ (y − f) with y = 0; grad −= Jᵀ weighted (gauss_newton.hpp:126-130)
+    k_weighted_misfit<<<grid_for(nres_), 256, 0, stream_>>>(nres_, lam, f_.p, d_wf_.p);
+    k_spmv<<<grid_for(n_), 256, 0, stream_>>>(n_, d_jcp_.p, d_jri_.p, d_jv_.p, d_jmap_.p, d_wf_.p,
                                               r1_.p);
-    k_axpby<<<grid_for(n_), 256, 0, stream_>>>(n_, 1.0, g_.p, lam, r1_.p, g_.p);
+    k_axpby<<<grid_for(n_), 256, 0, stream_>>>(n_, 1.0, g_.p, -1.0, r1_.p, g_.p);
     k_axpby<<<grid_for(n_), 256, 0, stream_>>>(n_, -1.0, g_.p, 0.0, g_.p, r1_.p);  // rhs = −grad
-    times_.kernel_launches += 6;
+    times_.kernel_launches += 7;
     fill_panels(d_qeff_.p, true);
     factor_now("gauss-newton");
     fac_->solve(2, 1, r1_.p, d_.p, true);

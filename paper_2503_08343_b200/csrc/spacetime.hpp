@@ -12,13 +12,15 @@
 
 #include "factor.hpp"
 #include "fem.hpp"
+#include "gram.hpp"
 
 namespace gmrf {
 
 // Device view of the Allen-Cahn residual data (spacetime.cu).
 struct AcDev {
   int ns, nt, nk;
-  double dt, eps2;
+  const double* dt;  // per-step Δt [nt-1]
+  double eps2;
   const char* slack;
   const int* kept;
   const i64* rp;
@@ -141,14 +143,16 @@ class SpaceTimePosterior {
   std::vector<i64> jcp_;      // J CSC column pointers
   std::vector<i32> jri_;      // J CSC rows
   std::vector<i64> jmap_;     // CSC position -> CSR value index
-  std::vector<i32> jt_off_;   // JᵀΛJ product map: pattern entry -> pair range
-  std::vector<std::pair<i32, i32>> jt_pairs_;  // (J value index, J value index)
+  // time grid t_s = t_end·s/(n_t−1) (as the oracle builds it), per-step Δt_s,
+  // T_s = 1/(Δt_s τ²) and √T_s (spatiotemporal.hpp:118-120)
+  std::vector<double> tg_, dts_, tstep_, sqt_;
+  // JᵀΛJ (lower entries, straight into the panels) and q_eff = sym(S Sᵀ)
+  std::unique_ptr<GramPlan> gram_j_, gram_s_;
 
   // device
   DevBuf<i64> d_pcp_, d_qmap_, d_scp_, d_srp_, d_jrp_, d_jcp_, d_jmap_;
-  DevBuf<i32> d_pri_, d_sri_, d_sci_, d_jci_, d_jri_, kept_, d_jt_off_;
-  DevBuf<int2> d_jt_pairs_;
-  DevBuf<double> d_qcond_, d_qeff_, d_sv_, d_svr_, d_jv_;
+  DevBuf<i32> d_pri_, d_sri_, d_sci_, d_jci_, d_jri_, kept_;
+  DevBuf<double> d_qcond_, d_qeff_, d_sv_, d_svr_, d_jv_, d_lam_, d_tstep_, d_dts_, d_xn_, d_wf_;
   DevBuf<i64> d_blk_cp_;
   DevBuf<i32> d_blk_ri_;
   DevBuf<double> d_blk_v_;

@@ -16,8 +16,23 @@ reference's AMD factorization is ~190 s per GN step and its Takahashi pass
                         the largest the reference's int32 nnz(L) survives).
   c4_burgers_200.npz    C4 shape at 199 x 200 with the full 10-step GN budget.
 
-Usage: python tests/golden/make_golden_full.py c4 | c3 | c5_16 | c5_32 | c4_200
+Usage: python tests/golden/make_golden_full.py c4 | c3 | c5_16 | c5_32 | c4_200 | c4_500
+       python tests/golden/make_golden_full.py floor:c4_200 ...
 Each run writes its fixture atomically (tmp + rename) plus a .log with timings.
+
+``order:<job>`` re-runs the unmodified reference chain with its fill-reducing
+ordering (AMD in gauss_newton.hpp:139 and cholesky_factor, gmrf.hpp:55,160)
+redirected to METIS nested dissection (oracle/_ref/libgmrfref_nd.so) and records
+the move in floors.json under "<fixture>/order": the reference's ordering floor
+(SURVEY §8(c) (i)), the primary tolerance scale of the GPU parity tests.
+
+``floor:<job>`` re-runs the same unmodified reference chain with every initial-
+condition value multiplied by (1 ± 2⁻⁵²) (oracle/ref_capi.cpp ulp_perturb,
+SURVEY §8(c) "floor2") and records in floors.json how far the reference's own
+outputs move (GN objective / decrement, mode, variances, relative). That is the
+reference's FP64 floor for the chain: one ulp of input noise, amplified by the
+conditioning of H (Λ_pde = 1e12) and by the Gauss-Newton trajectory. GPU parity
+is judged against a small multiple of it (tests/test_gpu_parity_full.py).
 """
 from __future__ import annotations
 
@@ -31,7 +46,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, os.path.abspath(os.path.join(HERE, "..", "..")))
 
-from oracle.pyoracle import Ref  # noqa: E402
+from oracle.pyoracle import REF_ND_SO, REF_SO, Ref  # noqa: E402
 
 TIMERS = ["t_prior", "t_condition", "t_gn", "t_laplace_build", "t_variance"]
 
@@ -51,12 +66,44 @@ def _save(name, out, b, t_wall):
     print(name, json.dumps(times), flush=True)
 
 
-def burgers(n_el, n_t, gn_iters, name):
-    # make_golden.spatiotemporal parameter layout (oracle/ref_capi.cpp:147-149)
+FLOOR_SEED = 7
+MODE = {"so": REF_SO, "tag": ""}  # order: jobs switch to the ND-ordering probe build
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def _record_floor(name, b):
+    """Compares a perturbed reference run with the committed fixture."""
+    z = np.load(os.path.join(HERE, name))
+    f = {"seed": FLOOR_SEED} if MODE["tag"] == "/ulp" else {"ordering": "metis_nd"}
+    for k, key in (("mean", "mode"), ("mean", "mean_post"), ("var", "var_post")):
+        if key in z.files and k not in f:
+            f[k] = _rel(b.vec(key), z[key])
+    if "gn_objective" in z.files:
+        for k in ("gn_objective", "gn_decrement"):
+            v = b.vec(k)
+            if len(v) == len(z[k]):
+                f[k.replace("gn_", "")] = float(np.max(np.abs(v - z[k]) / np.abs(z[k])))
+        f["same_trace"] = bool(np.array_equal(b.vec("gn_backtracks"), z["gn_backtracks"]))
+    path = os.path.join(HERE, "floors.json")
+    floors = json.load(open(path)) if os.path.exists(path) else {}
+    floors[name + MODE["tag"]] = f
+    with open(path + ".tmp", "w") as fh:
+        json.dump(floors, fh, indent=1, sort_keys=True)
+    os.replace(path + ".tmp", path)
+    print("floor", name, f, flush=True)
+
+
+def burgers(n_el, n_t, gn_iters, name, floor=False):
+    # make_golden.spatiotemporal parameter layout (oracle/ref_capi.cpp:157-160)
     p = [1, n_el, -1.0, 1.0, n_t, 1.0, 0.01 / np.pi, 0.5, 10, 1, 1, 10, 2, 1, 1.0, 1e-10, 1e8,
-         0, 1e12, gn_iters, 1, 1]
+         0, 1e12, gn_iters, 1, 1, 0, FLOOR_SEED if floor and MODE["tag"] == "/ulp" else 0]
     t0 = time.time()
-    b = Ref().build("spatiotemporal", p)
+    b = Ref(MODE["so"]).build("spatiotemporal", p)
+    if floor:
+        return _record_floor(name, b)
     out = {"params": np.array(p, np.float64)}
     for k in ["mean_cond", "mode", "mean_post", "var_post", "gn_objective", "gn_decrement",
               "gn_step", "gn_backtracks"]:
@@ -65,21 +112,26 @@ def burgers(n_el, n_t, gn_iters, name):
     _save(name, out, b, time.time() - t0)
 
 
-def heat(n_el, n_t, name):
+def heat(n_el, n_t, name, floor=False):
     p = [0, n_el, 0.0, 1.0, n_t, 1.0, 0.1, 0.0, 10, 1, 1, 10, 2, 1, 1.0, 1e-10, 1e6, 1003,
-         0, 0, 1, 0]
+         0, 0, 1, 0, 0, FLOOR_SEED if floor and MODE["tag"] == "/ulp" else 0]
     t0 = time.time()
-    b = Ref().build("spatiotemporal", p)
+    b = Ref(MODE["so"]).build("spatiotemporal", p)
+    if floor:
+        return _record_floor(name, b)
     out = {"params": np.array(p, np.float64)}
     for k in ["y_ic", "mean_post", "var_post"]:
         out[k] = b.vec(k)
     _save(name, out, b, time.time() - t0)
 
 
-def allen_cahn(n_cells, n_t, name, gn_iters=8):
-    p = [n_cells, n_t, 0.5, 0.0025, 10, 1, 1, 10, 2, 1, 1.0, 1e6, 1005, 1e12, gn_iters, 1, 1, 1]
+def allen_cahn(n_cells, n_t, name, gn_iters=8, floor=False):
+    p = [n_cells, n_t, 0.5, 0.0025, 10, 1, 1, 10, 2, 1, 1.0, 1e6, 1005, 1e12, gn_iters, 1, 1, 1,
+         FLOOR_SEED if floor and MODE["tag"] == "/ulp" else 0]
     t0 = time.time()
-    b = Ref().build("allen_cahn", p)
+    b = Ref(MODE["so"]).build("allen_cahn", p)
+    if floor:
+        return _record_floor(name, b)
     out = {"params": np.array(p, np.float64), "fd_rel_err": np.array([b.scalar("fd_rel_err")])}
     for k in ["u0", "mean_cond", "mode", "mean_post", "var_post", "gn_objective",
               "gn_decrement", "gn_step", "gn_backtracks"]:
@@ -89,14 +141,19 @@ def allen_cahn(n_cells, n_t, name, gn_iters=8):
 
 
 JOBS = {
-    "c4": lambda: burgers(999, 1000, 10, "c4_burgers_full.npz"),
-    "c4_200": lambda: burgers(199, 200, 10, "c4_burgers_200.npz"),
-    "c4_500": lambda: burgers(499, 500, 10, "c4_burgers_500.npz"),
-    "c3": lambda: heat(499, 1000, "c3_heat_full.npz"),
-    "c5_16": lambda: allen_cahn(15, 32, "c5_allen_cahn_16.npz"),
-    "c5_32": lambda: allen_cahn(31, 64, "c5_allen_cahn_32.npz"),
+    "c4": lambda fl: burgers(999, 1000, 10, "c4_burgers_full.npz", fl),
+    "c4_200": lambda fl: burgers(199, 200, 10, "c4_burgers_200.npz", fl),
+    "c4_500": lambda fl: burgers(499, 500, 10, "c4_burgers_500.npz", fl),
+    "c3": lambda fl: heat(499, 1000, "c3_heat_full.npz", fl),
+    "c5_16": lambda fl: allen_cahn(15, 32, "c5_allen_cahn_16.npz", floor=fl),
+    "c5_32": lambda fl: allen_cahn(31, 64, "c5_allen_cahn_32.npz", floor=fl),
 }
 
 if __name__ == "__main__":
     for job in sys.argv[1:]:
-        JOBS[job]()
+        kind = job.split(":")[0] if ":" in job else ""
+        if kind == "order":
+            MODE.update(so=REF_ND_SO, tag="/order")
+        elif kind == "floor":
+            MODE.update(tag="/ulp")
+        JOBS[job.split(":")[-1]](kind != "")
