@@ -208,9 +208,96 @@ int gmrf_factor_create_partitioned(const gmrf_symbolic_t* s, int32_t nranks, int
  * .normal() (kind 1, Box-Muller with the cached spare), host only — the
  * reference's seeded synthetic inputs without the reference. */
 int gmrf_rng_fill(uint64_t seed, int32_t kind, int64_t n, double* out);
+/* One Rng(seed) stream: n_uniform uniform() draws, then n_normal normal() draws,
+ * into out[n_uniform + n_normal] — SURVEY §8(d)'s pinned draw order (e.g. C1:
+ * 100 observation coordinates, then 100 noises). */
+int gmrf_rng_draw(uint64_t seed, int64_t n_uniform, int64_t n_normal, double* out);
 
 /* FP64 issue-rate microbenchmark (TFLOP/s) of DMMA m8n8k4 and DFMA. */
 int gmrf_bench_fp64(double* dmma_tflops, double* dfma_tflops);
+
+/* ---- Fixed-pattern conditioning update (north_star rows 1-2) ---------------
+ * H = symmetrize(base + c · Aᵀ diag(w) A) on the symbolic's pattern: the
+ * reference's condition_affine update (gmrf.hpp:150-155, A = observation
+ * operator, w = Λ), its Gauss-Newton matrix (gauss_newton.hpp:137-138, A = J_k,
+ * w = Λ_pde, base = q_eff) and Laplace precision (:231-232), and the Matérn
+ * precision (priors/matern.hpp:70-80, A = K, w = 1/m̃, c = 1/τ², no base).
+ * The plan (a product map: for each pattern entry, the pairs of A entries
+ * sharing a row) is built once per A pattern; updates stream values only and
+ * write the factor's panels directly — no permute, sort or triplet pass per
+ * refactorization (cholesky.hpp:117). Same per-entry summation order as the
+ * reference's SpGEMM + symmetrize. A: m × n CSR, columns ascending per row;
+ * every product A_kR A_kC must fall in the pattern (GMRF_ERR_STRUCTURAL). */
+typedef struct gmrf_gram gmrf_gram_t;
+int gmrf_gram_create(const gmrf_symbolic_t* s, int32_t m, const int64_t* a_row_ptr,
+                     const int32_t* a_col_idx, gmrf_gram_t** out);
+void gmrf_gram_free(gmrf_gram_t* g);
+/* Assembled values on the symbolic's CSC pattern (host in/out): out[nnz_q];
+ * base (nnz_q, may be NULL = 0), a_values (A's nnz, CSR order), w (m, NULL = 1). */
+int gmrf_gram_apply(gmrf_gram_t* g, const double* base, const double* a_values, const double* w,
+                    double c, double* out);
+/* gmrf_update_fixed_pattern: writes H straight into f's panels and factors it
+ * (cholesky_refactor of H). bad_index as gmrf_factor_numeric. Host arrays /
+ * device arrays (enqueued on the factor's stream). */
+int gmrf_factor_update_fixed_pattern(gmrf_factor_t* f, gmrf_gram_t* g, const double* base,
+                                     const double* a_values, const double* w, double c,
+                                     int32_t* bad_index);
+int gmrf_factor_update_fixed_pattern_device(gmrf_factor_t* f, gmrf_gram_t* g, const double* d_base,
+                                            const double* d_a_values, const double* d_w, double c,
+                                            int32_t* bad_index);
+
+/* ---- Matérn SPDE regression posterior (configs 1-2) -------------------------
+ * P1 FEM on an interval (dim 1: n_el elements over [xa, xb],
+ * build_interval_mesh, fem/mesh.hpp:63) or the unit square (dim 2: n_el × n_el
+ * cells split along the diagonal, build_unit_square_mesh, mesh.hpp:142). */
+typedef struct {
+  int32_t dim;
+  int32_t n_el;
+  double xa, xb;
+  double kappa; /* MaternSpec {κ, α, τ} (priors/matern.hpp) */
+  int32_t alpha;
+  double tau;
+} gmrf_matern_config_t;
+
+/* point_observation_operator / eval_basis (solver/info_operator.hpp:108-123,
+ * fem/space.hpp:67-109,376-394): A (m × n) with the P1 shape values of the
+ * element containing each point; CSR, 2 (1-D) or 3 (2-D) entries per row.
+ * Host only. Call with col_idx == NULL for the nnz (row_ptr[m] filled). */
+int gmrf_point_operator(const gmrf_matern_config_t* mesh, int32_t m, const double* points,
+                        int64_t* row_ptr, int32_t* col_idx, double* values);
+/* matern_prior (priors/matern.hpp:53-80): the prior precision Q assembled on
+ * the device (fixed-pattern Gram product of K = K_Δ + κ²M with the lumped mass),
+ * full symmetric CSC. col_ptr[n+1] first (row_idx == NULL), then the rest. */
+int gmrf_matern_prior(const gmrf_matern_config_t* cfg, int32_t* n, int64_t* col_ptr,
+                      int32_t* row_idx, double* values);
+
+/* Posterior of the Matérn prior conditioned on m point observations
+ * (condition_on(matern_prior, point_observation_operator), gmrf.hpp:145-170):
+ * Q assembly, Q + AᵀΛA straight into the factor, factorization, mean solve,
+ * Takahashi variances and sample_direct draws — all on the device. perm: the
+ * factor's ordering (new -> old) or NULL for nested dissection; samples depend
+ * on it, as the reference's (pass its AMD order to reproduce its draws). */
+typedef struct gmrf_regression gmrf_regression_t;
+int gmrf_regression_create(const gmrf_matern_config_t* cfg, int32_t m, const double* points,
+                           const int32_t* perm, gmrf_regression_t** out);
+/* y, noise_prec: m values. mean, var: n (may be NULL); samples: n × n_samples
+ * column-major (may be NULL), sample s = the s-th sample_direct(post, rng) of
+ * Rng(seed) (gmrf.hpp:182-184). */
+int gmrf_regression_run(gmrf_regression_t* h, const double* y, const double* noise_prec,
+                        int32_t want_var, int32_t n_samples, uint64_t seed, double* mean,
+                        double* var, double* samples);
+typedef struct {
+  int32_t n, m;
+  int64_t nnz_pattern, nnz_l;
+  double setup_host_ms, run_ms, flops_ref;
+  int64_t kernel_launches;
+} gmrf_regression_info_t;
+int gmrf_regression_info(const gmrf_regression_t* h, gmrf_regression_info_t* info);
+/* Q_prior and Q_post on the pattern (tests): col_ptr[n+1], row_idx, values. */
+int gmrf_regression_precisions(const gmrf_regression_t* h, int64_t* col_ptr, int32_t* row_idx,
+                               double* q_prior, double* q_post);
+gmrf_factor_t* gmrf_regression_factor(gmrf_regression_t* h); /* borrowed */
+void gmrf_regression_free(gmrf_regression_t* h);
 
 /* ---- Space-time posterior pipeline (1D space × implicit-Euler time) --------
  * The chain the reference runs in bench/runner.hpp:457-632 (run_burgers):

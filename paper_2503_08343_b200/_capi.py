@@ -75,6 +75,18 @@ class SpaceTimeInfo(C.Structure):
 vp = C.c_void_p
 
 
+class MaternConfig(C.Structure):
+    """gmrf_matern_config_t: P1 mesh + MaternSpec."""
+    _fields_ = [("dim", C.c_int32), ("n_el", C.c_int32), ("xa", C.c_double), ("xb", C.c_double),
+                ("kappa", C.c_double), ("alpha", C.c_int32), ("tau", C.c_double)]
+
+
+class RegressionInfo(C.Structure):
+    _fields_ = [("n", C.c_int32), ("m", C.c_int32), ("nnz_pattern", C.c_int64),
+                ("nnz_l", C.c_int64), ("setup_host_ms", C.c_double), ("run_ms", C.c_double),
+                ("flops_ref", C.c_double), ("kernel_launches", C.c_int64)]
+
+
 class CgConfig(C.Structure):
     _fields_ = [("rtol", C.c_double), ("atol", C.c_double), ("max_iter", C.c_int64),
                 ("preconditioner", C.c_int32)]
@@ -121,6 +133,7 @@ SIGNATURES = {
     "gmrf_factor_free": (None, [C.c_void_p]),
     "gmrf_bench_fp64": (C.c_int, [f64p, f64p]),
     "gmrf_rng_fill": (C.c_int, [C.c_uint64, C.c_int32, C.c_int64, f64p]),
+    "gmrf_rng_draw": (C.c_int, [C.c_uint64, C.c_int64, C.c_int64, f64p]),
     "gmrf_cg_solve": (C.c_int, [C.c_int32, i64p, i32p, f64p, f64p, f64p, C.POINTER(CgConfig),
                                 f64p, C.POINTER(CgResult)]),
     "gmrf_sample_cg": (C.c_int, [C.c_int32, i64p, i32p, f64p, C.c_int32, i64p, i32p, f64p, f64p,
@@ -142,6 +155,22 @@ SIGNATURES = {
     "gmrf_spacetime_jacobian": (C.c_int, [vp, f64p, i64p, i32p, f64p]),
     "gmrf_spacetime_free": (None, [vp]),
     "gmrf_spacetime_set_profile": (C.c_int, [vp, C.c_int32]),
+    "gmrf_gram_create": (C.c_int, [vp, C.c_int32, i64p, i32p, C.POINTER(vp)]),
+    "gmrf_gram_free": (None, [vp]),
+    "gmrf_gram_apply": (C.c_int, [vp, f64p, f64p, f64p, C.c_double, f64p]),
+    "gmrf_factor_update_fixed_pattern": (C.c_int, [vp, vp, f64p, f64p, f64p, C.c_double, i32p]),
+    "gmrf_factor_update_fixed_pattern_device": (C.c_int, [vp, vp, vp, vp, vp, C.c_double, i32p]),
+    "gmrf_point_operator": (C.c_int, [C.POINTER(MaternConfig), C.c_int32, f64p, i64p, i32p,
+                                      f64p]),
+    "gmrf_matern_prior": (C.c_int, [C.POINTER(MaternConfig), i32p, i64p, i32p, f64p]),
+    "gmrf_regression_create": (C.c_int, [C.POINTER(MaternConfig), C.c_int32, f64p, i32p,
+                                         C.POINTER(vp)]),
+    "gmrf_regression_run": (C.c_int, [vp, f64p, f64p, C.c_int32, C.c_int32, C.c_uint64, f64p,
+                                      f64p, f64p]),
+    "gmrf_regression_info": (C.c_int, [vp, C.POINTER(RegressionInfo)]),
+    "gmrf_regression_precisions": (C.c_int, [vp, i64p, i32p, f64p, f64p]),
+    "gmrf_regression_factor": (vp, [vp]),
+    "gmrf_regression_free": (None, [vp]),
     "gmrf_spacetime_kernel_stats": (C.c_int, [vp, C.c_void_p, C.c_int32, i32p]),
 }
 

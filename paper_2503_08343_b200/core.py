@@ -401,6 +401,13 @@ class Rng:
         """normal_vector(n) of a fresh Rng(seed)."""
         return self._fill(1, n)
 
+    def draw(self, n_uniform, n_normal):
+        """One fresh Rng(seed) stream: n_uniform uniform() then n_normal normal()."""
+        out = np.empty(int(n_uniform) + int(n_normal))
+        _check(_capi.load().gmrf_rng_draw(self.seed, int(n_uniform), int(n_normal),
+                                          ptr(out, f64p)))
+        return out[: int(n_uniform)], out[int(n_uniform):]
+
 
 def bench_fp64() -> tuple[float, float]:
     a, b = C.c_double(), C.c_double()

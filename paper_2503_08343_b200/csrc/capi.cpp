@@ -12,6 +12,8 @@
 #include "factor.hpp"
 #include "partition.hpp"
 #include "rng.hpp"
+#include "gram.hpp"
+#include "regression.hpp"
 #include "spacetime.hpp"
 
 static_assert(sizeof(gmrf_msg_t) == sizeof(gmrf::XferMsg), "gmrf_msg_t layout");
@@ -25,6 +27,16 @@ struct gmrf_symbolic {
 struct gmrf_factor {
   std::shared_ptr<const gmrf::Symbolic> s;
   std::unique_ptr<gmrf::DeviceFactor> f;
+};
+struct gmrf_gram {
+  std::shared_ptr<const gmrf::Symbolic> s;
+  std::unique_ptr<gmrf::GramPlan> g;
+  gmrf::i32 m = 0;
+  gmrf::DevBuf<double> a, w, base, out;
+};
+struct gmrf_regression {
+  std::unique_ptr<gmrf::RegressionPosterior> p;
+  gmrf_factor wrap;  // borrowed view of p's factor for the gmrf_factor_* entry points
 };
 struct gmrf_spacetime {
   gmrf::GnConfig cfg;
@@ -362,6 +374,15 @@ int gmrf_factor_stats(const gmrf_factor_t* f, gmrf_factor_stats_t* st) {
 
 void gmrf_factor_free(gmrf_factor_t* f) { delete f; }
 
+int gmrf_rng_draw(uint64_t seed, int64_t nu, int64_t nn, double* out) {
+  return guard([&] {
+    gmrf::require(nu >= 0 && nn >= 0, gmrf::kContract, "rng_draw: negative count");
+    gmrf::HostRng r(seed);
+    for (int64_t i = 0; i < nu; ++i) out[i] = r.uniform();
+    for (int64_t i = 0; i < nn; ++i) out[nu + i] = r.normal();
+  });
+}
+
 int gmrf_rng_fill(uint64_t seed, int32_t kind, int64_t n, double* out) {
   return guard([&] {
     gmrf::require(kind == 0 || kind == 1, gmrf::kContract, "rng_fill: kind must be 0 or 1");
@@ -539,6 +560,190 @@ int gmrf_spacetime_jacobian(gmrf_spacetime_t* h, const double* u, int64_t* rp_ou
 }
 
 void gmrf_spacetime_free(gmrf_spacetime_t* h) { delete h; }
+
+// ---- fixed-pattern Gram update ----------------------------------------------
+int gmrf_gram_create(const gmrf_symbolic_t* s, int32_t m, const int64_t* arp, const int32_t* aci,
+                     gmrf_gram_t** out) {
+  return guard([&] {
+    gmrf::require(m >= 0, gmrf::kDimension, "gram: negative row count");
+    auto h = std::make_unique<gmrf_gram>();
+    h->s = s->s;
+    h->m = m;
+    const gmrf::Symbolic& sy = *s->s;
+    h->g = std::make_unique<gmrf::GramPlan>(sy.n, sy.qcp.data(), sy.qri.data(), m, arp, aci,
+                                            nullptr, nullptr);
+    *out = h.release();
+  });
+}
+
+void gmrf_gram_free(gmrf_gram_t* g) { delete g; }
+
+namespace {
+// host arrays → the plan's device staging buffers
+void gram_stage(gmrf_gram_t* g, const double* base, const double* a, const double* w,
+                cudaStream_t st) {
+  const int64_t np = g->g->nnz_pattern(), na = g->g->nnz_a();
+  auto up = [&](gmrf::DevBuf<double>& b, const double* src, int64_t n) {
+    b.alloc(std::max<int64_t>(n, 1));
+    if (n) gmrf::cuda_check(cudaMemcpyAsync(b.p, src, n * 8, cudaMemcpyHostToDevice, st), "stage");
+  };
+  up(g->a, a, na);
+  if (w) up(g->w, w, g->m);
+  if (base) up(g->base, base, np);
+}
+}  // namespace
+
+int gmrf_gram_apply(gmrf_gram_t* g, const double* base, const double* a, const double* w, double c,
+                    double* out) {
+  return guard([&] {
+    gram_stage(g, base, a, w, nullptr);
+    g->out.alloc(std::max<int64_t>(g->g->nnz_pattern(), 1));
+    g->g->apply(g->a.p, w ? g->w.p : nullptr, c, base ? g->base.p : nullptr, g->out.p, nullptr,
+                nullptr, nullptr);
+    gmrf::cuda_check(cudaMemcpy(out, g->out.p, g->g->nnz_pattern() * 8, cudaMemcpyDeviceToHost),
+                     "gram out");
+  });
+}
+
+namespace {
+int update_fixed(gmrf_factor_t* f, gmrf_gram_t* g, const double* base, const double* a,
+                 const double* w, double c, int32_t* bad) {
+  int32_t b = -1;
+  const int rc = guard([&] {
+    gmrf::require(f->s.get() == g->s.get(), gmrf::kStructural,
+                  "update_fixed_pattern: plan built for another symbolic");
+    f->f->begin_numeric();
+    g->g->apply(a, w, c, base, nullptr, f->f->d_qmap(), f->f->d_l(), f->f->stream());
+    b = f->f->factor_panels();
+  });
+  if (bad) *bad = b;
+  if (rc == GMRF_OK && b >= 0) {
+    g_err = "cholesky: non-positive pivot at index " + std::to_string(b);
+    return GMRF_ERR_NOT_SPD;
+  }
+  return rc;
+}
+}  // namespace
+
+int gmrf_factor_update_fixed_pattern(gmrf_factor_t* f, gmrf_gram_t* g, const double* base,
+                                     const double* a, const double* w, double c, int32_t* bad) {
+  const int rc = guard([&] { gram_stage(g, base, a, w, f->f->stream()); });
+  if (rc != GMRF_OK) return rc;
+  return update_fixed(f, g, base ? g->base.p : nullptr, g->a.p, w ? g->w.p : nullptr, c, bad);
+}
+
+int gmrf_factor_update_fixed_pattern_device(gmrf_factor_t* f, gmrf_gram_t* g, const double* base,
+                                            const double* a, const double* w, double c,
+                                            int32_t* bad) {
+  return update_fixed(f, g, base, a, w, c, bad);
+}
+
+// ---- Matérn regression ----------------------------------------------------------
+namespace {
+gmrf::MeshSpec mesh_of(const gmrf_matern_config_t* c) {
+  gmrf::MeshSpec m;
+  m.dim = c->dim;
+  m.n_el = c->n_el;
+  m.xa = c->dim == 1 ? c->xa : 0.0;
+  m.xb = c->dim == 1 ? c->xb : 1.0;
+  gmrf::require(m.dim == 1 || m.dim == 2, gmrf::kContract, "mesh: dim must be 1 or 2");
+  gmrf::require(m.n_el >= 1, gmrf::kContract, "mesh: need at least one element");
+  gmrf::require(m.dim == 2 || m.xa < m.xb, gmrf::kContract, "build_interval_mesh: need a < b");
+  return m;
+}
+}  // namespace
+
+int gmrf_point_operator(const gmrf_matern_config_t* mesh, int32_t m, const double* pts,
+                        int64_t* rp, int32_t* ci, double* v) {
+  return guard([&] {
+    std::vector<int64_t> r;
+    std::vector<int32_t> c;
+    std::vector<double> x;
+    gmrf::point_operator(mesh_of(mesh), m, pts, r, c, x);
+    if (rp) std::memcpy(rp, r.data(), r.size() * sizeof(int64_t));
+    if (ci) std::memcpy(ci, c.data(), c.size() * sizeof(int32_t));
+    if (v) std::memcpy(v, x.data(), x.size() * sizeof(double));
+  });
+}
+
+int gmrf_matern_prior(const gmrf_matern_config_t* cfg, int32_t* n, int64_t* cp, int32_t* ri,
+                      double* v) {
+  return guard([&] {
+    gmrf::RegressionPosterior p(mesh_of(cfg), gmrf::MaternSpec{cfg->kappa, cfg->alpha, cfg->tau},
+                                0, nullptr, nullptr);
+    std::vector<int64_t> c;
+    std::vector<int32_t> r;
+    std::vector<double> q, qp;
+    p.copy_precisions(c, r, q, qp);
+    if (n) *n = p.n();
+    if (cp) std::memcpy(cp, c.data(), c.size() * sizeof(int64_t));
+    if (ri) std::memcpy(ri, r.data(), r.size() * sizeof(int32_t));
+    if (v) std::memcpy(v, q.data(), q.size() * sizeof(double));
+  });
+}
+
+int gmrf_regression_create(const gmrf_matern_config_t* cfg, int32_t m, const double* pts,
+                           const int32_t* perm, gmrf_regression_t** out) {
+  return guard([&] {
+    auto h = std::make_unique<gmrf_regression>();
+    h->p = std::make_unique<gmrf::RegressionPosterior>(
+        mesh_of(cfg), gmrf::MaternSpec{cfg->kappa, cfg->alpha, cfg->tau}, m, pts, perm);
+    h->wrap.s = h->p->symbolic_ptr();
+    h->wrap.f.reset(&h->p->factor());
+    *out = h.release();
+  });
+}
+
+int gmrf_regression_run(gmrf_regression_t* h, const double* y, const double* lam, int32_t want_var,
+                        int32_t ns, uint64_t seed, double* mean, double* var, double* samples) {
+  return guard([&] {
+    h->p->run(y, lam, want_var != 0, ns, seed);
+    const size_t n = static_cast<size_t>(h->p->n());
+    if (mean) gmrf::cuda_check(cudaMemcpy(mean, h->p->d_mean(), n * 8, cudaMemcpyDeviceToHost), "mean");
+    if (var && want_var)
+      gmrf::cuda_check(cudaMemcpy(var, h->p->d_var(), n * 8, cudaMemcpyDeviceToHost), "var");
+    if (samples && ns > 0)
+      gmrf::cuda_check(
+          cudaMemcpy(samples, h->p->d_samples(), n * ns * 8, cudaMemcpyDeviceToHost), "samples");
+  });
+}
+
+int gmrf_regression_info(const gmrf_regression_t* h, gmrf_regression_info_t* info) {
+  return guard([&] {
+    const auto& s = h->p->symbolic();
+    info->n = h->p->n();
+    info->m = h->p->m();
+    info->nnz_pattern = static_cast<int64_t>(s.qri.size());
+    info->nnz_l = s.nnz_l;
+    info->setup_host_ms = h->p->times().setup_host_ms;
+    info->run_ms = h->p->times().total_ms;
+    info->flops_ref = s.flops_ref;
+    info->kernel_launches = h->p->times().kernel_launches;
+  });
+}
+
+int gmrf_regression_precisions(const gmrf_regression_t* h, int64_t* cp, int32_t* ri, double* qpr,
+                               double* qpo) {
+  return guard([&] {
+    std::vector<int64_t> c;
+    std::vector<int32_t> r;
+    std::vector<double> a, b;
+    h->p->copy_precisions(c, r, a, b);
+    if (cp) std::memcpy(cp, c.data(), c.size() * sizeof(int64_t));
+    if (ri) std::memcpy(ri, r.data(), r.size() * sizeof(int32_t));
+    if (qpr) std::memcpy(qpr, a.data(), a.size() * 8);
+    if (qpo) std::memcpy(qpo, b.data(), b.size() * 8);
+  });
+}
+
+gmrf_factor_t* gmrf_regression_factor(gmrf_regression_t* h) {
+  return nullptr == h ? nullptr : &h->wrap;
+}
+
+void gmrf_regression_free(gmrf_regression_t* h) {
+  if (h) h->wrap.f.release();  // borrowed: owned by the posterior
+  delete h;
+}
 
 int gmrf_spacetime_set_profile(gmrf_spacetime_t* h, int32_t on) {
   return guard([&] {

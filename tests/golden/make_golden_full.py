@@ -85,7 +85,9 @@ def _record_floor(name, b):
         for k in ("gn_objective", "gn_decrement"):
             v = b.vec(k)
             if len(v) == len(z[k]):
-                f[k.replace("gn_", "")] = float(np.max(np.abs(v - z[k]) / np.abs(z[k])))
+                d = np.abs(v - z[k]) / np.abs(z[k])
+                f[k.replace("gn_", "")] = float(np.max(d))
+                f[k.replace("gn_", "") + "_per_iter"] = [float(x) for x in d]
         f["same_trace"] = bool(np.array_equal(b.vec("gn_backtracks"), z["gn_backtracks"]))
     path = os.path.join(HERE, "floors.json")
     floors = json.load(open(path)) if os.path.exists(path) else {}
@@ -140,7 +142,19 @@ def allen_cahn(n_cells, n_t, name, gn_iters=8, floor=False):
     _save(name, out, b, time.time() - t0)
 
 
+def matern(dim, name, floor=False):
+    """C1 / C2 regression (make_golden.matern1d / matern2d parameters); floor runs
+    only (the full fixtures are make_golden.py's)."""
+    p = ([999, 20.0, 2, 1.0, 100, 1001, 1e4, 0.01, 8, 2001, 1] if dim == 1 else
+         [255, 10.0, 2, 1.0, 2000, 1002, 400.0, 0.05, 2, 2002, 1])
+    assert floor and MODE["tag"] == "/order", "regression fixtures come from make_golden.py"
+    b = Ref(MODE["so"]).build("matern1d" if dim == 1 else "matern2d", p)
+    return _record_floor(name, b)
+
+
 JOBS = {
+    "c1": lambda fl: matern(1, "c1_matern1d.npz", fl),
+    "c2": lambda fl: matern(2, "c2_matern2d.npz", fl),
     "c4": lambda fl: burgers(999, 1000, 10, "c4_burgers_full.npz", fl),
     "c4_200": lambda fl: burgers(199, 200, 10, "c4_burgers_200.npz", fl),
     "c4_500": lambda fl: burgers(499, 500, 10, "c4_burgers_500.npz", fl),

@@ -87,7 +87,7 @@ def test_heat_posterior_vs_reference(port):
     a = golden_mat(z, "A_ic").to_scipy()
     rhs = a.T @ (z["noise_ic"] * z["y_ic"])
     floor, _ = ordering_floor(port, qref, rhs)
-    assert rel(mean, z["mean_post"]) <= max(10 * floor, 1e-12), (rel(mean, z["mean_post"]), floor)
+    assert rel(mean, z["mean_post"]) <= max(10 * floor, 1e-10), (rel(mean, z["mean_post"]), floor)
     assert rel(var, z["var_post"]) <= 1e-8
 
 
@@ -102,12 +102,12 @@ def test_burgers_gn_laplace_vs_reference(port):
     np.testing.assert_array_equal([t.step_size for t in trace], z["gn_step"])
     obj = np.array([t.objective for t in trace])
     dec = np.array([t.decrement for t in trace])
-    assert np.max(np.abs(obj - z["gn_objective"]) / np.abs(z["gn_objective"])) <= 1e-6
-    assert np.max(np.abs(dec - z["gn_decrement"]) / np.abs(z["gn_decrement"])) <= 1e-4
+    assert np.max(np.abs(obj - z["gn_objective"]) / np.abs(z["gn_objective"])) <= 1e-8
+    assert np.max(np.abs(dec - z["gn_decrement"]) / np.abs(z["gn_decrement"])) <= 1e-6
     qla = golden_mat(z, "Q_la").to_scipy()
     floor, _ = ordering_floor(port, qla, qla @ z["mode"])
-    assert rel(mean, z["mode"]) <= max(100 * floor, 1e-8), (rel(mean, z["mode"]), floor)
-    assert rel(var, z["var_post"]) <= 1e-6
+    assert rel(mean, z["mode"]) <= max(10 * floor, 1e-10), (rel(mean, z["mode"]), floor)
+    assert rel(var, z["var_post"]) <= 1e-8
 
 
 # ---- config 5 shape: 2-D unit square, Allen-Cahn residual -------------------
@@ -150,11 +150,11 @@ def test_allen_cahn_gn_laplace_vs_reference(port):
     np.testing.assert_array_equal([t.backtracks for t in trace], z["gn_backtracks"])
     np.testing.assert_array_equal([t.step_size for t in trace], z["gn_step"])
     obj = np.array([t.objective for t in trace])
-    assert np.max(np.abs(obj - z["gn_objective"]) / np.abs(z["gn_objective"])) <= 1e-6
+    assert np.max(np.abs(obj - z["gn_objective"]) / np.abs(z["gn_objective"])) <= 1e-8
     qla = golden_mat(z, "Q_la").to_scipy()
     floor, _ = ordering_floor(port, qla, qla @ z["mode"])
-    assert rel(mean, z["mode"]) <= max(100 * floor, 1e-8), (rel(mean, z["mode"]), floor)
-    assert rel(var, z["var_post"]) <= 1e-6
+    assert rel(mean, z["mode"]) <= max(10 * floor, 1e-10), (rel(mean, z["mode"]), floor)
+    assert rel(var, z["var_post"]) <= 1e-8
 
 
 def test_gn_stagnation_carries_trace():
