@@ -198,6 +198,104 @@ def fp64_peak_tflops():
 
 
 # ---------------------------------------------------------------------------
+# sub-records of the default run: config 2 end to end against the reference
+# measured on this host, and the config-5 shape one B200 holds
+# ---------------------------------------------------------------------------
+def _rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(b))
+
+
+def run_c2(steps, warmup, with_reference=True):
+    """Config 2 (2D Matérn regression, 256² nodes, 2000 points, mean + Takahashi
+    variances + 16 samples) through the product's public API, e2e from host data
+    (points in at setup; y, Λ in and mean, variances, samples out per step), and
+    the unmodified reference (oracle/_ref) on the same seeded inputs, measured
+    single-threaded on this host (no extrapolation)."""
+    import torch
+    from paper_2503_08343_b200.regression import RegressionPosterior, seeded_inputs
+    mesh, spec, pts, y, lam, ns, seed = seeded_inputs(2)
+    t0 = time.perf_counter()
+    post = RegressionPosterior(mesh, spec, pts)
+    setup_s = time.perf_counter() - t0
+    for _ in range(max(warmup, 1)):
+        post.run(y, lam, True, ns, seed)
+    torch.cuda.synchronize()
+    dev_ms, e2e = [], []
+    for _ in range(steps):
+        w0 = time.perf_counter()
+        mean, var, smp = post.run(y, lam, True, ns, seed)
+        e2e.append(time.perf_counter() - w0)
+        dev_ms.append(post.info().run_ms)
+    info = post.info()
+    out = {"workload": "config 2: 2D Matern regression posterior, P1 256x256 nodes (n=65,536), "
+                       "2000 seeded points, mean + Takahashi variances + 16 samples",
+           "value": float(np.median(dev_ms)) * 1e-3, "unit": "s",
+           "e2e": {"value": float(np.median(e2e)), "unit": "s",
+                   "h2d_bytes_per_step": 16 * post.m,
+                   "d2h_bytes_per_step": 8 * post.n * (2 + ns)},
+           "host_setup_s": setup_s, "nnz_l": info.nnz_l, "gpu_launches": int(info.kernel_launches),
+           "timing": "value: CUDA events around the device pipeline (y upload .. samples), median "
+                     "of steps; e2e: wall clock of RegressionPosterior.run incl. copies"}
+    if with_reference:
+        try:
+            from oracle.pyoracle import Ref
+            w0 = time.perf_counter()
+            b = Ref().build("matern2d", [255, 10.0, 2, 1.0, 2000, 1002, 400.0, 0.05, ns, 2002, 1])
+            ref_s = time.perf_counter() - w0
+            out["reference"] = {
+                "value": ref_s, "unit": "s", "cores": 1, "kind": "reference",
+                "sample": "the full config-2 chain (matern_prior, point_observation_operator, "
+                          "condition_on = AMD + factor + solve, variance_takahashi, 16 "
+                          "sample_direct), unmodified reference, measured (not extrapolated)",
+                "stages_s": {k: b.scalar(k) for k in ("t_prior", "t_condition", "t_variance",
+                                                      "t_samples")}}
+            out["speedup_e2e"] = ref_s / out["e2e"]["value"]
+            out["parity"] = {"mean_rel": _rel(mean, b.vec("mean_post")),
+                             "var_rel": _rel(var, b.vec("var_post"))}
+        except Exception as exc:  # oracle/_ref absent on this box
+            out["reference"] = {"value": None, "unavailable": str(exc)}
+    return out
+
+
+def run_c5(n_cells, n_t, steps, warmup, peak_fp64):
+    """The config-5 shape one B200 holds (Allen-Cahn, 8 GN steps + Laplace +
+    variances, seed 1005): device seconds per posterior and the Cholesky's
+    fraction of the FP64 peak."""
+    import torch
+    from paper_2503_08343_b200 import Rng
+    from paper_2503_08343_b200.spacetime import (GaussNewtonConfig, SpaceTimePosterior,
+                                                 SpaceTimeSpec)
+    spec = SpaceTimeSpec.allen_cahn(n_cells=n_cells, n_t=n_t)
+    t0 = time.perf_counter()
+    post = SpaceTimePosterior(spec, GaussNewtonConfig(max_iters=8))
+    setup_s = time.perf_counter() - t0
+    u0 = -0.1 + 0.2 * Rng(1005).uniforms(spec.n_space)
+    for _ in range(max(warmup, 1)):
+        post.run(u0, variances=True, copy_back=False)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(steps):
+        _, _, trace, _ = post.run(u0, variances=True, copy_back=False)
+    e1.record()
+    torch.cuda.synchronize()
+    info = post.info()
+    numeric_ms = info.numeric_ms / max(info.n_factorizations, 1)
+    tf = info.flops_ref / (numeric_ms * 1e-3) / 1e12
+    nn = n_cells + 1
+    return {"workload": f"config-5 shape: Allen-Cahn GN-Laplace posterior, {nn}x{nn} nodes x "
+                        f"{n_t} slices (n={post.n:,}), 8 GN steps + Laplace + variances, seed 1005",
+            "value": e0.elapsed_time(e1) / steps * 1e-3, "unit": "s", "host_setup_s": setup_s,
+            "cholesky_fp64": {"tflops": tf, "frac": tf / peak_fp64,
+                              "numeric_ms_per_factorization": numeric_ms,
+                              "factorizations_per_step": info.n_factorizations},
+            "phases_ms": {"gauss_newton": info.gn_ms, "laplace": info.laplace_ms,
+                          "variances": info.selinv_ms},
+            "gn_steps": len(trace), "nnz_l": info.nnz_l,
+            "factor_device_gb": info.factor_device_bytes / 1e9}
+
+
+# ---------------------------------------------------------------------------
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -207,6 +305,9 @@ def main():
     ap.add_argument("--n-el", type=int, default=999)
     ap.add_argument("--n-t", type=int, default=1000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the config-2 (with its measured reference) and config-5-shape "
+                         "sub-records of the default run")
     ap.add_argument("--workload", choices=["c4", "c5"], default="c4",
                     help="c4 (default, the headline): config-4 Burgers posterior at full size; "
                          "c5: config-5 Allen-Cahn posterior at the largest shape one B200 holds "
@@ -401,12 +502,21 @@ def main():
                 out["fp64_frac"] = out["tflops"] / peak_fp64
         return out
 
+    fac_row = agg("factor.")
+    for k in ("gbs", "hbm_frac"):  # extend-add bytes over all factor time: not a roofline
+        fac_row.pop(k, None)
+    fac_row["profiled_tflops"] = fac_row.pop("tflops", None)
+    fac_row["profiled_fp64_frac"] = fac_row.pop("fp64_frac", None)
+    fac_row["graph_tflops"] = chol_tflops
+    fac_row["graph_fp64_frac"] = chol_tflops / peak_fp64
     rows = {"1_assembly": agg("assemble."), "2_conditioning_update": agg("update."),
-            "3_factorization": {**agg("factor."), "tflops": chol_tflops,
-                                "fp64_frac": chol_tflops / peak_fp64},
+            "3_factorization": fac_row,
             "4_solves": agg("solve."), "5_selected_inversion": agg("selinv."),
+            "residual_jacobian": agg("residual."),
             "note": "profiled (serialized) kernel time per step; bytes = algorithmic (DESIGN.md §3); "
-                    "factorization tflops = Sigma c_j^2 / numeric time"}
+                    "factorization: profiled_* = executed (padded) flops over the serialized "
+                    "profiled kernels, graph_* = Sigma c_j^2 over the CUDA-graph numeric time "
+                    "(the headline)"}
 
     if rank != 0:
         if world > 1:
@@ -451,6 +561,11 @@ def main():
         except Exception as exc:  # oracle/_ref missing on this box
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference",
                                     "sample": f"unavailable: {exc}"}
+    if world == 1 and not c5 and not args.no_extras:
+        del post
+        torch.cuda.empty_cache()
+        line["c2"] = run_c2(args.steps, args.warmup, with_reference=not args.no_cpu_baseline)
+        line["c5_shape"] = run_c5(args.c5_cells, args.c5_slices, 1, 1, peak_fp64)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -648,27 +648,33 @@ double SpaceTimePosterior::dot(const double* a, const double* b, i64 n) {
   return out;
 }
 
+// Residual rows and Jacobian values (HBM-bound: the state slices s, s+1 of
+// each row's stencil read, one value written per row / per J entry).
 void SpaceTimePosterior::eval_residual(const double* d_u, double* d_f) {
-  if (spec_.residual == 2) {
-    k_ac_res<<<grid_for(nres_), 256, 0, stream_>>>(ac_dev(), d_u, d_f);
-    times_.kernel_launches += 1;
-    return;
-  }
-  BurgersDev B{ns_, nt_, static_cast<int>(kept_.n), spec_.diffusion, d_xn_.p, d_dts_.p,
-               d_slack_.p, kept_.p};
-  k_burgers_res<<<grid_for(nres_), 256, 0, stream_>>>(B, d_u, d_f);
+  const double bytes = 8.0 * nres_ + 16.0 * n_;
+  prof_.run(stream_, "residual.eval", 0.0, bytes, [&] {
+    if (spec_.residual == 2) {
+      k_ac_res<<<grid_for(nres_), 256, 0, stream_>>>(ac_dev(), d_u, d_f);
+    } else {
+      BurgersDev B{ns_, nt_, static_cast<int>(kept_.n), spec_.diffusion, d_xn_.p, d_dts_.p,
+                   d_slack_.p, kept_.p};
+      k_burgers_res<<<grid_for(nres_), 256, 0, stream_>>>(B, d_u, d_f);
+    }
+  });
   times_.kernel_launches += 1;
 }
 
 void SpaceTimePosterior::eval_jacobian(const double* d_u) {
-  if (spec_.residual == 2) {
-    k_ac_jac<<<grid_for(nres_), 256, 0, stream_>>>(ac_dev(), d_u, d_jrp_.p, d_jv_.p);
-    times_.kernel_launches += 1;
-    return;
-  }
-  BurgersDev B{ns_, nt_, static_cast<int>(kept_.n), spec_.diffusion, d_xn_.p, d_dts_.p,
-               d_slack_.p, kept_.p};
-  k_burgers_jac<<<grid_for(nres_), 256, 0, stream_>>>(B, d_u, d_jrp_.p, d_jv_.p);
+  const double bytes = 8.0 * static_cast<double>(jci_.size()) + 8.0 * nres_ + 16.0 * n_;
+  prof_.run(stream_, "residual.jacobian", 0.0, bytes, [&] {
+    if (spec_.residual == 2) {
+      k_ac_jac<<<grid_for(nres_), 256, 0, stream_>>>(ac_dev(), d_u, d_jrp_.p, d_jv_.p);
+    } else {
+      BurgersDev B{ns_, nt_, static_cast<int>(kept_.n), spec_.diffusion, d_xn_.p, d_dts_.p,
+                   d_slack_.p, kept_.p};
+      k_burgers_jac<<<grid_for(nres_), 256, 0, stream_>>>(B, d_u, d_jrp_.p, d_jv_.p);
+    }
+  });
   times_.kernel_launches += 1;
 }
 
