@@ -246,6 +246,41 @@ int gmrf_factor_update_fixed_pattern_device(gmrf_factor_t* f, gmrf_gram_t* g, co
                                             const double* d_a_values, const double* d_w, double c,
                                             int32_t* bad_index);
 
+/* Update system: H = symmetrize(B + Aᵀ diag(w) A) on the fixed union pattern
+ * and its device factor, B = Q (base_kind 0: b_* is Q, n × n CSC with values)
+ * or B = symmetrize(S Sᵀ) (base_kind 1: b_* is S, n × b_cols CSC). A: m × n CSC
+ * pattern; its values (same CSC order) and w arrive per refactor. perm: the
+ * factor's ordering (new -> old), NULL for nested dissection. One object per
+ * update site of the reference: condition_affine (gmrf.hpp:150-161),
+ * gauss_newton (gauss_newton.hpp:110-141), laplace_posterior (:228-232) —
+ * the drop-in headers under paper_2503_08343_b200/include use it. */
+typedef struct gmrf_update_system gmrf_update_system_t;
+int gmrf_update_system_create(int32_t n, int32_t base_kind, int32_t b_cols, const int64_t* b_col_ptr,
+                              const int32_t* b_row_idx, const double* b_values, int32_t m,
+                              const int64_t* a_col_ptr, const int32_t* a_row_idx,
+                              const int32_t* perm, gmrf_update_system_t** out);
+/* 1 if (m, A's CSC pattern) is the one the system was built for, else 0. */
+int gmrf_update_system_same_operator(const gmrf_update_system_t* h, int32_t m,
+                                     const int64_t* a_col_ptr, const int32_t* a_row_idx);
+/* H from A's values and w, factorized; GMRF_ERR_NOT_SPD with *bad_index as
+ * gmrf_factor_numeric. */
+int gmrf_update_system_refactor(gmrf_update_system_t* h, const double* a_values, const double* w,
+                                int32_t* bad_index);
+/* H's values only (no factorization), into values[nnz] in the union pattern's
+ * order: symmetrize(B + c · Aᵀ diag(w) A) — e.g. the Matérn precision with
+ * B = 0, A = K̂, w = 1/m̃, c = 1/τ² (priors/matern.hpp:70-80). */
+int gmrf_update_system_assemble(gmrf_update_system_t* h, const double* a_values, const double* w,
+                                double c, double* values);
+/* The union pattern (col_ptr[n+1]; row_idx == NULL queries) and H's values of
+ * the last refactor / assemble (values may be NULL). */
+int gmrf_update_system_matrix(const gmrf_update_system_t* h, int64_t* col_ptr, int32_t* row_idx,
+                              double* values);
+/* Borrowed views, valid while the system lives: its symbolic and its factor
+ * (for gmrf_solve*, gmrf_selinv_*, gmrf_sample_direct, gmrf_factor_l). */
+const gmrf_symbolic_t* gmrf_update_system_symbolic(const gmrf_update_system_t* h);
+gmrf_factor_t* gmrf_update_system_factor(gmrf_update_system_t* h);
+void gmrf_update_system_free(gmrf_update_system_t* h);
+
 /* ---- Matérn SPDE regression posterior (configs 1-2) -------------------------
  * P1 FEM on an interval (dim 1: n_el elements over [xa, xb],
  * build_interval_mesh, fem/mesh.hpp:63) or the unit square (dim 2: n_el × n_el

@@ -19,6 +19,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 PORT_SO = os.path.join(HERE, "_build", "liboracle.so")
 REF_SO = os.path.join(HERE, "_ref", "libgmrfref.so")
 REF_ND_SO = os.path.join(HERE, "_ref", "libgmrfref_nd.so")
+# the same reference chains compiled against the drop-in headers (the B200 engine
+# behind the reference API); not a checker — what tests/test_gpu_dropin.py checks
+REF_B200_SO = os.path.join(HERE, "_ref", "libgmrfref_b200.so")
 
 i32p = C.POINTER(C.c_int32)
 i64p = C.POINTER(C.c_int64)

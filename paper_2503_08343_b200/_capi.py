@@ -156,6 +156,15 @@ SIGNATURES = {
     "gmrf_spacetime_free": (None, [vp]),
     "gmrf_spacetime_set_profile": (C.c_int, [vp, C.c_int32]),
     "gmrf_gram_create": (C.c_int, [vp, C.c_int32, i64p, i32p, C.POINTER(vp)]),
+    "gmrf_update_system_create": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, i64p, i32p, f64p,
+                                            C.c_int32, i64p, i32p, i32p, C.POINTER(vp)]),
+    "gmrf_update_system_same_operator": (C.c_int, [vp, C.c_int32, i64p, i32p]),
+    "gmrf_update_system_refactor": (C.c_int, [vp, f64p, f64p, i32p]),
+    "gmrf_update_system_matrix": (C.c_int, [vp, i64p, i32p, f64p]),
+    "gmrf_update_system_assemble": (C.c_int, [vp, f64p, f64p, C.c_double, f64p]),
+    "gmrf_update_system_symbolic": (vp, [vp]),
+    "gmrf_update_system_factor": (vp, [vp]),
+    "gmrf_update_system_free": (None, [vp]),
     "gmrf_gram_free": (None, [vp]),
     "gmrf_gram_apply": (C.c_int, [vp, f64p, f64p, f64p, C.c_double, f64p]),
     "gmrf_factor_update_fixed_pattern": (C.c_int, [vp, vp, f64p, f64p, f64p, C.c_double, i32p]),

@@ -14,6 +14,7 @@
 #include "rng.hpp"
 #include "gram.hpp"
 #include "regression.hpp"
+#include "update_system.hpp"
 #include "spacetime.hpp"
 
 static_assert(sizeof(gmrf_msg_t) == sizeof(gmrf::XferMsg), "gmrf_msg_t layout");
@@ -37,6 +38,11 @@ struct gmrf_gram {
 struct gmrf_regression {
   std::unique_ptr<gmrf::RegressionPosterior> p;
   gmrf_factor wrap;  // borrowed view of p's factor for the gmrf_factor_* entry points
+};
+struct gmrf_update_system {
+  std::unique_ptr<gmrf::UpdateSystem> u;
+  gmrf_symbolic sym;  // views
+  gmrf_factor fac;
 };
 struct gmrf_spacetime {
   gmrf::GnConfig cfg;
@@ -636,6 +642,66 @@ int gmrf_factor_update_fixed_pattern_device(gmrf_factor_t* f, gmrf_gram_t* g, co
                                             const double* a, const double* w, double c,
                                             int32_t* bad) {
   return update_fixed(f, g, base, a, w, c, bad);
+}
+
+// ---- update system ------------------------------------------------------------------
+int gmrf_update_system_create(int32_t n, int32_t kind, int32_t bcols, const int64_t* bcp,
+                              const int32_t* bri, const double* bv, int32_t m, const int64_t* acp,
+                              const int32_t* ari, const int32_t* perm,
+                              gmrf_update_system_t** out) {
+  return guard([&] {
+    auto h = std::make_unique<gmrf_update_system>();
+    h->u = std::make_unique<gmrf::UpdateSystem>(n, kind, bcols, bcp, bri, bv, m, acp, ari, perm);
+    h->sym.s = h->u->symbolic();
+    h->fac.s = h->u->symbolic();
+    h->fac.f.reset(&h->u->factor());
+    *out = h.release();
+  });
+}
+
+int gmrf_update_system_same_operator(const gmrf_update_system_t* h, int32_t m, const int64_t* acp,
+                                     const int32_t* ari) {
+  return h->u->same_operator(m, acp, ari) ? 1 : 0;
+}
+
+int gmrf_update_system_refactor(gmrf_update_system_t* h, const double* a, const double* w,
+                                int32_t* bad) {
+  int32_t b = -1;
+  const int rc = guard([&] { b = h->u->refactor(a, w); });
+  if (bad) *bad = b;
+  if (rc == GMRF_OK && b >= 0) {
+    g_err = "cholesky: non-positive pivot at index " + std::to_string(b);
+    return GMRF_ERR_NOT_SPD;
+  }
+  return rc;
+}
+
+int gmrf_update_system_assemble(gmrf_update_system_t* h, const double* a, const double* w, double c,
+                                double* v) {
+  return guard([&] {
+    h->u->assemble(a, w, c);
+    if (v) h->u->copy_values(v);
+  });
+}
+
+int gmrf_update_system_matrix(const gmrf_update_system_t* h, int64_t* cp, int32_t* ri, double* v) {
+  return guard([&] {
+    const auto& c = h->u->col_ptr();
+    if (cp) std::memcpy(cp, c.data(), c.size() * sizeof(int64_t));
+    if (ri) std::memcpy(ri, h->u->row_idx().data(), h->u->row_idx().size() * sizeof(int32_t));
+    if (v) h->u->copy_values(v);
+  });
+}
+
+const gmrf_symbolic_t* gmrf_update_system_symbolic(const gmrf_update_system_t* h) {
+  return &h->sym;
+}
+
+gmrf_factor_t* gmrf_update_system_factor(gmrf_update_system_t* h) { return &h->fac; }
+
+void gmrf_update_system_free(gmrf_update_system_t* h) {
+  if (h) h->fac.f.release();  // borrowed view of the system's factor
+  delete h;
 }
 
 // ---- Matérn regression ----------------------------------------------------------

@@ -22,8 +22,8 @@ __global__ void k_gram_weight(i64 na, const i32* __restrict__ arow, const double
 __global__ void k_gram(i64 ne, const i64* __restrict__ ent, const i64* __restrict__ off,
                        const int2* __restrict__ pairs, const double* __restrict__ a,
                        const double* __restrict__ wa, double c, const double* __restrict__ base,
-                       double* __restrict__ out, const i64* __restrict__ qmap,
-                       double* __restrict__ L) {
+                       const i64* __restrict__ tpos, double* __restrict__ out,
+                       const i64* __restrict__ qmap, double* __restrict__ L) {
   for (i64 t = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; t < ne;
        t += static_cast<i64>(gridDim.x) * blockDim.x) {
     const i64 p = ent ? ent[t] : t;
@@ -36,7 +36,8 @@ __global__ void k_gram(i64 ne, const i64* __restrict__ ent, const i64* __restric
       s2 += ay * wa[xy.x];
     }
     const double b = base ? base[p] : 0.0;
-    const double v = 0.5 * (b + c * s1) + 0.5 * (b + c * s2);
+    const double bt = base && tpos ? base[tpos[t]] : b;
+    const double v = 0.5 * (b + c * s1) + 0.5 * (bt + c * s2);
     if (out) out[p] = v;
     if (L) {
       const i64 o = qmap[p];
@@ -52,7 +53,8 @@ int grid_of(i64 n) {
 }  // namespace
 
 GramPlan::GramPlan(i32 n, const i64* pcp, const i32* pri, i32 m, const i64* arp, const i32* aci,
-                   const std::vector<char>* need, cudaStream_t stream) {
+                   const std::vector<char>* need, cudaStream_t stream, const i64* vmap,
+                   bool base_transpose) {
   m_ = m;
   np_ = pcp[n];
   na_ = arp[m];
@@ -73,14 +75,16 @@ GramPlan::GramPlan(i32 n, const i64* pcp, const i32* pri, i32 m, const i64* arp,
         require(i == arp[k] || aci[i] > aci[i - 1], kStructural,
                 "gram: operator columns must be strictly ascending per row");
         const i64 q = nx[aci[i]]++;
+        const i64 vi = vmap ? vmap[i] : i;
+        require(vi >= 0 && vi < na_, kDimension, "gram: value map out of range");
         ak[q] = k;
-        av[q] = static_cast<i32>(i);
-        arow[i] = k;
+        av[q] = static_cast<i32>(vi);
+        arow[vi] = k;
       }
   }
   require(na_ < (1ll << 31), kContract, "gram: operator nnz exceeds int32 value indices");
   // product map over the computed entries
-  std::vector<i64> ent, off(1, 0);
+  std::vector<i64> ent, off(1, 0), tpos;
   std::vector<int2> pr;
   i64 covered = 0;
   for (i32 C = 0; C < n; ++C)
@@ -105,6 +109,13 @@ GramPlan::GramPlan(i32 n, const i64* pcp, const i32* pri, i32 m, const i64* arp,
       if (want) {
         if (need) ent.push_back(p);
         off.push_back(static_cast<i64>(pr.size()));
+        if (base_transpose) {  // position of (C, R): binary search in column R
+          const i32* b0 = pri + pcp[R];
+          const i32* b1 = pri + pcp[R + 1];
+          const i32* f = std::lower_bound(b0, b1, C);
+          require(f != b1 && *f == C, kStructural, "gram: pattern is not symmetric");
+          tpos.push_back(pcp[R] + (f - b0));
+        }
       }
     }
   // every product A_kR A_kC must have a home in the pattern
@@ -118,6 +129,7 @@ GramPlan::GramPlan(i32 n, const i64* pcp, const i32* pri, i32 m, const i64* arp,
   pairs_.upload(pr, stream);
   arow_.upload(arow, stream);
   wa_.alloc(std::max<i64>(na_, 1));
+  if (base_transpose) tpos_.upload(tpos, stream);
   if (need) {
     ent_.upload(ent, stream);
     ne_ = static_cast<i64>(ent.size());
@@ -136,8 +148,59 @@ void GramPlan::apply(const double* d_a, const double* d_w, double c, const doubl
   }
   if (ne_ > 0)
     k_gram<<<grid_of(ne_), 256, 0, stream>>>(ne_, ent_.p, off_.p, pairs_.p, d_a, wa, c, d_base,
-                                             d_out, d_qmap, d_L);
+                                             tpos_.p, d_out, d_qmap, d_L);
   cuda_check(cudaGetLastError(), "gram apply");
+}
+
+void gram_pattern(i32 n, i32 m, const i64* arp, const i32* aci, std::vector<i64>& cp,
+                  std::vector<i32>& ri) {
+  // columns of A: rows k touching column j
+  std::vector<i64> acp(static_cast<size_t>(n) + 1, 0);
+  for (i64 p = 0; p < arp[m]; ++p) acp[aci[p] + 1]++;
+  for (i32 j = 0; j < n; ++j) acp[j + 1] += acp[j];
+  std::vector<i32> ak(acp[n]);
+  {
+    std::vector<i64> nx(acp.begin(), acp.end() - 1);
+    for (i32 k = 0; k < m; ++k)
+      for (i64 p = arp[k]; p < arp[k + 1]; ++p) ak[nx[aci[p]]++] = k;
+  }
+  cp.assign(static_cast<size_t>(n) + 1, 0);
+  ri.clear();
+  std::vector<i32> mark(n, -1), col;
+  for (i32 j = 0; j < n; ++j) {
+    col.clear();
+    mark[j] = j;
+    col.push_back(j);  // the diagonal is always stored
+    for (i64 q = acp[j]; q < acp[j + 1]; ++q) {
+      const i32 k = ak[q];
+      for (i64 p = arp[k]; p < arp[k + 1]; ++p)
+        if (mark[aci[p]] != j) {
+          mark[aci[p]] = j;
+          col.push_back(aci[p]);
+        }
+    }
+    std::sort(col.begin(), col.end());
+    ri.insert(ri.end(), col.begin(), col.end());
+    cp[j + 1] = static_cast<i64>(ri.size());
+  }
+}
+
+void pattern_union(i32 n, const std::vector<i64>& acp, const std::vector<i32>& ari,
+                   const std::vector<i64>& bcp, const std::vector<i32>& bri, std::vector<i64>& cp,
+                   std::vector<i32>& ri) {
+  cp.assign(static_cast<size_t>(n) + 1, 0);
+  ri.clear();
+  ri.reserve(ari.size() + bri.size());
+  for (i32 j = 0; j < n; ++j) {
+    i64 a = acp[j], b = bcp[j];
+    while (a < acp[j + 1] || b < bcp[j + 1]) {
+      const i32 ra = a < acp[j + 1] ? ari[a] : n, rb = b < bcp[j + 1] ? bri[b] : n;
+      ri.push_back(std::min(ra, rb));
+      if (ra <= rb) ++a;
+      if (rb <= ra) ++b;
+    }
+    cp[j + 1] = static_cast<i64>(ri.size());
+  }
 }
 
 int GramPlan::launches(bool weighted) const { return (weighted && na_ > 0 ? 1 : 0) + (ne_ > 0); }

@@ -33,6 +33,14 @@
 
 namespace gmrf {
 
+// Full symmetric CSC pattern of AᵀA for an m × n CSR operator (with the diagonal).
+void gram_pattern(i32 n, i32 m, const i64* arp, const i32* aci, std::vector<i64>& cp,
+                  std::vector<i32>& ri);
+// Union of two sorted CSC patterns with n columns.
+void pattern_union(i32 n, const std::vector<i64>& acp, const std::vector<i32>& ari,
+                   const std::vector<i64>& bcp, const std::vector<i32>& bri, std::vector<i64>& cp,
+                   std::vector<i32>& ri);
+
 class GramPlan {
  public:
   // Pattern P: n × n full symmetric CSC (pcp, pri). A: m × n, CSR (arp, aci),
@@ -40,8 +48,13 @@ class GramPlan {
   // (StructuralError otherwise). lower_only: build sums only for entries with
   // R >= C in the pattern's own numbering that `need` marks (need == nullptr:
   // all entries).
+  // vmap (optional): CSR position → index of that value in the caller's value
+  // array (e.g. A handed over in CSC order). base_transpose: the base is not
+  // assumed exactly symmetric — the (C, R) half of the average uses base(C, R)
+  // (the reference symmetrizes base + product, gmrf.hpp:155).
   GramPlan(i32 n, const i64* pcp, const i32* pri, i32 m, const i64* arp, const i32* aci,
-           const std::vector<char>* need, cudaStream_t stream);
+           const std::vector<char>* need, cudaStream_t stream, const i64* vmap = nullptr,
+           bool base_transpose = false);
 
   // d_a: A values (CSR order, nnz), d_w: m weights (nullptr = 1), c: scale of
   // the product, d_base: pattern-order base values (nullptr = 0). Writes
@@ -63,6 +76,7 @@ class GramPlan {
   i64 np_ = 0, na_ = 0, npairs_ = 0, ne_ = 0;
   i32 m_ = 0;
   DevBuf<i64> ent_;     // computed entries (pattern positions) when a mask was given
+  DevBuf<i64> tpos_;    // per computed entry: pattern position of its transpose (base_transpose)
   DevBuf<i64> off_;     // np+1 pair offsets
   DevBuf<int2> pairs_;  // (index of A_kR, index of A_kC) in A's CSR value order
   DevBuf<i32> arow_;    // row k of every A value

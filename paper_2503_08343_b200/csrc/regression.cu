@@ -112,39 +112,6 @@ void point_operator(const MeshSpec& mesh, i32 m, const double* pts, std::vector<
   }
 }
 
-void gram_pattern(i32 n, i32 m, const i64* arp, const i32* aci, std::vector<i64>& cp,
-                  std::vector<i32>& ri) {
-  // columns of A: rows k touching column j
-  std::vector<i64> acp(static_cast<size_t>(n) + 1, 0);
-  for (i64 p = 0; p < arp[m]; ++p) acp[aci[p] + 1]++;
-  for (i32 j = 0; j < n; ++j) acp[j + 1] += acp[j];
-  std::vector<i32> ak(acp[n]);
-  {
-    std::vector<i64> nx(acp.begin(), acp.end() - 1);
-    for (i32 k = 0; k < m; ++k)
-      for (i64 p = arp[k]; p < arp[k + 1]; ++p) ak[nx[aci[p]]++] = k;
-  }
-  cp.assign(static_cast<size_t>(n) + 1, 0);
-  ri.clear();
-  std::vector<i32> mark(n, -1), col;
-  for (i32 j = 0; j < n; ++j) {
-    col.clear();
-    mark[j] = j;
-    col.push_back(j);  // the diagonal is always stored
-    for (i64 q = acp[j]; q < acp[j + 1]; ++q) {
-      const i32 k = ak[q];
-      for (i64 p = arp[k]; p < arp[k + 1]; ++p)
-        if (mark[aci[p]] != j) {
-          mark[aci[p]] = j;
-          col.push_back(aci[p]);
-        }
-    }
-    std::sort(col.begin(), col.end());
-    ri.insert(ri.end(), col.begin(), col.end());
-    cp[j + 1] = static_cast<i64>(ri.size());
-  }
-}
-
 RegressionPosterior::RegressionPosterior(const MeshSpec& mesh, const MaternSpec& spec, i32 m,
                                          const double* points, const i32* perm,
                                          cudaStream_t stream)
@@ -186,22 +153,10 @@ RegressionPosterior::RegressionPosterior(const MeshSpec& mesh, const MaternSpec&
   // pattern: KᵀK (contains AᵀA for P1: an element's vertices are mutually adjacent)
   gram_pattern(n_, mk, kcp.data(), kri.data(), pcp_, pri_);
   {
-    std::vector<i64> acp;
-    std::vector<i32> ari;
+    std::vector<i64> acp, ucp;
+    std::vector<i32> ari, uri;
     gram_pattern(n_, m, arp_.data(), aci_.data(), acp, ari);
-    // union (sorted merge per column)
-    std::vector<i64> ucp(static_cast<size_t>(n_) + 1, 0);
-    std::vector<i32> uri;
-    for (i32 j = 0; j < n_; ++j) {
-      i64 a = pcp_[j], b = acp[j];
-      while (a < pcp_[j + 1] || b < acp[j + 1]) {
-        const i32 ra = a < pcp_[j + 1] ? pri_[a] : n_, rb = b < acp[j + 1] ? ari[b] : n_;
-        uri.push_back(std::min(ra, rb));
-        if (ra <= rb) ++a;
-        if (rb <= ra) ++b;
-      }
-      ucp[j + 1] = static_cast<i64>(uri.size());
-    }
+    pattern_union(n_, pcp_, pri_, acp, ari, ucp, uri);
     pcp_.swap(ucp);
     pri_.swap(uri);
   }

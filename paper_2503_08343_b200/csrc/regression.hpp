@@ -39,9 +39,6 @@ struct MeshSpec {
 void point_operator(const MeshSpec& mesh, i32 m, const double* pts, std::vector<i64>& rp,
                     std::vector<i32>& ci, std::vector<double>& v);
 
-// Full symmetric CSC pattern of AᵀA for an m × n CSR operator (with the diagonal).
-void gram_pattern(i32 n, i32 m, const i64* arp, const i32* aci, std::vector<i64>& cp,
-                  std::vector<i32>& ri);
 
 class RegressionPosterior {
  public:

@@ -99,8 +99,9 @@ struct SymbolicHandle {
 struct FactorHandle {
   gmrf_factor_t* h = nullptr;
   std::shared_ptr<SymbolicHandle> sym;
+  std::shared_ptr<void> owner;  // set: h is a borrowed view kept alive by owner
   ~FactorHandle() {
-    if (!h) return;
+    if (!h || owner) return;
     if (sym) sym->release(h);
     else gmrf_factor_free(h);
   }
@@ -194,6 +195,35 @@ inline CholeskyFactor cholesky_refactor(const SymbolicFactor& s, const SparseMat
   }
   return f;
 }
+
+namespace b200 {
+/// A CholeskyFactor over a device factor that another object owns (an update
+/// system, gmrfpde/b200/update_system.hpp): perm from its symbolic, the host L
+/// as cholesky_refactor materialises it.
+inline CholeskyFactor wrap_factor(gmrf_factor_t* fh, const gmrf_symbolic_t* sh,
+                                  std::shared_ptr<void> owner) {
+  gmrf_symbolic_info_t info{};
+  check(gmrf_symbolic_info(sh, &info));
+  const Index n = info.n;
+  CholeskyFactor f;
+  f.perm.resize(n);
+  check(gmrf_symbolic_export(sh, f.perm.data(), nullptr, nullptr));
+  f.perm_inv = invert_permutation(f.perm);
+  auto h = std::make_shared<FactorHandle>();
+  h->h = fh;
+  h->owner = std::move(owner);
+  f.device = h;
+  f.L.nrows = f.L.ncols = n;
+  if (n <= host_l_max()) {
+    std::vector<int64_t> cp(n + 1);
+    f.L.row_idx.resize(info.nnz_l);
+    f.L.values.resize(info.nnz_l);
+    check(gmrf_factor_l(fh, cp.data(), f.L.row_idx.data(), f.L.values.data(), nullptr));
+    f.L.col_ptr.assign(cp.begin(), cp.end());
+  }
+  return f;
+}
+}  // namespace b200
 
 /// cholesky_factor(q, perm) (cholesky.hpp:164).
 inline CholeskyFactor cholesky_factor(const SparseMatrixCSC& q, const std::vector<Index>& perm) {

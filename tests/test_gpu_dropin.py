@@ -26,3 +26,90 @@ def test_reference_acceptance_suite_on_gpu():
     for crit in (1, 2, 10):  # the factor / solve / Takahashi criteria
         assert any(ln.startswith(f"PASS criterion-{crit}:") for ln in lines), out.stdout
     assert out.returncode == 0, out.stdout
+
+
+# ---- the reference's own chains through the drop-in rows (1)-(2) -------------
+# oracle/_ref/libgmrfref_b200.so is oracle/ref_capi.cpp (the reference API calls
+# that made the golden fixtures) compiled against the drop-in headers:
+# matern_prior, condition_affine, gauss_newton and laplace_posterior then run
+# their precision updates and factorizations on the B200. Run in a subprocess
+# (one reference build per process).
+DROPIN_SO = os.path.join(ROOT, "oracle", "_ref", "libgmrfref_b200.so")
+
+_CHAIN = r"""
+import json, sys, time
+import numpy as np
+sys.path.insert(0, {root!r})
+from oracle.pyoracle import Ref, REF_B200_SO
+kind, p = sys.argv[1], [float(x) for x in sys.argv[2].split(",")]
+t0 = time.perf_counter()
+b = Ref(REF_B200_SO).build(kind, p)
+wall = time.perf_counter() - t0
+out = {{"wall": wall}}
+for k in ("mode", "mean_post", "var_post", "gn_objective", "gn_decrement", "gn_step",
+          "gn_backtracks", "samples"):
+    try:
+        out[k] = b.vec(k).tolist()
+    except Exception:
+        pass
+print(json.dumps(out))
+"""
+
+
+def _run_chain(kind, params, timeout=1800):
+    import json
+    import sys
+    if not os.path.exists(DROPIN_SO):
+        pytest.skip("oracle/_ref/libgmrfref_b200.so not built (reference absent at build time)")
+    code = _CHAIN.format(root=ROOT)
+    out = subprocess.run([sys.executable, "-c", code, kind, ",".join(repr(float(x)) for x in params)],
+                         capture_output=True, text=True, timeout=timeout)
+    assert out.returncode == 0, out.stderr[-3000:]
+    return json.loads(out.stdout.strip().splitlines()[-1])
+
+
+def _rel(a, b):
+    import numpy as np
+    a, b = np.asarray(a), np.asarray(b)
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def _floor(fixture, key):
+    import json
+    from conftest import GOLDEN
+    fl = json.load(open(os.path.join(GOLDEN, "floors.json")))
+    return max(fl.get(fixture + s, {}).get(key, 0.0) for s in ("/order", "/ulp"))
+
+
+@pytest.mark.parametrize("fixture,kind,params", [
+    ("c1_matern1d.npz", "matern1d", [999, 20.0, 2, 1.0, 100, 1001, 1e4, 0.01, 0, 2001, 1]),
+    ("c2_matern2d.npz", "matern2d", [255, 10.0, 2, 1.0, 2000, 1002, 400.0, 0.05, 0, 2002, 1]),
+])
+def test_dropin_regression_chain_matches_reference(fixture, kind, params):
+    """matern_prior + condition_on + variance_takahashi of the reference API,
+    rows (1)-(2) on the device: same mean / variances as the CPU reference."""
+    from conftest import load_golden
+    z = load_golden(fixture)
+    r = _run_chain(kind, params)
+    assert _rel(r["mean_post"], z["mean_post"]) <= max(1e-10, 3 * _floor(fixture, "mean"))
+    assert _rel(r["var_post"], z["var_post"]) <= max(1e-8, 3 * _floor(fixture, "var"))
+
+
+def test_dropin_burgers_chain_matches_reference():
+    """The reference's Burgers chain (spatiotemporal_prior → condition_on →
+    gauss_newton(10) → laplace_posterior → variance_takahashi) through the
+    drop-in headers, at 200 nodes × 200 slices: identical GN iteration counts,
+    backtracks and steps; mode and variances within 10x the reference floor."""
+    import numpy as np
+    from conftest import load_golden
+    fixture = "c4_burgers_200.npz"
+    z = load_golden(fixture)
+    r = _run_chain("spatiotemporal", list(z["params"]))
+    np.testing.assert_array_equal(r["gn_backtracks"], z["gn_backtracks"])
+    np.testing.assert_array_equal(r["gn_step"], z["gn_step"])
+    obj = np.abs(np.array(r["gn_objective"]) - z["gn_objective"]) / np.abs(z["gn_objective"])
+    print("dropin c4_200", dict(wall=r["wall"], obj=obj.max(), mean=_rel(r["mode"], z["mode"]),
+                                var=_rel(r["var_post"], z["var_post"])))
+    assert obj.max() <= 10 * _floor(fixture, "objective")
+    assert _rel(r["mode"], z["mode"]) <= 10 * _floor(fixture, "mean")
+    assert _rel(r["var_post"], z["var_post"]) <= 10 * _floor(fixture, "var")
