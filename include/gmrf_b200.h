@@ -276,7 +276,9 @@ int gmrf_update_system_assemble(gmrf_update_system_t* h, const double* a_values,
 int gmrf_update_system_matrix(const gmrf_update_system_t* h, int64_t* col_ptr, int32_t* row_idx,
                               double* values);
 /* Borrowed views, valid while the system lives: its symbolic and its factor
- * (for gmrf_solve*, gmrf_selinv_*, gmrf_sample_direct, gmrf_factor_l). */
+ * (for gmrf_solve*, gmrf_selinv_*, gmrf_sample_direct, gmrf_factor_l); NULL
+ * before the first refactor (the symbolic analysis and factor storage are
+ * created on first use; assemble needs neither). */
 const gmrf_symbolic_t* gmrf_update_system_symbolic(const gmrf_update_system_t* h);
 gmrf_factor_t* gmrf_update_system_factor(gmrf_update_system_t* h);
 void gmrf_update_system_free(gmrf_update_system_t* h);

@@ -652,9 +652,6 @@ int gmrf_update_system_create(int32_t n, int32_t kind, int32_t bcols, const int6
   return guard([&] {
     auto h = std::make_unique<gmrf_update_system>();
     h->u = std::make_unique<gmrf::UpdateSystem>(n, kind, bcols, bcp, bri, bv, m, acp, ari, perm);
-    h->sym.s = h->u->symbolic();
-    h->fac.s = h->u->symbolic();
-    h->fac.f.reset(&h->u->factor());
     *out = h.release();
   });
 }
@@ -667,7 +664,14 @@ int gmrf_update_system_same_operator(const gmrf_update_system_t* h, int32_t m, c
 int gmrf_update_system_refactor(gmrf_update_system_t* h, const double* a, const double* w,
                                 int32_t* bad) {
   int32_t b = -1;
-  const int rc = guard([&] { b = h->u->refactor(a, w); });
+  const int rc = guard([&] {
+    b = h->u->refactor(a, w);
+    if (!h->fac.f) {  // views of the factor created by the first refactor
+      h->sym.s = h->u->symbolic();
+      h->fac.s = h->u->symbolic();
+      h->fac.f.reset(&h->u->factor());
+    }
+  });
   if (bad) *bad = b;
   if (rc == GMRF_OK && b >= 0) {
     g_err = "cholesky: non-positive pivot at index " + std::to_string(b);
@@ -694,10 +698,12 @@ int gmrf_update_system_matrix(const gmrf_update_system_t* h, int64_t* cp, int32_
 }
 
 const gmrf_symbolic_t* gmrf_update_system_symbolic(const gmrf_update_system_t* h) {
-  return &h->sym;
+  return h->sym.s ? &h->sym : nullptr;  // after the first refactor
 }
 
-gmrf_factor_t* gmrf_update_system_factor(gmrf_update_system_t* h) { return &h->fac; }
+gmrf_factor_t* gmrf_update_system_factor(gmrf_update_system_t* h) {
+  return h->fac.f ? &h->fac : nullptr;
+}
 
 void gmrf_update_system_free(gmrf_update_system_t* h) {
   if (h) h->fac.f.release();  // borrowed view of the system's factor

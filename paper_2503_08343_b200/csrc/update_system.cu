@@ -69,8 +69,7 @@ UpdateSystem::UpdateSystem(i32 n, int base_kind, i32 bcols, const i64* bcp, cons
   }
   gram_pattern(n, m, arp.data(), aci.data(), gcp, gri);
   pattern_union(n, bpc, bpr, gcp, gri, pcp_, pri_);
-  sym_ = std::make_shared<const Symbolic>(analyze(n, pcp_.data(), pri_.data(), perm));
-  fac_ = std::make_unique<DeviceFactor>(sym_, stream_);
+  if (perm) perm_.assign(perm, perm + n);
   const size_t np = pri_.size();
   base_.alloc(np);
   h_.alloc(np);
@@ -119,7 +118,15 @@ void UpdateSystem::assemble(const double* a_values, const double* w, double c) {
   gram_a_->apply(a_.p, w_.p, c, base_.p, h_.p, nullptr, nullptr, stream_);
 }
 
+void UpdateSystem::ensure_factor() {
+  if (fac_) return;  // symbolic analysis and factor storage on first use (assemble needs neither)
+  sym_ = std::make_shared<const Symbolic>(
+      analyze(n_, pcp_.data(), pri_.data(), perm_.empty() ? nullptr : perm_.data()));
+  fac_ = std::make_unique<DeviceFactor>(sym_, stream_);
+}
+
 int32_t UpdateSystem::refactor(const double* a_values, const double* w) {
+  ensure_factor();
   stage(a_values, w);
   fac_->begin_numeric();
   gram_a_->apply(a_.p, w_.p, 1.0, base_.p, h_.p, fac_->d_qmap(), fac_->d_l(), stream_);

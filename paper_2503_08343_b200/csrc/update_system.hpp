@@ -37,8 +37,16 @@ class UpdateSystem {
 
   i32 n() const { return n_; }
   i32 m() const { return m_; }
-  std::shared_ptr<const Symbolic> symbolic() const { return sym_; }
-  DeviceFactor& factor() { return *fac_; }
+  // created by the first refactor (ensure_factor)
+  std::shared_ptr<const Symbolic> symbolic() {
+    ensure_factor();
+    return sym_;
+  }
+  DeviceFactor& factor() {
+    ensure_factor();
+    return *fac_;
+  }
+  void ensure_factor();
   const std::vector<i64>& col_ptr() const { return pcp_; }
   const std::vector<i32>& row_idx() const { return pri_; }
   void copy_values(double* out) const;  // H of the last refactor / assemble, pattern order
@@ -47,7 +55,7 @@ class UpdateSystem {
   i32 n_, m_;
   cudaStream_t stream_;
   std::vector<i64> pcp_, acp_;
-  std::vector<i32> pri_, ari_;
+  std::vector<i32> pri_, ari_, perm_;
   std::shared_ptr<const Symbolic> sym_;
   std::unique_ptr<DeviceFactor> fac_;
   std::unique_ptr<GramPlan> gram_a_;
