@@ -199,6 +199,13 @@ int gmrf_partition_owners(const gmrf_symbolic_t* s, int32_t nranks, int32_t* own
  * for the solve phases]). Call with rows == NULL for the count. */
 int gmrf_partition_schedule(const gmrf_symbolic_t* s, const int32_t* owner, int64_t* rows,
                             int64_t* n_rows);
+/* Per-rank device memory plan (bytes) of a partitioned factorization with
+ * selected inversion, from the symbolic alone (host only): rows of 7 values
+ * per rank — L panels, Σ panels, update-matrix arena (factorization), the same
+ * arena in the selected inversion, replicated pattern-sized data, total, owned
+ * supernodes. owner == NULL: gmrf_partition_owners. */
+int gmrf_partition_memory(const gmrf_symbolic_t* s, int32_t nranks, const int32_t* owner,
+                          int64_t* rows);
 /* This rank's share of the factor. owner == NULL: gmrf_partition_owners. */
 int gmrf_factor_create_partitioned(const gmrf_symbolic_t* s, int32_t nranks, int32_t rank,
                                    const int32_t* owner, gmrf_exchange_fn fn, void* ctx,
@@ -399,6 +406,10 @@ int gmrf_spacetime_run(gmrf_spacetime_t* h, const double* u0, int32_t want_var, 
                        double* var, gmrf_gn_iter_t* trace, int32_t max_trace, int32_t* n_trace,
                        int32_t* converged);
 int gmrf_spacetime_info(const gmrf_spacetime_t* h, gmrf_spacetime_info_t* info);
+/* Host only: the symbolic analysis of the pipeline's factor (master pattern,
+ * geometric nested dissection, supernodes) without a device — for front
+ * statistics and the per-rank memory plan of a partitioned run. */
+int gmrf_spacetime_symbolic(const gmrf_spacetime_config_t* cfg, gmrf_symbolic_t** out);
 /* Device pointers of the last run's mean / variances (n doubles each). */
 int gmrf_spacetime_device_results(const gmrf_spacetime_t* h, const double** d_mean,
                                   const double** d_var);

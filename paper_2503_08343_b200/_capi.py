@@ -140,6 +140,7 @@ SIGNATURES = {
                                  f64p, C.POINTER(CgConfig), f64p]),
     "gmrf_partition_owners": (C.c_int, [vp, C.c_int32, i32p]),
     "gmrf_partition_schedule": (C.c_int, [vp, i32p, i64p, i64p]),
+    "gmrf_partition_memory": (C.c_int, [vp, C.c_int32, i32p, i64p]),
     "gmrf_factor_create_partitioned": (C.c_int, [vp, C.c_int32, C.c_int32, i32p, EXCHANGE_FN, vp,
                                                  C.POINTER(vp)]),
     "gmrf_spacetime_create_partitioned": (C.c_int, [C.POINTER(SpaceTimeConfig), C.c_int32,
@@ -148,6 +149,7 @@ SIGNATURES = {
     "gmrf_spacetime_run": (C.c_int, [vp, f64p, C.c_int32, f64p, f64p, C.POINTER(GnIter),
                                      C.c_int32, i32p, i32p]),
     "gmrf_spacetime_info": (C.c_int, [vp, C.POINTER(SpaceTimeInfo)]),
+    "gmrf_spacetime_symbolic": (C.c_int, [C.POINTER(SpaceTimeConfig), C.POINTER(vp)]),
     "gmrf_spacetime_device_results": (C.c_int, [vp, C.POINTER(vp), C.POINTER(vp)]),
     "gmrf_spacetime_pattern": (C.c_int, [vp, i64p, i32p, f64p, f64p]),
     "gmrf_spacetime_residual": (C.c_int, [vp, f64p, f64p]),

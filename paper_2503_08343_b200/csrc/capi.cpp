@@ -213,6 +213,22 @@ int gmrf_partition_schedule(const gmrf_symbolic_t* h, const int32_t* owner, int6
   });
 }
 
+int gmrf_partition_memory(const gmrf_symbolic_t* s, int32_t nranks, const int32_t* owner,
+                          int64_t* rows) {
+  return guard([&] {
+    gmrf::require(nranks >= 1, gmrf::kContract, "partition: nranks >= 1");
+    std::vector<int32_t> own = owner ? std::vector<int32_t>(owner, owner + s->s->ns)
+                                     : gmrf::partition_owners(*s->s, nranks);
+    const auto mem = gmrf::partition_memory(*s->s, own, nranks);
+    for (int r = 0; r < nranks; ++r) {
+      const gmrf::RankMemory& m = mem[r];
+      const int64_t v[7] = {m.l_panels, m.sigma_panels, m.u_arena_factor, m.u_arena_selinv,
+                            m.replicated, m.total(), m.supernodes};
+      std::memcpy(rows + 7 * r, v, sizeof(v));
+    }
+  });
+}
+
 int gmrf_factor_create_partitioned(const gmrf_symbolic_t* h, int32_t nranks, int32_t rank,
                                    const int32_t* owner, gmrf_exchange_fn fn, void* ctx,
                                    gmrf_factor_t** out) {
@@ -401,9 +417,7 @@ int gmrf_bench_fp64(double* a, double* b) {
   return guard([&] { gmrf::bench_fp64(a, b); });
 }
 
-static int spacetime_create(const gmrf_spacetime_config_t* c, const gmrf::PartitionSpec* part,
-                            gmrf_spacetime_t** out) {
-  return guard([&] {
+static gmrf::SpaceTimeSpec spacetime_spec(const gmrf_spacetime_config_t* c) {
     gmrf::SpaceTimeSpec s;
     s.n_el = c->n_el;
     s.xa = c->xa;
@@ -421,6 +435,21 @@ static int spacetime_create(const gmrf_spacetime_config_t* c, const gmrf::Partit
     s.residual = c->residual;
     s.pde_noise_prec = c->pde_noise_prec;
     s.dim = c->dim == 0 ? 1 : c->dim;
+    return s;
+}
+
+int gmrf_spacetime_symbolic(const gmrf_spacetime_config_t* c, gmrf_symbolic_t** out) {
+  return guard([&] {
+    auto h = std::make_unique<gmrf_symbolic>();
+    h->s = gmrf::SpaceTimePosterior::host_symbolic(spacetime_spec(c));
+    *out = h.release();
+  });
+}
+
+static int spacetime_create(const gmrf_spacetime_config_t* c, const gmrf::PartitionSpec* part,
+                            gmrf_spacetime_t** out) {
+  return guard([&] {
+    const gmrf::SpaceTimeSpec s = spacetime_spec(c);
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
       gmrf::fail(gmrf::kCuda, "no CUDA device: libgmrf_b200 has no CPU fallback");

@@ -57,6 +57,16 @@ void set_smem_attrs() {
 inline int nchunks(int w) { return (w + kNB - 1) / kNB; }
 
 // Tile GEMM launch: one CTA per 64×64 output tile.
+// Timeline marker (diagnostic, GMRF_TRACE=<file>): one thread stores the
+// global timer; bracketing launches on their streams (also inside the captured
+// graph) gives per-level start / end times of each launch class. No numerical
+// effect; adds one tiny node per marker.
+__global__ void k_mark(unsigned long long* buf, int idx) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  buf[idx] = t;
+}
+
 void launch_gemm(const GemmTask* tasks, int64_t n, cudaStream_t st) {
   k_gemm_tiles<<<static_cast<unsigned>(n), 128, 0, st>>>(tasks);
 }
@@ -118,6 +128,8 @@ DeviceFactor::DeviceFactor(std::shared_ptr<const Symbolic> sym, cudaStream_t str
     lptr_h_[k + 1] = lptr_h_[k] + (mine(k) ? static_cast<i64>(s.rows(k)) * s.w(k) : 0);
   if (const char* e = std::getenv("GMRF_U_STATIC")) u_static_ = e[0] != '0';
   if (const char* e = std::getenv("GMRF_DEFER")) defer_ = std::max(1, atoi(e));
+  if (const char* e = std::getenv("GMRF_INC_U")) inc_u_ = std::max(0, atoi(e));
+  if (const char* e = std::getenv("GMRF_TRACE")) trace_file_ = e;
   plan_update_storage();
   std::vector<i64> qm;
   if (part_) {  // Q entries of other ranks' supernodes are not stored here
@@ -332,13 +344,17 @@ DeviceFactor::DeviceFactor(std::shared_ptr<const Symbolic> sym, cudaStream_t str
     cuda_check(cudaDeviceGetStreamPriorityRange(&lo, &hi), "priorities");
     cuda_check(cudaStreamCreateWithPriority(&main_, cudaStreamNonBlocking, hi), "main stream");
     cuda_check(cudaStreamCreateWithPriority(&aux_, cudaStreamNonBlocking, lo), "aux stream");
+    cuda_check(cudaStreamCreateWithPriority(&uu_, cudaStreamNonBlocking, lo), "update stream");
     cuda_check(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming), "event");
   }
   ev_panel_.resize(flev_.size());
   ev_rest_.resize(flev_.size());
+  ev_uupd_.resize(flev_.size());
+  if (!trace_file_.empty()) tbuf_.alloc(flev_.size() * kTraceSlots);
   for (size_t l = 0; l < flev_.size(); ++l) {
     cuda_check(cudaEventCreateWithFlags(&ev_panel_[l], cudaEventDisableTiming), "event");
     cuda_check(cudaEventCreateWithFlags(&ev_rest_[l], cudaEventDisableTiming), "event");
+    cuda_check(cudaEventCreateWithFlags(&ev_uupd_[l], cudaEventDisableTiming), "event");
   }
   cuda_check(cudaStreamSynchronize(stream_), "factor setup");
 }
@@ -347,139 +363,31 @@ DeviceFactor::~DeviceFactor() {
   if (fgraph_) cudaGraphExecDestroy(fgraph_);
   for (cudaEvent_t e : ev_panel_) cudaEventDestroy(e);
   for (cudaEvent_t e : ev_rest_) cudaEventDestroy(e);
+  for (cudaEvent_t e : ev_uupd_) cudaEventDestroy(e);
   if (ev_fork_) cudaEventDestroy(ev_fork_);
+  if (uu_) cudaStreamDestroy(uu_);
   if (aux_) cudaStreamDestroy(aux_);
   if (main_) cudaStreamDestroy(main_);
 }
 
-// Lifetime-packed update-matrix storage, per phase. Factorization: U_k lives
-// from its supernode's first chunk level (extend-add, zeroing) to the parent's
-// first chunk level (the parent's extend-add reads it); a Schur complement
-// received from another rank from the exchange after the child's last level.
-// Selected inversion (levels top-down): Σ_RR(k) lives from its gather (or
-// receipt) to the last of its readers — k's own chunks and its children's
-// gathers. Regions are reused first-fit once their interval has ended, so the
-// buffer holds the live matrices of a level front, not Σ_s r_s² (C4: see
-// gmrf_factor_stats device_bytes). GMRF_U_STATIC=1: one slot per supernode.
-static std::vector<i64> plan_arena(const std::vector<i64>& size, const std::vector<int>& start,
-                                   const std::vector<int>& end, int ntime, i64& total) {
-  const int n = static_cast<int>(size.size());
-  std::vector<i64> off(n, 0);
-  std::vector<std::vector<int>> st(std::max(ntime, 1)), en(std::max(ntime, 1));
-  for (int k = 0; k < n; ++k)
-    if (size[k] > 0) {
-      st[start[k]].push_back(k);
-      en[end[k]].push_back(k);
-    }
-  std::map<i64, i64> by_off;             // free blocks: offset -> size
-  std::multimap<i64, i64> by_size;       // size -> offset
-  auto erase_free = [&](i64 o, i64 z) {
-    auto r = by_size.equal_range(z);
-    for (auto it = r.first; it != r.second; ++it)
-      if (it->second == o) {
-        by_size.erase(it);
-        break;
-      }
-    by_off.erase(o);
-  };
-  total = 0;
-  for (int t = 0; t < ntime; ++t) {
-    std::vector<int>& a = st[t];
-    std::stable_sort(a.begin(), a.end(), [&](int x, int y) { return size[x] > size[y]; });
-    for (int k : a) {
-      auto it = by_size.lower_bound(size[k]);
-      if (it == by_size.end()) {
-        off[k] = total;
-        total += size[k];
-        continue;
-      }
-      const i64 z = it->first, o = it->second;
-      erase_free(o, z);
-      off[k] = o;
-      if (z > size[k]) {
-        by_off[o + size[k]] = z - size[k];
-        by_size.insert({z - size[k], o + size[k]});
-      }
-    }
-    for (int k : en[t]) {
-      i64 o = off[k], z = size[k];
-      auto nx = by_off.lower_bound(o);
-      if (nx != by_off.end() && nx->first == o + z) {
-        const i64 no = nx->first, nz = nx->second;
-        erase_free(no, nz);
-        z += nz;
-      }
-      auto pv = by_off.lower_bound(o);
-      if (pv != by_off.begin()) {
-        --pv;
-        if (pv->first + pv->second == o) {
-          const i64 po = pv->first, pz = pv->second;
-          erase_free(po, pz);
-          o = po;
-          z += pz;
-        }
-      }
-      by_off[o] = z;
-      by_size.insert({z, o});
-    }
-  }
-  return off;
-}
-
 void DeviceFactor::plan_update_storage() {
   const Symbolic& s = *sym_;
-  std::vector<i64> size(s.ns, 0);
-  for (int k = 0; k < s.ns; ++k) {
-    const int p = s.sn_parent[k];
-    if (p >= 0 && (mine(k) || mine(p))) size[k] = static_cast<i64>(s.r(k)) * s.r(k);
-  }
   uptr_h_.assign(s.ns + 1, 0);
   uptrs_h_.assign(s.ns + 1, 0);
   if (u_static_) {
-    for (int k = 0; k < s.ns; ++k) uptr_h_[k + 1] = uptr_h_[k] + size[k];
+    for (int k = 0; k < s.ns; ++k) {
+      const int p = s.sn_parent[k];
+      const i64 z = (p >= 0 && (mine(k) || mine(p))) ? static_cast<i64>(s.r(k)) * s.r(k) : 0;
+      uptr_h_[k + 1] = uptr_h_[k] + z;
+    }
     uptrs_h_ = uptr_h_;
     u_arena_ = uptr_h_[s.ns];
     u_arena_f_ = u_arena_s_ = u_arena_;
     return;
   }
-  std::vector<int> f0, fl, s0, sl;
-  int nf = 0, nsl = 0;
-  chunk_levels(s, f0, fl, nf, kSmallRows);
-  chunk_levels(s, s0, sl, nsl, 0);
-  std::vector<int> a(s.ns, 0), b(s.ns, 0);
-  for (int k = 0; k < s.ns; ++k) {
-    const int p = s.sn_parent[k];
-    if (!size[k]) continue;
-    if (mine(k) && mine(p)) {
-      a[k] = f0[k];
-      b[k] = f0[p];
-    } else if (mine(k)) {  // sent to the parent's rank after its last level
-      a[k] = f0[k];
-      b[k] = fl[k];
-    } else {  // received from the child's rank
-      a[k] = fl[k];
-      b[k] = f0[p];
-    }
-  }
-  std::vector<i64> fo = plan_arena(size, a, b, nf, u_arena_f_);
-  // selected inversion, time = nsl - 1 - level
-  auto T = [&](int lvl) { return nsl - 1 - lvl; };
-  for (int k = 0; k < s.ns; ++k) {
-    const int p = s.sn_parent[k];
-    if (!size[k]) continue;
-    if (!mine(k)) {  // ghost gather on the parent's rank, sent right away
-      a[k] = b[k] = T(s0[p]);
-      continue;
-    }
-    int last = s0[k];  // lowest level still reading Σ_RR(k)
-    for (int q = s.ch_ptr[k]; q < s.ch_ptr[k + 1]; ++q) {
-      const int c = s.ch_list[q];
-      if (mine(c)) last = std::min(last, sl[c]);
-    }
-    a[k] = T(mine(p) ? sl[k] : s0[p]);
-    b[k] = T(last);
-  }
-  std::vector<i64> so = plan_arena(size, a, b, nsl, u_arena_s_);
+  std::vector<i64> fo, so;
+  plan_update_arenas(s, part_ ? owner_ : std::vector<i32>(s.ns, 0), rank_, fo, so, u_arena_f_,
+                     u_arena_s_);
   for (int k = 0; k < s.ns; ++k) {
     uptr_h_[k] = fo[k];
     uptrs_h_[k] = so[k];
@@ -548,13 +456,13 @@ void DeviceFactor::build_factor_plan() {
   // GEMM tasks per level: gm = the update of the chunk's NEXT column block (on
   // the critical chain), gr = the rest of the trailing update + the U SYRK
   // (overlapped with the next level's panel on the second stream)
-  std::vector<std::vector<GemmTask>> gm(nlev), gr(nlev);
+  std::vector<std::vector<GemmTask>> gm(nlev), gr(nlev), gu(nlev);
   // small-front buckets: rows ≤ 32 / ≤ 64 (k_small_front), rows ≤ 96 with
   // w ≤ 16 / 32 / 64 (k_small_front_rows), rows ≤ 96 with w > 64 (k_small_front)
   std::vector<std::vector<int32_t>> sm[kSmBuckets];
   for (auto& v : sm) v.resize(nlev);
   std::vector<double> ea_b(nlev, 0.0), po_f(nlev, 0.0), tr_f(nlev, 0.0), gm_f(nlev, 0.0),
-      gr_f(nlev, 0.0), sm_f(nlev, 0.0);
+      gr_f(nlev, 0.0), sm_f(nlev, 0.0), gu_f(nlev, 0.0);
   double* L = L_.p;
   double* U = U_.p;
   std::vector<int64_t> gpan(3 * static_cast<size_t>(nlev), 0);  // panel tasks of all ranks
@@ -571,7 +479,7 @@ void DeviceFactor::build_factor_plan() {
       trailing_jobs(w, c, [&](bool crit, int j0, int j1, int, int) {
         for (int jb = j0; jb < j1; jb += kTile) (crit ? ggm : ggr)[lv] += (rows - jb + kTile - 1) / kTile;
       });
-      if (c == nch - 1)
+      if (c == nch - 1 && !(inc_u_ && nch >= inc_u_))
         for (int jb = 0; jb < r; jb += kTile) ggr[lv] += (r - jb + kTile - 1) / kTile;
     }
   }
@@ -665,8 +573,30 @@ void DeviceFactor::build_factor_plan() {
             (crit ? gm_f : gr_f)[lv] += tile_flops(g, ib == jb);
           }
       });
+      // wide supernodes: U -= L21(c) L21(c)ᵀ right after this chunk (K = wk), off
+      // the panel chain; same per-tile accumulation order as one K = w SYRK
+      const bool inc = inc_u_ && nch >= inc_u_;
+      if (inc && r > 0)
+        for (int jb = 0; jb < r; jb += kTile)
+          for (int ib = jb; ib < r; ib += kTile) {
+            GemmTask g{};
+            g.c = Uk + ib + static_cast<int64_t>(jb) * r;
+            g.ldc = r;
+            g.m = std::min(kTile, r - ib);
+            g.n = std::min(kTile, r - jb);
+            g.a[0] = Lk + w + ib + static_cast<int64_t>(c0) * rows;
+            g.lda[0] = rows;
+            g.b[0] = Lk + w + jb + static_cast<int64_t>(c0) * rows;
+            g.ldb[0] = rows;
+            g.k[0] = wk;
+            g.flags = 2;
+            g.alpha = -1.0;
+            g.beta = 1.0;
+            gu[lv].push_back(g);
+            gu_f[lv] += tile_flops(g, ib == jb);
+          }
       // last chunk: full-width SYRK into the update matrix, U -= L21 L21ᵀ
-      if (c == nch - 1 && r > 0)
+      if (!inc && c == nch - 1 && r > 0)
         for (int jb = 0; jb < r; jb += kTile)
           for (int ib = jb; ib < r; ib += kTile) {
             GemmTask g{};
@@ -728,6 +658,10 @@ void DeviceFactor::build_factor_plan() {
       flev_[l].rrn = static_cast<int64_t>(rs.size());
       rdf.insert(rdf.end(), rs.begin(), rs.end());
       flev_[l].gr_flops = gr_f[l];
+      flev_[l].gu0 = static_cast<int64_t>(gmf.size());
+      flev_[l].gun = static_cast<int64_t>(gu[l].size());
+      flev_[l].gu_flops = gu_f[l];
+      gmf.insert(gmf.end(), gu[l].begin(), gu[l].end());
     }
     pof.insert(pof.end(), po[l].begin(), po[l].end());
     eaf.insert(eaf.end(), ea[l].begin(), ea[l].end());
@@ -1005,6 +939,7 @@ int32_t DeviceFactor::factor_panels() {
       launches_numeric_ = l0;
     }
     cuda_check(cudaGraphLaunch(fgraph_, stream_), "graph launch");
+    dump_trace();
     launches_numeric_ += graph_launches_;
   } else {
     enqueue_levels(la ? main_ : stream_, la ? aux_ : stream_, la, false);
@@ -1058,8 +993,10 @@ void DeviceFactor::enqueue_levels(cudaStream_t sa, cudaStream_t sb, bool la, boo
     int64_t nsmall = 0;
     for (int bk = 0; bk < kSmBuckets; ++bk) nsmall += lv.smn[bk];
     const bool assembles = lv.ean > 0 || nsmall > 0;
-    if (la && li > 0 && assembles)
+    if (la && li > 0 && assembles) {
       cuda_check(cudaStreamWaitEvent(sa, ev_rest_[li - 1], 0), "wait");
+      cuda_check(cudaStreamWaitEvent(sa, ev_uupd_[li - 1], 0), "wait");
+    }
     if (nsmall > 0) {
       pf.run(sa, pf.tag("factor.small_front", lvl), lv.sm_flops, 0.0, [&] {
         auto g = [&](int bk) { return static_cast<unsigned>(lv.smn[bk]); };
@@ -1085,6 +1022,10 @@ void DeviceFactor::enqueue_levels(cudaStream_t sa, cudaStream_t sb, bool la, boo
       });
       for (int bk = 0; bk < kSmBuckets; ++bk) launches_numeric_ += lv.smn[bk] > 0;
     }
+    auto mark = [&](cudaStream_t st, int slot) {
+      if (tbuf_.p) k_mark<<<1, 1, 0, st>>>(tbuf_.p, lvl * kTraceSlots + slot);
+    };
+    mark(sa, 8);
     if (lv.ean && !(whatif & 8)) {
       int blocks = static_cast<int>((lv.ean * 32 + 255) / 256);
       pf.run(sa, pf.tag("factor.extend_add", lvl), 0.0, lv.ea_bytes, [&] {
@@ -1093,6 +1034,7 @@ void DeviceFactor::enqueue_levels(cudaStream_t sa, cudaStream_t sb, bool la, boo
       });
       ++launches_numeric_;
     }
+    mark(sa, 0);
     // one-wave levels (the chain at the top of the tree) keep the fused row
     // sweep: one launch, no staging round trip; multi-wave levels split
     const bool two_phase = panel2_ && !(lv.prow[0] && lv.prow[1] && lv.prow[2]);
@@ -1155,10 +1097,12 @@ void DeviceFactor::enqueue_levels(cudaStream_t sa, cudaStream_t sb, bool la, boo
       });
       launches_numeric_ += (lv.pbn[0] > 0) + (lv.pbn[1] > 0) + (lv.pbn[2] > 0);
     }
+    mark(sa, 1);
     if (la) cuda_check(cudaEventRecord(ev_panel_[li], sa), "record");
     // next(l) writes block c+1, last written off the chain by the flush D levels back
     if (la && li >= static_cast<size_t>(defer_))
       cuda_check(cudaStreamWaitEvent(sa, ev_rest_[li - defer_], 0), "wait");
+    mark(sa, 2);
     if (lv.gmn && !(whatif & 4)) {
       pf.run(sa, pf.tag("factor.gemm_dmma", lvl), lv.gm_flops, 0.0, [&] {
         launch_gemm(gemm_.p + lv.gm0, lv.gmn, sa);
@@ -1168,7 +1112,9 @@ void DeviceFactor::enqueue_levels(cudaStream_t sa, cudaStream_t sb, bool la, boo
       });
       launches_numeric_ += 1 + (lv.rdn > 0);
     }
+    mark(sa, 3);
     if (la) cuda_check(cudaStreamWaitEvent(sb, ev_panel_[li], 0), "wait");
+    mark(sb, 4);
     if (lv.grn && !(whatif & 1)) {
       pf.run(sb, pf.tag("factor.gemm_dmma", lvl), lv.gr_flops, 0.0, [&] {
         launch_gemm(gemm_.p + lv.gr0, lv.grn, sb);
@@ -1178,12 +1124,25 @@ void DeviceFactor::enqueue_levels(cudaStream_t sa, cudaStream_t sb, bool la, boo
       });
       launches_numeric_ += 1 + (lv.rrn > 0);
     }
+    mark(sb, 5);
     if (la) cuda_check(cudaEventRecord(ev_rest_[li], sb), "record");
+    // incremental update-matrix accumulation (wide supernodes), third stream
+    cudaStream_t su = la ? uu_ : sa;
+    if (la) cuda_check(cudaStreamWaitEvent(su, ev_panel_[li], 0), "wait");
+    mark(su, 6);
+    if (lv.gun) {
+      pf.run(su, pf.tag("factor.gemm_dmma", lvl), lv.gu_flops, 0.0,
+             [&] { launch_gemm(gemm_.p + lv.gu0, lv.gun, su); });
+      ++launches_numeric_;
+    }
+    mark(su, 7);
+    if (la) cuda_check(cudaEventRecord(ev_uupd_[li], su), "record");
     if (part_ && !fx_[li].empty()) {
       // Schur complements completed at this level move to the parent's rank:
       // join both chains into stream_, exchange there, fork again
       if (la) {
         cuda_check(cudaStreamWaitEvent(sa, ev_rest_[li], 0), "wait");
+        cuda_check(cudaStreamWaitEvent(sa, ev_uupd_[li], 0), "wait");
         cuda_check(cudaEventRecord(ev_fork_, sa), "record");
         cuda_check(cudaStreamWaitEvent(stream_, ev_fork_, 0), "wait");
       }
@@ -1195,11 +1154,30 @@ void DeviceFactor::enqueue_levels(cudaStream_t sa, cudaStream_t sb, bool la, boo
     }
   }
   if (la) {  // join: the caller's stream continues after both chains
-    if (!flev_.empty()) cuda_check(cudaStreamWaitEvent(sa, ev_rest_[flev_.size() - 1], 0), "wait");
+    if (!flev_.empty()) {
+      cuda_check(cudaStreamWaitEvent(sa, ev_rest_[flev_.size() - 1], 0), "wait");
+      cuda_check(cudaStreamWaitEvent(sa, ev_uupd_[flev_.size() - 1], 0), "wait");
+    }
     if (!in_graph) {
       cuda_check(cudaEventRecord(ev_fork_, sa), "record");
       cuda_check(cudaStreamWaitEvent(stream_, ev_fork_, 0), "wait");
     }
+  }
+}
+
+void DeviceFactor::dump_trace() {
+  if (!tbuf_.p) return;
+  std::vector<unsigned long long> t(tbuf_.n);
+  cuda_check(cudaMemcpyAsync(t.data(), tbuf_.p, t.size() * 8, cudaMemcpyDeviceToHost, stream_), "trace");
+  cuda_check(cudaStreamSynchronize(stream_), "trace");
+  if (FILE* f = std::fopen(trace_file_.c_str(), "a")) {
+    for (size_t l = 0; l < flev_.size(); ++l) {
+      std::fprintf(f, "%zu", l);
+      for (int k = 0; k < kTraceSlots; ++k) std::fprintf(f, " %llu", t[l * kTraceSlots + k]);
+      std::fprintf(f, "\n");
+    }
+    std::fprintf(f, "end\n");
+    std::fclose(f);
   }
 }
 

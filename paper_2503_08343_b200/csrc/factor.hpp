@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <memory>
+#include <string>
 #include <vector>
 
 #include "kernels.cuh"
@@ -201,6 +202,8 @@ class DeviceFactor {
     int64_t gr0, grn, rr0, rrn;  // rest of the trailing update + U SYRK (second stream)
     double gr_flops;
     int64_t pd0[3], pdn[3], pt0[3], ptn[3];  // two-phase panel: diagonal / TRSM tasks
+    int64_t gu0, gun;  // incremental U updates of wide supernodes (third stream)
+    double gu_flops;
     bool prow[3];  // panel kernel per bucket: row sweep (one wave) or blocked; decided on
                    // the level's task count over ALL supernodes, so a partitioned factor
                    // runs the same kernels (same rounding) as the single-GPU one
@@ -223,9 +226,18 @@ class DeviceFactor {
   DevBuf<ReduceTask> red_, sred_;
   DevBuf<double> parts_, rparts_, sparts_;  // split-K partial tiles
   // lookahead: the rest-of-update GEMMs run on aux_ (events order the levels)
-  cudaStream_t main_ = nullptr, aux_ = nullptr;
+  cudaStream_t main_ = nullptr, aux_ = nullptr, uu_ = nullptr;
   cudaEvent_t ev_fork_ = nullptr;
-  std::vector<cudaEvent_t> ev_panel_, ev_rest_;
+  std::vector<cudaEvent_t> ev_panel_, ev_rest_, ev_uupd_;
+  // supernodes of at least inc_u_ chunks accumulate their update matrix chunk by
+  // chunk (U -= L21(c) L21(c)ᵀ right after chunk c's panel, on uu_) instead of
+  // one K = w SYRK after the last chunk on the critical path; 0 disables
+  int inc_u_ = 4;
+  // GMRF_TRACE=<file>: per-level timeline markers (k_mark), appended per factorization
+  static constexpr int kTraceSlots = 10;
+  std::string trace_file_;
+  DevBuf<unsigned long long> tbuf_;
+  void dump_trace();
   bool lookahead_ = true;
   int defer_ = 1;
   bool gemm_cap_ = true;  // cap bulk GEMM residency on one-wave levels (launch_gemm)  // trailing-update deferral depth (chunks per flush), trailing_jobs

@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <functional>
+#include <map>
 
 #include "kernels.cuh"
 
@@ -120,6 +121,155 @@ std::vector<XEdge> partition_schedule(const Symbolic& s, const std::vector<i32>&
     return a.sn < b.sn;
   });
   return e;
+}
+
+// Lifetime-packed update-matrix storage, per phase. Factorization: U_k lives
+// from its supernode's first chunk level (extend-add, zeroing) to the parent's
+// first chunk level (the parent's extend-add reads it); a Schur complement
+// received from another rank from the exchange after the child's last level.
+// Selected inversion (levels top-down): Σ_RR(k) lives from its gather (or
+// receipt) to the last of its readers — k's own chunks and its children's
+// gathers. Regions are reused first-fit once their interval has ended, so the
+// buffer holds the live matrices of a level front, not Σ_s r_s² (C4: see
+// gmrf_factor_stats device_bytes). GMRF_U_STATIC=1: one slot per supernode.
+std::vector<i64> plan_arena(const std::vector<i64>& size, const std::vector<int>& start,
+                                   const std::vector<int>& end, int ntime, i64& total) {
+  const int n = static_cast<int>(size.size());
+  std::vector<i64> off(n, 0);
+  std::vector<std::vector<int>> st(std::max(ntime, 1)), en(std::max(ntime, 1));
+  for (int k = 0; k < n; ++k)
+    if (size[k] > 0) {
+      st[start[k]].push_back(k);
+      en[end[k]].push_back(k);
+    }
+  std::map<i64, i64> by_off;             // free blocks: offset -> size
+  std::multimap<i64, i64> by_size;       // size -> offset
+  auto erase_free = [&](i64 o, i64 z) {
+    auto r = by_size.equal_range(z);
+    for (auto it = r.first; it != r.second; ++it)
+      if (it->second == o) {
+        by_size.erase(it);
+        break;
+      }
+    by_off.erase(o);
+  };
+  total = 0;
+  for (int t = 0; t < ntime; ++t) {
+    std::vector<int>& a = st[t];
+    std::stable_sort(a.begin(), a.end(), [&](int x, int y) { return size[x] > size[y]; });
+    for (int k : a) {
+      auto it = by_size.lower_bound(size[k]);
+      if (it == by_size.end()) {
+        off[k] = total;
+        total += size[k];
+        continue;
+      }
+      const i64 z = it->first, o = it->second;
+      erase_free(o, z);
+      off[k] = o;
+      if (z > size[k]) {
+        by_off[o + size[k]] = z - size[k];
+        by_size.insert({z - size[k], o + size[k]});
+      }
+    }
+    for (int k : en[t]) {
+      i64 o = off[k], z = size[k];
+      auto nx = by_off.lower_bound(o);
+      if (nx != by_off.end() && nx->first == o + z) {
+        const i64 no = nx->first, nz = nx->second;
+        erase_free(no, nz);
+        z += nz;
+      }
+      auto pv = by_off.lower_bound(o);
+      if (pv != by_off.begin()) {
+        --pv;
+        if (pv->first + pv->second == o) {
+          const i64 po = pv->first, pz = pv->second;
+          erase_free(po, pz);
+          o = po;
+          z += pz;
+        }
+      }
+      by_off[o] = z;
+      by_size.insert({z, o});
+    }
+  }
+  return off;
+}
+
+void plan_update_arenas(const Symbolic& s, const std::vector<i32>& owner, int rank,
+                        std::vector<i64>& fo, std::vector<i64>& so, i64& arena_f, i64& arena_s) {
+  auto mine = [&](int k) { return owner[k] == rank; };
+  std::vector<i64> size(s.ns, 0);
+  for (int k = 0; k < s.ns; ++k) {
+    const int p = s.sn_parent[k];
+    if (p >= 0 && (mine(k) || mine(p))) size[k] = static_cast<i64>(s.r(k)) * s.r(k);
+  }
+  std::vector<int> f0, fl, s0, sl;
+  int nf = 0, nsl = 0;
+  chunk_levels(s, f0, fl, nf, kSmallRows);
+  chunk_levels(s, s0, sl, nsl, 0);
+  std::vector<int> a(s.ns, 0), b(s.ns, 0);
+  for (int k = 0; k < s.ns; ++k) {
+    const int p = s.sn_parent[k];
+    if (!size[k]) continue;
+    if (mine(k) && mine(p)) {
+      a[k] = f0[k];
+      b[k] = f0[p];
+    } else if (mine(k)) {  // sent to the parent's rank after its last level
+      a[k] = f0[k];
+      b[k] = fl[k];
+    } else {  // received from the child's rank
+      a[k] = fl[k];
+      b[k] = f0[p];
+    }
+  }
+  fo = plan_arena(size, a, b, nf, arena_f);
+  // selected inversion, time = nsl - 1 - level
+  auto T = [&](int lvl) { return nsl - 1 - lvl; };
+  for (int k = 0; k < s.ns; ++k) {
+    const int p = s.sn_parent[k];
+    if (!size[k]) continue;
+    if (!mine(k)) {  // ghost gather on the parent's rank, sent right away
+      a[k] = b[k] = T(s0[p]);
+      continue;
+    }
+    int last = s0[k];  // lowest level still reading Σ_RR(k)
+    for (int q = s.ch_ptr[k]; q < s.ch_ptr[k + 1]; ++q) {
+      const int c = s.ch_list[q];
+      if (mine(c)) last = std::min(last, sl[c]);
+    }
+    a[k] = T(mine(p) ? sl[k] : s0[p]);
+    b[k] = T(last);
+  }
+  so = plan_arena(size, a, b, nsl, arena_s);
+}
+
+std::vector<RankMemory> partition_memory(const Symbolic& s, const std::vector<i32>& owner,
+                                         int nranks, int max_rhs) {
+  std::vector<RankMemory> out(nranks);
+  for (int r = 0; r < nranks; ++r) {
+    RankMemory& m = out[r];
+    for (int k = 0; k < s.ns; ++k)
+      if (owner[k] == r) {
+        m.l_panels += 8 * static_cast<i64>(s.rows(k)) * s.w(k);
+        m.supernodes += 1;
+        m.flops += [&] {
+          double f = 0;
+          for (int j = 0; j < s.w(k); ++j) f += static_cast<double>(s.rows(k) - j) * (s.rows(k) - j);
+          return f;
+        }();
+      }
+    std::vector<i64> fo, so;
+    i64 af = 0, as = 0;
+    plan_update_arenas(s, owner, r, fo, so, af, as);
+    m.u_arena_factor = 8 * af;
+    m.u_arena_selinv = 8 * as;
+    m.sigma_panels = m.l_panels;
+    // replicated per rank: Q values + qmap over the pattern, solve vectors
+    m.replicated = 16 * static_cast<i64>(s.qri.size()) + 8 * 4 * static_cast<i64>(s.n) * max_rhs;
+  }
+  return out;
 }
 
 }  // namespace gmrf

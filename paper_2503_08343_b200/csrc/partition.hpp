@@ -54,4 +54,34 @@ std::vector<i32> partition_owners(const Symbolic& s, int nranks);
 // Every cross-edge message of all four phases, ordered by (phase, point, sn).
 std::vector<XEdge> partition_schedule(const Symbolic& s, const std::vector<i32>& owner);
 
+// First-fit lifetime packing of buffers (size, [start, end] in time steps) into
+// one arena; returns offsets and the arena size.
+std::vector<i64> plan_arena(const std::vector<i64>& size, const std::vector<int>& start,
+                            const std::vector<int>& end, int ntime, i64& total);
+
+// Update-matrix arenas of one rank (factorization: fo, selected inversion: so;
+// offsets in doubles per supernode, sizes in arena_f / arena_s): U_k lives from
+// its first chunk level to the parent's first chunk level, Σ_RR(k) from its
+// gather to its last reader (DeviceFactor's storage, factor.cu).
+void plan_update_arenas(const Symbolic& s, const std::vector<i32>& owner, int rank,
+                        std::vector<i64>& fo, std::vector<i64>& so, i64& arena_f, i64& arena_s);
+
+// Per-rank device memory of a partitioned factorization with selected
+// inversion, from the symbolic alone (no device): the plan a multi-GPU run of
+// config 5 at full size is checked against before any GPU is involved.
+struct RankMemory {
+  i64 l_panels = 0;        // bytes of the owned supernodes' L panels
+  i64 sigma_panels = 0;    // Σ panels (same layout)
+  i64 u_arena_factor = 0;  // lifetime-packed update matrices, factorization
+  i64 u_arena_selinv = 0;  // the same buffer reused for Σ_RR in the selected inversion
+  i64 replicated = 0;      // Q values + map over the pattern, solve vectors
+  i64 supernodes = 0;
+  double flops = 0;        // Σ c² of the owned panels (padded)
+  i64 total() const {
+    return l_panels + sigma_panels + std::max(u_arena_factor, u_arena_selinv) + replicated;
+  }
+};
+std::vector<RankMemory> partition_memory(const Symbolic& s, const std::vector<i32>& owner,
+                                         int nranks, int max_rhs = 16);
+
 }  // namespace gmrf

@@ -357,6 +357,16 @@ SpaceTimePosterior::SpaceTimePosterior(const SpaceTimeSpec& spec, cudaStream_t s
   times_.assemble_ms = now_ms() - t0;
 }
 
+SpaceTimePosterior::SpaceTimePosterior(const SpaceTimeSpec& spec, HostOnly)
+    : spec_(spec), stream_(nullptr) {
+  build_host();
+}
+
+std::shared_ptr<const Symbolic> SpaceTimePosterior::host_symbolic(const SpaceTimeSpec& spec) {
+  SpaceTimePosterior p(spec, HostOnly{});
+  return p.sym_;
+}
+
 SpaceTimePosterior::~SpaceTimePosterior() {
   for (cudaEvent_t e : ev_)
     if (e) cudaEventDestroy(e);

@@ -79,6 +79,8 @@ class SpaceTimePosterior {
   // work (assembly, residuals, line search) is replicated on every rank.
   explicit SpaceTimePosterior(const SpaceTimeSpec& spec, cudaStream_t stream = nullptr,
                               const PartitionSpec* part = nullptr);
+  // Host part only (patterns, geometric ND, symbolic analysis): no device.
+  static std::shared_ptr<const Symbolic> host_symbolic(const SpaceTimeSpec& spec);
   ~SpaceTimePosterior();
 
   // Full pipeline from the IC values u0 (n_s, host). Returns the GN trace.
@@ -105,6 +107,8 @@ class SpaceTimePosterior {
   i32 n_res() const { return nres_; }
 
  private:
+  struct HostOnly {};
+  SpaceTimePosterior(const SpaceTimeSpec& spec, HostOnly);
   void build_host();
   void assemble_device();
   void assemble_values();

@@ -300,3 +300,23 @@ def cholesky_factor_partitioned(q, sym: SymbolicFactor | None = None, group=None
     f = PartitionedFactor(sym, nranks, rank, exchange)
     f.refactor(q.values)
     return f
+
+
+MEMORY_FIELDS = ("l_panels", "sigma_panels", "u_arena_factor", "u_arena_selinv", "replicated",
+                 "total", "supernodes")
+
+
+def memory_plan(sym_handle, nranks: int, owner=None):
+    """Per-rank device-memory plan (bytes) of a partitioned factorization with
+    selected inversion, from a symbolic handle alone (host only):
+    gmrf_partition_memory. Returns a list of dicts, one per rank."""
+    import ctypes as C
+    import numpy as np
+    from . import _capi
+    from ._capi import i32p, i64p, ptr
+    from .core import _check
+    rows = np.zeros((nranks, 7), np.int64)
+    own = None if owner is None else np.ascontiguousarray(owner, np.int32)
+    _check(_capi.load().gmrf_partition_memory(sym_handle, int(nranks), ptr(own, i32p),
+                                              ptr(rows, i64p)))
+    return [dict(zip(MEMORY_FIELDS, map(int, r))) for r in rows]

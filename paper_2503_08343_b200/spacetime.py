@@ -115,6 +115,36 @@ class GaussNewtonStagnation(NumericalError):
         return self._trace
 
 
+def _config(spec: "SpaceTimeSpec", gn: "GaussNewtonConfig | None" = None):
+    gn = gn or GaussNewtonConfig()
+    return _capi.SpaceTimeConfig(
+        spec.n_el, spec.xa, spec.xb, spec.n_t, spec.t_end, spec.diffusion, spec.advection,
+        spec.noise.kappa, spec.noise.alpha, spec.noise.tau, spec.init.kappa, spec.init.alpha,
+        spec.init.tau, spec.tau, spec.eps, int(spec.dirichlet), spec.ic_noise_prec,
+        spec.residual, spec.pde_noise_prec, gn.max_iters, gn.decrement_tol, gn.armijo_c,
+        gn.shrink, gn.max_backtracks, spec.dim)
+
+
+def host_symbolic(spec: "SpaceTimeSpec"):
+    """The pipeline factor's symbolic analysis on the host only (no device):
+    returns (info, supernodes) with supernodes = dict(first, rows, level, parent)."""
+    lib = _capi.load()
+    c = _config(spec)
+    h = C.c_void_p()
+    _check(lib.gmrf_spacetime_symbolic(C.byref(c), C.byref(h)))
+    try:
+        info = _capi.SymbolicInfo()
+        _check(lib.gmrf_symbolic_info(h, C.byref(info)))
+        ns = info.n_supernodes
+        first = np.empty(ns + 1, np.int32)
+        rows, level, parent = (np.empty(ns, np.int32) for _ in range(3))
+        _check(lib.gmrf_symbolic_supernodes(h, ptr(first, i32p), ptr(rows, i32p),
+                                            ptr(level, i32p), ptr(parent, i32p)))
+        return info, dict(first=first, rows=rows, level=level, parent=parent)
+    finally:
+        lib.gmrf_symbolic_free(h)
+
+
 class SpaceTimePosterior:
     def __init__(self, spec: SpaceTimeSpec, gn: GaussNewtonConfig | None = None,
                  partition=None):

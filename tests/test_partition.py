@@ -157,3 +157,49 @@ def test_gloo_exchange_world2(lib_built):
     assert out[0][0] and out[1][0], dict(out)
     assert out[0][1] == out[1][1] > 0
     assert out[0][2] > 1 and out[1][2] > 1
+
+
+# ---- per-rank memory plan (host only) ---------------------------------------
+def test_memory_plan_conserves_panels_and_shrinks_per_rank(lib_built):
+    """gmrf_partition_memory on the config-5 pipeline's own symbolic (32²×64
+    nodes·slices): the ranks' L panels partition the single-GPU panels exactly,
+    and every rank needs less memory than one GPU holding the whole factor."""
+    import ctypes as C
+    from paper_2503_08343_b200 import _capi
+    from paper_2503_08343_b200.core import _check
+    from paper_2503_08343_b200.spacetime import SpaceTimeSpec, _config
+    lib = _capi.load()
+    h = C.c_void_p()
+    _check(lib.gmrf_spacetime_symbolic(C.byref(_config(SpaceTimeSpec.allen_cahn(31, 64))),
+                                       C.byref(h)))
+    try:
+        one = pt.memory_plan(h, 1)[0]
+        info = _capi.SymbolicInfo()
+        _check(lib.gmrf_symbolic_info(h, C.byref(info)))
+        # panels hold rows × w per supernode: the padded lower trapezoid + the diagonal
+        # block's upper triangle
+        assert one["l_panels"] >= 8 * info.nnz_l_padded
+        for nr in (2, 4, 8):
+            plan = pt.memory_plan(h, nr)
+            assert sum(p["l_panels"] for p in plan) == one["l_panels"]
+            assert sum(p["supernodes"] for p in plan) == info.n_supernodes
+            assert max(p["total"] for p in plan) < one["total"]
+            assert all(p["u_arena_factor"] <= one["u_arena_factor"] + 8 * info.max_front ** 2
+                       for p in plan)
+    finally:
+        lib.gmrf_symbolic_free(h)
+
+
+def test_full_config5_memory_plan_fits_four_b200s():
+    """The committed plan of the full config 5 (128²×256, n = 4.19M;
+    tools/memory_plan.py, profiles/r02_c5_memory_plan.json — minutes of host
+    symbolic analysis, so generated once): one B200 (180 GB) cannot hold it,
+    4 ranks each fit below 170 GB."""
+    import json
+    path = os.path.join(os.path.dirname(__file__), "..", "profiles", "r02_c5_memory_plan.json")
+    if not os.path.exists(path):
+        pytest.skip("profiles/r02_c5_memory_plan.json not generated")
+    plan = json.load(open(path))
+    assert plan["n"] == 128 * 128 * 256
+    assert plan["ranks"]["1"]["max_total_gb"] > 180.0
+    assert plan["ranks"]["4"]["max_total_gb"] < 170.0
