@@ -232,7 +232,7 @@ class DeviceFactor {
   // supernodes of at least inc_u_ chunks accumulate their update matrix chunk by
   // chunk (U -= L21(c) L21(c)ᵀ right after chunk c's panel, on uu_) instead of
   // one K = w SYRK after the last chunk on the critical path; 0 disables
-  int inc_u_ = 4;
+  int inc_u_ = 0;
   // GMRF_TRACE=<file>: per-level timeline markers (k_mark), appended per factorization
   static constexpr int kTraceSlots = 10;
   std::string trace_file_;
