@@ -102,6 +102,13 @@ int gmrf_factor_numeric_device(gmrf_factor_t* f, const double* d_q_values, int32
 int gmrf_solve(gmrf_factor_t* f, int mode, int32_t nrhs, const double* b, double* x);
 int gmrf_solve_device(gmrf_factor_t* f, int mode, int32_t nrhs, const double* d_b, double* d_x);
 
+/* Selected inversion in place (on = 1): Σ overwrites L chunk by chunk, halving
+ * the factor's device memory; the factor is consumed (solves, samples and a
+ * second selected inversion fail with GMRF_ERR_CONTRACT until the next
+ * numeric factorization). Default 0 for generic factors; the pipelines
+ * (gmrf_spacetime_*, gmrf_regression_*) use it — variances are their last step.
+ * Set before the first selected inversion of the factor. */
+int gmrf_factor_set_selinv_inplace(gmrf_factor_t* f, int32_t on);
 /* takahashi_diagonal (core/takahashi.hpp:67): diag(Q⁻¹) in original order. */
 int gmrf_selinv_diag(gmrf_factor_t* f, double* diag);
 int gmrf_selinv_diag_device(gmrf_factor_t* f, double* d_diag);

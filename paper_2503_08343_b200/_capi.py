@@ -141,6 +141,7 @@ SIGNATURES = {
     "gmrf_partition_owners": (C.c_int, [vp, C.c_int32, i32p]),
     "gmrf_partition_schedule": (C.c_int, [vp, i32p, i64p, i64p]),
     "gmrf_partition_memory": (C.c_int, [vp, C.c_int32, i32p, i64p]),
+    "gmrf_factor_set_selinv_inplace": (C.c_int, [vp, C.c_int32]),
     "gmrf_factor_create_partitioned": (C.c_int, [vp, C.c_int32, C.c_int32, i32p, EXCHANGE_FN, vp,
                                                  C.POINTER(vp)]),
     "gmrf_spacetime_create_partitioned": (C.c_int, [C.POINTER(SpaceTimeConfig), C.c_int32,

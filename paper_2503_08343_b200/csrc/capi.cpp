@@ -213,6 +213,10 @@ int gmrf_partition_schedule(const gmrf_symbolic_t* h, const int32_t* owner, int6
   });
 }
 
+int gmrf_factor_set_selinv_inplace(gmrf_factor_t* f, int32_t on) {
+  return guard([&] { f->f->set_selinv_inplace(on != 0); });
+}
+
 int gmrf_partition_memory(const gmrf_symbolic_t* s, int32_t nranks, const int32_t* owner,
                           int64_t* rows) {
   return guard([&] {

@@ -418,7 +418,8 @@ SymDev DeviceFactor::symdev() const {
 }
 
 int64_t DeviceFactor::device_bytes() const {
-  return static_cast<int64_t>((L_.n + U_.n + Sig_.n + q_.n + P_.n + Uv_.n + v1_.n + v2_.n) *
+  return static_cast<int64_t>((L_.n + U_.n + Sig_.n + ystage_.n + q_.n + P_.n + Uv_.n + v1_.n +
+                               v2_.n) *
                               sizeof(double)) +
          static_cast<int64_t>(gemm_.n * sizeof(GemmTask) + sgemm_.n * sizeof(GemmTask));
 }
@@ -713,10 +714,26 @@ void DeviceFactor::build_factor_plan() {
 
 void DeviceFactor::build_selinv_plan() {
   const Symbolic& s = *sym_;
-  Sig_.alloc(std::max<int64_t>(lptr_h_[s.ns], 1));
+  // in place: Σ overwrites L chunk by chunk (each chunk's L is dead once its Σ
+  // columns exist: Y and W = L_{R,J}ᵀ Y are staged in a per-level workspace
+  // first), halving the factor's memory for the full config 5
+  if (!sel_inplace_) Sig_.alloc(std::max<int64_t>(lptr_h_[s.ns], 1));
   std::vector<int> lvl0, last;
   int nlev = 0;
   chunk_levels(s, lvl0, last, nlev, 0);
+  // per-level staging of Y (nbelow × w) and W / Z (w × w) of every chunk
+  std::vector<int64_t> yoff(nlev, 0);
+  for (int k = 0; k < s.ns; ++k) {
+    if (!mine(k)) continue;
+    for (int c = 0; c < nchunks(s.w(k)); ++c) {
+      const int c0 = c * kNB, wk = std::min(kNB, s.w(k) - c0);
+      yoff[lvl0[k] + c] += static_cast<int64_t>(s.rows(k) - c0) * wk;  // (nbelow + wk) · wk
+    }
+  }
+  int64_t ymax = 1;
+  for (int64_t v : yoff) ymax = std::max(ymax, v);
+  ystage_.alloc(ymax);
+  std::fill(yoff.begin(), yoff.end(), 0);
   std::vector<std::vector<ColTask>> ga(nlev), gg(nlev);
   std::vector<std::vector<GemmTask>> yg(nlev), zg(nlev);
   std::vector<std::vector<SelChunk>> tr(nlev), dg(nlev), mi(nlev);
@@ -724,7 +741,7 @@ void DeviceFactor::build_selinv_plan() {
       d_f(nlev, 0.0);
   double* L = L_.p;
   double* U = U_.p;
-  double* S = Sig_.p;
+  double* S = sig();
   for (int k = 0; k < s.ns; ++k) {
     const int w = s.w(k), rows = s.rows(k), r = rows - w;
     const int par = s.sn_parent[k];
@@ -756,10 +773,14 @@ void DeviceFactor::build_selinv_plan() {
         z_f[lv] += 2.0 * nb * wk * wk;
         d_f[lv] += 2.0 * wk * wk * wk;
       }
+      const int nbelow = rows - c0 - wk;
+      double* Yst = ystage_.p + yoff[lv];          // Y: nbelow × wk, ld nbelow
+      double* Wst = Yst + static_cast<int64_t>(nbelow) * wk;  // W, then Z: wk × wk
+      yoff[lv] += static_cast<int64_t>(nbelow + wk) * wk;
       auto ytile = [&](int i0, int i1) {
         GemmTask g{};
-        g.c = Sk + i0 + static_cast<int64_t>(c0) * rows;
-        g.ldc = rows;
+        g.c = Yst + (i0 - c0 - wk);
+        g.ldc = std::max(nbelow, 1);
         g.m = i1 - i0;
         g.n = wk;
         g.alpha = 1.0;
@@ -786,25 +807,48 @@ void DeviceFactor::build_selinv_plan() {
       };
       for (int i0 = c0 + wk; i0 < w; i0 += kTile) ytile(i0, std::min(i0 + kTile, w));
       for (int i0 = w; i0 < rows; i0 += kTile) ytile(i0, std::min(i0 + kTile, rows));
-      const int nbelow = rows - c0 - wk;
       const double* rdc = rdiag_.p + s.sn_first[k] + c0;
-      for (int t = 0; t * kTrsmRows < nbelow; ++t) tr[lv].push_back({Lk, Sk, rows, c0, wk, w, t, rdc});
+      // W = L_{R,J}ᵀ Y (before Σ_{R,J} may overwrite L_{R,J}); Z = −W L_JJ⁻¹ =
+      // L_{R,J}ᵀ Σ_{R,J} (takahashi.hpp:43-60 in supernodal form)
       GemmTask z{};
-      z.c = Sk + c0 + static_cast<int64_t>(c0) * rows;
-      z.ldc = rows;
+      z.c = Wst;
+      z.ldc = wk;
       z.m = wk;
       z.n = wk;
       z.a[0] = Lk + (c0 + wk) + static_cast<int64_t>(c0) * rows;
       z.lda[0] = rows;
-      z.b[0] = Sk + (c0 + wk) + static_cast<int64_t>(c0) * rows;
-      z.ldb[0] = rows;
+      z.b[0] = Yst;
+      z.ldb[0] = std::max(nbelow, 1);
       z.k[0] = nbelow;
       z.flags = 1;  // A transposed
       z.alpha = 1.0;
       z.beta = 0.0;
       zg[lv].push_back(z);
-      dg[lv].push_back({Lk, Sk, rows, c0, wk, w, 0, rdc});
-      for (int t = 0; t * 64 < p; ++t) mi[lv].push_back({Lk, Sk, rows, c0, wk, w, t, rdc});
+      SelChunk base{Lk, Sk, rows, c0, wk, w, 0, rdc, nullptr, nullptr, 0, 0, 0, Wst, wk};
+      for (int t = 0; t * kTrsmRows < nbelow; ++t) {  // Σ_{R,J} = −Y L_JJ⁻¹ into the Σ panel
+        SelChunk c = base;
+        c.tile = t;
+        c.src = Yst;
+        c.lds = nbelow;
+        c.dst = Sk + (c0 + wk) + static_cast<int64_t>(c0) * rows;
+        c.ldd = rows;
+        c.nrows = nbelow;
+        tr[lv].push_back(c);
+      }
+      {  // Z = −W L_JJ⁻¹, in its staging slot
+        SelChunk c = base;
+        c.src = Wst;
+        c.dst = Wst;
+        c.lds = c.ldd = wk;
+        c.nrows = wk;
+        tr[lv].push_back(c);
+      }
+      dg[lv].push_back(base);
+      for (int t = 0; t * 64 < p; ++t) {
+        SelChunk c = base;
+        c.tile = t;
+        mi[lv].push_back(c);
+      }
     }
   }
   std::vector<int64_t> gyt(nlev, 0), gzt(nlev, 0);  // Y / Z tiles of all ranks per level
@@ -1324,7 +1368,7 @@ void DeviceFactor::launch_solve_levels(bool fwd, bool bwd, double* y, int nr) {
 }
 
 void DeviceFactor::solve(int mode, int nrhs, const double* b, double* x, bool on_device) {
-  require(factored_, kContract, "solve: factor not computed");
+  require(factored_, kContract, "solve: factor not computed (or consumed by an in-place selected inversion)");
   require(mode >= 0 && mode <= 2, kContract, "solve_triangular: unknown mode");
   const Symbolic& s = *sym_;
   const int n = s.n;
@@ -1385,7 +1429,7 @@ void DeviceFactor::solve(int mode, int nrhs, const double* b, double* x, bool on
 }
 
 void DeviceFactor::selinv(double* diag_out, bool on_device) {
-  require(factored_, kContract, "selinv: factor not computed");
+  require(factored_, kContract, "selinv: factor not computed (or consumed by an in-place selected inversion)");
   if (!selinv_plan_) build_selinv_plan();
   const Symbolic& s = *sym_;
   launches_selinv_ = 0;
@@ -1397,7 +1441,7 @@ void DeviceFactor::selinv(double* diag_out, bool on_device) {
       int blocks = static_cast<int>((e.gan * 32 + 255) / 256);
       pf.run(stream_, pf.tag("selinv.gather", l), 0.0, e.ga_bytes, [&] {
         k_sel_gather<<<blocks, 256, 0, stream_>>>(sga_.p + e.ga0, static_cast<int>(e.gan), sd,
-                                                 snparent_.p, Sig_.p, U_.p);
+                                                 snparent_.p, sig(), U_.p);
       });
       ++launches_selinv_;
     }
@@ -1409,6 +1453,15 @@ void DeviceFactor::selinv(double* diag_out, bool on_device) {
                                                                             sparts_.p);
       });
       launches_selinv_ += 1 + (e.yrn > 0);
+    }
+    if (e.zn) {
+      pf.run(stream_, pf.tag("selinv.gemm_dmma", l), e.z_flops, 0.0, [&] {
+        launch_gemm(sgemm_.p + e.z0, e.zn, stream_);
+        if (e.zrn)
+          k_reduce_parts<<<static_cast<unsigned>(e.zrn), 256, 0, stream_>>>(sred_.p + e.zr0,
+                                                                            sparts_.p);
+      });
+      launches_selinv_ += 1 + (e.zrn > 0);
     }
     if (e.tn) {
       pf.run(stream_, pf.tag("selinv.trsm", l), e.t_flops, 0.0, [&] {
@@ -1423,15 +1476,6 @@ void DeviceFactor::selinv(double* diag_out, bool on_device) {
                                                                                        e.tb0[2]);
       });
       launches_selinv_ += (e.tbn[0] > 0) + (e.tbn[1] > 0) + (e.tbn[2] > 0);
-    }
-    if (e.zn) {
-      pf.run(stream_, pf.tag("selinv.gemm_dmma", l), e.z_flops, 0.0, [&] {
-        launch_gemm(sgemm_.p + e.z0, e.zn, stream_);
-        if (e.zrn)
-          k_reduce_parts<<<static_cast<unsigned>(e.zrn), 256, 0, stream_>>>(sred_.p + e.zr0,
-                                                                            sparts_.p);
-      });
-      launches_selinv_ += 1 + (e.zrn > 0);
     }
     if (e.dn) {
       pf.run(stream_, pf.tag("selinv.diag", l), e.d_flops, 0.0, [&] {
@@ -1457,7 +1501,7 @@ void DeviceFactor::selinv(double* diag_out, bool on_device) {
       int blocks = static_cast<int>((e.ggn * 32 + 255) / 256);
       pf.run(stream_, pf.tag("selinv.gather", l), 0.0, 0.0, [&] {
         k_sel_gather<<<blocks, 256, 0, stream_>>>(sga_.p + e.gg0, static_cast<int>(e.ggn), sd,
-                                                 snparent_.p, Sig_.p, U_.p);
+                                                 snparent_.p, sig(), U_.p);
       });
       ++launches_selinv_;
     }
@@ -1470,7 +1514,7 @@ void DeviceFactor::selinv(double* diag_out, bool on_device) {
   }
   if (s.n > 0) {
     k_extract_diag<<<std::max(1, std::min((s.n + 255) / 256, 148 * 8)), 256, 0, stream_>>>(
-        sd, col2sn_.p, perm_.p, Sig_.p, part_ ? colmine_.p : nullptr, out);
+        sd, col2sn_.p, perm_.p, sig(), part_ ? colmine_.p : nullptr, out);
     ++launches_selinv_;
     if (part_) exchange({{2, -1, -1, -1, out, static_cast<int64_t>(s.n)}});
   }
@@ -1481,12 +1525,13 @@ void DeviceFactor::selinv(double* diag_out, bool on_device) {
     cuda_check(cudaStreamSynchronize(stream_), "selinv");
   }
   selinv_done_ = true;
+  if (sel_inplace_) factored_ = false;  // L now holds Σ: solves need a new factorization
 }
 
 // Batches of up to kMaxRhs samples: z drawn on the host in the reference's
 // order, one multi-RHS upper solve (kUpper, cholesky.hpp:194-201), Pᵀ, + μ.
 void DeviceFactor::sample_direct(const double* d_mean, int ns, uint64_t seed, double* d_out) {
-  require(factored_, kContract, "sample_direct: factor not computed");
+  require(factored_, kContract, "sample_direct: factor not computed (or consumed by an in-place selected inversion)");
   const Symbolic& s = *sym_;
   const int n = s.n;
   if (n == 0 || ns <= 0) return;
@@ -1514,7 +1559,7 @@ void DeviceFactor::sample_direct(const double* d_mean, int ns, uint64_t seed, do
 void DeviceFactor::rbmc_variance(const double* d_qv, const double* d_mean, int ns, uint64_t seed,
                                  double* d_var) {
   require(ns >= 2, kContract, "rbmc_variance: need at least 2 samples");
-  require(factored_, kContract, "rbmc_variance: factor not computed");
+  require(factored_, kContract, "rbmc_variance: factor not computed (or consumed by an in-place selected inversion)");
   const Symbolic& s = *sym_;
   const int n = s.n;
   if (n == 0) return;
@@ -1570,8 +1615,8 @@ void DeviceFactor::copy_l_panels(std::vector<double>& out) const {
 }
 
 void DeviceFactor::copy_sig_panels(std::vector<double>& out) const {
-  out.resize(Sig_.n);
-  cuda_check(cudaMemcpyAsync(out.data(), Sig_.p, Sig_.n * sizeof(double), cudaMemcpyDeviceToHost,
+  out.resize(sel_inplace_ ? L_.n : Sig_.n);
+  cuda_check(cudaMemcpyAsync(out.data(), sig(), out.size() * sizeof(double), cudaMemcpyDeviceToHost,
                              stream_),
              "copy Sigma");
   cuda_check(cudaStreamSynchronize(stream_), "copy Sigma");

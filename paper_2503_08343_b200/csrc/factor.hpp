@@ -126,7 +126,15 @@ class DeviceFactor {
   const std::vector<i32>& owners() const { return owner_; }
 
   double* d_l() { return L_.p; }
-  double* d_sig() { return Sig_.p; }
+  double* d_sig() { return sig(); }
+  // Σ overwrites L (halves the factor's memory); after selinv the factor is
+  // consumed (solves fail until the next numeric factorization). Set before
+  // prepare_selinv / the first selinv.
+  void set_selinv_inplace(bool on) {
+    require(!selinv_plan_ || on == sel_inplace_, kContract, "selinv: in-place mode fixed by its plan");
+    sel_inplace_ = on;
+  }
+  bool selinv_inplace() const { return sel_inplace_; }
   bool factored() const { return factored_; }
   bool has_selinv() const { return selinv_done_; }
   int64_t device_bytes() const;
@@ -183,6 +191,9 @@ class DeviceFactor {
   DevBuf<int32_t> first_, rows_, relmap_, chptr_, chlist_, perm_, col2sn_, snparent_, status_;
   DevBuf<int64_t> rptr_, lptr_, uptr_, uptrs_, qmap_, pptr_, uvptr_;
   DevBuf<double> L_, U_, Sig_, q_, P_, Uv_, v1_, v2_, diag_, rdiag_;
+  DevBuf<double> ystage_;      // selected inversion: per-level Y / W staging
+  bool sel_inplace_ = false;
+  double* sig() const { return sel_inplace_ ? L_.p : Sig_.p; }
   DevBuf<SolveTile> tiles_;
   DevBuf<double> pf_;       // forward column-block partials (solve.cuh)
   DevBuf<unsigned> pfctr_;  // their arrival counters

@@ -65,13 +65,20 @@ struct ColTask {
 // Selected-inversion per-chunk dense work.
 struct SelChunk {
   const double* l;   // L panel of the supernode
-  double* sig;       // Σ panel of the supernode
+  double* sig;       // Σ panel of the supernode (may alias l: in-place selected inversion)
   int32_t ld;        // rows of the supernode
   int32_t c0;        // chunk offset inside the panel
   int32_t w;         // chunk width
   int32_t wsn;       // supernode width
   int32_t tile;      // TRSM row slab (for the TRSM kernel)
   const double* rd;  // 1/L_jj of the chunk's first column (factorization pivots)
+  // TRSM: rows [0, nrows) of src (ld lds) → dst (ld ldd), dst = −src · L_JJ⁻¹;
+  // diag: z = Z (w × w, ld ldz), Σ_JJ = L_JJ⁻ᵀ (L_JJ⁻¹ − Z)
+  const double* src;
+  double* dst;
+  int32_t lds, ldd, nrows;
+  const double* z;
+  int32_t ldz;
 };
 
 // One 64-row block of a wide supernode's triangle in the solves (solve_wide.cuh).

@@ -265,7 +265,19 @@ std::vector<RankMemory> partition_memory(const Symbolic& s, const std::vector<i3
     plan_update_arenas(s, owner, r, fo, so, af, as);
     m.u_arena_factor = 8 * af;
     m.u_arena_selinv = 8 * as;
-    m.sigma_panels = m.l_panels;
+    // the pipelines run the selected inversion in place (Σ overwrites L): only
+    // the per-level Y / W staging is extra (DeviceFactor::build_selinv_plan)
+    {
+      std::vector<int> l0, la;
+      int nl = 0;
+      chunk_levels(s, l0, la, nl, 0);
+      std::vector<i64> st(std::max(nl, 1), 0);
+      for (int k = 0; k < s.ns; ++k)
+        if (owner[k] == r)
+          for (int c = 0, w = s.w(k); c * kNB < w; ++c)
+            st[l0[k] + c] += static_cast<i64>(s.rows(k) - c * kNB) * std::min(kNB, w - c * kNB);
+      m.sigma_panels = 8 * *std::max_element(st.begin(), st.end());
+    }
     // replicated per rank: Q values + qmap over the pattern, solve vectors
     m.replicated = 16 * static_cast<i64>(s.qri.size()) + 8 * 4 * static_cast<i64>(s.n) * max_rhs;
   }

@@ -71,7 +71,7 @@ void plan_update_arenas(const Symbolic& s, const std::vector<i32>& owner, int ra
 // config 5 at full size is checked against before any GPU is involved.
 struct RankMemory {
   i64 l_panels = 0;        // bytes of the owned supernodes' L panels
-  i64 sigma_panels = 0;    // Σ panels (same layout)
+  i64 sigma_panels = 0;    // Σ beyond L: in-place selected inversion → its per-level staging
   i64 u_arena_factor = 0;  // lifetime-packed update matrices, factorization
   i64 u_arena_selinv = 0;  // the same buffer reused for Σ_RR in the selected inversion
   i64 replicated = 0;      // Q values + map over the pattern, solve vectors

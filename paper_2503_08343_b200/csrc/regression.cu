@@ -180,6 +180,7 @@ RegressionPosterior::RegressionPosterior(const MeshSpec& mesh, const MaternSpec&
   sym_ = std::make_shared<const Symbolic>(analyze(n_, pcp_.data(), pri_.data(), perm, opt));
   fac_ = std::make_unique<DeviceFactor>(sym_, stream_);
   fac_->set_profiler(&prof_);
+  fac_->set_selinv_inplace(true);
   gram_k_ = std::make_unique<GramPlan>(n_, pcp_.data(), pri_.data(), mk, kcp.data(), kri.data(),
                                        nullptr, stream_);
   gram_a_ = std::make_unique<GramPlan>(n_, pcp_.data(), pri_.data(), m, arp_.data(), aci_.data(),
@@ -243,13 +244,13 @@ void RegressionPosterior::run(const double* y, const double* noise_prec, bool va
     fail(kNotSpd, "condition_affine: cholesky: non-positive pivot at index " + std::to_string(bad));
   fac_->solve(2, 1, rhs_.p, mean_.p, true);  // μ_post = 0 + Q_post⁻¹ rhs
   times_.kernel_launches += fac_->launches_solve();
-  if (variances) {
-    fac_->selinv(var_.p, true);
-    times_.kernel_launches += fac_->launches_selinv();
-  }
   if (n_samples > 0) {
     samples_.alloc(static_cast<size_t>(n_) * n_samples);
     fac_->sample_direct(mean_.p, n_samples, seed, samples_.p);
+  }
+  if (variances) {  // last use of the factor: Σ overwrites L in place
+    fac_->selinv(var_.p, true);
+    times_.kernel_launches += fac_->launches_selinv();
   }
   ns_done_ = n_samples;
   cudaEventRecord(ev_[1], stream_);

@@ -1,7 +1,8 @@
 // Per-chunk dense steps of the supernodal selected inversion (takahashi.hpp
 // recurrences, supernodal form), register resident and barrier free:
-//   k_sel_trsm<W>: Σ_{R,J} = −Y · L_JJ⁻¹ for one 128-row slab, one row per
-//                  thread (x·L = b, right-looking over the columns, j descending);
+//   k_sel_trsm<W>: dst = −src · L_JJ⁻¹ for one 128-row slab, one row per
+//                  thread (x·L = b, right-looking over the columns, j descending):
+//                  Σ_{R,J} from Y, and Z = −W L_JJ⁻¹ from W = L_{R,J}ᵀ Y;
 //   k_sel_diag<W>: Σ_JJ = L_JJ⁻ᵀ (L_JJ⁻¹ − Z), one column per thread:
 //                  forward solve L x = e_c, subtract z_c, backward solve Lᵀ s = x.
 // W is the chunk width bucket (16/32/64, identity padded). L_JJ is staged once
@@ -37,14 +38,14 @@ __global__ void __launch_bounds__(kTrsmRows) k_sel_trsm_w(const SelChunk* __rest
     dg[tid] = tid < w ? Lk[tid + static_cast<int64_t>(tid) * ld] : 1.0;
     rd[tid] = tid < w ? t.rd[tid] : 1.0;
   }
-  const int nbelow = ld - t.c0 - w;
   const int r0 = t.tile * kTrsmRows;
-  const int nr = min(kTrsmRows, nbelow - r0);
-  double* B = t.sig + t.c0 + w + r0 + tid + static_cast<int64_t>(t.c0) * ld;
+  const int nr = min(kTrsmRows, t.nrows - r0);
+  const double* B = t.src + r0 + tid;
+  double* D = t.dst + r0 + tid;
   const bool act = tid < nr;
   double b[W];
 #pragma unroll
-  for (int j = 0; j < W; ++j) b[j] = (act && j < w) ? -B[static_cast<int64_t>(j) * ld] : 0.0;
+  for (int j = 0; j < W; ++j) b[j] = (act && j < w) ? -B[static_cast<int64_t>(j) * t.lds] : 0.0;
   __syncthreads();
 #pragma unroll
   for (int j = W - 1; j >= 0; --j) {
@@ -62,8 +63,9 @@ __global__ void __launch_bounds__(kTrsmRows) k_sel_trsm_w(const SelChunk* __rest
   if (act) {
 #pragma unroll
     for (int j = 0; j < W; ++j)
-      if (j < w) B[static_cast<int64_t>(j) * ld] = b[j];
+      if (j < w) D[static_cast<int64_t>(j) * t.ldd] = b[j];
   }
+  (void)ld;
 }
 
 template <int W>
@@ -107,9 +109,9 @@ __global__ void __launch_bounds__(W < 32 ? 32 : W) k_sel_diag_w(const SelChunk* 
 #pragma unroll
     for (int k = i + 1; k < W; ++k) x[k] = fma(-xi, Lc[i * P + k], x[k]);
   }
-  // x − z_c  (Z = L_{R,J}ᵀ Σ_{R,J}, stored in the Σ diagonal block)
+  // x − z_c  (Z = L_{R,J}ᵀ Σ_{R,J}, staged by the plan in its own w × w slot)
   if (act) {
-    const double* zc = Sk + static_cast<int64_t>(c) * ld;
+    const double* zc = t.z + static_cast<int64_t>(c) * t.ldz;
 #pragma unroll
     for (int k = 0; k < W; ++k)
       if (k < w) x[k] -= zc[k];
@@ -122,7 +124,7 @@ __global__ void __launch_bounds__(W < 32 ? 32 : W) k_sel_diag_w(const SelChunk* 
 #pragma unroll
     for (int k = 0; k < i; ++k) x[k] = fma(-si, Lt[i * P + k], x[k]);
   }
-  __syncthreads();  // every thread has read its z column before Σ_JJ is overwritten
+  __syncthreads();  // every thread has read L_JJ before Σ_JJ overwrites it (in place)
   if (act) {
 #pragma unroll
     for (int i = 0; i < W; ++i)

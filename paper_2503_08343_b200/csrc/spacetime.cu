@@ -619,6 +619,7 @@ void SpaceTimePosterior::assemble_device() {
     std::fprintf(stderr, "[gmrf] after %s: device free %.1f of %.1f GB\n", what, fr * 1e-9, tot * 1e-9);
   };
   mem("factor storage");
+  fac_->set_selinv_inplace(true);  // variances are the last use of each factorization
   fac_->prepare_selinv();
   mem("selected-inversion storage");
   fac_->set_profiler(&prof_);
