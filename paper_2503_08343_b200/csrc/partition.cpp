@@ -60,9 +60,13 @@ std::vector<i32> partition_owners(const Symbolic& s, int nranks) {
       if (s.sn_parent[k] < 0) top.roots.push_back(k);
     todo.push_back(std::move(top));
   }
-  while (!todo.empty()) {
-    Item it = std::move(todo.back());
-    todo.pop_back();
+  // separators (single roots over a rank range) go to the rank of their range
+  // holding the fewest separator panel bytes so far, top-down (breadth first):
+  // the big top fronts spread over the ranks instead of stacking on the lowest
+  // rank of every range (per-rank memory plan, gmrf_partition_memory)
+  std::vector<double> sep_bytes(nranks, 0.0);
+  for (size_t head = 0; head < todo.size(); ++head) {
+    Item it = std::move(todo[head]);
     if (it.roots.empty()) continue;
     if (it.r1 - it.r0 == 1) {
       for (int k : it.roots) fill(k, it.r0);
@@ -70,7 +74,11 @@ std::vector<i32> partition_owners(const Symbolic& s, int nranks) {
     }
     if (it.roots.size() == 1) {
       const int k = it.roots[0];
-      owner[k] = it.r0;
+      int best = it.r0;
+      for (int r = it.r0 + 1; r < it.r1; ++r)
+        if (sep_bytes[r] < sep_bytes[best]) best = r;
+      owner[k] = best;
+      sep_bytes[best] += static_cast<double>(s.rows(k)) * s.w(k);
       Item ch{{}, it.r0, it.r1};
       for (int q = s.ch_ptr[k]; q < s.ch_ptr[k + 1]; ++q) ch.roots.push_back(s.ch_list[q]);
       todo.push_back(std::move(ch));
