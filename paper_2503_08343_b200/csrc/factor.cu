@@ -9,6 +9,7 @@
 #include <string>
 
 #include "kernels.cu"  // single translation unit for all device code
+#include "gemm_wide.cuh"
 #include "panel.cuh"
 #include "panel2.cuh"
 #include "rng.hpp"
@@ -30,6 +31,9 @@ namespace {
 void set_smem_attrs() {
   static bool done = false;
   if (done) return;
+  cuda_check(cudaFuncSetAttribute(k_gemm_wide, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  gemm_wide_smem_bytes()),
+             "smem k_gemm_wide");
   cuda_check(cudaFuncSetAttribute(k_potrf_trsm<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   panel_smem_bytes<64>()),
              "smem k_potrf_trsm");
@@ -70,7 +74,10 @@ __global__ void k_mark(unsigned long long* buf, int idx) {
 void launch_gemm(const GemmTask* tasks, int64_t n, cudaStream_t st) {
   k_gemm_tiles<<<static_cast<unsigned>(n), 128, 0, st>>>(tasks);
 }
-constexpr unsigned kRowsMaxCtas = 148;  // one CTA per SM (k_panel_rows uses ~254 registers)
+// 128×128 tiles, TMA-staged (gemm_wide.cuh)
+void launch_gemm_wide(const GemmTask* tasks, int64_t n, cudaStream_t st) {
+  k_gemm_wide<<<static_cast<unsigned>(n), kWThreads, gemm_wide_smem_bytes(), st>>>(tasks);
+}
 
 template <int NR>
 void set_solve_smem(int maxw) {
@@ -128,7 +135,14 @@ DeviceFactor::DeviceFactor(std::shared_ptr<const Symbolic> sym, cudaStream_t str
     lptr_h_[k + 1] = lptr_h_[k] + (mine(k) ? static_cast<i64>(s.rows(k)) * s.w(k) : 0);
   if (const char* e = std::getenv("GMRF_U_STATIC")) u_static_ = e[0] != '0';
   if (const char* e = std::getenv("GMRF_DEFER")) defer_ = std::max(1, atoi(e));
+  if (const char* e = std::getenv("GMRF_DEFER_MIN")) defer_min_ = atoll(e);
   if (const char* e = std::getenv("GMRF_INC_U")) inc_u_ = std::max(0, atoi(e));
+  if (const char* e = std::getenv("GMRF_EA_SPLIT")) ea_split_ = e[0] != '0';
+  if (const char* e = std::getenv("GMRF_WIDE_K")) wide_min_k_ = atoi(e);
+  if (const char* e = std::getenv("GMRF_WIDE_R")) wide_min_r_ = atoi(e);
+  if (const char* e = std::getenv("GMRF_INC_B")) inc_b_ = std::max(1, atoi(e));
+  if (const char* e = std::getenv("GMRF_EA_CTA")) ea_cta_max_ = atoll(e);
+  if (const char* e = std::getenv("GMRF_ROWS_CTAS")) rows_max_ctas_ = static_cast<unsigned>(atoi(e));
   if (const char* e = std::getenv("GMRF_TRACE")) trace_file_ = e;
   plan_update_storage();
   std::vector<i64> qm;
@@ -343,18 +357,23 @@ DeviceFactor::DeviceFactor(std::shared_ptr<const Symbolic> sym, cudaStream_t str
     int lo = 0, hi = 0;
     cuda_check(cudaDeviceGetStreamPriorityRange(&lo, &hi), "priorities");
     cuda_check(cudaStreamCreateWithPriority(&main_, cudaStreamNonBlocking, hi), "main stream");
-    cuda_check(cudaStreamCreateWithPriority(&aux_, cudaStreamNonBlocking, lo), "aux stream");
+    // (numerically higher = lower priority) the bulk trailing updates feed the chain
+    // a level later, so they rank above the incremental U batches
+    const int mid = hi < lo ? lo - 1 : lo;
+    cuda_check(cudaStreamCreateWithPriority(&aux_, cudaStreamNonBlocking, mid), "aux stream");
     cuda_check(cudaStreamCreateWithPriority(&uu_, cudaStreamNonBlocking, lo), "update stream");
     cuda_check(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming), "event");
   }
   ev_panel_.resize(flev_.size());
   ev_rest_.resize(flev_.size());
   ev_uupd_.resize(flev_.size());
+  ev_eau_.resize(flev_.size());
   if (!trace_file_.empty()) tbuf_.alloc(flev_.size() * kTraceSlots);
   for (size_t l = 0; l < flev_.size(); ++l) {
     cuda_check(cudaEventCreateWithFlags(&ev_panel_[l], cudaEventDisableTiming), "event");
     cuda_check(cudaEventCreateWithFlags(&ev_rest_[l], cudaEventDisableTiming), "event");
     cuda_check(cudaEventCreateWithFlags(&ev_uupd_[l], cudaEventDisableTiming), "event");
+    cuda_check(cudaEventCreateWithFlags(&ev_eau_[l], cudaEventDisableTiming), "event");
   }
   cuda_check(cudaStreamSynchronize(stream_), "factor setup");
 }
@@ -364,6 +383,7 @@ DeviceFactor::~DeviceFactor() {
   for (cudaEvent_t e : ev_panel_) cudaEventDestroy(e);
   for (cudaEvent_t e : ev_rest_) cudaEventDestroy(e);
   for (cudaEvent_t e : ev_uupd_) cudaEventDestroy(e);
+  for (cudaEvent_t e : ev_eau_) cudaEventDestroy(e);
   if (ev_fork_) cudaEventDestroy(ev_fork_);
   if (uu_) cudaStreamDestroy(uu_);
   if (aux_) cudaStreamDestroy(aux_);
@@ -433,8 +453,8 @@ int64_t DeviceFactor::device_bytes() const {
 // right-looking (next block with chunk c; rest with chunk c).
 //   emit(crit, j0, j1, k0, k1): columns [j0, j1) -= L[:, k0:k1] L[j0:j1, k0:k1]ᵀ
 template <class F>
-void DeviceFactor::trailing_jobs(int w, int c, F&& emit) const {
-  const int D = defer_, nch = nchunks(w);
+void DeviceFactor::trailing_jobs(int w, int rows, int c, F&& emit) const {
+  const int D = defer_of(w, rows), nch = nchunks(w);
   auto last_flush_le = [D](int x) { return x < -1 ? -1 : ((x + 1) / D) * D - 1; };
   const int c1 = std::min(w, (c + 1) * kNB);
   if (c + 1 < nch) {
@@ -450,14 +470,16 @@ void DeviceFactor::build_factor_plan() {
   std::vector<int> lvl0, last;
   int nlev = 0;
   chunk_levels(s, lvl0, last, nlev, kSmallRows);
-  std::vector<std::vector<EaTask>> ea(nlev);
+  // extend-add tasks per level: panel columns (b < w, the panel step waits for
+  // them) and update-block columns (only the level's U SYRKs need them)
+  std::vector<std::vector<EaTask>> ea(nlev), eau(nlev);
   std::vector<int2> ea_pairs;  // (child, first row of its update column), child order
   std::vector<int32_t> cnt;
   std::vector<std::vector<PanelTask>> pan(nlev), po(nlev), pdg(nlev), ptr2(nlev);
   // GEMM tasks per level: gm = the update of the chunk's NEXT column block (on
   // the critical chain), gr = the rest of the trailing update + the U SYRK
   // (overlapped with the next level's panel on the second stream)
-  std::vector<std::vector<GemmTask>> gm(nlev), gr(nlev), gu(nlev);
+  std::vector<std::vector<GemmTask>> gm(nlev), gr(nlev), gu(nlev), gw(nlev);
   // small-front buckets: rows ≤ 32 / ≤ 64 (k_small_front), rows ≤ 96 with
   // w ≤ 16 / 32 / 64 (k_small_front_rows), rows ≤ 96 with w > 64 (k_small_front)
   std::vector<std::vector<int32_t>> sm[kSmBuckets];
@@ -468,6 +490,7 @@ void DeviceFactor::build_factor_plan() {
   double* U = U_.p;
   std::vector<int64_t> gpan(3 * static_cast<size_t>(nlev), 0);  // panel tasks of all ranks
   std::vector<int64_t> ggm(nlev, 0), ggr(nlev, 0);                // GEMM tiles of all ranks
+  std::vector<int> dwait(nlev, std::max(defer_, 1));  // smallest deferral depth among a level's supernodes
   for (int k = 0; k < s.ns; ++k) {
     const int w = s.w(k), rows = s.rows(k), r = rows - w;
     if (rows <= kSmallRows) continue;
@@ -475,12 +498,13 @@ void DeviceFactor::build_factor_plan() {
     for (int c = 0; c < nch; ++c) {
       const int c0 = c * kNB, wk = std::min(kNB, w - c0), nbelow = rows - c0 - wk;
       const int lv = lvl0[k] + c;
+      dwait[lv] = std::min(dwait[lv], defer_of(w, rows));
       gpan[3 * lv + (wk <= 16 ? 0 : (wk <= 32 ? 1 : 2))] +=
           std::max(1, (nbelow + kRowsSR - 1) / kRowsSR);
-      trailing_jobs(w, c, [&](bool crit, int j0, int j1, int, int) {
+      trailing_jobs(w, rows, c, [&](bool crit, int j0, int j1, int, int) {
         for (int jb = j0; jb < j1; jb += kTile) (crit ? ggm : ggr)[lv] += (rows - jb + kTile - 1) / kTile;
       });
-      if (c == nch - 1 && !(inc_u_ && nch >= inc_u_))
+      if (c == nch - 1 && !use_wide(r, w - (inc_u_ && nch >= inc_u_ ? (c / inc_b_) * inc_b_ * kNB : 0)))
         for (int jb = 0; jb < r; jb += kTile) ggr[lv] += (r - jb + kTile - 1) / kTile;
     }
   }
@@ -502,7 +526,7 @@ void DeviceFactor::build_factor_plan() {
       const int c0 = c * kNB, wk = std::min(kNB, w - c0);
       if (c == 0 && s.ch_ptr[k + 1] == s.ch_ptr[k] && r > 0) {
         // no children: the extend-add tasks only zero the update block
-        for (int b = w; b < rows; ++b) ea[lv].push_back({k, b, 0, 0});
+        for (int b = w; b < rows; ++b) eau[lv].push_back({k, b, 0, 0});
         ea_b[lv] += 4.0 * r * (r + 1.0);
       }
       if (c == 0 && s.ch_ptr[k + 1] > s.ch_ptr[k]) {
@@ -519,7 +543,7 @@ void DeviceFactor::build_factor_plan() {
         // (replaces a memset of all update matrices per factorization)
         for (int b = 0; b < rows; ++b) {
           if (cnt[b + 1] || b >= w)
-            ea[lv].push_back({k, b, static_cast<int32_t>(base + cnt[b]), cnt[b + 1]});
+            (b < w ? ea : eau)[lv].push_back({k, b, static_cast<int32_t>(base + cnt[b]), cnt[b + 1]});
           cnt[b + 1] += cnt[b];
         }
         ea_b[lv] += 4.0 * r * (r + 1.0);
@@ -554,7 +578,7 @@ void DeviceFactor::build_factor_plan() {
       // right-looking update of the trailing panel columns [j0, j1) with the
       // finished columns [k0, k1) (trailing_jobs: next block on the chain,
       // deferred bulk updates of the blocks further right)
-      trailing_jobs(w, c, [&](bool crit, int j0, int j1, int k0, int k1) {
+      trailing_jobs(w, rows, c, [&](bool crit, int j0, int j1, int k0, int k1) {
         for (int jb = j0; jb < j1; jb += kTile)
           for (int ib = jb; ib < rows; ib += kTile) {
             GemmTask g{};
@@ -576,8 +600,11 @@ void DeviceFactor::build_factor_plan() {
       });
       // wide supernodes: U -= L21(c) L21(c)ᵀ right after this chunk (K = wk), off
       // the panel chain; same per-tile accumulation order as one K = w SYRK
+      // (batches of inc_b_ chunks: K = inc_b_·kNB per pass over U; the last batch
+      // is the supernode's closing SYRK below)
       const bool inc = inc_u_ && nch >= inc_u_;
-      if (inc && r > 0)
+      const int kb0 = inc ? (c / inc_b_) * inc_b_ * kNB : 0;  // first column of chunk c's batch
+      if (inc && r > 0 && (c + 1) % inc_b_ == 0 && c != nch - 1)
         for (int jb = 0; jb < r; jb += kTile)
           for (int ib = jb; ib < r; ib += kTile) {
             GemmTask g{};
@@ -585,11 +612,11 @@ void DeviceFactor::build_factor_plan() {
             g.ldc = r;
             g.m = std::min(kTile, r - ib);
             g.n = std::min(kTile, r - jb);
-            g.a[0] = Lk + w + ib + static_cast<int64_t>(c0) * rows;
+            g.a[0] = Lk + w + ib + static_cast<int64_t>(kb0) * rows;
             g.lda[0] = rows;
-            g.b[0] = Lk + w + jb + static_cast<int64_t>(c0) * rows;
+            g.b[0] = Lk + w + jb + static_cast<int64_t>(kb0) * rows;
             g.ldb[0] = rows;
-            g.k[0] = wk;
+            g.k[0] = c0 + wk - kb0;
             g.flags = 2;
             g.alpha = -1.0;
             g.beta = 1.0;
@@ -597,23 +624,24 @@ void DeviceFactor::build_factor_plan() {
             gu_f[lv] += tile_flops(g, ib == jb);
           }
       // last chunk: full-width SYRK into the update matrix, U -= L21 L21ᵀ
-      if (!inc && c == nch - 1 && r > 0)
-        for (int jb = 0; jb < r; jb += kTile)
-          for (int ib = jb; ib < r; ib += kTile) {
+      const int tile_u = use_wide(r, w - kb0) ? kWTile : kTile;  // large SYRKs: 128×128 TMA-staged tiles
+      if (c == nch - 1 && r > 0)
+        for (int jb = 0; jb < r; jb += tile_u)
+          for (int ib = jb; ib < r; ib += tile_u) {
             GemmTask g{};
             g.c = Uk + ib + static_cast<int64_t>(jb) * r;
             g.ldc = r;
-            g.m = std::min(kTile, r - ib);
-            g.n = std::min(kTile, r - jb);
-            g.a[0] = Lk + w + ib;
+            g.m = std::min(tile_u, r - ib);
+            g.n = std::min(tile_u, r - jb);
+            g.a[0] = Lk + w + ib + static_cast<int64_t>(kb0) * rows;
             g.lda[0] = rows;
-            g.b[0] = Lk + w + jb;
+            g.b[0] = Lk + w + jb + static_cast<int64_t>(kb0) * rows;
             g.ldb[0] = rows;
-            g.k[0] = w;
+            g.k[0] = w - kb0;
             g.flags = 2;
             g.alpha = -1.0;
             g.beta = 1.0;
-            gr[lv].push_back(g);
+            (tile_u == kWTile ? gw : gr)[lv].push_back(g);
             gr_f[lv] += tile_flops(g, ib == jb);
           }
     }
@@ -663,9 +691,16 @@ void DeviceFactor::build_factor_plan() {
       flev_[l].gun = static_cast<int64_t>(gu[l].size());
       flev_[l].gu_flops = gu_f[l];
       gmf.insert(gmf.end(), gu[l].begin(), gu[l].end());
+      flev_[l].gw0 = static_cast<int64_t>(gmf.size());
+      flev_[l].gwn = static_cast<int64_t>(gw[l].size());
+      gmf.insert(gmf.end(), gw[l].begin(), gw[l].end());
     }
     pof.insert(pof.end(), po[l].begin(), po[l].end());
     eaf.insert(eaf.end(), ea[l].begin(), ea[l].end());
+    flev_[l].dwait = dwait[l];
+    flev_[l].eau0 = static_cast<int64_t>(eaf.size());
+    flev_[l].eaun = static_cast<int64_t>(eau[l].size());
+    eaf.insert(eaf.end(), eau[l].begin(), eau[l].end());
     // panel tasks grouped by width bucket (16 / 32 / 64) so each sub-launch
     // reserves only the shared memory its chunks need
     for (int bk = 0; bk < 3; ++bk) {
@@ -693,7 +728,7 @@ void DeviceFactor::build_factor_plan() {
       smf.insert(smf.end(), sm[bk][l].begin(), sm[bk][l].end());
     }
     flev_[l].sm_flops = sm_f[l];
-    for (int bk = 0; bk < 3; ++bk) flev_[l].prow[bk] = gpan[3 * l + bk] <= kRowsMaxCtas;
+    for (int bk = 0; bk < 3; ++bk) flev_[l].prow[bk] = gpan[3 * l + bk] <= rows_max_ctas_;
   }
   ea_.upload(eaf, stream_);
   eap_.upload(ea_pairs, stream_);
@@ -1032,11 +1067,12 @@ void DeviceFactor::enqueue_levels(cudaStream_t sa, cudaStream_t sb, bool la, boo
     // SYRKs, concurrently with the next level's panel. Ordering:
     //   rest(l)               after panel(l)           (reads the chunk's L)
     //   assembly(l)           after rest(l-1)          (children's U SYRKs)
-    //   next(l)               after rest(l-D)          (same tiles, k order; D = defer_)
+    //   next(l)               after rest(l-D)          (same tiles, k order; D = the level's
+    //                                                   smallest deferral depth, defer_of)
     // Profiling runs keep one stream so every launch is attributed to its class.
     int64_t nsmall = 0;
     for (int bk = 0; bk < kSmBuckets; ++bk) nsmall += lv.smn[bk];
-    const bool assembles = lv.ean > 0 || nsmall > 0;
+    const bool assembles = lv.ean > 0 || lv.eaun > 0 || nsmall > 0;
     if (la && li > 0 && assembles) {
       cuda_check(cudaStreamWaitEvent(sa, ev_rest_[li - 1], 0), "wait");
       cuda_check(cudaStreamWaitEvent(sa, ev_uupd_[li - 1], 0), "wait");
@@ -1070,15 +1106,29 @@ void DeviceFactor::enqueue_levels(cudaStream_t sa, cudaStream_t sb, bool la, boo
       if (tbuf_.p) k_mark<<<1, 1, 0, st>>>(tbuf_.p, lvl * kTraceSlots + slot);
     };
     mark(sa, 8);
-    if (lv.ean && !(whatif & 8)) {
-      int blocks = static_cast<int>((lv.ean * 32 + 255) / 256);
-      pf.run(sa, pf.tag("factor.extend_add", lvl), 0.0, lv.ea_bytes, [&] {
-        k_extend_add<<<blocks, 256, 0, sa>>>(ea_.p + lv.ea0, static_cast<int>(lv.ean), eap_.p, sd,
-                                                 L_.p, U_.p);
+    // extend-add: the panel columns on the chain; the update-block columns (needed
+    // only by the level's U SYRKs) on the bulk stream, beside the panel step
+    auto launch_ea = [&](cudaStream_t st, int64_t t0, int64_t tn, double bytes) {
+      const int blocks = static_cast<int>((tn * 32 + 255) / 256);
+      pf.run(st, pf.tag("factor.extend_add", lvl), 0.0, bytes, [&] {
+        if (tn <= ea_cta_max_)  // few long columns (top of the tree): one CTA per column
+          k_extend_add_cta<<<static_cast<unsigned>(tn), kEaCtaThreads, 0, st>>>(
+              ea_.p + t0, eap_.p, sd, L_.p, U_.p);
+        else
+          k_extend_add<<<blocks, 256, 0, st>>>(ea_.p + t0, static_cast<int>(tn), eap_.p, sd,
+                                               L_.p, U_.p);
       });
       ++launches_numeric_;
-    }
+    };
+    const double ea_share = lv.ean + lv.eaun > 0 ? static_cast<double>(lv.ean) / (lv.ean + lv.eaun) : 0.0;
+    if (lv.ean && !(whatif & 8)) launch_ea(sa, lv.ea0, lv.ean, lv.ea_bytes * ea_share);
     mark(sa, 0);
+    if (lv.eaun && !(whatif & 8)) {
+      const bool split = la && li > 0 && ea_split_;
+      if (split) cuda_check(cudaStreamWaitEvent(sb, ev_uupd_[li - 1], 0), "wait");
+      launch_ea(split ? sb : sa, lv.eau0, lv.eaun, lv.ea_bytes * (1.0 - ea_share));
+      if (split) cuda_check(cudaEventRecord(ev_eau_[li], sb), "record");
+    }
     // one-wave levels (the chain at the top of the tree) keep the fused row
     // sweep: one launch, no staging round trip; multi-wave levels split
     const bool two_phase = panel2_ && !(lv.prow[0] && lv.prow[1] && lv.prow[2]);
@@ -1144,8 +1194,8 @@ void DeviceFactor::enqueue_levels(cudaStream_t sa, cudaStream_t sb, bool la, boo
     mark(sa, 1);
     if (la) cuda_check(cudaEventRecord(ev_panel_[li], sa), "record");
     // next(l) writes block c+1, last written off the chain by the flush D levels back
-    if (la && li >= static_cast<size_t>(defer_))
-      cuda_check(cudaStreamWaitEvent(sa, ev_rest_[li - defer_], 0), "wait");
+    if (la && li >= static_cast<size_t>(lv.dwait))
+      cuda_check(cudaStreamWaitEvent(sa, ev_rest_[li - lv.dwait], 0), "wait");
     mark(sa, 2);
     if (lv.gmn && !(whatif & 4)) {
       pf.run(sa, pf.tag("factor.gemm_dmma", lvl), lv.gm_flops, 0.0, [&] {
@@ -1158,21 +1208,26 @@ void DeviceFactor::enqueue_levels(cudaStream_t sa, cudaStream_t sb, bool la, boo
     }
     mark(sa, 3);
     if (la) cuda_check(cudaStreamWaitEvent(sb, ev_panel_[li], 0), "wait");
+    // closing SYRKs of incrementally updated supernodes: after their earlier batches
+    if (la && li > 0 && inc_u_) cuda_check(cudaStreamWaitEvent(sb, ev_uupd_[li - 1], 0), "wait");
     mark(sb, 4);
-    if (lv.grn && !(whatif & 1)) {
+    if ((lv.grn || lv.gwn) && !(whatif & 1)) {
       pf.run(sb, pf.tag("factor.gemm_dmma", lvl), lv.gr_flops, 0.0, [&] {
-        launch_gemm(gemm_.p + lv.gr0, lv.grn, sb);
+        if (lv.gwn) launch_gemm_wide(gemm_.p + lv.gw0, lv.gwn, sb);
+        if (lv.grn) launch_gemm(gemm_.p + lv.gr0, lv.grn, sb);
         if (lv.rrn)
           k_reduce_parts<<<static_cast<unsigned>(lv.rrn), 256, 0, sb>>>(red_.p + lv.rr0,
                                                                         rparts_.p);
       });
-      launches_numeric_ += 1 + (lv.rrn > 0);
+      launches_numeric_ += (lv.grn > 0) + (lv.gwn > 0) + (lv.rrn > 0);
     }
     mark(sb, 5);
     if (la) cuda_check(cudaEventRecord(ev_rest_[li], sb), "record");
     // incremental update-matrix accumulation (wide supernodes), third stream
     cudaStream_t su = la ? uu_ : sa;
     if (la) cuda_check(cudaStreamWaitEvent(su, ev_panel_[li], 0), "wait");
+    if (la && li > 0 && ea_split_ && lv.eaun && lv.gun)  // U zeroed / assembled on the bulk stream
+      cuda_check(cudaStreamWaitEvent(su, ev_eau_[li], 0), "wait");
     mark(su, 6);
     if (lv.gun) {
       pf.run(su, pf.tag("factor.gemm_dmma", lvl), lv.gu_flops, 0.0,
@@ -1218,7 +1273,15 @@ void DeviceFactor::dump_trace() {
     for (size_t l = 0; l < flev_.size(); ++l) {
       std::fprintf(f, "%zu", l);
       for (int k = 0; k < kTraceSlots; ++k) std::fprintf(f, " %llu", t[l * kTraceSlots + k]);
-      std::fprintf(f, "\n");
+      const FLevel& lv = flev_[l];
+      long long nsm = 0;
+      for (int bk = 0; bk < kSmBuckets; ++bk) nsm += lv.smn[bk];
+      // task counts of the level: small fronts, extend-add columns, chunks, panel
+      // slabs (row sweep / TRSM), next-block tiles, bulk tiles, one-wave flag
+      std::fprintf(f, " | %lld %lld %lld %lld %lld %lld %lld %d\n", nsm, (long long)lv.ean,
+                   (long long)lv.pon, (long long)lv.pann,
+                   (long long)(lv.ptn[0] + lv.ptn[1] + lv.ptn[2]), (long long)lv.gmn,
+                   (long long)lv.grn, int(lv.prow[0] && lv.prow[1] && lv.prow[2]));
     }
     std::fprintf(f, "end\n");
     std::fclose(f);

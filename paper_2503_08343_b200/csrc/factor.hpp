@@ -35,9 +35,10 @@ struct DevBuf {
     if (count == n && p) return;
     reset();
     if (count == 0) return;
-    // + slack: 16-byte operand copies (load_operand) read whole 64-row tile columns,
-    // past the last row of a partial tile at the end of a buffer
-    cuda_check(cudaMalloc(&p, count * sizeof(T) + 1024), "cudaMalloc");
+    // + slack: 16-byte operand copies (load_operand) and the wide GEMM's bulk copies
+    // read whole 64- / 128-row tile columns, past the last row of a partial tile at
+    // the end of a buffer
+    cuda_check(cudaMalloc(&p, count * sizeof(T) + 2048), "cudaMalloc");
     n = count;
   }
   void upload(const std::vector<T>& v, cudaStream_t s) {
@@ -218,6 +219,9 @@ class DeviceFactor {
     bool prow[3];  // panel kernel per bucket: row sweep (one wave) or blocked; decided on
                    // the level's task count over ALL supernodes, so a partitioned factor
                    // runs the same kernels (same rounding) as the single-GPU one
+    int64_t eau0, eaun;  // extend-add tasks of update-block columns (bulk stream)
+    int dwait;           // the chain's next-block update waits for the bulk stream's level l - dwait
+    int64_t gw0, gwn;    // 128×128 tiles (k_gemm_wide) of the level's large U SYRKs / flushes (bulk stream)
   };
   DevBuf<int32_t> small_;
   std::vector<FLevel> flev_;
@@ -239,21 +243,34 @@ class DeviceFactor {
   // lookahead: the rest-of-update GEMMs run on aux_ (events order the levels)
   cudaStream_t main_ = nullptr, aux_ = nullptr, uu_ = nullptr;
   cudaEvent_t ev_fork_ = nullptr;
-  std::vector<cudaEvent_t> ev_panel_, ev_rest_, ev_uupd_;
+  std::vector<cudaEvent_t> ev_panel_, ev_rest_, ev_uupd_, ev_eau_;
   // supernodes of at least inc_u_ chunks accumulate their update matrix chunk by
   // chunk (U -= L21(c) L21(c)ᵀ right after chunk c's panel, on uu_) instead of
   // one K = w SYRK after the last chunk on the critical path; 0 disables
   int inc_u_ = 0;
+  // k_gemm_wide for bulk GEMMs with at least wide_min_r_ rows and K >= wide_min_k_ (0 disables)
+  int wide_min_r_ = 2048, wide_min_k_ = 512;
+  bool use_wide(int r, int K) const { return wide_min_k_ > 0 && r >= wide_min_r_ && K >= wide_min_k_; }
+  bool ea_split_ = true;           // update-block extend-add on the bulk stream (GMRF_EA_SPLIT=0: A/B)
+  int inc_b_ = 2;                  // chunks per incremental batch (K = inc_b_·kNB per pass over U)
+  int64_t ea_cta_max_ = 4096;      // extend-add: one CTA per column on levels with at most this many columns
+  unsigned rows_max_ctas_ = 148;   // row-sweep panel on levels with at most this many slabs (one wave)
   // GMRF_TRACE=<file>: per-level timeline markers (k_mark), appended per factorization
   static constexpr int kTraceSlots = 10;
   std::string trace_file_;
   DevBuf<unsigned long long> tbuf_;
   void dump_trace();
   bool lookahead_ = true;
-  int defer_ = 1;
+  int defer_ = 4;
   bool gemm_cap_ = true;  // cap bulk GEMM residency on one-wave levels (launch_gemm)  // trailing-update deferral depth (chunks per flush), trailing_jobs
   template <class F>
-  void trailing_jobs(int w, int c, F&& emit) const;
+  void trailing_jobs(int w, int rows, int c, F&& emit) const;
+  // deferral depth of a supernode: fronts whose panel exceeds defer_min_ entries
+  // (their K = kNB trailing passes are HBM-bound) flush every defer_ chunks
+  int64_t defer_min_ = 8ll << 20;
+  int defer_of(int w, int rows) const {
+    return static_cast<int64_t>(w) * rows >= defer_min_ ? defer_ : 1;
+  }
   bool use_graph_ = true;             // GMRF_NO_GRAPH=1 disables (A/B)
   bool panel2_ = true;                // GMRF_PANEL1=1: fused one-phase panel kernels (A/B)
   DevBuf<PanelTask> pd_, pt_;         // two-phase panel tasks

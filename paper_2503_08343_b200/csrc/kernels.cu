@@ -247,6 +247,52 @@ __global__ void k_extend_add(const EaTask* __restrict__ tasks, int ntasks,
   }
 }
 
+// Same assembly with one CTA per (front, front column): the levels at the top of
+// the tree have few but long columns (a few thousand rows, two large children),
+// where one warp per column is a chain of dependent gather rounds. The threads
+// of the CTA split each child's rows; children stay in ascending order (a
+// barrier between them), so every entry sums in the same order as k_extend_add.
+constexpr int kEaCtaThreads = 256;
+__global__ void __launch_bounds__(kEaCtaThreads) k_extend_add_cta(
+    const EaTask* __restrict__ tasks, const int2* __restrict__ pairs, SymDev sd,
+    double* __restrict__ L, double* __restrict__ U) {
+  const int tid = threadIdx.x;
+  const EaTask t = tasks[blockIdx.x];
+  const int s = t.sn, b = t.col;
+  const int w = sd.sn_first[s + 1] - sd.sn_first[s];
+  const int rows = static_cast<int>(sd.sn_rptr[s + 1] - sd.sn_rptr[s]);
+  const int r = rows - w;
+  double* Ls = L + sd.lptr[s];
+  double* Us = U + sd.uptr[s];
+  double* dst = b < w ? Ls + static_cast<int64_t>(b) * rows : Us + static_cast<int64_t>(b - w) * r - w;
+  if (b >= w) {
+    for (int a = b + tid; a < rows; a += kEaCtaThreads) dst[a] = 0.0;
+    __syncthreads();
+  }
+  for (int p = t.p0; p < t.p0 + t.np; ++p) {
+    const int2 cp = pairs[p];
+    const int c = cp.x, ib = cp.y;
+    const int wc = sd.sn_first[c + 1] - sd.sn_first[c];
+    const int rc = static_cast<int>(sd.sn_rptr[c + 1] - sd.sn_rptr[c]) - wc;
+    const int32_t* rel = sd.relmap + sd.sn_rptr[c] + wc;
+    const double* Uc = U + sd.uptr[c] + static_cast<int64_t>(ib) * rc;
+    int ia = ib + tid;
+    for (; ia + 3 * kEaCtaThreads < rc; ia += 4 * kEaCtaThreads) {
+      int t0 = rel[ia], t1 = rel[ia + kEaCtaThreads], t2 = rel[ia + 2 * kEaCtaThreads],
+          t3 = rel[ia + 3 * kEaCtaThreads];
+      double u0 = Uc[ia], u1 = Uc[ia + kEaCtaThreads], u2 = Uc[ia + 2 * kEaCtaThreads],
+             u3 = Uc[ia + 3 * kEaCtaThreads];
+      double d0 = dst[t0], d1 = dst[t1], d2 = dst[t2], d3 = dst[t3];
+      dst[t0] = d0 + u0;
+      dst[t1] = d1 + u1;
+      dst[t2] = d2 + u2;
+      dst[t3] = d3 + u3;
+    }
+    for (; ia < rc; ia += kEaCtaThreads) dst[rel[ia]] += Uc[ia];
+    __syncthreads();
+  }
+}
+
 // Q values → L panels through the precomputed offset map.
 __global__ void k_scatter_q(const double* __restrict__ q, const int64_t* __restrict__ qmap,
                             int64_t nnz, double* __restrict__ L) {

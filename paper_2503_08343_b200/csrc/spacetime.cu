@@ -457,6 +457,8 @@ void SpaceTimePosterior::build_host() {
     std::vector<char> first(static_cast<size_t>(n_), 0);
     for (int s = 0; s < nt_; ++s)
       for (int d = 0; d < ns_; ++d) first[static_cast<size_t>(s) * ns_ + d] = sl[d];
+    if (std::getenv("GMRF_VERBOSE"))
+      std::fprintf(stderr, "[gmrf] spacetime grid %d x %d x %d, coupling radii %d %d %d\n", nx, ny, nt_, rx, ry, rt);
     std::vector<i32> perm = grid_nd_order3(nx, ny, nt_, rx, ry, rt, first);
     SymbolicOptions opt;
     opt.postorder_given = true;

@@ -75,7 +75,12 @@ def _rel(a, b):
 
 
 def _record_floor(name, b):
-    """Compares a perturbed reference run with the committed fixture."""
+    """Compares a perturbed reference run with the committed fixture (waits for a
+    fixture job started alongside to finish)."""
+    for _ in range(6 * 240):
+        if os.path.exists(os.path.join(HERE, name)):
+            break
+        time.sleep(10)
     z = np.load(os.path.join(HERE, name))
     f = {"seed": FLOOR_SEED} if MODE["tag"] == "/ulp" else {"ordering": "metis_nd"}
     for k, key in (("mean", "mode"), ("mean", "mean_post"), ("var", "var_post")):
@@ -107,8 +112,11 @@ def burgers(n_el, n_t, gn_iters, name, floor=False):
     if floor:
         return _record_floor(name, b)
     out = {"params": np.array(p, np.float64)}
-    for k in ["mean_cond", "mode", "mean_post", "var_post", "gn_objective", "gn_decrement",
-              "gn_step", "gn_backtracks"]:
+    keys = ["mean_cond", "mode", "mean_post", "var_post", "gn_objective", "gn_decrement",
+            "gn_step", "gn_backtracks"]
+    if n_el * n_t > 500000:  # full size: the Laplace mean is the mode; keep the fixture small
+        keys = [k for k in keys if k not in ("mean_cond", "mean_post")]
+    for k in keys:
         out[k] = b.vec(k)
     out["gn_converged"] = np.array(b.scalar("gn_converged"))
     _save(name, out, b, time.time() - t0)
