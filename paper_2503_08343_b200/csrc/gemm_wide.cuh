@@ -33,7 +33,8 @@ constexpr int kWKC = 16;                    // K per stage
 constexpr int kWStages = 4;                 // ring depth
 constexpr int kWPitch = kWTile + 4;         // smem column pitch (doubles): ≡ 4 mod 16 → the 4 k-rows of a
                                             // fragment load fall in disjoint bank groups
-constexpr int kWConsumers = 8;              // consumer warps
+constexpr int kWConsumers = 8;              // consumer warps (+ 1 producer warp: 3 warps on one SM
+                                            // sub-partition, so ptxas caps the kernel at 168 registers)
 constexpr int kWThreads = 32 * (kWConsumers + 1);
 constexpr int kWColBytes = (kWTile + 2) * 8;  // bytes per bulk copy (one element of alignment slack)
 
@@ -216,5 +217,6 @@ __global__ void __launch_bounds__(kWThreads, 1) k_gemm_wide(const GemmTask* __re
       }
   }
 }
+
 
 }  // namespace gmrf

@@ -41,7 +41,9 @@ __device__ __forceinline__ void cp_async_wait() {
 // 32x32 sub-tile = 4x4 DMMA m8n8 fragments. K staged in chunks of 16.
 // ---------------------------------------------------------------------------
 constexpr int kKC = 16;
-constexpr int kPad = 72;  // smem row pitch (doubles): conflict-free fragment loads
+constexpr int kPad = 68;  // smem row pitch (doubles), ≡ 4 mod 16: the four k-rows of a fragment load
+                          // (LDS.64, 16 lanes per wavefront) fall in disjoint bank groups (72 gave 2-way
+                          // conflicts on every load: ncu l1tex__data_bank_conflicts, r02_ncu_summary.txt)
 
 // 16-byte copy, zero-filled when !pred
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {

@@ -13,6 +13,7 @@
 
 #include "kernels.cu"
 #include "gemm_wide.cuh"
+#include "../tools/gemm_wide_tn.cuh"
 
 using namespace gmrf;
 
@@ -127,6 +128,47 @@ int main(int argc, char** argv) {
            f64 / (m128 * 1e-3) / 1e12, h);
     fflush(stdout);
     cudaFree(A); cudaFree(C0); cudaFree(C1); cudaFree(d64); cudaFree(d128); cudaFree(cnt);
+  }
+  // K-contiguous operands (selected inversion: Y_R = Sigma_RR * L_RJ): C (r x w) = S (r x r, symmetric,
+  // read transposed) * L (r x w block of a panel with ld rows), 64x64 k_gemm_tiles vs k_gemm_wide_tn
+  CK(cudaFuncSetAttribute(k_gemm_wide_tn, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm_wide_tn_smem_bytes()));
+  struct TN { const char* name; int r, w, rows; };
+  for (const TN& s : {TN{"tn_r8450_w3900", 8450, 3900, 12350}, TN{"tn_r4225_w4160", 4225, 4160, 8385},
+                      TN{"tn_r1996_w1000", 1996, 1000, 2996}}) {
+    const int64_t ssz = (int64_t)s.r * s.r + 4096, lsz = (int64_t)s.rows * s.w + 4096, csz = (int64_t)s.r * s.w + 4096;
+    double *S, *L, *C0, *C1;
+    CK(cudaMalloc(&S, ssz * 8)); CK(cudaMalloc(&L, lsz * 8)); CK(cudaMalloc(&C0, csz * 8)); CK(cudaMalloc(&C1, csz * 8));
+    k_fill<<<1024, 256>>>(S, ssz, 3);
+    k_fill<<<1024, 256>>>(L, lsz, 4);
+    CK(cudaMemset(C0, 0, csz * 8)); CK(cudaMemset(C1, 0, csz * 8));
+    auto mk = [&](int T, double* C, std::vector<GemmTask>& out, double& fl) {
+      for (int jb = 0; jb < s.w; jb += T)
+        for (int ib = 0; ib < s.r; ib += T) {
+          GemmTask g{};
+          g.c = C + ib + (int64_t)jb * s.r; g.ldc = s.r;
+          g.m = std::min(T, s.r - ib); g.n = std::min(T, s.w - jb);
+          g.a[0] = S + (int64_t)ib * s.r; g.lda[0] = s.r;
+          g.b[0] = L + (s.rows - s.r) + (int64_t)jb * s.rows; g.ldb[0] = s.rows;
+          g.k[0] = s.r; g.flags = 1; g.alpha = 1.0; g.beta = 0.0;
+          out.push_back(g); fl += 2.0 * g.m * g.n * s.r;
+        }
+    };
+    std::vector<GemmTask> t64, t128; double f64 = 0, f128 = 0;
+    mk(64, C0, t64, f64); mk(128, C1, t128, f128);
+    GemmTask *d64, *d128;
+    CK(cudaMalloc(&d64, t64.size() * sizeof(GemmTask))); CK(cudaMalloc(&d128, t128.size() * sizeof(GemmTask)));
+    CK(cudaMemcpy(d64, t64.data(), t64.size() * sizeof(GemmTask), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d128, t128.data(), t128.size() * sizeof(GemmTask), cudaMemcpyHostToDevice));
+    const float m64 = time_launch(k_gemm_tiles, d64, t64.size(), 128, 0, reps);
+    const float m128 = time_launch(k_gemm_wide_tn, d128, t128.size(), kWThreads, gemm_wide_tn_smem_bytes(), reps);
+    unsigned long long* cnt; CK(cudaMalloc(&cnt, 8)); CK(cudaMemset(cnt, 0, 8));
+    k_diff<<<1024, 256>>>(C0, C1, (int64_t)s.r * s.w, cnt);
+    unsigned long long h = 0; CK(cudaMemcpy(&h, cnt, 8, cudaMemcpyDeviceToHost));
+    printf("%-16s base64 %6zu tiles %9.1f us %6.2f TF/s | wide_tn %6zu tiles %9.1f us %6.2f TF/s | mismatches %llu\n",
+           s.name, t64.size(), m64 * 1e3, f64 / (m64 * 1e-3) / 1e12, t128.size(), m128 * 1e3,
+           f64 / (m128 * 1e-3) / 1e12, h);
+    fflush(stdout);
+    cudaFree(S); cudaFree(L); cudaFree(C0); cudaFree(C1); cudaFree(d64); cudaFree(d128); cudaFree(cnt);
   }
   return 0;
 }
