@@ -139,6 +139,7 @@ DeviceFactor::DeviceFactor(std::shared_ptr<const Symbolic> sym, cudaStream_t str
   if (const char* e = std::getenv("GMRF_INC_U")) inc_u_ = std::max(0, atoi(e));
   if (const char* e = std::getenv("GMRF_EA_SPLIT")) ea_split_ = e[0] != '0';
   if (const char* e = std::getenv("GMRF_WIDE_K")) wide_min_k_ = atoi(e);
+  if (const char* e = std::getenv("GMRF_GEMM_NEXT")) gemm_next_ = e[0] != '0';
   if (const char* e = std::getenv("GMRF_WIDE_R")) wide_min_r_ = atoi(e);
   if (const char* e = std::getenv("GMRF_INC_B")) inc_b_ = std::max(1, atoi(e));
   if (const char* e = std::getenv("GMRF_EA_CTA")) ea_cta_max_ = atoll(e);
@@ -491,6 +492,7 @@ void DeviceFactor::build_factor_plan() {
   std::vector<int64_t> gpan(3 * static_cast<size_t>(nlev), 0);  // panel tasks of all ranks
   std::vector<int64_t> ggm(nlev, 0), ggr(nlev, 0);                // GEMM tiles of all ranks
   std::vector<int> dwait(nlev, std::max(defer_, 1));  // smallest deferral depth among a level's supernodes
+  std::vector<int> kcrit(nlev, 0);                    // longest K among a level's next-block updates
   for (int k = 0; k < s.ns; ++k) {
     const int w = s.w(k), rows = s.rows(k), r = rows - w;
     if (rows <= kSmallRows) continue;
@@ -501,8 +503,9 @@ void DeviceFactor::build_factor_plan() {
       dwait[lv] = std::min(dwait[lv], defer_of(w, rows));
       gpan[3 * lv + (wk <= 16 ? 0 : (wk <= 32 ? 1 : 2))] +=
           std::max(1, (nbelow + kRowsSR - 1) / kRowsSR);
-      trailing_jobs(w, rows, c, [&](bool crit, int j0, int j1, int, int) {
+      trailing_jobs(w, rows, c, [&](bool crit, int j0, int j1, int k0, int k1) {
         for (int jb = j0; jb < j1; jb += kTile) (crit ? ggm : ggr)[lv] += (rows - jb + kTile - 1) / kTile;
+        if (crit) kcrit[lv] = std::max(kcrit[lv], k1 - k0);
       });
       if (c == nch - 1 && !use_wide(r, w - (inc_u_ && nch >= inc_u_ ? (c / inc_b_) * inc_b_ * kNB : 0)))
         for (int jb = 0; jb < r; jb += kTile) ggr[lv] += (r - jb + kTile - 1) / kTile;
@@ -578,14 +581,20 @@ void DeviceFactor::build_factor_plan() {
       // right-looking update of the trailing panel columns [j0, j1) with the
       // finished columns [k0, k1) (trailing_jobs: next block on the chain,
       // deferred bulk updates of the blocks further right)
+      // one-wave levels (the chain at the top of the tree): the next-block update
+      // runs on 32×32 tiles with one-shot operand loads (k_gemm_next)
+      const bool next32 = gemm_next_ && kcrit[lv] <= kNKMax &&
+                          gpan[3 * lv] <= rows_max_ctas_ && gpan[3 * lv + 1] <= rows_max_ctas_ &&
+                          gpan[3 * lv + 2] <= rows_max_ctas_;
       trailing_jobs(w, rows, c, [&](bool crit, int j0, int j1, int k0, int k1) {
-        for (int jb = j0; jb < j1; jb += kTile)
-          for (int ib = jb; ib < rows; ib += kTile) {
+        const int T = crit && next32 ? kNTile : kTile;
+        for (int jb = j0; jb < j1; jb += T)
+          for (int ib = jb; ib < rows; ib += T) {
             GemmTask g{};
             g.c = Lk + ib + static_cast<int64_t>(jb) * rows;
             g.ldc = rows;
-            g.m = std::min(kTile, rows - ib);
-            g.n = std::min(kTile, w - jb);
+            g.m = std::min(T, rows - ib);
+            g.n = std::min(T, std::min(w, j1) - jb);
             g.a[0] = Lk + ib + static_cast<int64_t>(k0) * rows;
             g.lda[0] = rows;
             g.b[0] = Lk + jb + static_cast<int64_t>(k0) * rows;
@@ -698,6 +707,8 @@ void DeviceFactor::build_factor_plan() {
     pof.insert(pof.end(), po[l].begin(), po[l].end());
     eaf.insert(eaf.end(), ea[l].begin(), ea[l].end());
     flev_[l].dwait = dwait[l];
+    flev_[l].gm32 = gemm_next_ && kcrit[l] <= kNKMax && gpan[3 * l] <= rows_max_ctas_ &&
+                    gpan[3 * l + 1] <= rows_max_ctas_ && gpan[3 * l + 2] <= rows_max_ctas_;
     flev_[l].eau0 = static_cast<int64_t>(eaf.size());
     flev_[l].eaun = static_cast<int64_t>(eau[l].size());
     eaf.insert(eaf.end(), eau[l].begin(), eau[l].end());
@@ -1199,7 +1210,10 @@ void DeviceFactor::enqueue_levels(cudaStream_t sa, cudaStream_t sb, bool la, boo
     mark(sa, 2);
     if (lv.gmn && !(whatif & 4)) {
       pf.run(sa, pf.tag("factor.gemm_dmma", lvl), lv.gm_flops, 0.0, [&] {
-        launch_gemm(gemm_.p + lv.gm0, lv.gmn, sa);
+        if (lv.gm32)
+          k_gemm_next<<<static_cast<unsigned>(lv.gmn), 128, 0, sa>>>(gemm_.p + lv.gm0);
+        else
+          launch_gemm(gemm_.p + lv.gm0, lv.gmn, sa);
         if (lv.rdn)
           k_reduce_parts<<<static_cast<unsigned>(lv.rdn), 256, 0, sa>>>(red_.p + lv.rd0,
                                                                              parts_.p);

@@ -221,6 +221,7 @@ class DeviceFactor {
                    // runs the same kernels (same rounding) as the single-GPU one
     int64_t eau0, eaun;  // extend-add tasks of update-block columns (bulk stream)
     int dwait;           // the chain's next-block update waits for the bulk stream's level l - dwait
+    bool gm32;           // the next-block update runs on 32×32 tiles (k_gemm_next)
     int64_t gw0, gwn;    // 128×128 tiles (k_gemm_wide) of the level's large U SYRKs / flushes (bulk stream)
   };
   DevBuf<int32_t> small_;
@@ -251,6 +252,7 @@ class DeviceFactor {
   // k_gemm_wide for bulk GEMMs with at least wide_min_r_ rows and K >= wide_min_k_ (0 disables)
   int wide_min_r_ = 2048, wide_min_k_ = 512;
   bool use_wide(int r, int K) const { return wide_min_k_ > 0 && r >= wide_min_r_ && K >= wide_min_k_; }
+  bool gemm_next_ = true;          // k_gemm_next for the chain GEMMs of one-wave levels (GMRF_GEMM_NEXT=0: A/B)
   bool ea_split_ = true;           // update-block extend-add on the bulk stream (GMRF_EA_SPLIT=0: A/B)
   int inc_b_ = 2;                  // chunks per incremental batch (K = inc_b_·kNB per pass over U)
   int64_t ea_cta_max_ = 4096;      // extend-add: one CTA per column on levels with at most this many columns

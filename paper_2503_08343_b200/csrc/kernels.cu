@@ -189,6 +189,93 @@ __global__ void __launch_bounds__(128, 4) k_gemm_tiles(const GemmTask* __restric
 }
 
 // ---------------------------------------------------------------------------
+// Chain GEMM of the one-wave levels at the top of the tree: the update of a
+// chunk's NEXT column block (K ≤ 64, a few dozen 64×64 tiles) sits on the
+// factorization's critical path between two panel steps, where a 64×64 tile per
+// CTA is four dependent K-stage round trips plus 256 DMMAs per warp (~8 µs for
+// 0.5 MFLOP). Here a CTA owns a 32×32 tile (four times the CTAs, still under
+// one wave), issues ALL its operand copies at once (K ≤ 64: one memory round
+// trip) and each warp runs 2×2 fragments. Same K order per output entry as
+// k_gemm_tiles (4 at a time, ascending): bit-identical. One segment, A not
+// transposed, B transposed (the trailing-update form).
+// ---------------------------------------------------------------------------
+constexpr int kNTile = 32;            // output tile
+constexpr int kNKMax = 64;            // K handled in one shot
+constexpr int kNPad = kNTile + 4;     // ≡ 4 mod 16 doubles: conflict-free fragment loads
+__global__ void __launch_bounds__(128) k_gemm_next(const GemmTask* __restrict__ tasks) {
+  __shared__ __align__(16) double As[kNKMax][kNPad];
+  __shared__ __align__(16) double Bs[kNKMax][kNPad];
+  const GemmTask& t = tasks[blockIdx.x];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp & 1, wn = warp >> 1;
+  const int m = t.m, n = t.n, K = t.k[0];
+  const double* A = t.a[0];
+  const double* B = t.b[0];
+  const int lda = t.lda[0], ldb = t.ldb[0];
+  {
+    // column kk of each operand in 16-byte chunks from its aligned start (phase
+    // shift as in load_operand); columns past K are zero filled
+    constexpr int CH = kNTile / 2 + 1;
+    for (int idx = tid; idx < kNKMax * CH; idx += 128) {
+      const int kk = idx / CH, ch = idx - kk * CH;
+      const bool ok = kk < K;
+      const double* ca = A + static_cast<int64_t>(kk) * lda;
+      const double* cb = B + static_cast<int64_t>(kk) * ldb;
+      cp_async16(&As[kk][2 * ch], ok ? ca - col_phase(ca) + 2 * ch : A - col_phase(A), ok);
+      cp_async16(&Bs[kk][2 * ch], ok ? cb - col_phase(cb) + 2 * ch : B - col_phase(B), ok);
+    }
+    cp_async_commit();
+  }
+  const double alpha = t.alpha, beta = t.beta;
+  double* C = t.c;
+  const int64_t ldc = t.ldc;
+  double acc[2][2][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int row = wm * 16 + i * 8 + (lane >> 2);
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int col = wn * 16 + j * 8 + (lane & 3) * 2 + e;
+        acc[i][j][e] = (beta != 0.0 && row < m && col < n) ? beta * C[row + col * ldc] : 0.0;
+      }
+  }
+  const int pa0 = col_phase(A), la = lda & 1;
+  const int pb0 = col_phase(B), lb = ldb & 1;
+  cp_async_wait<0>();
+  __syncthreads();
+  // as many 4-wide K steps as k_gemm_tiles runs (whole 16-column stages; the
+  // columns past K are zero), so even signed zeros come out the same
+  const int nks = ((K + kKC - 1) / kKC) * (kKC / 4);
+  for (int ks = 0; ks < nks; ++ks) {
+    const int kr = 4 * ks + (lane & 3);
+    const int sa = pa0 ^ (kr & la), sb = pb0 ^ (kr & lb);
+    double af[2], bf[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) af[i] = alpha * As[kr][wm * 16 + i * 8 + (lane >> 2) + sa];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) bf[j] = Bs[kr][wn * 16 + j * 8 + (lane >> 2) + sb];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int row = wm * 16 + i * 8 + (lane >> 2);
+    if (row >= m) continue;
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int col = wn * 16 + j * 8 + (lane & 3) * 2 + e;
+        if (col < n) C[row + col * ldc] = acc[i][j][e];
+      }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // (panel step: panel.cuh)
 // ---------------------------------------------------------------------------
 // Extend-add (multifrontal assembly), gather form: one warp per (front, front
