@@ -140,6 +140,7 @@ DeviceFactor::DeviceFactor(std::shared_ptr<const Symbolic> sym, cudaStream_t str
   if (const char* e = std::getenv("GMRF_EA_SPLIT")) ea_split_ = e[0] != '0';
   if (const char* e = std::getenv("GMRF_WIDE_K")) wide_min_k_ = atoi(e);
   if (const char* e = std::getenv("GMRF_GEMM_NEXT")) gemm_next_ = e[0] != '0';
+  if (const char* e = std::getenv("GMRF_NEXT_TILES")) next_max_tiles_ = atoll(e);
   if (const char* e = std::getenv("GMRF_WIDE_R")) wide_min_r_ = atoi(e);
   if (const char* e = std::getenv("GMRF_INC_B")) inc_b_ = std::max(1, atoi(e));
   if (const char* e = std::getenv("GMRF_EA_CTA")) ea_cta_max_ = atoll(e);
@@ -581,11 +582,9 @@ void DeviceFactor::build_factor_plan() {
       // right-looking update of the trailing panel columns [j0, j1) with the
       // finished columns [k0, k1) (trailing_jobs: next block on the chain,
       // deferred bulk updates of the blocks further right)
-      // one-wave levels (the chain at the top of the tree): the next-block update
-      // runs on 32×32 tiles with one-shot operand loads (k_gemm_next)
-      const bool next32 = gemm_next_ && kcrit[lv] <= kNKMax &&
-                          gpan[3 * lv] <= rows_max_ctas_ && gpan[3 * lv + 1] <= rows_max_ctas_ &&
-                          gpan[3 * lv + 2] <= rows_max_ctas_;
+      // levels whose next-block updates are at most about one wave of 32×32 tiles (the
+      // chain at the top of the tree): one-shot operand loads, k_gemm_next
+      const bool next32 = gemm_next_ && kcrit[lv] <= kNKMax && ggm[lv] <= next_max_tiles_;
       trailing_jobs(w, rows, c, [&](bool crit, int j0, int j1, int k0, int k1) {
         const int T = crit && next32 ? kNTile : kTile;
         for (int jb = j0; jb < j1; jb += T)
@@ -707,8 +706,7 @@ void DeviceFactor::build_factor_plan() {
     pof.insert(pof.end(), po[l].begin(), po[l].end());
     eaf.insert(eaf.end(), ea[l].begin(), ea[l].end());
     flev_[l].dwait = dwait[l];
-    flev_[l].gm32 = gemm_next_ && kcrit[l] <= kNKMax && gpan[3 * l] <= rows_max_ctas_ &&
-                    gpan[3 * l + 1] <= rows_max_ctas_ && gpan[3 * l + 2] <= rows_max_ctas_;
+    flev_[l].gm32 = gemm_next_ && kcrit[l] <= kNKMax && ggm[l] <= next_max_tiles_;
     flev_[l].eau0 = static_cast<int64_t>(eaf.size());
     flev_[l].eaun = static_cast<int64_t>(eau[l].size());
     eaf.insert(eaf.end(), eau[l].begin(), eau[l].end());

@@ -252,6 +252,7 @@ class DeviceFactor {
   // k_gemm_wide for bulk GEMMs with at least wide_min_r_ rows and K >= wide_min_k_ (0 disables)
   int wide_min_r_ = 2048, wide_min_k_ = 512;
   bool use_wide(int r, int K) const { return wide_min_k_ > 0 && r >= wide_min_r_ && K >= wide_min_k_; }
+  int64_t next_max_tiles_ = 222;   // ... on levels with at most this many 64×64 next-block tiles (over all ranks)
   bool gemm_next_ = true;          // k_gemm_next for the chain GEMMs of one-wave levels (GMRF_GEMM_NEXT=0: A/B)
   bool ea_split_ = true;           // update-block extend-add on the bulk stream (GMRF_EA_SPLIT=0: A/B)
   int inc_b_ = 2;                  // chunks per incremental batch (K = inc_b_·kNB per pass over U)
