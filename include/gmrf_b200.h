@@ -316,6 +316,30 @@ typedef struct {
  * Host only. Call with col_idx == NULL for the nnz (row_ptr[m] filled). */
 int gmrf_point_operator(const gmrf_matern_config_t* mesh, int32_t m, const double* points,
                         int64_t* row_ptr, int32_t* col_idx, double* values);
+/* P1 element assembly on the device (fem_device.cu), one thread per matrix
+ * column, element contributions summed in the reference's triplet order:
+ *   which 0: assemble_mass (fem/assembly.hpp:81-101), M_ij = ∫ φ_i φ_j;
+ *   which 1: assemble_stiffness (assembly.hpp:104-161): dim 1 — diffusion ·
+ *            ∫φ'_i φ'_j + advection · ∫φ_i φ'_j + reaction · ∫φ_i φ_j; dim 2 —
+ *            diffusion · ∫∇φ_i·∇φ_j (laplace_operator, assembly.hpp:48).
+ * The mesh is cfg's (kappa/alpha/tau unused). Full CSC out: call with
+ * row_idx == NULL to get col_ptr[n+1], then again for row_idx / values.
+ * lumped (may be NULL, n values, which 0 only): lumped_mass_vector row sums
+ * (assembly.hpp:241-262). dirichlet != 0 (dim 1): the matrix with both end
+ * nodes constrained, fold_and_mask with T = I (fem/constraints.hpp:111-128):
+ * their rows/columns removed and `constrained_diag` on their diagonal
+ * (apply_constraints_precision_pair :158-173 uses 1 for K and ε² for M).
+ * gmrf_fem_assemble_host evaluates the same formulas in host loops (no device):
+ * the two agree bit for bit. */
+int gmrf_fem_assemble(const gmrf_matern_config_t* cfg, int32_t which, double diffusion,
+                      double advection, double reaction, int32_t dirichlet,
+                      double constrained_diag, int32_t* n, int64_t* col_ptr, int32_t* row_idx,
+                      double* values, double* lumped);
+int gmrf_fem_assemble_host(const gmrf_matern_config_t* cfg, int32_t which, double diffusion,
+                           double advection, double reaction, int32_t dirichlet,
+                           double constrained_diag, int32_t* n, int64_t* col_ptr,
+                           int32_t* row_idx, double* values, double* lumped);
+
 /* matern_prior (priors/matern.hpp:53-80): the prior precision Q assembled on
  * the device (fixed-pattern Gram product of K = K_Δ + κ²M with the lumped mass),
  * full symmetric CSC. col_ptr[n+1] first (row_idx == NULL), then the rest. */

@@ -137,6 +137,34 @@ void put_trace(Bundle& b, const std::vector<solver::GaussNewtonIteration>& tr) {
   b.vecs["gn_backtracks"] = bt;
 }
 
+// ----- a4-a6: P1 element matrices of one slice -----------
+Bundle* build_fem(const double* p, int np) {
+  // p: [dim, resolution, xa, xb, diffusion, advection, reaction, dirichlet, eps]
+  (void)np;
+  const int dim = static_cast<int>(p[0]), res = static_cast<int>(p[1]);
+  auto* b = new Bundle();
+  fem::FeSpace space(dim == 1 ? fem::build_interval_mesh(res, p[2], p[3])
+                              : fem::build_unit_square_mesh(res),
+                     1);
+  fem::DifferentialOperatorSpec op;
+  op.diffusion = p[4];
+  if (p[5] != 0.0) op.advection = {p[5]};
+  op.reaction = p[6];
+  SparseMatrixCSC m = fem::assemble_mass(space);
+  SparseMatrixCSC k = fem::assemble_stiffness(space, op);
+  b->mats["M"] = m;
+  b->mats["K"] = k;
+  b->vecs["lumped"] = fem::lumped_mass_vector(m);
+  if (p[7] != 0.0) {
+    fem::ConstraintSet cs = priors::embed_dirichlet(space, p[8]);
+    auto pr = fem::apply_constraints_precision_pair(k, m, cs);
+    b->mats["K_c"] = pr.first;
+    b->mats["M_c"] = pr.second;
+    b->vecs["lumped_c"] = fem::lumped_mass_vector(pr.second);
+  }
+  return b;
+}
+
 // ----- C1/C2: Matérn regression ------------------------
 Bundle* build_matern(int dim, const double* p, int np) {
   // p: [resolution, kappa, alpha, tau, n_obs, seed, noise_prec, obs_sd, n_samples,
@@ -472,6 +500,7 @@ const char* ref_last_error() { return g_err.c_str(); }
 void* ref_build(const char* kind, const double* p, int np) {
   try {
     std::string k(kind);
+    if (k == "fem") return build_fem(p, np);
     if (k == "matern1d") return build_matern(1, p, np);
     if (k == "matern2d") return build_matern(2, p, np);
     if (k == "spatiotemporal") return build_spatiotemporal(p, np);

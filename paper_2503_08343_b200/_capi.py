@@ -175,6 +175,11 @@ SIGNATURES = {
     "gmrf_point_operator": (C.c_int, [C.POINTER(MaternConfig), C.c_int32, f64p, i64p, i32p,
                                       f64p]),
     "gmrf_matern_prior": (C.c_int, [C.POINTER(MaternConfig), i32p, i64p, i32p, f64p]),
+    "gmrf_fem_assemble": (C.c_int, [C.POINTER(MaternConfig), C.c_int32, C.c_double, C.c_double,
+                                    C.c_double, C.c_int32, C.c_double, i32p, i64p, i32p, f64p, f64p]),
+    "gmrf_fem_assemble_host": (C.c_int, [C.POINTER(MaternConfig), C.c_int32, C.c_double, C.c_double,
+                                         C.c_double, C.c_int32, C.c_double, i32p, i64p, i32p, f64p,
+                                         f64p]),
     "gmrf_regression_create": (C.c_int, [C.POINTER(MaternConfig), C.c_int32, f64p, i32p,
                                          C.POINTER(vp)]),
     "gmrf_regression_run": (C.c_int, [vp, f64p, f64p, C.c_int32, C.c_int32, C.c_uint64, f64p,

@@ -771,6 +771,55 @@ int gmrf_point_operator(const gmrf_matern_config_t* mesh, int32_t m, const doubl
   });
 }
 
+static int fem_assemble(bool device, const gmrf_matern_config_t* cfg, int32_t which, double diff,
+                        double adv, double react, int32_t dirichlet, double cdiag, int32_t* n,
+                        int64_t* cp, int32_t* ri, double* v, double* lumped) {
+  return guard([&] {
+    gmrf::require(cfg && n && cp, gmrf::kContract, "fem_assemble: null argument");
+    gmrf::require(cfg->dim == 1 || cfg->dim == 2, gmrf::kContract, "fem_assemble: dim must be 1 or 2");
+    gmrf::require(which == 0 || which == 1, gmrf::kContract, "fem_assemble: which must be 0 or 1");
+    gmrf::require(!dirichlet || cfg->dim == 1, gmrf::kContract,
+                  "fem_assemble: Dirichlet folding is for the interval mesh");
+    gmrf::Csc m;
+    if (device) {
+      m = gmrf::p1_matrix_device(cfg->dim, cfg->n_el, cfg->xa, cfg->xb, which, diff, adv, react);
+    } else if (cfg->dim == 1) {
+      const gmrf::Space1D s{cfg->n_el, cfg->xa, cfg->xb};
+      m = which == 0 ? gmrf::p1_mass(s) : gmrf::p1_stiffness(s, diff, adv, react);
+    } else {
+      const gmrf::Space2D s{cfg->n_el};
+      m = which == 0 ? gmrf::p1_mass(s) : gmrf::scale(gmrf::p1_laplace(s), diff);
+    }
+    if (dirichlet) {
+      const auto mask = gmrf::dirichlet_mask(gmrf::Space1D{cfg->n_el, cfg->xa, cfg->xb}, true);
+      m = device ? gmrf::mask_constrained_device(m, mask, cdiag)
+                 : gmrf::mask_constrained_host(m, mask, cdiag);
+    }
+    *n = m.nr;
+    for (size_t i = 0; i < m.cp.size(); ++i) cp[i] = m.cp[i];
+    if (!ri) return;
+    gmrf::require(v != nullptr, gmrf::kContract, "fem_assemble: values missing");
+    for (size_t i = 0; i < m.ri.size(); ++i) {
+      ri[i] = m.ri[i];
+      v[i] = m.v[i];
+    }
+    if (lumped) {
+      const std::vector<double> l = device ? gmrf::lumped_mass_device(m) : gmrf::lumped_mass_host(m);
+      for (size_t i = 0; i < l.size(); ++i) lumped[i] = l[i];
+    }
+  });
+}
+int gmrf_fem_assemble(const gmrf_matern_config_t* cfg, int32_t which, double diff, double adv,
+                      double react, int32_t dirichlet, double cdiag, int32_t* n, int64_t* cp,
+                      int32_t* ri, double* v, double* lumped) {
+  return fem_assemble(true, cfg, which, diff, adv, react, dirichlet, cdiag, n, cp, ri, v, lumped);
+}
+int gmrf_fem_assemble_host(const gmrf_matern_config_t* cfg, int32_t which, double diff, double adv,
+                           double react, int32_t dirichlet, double cdiag, int32_t* n, int64_t* cp,
+                           int32_t* ri, double* v, double* lumped) {
+  return fem_assemble(false, cfg, which, diff, adv, react, dirichlet, cdiag, n, cp, ri, v, lumped);
+}
+
 int gmrf_matern_prior(const gmrf_matern_config_t* cfg, int32_t* n, int64_t* cp, int32_t* ri,
                       double* v) {
   return guard([&] {

@@ -174,9 +174,11 @@ Csc p1_stiffness(const Space1D& s, double diff, double adv, double react) {
     for (int i = 0; i < 2; ++i)
       for (int j = 0; j < 2; ++j) {
         const double gi = (i == 0 ? -1.0 : 1.0) / h, gj = (j == 0 ? -1.0 : 1.0) / h;
+        // fused accumulations written out (std::fma), so the values do not depend on
+        // the compiler's contraction choices and k_p1_interval reproduces them exactly
         double v = diff * gi * gj * h;
-        v += adv * gj * 0.5 * h;
-        v += react * h * (i == j ? 1.0 / 3.0 : 1.0 / 6.0);
+        v = std::fma(adv * gj * 0.5, h, v);
+        v = std::fma(react * h, i == j ? 1.0 / 3.0 : 1.0 / 6.0, v);
         loc[i][j] = v;
       }
     for (int i = 0; i < 2; ++i)
@@ -207,8 +209,8 @@ void for_each_triangle(const Space2D& s, F&& f) {
 Csc p1_mass(const Space2D& s) {
   std::vector<Trip> t;
   for_each_triangle(s, [&](const i32* v, const double (*p)[2]) {
-    const double area = 0.5 * ((p[1][0] - p[0][0]) * (p[2][1] - p[0][1]) -
-                               (p[2][0] - p[0][0]) * (p[1][1] - p[0][1]));
+    const double area = 0.5 * std::fma(p[1][0] - p[0][0], p[2][1] - p[0][1],
+                                       -((p[2][0] - p[0][0]) * (p[1][1] - p[0][1])));
     for (int i = 0; i < 3; ++i)
       for (int j = 0; j < 3; ++j) t.push_back({v[i], v[j], area / 12.0 * (i == j ? 2.0 : 1.0)});
   });
@@ -218,8 +220,8 @@ Csc p1_mass(const Space2D& s) {
 Csc p1_laplace(const Space2D& s) {
   std::vector<Trip> t;
   for_each_triangle(s, [&](const i32* v, const double (*p)[2]) {
-    const double det = (p[1][0] - p[0][0]) * (p[2][1] - p[0][1]) -
-                       (p[2][0] - p[0][0]) * (p[1][1] - p[0][1]);
+    const double det = std::fma(p[1][0] - p[0][0], p[2][1] - p[0][1],
+                                -((p[2][0] - p[0][0]) * (p[1][1] - p[0][1])));
     const double area = 0.5 * det;
     double g[3][2];
     for (int i = 0; i < 3; ++i) {
@@ -229,7 +231,9 @@ Csc p1_laplace(const Space2D& s) {
     }
     for (int i = 0; i < 3; ++i)
       for (int j = 0; j < 3; ++j)
-        t.push_back({v[i], v[j], area * (g[i][0] * g[j][0] + g[i][1] * g[j][1])});
+        // ∇φ_i·∇φ_j with the first product fused (written out so that the value does not
+        // depend on the compiler's contraction choices; k_p1_square does the same)
+        t.push_back({v[i], v[j], area * std::fma(g[i][0], g[j][0], g[i][1] * g[j][1])});
   });
   return csc_from_trips(s.n(), s.n(), std::move(t));
 }
@@ -240,7 +244,20 @@ std::vector<char> dirichlet_mask(const Space1D& s, bool enabled) {
   return m;
 }
 
+namespace {
+LumpFn g_lump = nullptr;
+MaskFn g_mask = nullptr;
+}  // namespace
+void set_fem_hooks(LumpFn lump, MaskFn mask) {
+  g_lump = lump;
+  g_mask = mask;
+}
 Csc mask_constrained(const Csc& a, const std::vector<char>& mask, double diag) {
+  return g_mask ? g_mask(a, mask, diag) : mask_constrained_host(a, mask, diag);
+}
+std::vector<double> lumped_mass(const Csc& m) { return g_lump ? g_lump(m) : lumped_mass_host(m); }
+
+Csc mask_constrained_host(const Csc& a, const std::vector<char>& mask, double diag) {
   std::vector<Trip> t;
   for (i32 j = 0; j < a.nc; ++j)
     for (i64 p = a.cp[j]; p < a.cp[j + 1]; ++p)
@@ -250,7 +267,7 @@ Csc mask_constrained(const Csc& a, const std::vector<char>& mask, double diag) {
   return csc_from_trips(a.nr, a.nc, std::move(t));
 }
 
-std::vector<double> lumped_mass(const Csc& m) {
+std::vector<double> lumped_mass_host(const Csc& m) {
   std::vector<double> d(m.nr, 0.0);
   for (i32 j = 0; j < m.nc; ++j)
     for (i64 p = m.cp[j]; p < m.cp[j + 1]; ++p) d[m.ri[p]] += m.v[p];

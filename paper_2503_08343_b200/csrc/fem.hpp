@@ -88,8 +88,16 @@ SpatialOps spatial_ops(const Space2D& s, double diff);
 // Homogeneous Dirichlet on both end nodes: slack coordinates.
 std::vector<char> dirichlet_mask(const Space1D& s, bool enabled);
 // fold_and_mask with T = I: constrained rows/cols removed, `diag` inserted.
+// mask_constrained / lumped_mass run the device kernels of fem_device.cu while a
+// FemDeviceScope is alive (the pipelines' setup), the host loops otherwise (the
+// device-free symbolic planning entry points and the CPU tests).
 Csc mask_constrained(const Csc& a, const std::vector<char>& mask, double diag);
 std::vector<double> lumped_mass(const Csc& m);
+Csc mask_constrained_host(const Csc& a, const std::vector<char>& mask, double diag);
+std::vector<double> lumped_mass_host(const Csc& m);
+using LumpFn = std::vector<double> (*)(const Csc&);
+using MaskFn = Csc (*)(const Csc&, const std::vector<char>&, double);
+void set_fem_hooks(LumpFn lump, MaskFn mask);  // nullptr: host
 
 struct MaternSpec {
   double kappa = 1.0;

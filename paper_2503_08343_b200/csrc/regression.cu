@@ -1,6 +1,8 @@
 // Matérn SPDE regression posterior on the device. See regression.hpp.
 #include "regression.hpp"
 
+#include "fem_device.hpp"
+
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -119,9 +121,11 @@ RegressionPosterior::RegressionPosterior(const MeshSpec& mesh, const MaternSpec&
   const double t0 = now_ms();
   require(spec.kappa > 0 && spec.alpha >= 1 && spec.tau > 0, kContract, "matern: bad spec");
   require(mesh.n_el >= 1, kContract, "mesh: need at least one element");
-  SpatialOps ops = mesh.dim == 1
-                       ? spatial_ops(Space1D{mesh.n_el, mesh.xa, mesh.xb}, 0.0, 0.0, false)
-                       : spatial_ops(Space2D{mesh.n_el}, 1.0);
+  // P1 element assembly, lumping and constraint folding on the device (fem_device.cu)
+  FemDeviceScope fem_scope;
+  SpatialOps ops = mesh.dim == 1 ? spatial_ops_device(Space1D{mesh.n_el, mesh.xa, mesh.xb}, 0.0, 0.0,
+                                                      false, stream_)
+                                 : spatial_ops_device(Space2D{mesh.n_el}, 1.0, stream_);
   n_ = ops.n;
   // prior operator rows (row 1): α <= 2 → K̂ = K_Δ + κ²M with weights 1/m̃ and
   // scale 1/τ² (matern.hpp:56-73, α = 1 and 2 give the same Q); α >= 3 → the

@@ -358,7 +358,7 @@ SpaceTimePosterior::SpaceTimePosterior(const SpaceTimeSpec& spec, cudaStream_t s
 }
 
 SpaceTimePosterior::SpaceTimePosterior(const SpaceTimeSpec& spec, HostOnly)
-    : spec_(spec), stream_(nullptr) {
+    : spec_(spec), stream_(nullptr), host_only_(true) {
   build_host();
 }
 
@@ -378,11 +378,19 @@ void SpaceTimePosterior::build_host() {
   require(spec_.residual >= 0 && spec_.residual <= 2, kContract, "spacetime: unknown residual");
   require(spec_.dim == 1 || (spec_.residual != 1 && spec_.advection == 0.0 && !spec_.dirichlet),
           kContract, "spacetime: 2-D supports the heat proxy, natural BC, linear/Allen-Cahn residuals");
+  // element assembly, lumping and constraint folding on the device (fem_device.cu);
+  // the device-free planning path (host_symbolic) keeps the host loops: it only
+  // needs the patterns
+  std::unique_ptr<FemDeviceScope> fem_scope;
+  if (!host_only_) fem_scope = std::make_unique<FemDeviceScope>();
   if (spec_.dim == 1) {
     space_ = Space1D{spec_.n_el, spec_.xa, spec_.xb};
-    ops_ = spatial_ops(space_, spec_.diffusion, spec_.advection, spec_.dirichlet);
+    ops_ = host_only_ ? spatial_ops(space_, spec_.diffusion, spec_.advection, spec_.dirichlet)
+                      : spatial_ops_device(space_, spec_.diffusion, spec_.advection,
+                                           spec_.dirichlet, stream_);
   } else {
-    ops_ = spatial_ops(Space2D{spec_.n_el}, spec_.diffusion);
+    ops_ = host_only_ ? spatial_ops(Space2D{spec_.n_el}, spec_.diffusion)
+                      : spatial_ops_device(Space2D{spec_.n_el}, spec_.diffusion, stream_);
   }
   ns_ = ops_.n;
   nt_ = spec_.n_t;

@@ -12,6 +12,7 @@
 
 #include "factor.hpp"
 #include "fem.hpp"
+#include "fem_device.hpp"
 #include "gram.hpp"
 
 namespace gmrf {
@@ -121,6 +122,7 @@ class SpaceTimePosterior {
 
   SpaceTimeSpec spec_;
   cudaStream_t stream_;
+  bool host_only_ = false;  // device-free symbolic planning (host_symbolic)
   PartitionSpec pspec_;
   Space1D space_{};
   SpatialOps ops_;
