@@ -453,10 +453,13 @@ def main():
     step_kernel_ms = sum(v["ms"] for v in stats.values())
     dom_name, dom = max(stats.items(), key=lambda kv: kv[1]["ms"])
     # DRAM traffic per launch of the dominant kernel class, from the committed ncu
-    # capture (profiles/r01_ncu_traffic.json, tools/ncu_traffic.py), when present
+    # capture (profiles/r02_ncu_traffic.json, tools/ncu_traffic.py), when present
     traffic = None
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")) as fh:
+        tpath = os.path.join(ROOT, "profiles", "r02_ncu_traffic.json")
+        if not os.path.exists(tpath):
+            tpath = os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")
+        with open(tpath) as fh:
             tr = json.load(fh).get(dom_name, {})
             if tr.get("workload", "c4") == args.workload:
                 traffic = tr.get("dram_bytes_per_launch")
