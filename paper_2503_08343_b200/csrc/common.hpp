@@ -1,9 +1,12 @@
 // Shared host-side types and error plumbing for libgmrf_b200.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
+#include <exception>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 namespace gmrf {
@@ -31,6 +34,38 @@ struct Error : std::runtime_error {
 
 inline void require(bool c, Status s, const std::string& m) {
   if (!c) fail(s, m);
+}
+
+// Host setup loops over columns / entries that are independent of one another
+// (plan construction): fn(begin, end, thread) on contiguous ranges of [0, n).
+// Exceptions thrown by fn are rethrown on the calling thread.
+template <typename F>
+inline void parallel_ranges(int64_t n, F&& fn, int max_threads = 32) {
+  unsigned hw = std::thread::hardware_concurrency();
+  int t = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>({static_cast<int64_t>(hw ? hw : 1),
+                                                                  max_threads, n / 4096 + 1})));
+  if (t == 1) {
+    fn(static_cast<int64_t>(0), n, 0);
+    return;
+  }
+  std::vector<std::thread> th;
+  std::vector<std::exception_ptr> err(t);
+  for (int i = 0; i < t; ++i)
+    th.emplace_back([&, i] {
+      try {
+        fn(n * i / t, n * (i + 1) / t, i);
+      } catch (...) {
+        err[i] = std::current_exception();
+      }
+    });
+  for (auto& x : th) x.join();
+  for (auto& e : err)
+    if (e) std::rethrow_exception(e);
+}
+inline int parallel_threads(int64_t n, int max_threads = 32) {
+  unsigned hw = std::thread::hardware_concurrency();
+  return static_cast<int>(std::max<int64_t>(
+      1, std::min<int64_t>({static_cast<int64_t>(hw ? hw : 1), max_threads, n / 4096 + 1})));
 }
 
 }  // namespace gmrf

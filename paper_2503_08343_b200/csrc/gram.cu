@@ -1,6 +1,8 @@
 // Fixed-pattern weighted Gram update (gram.hpp).
 #include "gram.hpp"
 
+#include <memory>
+
 #include <algorithm>
 #include <string>
 
@@ -83,50 +85,90 @@ GramPlan::GramPlan(i32 n, const i64* pcp, const i32* pri, i32 m, const i64* arp,
       }
   }
   require(na_ < (1ll << 31), kContract, "gram: operator nnz exceeds int32 value indices");
-  // product map over the computed entries
-  std::vector<i64> ent, off(1, 0), tpos;
-  std::vector<int2> pr;
-  i64 covered = 0;
-  for (i32 C = 0; C < n; ++C)
-    for (i64 p = pcp[C]; p < pcp[C + 1]; ++p) {
-      const i32 R = pri[p];
-      const bool want = !need || (*need)[p];
-      i64 x = acp[R], xe = acp[R + 1], y = acp[C], ye = acp[C + 1];
-      i64 cnt = 0;
-      while (x < xe && y < ye) {
-        if (ak[x] < ak[y]) {
-          ++x;
-        } else if (ak[y] < ak[x]) {
-          ++y;
-        } else {
-          if (want) pr.push_back(make_int2(av[x], av[y]));
-          ++cnt;
-          ++x;
-          ++y;
+  // product map over the computed entries: count the shared rows of every
+  // pattern entry, prefix-sum, then fill — both merge passes run over column
+  // ranges on the host threads (the map of config 4's S Sᵀ has 2e8 pairs, the
+  // config-5 shapes' 2e9)
+  const i64 npat = pcp[n];
+  std::vector<i32> cnt(static_cast<size_t>(npat), 0);
+  std::vector<i64> cov(parallel_threads(n), 0);
+  parallel_ranges(n, [&](int64_t c0, int64_t c1, int t) {
+    i64 covered_t = 0;
+    for (i32 C = static_cast<i32>(c0); C < static_cast<i32>(c1); ++C)
+      for (i64 p = pcp[C]; p < pcp[C + 1]; ++p) {
+        const i32 R = pri[p];
+        i64 x = acp[R], xe = acp[R + 1], y = acp[C], ye = acp[C + 1];
+        i32 c = 0;
+        while (x < xe && y < ye) {
+          if (ak[x] < ak[y]) {
+            ++x;
+          } else if (ak[y] < ak[x]) {
+            ++y;
+          } else {
+            ++c;
+            ++x;
+            ++y;
+          }
         }
+        cnt[p] = c;
+        covered_t += c;
       }
-      covered += cnt;
-      if (want) {
-        if (need) ent.push_back(p);
-        off.push_back(static_cast<i64>(pr.size()));
+    cov[t] = covered_t;
+  });
+  i64 covered = 0;
+  for (i64 c : cov) covered += c;
+  std::vector<i64> ent, off(1, 0), tpos;
+  std::vector<i64> slot(static_cast<size_t>(npat), -1);  // pattern entry → computed-entry index
+  for (i64 p = 0; p < npat; ++p) {
+    if (need && !(*need)[p]) continue;
+    slot[p] = static_cast<i64>(off.size()) - 1;
+    if (need) ent.push_back(p);
+    off.push_back(off.back() + cnt[p]);
+  }
+  const i64 npr = off.back();
+  std::unique_ptr<int2[]> pr(new int2[std::max<i64>(npr, 1)]);  // uninitialised: filled below
+  if (base_transpose) tpos.assign(off.size() - 1, 0);
+  parallel_ranges(n, [&](int64_t c0, int64_t c1, int) {
+    for (i32 C = static_cast<i32>(c0); C < static_cast<i32>(c1); ++C)
+      for (i64 p = pcp[C]; p < pcp[C + 1]; ++p) {
+        const i64 e = slot[p];
+        if (e < 0) continue;
+        const i32 R = pri[p];
+        i64 x = acp[R], xe = acp[R + 1], y = acp[C], ye = acp[C + 1];
+        int2* out = pr.get() + off[e];
+        while (x < xe && y < ye) {
+          if (ak[x] < ak[y]) {
+            ++x;
+          } else if (ak[y] < ak[x]) {
+            ++y;
+          } else {
+            *out++ = make_int2(av[x], av[y]);
+            ++x;
+            ++y;
+          }
+        }
         if (base_transpose) {  // position of (C, R): binary search in column R
           const i32* b0 = pri + pcp[R];
           const i32* b1 = pri + pcp[R + 1];
           const i32* f = std::lower_bound(b0, b1, C);
           require(f != b1 && *f == C, kStructural, "gram: pattern is not symmetric");
-          tpos.push_back(pcp[R] + (f - b0));
+          tpos[e] = pcp[R] + (f - b0);
         }
       }
-    }
+  });
   // every product A_kR A_kC must have a home in the pattern
   i64 total = 0;
   for (i32 k = 0; k < m; ++k) total += (arp[k + 1] - arp[k]) * (arp[k + 1] - arp[k]);
   require(covered == total, kStructural,
           "gram: pattern does not contain the operator's product pattern (" +
               std::to_string(covered) + " of " + std::to_string(total) + " products)");
-  npairs_ = static_cast<i64>(pr.size());
+  npairs_ = npr;
   off_.upload(off, stream);
-  pairs_.upload(pr, stream);
+  pairs_.alloc(static_cast<size_t>(std::max<i64>(npr, 1)));
+  if (npr)
+    cuda_check(cudaMemcpyAsync(pairs_.p, pr.get(), static_cast<size_t>(npr) * sizeof(int2),
+                               cudaMemcpyHostToDevice, stream),
+               "gram pairs upload");
   arow_.upload(arow, stream);
   wa_.alloc(std::max<i64>(na_, 1));
   if (base_transpose) tpos_.upload(tpos, stream);

@@ -378,6 +378,14 @@ void SpaceTimePosterior::build_host() {
   require(spec_.residual >= 0 && spec_.residual <= 2, kContract, "spacetime: unknown residual");
   require(spec_.dim == 1 || (spec_.residual != 1 && spec_.advection == 0.0 && !spec_.dirichlet),
           kContract, "spacetime: 2-D supports the heat proxy, natural BC, linear/Allen-Cahn residuals");
+  double t_stage = now_ms();
+  auto stage = [&](const char* what) {  // GMRF_VERBOSE: host setup time per stage
+    if (std::getenv("GMRF_VERBOSE")) {
+      const double t = now_ms();
+      std::fprintf(stderr, "[gmrf] host setup: %-28s %8.1f ms\n", what, t - t_stage);
+      t_stage = t;
+    }
+  };
   // element assembly, lumping and constraint folding on the device (fem_device.cu);
   // the device-free planning path (host_symbolic) keeps the host loops: it only
   // needs the patterns
@@ -412,6 +420,7 @@ void SpaceTimePosterior::build_host() {
   // spatial coupling stencil (P1 element adjacency = the mass pattern)
   Csc stencil = ops_.mass;
 
+  stage("spatial blocks");
   // ---- templates: spatial patterns of the diagonal / upper off-diagonal blocks
   // (every prior block, plus stencil² which carries JᵀΛJ of a residual whose
   // rows couple the stencil of a DoF in two consecutive slices)
@@ -449,6 +458,7 @@ void SpaceTimePosterior::build_host() {
       pcp_[C + 1] = static_cast<i64>(pri_.size());
     }
 
+  stage("master pattern");
   // ---- symbolic: geometric nested dissection of the space-time grid (separator
   // thickness = the coupling radii of the pattern), shared by every
   // factorization of the run
@@ -473,6 +483,7 @@ void SpaceTimePosterior::build_host() {
     sym_ = std::make_shared<const Symbolic>(analyze(n_, pcp_.data(), pri_.data(), perm.data(), opt));
   }
 
+  stage("ordering + symbolic");
   // ---- S_cond = [S_prior | Aᵀ L_ε] (gmrf.hpp:165), CSC, columns in the reference order
   s_ = Csc{};
   s_.nr = n_;
@@ -509,6 +520,7 @@ void SpaceTimePosterior::build_host() {
   s_.nc = static_cast<i32>(s_.cp.size()) - 1;
   ms_ = s_.nc;
 
+  stage("square-root pattern");
   // ---- residual Jacobian pattern (CSR rows, then CSC with a value map): row
   // (step s, kept DoF d) couples the stencil of d in slices s and s+1, slack
   // columns skipped (residual.hpp:353-377)
@@ -544,6 +556,15 @@ void SpaceTimePosterior::build_host() {
 }
 
 void SpaceTimePosterior::assemble_device() {
+  double t_stage = now_ms();
+  auto stage = [&](const char* what) {  // GMRF_VERBOSE: device setup time per stage
+    if (std::getenv("GMRF_VERBOSE")) {
+      cudaStreamSynchronize(stream_);
+      const double t = now_ms();
+      std::fprintf(stderr, "[gmrf] device setup: %-26s %8.1f ms\n", what, t - t_stage);
+      t_stage = t;
+    }
+  };
   const auto& sl = blk_.slack;
   d_pcp_.upload(pcp_, stream_);
   d_pri_.upload(pri_, stream_);
@@ -579,8 +600,10 @@ void SpaceTimePosterior::assemble_device() {
   d_sv_.upload(s_.v, stream_);
   // q_eff = sym(S Sᵀ) (gauss_newton.hpp:112-113): Gram product of Sᵀ, whose rows
   // are S's columns, over the master pattern
+  stage("uploads");
   gram_s_ = std::make_unique<GramPlan>(n_, pcp_.data(), pri_.data(), ms_, s_.cp.data(),
                                        s_.ri.data(), nullptr, stream_);
+  stage("Gram plan S S^T");
   assemble_values();
   Csc sr = transpose(s_);
   d_srp_.upload(sr.cp, stream_);
@@ -601,8 +624,10 @@ void SpaceTimePosterior::assemble_device() {
     // JᵀΛJ over the entries the factorization reads (qmap >= 0), written into the panels
     std::vector<char> need(pri_.size());
     for (size_t p = 0; p < need.size(); ++p) need[p] = sym_->qmap[p] >= 0;
+    stage("assembly + S rows");
     gram_j_ = std::make_unique<GramPlan>(n_, pcp_.data(), pri_.data(), nres_, jrp_.data(),
                                          jci_.data(), &need, stream_);
+    stage("Gram plan J^T J");
     d_lam_.upload(std::vector<double>(nres_, spec_.pde_noise_prec), stream_);
     d_wf_.alloc(std::max(nres_, 1));
     d_jrp_.upload(jrp_, stream_);
@@ -621,7 +646,9 @@ void SpaceTimePosterior::assemble_device() {
                  n_, pri_.size(), static_cast<long long>(gram_j_ ? gram_j_->pairs() : 0),
                  static_cast<long long>(gram_s_->pairs()),
                  static_cast<long long>(sym_->nnz_l_padded));
+  stage("Jacobian uploads");
   fac_ = std::make_unique<DeviceFactor>(sym_, stream_, pspec_.nranks > 1 ? &pspec_ : nullptr);
+  stage("factor plan + storage");
   auto mem = [&](const char* what) {
     if (!std::getenv("GMRF_VERBOSE")) return;
     size_t fr = 0, tot = 0;
@@ -631,6 +658,7 @@ void SpaceTimePosterior::assemble_device() {
   mem("factor storage");
   fac_->set_selinv_inplace(true);  // variances are the last use of each factorization
   fac_->prepare_selinv();
+  stage("selected-inversion plan");
   mem("selected-inversion storage");
   fac_->set_profiler(&prof_);
   for (DevBuf<double>* v : {&mean_cond_, &mean_, &var_, &x_, &c_, &g_, &d_, &cand_, &r1_, &u0_})
