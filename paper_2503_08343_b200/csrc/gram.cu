@@ -1,7 +1,7 @@
 // Fixed-pattern weighted Gram update (gram.hpp).
 #include "gram.hpp"
 
-#include <memory>
+#include <cub/cub.cuh>
 
 #include <algorithm>
 #include <string>
@@ -48,6 +48,81 @@ __global__ void k_gram(i64 ne, const i64* __restrict__ ent, const i64* __restric
   }
 }
 
+// ---- product map, built on the device -------------------------------------------
+// For pattern entry p = (R, C): the rows k shared by columns R and C of A (both
+// lists ascending) — counted (pass 1), then written as (value index of A_kR,
+// value index of A_kC) pairs at the entry's offset (pass 2). One thread per
+// pattern column walks its entries; masked entries are not computed.
+__global__ void k_gram_count(i32 n, const i64* __restrict__ pcp, const i32* __restrict__ pri,
+                             const i64* __restrict__ acp, const i32* __restrict__ ak,
+                             const char* __restrict__ need, i64* __restrict__ cnt,
+                             unsigned long long* __restrict__ covered) {
+  unsigned long long cov = 0;
+  for (i32 C = blockIdx.x * blockDim.x + threadIdx.x; C < n; C += gridDim.x * blockDim.x)
+    for (i64 p = pcp[C]; p < pcp[C + 1]; ++p) {
+      const i32 R = pri[p];
+      i64 x = acp[R], y = acp[C];
+      const i64 xe = acp[R + 1], ye = acp[C + 1];
+      i64 c = 0;
+      while (x < xe && y < ye) {
+        const i32 kx = ak[x], ky = ak[y];
+        c += kx == ky;
+        x += kx <= ky;
+        y += ky <= kx;
+      }
+      cov += static_cast<unsigned long long>(c);
+      cnt[p] = (!need || need[p]) ? c : 0;
+    }
+  if (cov) atomicAdd(covered, cov);  // integer: order does not matter
+}
+
+__global__ void k_gram_fill(i32 n, const i64* __restrict__ pcp, const i32* __restrict__ pri,
+                            const i64* __restrict__ acp, const i32* __restrict__ ak,
+                            const i32* __restrict__ av, const char* __restrict__ need,
+                            const i64* __restrict__ poff, int2* __restrict__ pairs) {
+  for (i32 C = blockIdx.x * blockDim.x + threadIdx.x; C < n; C += gridDim.x * blockDim.x)
+    for (i64 p = pcp[C]; p < pcp[C + 1]; ++p) {
+      if (need && !need[p]) continue;
+      const i32 R = pri[p];
+      i64 x = acp[R], y = acp[C];
+      const i64 xe = acp[R + 1], ye = acp[C + 1];
+      int2* out = pairs + poff[p];
+      while (x < xe && y < ye) {
+        const i32 kx = ak[x], ky = ak[y];
+        if (kx == ky) *out++ = make_int2(av[x], av[y]);
+        x += kx <= ky;
+        y += ky <= kx;
+      }
+    }
+}
+
+// off[e] (computed entries only, compacted) from the per-pattern-entry offsets
+__global__ void k_gram_compact(i64 ne, const i64* __restrict__ ent, const i64* __restrict__ poff,
+                               i64 total, i64* __restrict__ off) {
+  for (i64 e = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; e <= ne;
+       e += static_cast<i64>(gridDim.x) * blockDim.x)
+    off[e] = e < ne ? poff[ent[e]] : total;
+}
+
+// position of the transposed entry (C, R) of every computed entry (R, C)
+__global__ void k_gram_tpos(i32 n, const i64* __restrict__ pcp, const i32* __restrict__ pri,
+                            const i64* __restrict__ slot, i64* __restrict__ tpos,
+                            int* __restrict__ bad) {
+  for (i32 C = blockIdx.x * blockDim.x + threadIdx.x; C < n; C += gridDim.x * blockDim.x)
+    for (i64 p = pcp[C]; p < pcp[C + 1]; ++p) {
+      const i64 e = slot ? slot[p] : p;
+      if (e < 0) continue;
+      const i32 R = pri[p];
+      i64 lo = pcp[R], hi = pcp[R + 1];
+      while (lo < hi) {
+        const i64 mid = (lo + hi) >> 1;
+        if (pri[mid] < C) lo = mid + 1; else hi = mid;
+      }
+      if (lo < pcp[R + 1] && pri[lo] == C) tpos[e] = lo;
+      else *bad = 1;
+    }
+}
+
 int grid_of(i64 n) {
   return static_cast<int>(std::max<i64>(1, std::min<i64>((n + 255) / 256, 148 * 16)));
 }
@@ -85,77 +160,89 @@ GramPlan::GramPlan(i32 n, const i64* pcp, const i32* pri, i32 m, const i64* arp,
       }
   }
   require(na_ < (1ll << 31), kContract, "gram: operator nnz exceeds int32 value indices");
-  // product map over the computed entries: count the shared rows of every
-  // pattern entry, prefix-sum, then fill — both merge passes run over column
-  // ranges on the host threads (the map of config 4's S Sᵀ has 2e8 pairs, the
-  // config-5 shapes' 2e9)
+  // product map over the computed entries, built on the device: count the
+  // shared rows of every pattern entry, exclusive scan, fill (config 4's S Sᵀ
+  // map has 2e8 pairs, the config-5 shapes' 2e9 — seconds to a minute of host
+  // merging plus a pageable upload otherwise)
   const i64 npat = pcp[n];
-  std::vector<i32> cnt(static_cast<size_t>(npat), 0);
-  std::vector<i64> cov(parallel_threads(n), 0);
-  parallel_ranges(n, [&](int64_t c0, int64_t c1, int t) {
-    i64 covered_t = 0;
-    for (i32 C = static_cast<i32>(c0); C < static_cast<i32>(c1); ++C)
-      for (i64 p = pcp[C]; p < pcp[C + 1]; ++p) {
-        const i32 R = pri[p];
-        i64 x = acp[R], xe = acp[R + 1], y = acp[C], ye = acp[C + 1];
-        i32 c = 0;
-        while (x < xe && y < ye) {
-          if (ak[x] < ak[y]) {
-            ++x;
-          } else if (ak[y] < ak[x]) {
-            ++y;
-          } else {
-            ++c;
-            ++x;
-            ++y;
-          }
-        }
-        cnt[p] = c;
-        covered_t += c;
-      }
-    cov[t] = covered_t;
-  });
-  i64 covered = 0;
-  for (i64 c : cov) covered += c;
-  std::vector<i64> ent, off(1, 0), tpos;
-  std::vector<i64> slot(static_cast<size_t>(npat), -1);  // pattern entry → computed-entry index
-  for (i64 p = 0; p < npat; ++p) {
-    if (need && !(*need)[p]) continue;
-    slot[p] = static_cast<i64>(off.size()) - 1;
-    if (need) ent.push_back(p);
-    off.push_back(off.back() + cnt[p]);
+  DevBuf<i64> d_pcp, d_acp, d_cnt, d_poff, d_slot;
+  DevBuf<i32> d_pri, d_ak, d_av;
+  DevBuf<char> d_need;
+  DevBuf<unsigned long long> d_cov;
+  DevBuf<int> d_bad;
+  d_pcp.alloc(static_cast<size_t>(n) + 1);
+  d_pri.alloc(static_cast<size_t>(std::max<i64>(npat, 1)));
+  cuda_check(cudaMemcpyAsync(d_pcp.p, pcp, (static_cast<size_t>(n) + 1) * sizeof(i64),
+                             cudaMemcpyHostToDevice, stream), "copy pattern");
+  if (npat)
+    cuda_check(cudaMemcpyAsync(d_pri.p, pri, static_cast<size_t>(npat) * sizeof(i32),
+                               cudaMemcpyHostToDevice, stream), "copy pattern");
+  d_acp.upload(acp, stream);
+  d_ak.upload(ak, stream);
+  d_av.upload(av, stream);
+  if (need) d_need.upload(*need, stream);
+  cuda_check(cudaStreamSynchronize(stream), "gram plan inputs");
+  d_cnt.alloc(static_cast<size_t>(npat) + 1);
+  d_poff.alloc(static_cast<size_t>(npat) + 1);
+  d_cov.alloc(1);
+  cuda_check(cudaMemsetAsync(d_cov.p, 0, sizeof(unsigned long long), stream), "memset");
+  cuda_check(cudaMemsetAsync(d_cnt.p + npat, 0, sizeof(i64), stream), "memset");
+  const int gc = grid_of(n);
+  k_gram_count<<<gc, 256, 0, stream>>>(n, d_pcp.p, d_pri.p, d_acp.p, d_ak.p,
+                                       need ? d_need.p : nullptr, d_cnt.p, d_cov.p);
+  {
+    size_t tmp_bytes = 0;
+    cuda_check(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, d_cnt.p, d_poff.p, npat + 1, stream),
+               "scan size");
+    DevBuf<char> tmp;
+    tmp.alloc(tmp_bytes + 1);
+    cuda_check(cub::DeviceScan::ExclusiveSum(tmp.p, tmp_bytes, d_cnt.p, d_poff.p, npat + 1, stream),
+               "scan");
+    cuda_check(cudaStreamSynchronize(stream), "gram plan scan");
   }
-  const i64 npr = off.back();
-  std::unique_ptr<int2[]> pr(new int2[std::max<i64>(npr, 1)]);  // uninitialised: filled below
-  if (base_transpose) tpos.assign(off.size() - 1, 0);
-  parallel_ranges(n, [&](int64_t c0, int64_t c1, int) {
-    for (i32 C = static_cast<i32>(c0); C < static_cast<i32>(c1); ++C)
-      for (i64 p = pcp[C]; p < pcp[C + 1]; ++p) {
-        const i64 e = slot[p];
-        if (e < 0) continue;
-        const i32 R = pri[p];
-        i64 x = acp[R], xe = acp[R + 1], y = acp[C], ye = acp[C + 1];
-        int2* out = pr.get() + off[e];
-        while (x < xe && y < ye) {
-          if (ak[x] < ak[y]) {
-            ++x;
-          } else if (ak[y] < ak[x]) {
-            ++y;
-          } else {
-            *out++ = make_int2(av[x], av[y]);
-            ++x;
-            ++y;
-          }
-        }
-        if (base_transpose) {  // position of (C, R): binary search in column R
-          const i32* b0 = pri + pcp[R];
-          const i32* b1 = pri + pcp[R + 1];
-          const i32* f = std::lower_bound(b0, b1, C);
-          require(f != b1 && *f == C, kStructural, "gram: pattern is not symmetric");
-          tpos[e] = pcp[R] + (f - b0);
-        }
-      }
-  });
+  i64 npr = 0;
+  unsigned long long covered_u = 0;
+  cuda_check(cudaMemcpyAsync(&npr, d_poff.p + npat, sizeof(i64), cudaMemcpyDeviceToHost, stream), "copy");
+  cuda_check(cudaMemcpyAsync(&covered_u, d_cov.p, sizeof(covered_u), cudaMemcpyDeviceToHost, stream),
+             "copy");
+  cuda_check(cudaStreamSynchronize(stream), "gram plan counts");
+  const i64 covered = static_cast<i64>(covered_u);
+  pairs_.alloc(static_cast<size_t>(std::max<i64>(npr, 1)));
+  k_gram_fill<<<gc, 256, 0, stream>>>(n, d_pcp.p, d_pri.p, d_acp.p, d_ak.p, d_av.p,
+                                      need ? d_need.p : nullptr, d_poff.p, pairs_.p);
+  // computed-entry list (host: a pass over the mask) and compacted offsets
+  std::vector<i64> ent;
+  if (need) {
+    for (i64 p = 0; p < npat; ++p)
+      if ((*need)[p]) ent.push_back(p);
+    ent_.upload(ent, stream);
+    ne_ = static_cast<i64>(ent.size());
+    off_.alloc(static_cast<size_t>(ne_) + 1);
+    k_gram_compact<<<grid_of(ne_ + 1), 256, 0, stream>>>(ne_, ent_.p, d_poff.p, npr, off_.p);
+  } else {
+    ne_ = np_;
+    off_.alloc(static_cast<size_t>(npat) + 1);
+    cuda_check(cudaMemcpyAsync(off_.p, d_poff.p, (static_cast<size_t>(npat) + 1) * sizeof(i64),
+                               cudaMemcpyDeviceToDevice, stream),
+               "copy offsets");
+  }
+  std::vector<i64> slot;
+  if (base_transpose) {
+    tpos_.alloc(static_cast<size_t>(std::max<i64>(ne_, 1)));
+    d_bad.alloc(1);
+    cuda_check(cudaMemsetAsync(d_bad.p, 0, sizeof(int), stream), "memset");
+    if (need) {  // pattern entry → computed-entry index
+      slot.assign(static_cast<size_t>(npat), -1);
+      for (i64 e = 0; e < ne_; ++e) slot[ent[e]] = e;
+      d_slot.upload(slot, stream);
+    }
+    k_gram_tpos<<<gc, 256, 0, stream>>>(n, d_pcp.p, d_pri.p, need ? d_slot.p : nullptr, tpos_.p,
+                                        d_bad.p);
+    int bad = 0;
+    cuda_check(cudaMemcpyAsync(&bad, d_bad.p, sizeof(int), cudaMemcpyDeviceToHost, stream), "copy");
+    cuda_check(cudaStreamSynchronize(stream), "gram plan transpose map");
+    require(bad == 0, kStructural, "gram: pattern is not symmetric");
+  }
   // every product A_kR A_kC must have a home in the pattern
   i64 total = 0;
   for (i32 k = 0; k < m; ++k) total += (arp[k + 1] - arp[k]) * (arp[k + 1] - arp[k]);
@@ -163,21 +250,9 @@ GramPlan::GramPlan(i32 n, const i64* pcp, const i32* pri, i32 m, const i64* arp,
           "gram: pattern does not contain the operator's product pattern (" +
               std::to_string(covered) + " of " + std::to_string(total) + " products)");
   npairs_ = npr;
-  off_.upload(off, stream);
-  pairs_.alloc(static_cast<size_t>(std::max<i64>(npr, 1)));
-  if (npr)
-    cuda_check(cudaMemcpyAsync(pairs_.p, pr.get(), static_cast<size_t>(npr) * sizeof(int2),
-                               cudaMemcpyHostToDevice, stream),
-               "gram pairs upload");
   arow_.upload(arow, stream);
   wa_.alloc(std::max<i64>(na_, 1));
-  if (base_transpose) tpos_.upload(tpos, stream);
-  if (need) {
-    ent_.upload(ent, stream);
-    ne_ = static_cast<i64>(ent.size());
-  } else {
-    ne_ = np_;
-  }
+  cuda_check(cudaGetLastError(), "gram plan kernels");
   cuda_check(cudaStreamSynchronize(stream), "gram plan upload");
 }
 
