@@ -318,6 +318,9 @@ def main():
                     help="N>1: one posterior, its factorization / solves / selected inversion "
                          "partitioned along the top ND separators across the ranks (NCCL), "
                          "strong scaling; default: one independent posterior per GPU")
+    ap.add_argument("--torch-exchange", action="store_true",
+                    help="--partition: move the messages through the torch.distributed callback "
+                         "instead of the library's own NCCL calls")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -386,9 +389,9 @@ def main():
         gn_iters = 10
     t0 = time.perf_counter()
     if partitioned:
-        from paper_2503_08343_b200.partition import TorchExchange
+        from paper_2503_08343_b200.partition import NcclExchange, TorchExchange
         post = SpaceTimePosterior(spec, GaussNewtonConfig(max_iters=gn_iters),
-                                  partition=(world, rank, TorchExchange()))
+                                  partition=(world, rank, TorchExchange() if args.torch_exchange else NcclExchange()))
     else:
         post = SpaceTimePosterior(spec, GaussNewtonConfig(max_iters=gn_iters))
     host_setup_s = time.perf_counter() - t0

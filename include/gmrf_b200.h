@@ -199,6 +199,20 @@ typedef struct {
 typedef int (*gmrf_exchange_fn)(void* ctx, const gmrf_msg_t* msgs, int32_t count,
                                 void* cuda_stream);
 
+/* Native NCCL transport (csrc/nccl_exchange.cpp): gmrf_nccl_exchange() is a
+ * gmrf_exchange_fn that posts the messages on the factor's stream with
+ * ncclSend / ncclRecv (one group per exchange point) and ncclAllReduce; pass it
+ * with ctx = the communicator from gmrf_nccl_comm_create. Rank 0 obtains the
+ * 128-byte unique id (gmrf_nccl_unique_id) and hands it to the other ranks by
+ * any means (torch.distributed broadcast, MPI, a file); every rank then calls
+ * gmrf_nccl_comm_create with the GPU it will use already current. NCCL is
+ * loaded at run time (the process's libnccl.so.2, or $GMRF_NCCL_LIB). */
+int gmrf_nccl_unique_id(uint8_t* id128);
+int gmrf_nccl_comm_create(int32_t nranks, int32_t rank, const uint8_t* id128, void** comm);
+void gmrf_nccl_comm_destroy(void* comm);
+gmrf_exchange_fn gmrf_nccl_exchange(void);
+const char* gmrf_nccl_last_error(void);
+
 /* Owner rank of each supernode (ns entries) for nranks ranks. Host only. */
 int gmrf_partition_owners(const gmrf_symbolic_t* s, int32_t nranks, int32_t* owner);
 /* The full cross-edge message schedule for an owner map (host only, tests):

@@ -146,6 +146,11 @@ SIGNATURES = {
                                                  C.POINTER(vp)]),
     "gmrf_spacetime_create_partitioned": (C.c_int, [C.POINTER(SpaceTimeConfig), C.c_int32,
                                                     C.c_int32, EXCHANGE_FN, vp, C.POINTER(vp)]),
+    "gmrf_nccl_unique_id": (C.c_int, [C.POINTER(C.c_uint8)]),
+    "gmrf_nccl_comm_create": (C.c_int, [C.c_int32, C.c_int32, C.POINTER(C.c_uint8), C.POINTER(vp)]),
+    "gmrf_nccl_comm_destroy": (None, [vp]),
+    "gmrf_nccl_exchange": (EXCHANGE_FN, []),
+    "gmrf_nccl_last_error": (C.c_char_p, []),
     "gmrf_spacetime_create": (C.c_int, [C.POINTER(SpaceTimeConfig), C.POINTER(vp)]),
     "gmrf_spacetime_run": (C.c_int, [vp, f64p, C.c_int32, f64p, f64p, C.POINTER(GnIter),
                                      C.c_int32, i32p, i32p]),

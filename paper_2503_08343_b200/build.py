@@ -55,7 +55,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
             f.result()
     if force or _stale(LIB, objs):
         _run(["nvcc", "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB, *objs,
-              METIS, "-lcudart", "-lm"])
+              METIS, "-lcudart", "-lm", "-ldl"])
     return LIB
 
 

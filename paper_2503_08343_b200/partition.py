@@ -20,6 +20,9 @@ The library calls back into an ``Exchange`` here for the transport:
   (backend ``nccl``) the messages are device buffers enqueued on the factor's
   stream: NVLink/NVSwitch between the B200s of one box. On CPU (``gloo``) the
   same code moves host buffers (tests).
+* ``NcclExchange`` — the native transport: ``ncclSend`` / ``ncclRecv`` /
+  ``ncclAllReduce`` posted by the library itself on the factor's stream
+  (csrc/nccl_exchange.cpp), no Python at the exchange points.
 * ``LoopbackGroup`` — several ranks in one process on one GPU (tests): each
   rank runs in its own thread, messages are device-to-device copies matched by
   (src, dst, phase, child). Host-side waits only; no kernel waits on another
@@ -166,6 +169,51 @@ class TorchExchange(Exchange):
             body()
 
 
+class NcclExchange:
+    """Native NCCL transport (csrc/nccl_exchange.cpp): the library posts
+    ncclSend / ncclRecv / ncclAllReduce on the factor's stream itself — no Python
+    at the exchange points. One communicator per process over ``nranks`` ranks;
+    rank 0's unique id is broadcast with torch.distributed (any backend), or pass
+    ``unique_id`` (128 bytes) obtained otherwise. The current CUDA device must be
+    the one this rank uses."""
+
+    def __init__(self, nranks=None, rank=None, unique_id=None, group=None):
+        lib = _capi.load()
+        if nranks is None or rank is None:
+            import torch.distributed as dist
+            nranks, rank = dist.get_world_size(group), dist.get_rank(group)
+        if unique_id is None:
+            uid = (C.c_uint8 * 128)()
+            if rank == 0:
+                _check_nccl(lib, lib.gmrf_nccl_unique_id(uid))
+            if nranks > 1:
+                import torch.distributed as dist
+                box = [bytes(uid)]
+                dist.broadcast_object_list(box, src=0, group=group)
+                uid = (C.c_uint8 * 128).from_buffer_copy(box[0])
+        else:
+            uid = (C.c_uint8 * 128).from_buffer_copy(bytes(unique_id))
+        comm = C.c_void_p()
+        _check_nccl(lib, lib.gmrf_nccl_comm_create(int(nranks), int(rank), uid, C.byref(comm)))
+        self.ctx = comm
+        self.fn = lib.gmrf_nccl_exchange()
+        self.nranks, self.rank = int(nranks), int(rank)
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            _capi.load().gmrf_nccl_comm_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        self.close()
+
+
+def _check_nccl(lib, rc):
+    if rc != 0:
+        from .core import DeviceError
+        raise DeviceError(lib.gmrf_nccl_last_error().decode() or "NCCL transport failed")
+
+
 class LoopbackGroup:
     """``nranks`` ranks of a partitioned factor inside one process on one GPU
     (tests): ``exchange(rank)`` gives each rank's transport; run each rank's
@@ -280,7 +328,8 @@ class PartitionedFactor(CholeskyFactor):
         o = None if owner is None else np.ascontiguousarray(owner, np.int32)
         h = C.c_void_p()
         _check(_capi.load().gmrf_factor_create_partitioned(sym._h, self.nranks, self.rank,
-                                                           ptr(o, i32p), exchange.fn, None,
+                                                           ptr(o, i32p), exchange.fn,
+                                                           getattr(exchange, "ctx", None),
                                                            C.byref(h)))
         self._h = h
         self.perm = sym.perm

@@ -168,7 +168,8 @@ class SpaceTimePosterior:
             nranks, rank, exchange = partition
             self._exchange = exchange  # the C callback must outlive the handle
             _check(lib.gmrf_spacetime_create_partitioned(C.byref(c), nranks, rank, exchange.fn,
-                                                         None, C.byref(h)))
+                                                         getattr(exchange, "ctx", None),
+                                                         C.byref(h)))
         self._h = h
         self.n = self.info().n
 
