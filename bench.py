@@ -103,7 +103,25 @@ def reference_sample(n_el=SAMPLE[0], n_t=SAMPLE[1]):
         "stages_sample_s": {"numeric_x%d" % n_fact: fact, "takahashi": taka, "amd_symbolic": sym,
                             "rest": rest},
         "cpu": cpu_model(),
+        **measured_full_reference(),
     }
+
+
+def measured_full_reference():
+    """The reference's own stage timings for the FULL config-4 workload, when the
+    full-size fixture is committed (tests/golden/c4_burgers_full.npz, written by
+    make_golden_full.py in the build container: single core, other jobs running
+    beside it): a measured anchor for the extrapolation above, not timed on this box."""
+    try:
+        import numpy as np
+        z = np.load(os.path.join(ROOT, "tests", "golden", "c4_burgers_full.npz"))
+        t = json.loads(str(z["ref_times_json"]))
+        return {"reference_full_run": {
+            "stages_s": t, "wall_s": t.get("t_wall"),
+            "where": "build container, 1 core (tests/golden/make_golden_full.py c4), n=1e6, "
+                     "10 GN steps + Laplace + Takahashi; not this box"}}
+    except Exception:  # noqa: BLE001 - fixture absent: no anchor
+        return {}
 
 
 def cpu_model():

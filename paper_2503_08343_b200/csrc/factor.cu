@@ -1207,7 +1207,7 @@ void DeviceFactor::enqueue_levels(cudaStream_t sa, cudaStream_t sb, bool la, boo
       cuda_check(cudaStreamWaitEvent(sa, ev_rest_[li - lv.dwait], 0), "wait");
     mark(sa, 2);
     if (lv.gmn && !(whatif & 4)) {
-      pf.run(sa, pf.tag("factor.gemm_dmma", lvl), lv.gm_flops, 0.0, [&] {
+      pf.run(sa, pf.tag(lv.gm32 ? "factor.gemm_next" : "factor.gemm_dmma", lvl), lv.gm_flops, 0.0, [&] {
         if (lv.gm32)
           k_gemm_next<<<static_cast<unsigned>(lv.gmn), 128, 0, sa>>>(gemm_.p + lv.gm0);
         else
