@@ -22,17 +22,20 @@ constexpr int sel_diag_smem_bytes() {
 
 template <int W>
 __global__ void __launch_bounds__(kTrsmRows) k_sel_trsm_w(const SelChunk* __restrict__ tasks) {
-  __shared__ __align__(16) double Lr[W * W];  // Lr[j*W + k] = L_jk (row j of L_JJ, k < j)
+  constexpr int LP = W + 2;  // even pitch: rows stay 16-byte aligned for the double2 reads
+  __shared__ __align__(16) double Lr[W * LP];  // Lr[j*LP + k] = L_jk (row j of L_JJ, k < j)
   __shared__ double dg[W], rd[W];
   const SelChunk& t = tasks[blockIdx.x];
   const int w = t.w, ld = t.ld, tid = threadIdx.x;
   const double* Lk = t.l + t.c0 + static_cast<int64_t>(t.c0) * ld;
   // fully unrolled (compile-time trip count): every thread's loads are in flight
-  // together instead of one memory round trip per element
+  // together instead of one memory round trip per element; consecutive threads
+  // read consecutive rows of a column (coalesced), the transpose happens in the
+  // shared-memory write
 #pragma unroll
   for (int idx = tid; idx < W * W; idx += kTrsmRows) {
-    const int j = idx / W, k = idx % W;  // consecutive threads: consecutive k (row j)
-    Lr[idx] = (k < j && j < w) ? Lk[j + static_cast<int64_t>(k) * ld] : 0.0;
+    const int j = idx % W, k = idx / W;
+    Lr[j * LP + k] = (k < j && j < w) ? Lk[j + static_cast<int64_t>(k) * ld] : 0.0;
   }
   if (tid < W) {
     dg[tid] = tid < w ? Lk[tid + static_cast<int64_t>(tid) * ld] : 1.0;
@@ -51,7 +54,7 @@ __global__ void __launch_bounds__(kTrsmRows) k_sel_trsm_w(const SelChunk* __rest
   for (int j = W - 1; j >= 0; --j) {
     const double x = div_rn(b[j], dg[j], rd[j]);
     b[j] = x;
-    const double* lj = Lr + j * W;
+    const double* lj = Lr + j * LP;
 #pragma unroll
     for (int k = 0; k + 1 < j; k += 2) {
       const double2 v = *reinterpret_cast<const double2*>(lj + k);
