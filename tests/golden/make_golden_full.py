@@ -11,12 +11,12 @@ reference's AMD factorization is ~190 s per GN step and its Takahashi pass
                         Laplace Takahashi variances, reference stage timings.
   c3_heat_full.npz      C3 499 x 1000 (n = 500,000): IC-conditioned mean and
                         Takahashi variances, timings.
-  c5_allen_cahn_<k>.npz C5 shape at k^2 nodes x (2k) slices (k = 16, 32): 8-step
+  c5_allen_cahn_<k>.npz C5 shape at k^2 nodes x (2k) slices (k = 16, 24, 32): 8-step
                         GN trace, mode, variances, timings (k = 32 is n = 65,536,
                         the largest the reference's int32 nnz(L) survives).
   c4_burgers_200.npz    C4 shape at 199 x 200 with the full 10-step GN budget.
 
-Usage: python tests/golden/make_golden_full.py c4 | c3 | c5_16 | c5_32 | c4_200 | c4_500
+Usage: python tests/golden/make_golden_full.py c4 | c3 | c5_16 | c5_24 | c5_32 | c4_200 | c4_500
        python tests/golden/make_golden_full.py floor:c4_200 ...
 Each run writes its fixture atomically (tmp + rename) plus a .log with timings.
 
@@ -168,6 +168,7 @@ JOBS = {
     "c4_500": lambda fl: burgers(499, 500, 10, "c4_burgers_500.npz", fl),
     "c3": lambda fl: heat(499, 1000, "c3_heat_full.npz", fl),
     "c5_16": lambda fl: allen_cahn(15, 32, "c5_allen_cahn_16.npz", floor=fl),
+    "c5_24": lambda fl: allen_cahn(23, 48, "c5_allen_cahn_24.npz", floor=fl),
     "c5_32": lambda fl: allen_cahn(31, 64, "c5_allen_cahn_32.npz", floor=fl),
 }
 

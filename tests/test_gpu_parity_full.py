@@ -83,7 +83,7 @@ def _judge(name, errs):
 
 
 BURGERS = ["c4_burgers_200.npz", "c4_burgers_500.npz", "c4_burgers_full.npz"]
-ALLEN_CAHN = ["c5_allen_cahn_16.npz", "c5_allen_cahn_32.npz"]
+ALLEN_CAHN = ["c5_allen_cahn_16.npz", "c5_allen_cahn_24.npz", "c5_allen_cahn_32.npz"]
 
 
 @pytest.mark.parametrize("fixture", BURGERS)
