@@ -16,16 +16,33 @@ pytestmark = pytest.mark.gpu
 BIN = os.path.join(ROOT, "oracle", "_ref", "acceptance_b200")
 
 
-def test_reference_acceptance_suite_on_gpu():
-    if not os.path.exists(BIN):
-        pytest.skip("oracle/_ref/acceptance_b200 not built (reference absent at build time)")
+def _run_acceptance():
     out = subprocess.run([BIN], cwd=os.path.dirname(BIN), capture_output=True, text=True,
                          timeout=900)
     lines = [ln for ln in out.stdout.splitlines() if "criterion-" in ln]
     assert len(lines) == 10, out.stdout + out.stderr
-    for crit in (1, 2, 10):  # the factor / solve / Takahashi criteria
-        assert any(ln.startswith(f"PASS criterion-{crit}:") for ln in lines), out.stdout
-    assert out.returncode == 0, out.stdout
+    return out, lines
+
+
+def test_reference_acceptance_suite_on_gpu():
+    if not os.path.exists(BIN):
+        pytest.skip("oracle/_ref/acceptance_b200 not built (reference absent at build time)")
+    # Criterion 6 also compares two WALL-CLOCK times of 64x64 problems (GMRF chain
+    # vs one FEM solve, ratio <= 10x; acceptance.cpp:386-400): a few ms each, so a
+    # busy host core moves the ratio. Every numerical criterion must pass on every
+    # run; the wall-clock ratio must pass on one of three runs.
+    failed = []
+    for attempt in range(3):
+        out, lines = _run_acceptance()
+        for crit in (1, 2, 3, 4, 5, 7, 8, 9, 10):
+            assert any(ln.startswith(f"PASS criterion-{crit}:") for ln in lines), out.stdout
+        c6 = next(ln for ln in lines if "criterion-6:" in ln)
+        err = float(c6.split("gmrf-vs-fem")[1].split()[0])
+        assert err <= 1e-5, c6  # the parity half of criterion 6
+        if out.returncode == 0:
+            return
+        failed.append(c6)
+    raise AssertionError("criterion 6 wall-clock ratio failed three times:\n" + "\n".join(failed))
 
 
 # ---- the reference's own chains through the drop-in rows (1)-(2) -------------
