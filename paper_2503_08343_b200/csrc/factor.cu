@@ -140,6 +140,7 @@ DeviceFactor::DeviceFactor(std::shared_ptr<const Symbolic> sym, cudaStream_t str
   if (const char* e = std::getenv("GMRF_EA_SPLIT")) ea_split_ = e[0] != '0';
   if (const char* e = std::getenv("GMRF_WIDE_K")) wide_min_k_ = atoi(e);
   if (const char* e = std::getenv("GMRF_GEMM_NEXT")) gemm_next_ = e[0] != '0';
+  if (const char* e = std::getenv("GMRF_SEL_BLOCK")) sel_block_max_w_ = atoi(e);  // 0: chunk chain only
   if (const char* e = std::getenv("GMRF_NEXT_TILES")) next_max_tiles_ = atoll(e);
   if (const char* e = std::getenv("GMRF_WIDE_R")) wide_min_r_ = atoi(e);
   if (const char* e = std::getenv("GMRF_INC_B")) inc_b_ = std::max(1, atoi(e));
@@ -765,15 +766,10 @@ void DeviceFactor::build_selinv_plan() {
   std::vector<int> lvl0, last;
   int nlev = 0;
   chunk_levels(s, lvl0, last, nlev, 0);
-  // per-level staging of Y (nbelow × w) and W / Z (w × w) of every chunk
-  std::vector<int64_t> yoff(nlev, 0);
-  for (int k = 0; k < s.ns; ++k) {
-    if (!mine(k)) continue;
-    for (int c = 0; c < nchunks(s.w(k)); ++c) {
-      const int c0 = c * kNB, wk = std::min(kNB, s.w(k) - c0);
-      yoff[lvl0[k] + c] += static_cast<int64_t>(s.rows(k) - c0) * wk;  // (nbelow + wk) · wk
-    }
-  }
+  // per-level staging: Y (nbelow × w) and W / Z (w × w) of every chunk; W = L_JJ⁻¹
+  // (w × w) and Gn (r × w) of every blocked supernode at its top chunk level
+  std::vector<int64_t> yoff = selinv_staging(s, part_ ? &owner_ : nullptr, rank_, sel_block_max_w_);
+  yoff.resize(std::max<size_t>(yoff.size(), nlev), 0);
   int64_t ymax = 1;
   for (int64_t v : yoff) ymax = std::max(ymax, v);
   ystage_.alloc(ymax);
@@ -786,6 +782,144 @@ void DeviceFactor::build_selinv_plan() {
   double* L = L_.p;
   double* U = U_.p;
   double* S = sig();
+  // ---- blocked selected inversion of one supernode (selinv.cuh): stage ids
+  // order the launches of a level; supernodes of one level share the stages
+  constexpr int kStG = 1000, kStY = 1001, kStJ = 1002, kStM = 1003;
+  auto blocked_tasks = [&](int w, int r, const double* Lk, double* Sk, const double* Uk,
+                           double* Wv, double* Gn, const double* rdk, auto&& gem, auto&& chk) {
+    const int rows = w + r;
+    const int64_t lw = w, lr = std::max(r, 1);
+    for (int c0 = 0; c0 < w; c0 += kNB) {  // inverses of the diagonal blocks
+      SelChunk t{};
+      t.l = Lk;
+      t.sig = Sk;
+      t.ld = rows;
+      t.c0 = c0;
+      t.w = std::min(kNB, w - c0);
+      t.wsn = w;
+      t.rd = rdk + c0;
+      t.dst = Wv + c0 + c0 * lw;
+      t.ldd = w;
+      chk(0, t);
+    }
+    int depth = 0;
+    for (int bs = kNB; bs < w; bs *= 2, ++depth) {
+      // [A 0; B C]⁻¹ = [A⁻¹ 0; −C⁻¹ B A⁻¹ C⁻¹]: Tᵀ = A⁻ᵀ Bᵀ goes to the (unused)
+      // mirror block above the diagonal, then X = −C⁻¹ T over B's place in W
+      for (int a0 = 0; a0 + bs < w; a0 += 2 * bs) {
+        const int a1 = a0 + bs, c1 = std::min(a0 + 2 * bs, w), mb = c1 - a1;
+        for (int i0 = 0; i0 < bs; i0 += kTile)
+          for (int j0 = 0; j0 < mb; j0 += kTile) {
+            GemmTask g{};
+            g.c = Wv + (a0 + i0) + (a1 + j0) * lw;
+            g.ldc = w;
+            g.m = std::min(kTile, bs - i0);
+            g.n = std::min(kTile, mb - j0);
+            g.a[0] = Wv + (a0 + i0) + (a0 + i0) * lw;
+            g.lda[0] = w;
+            g.b[0] = Lk + (a1 + j0) + static_cast<int64_t>(a0 + i0) * rows;
+            g.ldb[0] = rows;
+            g.k[0] = bs - i0;
+            g.flags = 1 | 2;
+            g.alpha = 1.0;
+            gem(1 + 2 * depth, g);
+          }
+        for (int i0 = 0; i0 < mb; i0 += kTile)
+          for (int j0 = 0; j0 < bs; j0 += kTile) {
+            GemmTask g{};
+            g.c = Wv + (a1 + i0) + (a0 + j0) * lw;
+            g.ldc = w;
+            g.m = std::min(kTile, mb - i0);
+            g.n = std::min(kTile, bs - j0);
+            g.a[0] = Wv + (a1 + i0) + a1 * lw;
+            g.lda[0] = w;
+            g.b[0] = Wv + (a0 + j0) + a1 * lw;
+            g.ldb[0] = w;
+            g.k[0] = std::min(i0 + kTile, mb);
+            g.flags = 2;
+            g.alpha = -1.0;
+            gem(2 + 2 * depth, g);
+          }
+      }
+    }
+    for (int j0 = 0; j0 < w; j0 += kTile) {
+      const int nn = std::min(kTile, w - j0);
+      for (int i0 = 0; i0 < r; i0 += kTile) {
+        const int mm = std::min(kTile, r - i0);
+        GemmTask g{};  // Gn = −L_RJ W
+        g.c = Gn + i0 + j0 * lr;
+        g.ldc = static_cast<int>(lr);
+        g.m = mm;
+        g.n = nn;
+        g.a[0] = Lk + (w + i0) + static_cast<int64_t>(j0) * rows;
+        g.lda[0] = rows;
+        g.b[0] = Wv + j0 + j0 * lw;
+        g.ldb[0] = w;
+        g.k[0] = w - j0;
+        g.alpha = -1.0;
+        gem(kStG, g);
+        GemmTask y{};  // Σ_RJ = Σ_RR Gn
+        y.c = Sk + (w + i0) + static_cast<int64_t>(j0) * rows;
+        y.ldc = rows;
+        y.m = mm;
+        y.n = nn;
+        y.a[0] = Uk + i0;
+        y.lda[0] = static_cast<int>(lr);
+        y.b[0] = Gn + j0 * lr;
+        y.ldb[0] = static_cast<int>(lr);
+        y.k[0] = r;
+        y.alpha = 1.0;
+        gem(kStY, y);
+      }
+      for (int i0 = j0; i0 < w; i0 += kTile) {
+        const int mm = std::min(kTile, w - i0);
+        GemmTask g{};  // Σ_JJ = Wᵀ W + Gnᵀ Σ_RJ (lower tiles, mirrored afterwards)
+        g.c = Sk + i0 + static_cast<int64_t>(j0) * rows;
+        g.ldc = rows;
+        g.m = mm;
+        g.n = nn;
+        g.a[0] = Wv + i0 + i0 * lw;
+        g.lda[0] = w;
+        g.b[0] = Wv + i0 + j0 * lw;
+        g.ldb[0] = w;
+        g.k[0] = w - i0;
+        g.flags = 1;
+        if (r > 0) {
+          g.a[1] = Gn + i0 * lr;
+          g.lda[1] = static_cast<int>(lr);
+          g.b[1] = Sk + w + static_cast<int64_t>(j0) * rows;
+          g.ldb[1] = rows;
+          g.k[1] = r;
+          g.flags |= 1 << 2;
+        }
+        g.alpha = 1.0;
+        gem(kStJ, g);
+        SelChunk t{};
+        t.sig = Sk;
+        t.ld = rows;
+        t.c0 = i0;
+        t.tile = j0;
+        t.w = mm;
+        t.wsn = nn;
+        chk(kStM, t);
+      }
+    }
+  };
+  struct StageBuild {
+    std::vector<GemmTask> g;
+    std::vector<SelChunk> c;
+    int64_t tiles_all = 0;  // GEMM tiles of every rank (split-K decided on these)
+    double flops = 0.0;
+  };
+  std::vector<std::map<int, StageBuild>> bsb(nlev);
+  for (int k = 0; k < s.ns; ++k) {  // tile counts over all ranks' supernodes
+    const int w = s.w(k);
+    if (!sel_blocked(w, sel_block_max_w_)) continue;
+    auto& lv = bsb[lvl0[k] + nchunks(w) - 1];
+    blocked_tasks(w, s.rows(k) - w, L, L, L, L, L, L,
+                  [&](int st, const GemmTask&) { ++lv[st].tiles_all; },
+                  [&](int, const SelChunk&) {});
+  }
   for (int k = 0; k < s.ns; ++k) {
     const int w = s.w(k), rows = s.rows(k), r = rows - w;
     const int par = s.sn_parent[k];
@@ -802,6 +936,27 @@ void DeviceFactor::build_selinv_plan() {
     double* Sk = S + lptr_h_[k];
     double* Uk = U + uptrs_h_[k];
     const int nch = nchunks(w);
+    if (sel_blocked(w, sel_block_max_w_)) {
+      const int lv = lvl0[k] + nch - 1;
+      if (r > 0 && mine(par)) {  // else received from the parent's rank
+        for (int b = 0; b < r; ++b) ga[lv].push_back({k, b});
+        ga_b[lv] += 16.0 * r * r;
+      }
+      double* Wv = ystage_.p + yoff[lv];
+      double* Gn = Wv + static_cast<int64_t>(w) * w;
+      yoff[lv] += static_cast<int64_t>(w) * w + static_cast<int64_t>(r) * w;
+      auto& lvb = bsb[lv];
+      blocked_tasks(w, r, Lk, Sk, Uk, Wv, Gn, rdiag_.p + s.sn_first[k],
+                    [&](int st, const GemmTask& g) {
+                      lvb[st].g.push_back(g);
+                      lvb[st].flops += 2.0 * g.m * g.n * (static_cast<double>(g.k[0]) + g.k[1]);
+                    },
+                    [&](int st, const SelChunk& c) {
+                      lvb[st].c.push_back(c);
+                      if (st == 0) lvb[st].flops += static_cast<double>(c.w) * c.w * c.w / 3.0;
+                    });
+      continue;
+    }
     for (int c = nch - 1; c >= 0; --c) {
       const int lv = lvl0[k] + c;
       const int c0 = c * kNB, wk = std::min(kNB, w - c0);
@@ -898,6 +1053,7 @@ void DeviceFactor::build_selinv_plan() {
   std::vector<int64_t> gyt(nlev, 0), gzt(nlev, 0);  // Y / Z tiles of all ranks per level
   for (int k = 0; k < s.ns; ++k) {
     const int w = s.w(k), rows = s.rows(k);
+    if (sel_blocked(w, sel_block_max_w_)) continue;
     for (int c = 0; c < nchunks(w); ++c) {
       const int c0 = c * kNB, wk = std::min(kNB, w - c0);
       gyt[lvl0[k] + c] += (w - c0 - wk + kTile - 1) / kTile + (rows - w + kTile - 1) / kTile;
@@ -911,7 +1067,10 @@ void DeviceFactor::build_selinv_plan() {
   int64_t maxp = 1;
   for (int l = 0; l < nlev; ++l)
     maxp = std::max(maxp, std::max(split_k_parts(yg[l], gyt[l]), split_k_parts(zg[l], gzt[l])));
+  for (int l = 0; l < nlev; ++l)
+    for (auto& [st, b] : bsb[l]) maxp = std::max(maxp, split_k_parts(b.g, b.tiles_all));
   sparts_.alloc(maxp * kTile * kTile);
+  std::vector<SelChunk> blf;
   slev_.assign(nlev, {});
   for (int l = 0; l < nlev; ++l) {
     SLevel& e = slev_[l];
@@ -957,6 +1116,22 @@ void DeviceFactor::build_selinv_plan() {
     e.mi0 = mif.size();
     e.min_ = mi[l].size();
     mif.insert(mif.end(), mi[l].begin(), mi[l].end());
+    for (auto& [st, b] : bsb[l]) {  // std::map: ascending stage id = launch order
+      if (!b.g.empty()) {
+        gs.clear();
+        rs.clear();
+        split_k_level(b.g, gs, rs, sparts_.p, b.tiles_all);
+        e.bst.push_back({0, static_cast<int64_t>(gmf.size()), static_cast<int64_t>(gs.size()),
+                         static_cast<int64_t>(rdf.size()), static_cast<int64_t>(rs.size()), b.flops});
+        gmf.insert(gmf.end(), gs.begin(), gs.end());
+        rdf.insert(rdf.end(), rs.begin(), rs.end());
+      }
+      if (!b.c.empty()) {
+        e.bst.push_back({st == 0 ? 1 : 2, static_cast<int64_t>(blf.size()),
+                         static_cast<int64_t>(b.c.size()), 0, 0, b.flops});
+        blf.insert(blf.end(), b.c.begin(), b.c.end());
+      }
+    }
     e.ga_bytes = ga_b[l];
     e.y_flops = y_f[l];
     e.t_flops = t_f[l];
@@ -969,6 +1144,7 @@ void DeviceFactor::build_selinv_plan() {
   strsm_.upload(trf, stream_);
   sdiag_.upload(dgf, stream_);
   smir_.upload(mif, stream_);
+  sblk_.upload(blf, stream_);
   sx_.assign(nlev, {});
   for (const XEdge& e : sched_)
     if (e.phase == kXSelinv)
@@ -1519,6 +1695,27 @@ void DeviceFactor::selinv(double* diag_out, bool on_device) {
                                                  snparent_.p, sig(), U_.p);
       });
       ++launches_selinv_;
+    }
+    for (const SLevel::BStage& b : e.bst) {
+      if (b.kind == 0) {
+        pf.run(stream_, pf.tag("selinv.gemm_dmma", l), b.flops, 0.0, [&] {
+          launch_gemm(sgemm_.p + b.t0, b.tn, stream_);
+          if (b.rn)
+            k_reduce_parts<<<static_cast<unsigned>(b.rn), 256, 0, stream_>>>(sred_.p + b.r0,
+                                                                             sparts_.p);
+        });
+        launches_selinv_ += 1 + (b.rn > 0);
+      } else if (b.kind == 1) {
+        pf.run(stream_, pf.tag("selinv.diag", l), b.flops, 0.0, [&] {
+          k_tri_inv64<<<static_cast<unsigned>(b.tn), 64, 0, stream_>>>(sblk_.p + b.t0);
+        });
+        ++launches_selinv_;
+      } else {
+        pf.run(stream_, pf.tag("selinv.mirror", l), 0.0, 0.0, [&] {
+          k_sel_mirror_blk<<<static_cast<unsigned>(b.tn), 256, 0, stream_>>>(sblk_.p + b.t0);
+        });
+        ++launches_selinv_;
+      }
     }
     if (e.yn) {
       pf.run(stream_, pf.tag("selinv.gemm_dmma", l), e.y_flops, 0.0, [&] {

@@ -238,6 +238,15 @@ class DeviceFactor {
     int64_t yr0, yrn, zr0, zrn;  // split-K reductions of the Y and Z tiles
     int64_t tb0[3], tbn[3], db0[3], dbn[3];  // TRSM / diag chunks by width bucket 16/32/64
     int64_t mi0, min_;                       // Σ_{P,J} → Σ_{J,P} mirror tiles
+    // blocked selected inversion of the level's multi-chunk supernodes
+    // (selinv.cuh): launches in order; kind 0 = GEMM tiles of sgemm_ (+ split-K
+    // reductions of sred_), 1 = diagonal-block inverses, 2 = Σ_JJ mirror tiles (sblk_)
+    struct BStage {
+      int kind;
+      int64_t t0, tn, r0, rn;
+      double flops;
+    };
+    std::vector<BStage> bst;
   };
   DevBuf<ReduceTask> red_, sred_;
   DevBuf<double> parts_, rparts_, sparts_;  // split-K partial tiles
@@ -286,7 +295,12 @@ class DeviceFactor {
   std::vector<SLevel> slev_;
   DevBuf<ColTask> sga_;
   DevBuf<GemmTask> sgemm_;
-  DevBuf<SelChunk> strsm_, sdiag_, smir_;
+  DevBuf<SelChunk> strsm_, sdiag_, smir_, sblk_;
+  // supernodes of 2+ chunks and at most this many columns run the blocked
+  // selected inversion (W = L_JJ⁻¹ by recursive doubling + four GEMM stages)
+  // instead of the chunk chain; GMRF_SEL_BLOCK=0 disables (A/B). The cap bounds
+  // the w² + r·w staging (partition_memory models the same rule).
+  int sel_block_max_w_ = kSelBlockMaxW;
   bool selinv_plan_ = false;
 
   std::vector<int64_t> lvl_ptr_;

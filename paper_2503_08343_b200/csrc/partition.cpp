@@ -253,6 +253,25 @@ void plan_update_arenas(const Symbolic& s, const std::vector<i32>& owner, int ra
   so = plan_arena(size, a, b, nsl, arena_s);
 }
 
+std::vector<i64> selinv_staging(const Symbolic& s, const std::vector<i32>* owner, int rank,
+                                int block_max_w) {
+  std::vector<int> l0, la;
+  int nl = 0;
+  chunk_levels(s, l0, la, nl, 0);
+  std::vector<i64> st(std::max(nl, 1), 0);
+  for (int k = 0; k < s.ns; ++k) {
+    if (owner && (*owner)[k] != rank) continue;
+    const int w = s.w(k), rows = s.rows(k), nch = (w + kNB - 1) / kNB;
+    if (sel_blocked(w, block_max_w)) {
+      st[l0[k] + nch - 1] += static_cast<i64>(w) * w + static_cast<i64>(rows - w) * w;
+      continue;
+    }
+    for (int c = 0; c * kNB < w; ++c)
+      st[l0[k] + c] += static_cast<i64>(rows - c * kNB) * std::min(kNB, w - c * kNB);
+  }
+  return st;
+}
+
 std::vector<RankMemory> partition_memory(const Symbolic& s, const std::vector<i32>& owner,
                                          int nranks, int max_rhs) {
   std::vector<RankMemory> out(nranks);
@@ -276,14 +295,7 @@ std::vector<RankMemory> partition_memory(const Symbolic& s, const std::vector<i3
     // the pipelines run the selected inversion in place (Σ overwrites L): only
     // the per-level Y / W staging is extra (DeviceFactor::build_selinv_plan)
     {
-      std::vector<int> l0, la;
-      int nl = 0;
-      chunk_levels(s, l0, la, nl, 0);
-      std::vector<i64> st(std::max(nl, 1), 0);
-      for (int k = 0; k < s.ns; ++k)
-        if (owner[k] == r)
-          for (int c = 0, w = s.w(k); c * kNB < w; ++c)
-            st[l0[k] + c] += static_cast<i64>(s.rows(k) - c * kNB) * std::min(kNB, w - c * kNB);
+      const std::vector<i64> st = selinv_staging(s, &owner, r, kSelBlockMaxW);
       m.sigma_panels = 8 * *std::max_element(st.begin(), st.end());
     }
     // replicated per rank: Q values + qmap over the pattern, solve vectors

@@ -47,6 +47,16 @@ struct XEdge {
 void chunk_levels(const Symbolic& s, std::vector<int>& lvl0, std::vector<int>& last, int& nlev,
                   int small_rows);
 
+// Selected inversion: supernodes of 2+ chunks and at most max_w columns are
+// inverted whole (blocked; staging w² + r·w doubles at their top chunk level),
+// the others chunk by chunk (staging (rows − c0)·w_c per chunk level).
+constexpr int kSelBlockMaxW = 4096;
+inline bool sel_blocked(int w, int max_w) { return w > 64 && w <= max_w; }
+// Per-chunk-level staging (doubles) of the supernodes with owner[k] == rank
+// (owner == nullptr: all), as DeviceFactor::build_selinv_plan lays it out.
+std::vector<i64> selinv_staging(const Symbolic& s, const std::vector<i32>* owner, int rank,
+                                int block_max_w);
+
 // Subtree-to-subcube ownership of the supernodes for `nranks` ranks, balanced by
 // subtree flops. nranks == 1 gives all zeros.
 std::vector<i32> partition_owners(const Symbolic& s, int nranks);

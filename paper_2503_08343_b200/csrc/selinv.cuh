@@ -158,4 +158,70 @@ __global__ void __launch_bounds__(256) k_sel_mirror(const SelChunk* __restrict__
   }
 }
 
+// ---------------------------------------------------------------------------
+// Blocked selected inversion of a multi-chunk supernode (factor.cu,
+// build_selinv_plan): instead of a chain of 64-column chunk steps, the whole
+// supernode J (w columns, rows R below) is done with a few batched GEMM stages:
+//   W  = L_JJ⁻¹                     (k_tri_inv64 on the diagonal blocks, then
+//                                    log2(chunks) merge steps  X = −C⁻¹ B A⁻¹)
+//   Gn = −L_RJ W,  Σ_RJ = Σ_RR Gn,  Σ_JJ = Wᵀ W + Gnᵀ Σ_RJ
+// (takahashi.hpp:43-60 in supernodal form, e.g. Lin et al., SelInv).
+//
+// k_tri_inv64: dst (w × w block of the W workspace, zeros above the diagonal)
+// = inverse of the chunk's lower-triangular diagonal block; one column per
+// thread, forward substitution L x = e_c with L_JJ staged in shared memory.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(64) k_tri_inv64(const SelChunk* __restrict__ tasks) {
+  constexpr int W = 64, P = W + 1;
+  __shared__ double Lc[W * P];  // Lc[i*P + k] = L_ki (column i), k >= i
+  __shared__ double rd[W];
+  const SelChunk& t = tasks[blockIdx.x];
+  const int w = t.w, ld = t.ld, tid = threadIdx.x;
+  const double* Lk = t.l + t.c0 + static_cast<int64_t>(t.c0) * ld;
+#pragma unroll 16
+  for (int idx = tid; idx < W * W; idx += W) {
+    const int i = idx / W, k = idx % W;
+    const bool in = i < w && k < w;
+    Lc[i * P + k] = (in && k >= i) ? Lk[k + static_cast<int64_t>(i) * ld] : (k == i ? 1.0 : 0.0);
+  }
+  rd[tid] = tid < w ? t.rd[tid] : 1.0;
+  const int c = tid;
+  double x[W];
+#pragma unroll
+  for (int k = 0; k < W; ++k) x[k] = (k == c) ? 1.0 : 0.0;
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < W; ++i) {
+    const double xi = div_rn(x[i], Lc[i * P + i], rd[i]);
+    x[i] = xi;
+#pragma unroll
+    for (int k = i + 1; k < W; ++k) x[k] = fma(-xi, Lc[i * P + k], x[k]);
+  }
+  if (c < w) {
+    double* D = t.dst + static_cast<int64_t>(c) * t.ldd;
+#pragma unroll
+    for (int i = 0; i < W; ++i)
+      if (i < w) D[i] = i >= c ? x[i] : 0.0;
+  }
+}
+
+// Σ_JJ tile (rows c0.., columns tile.., w × wsn entries, c0 >= tile) mirrored
+// into the upper triangle: Σ[j, i] = Σ[i, j] for i > j, through shared memory.
+__global__ void __launch_bounds__(256) k_sel_mirror_blk(const SelChunk* __restrict__ tasks) {
+  __shared__ double T[64][65];
+  const SelChunk& t = tasks[blockIdx.x];
+  const int m = t.w, n = t.wsn, i0 = t.c0, j0 = t.tile, tid = threadIdx.x;
+  const int64_t ld = t.ld;
+  double* S = t.sig;
+  for (int idx = tid; idx < 64 * n; idx += blockDim.x) {
+    const int i = idx & 63, j = idx >> 6;
+    if (i < m) T[j][i] = S[(i0 + i) + (j0 + j) * ld];
+  }
+  __syncthreads();
+  for (int idx = tid; idx < 64 * m; idx += blockDim.x) {
+    const int j = idx & 63, i = idx >> 6;
+    if (j < n && i0 + i > j0 + j) S[(j0 + j) + (i0 + i) * ld] = T[j][i];
+  }
+}
+
 }  // namespace gmrf
