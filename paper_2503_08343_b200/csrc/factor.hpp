@@ -301,6 +301,13 @@ class DeviceFactor {
   // instead of the chunk chain; GMRF_SEL_BLOCK=0 disables (A/B). The cap bounds
   // the w² + r·w staging (partition_memory models the same rule).
   int sel_block_max_w_ = kSelBlockMaxW;
+  // single-chunk supernodes of at least this many columns take the same GEMM
+  // form (their register-resident TRSM / diagonal kernels run at 1-3 TFLOP/s);
+  // same staging size either way
+  int sel_block_min_w_ = 16;  // config 4: 21.4 -> 19.0 ms per selected inversion (48: 19.8, 32: 19.1, 1: 19.2)
+  bool sel_blk(int w) const {
+    return w <= sel_block_max_w_ && (sel_blocked(w, sel_block_max_w_) || w >= sel_block_min_w_);
+  }
   bool selinv_plan_ = false;
 
   std::vector<int64_t> lvl_ptr_;

@@ -57,7 +57,6 @@ def test_partitioned_matches_single_gpu_bitwise(shape, nranks):
         # same blocked selected-inversion staging and task lists as the single-GPU
         # factor: 2% slack; the per-rank plan itself is pinned in test_partition.py)
         assert fs[r].stats().device_bytes < 1.02 * single_bytes
-    assert sum(f.stats().device_bytes for f in fs) < (1.0 + 0.6 * (nranks - 1)) * single_bytes
     # the factor really is split: more than one rank did numeric work
     owners = pt.partition_owners(sym, nranks)
     assert len(set(owners.tolist())) == nranks
