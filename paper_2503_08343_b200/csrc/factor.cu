@@ -141,7 +141,7 @@ DeviceFactor::DeviceFactor(std::shared_ptr<const Symbolic> sym, cudaStream_t str
   if (const char* e = std::getenv("GMRF_WIDE_K")) wide_min_k_ = atoi(e);
   if (const char* e = std::getenv("GMRF_WIDE_R")) wide_min_r_ = atoi(e);
   if (const char* e = std::getenv("GMRF_GEMM_NEXT")) gemm_next_ = e[0] != '0';
-  if (const char* e = std::getenv("GMRF_SEL_BLOCK")) sel_block_max_w_ = atoi(e);  // 0: chunk chain only
+  if (const char* e = std::getenv("GMRF_SEL_BLOCK")) sel_block_stage_ = atoll(e);  // per-level staging bound in doubles; 0: chunk chain only
   if (const char* e = std::getenv("GMRF_SEL_BLOCK_MIN")) sel_block_min_w_ = atoi(e);
   if (const char* e = std::getenv("GMRF_NEXT_TILES")) next_max_tiles_ = atoll(e);
   if (const char* e = std::getenv("GMRF_WIDE_R")) wide_min_r_ = atoi(e);
@@ -770,7 +770,8 @@ void DeviceFactor::build_selinv_plan() {
   chunk_levels(s, lvl0, last, nlev, 0);
   // per-level staging: Y (nbelow × w) and W / Z (w × w) of every chunk; W = L_JJ⁻¹
   // (w × w) and Gn (r × w) of every blocked supernode at its top chunk level
-  std::vector<int64_t> yoff = selinv_staging(s, part_ ? &owner_ : nullptr, rank_, sel_block_max_w_);
+  sel_blk_ = selinv_blocked(s, sel_block_stage_, sel_block_stage_ > 0 ? sel_block_min_w_ : kNB + 1);
+  std::vector<int64_t> yoff = selinv_staging(s, part_ ? &owner_ : nullptr, rank_, sel_blk_);
   yoff.resize(std::max<size_t>(yoff.size(), nlev), 0);
   int64_t ymax = 1;
   for (int64_t v : yoff) ymax = std::max(ymax, v);
@@ -916,7 +917,7 @@ void DeviceFactor::build_selinv_plan() {
   std::vector<std::map<int, StageBuild>> bsb(nlev);
   for (int k = 0; k < s.ns; ++k) {  // tile counts over all ranks' supernodes
     const int w = s.w(k);
-    if (!sel_blk(w)) continue;
+    if (!sel_blk_[k]) continue;
     auto& lv = bsb[lvl0[k] + nchunks(w) - 1];
     blocked_tasks(w, s.rows(k) - w, L, L, L, L, L, L,
                   [&](int st, const GemmTask&) { ++lv[st].tiles_all; },
@@ -938,7 +939,7 @@ void DeviceFactor::build_selinv_plan() {
     double* Sk = S + lptr_h_[k];
     double* Uk = U + uptrs_h_[k];
     const int nch = nchunks(w);
-    if (sel_blk(w)) {
+    if (sel_blk_[k]) {
       const int lv = lvl0[k] + nch - 1;
       if (r > 0 && mine(par)) {  // else received from the parent's rank
         for (int b = 0; b < r; ++b) ga[lv].push_back({k, b});
@@ -1055,7 +1056,7 @@ void DeviceFactor::build_selinv_plan() {
   std::vector<int64_t> gyt(nlev, 0), gzt(nlev, 0);  // Y / Z tiles of all ranks per level
   for (int k = 0; k < s.ns; ++k) {
     const int w = s.w(k), rows = s.rows(k);
-    if (sel_blk(w)) continue;
+    if (sel_blk_[k]) continue;
     for (int c = 0; c < nchunks(w); ++c) {
       const int c0 = c * kNB, wk = std::min(kNB, w - c0);
       gyt[lvl0[k] + c] += (w - c0 - wk + kTile - 1) / kTile + (rows - w + kTile - 1) / kTile;

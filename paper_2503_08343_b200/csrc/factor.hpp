@@ -296,18 +296,16 @@ class DeviceFactor {
   DevBuf<ColTask> sga_;
   DevBuf<GemmTask> sgemm_;
   DevBuf<SelChunk> strsm_, sdiag_, smir_, sblk_;
-  // supernodes of 2+ chunks and at most this many columns run the blocked
-  // selected inversion (W = L_JJ⁻¹ by recursive doubling + four GEMM stages)
-  // instead of the chunk chain; GMRF_SEL_BLOCK=0 disables (A/B). The cap bounds
-  // the w² + r·w staging (partition_memory models the same rule).
-  int sel_block_max_w_ = kSelBlockMaxW;
-  // single-chunk supernodes of at least this many columns take the same GEMM
-  // form (their register-resident TRSM / diagonal kernels run at 1-3 TFLOP/s);
-  // same staging size either way
-  int sel_block_min_w_ = 16;  // config 4: 21.4 -> 19.0 ms per selected inversion (48: 19.8, 32: 19.1, 1: 19.2)
-  bool sel_blk(int w) const {
-    return w <= sel_block_max_w_ && (sel_blocked(w, sel_block_max_w_) || w >= sel_block_min_w_);
-  }
+  // blocked selected inversion (W = L_JJ⁻¹ by recursive doubling + four GEMM
+  // stages instead of the chunk chain): multi-chunk supernodes while their
+  // level's staging stays under sel_block_stage_ doubles, single-chunk ones of at
+  // least sel_block_min_w_ columns (their register-resident TRSM / diagonal
+  // kernels run at 1-3 TFLOP/s; config 4: 21.4 -> 19.0 ms per selected inversion
+  // at 16; 48: 19.8, 32: 19.1, 1: 19.2). selinv_blocked (partition.hpp) decides,
+  // partition_memory models the same rule; GMRF_SEL_BLOCK=0 disables (A/B).
+  long long sel_block_stage_ = kSelBlockLevelStage;
+  int sel_block_min_w_ = 16;
+  std::vector<char> sel_blk_;
   bool selinv_plan_ = false;
 
   std::vector<int64_t> lvl_ptr_;

@@ -253,8 +253,31 @@ void plan_update_arenas(const Symbolic& s, const std::vector<i32>& owner, int ra
   so = plan_arena(size, a, b, nsl, arena_s);
 }
 
+std::vector<char> selinv_blocked(const Symbolic& s, long long max_level_stage, int min_single_w) {
+  std::vector<int> l0, la;
+  int nl = 0;
+  chunk_levels(s, l0, la, nl, 0);
+  std::vector<i64> tot(std::max(nl, 1), 0);
+  std::vector<char> blk(s.ns, 0);
+  if (max_level_stage <= 0) return blk;
+  for (int k = 0; k < s.ns; ++k) {
+    const int w = s.w(k), rows = s.rows(k), nch = (w + kNB - 1) / kNB;
+    if (w <= kNB) {
+      blk[k] = w >= min_single_w;
+      continue;
+    }
+    const i64 need = static_cast<i64>(w) * rows;  // w² + r·w
+    i64& t = tot[l0[k] + nch - 1];
+    if (t + need <= max_level_stage) {
+      t += need;
+      blk[k] = 1;
+    }
+  }
+  return blk;
+}
+
 std::vector<i64> selinv_staging(const Symbolic& s, const std::vector<i32>* owner, int rank,
-                                int block_max_w) {
+                                const std::vector<char>& blocked) {
   std::vector<int> l0, la;
   int nl = 0;
   chunk_levels(s, l0, la, nl, 0);
@@ -262,8 +285,8 @@ std::vector<i64> selinv_staging(const Symbolic& s, const std::vector<i32>* owner
   for (int k = 0; k < s.ns; ++k) {
     if (owner && (*owner)[k] != rank) continue;
     const int w = s.w(k), rows = s.rows(k), nch = (w + kNB - 1) / kNB;
-    if (sel_blocked(w, block_max_w)) {
-      st[l0[k] + nch - 1] += static_cast<i64>(w) * w + static_cast<i64>(rows - w) * w;
+    if (blocked[k]) {
+      st[l0[k] + nch - 1] += static_cast<i64>(w) * rows;
       continue;
     }
     for (int c = 0; c * kNB < w; ++c)
@@ -275,6 +298,7 @@ std::vector<i64> selinv_staging(const Symbolic& s, const std::vector<i32>* owner
 std::vector<RankMemory> partition_memory(const Symbolic& s, const std::vector<i32>& owner,
                                          int nranks, int max_rhs) {
   std::vector<RankMemory> out(nranks);
+  const std::vector<char> sel_blk = selinv_blocked(s, kSelBlockLevelStage, 16);
   for (int r = 0; r < nranks; ++r) {
     RankMemory& m = out[r];
     for (int k = 0; k < s.ns; ++k)
@@ -295,7 +319,7 @@ std::vector<RankMemory> partition_memory(const Symbolic& s, const std::vector<i3
     // the pipelines run the selected inversion in place (Σ overwrites L): only
     // the per-level Y / W staging is extra (DeviceFactor::build_selinv_plan)
     {
-      const std::vector<i64> st = selinv_staging(s, &owner, r, kSelBlockMaxW);
+      const std::vector<i64> st = selinv_staging(s, &owner, r, sel_blk);
       m.sigma_panels = 8 * *std::max_element(st.begin(), st.end());
     }
     // replicated per rank: Q values + qmap over the pattern, solve vectors

@@ -47,15 +47,20 @@ struct XEdge {
 void chunk_levels(const Symbolic& s, std::vector<int>& lvl0, std::vector<int>& last, int& nlev,
                   int small_rows);
 
-// Selected inversion: supernodes of 2+ chunks and at most max_w columns are
-// inverted whole (blocked; staging w² + r·w doubles at their top chunk level),
-// the others chunk by chunk (staging (rows − c0)·w_c per chunk level).
-constexpr int kSelBlockMaxW = 4096;
-inline bool sel_blocked(int w, int max_w) { return w > 64 && w <= max_w; }
+// Selected inversion: which supernodes are inverted whole (blocked: W = L_JJ⁻¹
+// w² plus Gn r·w doubles of staging at their top chunk level) instead of chunk by
+// chunk (staging (rows − c0)·w_c per chunk level). Multi-chunk supernodes are
+// admitted in index order while the staging of ALL supernodes ending on the same
+// chunk level — over every rank, so a partitioned factor takes the same decisions
+// (same rounding) as the single-GPU one and no rank exceeds the bound — stays
+// under max_level_stage doubles; single-chunk supernodes of at least
+// min_single_w columns always (same staging either way).
+constexpr long long kSelBlockLevelStage = 1ll << 28;  // doubles (2 GiB)
+std::vector<char> selinv_blocked(const Symbolic& s, long long max_level_stage, int min_single_w);
 // Per-chunk-level staging (doubles) of the supernodes with owner[k] == rank
 // (owner == nullptr: all), as DeviceFactor::build_selinv_plan lays it out.
 std::vector<i64> selinv_staging(const Symbolic& s, const std::vector<i32>* owner, int rank,
-                                int block_max_w);
+                                const std::vector<char>& blocked);
 
 // Subtree-to-subcube ownership of the supernodes for `nranks` ranks, balanced by
 // subtree flops. nranks == 1 gives all zeros.

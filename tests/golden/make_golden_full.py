@@ -26,6 +26,9 @@ redirected to METIS nested dissection (oracle/_ref/libgmrfref_nd.so) and records
 the move in floors.json under "<fixture>/order": the reference's ordering floor
 (SURVEY §8(c) (i)), the primary tolerance scale of the GPU parity tests.
 
+``floor_novar:<job>`` / ``order_novar:<job>`` are ``floor:`` / ``order:`` without the variance pass (the full-size C4
+probe: the Takahashi pass alone is hours there).
+
 ``floor:<job>`` re-runs the same unmodified reference chain with every initial-
 condition value multiplied by (1 ± 2⁻⁵²) (oracle/ref_capi.cpp ulp_perturb,
 SURVEY §8(c) "floor2") and records in floors.json how far the reference's own
@@ -85,7 +88,10 @@ def _record_floor(name, b):
     f = {"seed": FLOOR_SEED} if MODE["tag"] == "/ulp" else {"ordering": "metis_nd"}
     for k, key in (("mean", "mode"), ("mean", "mean_post"), ("var", "var_post")):
         if key in z.files and k not in f:
-            f[k] = _rel(b.vec(key), z[key])
+            try:
+                f[k] = _rel(b.vec(key), z[key])
+            except Exception:  # stage not run by this probe (floor_novar)
+                pass
     if "gn_objective" in z.files:
         for k in ("gn_objective", "gn_decrement"):
             v = b.vec(k)
@@ -106,7 +112,8 @@ def _record_floor(name, b):
 def burgers(n_el, n_t, gn_iters, name, floor=False):
     # make_golden.spatiotemporal parameter layout (oracle/ref_capi.cpp:157-160)
     p = [1, n_el, -1.0, 1.0, n_t, 1.0, 0.01 / np.pi, 0.5, 10, 1, 1, 10, 2, 1, 1.0, 1e-10, 1e8,
-         0, 1e12, gn_iters, 1, 1, 0, FLOOR_SEED if floor and MODE["tag"] == "/ulp" else 0]
+         0, 1e12, gn_iters, 0 if MODE.get("novar") else 1, 1, 0,
+         FLOOR_SEED if floor and MODE["tag"] == "/ulp" else 0]
     t0 = time.time()
     b = Ref(MODE["so"]).build("spatiotemporal", p)
     if floor:
@@ -179,4 +186,10 @@ if __name__ == "__main__":
             MODE.update(so=REF_ND_SO, tag="/order")
         elif kind == "floor":
             MODE.update(tag="/ulp")
+        elif kind == "order_novar":
+            MODE.update(so=REF_ND_SO, tag="/order", novar=True)
+        elif kind == "floor_novar":
+            # full-size probe without the Takahashi pass (hours at n = 1e6): GN trace
+            # and mode floors only
+            MODE.update(tag="/ulp", novar=True)
         JOBS[job.split(":")[-1]](kind != "")

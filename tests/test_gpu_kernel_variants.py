@@ -71,3 +71,28 @@ def test_chain_variants_are_bit_identical(env):
     spec = SpaceTimeSpec.burgers(299, 300)
     u0 = -np.sin(np.pi * spec.node_x())
     _same(_run(spec, u0, {}, gn=2), _run(spec, u0, env, gn=2))
+
+
+@pytest.mark.parametrize("shape", ["burgers", "allen_cahn"])
+def test_blocked_selected_inversion_matches_chunk_chain(shape):
+    """The blocked selected inversion (W = L_JJ⁻¹ by recursive doubling, then
+    Gn = −L_RJ W, Σ_RJ = Σ_RR Gn, Σ_JJ = WᵀW + GnᵀΣ_RJ as GEMM stages; selinv.cuh)
+    and the 64-column chunk chain (GMRF_SEL_BLOCK=0) evaluate the same Takahashi
+    recurrences (takahashi.hpp:43-60) in different association orders: the
+    factorization, mean and GN trace must be untouched, the variances agree to
+    rounding amplified by the conditioning of the diagonal blocks."""
+    if shape == "burgers":
+        spec = SpaceTimeSpec.burgers(299, 300)
+        u0 = -np.sin(np.pi * spec.node_x())
+    else:
+        spec = SpaceTimeSpec.allen_cahn(31, 64)
+        u0 = np.random.default_rng(1005).uniform(-0.1, 0.1, spec.n_space)
+    blocked = _run(spec, u0, {}, gn=2)
+    chain = _run(spec, u0, {"GMRF_SEL_BLOCK": "0"}, gn=2)
+    only_wide = _run(spec, u0, {"GMRF_SEL_BLOCK_MIN": "65"}, gn=2)
+    for other in (chain, only_wide):
+        assert blocked[2] == other[2]
+        np.testing.assert_array_equal(blocked[0], other[0])
+        assert np.all(other[1] > 0)
+        rel = np.abs(blocked[1] - other[1]) / other[1]
+        assert rel.max() <= 1e-9, rel.max()
