@@ -141,6 +141,8 @@ DeviceFactor::DeviceFactor(std::shared_ptr<const Symbolic> sym, cudaStream_t str
   if (const char* e = std::getenv("GMRF_WIDE_K")) wide_min_k_ = atoi(e);
   if (const char* e = std::getenv("GMRF_WIDE_R")) wide_min_r_ = atoi(e);
   if (const char* e = std::getenv("GMRF_GEMM_NEXT")) gemm_next_ = e[0] != '0';
+  if (const char* e = std::getenv("GMRF_FUSE_FWD")) fuse_fwd_ = e[0] != '0';
+  if (const char* e = std::getenv("GMRF_FUSE_LATE")) fuse_late_ = e[0] != '0';
   if (const char* e = std::getenv("GMRF_SEL_BLOCK")) sel_block_stage_ = atoll(e);  // per-level staging bound in doubles; 0: chunk chain only
   if (const char* e = std::getenv("GMRF_SEL_BLOCK_MIN")) sel_block_min_w_ = atoi(e);
   if (const char* e = std::getenv("GMRF_NEXT_TILES")) next_max_tiles_ = atoll(e);
@@ -367,7 +369,9 @@ DeviceFactor::DeviceFactor(std::shared_ptr<const Symbolic> sym, cudaStream_t str
     const int mid = hi < lo ? lo - 1 : lo;
     cuda_check(cudaStreamCreateWithPriority(&aux_, cudaStreamNonBlocking, mid), "aux stream");
     cuda_check(cudaStreamCreateWithPriority(&uu_, cudaStreamNonBlocking, lo), "update stream");
+    cuda_check(cudaStreamCreateWithPriority(&sf_, cudaStreamNonBlocking, lo), "fused-solve stream");
     cuda_check(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming), "event");
+    cuda_check(cudaEventCreateWithFlags(&ev_fs_, cudaEventDisableTiming), "event");
   }
   ev_panel_.resize(flev_.size());
   ev_rest_.resize(flev_.size());
@@ -385,6 +389,9 @@ DeviceFactor::DeviceFactor(std::shared_ptr<const Symbolic> sym, cudaStream_t str
 
 DeviceFactor::~DeviceFactor() {
   if (fgraph_) cudaGraphExecDestroy(fgraph_);
+  if (fgraph_fs_) cudaGraphExecDestroy(fgraph_fs_);
+  if (ev_fs_) cudaEventDestroy(ev_fs_);
+  if (sf_) cudaStreamDestroy(sf_);
   for (cudaEvent_t e : ev_panel_) cudaEventDestroy(e);
   for (cudaEvent_t e : ev_rest_) cudaEventDestroy(e);
   for (cudaEvent_t e : ev_uupd_) cudaEventDestroy(e);
@@ -746,6 +753,54 @@ void DeviceFactor::build_factor_plan() {
   eap_.upload(ea_pairs, stream_);
   pan_.upload(panf, stream_);
   po_.upload(pof, stream_);
+  {  // fused forward sweep: tree levels below the first wide supernode
+    int lf = s.n_levels;
+    for (int l = 0; l < s.n_levels; ++l)
+      if (lvl_ptr_[l + 1] - lvl_ptr_[l] > lvl_nrm_[l]) {
+        lf = l;
+        break;
+      }
+    fuse_levels_ = part_ ? 0 : lf;
+    fs_ready_.assign(fuse_levels_, 0);
+    std::vector<std::vector<PanelTask>> byl(fuse_levels_);
+    for (int k = 0; k < s.ns; ++k) {
+      const int tl = s.sn_level[k];
+      if (tl >= fuse_levels_) continue;
+      const int w = s.w(k), rows = s.rows(k);
+      if (rows <= kSmallRows) {  // small fronts leave L in its final layout
+        fs_ready_[tl] = std::max(fs_ready_[tl], lvl0[k]);
+        continue;
+      }
+      fs_ready_[tl] = std::max(fs_ready_[tl], lvl0[k] + nchunks(w) - 1);
+      double* Lk = L + lptr_h_[k];
+      for (int c0 = 0; c0 < w; c0 += kNB) {
+        const int wk = std::min(kNB, w - c0);
+        byl[tl].push_back({Lk + c0 + static_cast<int64_t>(c0) * rows, rows, wk, rows - c0 - wk, 0,
+                           s.sn_first[k] + c0});
+      }
+    }
+    for (int l = 1; l < fuse_levels_; ++l) fs_ready_[l] = std::max(fs_ready_[l], fs_ready_[l - 1]);
+    // A/B knob: hold the sweep back until the one-wave chain at the top of the tree.
+    // Measured on config 4 (per factorization + solve): sweep as soon as ready +0.21 ms
+    // of factorization for 0.50 ms less solve; held back +0.32 ms (its CTAs delay the
+    // chain's launches more than they cost beside the throughput-bound bottom levels).
+    if (fuse_late_) {
+      int start = nlev;
+      for (int li = nlev - 1; li >= 0; --li) {
+        if (!(flev_[li].prow[0] && flev_[li].prow[1] && flev_[li].prow[2])) break;
+        start = li;
+      }
+      if (start < nlev)
+        for (int l = 0; l < fuse_levels_; ++l) fs_ready_[l] = std::max(fs_ready_[l], start);
+    }
+    std::vector<PanelTask> flat;
+    pof_ptr_.assign(fuse_levels_ + 1, 0);
+    for (int l = 0; l < fuse_levels_; ++l) {
+      flat.insert(flat.end(), byl[l].begin(), byl[l].end());
+      pof_ptr_[l + 1] = static_cast<int64_t>(flat.size());
+    }
+    pof_.upload(flat, stream_);
+  }
   pd_.upload(pdf, stream_);
   pt_.upload(ptf, stream_);
   stage_.alloc(max_slots * kL11Slot);
@@ -1183,31 +1238,47 @@ int32_t DeviceFactor::numeric(const double* q, bool q_on_device) {
   return factor_panels();
 }
 
-int32_t DeviceFactor::factor_panels() {
+int32_t DeviceFactor::factor_panels(const double* fwd_rhs) {
   const Symbolic& s = *sym_;
   KernelProfiler& pf = *prof_;
   const bool la = lookahead_ && !pf.on;
+  const bool graph = la && !part_ && use_graph_;
+  const bool fuse = fwd_rhs && graph && fuse_fwd_ && fuse_levels_ > 0;
+  rhs_pending_ = false;
+  if (fwd_rhs && s.n > 0) {
+    ensure_solve_ws(1);
+    launches_solve_ = 0;
+    k_permute_gather<<<static_cast<int>(std::min<int64_t>((s.n + 255) / 256, 148 * 8)), 256, 0,
+                       stream_>>>(fwd_rhs, perm_.p, s.n, 1, v1_.p);
+    ++launches_solve_;
+    rhs_pending_ = true;
+    fwd_done_ = 0;
+  }
   // The level sequence is fixed per symbolic: captured once into a CUDA graph
   // (both lookahead streams, their event edges) and replayed per factorization,
   // so the ~100-level chain at the top of the tree is not paced by host launches.
-  if (la && !part_ && use_graph_) {
-    if (!fgraph_) {
-      const int64_t l0 = launches_numeric_;
+  if (graph) {
+    cudaGraphExec_t& exec = fuse ? fgraph_fs_ : fgraph_;
+    int64_t& glaunches = fuse ? graph_fs_launches_ : graph_launches_;
+    if (!exec) {
+      const int64_t l0 = launches_numeric_, s0 = launches_solve_;
       cuda_check(cudaStreamBeginCapture(main_, cudaStreamCaptureModeThreadLocal), "capture");
-      enqueue_levels(main_, aux_, true, true);
+      enqueue_levels(main_, aux_, true, true, fuse);
       cudaGraph_t g = nullptr;
       cuda_check(cudaStreamEndCapture(main_, &g), "end capture");
       // per-node priorities (copied from the capturing streams): the chain runs
       // ahead of the bulk updates, as it does with plain stream launches
-      cuda_check(cudaGraphInstantiate(&fgraph_, g, cudaGraphInstantiateFlagUseNodePriority),
+      cuda_check(cudaGraphInstantiate(&exec, g, cudaGraphInstantiateFlagUseNodePriority),
                  "graph instantiate");
       cuda_check(cudaGraphDestroy(g), "graph destroy");
-      graph_launches_ = launches_numeric_ - l0;
+      glaunches = (launches_numeric_ - l0) + (launches_solve_ - s0);
       launches_numeric_ = l0;
+      launches_solve_ = s0;
     }
-    cuda_check(cudaGraphLaunch(fgraph_, stream_), "graph launch");
+    cuda_check(cudaGraphLaunch(exec, stream_), "graph launch");
     dump_trace();
-    launches_numeric_ += graph_launches_;
+    launches_numeric_ += glaunches;
+    if (fuse) fwd_done_ = fuse_levels_;
   } else {
     enqueue_levels(la ? main_ : stream_, la ? aux_ : stream_, la, false);
   }
@@ -1233,7 +1304,8 @@ int32_t DeviceFactor::factor_panels() {
 // bulk stream sb (la: two-stream lookahead, else sa == sb == stream_). In a
 // graph capture sa is the origin stream and the fork/join to stream_ is left
 // to the graph launch.
-void DeviceFactor::enqueue_levels(cudaStream_t sa, cudaStream_t sb, bool la, bool in_graph) {
+void DeviceFactor::enqueue_levels(cudaStream_t sa, cudaStream_t sb, bool la, bool in_graph,
+                                  bool fuse_fwd) {
   const SymDev sd = symdev();
   KernelProfiler& pf = *prof_;
   // GMRF_WHATIF_BUILD: diagnostic-only build (tools/) that drops launch classes to
@@ -1247,6 +1319,7 @@ void DeviceFactor::enqueue_levels(cudaStream_t sa, cudaStream_t sb, bool la, boo
     cuda_check(cudaEventRecord(ev_fork_, stream_), "record");
     cuda_check(cudaStreamWaitEvent(sa, ev_fork_, 0), "wait");
   }
+  int fs_next = 0;  // next tree level of the fused forward sweep
   for (size_t li = 0; li < flev_.size(); ++li) {
     const FLevel& lv = flev_[li];
     const int lvl = static_cast<int>(li);
@@ -1381,6 +1454,22 @@ void DeviceFactor::enqueue_levels(cudaStream_t sa, cudaStream_t sb, bool la, boo
     }
     mark(sa, 1);
     if (la) cuda_check(cudaEventRecord(ev_panel_[li], sa), "record");
+    if (fuse_fwd) {
+      // forward sweep of the tree levels whose panels are final now: diagonal
+      // blocks moved into place for these chunks, then the level's solve kernels
+      bool waited = false;
+      for (; fs_next < fuse_levels_ && fs_ready_[fs_next] <= lvl; ++fs_next) {
+        if (!waited) cuda_check(cudaStreamWaitEvent(sf_, ev_panel_[li], 0), "wait");
+        waited = true;
+        const int64_t nc = pof_ptr_[fs_next + 1] - pof_ptr_[fs_next];
+        if (nc) {
+          k_diag_writeback<<<static_cast<unsigned>(nc), 128, 0, sf_>>>(pof_.p + pof_ptr_[fs_next],
+                                                                    diag_.p, rdiag_.p);
+          ++launches_numeric_;
+        }
+        fwd_level<1>(fs_next, v1_.p, 1, sf_);
+      }
+    }
     // next(l) writes block c+1, last written off the chain by the flush D levels back
     if (la && li >= static_cast<size_t>(lv.dwait))
       cuda_check(cudaStreamWaitEvent(sa, ev_rest_[li - lv.dwait], 0), "wait");
@@ -1448,11 +1537,16 @@ void DeviceFactor::enqueue_levels(cudaStream_t sa, cudaStream_t sb, bool la, boo
       cuda_check(cudaStreamWaitEvent(sa, ev_rest_[flev_.size() - 1], 0), "wait");
       cuda_check(cudaStreamWaitEvent(sa, ev_uupd_[flev_.size() - 1], 0), "wait");
     }
+    if (fuse_fwd && fs_next > 0) {
+      cuda_check(cudaEventRecord(ev_fs_, sf_), "record");
+      cuda_check(cudaStreamWaitEvent(sa, ev_fs_, 0), "wait");
+    }
     if (!in_graph) {
       cuda_check(cudaEventRecord(ev_fork_, sa), "record");
       cuda_check(cudaStreamWaitEvent(stream_, ev_fork_, 0), "wait");
     }
   }
+  require(!fuse_fwd || fs_next == fuse_levels_, kContract, "fused forward sweep: levels left over");
 }
 
 void DeviceFactor::dump_trace() {
@@ -1517,6 +1611,11 @@ void DeviceFactor::exchange_solve(int phase, int level, int nr, double* y) {
 void DeviceFactor::ensure_solve_ws(int nrhs) {
   if (nrhs <= ws_nrhs_) return;
   const Symbolic& s = *sym_;
+  if (fgraph_fs_) {  // the captured forward launches hold the old workspace pointers
+    cuda_check(cudaStreamSynchronize(stream_), "solve workspace");
+    cudaGraphExecDestroy(fgraph_fs_);
+    fgraph_fs_ = nullptr;
+  }
   Uv_.alloc(std::max<int64_t>(uv_total_ * nrhs, 1));
   P_.alloc(std::max<int64_t>(p_total_ * nrhs, 1));
   v1_.alloc(std::max<int64_t>(static_cast<int64_t>(s.n) * nrhs, 1));
@@ -1524,8 +1623,63 @@ void DeviceFactor::ensure_solve_ws(int nrhs) {
   ws_nrhs_ = nrhs;
 }
 
+// Forward-solve launches of tree level l on stream st (solve(); also captured
+// into the factorization graph by the fused forward sweep).
 template <int NR>
-void DeviceFactor::launch_solve_levels(bool fwd, bool bwd, double* y, int nr) {
+void DeviceFactor::fwd_level(int l, double* y, int nr, cudaStream_t st) {
+  const SymDev sd = symdev();
+  KernelProfiler& pf = *prof_;
+  const double* L = L_.p;
+  const double* rdiag = rdiag_.p;
+  const int32_t* lvl_sn = lvl_sn_.p;
+  const int smem_diag =
+      (maxw_ * NR + 64 * 65 + kSolveFuseRows * NR) * static_cast<int>(sizeof(double));
+  constexpr int smem_wide = wide_smem_bytes<NR>();
+  int64_t& launches = launches_solve_;
+  auto coop = [&](const void* fn, int64_t grid, void** args) {
+    cuda_check(cudaLaunchCooperativeKernel(fn, dim3(static_cast<unsigned>(grid)), dim3(256), args,
+                                           smem_wide, st),
+               "wide solve launch");
+    ++launches;
+  };
+  const int nrm = static_cast<int>(lvl_nrm_[l]);
+  const int nw = static_cast<int>(lvl_ptr_[l + 1] - lvl_ptr_[l]) - nrm;
+  const int nt = static_cast<int>(tile_ptr_[l + 1] - tile_ptr_[l]);
+  const int nsm = NR <= 4 ? static_cast<int>(lvl_nsm_[l]) : 0;
+  pf.run(st, pf.tag("solve.forward", l), 0.0, lvl_bytes_[l], [&] {
+    if constexpr (NR <= 4) if (nsm) {
+      k_fsolve_small<NR><<<(nsm + kSmallSolveWarps - 1) / kSmallSolveWarps, 32 * kSmallSolveWarps,
+                           0, st>>>(lvl_sn + lvl_ptr_[l], nsm, sd, L, y, nr, Uv_.p, uvptr_.p,
+                                    rdiag);
+      ++launches;
+    }
+    if (nrm > nsm) {
+      k_fsolve_diag<NR><<<nrm - nsm, 256, smem_diag, st>>>(lvl_sn + lvl_ptr_[l] + nsm, sd, L, y,
+                                                           nr, Uv_.p, uvptr_.p, rdiag);
+      ++launches;
+    }
+    if (nw) {
+      k_fsolve_wide_prep<NR><<<nw, 256, 0, st>>>(lvl_sn + lvl_ptr_[l] + nrm, sd, y, nr, Uv_.p,
+                                                 uvptr_.p);
+      ++launches;
+      for (int64_t g = wl_ptr_[l]; g < wl_ptr_[l + 1]; ++g) {
+        const WideBlock* tasks = wfwd_.p + wgroups_[g].t0;
+        double* xw = wx_.p;
+        void* args[] = {&tasks, const_cast<SymDev*>(&sd), &L, &y, &nr, &rdiag, &xw};
+        coop(reinterpret_cast<const void*>(k_fsolve_wide<NR>), wgroups_[g].nt, args);
+      }
+    }
+  });
+  if (nt)
+    pf.run(st, pf.tag("solve.forward_off", l), 0.0, 0.0, [&] {
+      k_fsolve_off<NR><<<nt, kSolveRows, 0, st>>>(tiles_.p + tile_ptr_[l], sd, L, y, nr, Uv_.p,
+                                                  uvptr_.p, pf_.p, pfctr_.p);
+      ++launches;
+    });
+}
+
+template <int NR>
+void DeviceFactor::launch_solve_levels(bool fwd, bool bwd, double* y, int nr, int fwd_from) {
   const Symbolic& s = *sym_;
   const SymDev sd = symdev();
   KernelProfiler& pf = *prof_;
@@ -1550,41 +1704,8 @@ void DeviceFactor::launch_solve_levels(bool fwd, bool bwd, double* y, int nr) {
     ++launches;
   };
   if (fwd)
-    for (int l = 0; l < s.n_levels; ++l) {
-      const int nrm = static_cast<int>(lvl_nrm_[l]);
-      const int nw = static_cast<int>(lvl_ptr_[l + 1] - lvl_ptr_[l]) - nrm;
-      const int nt = static_cast<int>(tile_ptr_[l + 1] - tile_ptr_[l]);
-      const int nsm = NR <= 4 ? static_cast<int>(lvl_nsm_[l]) : 0;
-      pf.run(st, pf.tag("solve.forward", l), 0.0, lvl_bytes_[l], [&] {
-        if constexpr (NR <= 4) if (nsm) {
-          k_fsolve_small<NR><<<(nsm + kSmallSolveWarps - 1) / kSmallSolveWarps, 32 * kSmallSolveWarps,
-                               0, st>>>(lvl_sn + lvl_ptr_[l], nsm, sd, L, y, nr, Uv_.p, uvptr_.p,
-                                        rdiag);
-          ++launches;
-        }
-        if (nrm > nsm) {
-          k_fsolve_diag<NR><<<nrm - nsm, 256, smem_diag, st>>>(lvl_sn + lvl_ptr_[l] + nsm, sd, L, y,
-                                                               nr, Uv_.p, uvptr_.p, rdiag);
-          ++launches;
-        }
-        if (nw) {
-          k_fsolve_wide_prep<NR><<<nw, 256, 0, st>>>(lvl_sn + lvl_ptr_[l] + nrm, sd, y, nr, Uv_.p,
-                                                     uvptr_.p);
-          ++launches;
-          for (int64_t g = wl_ptr_[l]; g < wl_ptr_[l + 1]; ++g) {
-            const WideBlock* tasks = wfwd_.p + wgroups_[g].t0;
-            double* xw = wx_.p;
-            void* args[] = {&tasks, const_cast<SymDev*>(&sd), &L, &y, &nr, &rdiag, &xw};
-            coop(reinterpret_cast<const void*>(k_fsolve_wide<NR>), wgroups_[g].nt, args);
-          }
-        }
-      });
-      if (nt)
-        pf.run(st, pf.tag("solve.forward_off", l), 0.0, 0.0, [&] {
-          k_fsolve_off<NR><<<nt, kSolveRows, 0, st>>>(tiles_.p + tile_ptr_[l], sd, L, y, nr, Uv_.p,
-                                                      uvptr_.p, pf_.p, pfctr_.p);
-          ++launches;
-        });
+    for (int l = fwd_from; l < s.n_levels; ++l) {
+      fwd_level<NR>(l, y, nr, st);
       if (part_) exchange_solve(kXFsolve, l, nr, y);
     }
   if (bwd)
@@ -1801,6 +1922,29 @@ void DeviceFactor::selinv(double* diag_out, bool on_device) {
   }
   selinv_done_ = true;
   if (sel_inplace_) factored_ = false;  // L now holds Σ: solves need a new factorization
+}
+
+// Completes the solve started by factor_panels(fwd_rhs): forward levels not
+// covered by the fused sweep, backward sweep, permutation back (same launches
+// as solve(kFull) on one right-hand side).
+void DeviceFactor::solve_pending(double* x_dev) {
+  require(factored_, kContract, "solve_pending: factor not computed");
+  require(rhs_pending_, kContract, "solve_pending: no right-hand side was passed to factor_panels");
+  const Symbolic& s = *sym_;
+  const int n = s.n;
+  rhs_pending_ = false;
+  if (n == 0) return;
+  double* y = v1_.p;
+  const int pblocks = static_cast<int>(std::min<int64_t>((n + 255) / 256, 148 * 8));
+  launch_solve_levels<1>(true, true, y, 1, fwd_done_);
+  if (part_) {
+    k_mask_cols<<<pblocks, 256, 0, stream_>>>(y, colmine_.p, n, 1);
+    ++launches_solve_;
+    exchange({{2, -1, -1, -1, y, static_cast<int64_t>(n)}});
+  }
+  k_permute_scatter<<<pblocks, 256, 0, stream_>>>(y, perm_.p, n, 1, x_dev);
+  ++launches_solve_;
+  cuda_check(cudaGetLastError(), "solve launch");
 }
 
 // Batches of up to kMaxRhs samples: z drawn on the host in the reference's

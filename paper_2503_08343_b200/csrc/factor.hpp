@@ -96,7 +96,14 @@ class DeviceFactor {
   // updates, spacetime.cu): begin_numeric zeroes the storage, the caller fills
   // L through d_qmap(), factor_panels runs the levels and returns like numeric.
   void begin_numeric();
-  int32_t factor_panels();
+  // fwd_rhs (device, original coordinates, one right-hand side): the forward
+  // sweep of H x = rhs rides along with the factorization — tree levels without
+  // wide supernodes are solved on a side stream of the replayed graph as soon as
+  // their panels are final (the top of the tree leaves most SMs idle), the same
+  // kernels on the same data as solve(): bit-identical. solve_pending(x) then
+  // runs the remaining forward levels, the backward sweep and the permutation.
+  int32_t factor_panels(const double* fwd_rhs = nullptr);
+  void solve_pending(double* x_dev);
   const int64_t* d_qmap() const { return qmap_.p; }
   // Solves; b/x are n×nrhs column-major (original coordinates for kFull,
   // permuted coordinates for kLower/kUpper, as cholesky.hpp:179-222).
@@ -151,13 +158,15 @@ class DeviceFactor {
   void build_selinv_plan();
   void ensure_solve_ws(int nrhs);
   template <int NR>
-  void launch_solve_levels(bool fwd, bool bwd, double* y, int nr);
+  void launch_solve_levels(bool fwd, bool bwd, double* y, int nr, int fwd_from = 0);
   SymDev symdev() const;
   SymDev symdev_sel() const;  // same, with the selected inversion's U offsets
   void plan_update_storage();
   bool mine(int k) const { return !part_ || owner_[k] == rank_; }
   void exchange(const std::vector<XferMsg>& m);
-  void enqueue_levels(cudaStream_t sa, cudaStream_t sb, bool la, bool in_graph);
+  void enqueue_levels(cudaStream_t sa, cudaStream_t sb, bool la, bool in_graph, bool fuse_fwd = false);
+  template <int NR>
+  void fwd_level(int l, double* y, int nr, cudaStream_t st);
   void exchange_solve(int phase, int level, int nr, double* y);
 
   std::shared_ptr<const Symbolic> sym_;
@@ -288,6 +297,20 @@ class DeviceFactor {
   DevBuf<PanelTask> pd_, pt_;         // two-phase panel tasks
   DevBuf<double> stage_;              // per-level L11 staging slots (panel2.cuh)
   cudaGraphExec_t fgraph_ = nullptr;  // captured chunk-level sequence
+  // fused forward sweep (factor_panels(fwd_rhs)): a second captured sequence with
+  // the forward-solve launches of tree levels [0, fuse_levels_) on sf_
+  cudaGraphExec_t fgraph_fs_ = nullptr;
+  int64_t graph_fs_launches_ = 0;
+  cudaStream_t sf_ = nullptr;
+  cudaEvent_t ev_fs_ = nullptr;
+  bool fuse_fwd_ = true;            // GMRF_FUSE_FWD=0 disables (A/B)
+  bool fuse_late_ = false;          // GMRF_FUSE_LATE=1: hold the fused sweep back until the one-wave chain (A/B: slower)
+  int fuse_levels_ = 0;             // tree levels below the first one with a wide supernode
+  std::vector<int> fs_ready_;       // chunk level whose panel step completes tree levels <= l
+  DevBuf<PanelTask> pof_;           // chunks by tree level (per-level diagonal write-back)
+  std::vector<int64_t> pof_ptr_;
+  int fwd_done_ = 0;                // forward levels already solved for the pending rhs
+  bool rhs_pending_ = false;
   int64_t graph_launches_ = 0;
   std::vector<double> lvl_bytes_;  // solve: L panel + row-index bytes per tree level
   KernelProfiler own_prof_;

@@ -803,10 +803,12 @@ std::vector<GnIter> SpaceTimePosterior::run(const double* u0, const GnConfig& cf
     cudaEventElapsedTime(&ms, e0, e1);
     acc += ms;
   };
-  auto factor_now = [&](const char* what) {
+  // rhs: the system's right-hand side, whose forward sweep rides along with the
+  // factorization (DeviceFactor::factor_panels); solve_pending finishes it
+  auto factor_now = [&](const char* what, const double* rhs = nullptr) {
     cudaEvent_t a = ev_[2], b = ev_[3];
     cudaEventRecord(a, stream_);
-    int32_t bad = fac_->factor_panels();
+    int32_t bad = fac_->factor_panels(rhs);
     cudaEventRecord(b, stream_);
     cudaEventSynchronize(b);
     float ms = 0;
@@ -829,8 +831,8 @@ std::vector<GnIter> SpaceTimePosterior::run(const double* u0, const GnConfig& cf
     cuda_check(cudaMemsetAsync(r1_.p, 0, n_ * sizeof(double), stream_), "rhs");
     k_ic_rhs<<<grid_for(ns_), 256, 0, stream_>>>(ns_, u0_.p, spec_.ic_noise_prec, r1_.p);
     fill_panels(d_qcond_.p, false);
-    factor_now("conditioning");
-    fac_->solve(2, 1, r1_.p, mean_cond_.p, true);
+    factor_now("conditioning", r1_.p);
+    fac_->solve_pending(mean_cond_.p);
     times_.kernel_launches += 1 + fac_->launches_solve();
   });
 
@@ -871,8 +873,8 @@ std::vector<GnIter> SpaceTimePosterior::run(const double* u0, const GnConfig& cf
     k_axpby<<<grid_for(n_), 256, 0, stream_>>>(n_, -1.0, g_.p, 0.0, g_.p, r1_.p);  // rhs = −grad
     times_.kernel_launches += 7;
     fill_panels(d_qeff_.p, true);
-    factor_now("gauss-newton");
-    fac_->solve(2, 1, r1_.p, d_.p, true);
+    factor_now("gauss-newton", r1_.p);
+    fac_->solve_pending(d_.p);
     times_.kernel_launches += fac_->launches_solve();
     const double gd = dot(g_.p, d_.p, n_);
     const double decrement = std::sqrt(std::max(0.0, -gd));

@@ -68,8 +68,10 @@ def _floors(name):
     path = os.path.join(GOLDEN, "floors.json")
     fl = json.load(open(path)) if os.path.exists(path) else {}
     probes = [fl[k] for k in (name + "/order", name + "/ulp") if k in fl]
-    if not probes:
-        pytest.skip(f"reference floor for {name} not measured yet (make_golden_full.py order:/floor:)")
+    if name + "/order" not in fl:
+        # the product factors in a nested-dissection order, the fixture's reference run
+        # in AMD order: the ordering probe is the tolerance scale that applies
+        pytest.skip(f"ordering floor for {name} not measured yet (make_golden_full.py order:)")
     return {k: max(p.get(k, 0.0) for p in probes) for k in BOUND}
 
 
