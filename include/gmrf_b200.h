@@ -441,6 +441,11 @@ typedef struct {
   int64_t nnz_pattern, nnz_l, nnz_l_padded;
   double flops_ref, flops_sn;
   int64_t factor_device_bytes; /* L panels + lifetime-packed update matrices + Σ panels + work */
+  /* numeric_ms covers every factorization, including the forward sweep that rides along
+   * with those followed by a solve; numeric_pure_ms / n_pure_factorizations count only the
+   * factorizations with nothing fused (the Laplace precision): the Cholesky rate. */
+  double numeric_pure_ms;
+  int32_t n_pure_factorizations;
 } gmrf_spacetime_info_t;
 
 int gmrf_spacetime_create(const gmrf_spacetime_config_t* cfg, gmrf_spacetime_t** out);

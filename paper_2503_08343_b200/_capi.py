@@ -69,6 +69,7 @@ class SpaceTimeInfo(C.Structure):
         ("n_res", C.c_int32), ("nnz_pattern", C.c_int64), ("nnz_l", C.c_int64),
         ("nnz_l_padded", C.c_int64), ("flops_ref", C.c_double), ("flops_sn", C.c_double),
         ("factor_device_bytes", C.c_int64),
+        ("numeric_pure_ms", C.c_double), ("n_pure_factorizations", C.c_int32),
     ]
 
 

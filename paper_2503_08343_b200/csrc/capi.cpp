@@ -519,6 +519,8 @@ int gmrf_spacetime_info(const gmrf_spacetime_t* h, gmrf_spacetime_info_t* info) 
     info->selinv_ms = t.selinv_ms;
     info->numeric_ms = t.numeric_ms;
     info->n_factorizations = t.n_factorizations;
+    info->numeric_pure_ms = t.numeric_pure_ms;
+    info->n_pure_factorizations = t.n_pure_factorizations;
     info->kernel_launches = t.kernel_launches;
     info->n = h->p->n();
     info->n_space = h->p->n_space();

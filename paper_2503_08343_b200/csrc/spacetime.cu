@@ -815,6 +815,10 @@ std::vector<GnIter> SpaceTimePosterior::run(const double* u0, const GnConfig& cf
     cudaEventElapsedTime(&ms, a, b);
     times_.numeric_ms += ms;
     times_.n_factorizations += 1;
+    if (!rhs) {
+      times_.numeric_pure_ms += ms;
+      times_.n_pure_factorizations += 1;
+    }
     times_.kernel_launches += fac_->launches_numeric();
     if (bad >= 0)
       throw Error(kNotSpd, std::string(what) + ": cholesky: non-positive pivot at index " +

@@ -71,6 +71,8 @@ struct PhaseTimes {
   double selinv_ms = 0;       // marginal variances
   double numeric_ms = 0;      // sum of all numeric factorizations
   i32 n_factorizations = 0;
+  double numeric_pure_ms = 0;  // factorizations with no fused forward sweep
+  i32 n_pure_factorizations = 0;
   i64 kernel_launches = 0;
 };
 
