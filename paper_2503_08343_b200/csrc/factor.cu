@@ -245,6 +245,25 @@ DeviceFactor::DeviceFactor(std::shared_ptr<const Symbolic> sym, cudaStream_t str
     wfwd_.upload(wf, stream_);
     wbwd_.upload(wb, stream_);
     wx_.alloc(std::max<int64_t>(2 * nflag * 64 * kMaxRhs, 1));
+    if (const char* e = std::getenv("GMRF_WIDE_INV")) wide_inv_ = e[0] != '0';
+    if (wide_inv_ && nflag) {
+      winv_.alloc(nflag * 64 * 64);
+      std::vector<SelChunk> wt;
+      for (const WideBlock& t : wf) {
+        const int k = t.sn, rows = s.rows(k), c0 = t.b * 64;
+        SelChunk c{};
+        c.l = L_.p + lptr_h_[k];
+        c.ld = rows;
+        c.c0 = c0;
+        c.w = std::min(64, s.w(k) - c0);
+        c.wsn = s.w(k);
+        c.rd = rdiag_.p + s.sn_first[k] + c0;
+        c.dst = winv_.p + static_cast<int64_t>(t.flag0 + t.b) * 64 * 64;
+        c.ldd = 64;
+        wt.push_back(c);
+      }
+      winv_tasks_.upload(wt, stream_);
+    }
   }
   lvl_sn_.upload(lsn, stream_);
   // solve workspaces: update vectors (r_s) and backward partials (tiles_s × w_s),
@@ -1289,6 +1308,12 @@ int32_t DeviceFactor::factor_panels(const double* fwd_rhs) {
     });
     ++launches_numeric_;
   }
+  if (winv_tasks_.n) {  // inverted diagonal blocks of the wide supernodes, for the solves
+    pf.run(stream_, "factor.wide_block_inverse", winv_tasks_.n * (64.0 * 64 * 64 / 3.0), 0.0, [&] {
+      k_tri_inv64<<<static_cast<unsigned>(winv_tasks_.n), 64, 0, stream_>>>(winv_tasks_.p);
+    });
+    ++launches_numeric_;
+  }
   cuda_check(cudaGetLastError(), "factor launch");
   if (part_) exchange({{3, -1, -1, -1, status_.p, 1}});  // smallest failing pivot over ranks
   int st = INT_MAX;
@@ -1665,7 +1690,8 @@ void DeviceFactor::fwd_level(int l, double* y, int nr, cudaStream_t st) {
       for (int64_t g = wl_ptr_[l]; g < wl_ptr_[l + 1]; ++g) {
         const WideBlock* tasks = wfwd_.p + wgroups_[g].t0;
         double* xw = wx_.p;
-        void* args[] = {&tasks, const_cast<SymDev*>(&sd), &L, &y, &nr, &rdiag, &xw};
+        const double* wi = winv_.p;
+        void* args[] = {&tasks, const_cast<SymDev*>(&sd), &L, &y, &nr, &rdiag, &xw, &wi};
         coop(reinterpret_cast<const void*>(k_fsolve_wide<NR>), wgroups_[g].nt, args);
       }
     }
@@ -1734,7 +1760,8 @@ void DeviceFactor::launch_solve_levels(bool fwd, bool bwd, double* y, int nr, in
           const double* P = P_.p;
           const int64_t* pptr = pptr_.p;
           double* xw = wx_.p + wide_blocks_ * 64 * nr;
-          void* args[] = {&tasks, const_cast<SymDev*>(&sd), &L, &y, &nr, &P, &pptr, &rdiag, &xw};
+          const double* wi = winv_.p;
+          void* args[] = {&tasks, const_cast<SymDev*>(&sd), &L, &y, &nr, &P, &pptr, &rdiag, &xw, &wi};
           coop(reinterpret_cast<const void*>(k_bsolve_wide<NR>), wgroups_[g].nt, args);
         }
       });

@@ -346,6 +346,12 @@ class DeviceFactor {
   std::vector<WideGroup> wgroups_;
   DevBuf<WideBlock> wfwd_, wbwd_;
   DevBuf<double> wx_;  // wide-solve block exchange: solved 64-row blocks, sentinel until written
+  // inverted 64×64 diagonal blocks of the wide supernodes (k_tri_inv64 after every
+  // factorization): a wide-block step ends with a 64×64 GEMV on all 256 threads
+  // instead of a 64-step dependent warp substitution. GMRF_WIDE_INV=0: substitution (A/B)
+  bool wide_inv_ = true;
+  DevBuf<double> winv_;
+  DevBuf<SelChunk> winv_tasks_;
   int64_t wide_blocks_ = 0;
 
   int64_t launches_numeric_ = 0, launches_solve_ = 0, launches_selinv_ = 0;

@@ -95,6 +95,15 @@ __device__ __forceinline__ void wide_stage_diag(double* Lb, double* rdl, const d
   if (static_cast<int>(threadIdx.x) < nbr) cpasync8(&rdl[threadIdx.x], rdiag + threadIdx.x);
 }
 
+// stage the inverted diagonal block (k_tri_inv64 output, 64×64 slot, only nbr × nbr written)
+__device__ __forceinline__ void wide_stage_inv(double* Lb, const double* Wb, int nbr) {
+  for (int idx = threadIdx.x; idx < 64 * 64; idx += blockDim.x) {
+    const int i = idx & 63, j = idx >> 6;
+    if (i < nbr && j < nbr) cpasync8(&Lb[j * kWideLd + i], Wb + i + j * 64);
+    else Lb[j * kWideLd + i] = 0.0;
+  }
+}
+
 // stage the tile L[r0 .. r0+nr) × [c0 .. c0+nc) (column-major, zero padded to 64×64)
 __device__ __forceinline__ void wide_stage_tile(double* T, const double* Ls, int rows, int r0,
                                                 int nr, int c0, int nc) {
@@ -113,9 +122,10 @@ __global__ void __launch_bounds__(256) k_fsolve_wide(const WideBlock* __restrict
                                                      SymDev sd, const double* __restrict__ L,
                                                      double* __restrict__ y, int nrhs,
                                                      const double* __restrict__ rdiag,
-                                                     double* __restrict__ xw) {
+                                                     double* __restrict__ xw,
+                                                     const double* __restrict__ winv) {
   extern __shared__ double sm[];
-  double* Lb = sm;                      // diagonal block, [j*65 + i]
+  double* Lb = sm;                      // diagonal block (or its inverse), [j*65 + i]
   double* T0 = Lb + 64 * kWideLd;       // L[b, m] tiles, double buffered
   double* acc = T0 + 2 * 64 * kWideLd;  // [rr*64 + i]
   double* ym = acc + 64 * NR;           // [rr*64 + j]
@@ -129,13 +139,14 @@ __global__ void __launch_bounds__(256) k_fsolve_wide(const WideBlock* __restrict
   const int n = sd.n, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const double* Ls = L + sd.lptr[s];
   const int i0 = t.b * 64, nbr = min(64, w - i0);
-  wide_stage_diag(Lb, rdl, Ls, rows, i0, nbr, rdiag + f0 + i0);
+  if (winv) wide_stage_inv(Lb, winv + static_cast<int64_t>(t.flag0 + t.b) * 64 * 64, nbr);
+  else wide_stage_diag(Lb, rdl, Ls, rows, i0, nbr, rdiag + f0 + i0);
   cp_commit();
   if (t.b > 0) wide_stage_tile(T0, Ls, rows, i0, nbr, 0, 64);
   cp_commit();
-  for (int idx = tid; idx < nbr * nrhs; idx += blockDim.x) {
-    const int i = idx % nbr, rr = idx / nbr;
-    acc[rr * 64 + i] = y[f0 + i0 + i + static_cast<int64_t>(rr) * n];
+  for (int idx = tid; idx < 64 * nrhs; idx += blockDim.x) {
+    const int i = idx & 63, rr = idx >> 6;
+    acc[rr * 64 + i] = i < nbr ? y[f0 + i0 + i + static_cast<int64_t>(rr) * n] : 0.0;
   }
   const int i = tid & 63, q = tid >> 6;  // row i, column quarter q
   for (int m = 0; m < t.b; ++m) {
@@ -171,7 +182,33 @@ __global__ void __launch_bounds__(256) k_fsolve_wide(const WideBlock* __restrict
   }
   cp_wait<0>();
   __syncthreads();
-  if (warp == 0) {
+  if (winv) {
+    // y_b = L_bb⁻¹ acc: one 64×64 GEMV on all threads (column quarters, fixed sum order)
+    double part[NR];
+#pragma unroll
+    for (int rr = 0; rr < NR; ++rr) part[rr] = 0.0;
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const double l = Lb[(q * 16 + u) * kWideLd + i];
+#pragma unroll
+      for (int rr = 0; rr < NR; ++rr)
+        if (rr < nrhs) part[rr] += l * acc[rr * 64 + q * 16 + u];
+    }
+#pragma unroll
+    for (int rr = 0; rr < NR; ++rr) red[(q * NR + rr) * 64 + i] = part[rr];
+    __syncthreads();
+    if (tid < nbr) {
+#pragma unroll
+      for (int rr = 0; rr < NR; ++rr) {
+        if (rr >= nrhs) break;
+        const double v = (red[rr * 64 + tid] + red[(NR + rr) * 64 + tid]) +
+                         (red[(2 * NR + rr) * 64 + tid] + red[(3 * NR + rr) * 64 + tid]);
+        if (t.b + 1 < t.nb)
+          wide_publish(xw + static_cast<int64_t>(t.flag0 + t.b) * 64 * nrhs + rr * 64 + tid, v);
+        y[f0 + i0 + tid + static_cast<int64_t>(rr) * n] = v;
+      }
+    }
+  } else if (warp == 0) {
     double v0[NR], v1[NR];
 #pragma unroll
     for (int rr = 0; rr < NR; ++rr) {
@@ -215,7 +252,8 @@ __global__ void __launch_bounds__(256) k_bsolve_wide(const WideBlock* __restrict
                                                      const double* __restrict__ P,
                                                      const int64_t* __restrict__ pptr,
                                                      const double* __restrict__ rdiag,
-                                                     double* __restrict__ xw) {
+                                                     double* __restrict__ xw,
+                                                     const double* __restrict__ winv) {
   extern __shared__ double sm[];
   double* Lb = sm;
   double* T0 = Lb + 64 * kWideLd;       // L[m, b] tiles, double buffered
@@ -232,7 +270,8 @@ __global__ void __launch_bounds__(256) k_bsolve_wide(const WideBlock* __restrict
   const int n = sd.n, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const double* Ls = L + sd.lptr[s];
   const int i0 = t.b * 64, nbr = min(64, w - i0);
-  wide_stage_diag(Lb, rdl, Ls, rows, i0, nbr, rdiag + f0 + i0);
+  if (winv) wide_stage_inv(Lb, winv + static_cast<int64_t>(t.flag0 + t.b) * 64 * 64, nbr);
+  else wide_stage_diag(Lb, rdl, Ls, rows, i0, nbr, rdiag + f0 + i0);
   cp_commit();
   const int mlast = t.nb - 1;
   if (mlast > t.b) wide_stage_tile(T0, Ls, rows, mlast * 64, w - mlast * 64, i0, nbr);
@@ -240,11 +279,14 @@ __global__ void __launch_bounds__(256) k_bsolve_wide(const WideBlock* __restrict
   {
     const int ntiles = (r + kSolveRows - 1) / kSolveRows;
     const double* Ps = P + pptr[s] * nrhs;
-    for (int idx = tid; idx < nbr * nrhs; idx += blockDim.x) {
-      const int a = idx % nbr, rr = idx / nbr;
-      double v = x[f0 + i0 + a + static_cast<int64_t>(rr) * n];
-      for (int tt = 0; tt < ntiles; ++tt)
-        v -= Ps[(static_cast<int64_t>(tt) * w) * nrhs + rr * w + i0 + a];
+    for (int idx = tid; idx < 64 * nrhs; idx += blockDim.x) {
+      const int a = idx & 63, rr = idx >> 6;
+      double v = 0.0;
+      if (a < nbr) {
+        v = x[f0 + i0 + a + static_cast<int64_t>(rr) * n];
+        for (int tt = 0; tt < ntiles; ++tt)
+          v -= Ps[(static_cast<int64_t>(tt) * w) * nrhs + rr * w + i0 + a];
+      }
       acc[rr * 64 + a] = v;
     }
   }
@@ -284,7 +326,33 @@ __global__ void __launch_bounds__(256) k_bsolve_wide(const WideBlock* __restrict
   }
   cp_wait<0>();
   __syncthreads();
-  if (warp == 0) {
+  if (winv) {
+    // x_b = L_bb⁻ᵀ acc: x_j = Σ_i W_ij acc_i (row quarters, fixed sum order)
+    double part[NR];
+#pragma unroll
+    for (int rr = 0; rr < NR; ++rr) part[rr] = 0.0;
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const double l = Lb[j * kWideLd + q * 16 + u];
+#pragma unroll
+      for (int rr = 0; rr < NR; ++rr)
+        if (rr < nrhs) part[rr] += l * acc[rr * 64 + q * 16 + u];
+    }
+#pragma unroll
+    for (int rr = 0; rr < NR; ++rr) red[(q * NR + rr) * 64 + j] = part[rr];
+    __syncthreads();
+    if (tid < nbr) {
+#pragma unroll
+      for (int rr = 0; rr < NR; ++rr) {
+        if (rr >= nrhs) break;
+        const double v = (red[rr * 64 + tid] + red[(NR + rr) * 64 + tid]) +
+                         (red[(2 * NR + rr) * 64 + tid] + red[(3 * NR + rr) * 64 + tid]);
+        if (t.b > 0)
+          wide_publish(xw + static_cast<int64_t>(t.flag0 + t.b) * 64 * nrhs + rr * 64 + tid, v);
+        x[f0 + i0 + tid + static_cast<int64_t>(rr) * n] = v;
+      }
+    }
+  } else if (warp == 0) {
     double v0[NR], v1[NR];
 #pragma unroll
     for (int rr = 0; rr < NR; ++rr) {

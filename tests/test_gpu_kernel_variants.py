@@ -96,3 +96,13 @@ def test_blocked_selected_inversion_matches_chunk_chain(shape):
         assert np.all(other[1] > 0)
         rel = np.abs(blocked[1] - other[1]) / other[1]
         assert rel.max() <= 1e-9, rel.max()
+
+
+def test_inverted_wide_blocks_match_substitution():
+    """Wide supernodes end each 64-row block step of the solves with a GEMV against
+    the inverted diagonal block (k_tri_inv64 after every factorization) instead of
+    a 64-step warp substitution (GMRF_WIDE_INV=0): same Gauss-Newton path, values
+    to rounding."""
+    spec = SpaceTimeSpec.burgers(299, 300)
+    u0 = -np.sin(np.pi * spec.node_x())
+    _close(_run(spec, u0, {}, gn=3), _run(spec, u0, {"GMRF_WIDE_INV": "0"}, gn=3), tol=1e-8)

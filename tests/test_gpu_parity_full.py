@@ -56,8 +56,12 @@ def _check_trace(z, trace):
     np.testing.assert_array_equal([t.step_size for t in trace], z["gn_step"])
     obj = np.array([t.objective for t in trace])
     dec = np.array([t.decrement for t in trace])
+    # a decrement below the reference's own convergence resolution (it stops at
+    # 0.5·dec² <= 1e-14·(1 + |objective|), gauss_newton.hpp:187-188) is compared on
+    # that scale: relative error of a quantity the reference treats as zero means nothing
+    res = np.sqrt(2e-14 * (1.0 + np.abs(z["gn_objective"])))
     return (float(np.max(np.abs(obj - z["gn_objective"]) / np.abs(z["gn_objective"]))),
-            float(np.max(np.abs(dec - z["gn_decrement"]) / np.abs(z["gn_decrement"]))))
+            float(np.max(np.abs(dec - z["gn_decrement"]) / np.maximum(np.abs(z["gn_decrement"]), res))))
 
 
 K = 10.0
@@ -72,7 +76,17 @@ def _floors(name):
         # the product factors in a nested-dissection order, the fixture's reference run
         # in AMD order: the ordering probe is the tolerance scale that applies
         pytest.skip(f"ordering floor for {name} not measured yet (make_golden_full.py order:)")
-    return {k: max(p.get(k, 0.0) for p in probes) for k in BOUND}
+    out = {k: max(p.get(k, 0.0) for p in probes) for k in BOUND}
+    if not any("var" in p for p in probes):
+        # full-size probes skip the reference's Takahashi pass (hours at n = 1e6;
+        # make_golden_full.py order_novar: / floor_novar:): the variance floor is the
+        # measured mean floor times the SMALLEST var/mean floor ratio the same family
+        # shows at the sizes where both were measured (0.5-0.8 for config 4)
+        fam = name.split("_")[0]
+        ratios = [v["var"] / v["mean"] for key, v in fl.items()
+                  if key.startswith(fam) and "var" in v and v.get("mean", 0.0) > 0.0]
+        out["var"] = out["mean"] * min(ratios)
+    return out
 
 
 def _judge(name, errs):
