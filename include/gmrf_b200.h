@@ -294,6 +294,13 @@ int gmrf_update_system_same_operator(const gmrf_update_system_t* h, int32_t m,
  * gmrf_factor_numeric. */
 int gmrf_update_system_refactor(gmrf_update_system_t* h, const double* a_values, const double* w,
                                 int32_t* bad_index);
+/* refactor followed by the solve H x = b (host vectors of n values): the step
+ * gauss_newton takes every iteration (gauss_newton.hpp:137-141). The forward
+ * sweep rides along with the factorization on the device; same results as
+ * gmrf_update_system_refactor + gmrf_solve(GMRF_SOLVE_FULL). */
+int gmrf_update_system_refactor_solve(gmrf_update_system_t* h, const double* a_values,
+                                      const double* w, const double* b, double* x,
+                                      int32_t* bad_index);
 /* H's values only (no factorization), into values[nnz] in the union pattern's
  * order: symmetrize(B + c · Aᵀ diag(w) A) — e.g. the Matérn precision with
  * B = 0, A = K̂, w = 1/m̃, c = 1/τ² (priors/matern.hpp:70-80). */

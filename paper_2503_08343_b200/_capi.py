@@ -169,6 +169,7 @@ SIGNATURES = {
                                             C.c_int32, i64p, i32p, i32p, C.POINTER(vp)]),
     "gmrf_update_system_same_operator": (C.c_int, [vp, C.c_int32, i64p, i32p]),
     "gmrf_update_system_refactor": (C.c_int, [vp, f64p, f64p, i32p]),
+    "gmrf_update_system_refactor_solve": (C.c_int, [vp, f64p, f64p, f64p, f64p, i32p]),
     "gmrf_update_system_matrix": (C.c_int, [vp, i64p, i32p, f64p]),
     "gmrf_update_system_assemble": (C.c_int, [vp, f64p, f64p, C.c_double, f64p]),
     "gmrf_update_system_symbolic": (vp, [vp]),

@@ -715,6 +715,26 @@ int gmrf_update_system_refactor(gmrf_update_system_t* h, const double* a, const 
   return rc;
 }
 
+int gmrf_update_system_refactor_solve(gmrf_update_system_t* h, const double* a, const double* w,
+                                      const double* b, double* x, int32_t* bad) {
+  int32_t bi = -1;
+  const int rc = guard([&] {
+    bi = h->u->refactor(a, w, b);
+    if (!h->fac.f) {
+      h->sym.s = h->u->symbolic();
+      h->fac.s = h->u->symbolic();
+      h->fac.f.reset(&h->u->factor());
+    }
+    if (bi < 0) h->u->solve_pending(x);
+  });
+  if (bad) *bad = bi;
+  if (rc == GMRF_OK && bi >= 0) {
+    g_err = "cholesky: non-positive pivot at index " + std::to_string(bi);
+    return GMRF_ERR_NOT_SPD;
+  }
+  return rc;
+}
+
 int gmrf_update_system_assemble(gmrf_update_system_t* h, const double* a, const double* w, double c,
                                 double* v) {
   return guard([&] {

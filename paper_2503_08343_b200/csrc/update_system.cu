@@ -125,12 +125,24 @@ void UpdateSystem::ensure_factor() {
   fac_ = std::make_unique<DeviceFactor>(sym_, stream_);
 }
 
-int32_t UpdateSystem::refactor(const double* a_values, const double* w) {
+int32_t UpdateSystem::refactor(const double* a_values, const double* w, const double* rhs) {
   ensure_factor();
   stage(a_values, w);
+  if (rhs) {
+    if (rhs_.n < static_cast<size_t>(std::max(n_, 1))) rhs_.alloc(std::max(n_, 1));
+    cuda_check(cudaMemcpyAsync(rhs_.p, rhs, n_ * sizeof(double), cudaMemcpyHostToDevice, stream_),
+               "rhs");
+  }
   fac_->begin_numeric();
   gram_a_->apply(a_.p, w_.p, 1.0, base_.p, h_.p, fac_->d_qmap(), fac_->d_l(), stream_);
-  return fac_->factor_panels();
+  return fac_->factor_panels(rhs ? rhs_.p : nullptr);
+}
+
+void UpdateSystem::solve_pending(double* x) {
+  if (x_.n < static_cast<size_t>(std::max(n_, 1))) x_.alloc(std::max(n_, 1));
+  fac_->solve_pending(x_.p);
+  cuda_check(cudaMemcpyAsync(x, x_.p, n_ * sizeof(double), cudaMemcpyDeviceToHost, stream_), "x");
+  cuda_check(cudaStreamSynchronize(stream_), "solve");
 }
 
 void UpdateSystem::copy_values(double* out) const {

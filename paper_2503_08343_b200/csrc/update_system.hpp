@@ -30,7 +30,10 @@ class UpdateSystem {
                cudaStream_t stream = nullptr);
   // H from A's values (CSC order) and the m weights; factor. Returns -1 or the
   // original index of the failing pivot (cholesky.hpp:153-156).
-  int32_t refactor(const double* a_values, const double* w);
+  // rhs (host, n values, optional): the forward sweep of H x = rhs rides along
+  // with the factorization (DeviceFactor::factor_panels); solve_pending(x) finishes it.
+  int32_t refactor(const double* a_values, const double* w, const double* rhs = nullptr);
+  void solve_pending(double* x);
   // values only: H = sym(B + c·AᵀWA) into the pattern-order buffer (no factor)
   void assemble(const double* a_values, const double* w, double c);
   bool same_operator(i32 m, const i64* acp, const i32* ari) const;
@@ -60,7 +63,7 @@ class UpdateSystem {
   std::unique_ptr<DeviceFactor> fac_;
   std::unique_ptr<GramPlan> gram_a_;
   void stage(const double* a_values, const double* w);
-  DevBuf<double> base_, h_, a_, w_;
+  DevBuf<double> base_, h_, a_, w_, rhs_, x_;
 };
 
 }  // namespace gmrf

@@ -47,6 +47,16 @@ class UpdateSystem : public std::enable_shared_from_this<UpdateSystem> {
     const int rc = gmrf_update_system_refactor(h_, a.values.data(), w.data(), &bad);
     if (rc != GMRF_OK) raise(rc, bad);
   }
+  // refactor + solve H x = b in one call (the forward sweep rides along with the
+  // factorization on the device)
+  Vector refactor_solve(const SparseMatrixCSC& a, const Vector& w, const Vector& b) {
+    int32_t bad = -1;
+    Vector x(b.size());
+    const int rc =
+        gmrf_update_system_refactor_solve(h_, a.values.data(), w.data(), b.data(), x.data(), &bad);
+    if (rc != GMRF_OK) raise(rc, bad);
+    return x;
+  }
   // H's values only, c scaling the product
   void assemble(const SparseMatrixCSC& a, const Vector& w, Real c) {
     check(gmrf_update_system_assemble(h_, a.values.data(), w.data(), c, nullptr));

@@ -66,8 +66,7 @@ inline GaussNewtonResult gauss_newton(const Gmrf& prior, const NonlinearResidual
       sys = b200::UpdateSystem::make(use_sqrt ? b200::UpdateSystem::kSqrt
                                               : b200::UpdateSystem::kPrecision,
                                      use_sqrt ? prior.sqrt() : prior.precision(), jac);
-    sys->refactor(jac, res.noise_precision);
-    const Vector direction = sys->solve(scaled(grad, -1.0));
+    const Vector direction = sys->refactor_solve(jac, res.noise_precision, scaled(grad, -1.0));
 
     GaussNewtonIteration rec;
     rec.iter = iter;
