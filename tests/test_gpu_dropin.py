@@ -130,3 +130,71 @@ def test_dropin_burgers_chain_matches_reference():
     assert obj.max() <= 10 * _floor(fixture, "objective")
     assert _rel(r["mode"], z["mode"]) <= 10 * _floor(fixture, "mean")
     assert _rel(r["var_post"], z["var_post"]) <= 10 * _floor(fixture, "var")
+
+
+def test_update_system_refactor_solve_matches_refactor_then_solve():
+    """gmrf_update_system_refactor_solve (the Gauss-Newton step as one call, forward
+    sweep fused into the factorization graph) against gmrf_update_system_refactor +
+    gmrf_solve on the same system: identical bits, and the solution of
+    H = sym(Q + AᵀWA) to rounding (gauss_newton.hpp:137-141)."""
+    import ctypes as C
+
+    import numpy as np
+    import scipy.sparse as sp
+    import scipy.sparse.linalg as spla
+
+    from paper_2503_08343_b200 import _capi
+    from paper_2503_08343_b200.core import _check
+
+    lib = _capi.load()
+    g = 70  # 4900 unknowns: separators wider than 128 columns (wide solve kernels too)
+    n = g * g
+    lap = sp.kron(sp.eye(g), sp.diags([-1, 2.5, -1], [-1, 0, 1], (g, g))) + \
+        sp.kron(sp.diags([-1, 2.5, -1], [-1, 0, 1], (g, g)), sp.eye(g))
+    q = sp.csc_matrix(lap, dtype=np.float64)
+    q.sort_indices()
+    rng = np.random.default_rng(11)
+    m = 600
+    rows = np.repeat(np.arange(m), 3)
+    cols = rng.integers(0, n, size=3 * m)
+    a = sp.csc_matrix((rng.standard_normal(3 * m), (rows, cols)), shape=(m, n))
+    a.sum_duplicates()
+    a.sort_indices()
+    w = rng.uniform(0.5, 2.0, m)
+    b = rng.standard_normal(n)
+
+    def i64(v):
+        return np.ascontiguousarray(v, np.int64)
+
+    def i32(v):
+        return np.ascontiguousarray(v, np.int32)
+
+    def p(arr, t):
+        return arr.ctypes.data_as(C.POINTER(t))
+
+    qcp, qri, qv = i64(q.indptr), i32(q.indices), np.ascontiguousarray(q.data)
+    acp, ari, av = i64(a.indptr), i32(a.indices), np.ascontiguousarray(a.data)
+    outs = []
+    for fused in (False, True):
+        h = C.c_void_p()
+        _check(lib.gmrf_update_system_create(n, 0, n, p(qcp, C.c_int64), p(qri, C.c_int32),
+                                             p(qv, C.c_double), m, p(acp, C.c_int64),
+                                             p(ari, C.c_int32), None, C.byref(h)))
+        x = np.zeros(n)
+        bad = C.c_int32(-1)
+        for _ in range(2):  # second pass replays the captured graph
+            if fused:
+                _check(lib.gmrf_update_system_refactor_solve(h, p(av, C.c_double), p(w, C.c_double),
+                                                             p(b, C.c_double), p(x, C.c_double),
+                                                             C.byref(bad)))
+            else:
+                _check(lib.gmrf_update_system_refactor(h, p(av, C.c_double), p(w, C.c_double),
+                                                       C.byref(bad)))
+                _check(lib.gmrf_solve(lib.gmrf_update_system_factor(h), 2, 1, p(b, C.c_double),
+                                      p(x, C.c_double)))
+        outs.append(x.copy())
+        lib.gmrf_update_system_free(h)
+    np.testing.assert_array_equal(outs[0], outs[1])
+    hmat = (q + a.T @ sp.diags(w) @ a).tocsc()
+    ref = spla.spsolve(hmat, b)
+    assert np.linalg.norm(outs[1] - ref) <= 1e-10 * np.linalg.norm(ref)
