@@ -108,8 +108,10 @@ __host__ __device__ constexpr int small_rows_threads() {
   return panel_rows_diag<W>() + small_rows_slab<W>();
 }
 
+// W <= 32: three CTAs per SM (the 96×97 front in shared memory allows three; the
+// default register allocation of 255 only two)
 template <int W>
-__global__ void __launch_bounds__(small_rows_threads<W>(), 1)
+__global__ void __launch_bounds__(small_rows_threads<W>(), W <= 32 ? 3 : 1)
     k_small_front_rows(const int32_t* __restrict__ sns, SymDev sd, double* __restrict__ L,
                        double* __restrict__ U, int32_t* __restrict__ status,
                        double* __restrict__ rdiag) {
