@@ -98,7 +98,7 @@ __device__ __forceinline__ void load_operand(double (*dst)[kPad], const double* 
 // The accumulator starts from beta*C (issued with the first operand loads, so
 // the C round trip overlaps them instead of trailing the MMA loop) and alpha is
 // folded into the A fragments (alpha = ±1 in every plan: exact).
-__global__ void __launch_bounds__(128, 4) k_gemm_tiles(const GemmTask* __restrict__ tasks) {
+__global__ void __launch_bounds__(128, 5) k_gemm_tiles(const GemmTask* __restrict__ tasks) {
   __shared__ __align__(16) double As[2][kKC][kPad];
   __shared__ __align__(16) double Bs[2][kKC][kPad];
   const GemmTask& t = tasks[blockIdx.x];
